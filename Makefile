@@ -1,0 +1,41 @@
+# Builds the product library (CUDA for sm_100a + the C ABI) and the oracle.
+#   make            -> paper_1905_01294_b200/lib/libmgk.so, oracle/liboracle.so
+#   make ref        -> oracle/_ref/libmatgraph_ref.so (needs /root/reference)
+NVCC    ?= nvcc
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_1905_01294_b200
+CSRC    := $(PKG)/csrc
+BUILD   := build
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
+           -Iinclude -I$(CSRC) --expt-relaxed-constexpr
+CU      := $(CSRC)/mgk_graph.cu $(CSRC)/mgk_ss.cu $(CSRC)/mgk_ms.cu
+CPP     := $(CSRC)/mgk_capi.cpp $(CSRC)/mgk_host.cpp
+OBJS    := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU)) $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP))
+HDRS    := include/mgk.h $(CSRC)/mgk_internal.cuh $(CSRC)/mgk_device.cuh
+LIB     := $(PKG)/lib/libmgk.so
+
+.PHONY: all lib oracle ref clean
+all: lib oracle
+
+lib: $(LIB)
+
+$(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o $@ $< 2> $(BUILD)/$*.ptxas.txt || (cat $(BUILD)/$*.ptxas.txt; false)
+
+$(BUILD)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c -o $@ $<
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle oracle
+
+ref:
+	$(MAKE) -s -C oracle ref
+
+clean:
+	rm -rf $(BUILD) $(LIB)

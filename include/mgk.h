@@ -1,0 +1,183 @@
+/*
+ * mgk — the B200 k-hop count engine behind a plain C ABI.
+ *
+ * This is the drop-in boundary for the reference's k-hop hot path
+ * (matgraph, /root/reference/proj). Every entry point names the reference
+ * interface it replaces. No exceptions and no C++/torch types cross this
+ * boundary: plain pointers, sizes and int status codes, with the message of
+ * the last failure on this thread in mgk_last_error().
+ *
+ * Semantics are the reference's, bit for bit:
+ *   k_hop_frontier  proj/core/src/execute.cpp:347-371
+ *       frontier = visited = {seed}; for hop 1..k:
+ *           frontier = vxm(frontier, A, mask = NOT visited)   (sparse.cpp:253-290)
+ *           if frontier empty: break
+ *           visited = ewise_union(visited, frontier)          (sparse.cpp:365-377)
+ *       exact      -> frontier   (vertices at shortest distance exactly k)
+ *       cumulative -> visited \ {seed}  (distance 1..k)
+ *   k_hop_count     proj/core/src/execute.cpp:373-375  = nvals(k_hop_frontier)
+ *
+ * Status codes follow the reference's error classes
+ * (proj/core/include/matgraph/error.hpp:10-66): MGK_ECONTRACT <-> ContractError
+ * with the reference's exact message text, MGK_EHARNESS <-> HarnessError,
+ * everything else maps to matgraph::Error.
+ */
+#ifndef MGK_H
+#define MGK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MGK_ABI_VERSION 1
+
+/* status codes */
+#define MGK_OK 0
+#define MGK_ECONTRACT 1 /* precondition violated (ContractError): bad seed, k, sizes */
+#define MGK_EHARNESS 2  /* harness setup failure (HarnessError), e.g. too few seeds */
+#define MGK_ECUDA 3     /* CUDA runtime / launch failure (matgraph::Error) */
+#define MGK_ENOMEM 4    /* device or host allocation failed */
+#define MGK_ERANGE 5    /* graph exceeds uint32 device indices (n or nnz >= 2^32) */
+
+/* TraverseMode, proj/core/include/matgraph/plan.hpp:17 */
+#define MGK_EXACT 0
+#define MGK_CUMULATIVE 1
+
+/* traversal engines */
+#define MGK_ENGINE_AUTO 0   /* 1 seed -> SINGLE, more -> LANES */
+#define MGK_ENGINE_SINGLE 1 /* bitmap direction-optimizing BFS, one seed at a time */
+#define MGK_ENGINE_LANES 2  /* bit-parallel multi-source: 64 seeds per uint64 lane word */
+
+#define MGK_MAX_HOPS 32 /* kMaxHops, proj/core/include/matgraph/ast.hpp:15 */
+
+typedef struct mgk_graph mgk_graph;
+
+/* Per-level work counters of one call (summed over seeds / batches). */
+typedef struct mgk_level {
+    uint64_t frontier;    /* (seed, vertex) pairs discovered at this hop: sum of |F_l| */
+    uint64_t vertices;    /* distinct vertices discovered (LANES: |union of lane frontiers|) */
+    uint64_t edges;       /* push-equivalent edges E: sum over seeds of outdeg(F_{l-1}) */
+    uint64_t union_edges; /* edges of the distinct frontier vertices (what a push pass reads) */
+    uint64_t scanned;     /* adjacency entries the kernel actually read at this hop */
+    uint64_t candidates;  /* pull: unvisited candidate vertices examined */
+    uint32_t runs;        /* seeds (SINGLE) or batches (LANES) that expanded this hop */
+    uint32_t pull_runs;   /* ... of which ran the hop in the pull (CSC) direction */
+    uint64_t ns;          /* device time in this hop (%globaltimer, summed over runs) */
+} mgk_level;
+
+typedef struct mgk_stats {
+    uint32_t engine;       /* MGK_ENGINE_SINGLE or MGK_ENGINE_LANES */
+    uint32_t lanes;        /* seeds per batch (LANES) or 1 */
+    uint32_t batches;      /* batches (LANES) or seeds (SINGLE) */
+    uint32_t hops;         /* deepest hop expanded by any run */
+    uint32_t grid;         /* persistent CTAs launched */
+    uint32_t block;        /* threads per CTA */
+    double kernel_ms;      /* CUDA-event time of the traversal launch(es) */
+    mgk_level level[MGK_MAX_HOPS + 1];
+} mgk_stats;
+
+/* ---- graph lifetime ---------------------------------------------------------
+ * Replaces the read side of PropertyGraph::relation_matrix
+ * (proj/core/src/graph.cpp:84-88) and transposed_matrix (:90-102): the CSR of
+ * one relation (or ANY) is uploaded once, narrowed to uint32, and the CSC
+ * (= CSR of A^T, sparse.cpp:379-403) is built on the device. `nrows` is the
+ * matrix dimension (the store's capacity, graph.cpp:26); `row_ptr` has nrows+1
+ * entries and `col_idx` nnz entries with strictly ascending columns per row
+ * (the SparseMatrix invariant, sparse.hpp:80-82). Checked: row_ptr monotone,
+ * row_ptr[nrows] == nnz, columns < nrows. */
+int mgk_graph_upload(int device, uint64_t nrows, uint64_t nnz, const uint64_t* row_ptr,
+                     const uint64_t* col_idx, mgk_graph** out);
+/* Same from uint32 arrays (the bench graphs; m < 2^32). */
+int mgk_graph_upload_u32(int device, uint64_t nrows, uint64_t nnz, const uint32_t* row_ptr,
+                         const uint32_t* col_idx, mgk_graph** out);
+/* Build the device graph straight from an edge list: sort, drop duplicates
+ * (PropertyGraph::flush_slot, graph.cpp:182-215) and assemble CSR + CSC on the
+ * GPU. Self-loops are kept (they never change a count). Endpoints must be
+ * < nrows (build_bench_graph's ContractError, bench.cpp:189-193). */
+int mgk_graph_from_edges(int device, uint64_t nrows, uint64_t nedges, const uint32_t* src,
+                         const uint32_t* dst, mgk_graph** out);
+int mgk_graph_free(mgk_graph* g);
+int mgk_graph_info(const mgk_graph* g, uint64_t* nrows, uint64_t* nnz, int* device);
+/* Copy the device CSR back (uint32; either pointer may be NULL). */
+int mgk_graph_download_csr(const mgk_graph* g, uint32_t* row_ptr, uint32_t* col_idx);
+int mgk_graph_download_csc(const mgk_graph* g, uint32_t* col_ptr, uint32_t* row_idx);
+/* Device memory held by the graph and its workspaces, in bytes. */
+uint64_t mgk_graph_device_bytes(const mgk_graph* g);
+
+/* ---- the hot path -------------------------------------------------------------
+ * k_hop_count for a batch of seeds (execute.cpp:373-375 once per seed).
+ * HOST buffers: seeds[nseeds] (uint64 node ids, as KHopQuery::seed), counts[nseeds].
+ * Errors (checked before any device work, in seed order):
+ *   seed >= nrows  -> MGK_ECONTRACT "k-hop seed {s} is not an allocated node"
+ *   k outside 1..32 -> MGK_ECONTRACT "k-hop count {k} outside [1, 32]"
+ * (execute.cpp:348-354). Reentrant: concurrent calls on one graph use separate
+ * workspaces and streams. `stats` may be NULL. */
+int mgk_khop_count(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                   uint64_t* counts);
+int mgk_khop_count_ex(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                      int engine, uint64_t* counts, mgk_stats* stats);
+
+/* Device-resident variant: d_seeds (uint32) and d_counts (uint64) are DEVICE
+ * pointers on the graph's device; work is enqueued on `stream`
+ * (a cudaStream_t, NULL = legacy default) and returns without synchronizing.
+ * Seeds are NOT range-checked on this path (the caller owns them; use
+ * mgk_khop_count for checked calls). Calls on one stream share one workspace
+ * and serialize on that stream. */
+int mgk_khop_count_device(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
+                          int mode, int engine, uint64_t* d_counts, void* stream);
+/* Work counters of the last device-path call on `stream` (synchronize first;
+ * kernel_ms is 0 on this path — time it with your own events). */
+int mgk_khop_device_stats(mgk_graph* g, void* stream, mgk_stats* stats);
+
+/* k_hop_frontier (execute.cpp:347-371): the sorted ids of the result set.
+ * Writes min(*n_out, cap) ids; *n_out = total. Same checks as above. */
+int mgk_khop_frontier(mgk_graph* g, uint64_t seed, uint32_t k, int mode, uint64_t* ids,
+                      uint64_t cap, uint64_t* n_out);
+
+/* Engine tuning knobs (0 keeps the default). alpha/beta: Beamer-style
+ * push->pull when frontier edges > unexplored edges / alpha, pull->push when
+ * frontier < n / beta. Mostly for experiments and tests that force a
+ * direction: force_dir 0 auto, 1 push only, 2 pull only (pull needs hop >= 2
+ * frontier state, so hop 1 always pushes). lanes_words: 64-lane words per
+ * vertex in the LANES engine (1, 2, 4 or 8). */
+typedef struct mgk_tuning {
+    uint32_t alpha;
+    uint32_t beta;
+    uint32_t force_dir;
+    uint32_t lanes_words;
+} mgk_tuning;
+int mgk_graph_set_tuning(mgk_graph* g, const mgk_tuning* t);
+int mgk_graph_get_tuning(const mgk_graph* g, mgk_tuning* t);
+
+const char* mgk_last_error(void);
+int mgk_abi_version(void);
+int mgk_device_count(void);
+
+/* ---- harness helpers (host C++; not on the timed path) ---------------------
+ * The bench graphs of BASELINE.json: the reference's R-MAT recipe
+ * (proj/core/src/bench.cpp:107-137: per level one 53-bit uniform draw from
+ * mt19937_64, quadrant a/b/c/d) run in fixed-size chunks, each chunk with its
+ * own mt19937_64 stream seeded from (rng_seed, chunk), until `target_unique`
+ * distinct non-loop edges exist (0 = emit exactly edge_factor << scale raw
+ * edges, like rmat_generate). relabel: 0 none, 1 seeded random permutation of
+ * all 2^scale ids, 2 drop isolated ids and renumber survivors by a seeded
+ * permutation. Output: deduplicated, loop-free CSR (uint32), *n_out vertices.
+ * Two-phase: call with row_ptr = NULL to learn *n_out / *nnz_out sizes
+ * (the generated graph is cached per thread for the second call). */
+int mgk_gen_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                     uint64_t rng_seed, uint64_t target_unique, int relabel, int threads,
+                     uint64_t* n_out, uint64_t* nnz_out, uint32_t* row_ptr, uint32_t* col_idx);
+/* pick_seeds (bench.cpp:200-218) over a uint32 CSR: eligible = ids with a
+ * non-empty row, partial Fisher-Yates with mt19937_64(rng_seed) and
+ * rejection-sampled draws. MGK_EHARNESS
+ * "need {n} seeds but only {e} nodes have out-degree >= 1" when short. */
+int mgk_pick_seeds_csr(uint64_t nrows, const uint32_t* row_ptr, uint64_t n, uint64_t rng_seed,
+                       uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGK_H */

@@ -1,0 +1,228 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product path.
+//
+// A plain C wrapper around the *unmodified* reference library (matgraph,
+// compiled from /root/reference/proj/core/src with -Dmatgraph=matgraph_ref by
+// oracle/Makefile into oracle/_ref/libmatgraph_ref.so). It exists so Python
+// tests, golden-fixture generation and bench.py's reference arm can drive the
+// reference's own code path through ctypes:
+//   build_bench_graph      proj/core/src/bench.cpp:185-198
+//   k_hop_count/frontier   proj/core/src/execute.cpp:347-375
+//   pick_seeds             proj/core/src/bench.cpp:200-218
+//   rmat_generate          proj/core/src/bench.cpp:107-137
+//   BfsOracle::count       proj/core/src/bench.cpp:233-259
+// Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+// --impl reference) may load this library.
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "matgraph/bench.hpp"
+#include "matgraph/error.hpp"
+#include "matgraph/execute.hpp"
+#include "matgraph/graph.hpp"
+
+using matgraph_ref::PropertyGraph;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(const std::exception& e) {
+    g_err = e.what();
+    if (dynamic_cast<const matgraph_ref::ContractError*>(&e)) return 1;
+    if (dynamic_cast<const matgraph_ref::HarnessError*>(&e)) return 2;
+    if (dynamic_cast<const matgraph_ref::Error*>(&e)) return 3;
+    return 4;
+}
+
+matgraph_ref::TraverseMode to_mode(int mode) {
+    return mode == 1 ? matgraph_ref::TraverseMode::Cumulative : matgraph_ref::TraverseMode::Exact;
+}
+
+matgraph_ref::RelationRef to_rel(const char* relation) {
+    if (relation == nullptr) return matgraph_ref::RelationRef::any();
+    return matgraph_ref::RelationRef(relation);
+}
+
+matgraph_ref::EdgeList to_edges(const uint32_t* src, const uint32_t* dst, uint64_t m) {
+    matgraph_ref::EdgeList edges(m);
+    for (uint64_t i = 0; i < m; ++i) edges[i] = {src[i], dst[i]};
+    return edges;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// ---- graph construction -----------------------------------------------------
+
+void* ref_graph_new(uint64_t capacity) { return new PropertyGraph(capacity); }
+
+int ref_graph_create_nodes(void* g, uint64_t count) {
+    try {
+        auto* graph = static_cast<PropertyGraph*>(g);
+        for (uint64_t i = 0; i < count; ++i) graph->create_node({});
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_graph_create_edge(void* g, uint64_t src, const char* relation, uint64_t dst) {
+    try {
+        static_cast<PropertyGraph*>(g)->create_edge(src, relation, dst);
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_build_bench_graph(const uint32_t* src, const uint32_t* dst, uint64_t m,
+                          uint64_t node_count, void** out) {
+    try {
+        auto edges = to_edges(src, dst, m);
+        *out = new PropertyGraph(matgraph_ref::build_bench_graph(edges, node_count));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+void ref_graph_free(void* g) { delete static_cast<PropertyGraph*>(g); }
+
+uint64_t ref_graph_node_count(void* g) { return static_cast<PropertyGraph*>(g)->node_count(); }
+
+// CSR of relation_matrix(rel): nrows + nnz first (row_ptr/col_idx may be NULL).
+int ref_graph_relation_csr(void* g, const char* relation, uint64_t* nrows, uint64_t* nnz,
+                           uint64_t* row_ptr, uint64_t* col_idx) {
+    try {
+        const auto& m = static_cast<PropertyGraph*>(g)->relation_matrix(to_rel(relation));
+        *nrows = m.nrows();
+        *nnz = m.nvals();
+        if (row_ptr) std::memcpy(row_ptr, m.row_ptr().data(), (m.nrows() + 1) * 8);
+        if (col_idx) std::memcpy(col_idx, m.col_idx().data(), m.nvals() * 8);
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// ---- the hot path -------------------------------------------------------------
+
+int ref_k_hop_count(void* g, uint64_t seed, uint32_t k, int mode, const char* relation,
+                    uint64_t* out) {
+    try {
+        *out = matgraph_ref::k_hop_count(*static_cast<PropertyGraph*>(g),
+                                         {seed, k, to_rel(relation), to_mode(mode)});
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_k_hop_frontier(void* g, uint64_t seed, uint32_t k, int mode, const char* relation,
+                       uint64_t* ids, uint64_t cap, uint64_t* n) {
+    try {
+        auto v = matgraph_ref::k_hop_frontier(*static_cast<PropertyGraph*>(g),
+                                              {seed, k, to_rel(relation), to_mode(mode)});
+        *n = v.nvals();
+        const auto idx = v.indices();
+        for (uint64_t i = 0; i < idx.size() && i < cap; ++i) ids[i] = idx[i];
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// Seed-parallel timing harness over the reference's k_hop_count (the
+// reference's own server runs one whole query per worker thread,
+// proj/core/src/server.cpp:417-432). Seeds are dealt round-robin from an
+// atomic cursor; counts land in seed order; *elapsed_s is wall time.
+int ref_k_hop_count_many(void* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                         int threads, uint64_t* counts, double* elapsed_s) {
+    auto* graph = static_cast<PropertyGraph*>(g);
+    try {
+        graph->relation_matrix();  // flush once, outside the timed region
+    } catch (const std::exception& e) { return fail(e); }
+    if (threads < 1) threads = 1;
+    std::atomic<uint64_t> cursor{0};
+    std::atomic<int> status{0};
+    std::string first_err;
+    std::atomic<bool> err_taken{false};
+    auto worker = [&] {
+        for (;;) {
+            const uint64_t i = cursor.fetch_add(1);
+            if (i >= nseeds) return;
+            try {
+                counts[i] = matgraph_ref::k_hop_count(
+                    *graph, {seeds[i], k, matgraph_ref::RelationRef::any(), to_mode(mode)});
+            } catch (const std::exception& e) {
+                if (!err_taken.exchange(true)) {
+                    first_err = e.what();
+                    status = 1;
+                }
+                return;
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (status != 0) g_err = first_err;
+    return status;
+}
+
+// ---- harness pieces -------------------------------------------------------------
+
+int ref_pick_seeds(void* g, uint64_t n, uint64_t rng_seed, uint64_t* out) {
+    try {
+        auto seeds = matgraph_ref::pick_seeds(*static_cast<PropertyGraph*>(g), n, rng_seed);
+        for (uint64_t i = 0; i < seeds.size(); ++i) out[i] = seeds[i];
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_rmat_generate(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                      double d, uint64_t rng_seed, uint32_t* src, uint32_t* dst,
+                      uint64_t* m) {
+    try {
+        matgraph_ref::RmatParams p;
+        p.scale = scale;
+        p.edge_factor = edge_factor;
+        p.a = a;
+        p.b = b;
+        p.c = c;
+        p.d = d;
+        p.rng_seed = rng_seed;
+        p.validate();
+        if (src == nullptr) {
+            *m = p.edge_count();
+            return 0;
+        }
+        auto edges = matgraph_ref::rmat_generate(p);
+        *m = edges.size();
+        for (uint64_t i = 0; i < edges.size(); ++i) {
+            src[i] = edges[i].src;
+            dst[i] = edges[i].dst;
+        }
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+void* ref_bfs_oracle_new(const uint32_t* src, const uint32_t* dst, uint64_t m, uint64_t n) {
+    try {
+        return new matgraph_ref::BfsOracle(to_edges(src, dst, m), n);
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+int ref_bfs_oracle_count(void* o, uint64_t seed, uint32_t k, int mode, uint64_t* out) {
+    try {
+        *out = static_cast<matgraph_ref::BfsOracle*>(o)->count(seed, k, to_mode(mode));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+void ref_bfs_oracle_free(void* o) { delete static_cast<matgraph_ref::BfsOracle*>(o); }
+
+}  // extern "C"

@@ -1,0 +1,583 @@
+// The C ABI (include/mgk.h): validation with the reference's error texts,
+// a per-graph workspace pool (reentrant calls), engine dispatch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mgk_internal.cuh"
+
+struct mgk_graph {
+    mgk::Graph g;
+    std::map<cudaStream_t, mgk::Workspace*> stream_ws;  // device-path workspaces
+};
+
+namespace mgk {
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+    cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation)
+        return fail(MGK_ENOMEM, "%s: out of device memory", what);
+    return fail(MGK_ECUDA, "%s: CUDA error %d (%s)", what, (int)e, cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename F>
+void parallel_for(uint64_t n, F&& f) {
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (n < (1u << 16) || nt == 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    const uint64_t step = (n + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t) {
+        const uint64_t a = t * step, b = std::min(n, a + step);
+        if (a < b) ts.emplace_back([&f, a, b] { f(a, b); });
+    }
+    for (auto& t : ts) t.join();
+}
+
+cudaError_t create_ws(Graph* g, Workspace* ws, bool own_stream) {
+    ws->device = g->device;
+    cudaError_t e;
+    if (own_stream && (e = cudaStreamCreateWithFlags(&ws->stream, cudaStreamNonBlocking))) return e;
+    if ((e = cudaEventCreate(&ws->ev0))) return e;
+    if ((e = cudaEventCreate(&ws->ev1))) return e;
+    if ((e = cudaMalloc(&ws->qctl, 4 * sizeof(QCtl)))) return e;
+    if ((e = cudaMalloc(&ws->misc, 16 * 8))) return e;
+    if ((e = cudaMalloc(&ws->lc, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters)))) return e;
+    if ((e = cudaMemset(ws->qctl, 0, 4 * sizeof(QCtl)))) return e;
+    if ((e = cudaMemset(ws->misc, 0, 16 * 8))) return e;
+    ws->bytes += 4 * sizeof(QCtl) + 128 + (MGK_MAX_HOPS + 2) * sizeof(LevelCounters);
+    return cudaSuccess;
+}
+
+void destroy_ws(Workspace* ws, bool own_stream) {
+    cudaFree(ws->visited);
+    for (auto* p : ws->fb) cudaFree(p);
+    for (auto* p : ws->ss_items) cudaFree(p);
+    cudaFree(ws->lv);
+    cudaFree(ws->lf[0]);
+    cudaFree(ws->lf[1]);
+    cudaFree(ws->touched);
+    cudaFree(ws->rlog);
+    for (auto* p : ws->ms_items) cudaFree(p);
+    cudaFree(ws->lane_cnt);
+    cudaFree(ws->active);
+    cudaFree(ws->qctl);
+    cudaFree(ws->misc);
+    cudaFree(ws->lc);
+    cudaFree(ws->d_seeds);
+    cudaFree(ws->d_counts);
+    if (ws->h_pinned) cudaFreeHost(ws->h_pinned);
+    if (ws->ev0) cudaEventDestroy(ws->ev0);
+    if (ws->ev1) cudaEventDestroy(ws->ev1);
+    if (own_stream && ws->stream) cudaStreamDestroy(ws->stream);
+}
+
+Workspace* acquire_ws(Graph* g, int* rc) {
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        if (!g->free_ws.empty()) {
+            Workspace* ws = g->free_ws.back().release();
+            g->free_ws.pop_back();
+            return ws;
+        }
+    }
+    auto* ws = new (std::nothrow) Workspace();
+    if (!ws) {
+        *rc = fail(MGK_ENOMEM, "out of host memory");
+        return nullptr;
+    }
+    cudaError_t e = create_ws(g, ws, true);
+    if (e) {
+        destroy_ws(ws, true);
+        delete ws;
+        *rc = fail_cuda(e, "workspace");
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->all_ws.push_back(ws);
+    return ws;
+}
+
+void release_ws(Graph* g, Workspace* ws) {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->free_ws.emplace_back(ws);
+}
+
+int pick_words(const Graph* g, uint64_t nseeds) {
+    if (g->tuning.lanes_words) return (int)g->tuning.lanes_words;
+    const uint64_t want = (nseeds + 63) / 64;
+    int W = 1;
+    while (W < 8 && (uint64_t)W < want) W <<= 1;
+    return W;
+}
+
+int check_query(const Graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k) {
+    // execute.cpp:348-354: seed first, then k
+    for (uint64_t i = 0; i < nseeds; ++i)
+        if (seeds[i] >= g->dg.n)
+            return fail(MGK_ECONTRACT, "k-hop seed %llu is not an allocated node",
+                        (unsigned long long)seeds[i]);
+    if (k < 1 || k > MGK_MAX_HOPS)
+        return fail(MGK_ECONTRACT, "k-hop count %u outside [1, %d]", k, MGK_MAX_HOPS);
+    return MGK_OK;
+}
+
+cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_t nseeds,
+                       uint32_t k, int mode, int engine, unsigned long long* d_counts,
+                       cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
+                       int* W_out) {
+    cudaError_t e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
+    if (e) return e;
+    if (nseeds == 0) return cudaSuccess;
+    Launch L{};
+    L.g = g;
+    L.ws = ws;
+    L.d_seeds = d_seeds;
+    L.nseeds = nseeds;
+    L.k = k;
+    L.mode = mode;
+    L.d_counts = d_counts;
+    L.stream = stream;
+    L.tuning = g->tuning;
+    if (engine == MGK_ENGINE_AUTO) engine = nseeds == 1 ? MGK_ENGINE_SINGLE : MGK_ENGINE_LANES;
+    *used_engine = engine;
+    if (engine == MGK_ENGINE_SINGLE) {
+        e = launch_single(L);
+        *W_out = 0;
+    } else {
+        L.lanes_words = pick_words(g, nseeds);
+        *W_out = L.lanes_words;
+        e = launch_lanes(L);
+    }
+    *grid = L.grid;
+    *block = L.block;
+    return e;
+}
+
+cudaError_t ensure_staging(Workspace* ws, uint64_t nseeds) {
+    if (ws->seeds_cap >= nseeds) return cudaSuccess;
+    cudaFree(ws->d_seeds);
+    cudaFree(ws->d_counts);
+    if (ws->h_pinned) cudaFreeHost(ws->h_pinned);
+    ws->d_seeds = nullptr;
+    ws->d_counts = nullptr;
+    ws->h_pinned = nullptr;
+    ws->seeds_cap = 0;
+    const uint64_t cap = std::max<uint64_t>(nseeds, 1024);
+    cudaError_t e;
+    if ((e = cudaMalloc(&ws->d_seeds, cap * 4))) return e;
+    if ((e = cudaMalloc(&ws->d_counts, cap * 8))) return e;
+    if ((e = cudaMallocHost(&ws->h_pinned, cap * 8))) return e;
+    ws->seeds_cap = cap;
+    return cudaSuccess;
+}
+
+void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint64_t nseeds,
+                uint32_t grid, uint32_t block, float ms) {
+    std::memset(st, 0, sizeof *st);
+    st->engine = (uint32_t)engine;
+    st->lanes = engine == MGK_ENGINE_LANES ? 64u * (uint32_t)W : 1u;
+    st->batches = (uint32_t)(engine == MGK_ENGINE_LANES ? (nseeds + st->lanes - 1) / st->lanes : nseeds);
+    st->grid = grid;
+    st->block = block;
+    st->kernel_ms = ms;
+    for (int h = 0; h <= MGK_MAX_HOPS; ++h) {
+        mgk_level& L = st->level[h];
+        L.frontier = lc[h].frontier;
+        L.vertices = lc[h].vertices;
+        L.edges = lc[h].edges;
+        L.union_edges = lc[h].union_edges;
+        L.scanned = lc[h].scanned;
+        L.candidates = lc[h].candidates;
+        L.runs = lc[h].runs;
+        L.pull_runs = lc[h].pull_runs;
+        L.ns = lc[h].ns;
+        if (h > 0 && L.runs) st->hops = (uint32_t)h;
+    }
+}
+
+int validate_csr_u64(uint64_t nrows, uint64_t nnz, const uint64_t* rp, const uint64_t* ci) {
+    if (nrows >= 0xFFFFFFFFull) return fail(MGK_ERANGE, "graph has %llu rows; the device path holds < 2^32", (unsigned long long)nrows);
+    if (nnz >= 0xFFFFFFFFull) return fail(MGK_ERANGE, "graph has %llu entries; the device path holds < 2^32", (unsigned long long)nnz);
+    if (rp[0] != 0 || rp[nrows] != nnz)
+        return fail(MGK_ECONTRACT, "row_ptr must start at 0 and end at nnz (%llu)", (unsigned long long)nnz);
+    for (uint64_t r = 0; r < nrows; ++r)
+        if (rp[r + 1] < rp[r]) return fail(MGK_ECONTRACT, "row_ptr decreases at row %llu", (unsigned long long)r);
+    for (uint64_t p = 0; p < nnz; ++p)
+        if (ci[p] >= nrows)
+            return fail(MGK_ECONTRACT, "column %llu out of range for %llu rows", (unsigned long long)ci[p],
+                        (unsigned long long)nrows);
+    return MGK_OK;
+}
+
+int finish_upload(int device, uint64_t nrows, uint64_t nnz, const uint32_t* rp, const uint32_t* ci,
+                  mgk_graph** out) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MGK_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(MGK_ECONTRACT, "device %d out of range [0, %d)", device, ndev);
+    DeviceGuard dg(device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = device;
+    h->g.dg.n = (uint32_t)nrows;
+    h->g.dg.m = nnz;
+    cudaError_t e = build_device_graph(&h->g, rp, ci);
+    if (e) {
+        free_device_graph(&h->g);
+        delete h;
+        return fail_cuda(e, "graph upload");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
+}  // namespace
+
+void set_last_error(const std::string& msg) { t_err = msg; }
+
+}  // namespace mgk
+
+using namespace mgk;
+
+extern "C" {
+
+const char* mgk_last_error(void) { return t_err.c_str(); }
+int mgk_abi_version(void) { return MGK_ABI_VERSION; }
+
+int mgk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int mgk_graph_upload(int device, uint64_t nrows, uint64_t nnz, const uint64_t* row_ptr,
+                     const uint64_t* col_idx, mgk_graph** out) {
+    if (!out || !row_ptr || (nnz && !col_idx)) return fail(MGK_ECONTRACT, "null argument");
+    int rc = validate_csr_u64(nrows, nnz, row_ptr, col_idx);
+    if (rc) return rc;
+    std::vector<uint32_t> rp(nrows + 1), ci(std::max<uint64_t>(nnz, 1));
+    parallel_for(nrows + 1, [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) rp[i] = (uint32_t)row_ptr[i];
+    });
+    parallel_for(nnz, [&](uint64_t a, uint64_t b) {
+        for (uint64_t i = a; i < b; ++i) ci[i] = (uint32_t)col_idx[i];
+    });
+    return finish_upload(device, nrows, nnz, rp.data(), ci.data(), out);
+}
+
+int mgk_graph_upload_u32(int device, uint64_t nrows, uint64_t nnz, const uint32_t* row_ptr,
+                         const uint32_t* col_idx, mgk_graph** out) {
+    if (!out || !row_ptr || (nnz && !col_idx)) return fail(MGK_ECONTRACT, "null argument");
+    if (nrows >= 0xFFFFFFFFull || nnz >= 0xFFFFFFFFull)
+        return fail(MGK_ERANGE, "graph exceeds uint32 device indices");
+    if (row_ptr[0] != 0 || row_ptr[nrows] != nnz)
+        return fail(MGK_ECONTRACT, "row_ptr must start at 0 and end at nnz (%llu)", (unsigned long long)nnz);
+    int bad = 0;
+    parallel_for(nrows, [&](uint64_t a, uint64_t b) {
+        for (uint64_t r = a; r < b; ++r)
+            if (row_ptr[r + 1] < row_ptr[r]) bad = 1;
+    });
+    if (bad) return fail(MGK_ECONTRACT, "row_ptr decreases");
+    parallel_for(nnz, [&](uint64_t a, uint64_t b) {
+        for (uint64_t p = a; p < b; ++p)
+            if (col_idx[p] >= nrows) bad = 2;
+    });
+    if (bad) return fail(MGK_ECONTRACT, "column out of range for %llu rows", (unsigned long long)nrows);
+    return finish_upload(device, nrows, nnz, row_ptr, col_idx, out);
+}
+
+int mgk_graph_from_edges(int device, uint64_t nrows, uint64_t nedges, const uint32_t* src,
+                         const uint32_t* dst, mgk_graph** out) {
+    if (!out || (nedges && (!src || !dst))) return fail(MGK_ECONTRACT, "null argument");
+    if (nrows >= 0xFFFFFFFFull) return fail(MGK_ERANGE, "graph exceeds uint32 device indices");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MGK_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(MGK_ECONTRACT, "device %d out of range", device);
+    // bench.cpp:189-193 contract, checked on the host so the message names the edge
+    for (uint64_t i = 0; i < nedges; ++i)
+        if (src[i] >= nrows || dst[i] >= nrows)
+            return fail(MGK_ECONTRACT, "edge (%u, %u) outside the %llu-node range", src[i], dst[i],
+                        (unsigned long long)nrows);
+    DeviceGuard dg(device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = device;
+    h->g.dg.n = (uint32_t)nrows;
+    cudaError_t e = build_device_graph_from_edges(&h->g, src, dst, nedges);
+    if (e) {
+        free_device_graph(&h->g);
+        delete h;
+        return fail_cuda(e, "graph build");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
+int mgk_graph_free(mgk_graph* h) {
+    if (!h) return MGK_OK;
+    DeviceGuard dg(h->g.device);
+    cudaDeviceSynchronize();
+    for (Workspace* ws : h->g.all_ws) {
+        destroy_ws(ws, true);
+        delete ws;
+    }
+    for (auto& f : h->g.free_ws) f.release();
+    for (auto& kv : h->stream_ws) {
+        destroy_ws(kv.second, false);
+        delete kv.second;
+    }
+    free_device_graph(&h->g);
+    delete h;
+    return MGK_OK;
+}
+
+int mgk_graph_info(const mgk_graph* h, uint64_t* nrows, uint64_t* nnz, int* device) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (nrows) *nrows = h->g.dg.n;
+    if (nnz) *nnz = h->g.dg.m;
+    if (device) *device = h->g.device;
+    return MGK_OK;
+}
+
+uint64_t mgk_graph_device_bytes(const mgk_graph* h) {
+    if (!h) return 0;
+    uint64_t b = h->g.bytes;
+    for (Workspace* ws : h->g.all_ws) b += ws->bytes;
+    for (auto& kv : h->stream_ws) b += kv.second->bytes;
+    return b;
+}
+
+int mgk_graph_download_csr(const mgk_graph* h, uint32_t* row_ptr, uint32_t* col_idx) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    DeviceGuard dg(h->g.device);
+    cudaError_t e = cudaSuccess;
+    if (row_ptr) e = cudaMemcpy(row_ptr, h->g.rp, (size_t)(h->g.dg.n + 1) * 4, cudaMemcpyDeviceToHost);
+    if (!e && col_idx && h->g.dg.m) e = cudaMemcpy(col_idx, h->g.ci, h->g.dg.m * 4, cudaMemcpyDeviceToHost);
+    return e ? fail_cuda(e, "download") : MGK_OK;
+}
+
+int mgk_graph_download_csc(const mgk_graph* h, uint32_t* col_ptr, uint32_t* row_idx) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    DeviceGuard dg(h->g.device);
+    cudaError_t e = cudaSuccess;
+    if (col_ptr) e = cudaMemcpy(col_ptr, h->g.cp, (size_t)(h->g.dg.n + 1) * 4, cudaMemcpyDeviceToHost);
+    if (!e && row_idx && h->g.dg.m) e = cudaMemcpy(row_idx, h->g.ri, h->g.dg.m * 4, cudaMemcpyDeviceToHost);
+    return e ? fail_cuda(e, "download") : MGK_OK;
+}
+
+int mgk_graph_set_tuning(mgk_graph* h, const mgk_tuning* t) {
+    if (!h || !t) return fail(MGK_ECONTRACT, "null argument");
+    if (t->force_dir > 2) return fail(MGK_ECONTRACT, "force_dir must be 0, 1 or 2");
+    if (t->lanes_words && t->lanes_words != 1 && t->lanes_words != 2 && t->lanes_words != 4 &&
+        t->lanes_words != 8)
+        return fail(MGK_ECONTRACT, "lanes_words must be 1, 2, 4 or 8");
+    std::lock_guard<std::mutex> lk(h->g.mu);
+    if (t->alpha) h->g.tuning.alpha = t->alpha;
+    if (t->beta) h->g.tuning.beta = t->beta;
+    h->g.tuning.force_dir = t->force_dir;
+    h->g.tuning.lanes_words = t->lanes_words;
+    return MGK_OK;
+}
+
+int mgk_graph_get_tuning(const mgk_graph* h, mgk_tuning* t) {
+    if (!h || !t) return fail(MGK_ECONTRACT, "null argument");
+    t->alpha = h->g.tuning.alpha;
+    t->beta = h->g.tuning.beta;
+    t->force_dir = h->g.tuning.force_dir;
+    t->lanes_words = h->g.tuning.lanes_words;
+    return MGK_OK;
+}
+
+int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                      int engine, uint64_t* counts, mgk_stats* stats) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (nseeds && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+    Graph* g = &h->g;
+    int rc = check_query(g, seeds, nseeds, k);
+    if (rc) return rc;
+    if (nseeds >= 0xFFFFFFFFull) return fail(MGK_ECONTRACT, "too many seeds");
+    DeviceGuard dg(g->device);
+    Workspace* ws = acquire_ws(g, &rc);
+    if (!ws) return rc;
+    cudaError_t e = ensure_staging(ws, nseeds);
+    if (e) {
+        release_ws(g, ws);
+        return fail_cuda(e, "staging");
+    }
+    // seeds: host uint64 -> pinned uint32 -> device (inside the caller's timing)
+    uint32_t* hs = reinterpret_cast<uint32_t*>(ws->h_pinned);
+    for (uint64_t i = 0; i < nseeds; ++i) hs[i] = (uint32_t)seeds[i];
+    uint32_t grid = 0, block = 0;
+    int used = 0, W = 0;
+    float ms = 0.f;
+    do {
+        if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
+        if ((e = cudaEventRecord(ws->ev0, ws->stream))) break;
+        if ((e = run_engine(g, ws, ws->d_seeds, nseeds, k, mode, engine, ws->d_counts, ws->stream,
+                            &grid, &block, &used, &W)))
+            break;
+        if ((e = cudaEventRecord(ws->ev1, ws->stream))) break;
+        if ((e = cudaMemcpyAsync(ws->h_pinned, ws->d_counts, nseeds * 8, cudaMemcpyDeviceToHost, ws->stream)))
+            break;
+        if ((e = cudaStreamSynchronize(ws->stream))) break;
+        std::memcpy(counts, ws->h_pinned, nseeds * 8);
+        if (stats) {
+            cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+            LevelCounters lc[MGK_MAX_HOPS + 2];
+            if ((e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost))) break;
+            fill_stats(stats, lc, used, W, nseeds, grid, block, ms);
+        }
+    } while (0);
+    release_ws(g, ws);
+    return e ? fail_cuda(e, "k-hop count") : MGK_OK;
+}
+
+int mgk_khop_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                   uint64_t* counts) {
+    return mgk_khop_count_ex(h, seeds, nseeds, k, mode, MGK_ENGINE_AUTO, counts, nullptr);
+}
+
+int mgk_khop_count_device(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
+                          int mode, int engine, uint64_t* d_counts, void* stream) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (k < 1 || k > MGK_MAX_HOPS) return fail(MGK_ECONTRACT, "k-hop count %u outside [1, %d]", k, MGK_MAX_HOPS);
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+    Graph* g = &h->g;
+    DeviceGuard dg(g->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    Workspace* ws = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        auto it = h->stream_ws.find(s);
+        if (it != h->stream_ws.end()) ws = it->second;
+    }
+    if (!ws) {
+        ws = new (std::nothrow) Workspace();
+        if (!ws) return fail(MGK_ENOMEM, "out of host memory");
+        cudaError_t e = create_ws(g, ws, false);
+        if (e) {
+            destroy_ws(ws, false);
+            delete ws;
+            return fail_cuda(e, "workspace");
+        }
+        ws->stream = s;
+        std::lock_guard<std::mutex> lk(g->mu);
+        h->stream_ws[s] = ws;
+    }
+    uint32_t grid = 0, block = 0;
+    int used = 0, W = 0;
+    cudaError_t e = run_engine(g, ws, d_seeds, nseeds, k, mode, engine,
+                               reinterpret_cast<unsigned long long*>(d_counts), s, &grid, &block, &used, &W);
+    ws->misc_engine = used;
+    ws->misc_W = W;
+    ws->misc_grid = grid;
+    ws->misc_block = block;
+    ws->misc_nseeds = nseeds;
+    return e ? fail_cuda(e, "k-hop count (device)") : MGK_OK;
+}
+
+int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
+    if (!h || !stats) return fail(MGK_ECONTRACT, "null argument");
+    Workspace* ws = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(h->g.mu);
+        auto it = h->stream_ws.find((cudaStream_t)stream);
+        if (it != h->stream_ws.end()) ws = it->second;
+    }
+    if (!ws) return fail(MGK_ECONTRACT, "no device-path call was made on this stream");
+    DeviceGuard dg(h->g.device);
+    LevelCounters lc[MGK_MAX_HOPS + 2];
+    cudaError_t e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
+    if (e) return fail_cuda(e, "stats");
+    fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f);
+    return MGK_OK;
+}
+
+int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_t* ids, uint64_t cap,
+                      uint64_t* n_out) {
+    if (!h || !n_out || (cap && !ids)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    Graph* g = &h->g;
+    int rc = check_query(g, &seed, 1, k);
+    if (rc) return rc;
+    DeviceGuard dg(g->device);
+    Workspace* ws = acquire_ws(g, &rc);
+    if (!ws) return rc;
+    cudaError_t e = ensure_staging(ws, 1);
+    unsigned long long* d_ids = nullptr;
+    unsigned long long* d_n = nullptr;
+    do {
+        if (e) break;
+        uint32_t s32 = (uint32_t)seed;
+        reinterpret_cast<uint32_t*>(ws->h_pinned)[0] = s32;
+        if ((e = cudaMemcpyAsync(ws->d_seeds, ws->h_pinned, 4, cudaMemcpyHostToDevice, ws->stream))) break;
+        uint32_t grid = 0, block = 0;
+        int used = 0, W = 0;
+        if ((e = run_engine(g, ws, ws->d_seeds, 1, k, mode, MGK_ENGINE_SINGLE, ws->d_counts, ws->stream,
+                            &grid, &block, &used, &W)))
+            break;
+        if ((e = cudaMalloc(&d_ids, (size_t)std::max<uint32_t>(g->dg.n, 1) * 8))) break;
+        if ((e = cudaMalloc(&d_n, 8))) break;
+        if ((e = single_result_ids(g, ws, k, mode, s32, d_ids, d_n, ws->stream))) break;
+        unsigned long long n = 0;
+        if ((e = cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, ws->stream))) break;
+        if ((e = cudaStreamSynchronize(ws->stream))) break;
+        *n_out = n;
+        const uint64_t take = std::min<uint64_t>(n, cap);
+        if (take && (e = cudaMemcpy(ids, d_ids, take * 8, cudaMemcpyDeviceToHost))) break;
+    } while (0);
+    cudaFree(d_ids);
+    cudaFree(d_n);
+    release_ws(g, ws);
+    return e ? fail_cuda(e, "k-hop frontier") : MGK_OK;
+}
+
+}  // extern "C"

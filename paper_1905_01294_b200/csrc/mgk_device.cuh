@@ -1,0 +1,190 @@
+// Device-side building blocks shared by the traversal engines (sm_100a).
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "mgk_internal.cuh"
+
+namespace mgk {
+namespace dev {
+
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Loads of mutable state that other SMs update inside the same launch go to
+// L2 (ld.global.cg) so a stale L1 line never hides a concurrent update.
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_cg(const unsigned long long* p) {
+    return __ldcg(p);
+}
+__device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
+    return *reinterpret_cast<const volatile unsigned int*>(p);
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+// Inclusive warp scan (all 32 lanes must call).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(kFull, v, d);
+        if (lane >= (uint32_t)d) v += t;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(kFull, v, d);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_or_u64(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v |= __shfl_xor_sync(kFull, v, d);
+    return v;
+}
+
+// Smallest lane j whose inclusive prefix incl_j > x (x < incl_31), via a
+// 5-step shuffle binary search. All lanes must call (x may differ per lane).
+__device__ __forceinline__ uint32_t warp_owner(uint32_t incl, uint32_t x) {
+    uint32_t lo = 0;
+#pragma unroll
+    for (uint32_t step = 16; step >= 1; step >>= 1) {
+        const uint32_t probe = __shfl_sync(kFull, incl, lo + step - 1);
+        if (probe <= x) lo += step;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Per-warp shared-memory staging of discovered vertex ids. Discoveries are
+// appended with a ballot (no atomics); a global reservation is taken only
+// when the stage is nearly full or at the end of a phase, so a hot queue tail
+// sees one atomic per ~200 vertices instead of one per warp step.
+template <int CAP>
+struct Stage {
+    uint32_t* buf;  // CAP entries in shared memory, private to this warp
+    uint32_t n;     // warp-uniform fill
+    __device__ __forceinline__ void push(bool pred, uint32_t v) {
+        const unsigned m = __ballot_sync(kFull, pred);
+        if (pred) buf[n + __popc(m & lanemask_lt())] = v;
+        n += __popc(m);
+        __syncwarp();
+    }
+    __device__ __forceinline__ bool full() const { return n > CAP - 32; }
+};
+
+// Warp-wide: append n staged ids to list[*tail ...] (one atomic).
+__device__ __forceinline__ void emit_list(const uint32_t* buf, uint32_t n, uint32_t* list,
+                                          unsigned int* tail) {
+    if (n == 0) return;
+    uint32_t base = 0;
+    if (lane_id() == 0) base = atomicAdd(tail, n);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t i = lane_id(); i < n; i += 32) list[base + i] = buf[i];
+    __syncwarp();
+}
+
+// Warp-wide: append push work items for n staged vertices: each vertex with
+// out-degree d yields ceil(d / kChunk) slices of its CSR row. One reservation
+// per call. Item is uint2 {begin, end} or uint4 {begin, end, src, 0}.
+__device__ __forceinline__ void store_item(uint2* items, uint32_t at, uint32_t s, uint32_t e,
+                                           uint32_t) {
+    items[at] = make_uint2(s, e);
+}
+__device__ __forceinline__ void store_item(uint4* items, uint32_t at, uint32_t s, uint32_t e,
+                                           uint32_t src) {
+    items[at] = make_uint4(s, e, src, 0);
+}
+
+template <typename Item>
+__device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, const uint32_t* buf,
+                                           uint32_t n, Item* items, unsigned int* nitems) {
+    if (n == 0) return;
+    const uint32_t lane = lane_id();
+    uint32_t tot = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t u = buf[i];
+        tot += (__ldg(rp + u + 1) - __ldg(rp + u) + kChunk - 1) / kChunk;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
+    if (tot == 0) return;
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(nitems, tot);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t u = 0, b = 0, deg = 0;
+        if (i < n) {
+            u = buf[i];
+            b = __ldg(rp + u);
+            deg = __ldg(rp + u + 1) - b;
+        }
+        const uint32_t nit = (deg + kChunk - 1) / kChunk;
+        const uint32_t incl = warp_incl_scan(nit);
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const uint32_t excl = incl - nit;
+        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
+            const uint32_t bj = __shfl_sync(kFull, b, j);
+            const uint32_t dj = __shfl_sync(kFull, deg, j);
+            const uint32_t ej = __shfl_sync(kFull, excl, j);
+            const uint32_t uj = __shfl_sync(kFull, u, j);
+            if (x < total) {
+                const uint32_t s = bj + (x - ej) * kChunk;
+                store_item(items, base + x, s, min(s + kChunk, bj + dj), uj);
+            }
+        }
+        base += total;
+    }
+    __syncwarp();
+}
+
+// Block-level accumulation of counters, flushed once per phase.
+struct PhaseAcc {
+    unsigned long long frontier, vertices, edges, union_edges, scanned, candidates;
+    __device__ void zero() { frontier = vertices = edges = union_edges = scanned = candidates = 0; }
+};
+
+// Flush per-thread counters into a LevelCounters record with one atomic per
+// warp per field (values reduced over the warp first).
+__device__ __forceinline__ void flush_counters(LevelCounters* lc, PhaseAcc& a) {
+    const unsigned long long f = warp_sum_u64(a.frontier);
+    const unsigned long long v = warp_sum_u64(a.vertices);
+    const unsigned long long e = warp_sum_u64(a.edges);
+    const unsigned long long u = warp_sum_u64(a.union_edges);
+    const unsigned long long s = warp_sum_u64(a.scanned);
+    const unsigned long long c = warp_sum_u64(a.candidates);
+    if (lane_id() == 0) {
+        if (f) atomicAdd(&lc->frontier, f);
+        if (v) atomicAdd(&lc->vertices, v);
+        if (e) atomicAdd(&lc->edges, e);
+        if (u) atomicAdd(&lc->union_edges, u);
+        if (s) atomicAdd(&lc->scanned, s);
+        if (c) atomicAdd(&lc->candidates, c);
+    }
+    a.zero();
+}
+
+}  // namespace dev
+}  // namespace mgk

@@ -1,0 +1,294 @@
+// Device-resident graph: uint32 CSR + CSC built once per upload.
+//
+// Replaces, for the k-hop path, the store's read side:
+//   PropertyGraph::relation_matrix   proj/core/src/graph.cpp:84-88
+//   PropertyGraph::transposed_matrix proj/core/src/graph.cpp:90-102
+//   transpose (counting sort)        proj/core/src/sparse.cpp:379-403
+//   flush_slot (sort + dedup)        proj/core/src/graph.cpp:182-215
+// The CSC is produced by a radix sort of (col << 32 | row) keys on the GPU,
+// so in-neighbour lists come out ascending exactly like the reference's
+// transpose. A zero-in-degree bitmap lets the pull pass skip vertices that
+// can never be reached.
+#include <cub/cub.cuh>
+
+#include "mgk_internal.cuh"
+
+namespace mgk {
+namespace {
+
+#define MGK_TRY(x)                         \
+    do {                                   \
+        cudaError_t e_ = (x);              \
+        if (e_ != cudaSuccess) return e_;  \
+    } while (0)
+
+constexpr int kTB = 256;
+
+inline unsigned blocks_for(uint64_t n) { return (unsigned)std::min<uint64_t>((n + kTB - 1) / kTB, 148ull * 64); }
+
+// row id of every CSR entry (grid-stride over rows; long rows split by a
+// block-per-row pass below would be faster, but this runs once per load).
+__global__ void expand_rows(const uint32_t* rp, uint32_t n, uint64_t m, unsigned long long* keys) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        // upper_bound(rp, p) - 1
+        uint32_t lo = 0, hi = n;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (rp[mid + 1] <= p) lo = mid + 1;
+            else hi = mid;
+        }
+        keys[p] = lo;  // row in the low bits, column filled in by fill_cols
+    }
+}
+
+__global__ void fill_cols(const uint32_t* ci, uint64_t m, unsigned long long* keys) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        keys[p] |= (unsigned long long)ci[p] << 32;
+}
+
+// sorted (major << 32 | minor) keys -> ptr[n+1] over the major ids and the
+// minor ids in order.
+__global__ void keys_to_csr(const unsigned long long* keys, uint64_t m, uint32_t n, uint32_t* ptr,
+                            uint32_t* minor) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p <= m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t cur = p < m ? (keys[p] >> 32) : n;
+        const uint64_t prev = p > 0 ? (keys[p - 1] >> 32) : (uint64_t)-1;
+        if (p < m) minor[p] = (uint32_t)keys[p];
+        for (uint64_t c = prev + 1; c <= cur && c <= n; ++c) ptr[c] = (uint32_t)p;
+    }
+}
+
+__global__ void no_in_bitmap(const uint32_t* cp, uint32_t n, uint32_t nwords, uint32_t* bits) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += gridDim.x * blockDim.x) {
+        uint32_t x = 0;
+        for (uint32_t b = 0; b < 32; ++b) {
+            const uint32_t u = w * 32 + b;
+            if (u >= n || cp[u + 1] == cp[u]) x |= 1u << b;
+        }
+        bits[w] = x;
+    }
+}
+
+__global__ void pack_edges(const uint32_t* src, const uint32_t* dst, uint64_t m, uint32_t n,
+                           unsigned long long* keys, unsigned int* bad) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = src[p], d = dst[p];
+        if (s >= n || d >= n) atomicMin(bad, (unsigned int)(p < 0xFFFFFFFEull ? p : 0xFFFFFFFEull));
+        keys[p] = ((unsigned long long)s << 32) | d;
+    }
+}
+
+// keep[p] = 1 if keys[p] differs from keys[p-1]
+__global__ void mark_unique(const unsigned long long* keys, uint64_t m, uint32_t* keep) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        keep[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1u : 0u;
+}
+
+__global__ void swap_halves(unsigned long long* keys, uint64_t m) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[p];
+        keys[p] = (k << 32) | (k >> 32);
+    }
+}
+
+int key_bits(uint32_t n) {
+    int b = 1;
+    while (b < 32 && (1ull << b) < n) ++b;
+    return b;
+}
+
+cudaError_t radix_sort_keys(unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
+                            int end_bit, cudaStream_t s) {
+    cub::DoubleBuffer<unsigned long long> db(keys, alt);
+    size_t tmp = 0;
+    MGK_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)m, 0, end_bit, s));
+    void* t = nullptr;
+    MGK_TRY(cudaMallocAsync(&t, tmp, s));
+    MGK_TRY(cub::DeviceRadixSort::SortKeys(t, tmp, db, (int64_t)m, 0, end_bit, s));
+    MGK_TRY(cudaFreeAsync(t, s));
+    if (db.Current() != keys) std::swap(keys, alt);
+    return cudaSuccess;
+}
+
+// Given device CSR (rp, ci) fill CSC (cp, ri) and the no_in bitmap.
+cudaError_t build_csc(Graph* g, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    const uint64_t m = g->dg.m;
+    if (m > 0) {
+        unsigned long long *keys = nullptr, *alt = nullptr;
+        MGK_TRY(cudaMallocAsync(&keys, m * 8, s));
+        MGK_TRY(cudaMallocAsync(&alt, m * 8, s));
+        expand_rows<<<blocks_for(m), kTB, 0, s>>>(g->rp, n, m, keys);
+        fill_cols<<<blocks_for(m), kTB, 0, s>>>(g->ci, m, keys);
+        MGK_TRY(radix_sort_keys(keys, alt, m, 32 + key_bits(n), s));
+        keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
+        MGK_TRY(cudaFreeAsync(keys, s));
+        MGK_TRY(cudaFreeAsync(alt, s));
+    } else {
+        MGK_TRY(cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s));
+    }
+    no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
+    return cudaGetLastError();
+}
+
+cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
+    g->dg.n = n;
+    g->dg.nwords = (n + 31) / 32;
+    g->dg.m = m;
+    const size_t mp = (size_t)std::max<uint64_t>(m, 1);
+    MGK_TRY(cudaMalloc(&g->rp, (size_t)(n + 1) * 4));
+    MGK_TRY(cudaMalloc(&g->ci, mp * 4));
+    MGK_TRY(cudaMalloc(&g->cp, (size_t)(n + 1) * 4));
+    MGK_TRY(cudaMalloc(&g->ri, mp * 4));
+    MGK_TRY(cudaMalloc(&g->no_in, (size_t)(g->dg.nwords + 1) * 4));
+    g->bytes = 2 * (size_t)(n + 1) * 4 + 2 * mp * 4 + (size_t)(g->dg.nwords + 1) * 4;
+    g->dg.rp = g->rp;
+    g->dg.ci = g->ci;
+    g->dg.cp = g->cp;
+    g->dg.ri = g->ri;
+    g->dg.no_in = g->no_in;
+    return cudaSuccess;
+}
+
+}  // namespace
+
+cudaError_t exclusive_scan_u32(uint32_t* data, uint32_t n, unsigned long long* total,
+                               cudaStream_t s) {
+    // out-of-place into a temp, then copy back; total = last excl + last value
+    uint32_t* out = nullptr;
+    MGK_TRY(cudaMallocAsync(&out, (size_t)(n + 1) * 4, s));
+    size_t tmp = 0;
+    MGK_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp, data, out, (int)(n + 1), s));
+    void* t = nullptr;
+    MGK_TRY(cudaMallocAsync(&t, tmp, s));
+    // data[n] must be 0 so out[n] is the total; write it first
+    MGK_TRY(cudaMemsetAsync(data + n, 0, 4, s));
+    MGK_TRY(cub::DeviceScan::ExclusiveSum(t, tmp, data, out, (int)(n + 1), s));
+    MGK_TRY(cudaMemcpyAsync(data, out, (size_t)(n + 1) * 4, cudaMemcpyDeviceToDevice, s));
+    // widen the uint32 total into *total
+    MGK_TRY(cudaMemsetAsync(total, 0, 8, s));
+    MGK_TRY(cudaMemcpyAsync(total, out + n, 4, cudaMemcpyDeviceToDevice, s));
+    MGK_TRY(cudaFreeAsync(t, s));
+    MGK_TRY(cudaFreeAsync(out, s));
+    return cudaSuccess;
+}
+
+cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h_ci) {
+    const uint32_t n = g->dg.n;
+    const uint64_t m = g->dg.m;
+    MGK_TRY(alloc_graph(g, n, m));
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    MGK_TRY(cudaMemcpyAsync(g->rp, h_rp, (size_t)(n + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (m) MGK_TRY(cudaMemcpyAsync(g->ci, h_ci, m * 4, cudaMemcpyHostToDevice, s));
+    cudaError_t e = build_csc(g, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e;
+}
+
+cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const uint32_t* h_dst,
+                                          uint64_t nedges) {
+    const uint32_t n = g->dg.n;
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint64_t m = 0;
+    cudaError_t e = cudaSuccess;
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    uint32_t *src = nullptr, *dst = nullptr, *keep = nullptr;
+    unsigned int* bad = nullptr;
+    do {
+        const size_t np = (size_t)std::max<uint64_t>(nedges, 1);
+        if ((e = cudaMallocAsync(&keys, np * 8, s))) break;
+        if ((e = cudaMallocAsync(&alt, np * 8, s))) break;
+        if ((e = cudaMallocAsync(&src, np * 4, s))) break;
+        if ((e = cudaMallocAsync(&dst, np * 4, s))) break;
+        if ((e = cudaMallocAsync(&bad, 4, s))) break;
+        if ((e = cudaMemsetAsync(bad, 0xFF, 4, s))) break;
+        if (nedges) {
+            if ((e = cudaMemcpyAsync(src, h_src, nedges * 4, cudaMemcpyHostToDevice, s))) break;
+            if ((e = cudaMemcpyAsync(dst, h_dst, nedges * 4, cudaMemcpyHostToDevice, s))) break;
+            pack_edges<<<blocks_for(nedges), kTB, 0, s>>>(src, dst, nedges, n, keys, bad);
+        }
+        unsigned int h_bad = 0;
+        if ((e = cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, s))) break;
+        if ((e = cudaStreamSynchronize(s))) break;
+        if (h_bad != 0xFFFFFFFFu) {
+            e = cudaErrorInvalidValue;  // caller reports the ContractError
+            break;
+        }
+        cudaFreeAsync(src, s);
+        cudaFreeAsync(dst, s);
+        src = dst = nullptr;
+        if (nedges) {
+            if ((e = radix_sort_keys(keys, alt, nedges, 32 + key_bits(n), s))) break;
+            // dedup: keep first of each run, compact with cub::DeviceSelect::Flagged
+            if ((e = cudaMallocAsync(&keep, nedges * 4, s))) break;
+            mark_unique<<<blocks_for(nedges), kTB, 0, s>>>(keys, nedges, keep);
+            unsigned long long* d_num = nullptr;
+            if ((e = cudaMallocAsync(&d_num, 8, s))) break;
+            size_t tmp = 0;
+            if ((e = cub::DeviceSelect::Flagged(nullptr, tmp, keys, keep, alt, d_num, (int64_t)nedges, s)))
+                break;
+            void* t = nullptr;
+            if ((e = cudaMallocAsync(&t, tmp, s))) break;
+            if ((e = cub::DeviceSelect::Flagged(t, tmp, keys, keep, alt, d_num, (int64_t)nedges, s)))
+                break;
+            unsigned long long h_num = 0;
+            if ((e = cudaMemcpyAsync(&h_num, d_num, 8, cudaMemcpyDeviceToHost, s))) break;
+            if ((e = cudaStreamSynchronize(s))) break;
+            cudaFreeAsync(t, s);
+            cudaFreeAsync(d_num, s);
+            std::swap(keys, alt);
+            m = h_num;
+        }
+        if (m >= 0xFFFFFFFFull) {
+            e = cudaErrorInvalidValue;
+            break;
+        }
+        g->dg.m = m;
+        if ((e = alloc_graph(g, n, m))) break;
+        if (m) {
+            keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->rp, g->ci);
+        } else {
+            if ((e = cudaMemsetAsync(g->rp, 0, (size_t)(n + 1) * 4, s))) break;
+        }
+        // CSC: swap halves, sort again
+        if (m) {
+            swap_halves<<<blocks_for(m), kTB, 0, s>>>(keys, m);
+            if ((e = radix_sort_keys(keys, alt, m, 32 + key_bits(n), s))) break;
+            keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
+        } else {
+            if ((e = cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s))) break;
+        }
+        no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
+        if ((e = cudaGetLastError())) break;
+        e = cudaStreamSynchronize(s);
+    } while (0);
+    if (keys) cudaFreeAsync(keys, s);
+    if (alt) cudaFreeAsync(alt, s);
+    if (src) cudaFreeAsync(src, s);
+    if (dst) cudaFreeAsync(dst, s);
+    if (keep) cudaFreeAsync(keep, s);
+    if (bad) cudaFreeAsync(bad, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e;
+}
+
+void free_device_graph(Graph* g) {
+    cudaFree(g->rp);
+    cudaFree(g->ci);
+    cudaFree(g->cp);
+    cudaFree(g->ri);
+    cudaFree(g->no_in);
+    g->rp = g->ci = g->cp = g->ri = g->no_in = nullptr;
+}
+
+}  // namespace mgk

@@ -1,0 +1,148 @@
+// Internal declarations shared by the mgk translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mgk.h"
+
+namespace mgk {
+
+constexpr uint32_t kFull = 0xFFFFFFFFu;
+constexpr uint32_t kChunk = 32;  // max adjacency entries per push work item
+
+// ---- device graph -------------------------------------------------------------
+// uint32 CSR + CSC, 256-B aligned (cudaMalloc), immutable after build.
+struct DevGraph {
+    uint32_t n = 0;       // matrix dimension
+    uint32_t nwords = 0;  // ceil(n / 32) bitmap words
+    uint64_t m = 0;       // stored entries
+    const uint32_t* rp = nullptr;     // row_ptr[n+1]
+    const uint32_t* ci = nullptr;     // col_idx[m], ascending per row
+    const uint32_t* cp = nullptr;     // col_ptr[n+1] (CSC)
+    const uint32_t* ri = nullptr;     // row_idx[m], ascending per column
+    const uint32_t* no_in = nullptr;  // bitmap: zero in-degree (and padding ids >= n)
+};
+
+// Per-level device counters, mirrored into mgk_level on the host.
+struct LevelCounters {
+    unsigned long long frontier;
+    unsigned long long vertices;
+    unsigned long long edges;
+    unsigned long long union_edges;
+    unsigned long long scanned;
+    unsigned long long candidates;
+    unsigned int runs;
+    unsigned int pull_runs;
+    unsigned long long ns;
+};
+static_assert(sizeof(LevelCounters) == 8 * 8, "layout");
+
+// Queue control block of one frontier buffer.
+struct QCtl {
+    unsigned int nitems;       // push work items written
+    unsigned int nfound;       // vertices discovered (incl. zero out-degree)
+    unsigned long long edges;  // sum of outdeg over discovered vertices
+    unsigned long long indeg;  // sum of indeg over discovered vertices
+    unsigned long long pad;
+};
+
+struct Tuning {
+    uint32_t alpha = 15;  // push -> pull when frontier edges > unexplored in-edges / alpha
+    uint32_t beta = 24;   // pull -> push when frontier vertices < n / beta
+    uint32_t force_dir = 0;
+    uint32_t lanes_words = 0;  // 0 = auto
+};
+
+// Workspace for one in-flight call. Sized for the graph; reused across calls.
+struct Workspace {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // single-source engine
+    uint32_t* visited = nullptr;
+    uint32_t* fb[3] = {nullptr, nullptr, nullptr};
+    uint2* ss_items[2] = {nullptr, nullptr};
+    // lanes engine (allocated lazily for the widest W used)
+    int lanes_words = 0;
+    unsigned long long* lv = nullptr;     // V  [n * W]
+    unsigned long long* lf[2] = {nullptr, nullptr};  // F  [n * W] x2
+    uint32_t* touched = nullptr;          // [nwords]
+    uint32_t* rlog = nullptr;             // raw discovery log
+    uint64_t rlog_cap = 0;
+    uint4* ms_items[2] = {nullptr, nullptr};
+    unsigned long long* lane_cnt = nullptr;  // [(MGK_MAX_HOPS+1) * 64 * W]
+    unsigned long long* active = nullptr;    // [2 * W]
+    // shared small control block
+    QCtl* qctl = nullptr;                    // [3]
+    unsigned long long* misc = nullptr;      // [16]
+    LevelCounters* lc = nullptr;             // [MGK_MAX_HOPS+1]
+    uint32_t* d_seeds = nullptr;             // staging for host calls
+    unsigned long long* d_counts = nullptr;
+    uint64_t seeds_cap = 0;
+    uint64_t* h_pinned = nullptr;            // pinned host staging (seeds/counts)
+    uint64_t h_pinned_cap = 0;
+    uint64_t bytes = 0;
+    // last device-path launch (mgk_khop_device_stats)
+    int misc_engine = 0, misc_W = 0;
+    uint32_t misc_grid = 0, misc_block = 0;
+    uint64_t misc_nseeds = 0;
+};
+
+struct Graph {
+    int device = 0;
+    DevGraph dg;
+    uint32_t* rp = nullptr;
+    uint32_t* ci = nullptr;
+    uint32_t* cp = nullptr;
+    uint32_t* ri = nullptr;
+    uint32_t* no_in = nullptr;
+    uint64_t bytes = 0;
+    Tuning tuning;
+    std::mutex mu;
+    std::vector<std::unique_ptr<Workspace>> free_ws;
+    std::vector<Workspace*> all_ws;
+    uint64_t ws_bytes = 0;
+};
+
+// ---- engine launch interface (mgk_ss.cu / mgk_ms.cu) ---------------------------
+struct Launch {
+    const Graph* g;
+    Workspace* ws;
+    const uint32_t* d_seeds;
+    uint64_t nseeds;
+    uint32_t k;
+    int mode;
+    unsigned long long* d_counts;
+    cudaStream_t stream;
+    Tuning tuning;
+    int lanes_words;  // LANES engine only
+    uint32_t grid = 0, block = 0;  // out
+};
+
+cudaError_t launch_single(Launch& L);
+cudaError_t launch_lanes(Launch& L);
+// Compacts the final result bitmap of the last single-seed run into sorted ids.
+cudaError_t single_result_ids(const Graph* g, Workspace* ws, uint32_t k, int mode, uint32_t seed,
+                              unsigned long long* d_ids, unsigned long long* d_n, cudaStream_t s);
+
+// In-place exclusive scan of data[0..n) (data must hold n+1 entries); *total
+// (device) receives the sum.
+cudaError_t exclusive_scan_u32(uint32_t* data, uint32_t n, unsigned long long* total,
+                               cudaStream_t s);
+
+cudaError_t ensure_single_ws(const Graph* g, Workspace* ws);
+cudaError_t ensure_lanes_ws(const Graph* g, Workspace* ws, int W);
+
+// graph build (mgk_graph.cu)
+cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h_ci);
+cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const uint32_t* h_dst,
+                                          uint64_t nedges);
+void free_device_graph(Graph* g);
+
+}  // namespace mgk

@@ -1,0 +1,678 @@
+// LANES engine: bit-parallel multi-source k-hop, 64 seeds per uint64 lane word.
+//
+// A batch of up to 64*W seeds shares every adjacency pass: each vertex carries
+// W uint64 words of visited (V), current-frontier (F) and next-frontier bits,
+// bit (i % 64) of word (i / 64) belonging to seed i of the batch. One hop of
+// the reference loop (proj/core/src/execute.cpp:359-363) for all lanes at once:
+//   push:  for each frontier vertex v, each out-neighbour u:
+//              F'[u] |= F[v] & ~V[u]                (vxm with NOT visited mask)
+//   pull:  for each vertex u with a lane still unvisited:
+//              F'[u] = (OR over in-neighbours v of F[v]) & ~V[u] & active,
+//              stopping as soon as every needed lane is covered
+//   then   V[u] |= F'[u]                            (ewise_union)
+// Per-lane counts are popcounts of bit columns (ballot + popc per bit) over
+// the discovered vertices: exact = |F_k| per lane, cumulative = sum over hops.
+// Lanes are independent, so each lane's answer equals the single-seed
+// k_hop_count bit for bit (a lane whose frontier empties stays empty, which is
+// the reference's early exit at :361).
+//
+// Sparse bookkeeping keeps the cost proportional to the vertices a batch
+// touches: a discovery list per hop (raw list R, one entry per vertex whose
+// F' became non-zero) drives the finalize pass, the clearing of the previous
+// frontier and the final clearing of V.
+#include "mgk_device.cuh"
+
+namespace mgk {
+namespace {
+
+using namespace dev;
+
+constexpr int kBlock = 512;
+constexpr int kWarps = kBlock / 32;
+constexpr int kStageCap = 256;
+
+struct MSParams {
+    DevGraph g;
+    const uint32_t* seeds;
+    uint64_t nseeds;
+    uint32_t k;
+    int mode;
+    unsigned long long* counts;
+    unsigned long long* V;
+    unsigned long long* F0;
+    unsigned long long* F1;
+    uint32_t* touched;
+    uint32_t* R0;  // discovery lists, ping-pong by hop parity
+    uint32_t* R1;
+    uint32_t* clog;  // copy of every discovery list of the batch (for clearing V)
+    uint64_t clog_cap;
+    uint4* items0;
+    uint4* items1;
+    unsigned long long* lane_cnt;  // [(k+1) * 64W]
+    unsigned long long* active;    // [2 * W]
+    QCtl* qctl;                    // [2] by hop parity; .pad = push-equivalent edges
+    unsigned long long* misc;      // [0] unexplored in-edges
+    LevelCounters* lc;
+    uint32_t alpha, beta, force_dir;
+};
+
+template <int W>
+struct LaneWord {
+    unsigned long long w[W];
+};
+
+template <int W>
+__device__ __forceinline__ LaneWord<W> load_lw(const unsigned long long* p) {
+    LaneWord<W> r;
+    if constexpr (W == 1) {
+        r.w[0] = p[0];
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i += 2) {
+            const ulonglong2 t = *reinterpret_cast<const ulonglong2*>(p + i);
+            r.w[i] = t.x;
+            r.w[i + 1] = t.y;
+        }
+    }
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ LaneWord<W> load_lw_cg(const unsigned long long* p) {
+    LaneWord<W> r;
+    if constexpr (W == 1) {
+        r.w[0] = __ldcg(p);
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i += 2) {
+            const ulonglong2 t = __ldcg(reinterpret_cast<const ulonglong2*>(p + i));
+            r.w[i] = t.x;
+            r.w[i + 1] = t.y;
+        }
+    }
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ void store_lw(unsigned long long* p, const LaneWord<W>& v) {
+    if constexpr (W == 1) {
+        p[0] = v.w[0];
+    } else {
+#pragma unroll
+        for (int i = 0; i < W; i += 2)
+            *reinterpret_cast<ulonglong2*>(p + i) = make_ulonglong2(v.w[i], v.w[i + 1]);
+    }
+}
+
+__device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
+    return (i & 1) ? P.items1 : P.items0;
+}
+__device__ __forceinline__ uint32_t* R_of(const MSParams& P, uint32_t i) {
+    return (i & 1) ? P.R1 : P.R0;
+}
+__device__ __forceinline__ unsigned long long* F_of(const MSParams& P, uint32_t i) {
+    return (i & 1) ? P.F1 : P.F0;
+}
+
+struct Acc {
+    unsigned long long found, edges, indeg, scanned, candidates, pairs, pe;
+    __device__ void zero() { found = edges = indeg = scanned = candidates = pairs = pe = 0; }
+};
+
+// Block reduce + flush. found/edges/indeg describe discovered vertices (-> q);
+// pairs/pe describe finalized lane-vertex pairs (-> lc / qf).
+__device__ void block_flush(Acc& a, QCtl* q, QCtl* qf, LevelCounters* lc, LevelCounters* lc_next,
+                            unsigned long long* unexplored) {
+    __shared__ unsigned long long s[7];
+    if (threadIdx.x < 7) s[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long v[7] = {a.found, a.edges, a.indeg, a.scanned, a.candidates, a.pairs, a.pe};
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+        v[i] = warp_sum_u64(v[i]);
+        if (lane_id() == 0 && v[i]) atomicAdd(&s[i], v[i]);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (s[0]) atomicAdd(&lc->vertices, s[0]);
+        if (s[1]) atomicAdd(&q->edges, s[1]);
+        if (s[2]) {
+            atomicAdd(&q->indeg, s[2]);
+            atomicAdd(unexplored, 0ULL - s[2]);
+        }
+        if (s[3]) atomicAdd(&lc->scanned, s[3]);
+        if (s[4]) atomicAdd(&lc->candidates, s[4]);
+        if (s[5]) atomicAdd(&lc->frontier, s[5]);
+        if (s[6]) {
+            atomicAdd(&qf->pad, s[6]);
+            if (lc_next) atomicAdd(&lc_next->edges, s[6]);
+        }
+    }
+    __syncthreads();
+    a.zero();
+}
+
+__device__ __forceinline__ void count_discovered(const DevGraph& g, uint32_t u, bool first, Acc& acc) {
+    acc.found += 1;
+    acc.edges += __ldg(g.rp + u + 1) - __ldg(g.rp + u);
+    if (first) acc.indeg += __ldg(g.cp + u + 1) - __ldg(g.cp + u);
+}
+
+// ---- push expand -----------------------------------------------------------------
+template <int W>
+__device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
+                           const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
+                           QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
+                           uint32_t nwarps) {
+    const uint32_t lane = lane_id();
+    const DevGraph& g = P.g;
+    for (uint32_t base = warp_gid * 32; base < nitems; base += nwarps * 32) {
+        const uint32_t idx = base + lane;
+        const uint4 it = idx < nitems ? items[idx] : make_uint4(0, 0, 0, 0);
+        const uint32_t len = it.y - it.x;
+        const uint32_t incl = warp_incl_scan(len);
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const uint32_t off = it.x - (incl - len);
+        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            const bool valid = x < total;
+            const uint32_t j = warp_owner(incl, valid ? x : total - 1);
+            const uint32_t pos = __shfl_sync(kFull, off, j) + x;
+            const uint32_t src = __shfl_sync(kFull, it.z, j);
+            bool first = false;
+            uint32_t u = 0;
+            if (valid) {
+                u = __ldg(g.ci + pos);
+                const LaneWord<W> f = load_lw<W>(Fc + (size_t)src * W);
+                const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
+                LaneWord<W> m;
+                bool any = false;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    m.w[i] = f.w[i] & ~vis.w[i];
+                    any |= m.w[i] != 0;
+                }
+                if (any) {
+                    unsigned long long* fn = Fn + (size_t)u * W;
+                    const LaneWord<W> cur = load_lw_cg<W>(fn);
+                    bool need = false;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        if ((cur.w[i] & m.w[i]) != m.w[i]) {
+                            atomicOr(fn + i, m.w[i]);
+                            need = true;
+                        }
+                    }
+                    if (need) {
+                        const uint32_t bit = 1u << (u & 31);
+                        const uint32_t old = atomicOr(P.touched + (u >> 5), bit);
+                        if (!(old & bit)) {
+                            first = true;
+                            bool fresh = true;
+#pragma unroll
+                            for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
+                            count_discovered(g, u, fresh, acc);
+                        }
+                    }
+                }
+            }
+            acc.scanned += valid;
+            st.push(first, u);
+            if (st.full()) {
+                emit_list(st.buf, st.n, Rn, &qn->nitems);
+                st.n = 0;
+            }
+        }
+    }
+    emit_list(st.buf, st.n, Rn, &qn->nitems);
+    st.n = 0;
+}
+
+// ---- pull expand -------------------------------------------------------------
+template <int W>
+__device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
+                           const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
+                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
+    const uint32_t lane = lane_id();
+    const DevGraph& g = P.g;
+    for (uint32_t w = warp_gid; w < g.nwords; w += nwarps) {
+        const uint32_t noin = __ldg(g.no_in + w);
+        if (noin == kFull) continue;
+        const uint32_t u = w * 32 + lane;
+        LaneWord<W> need, vis;
+#pragma unroll
+        for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
+        bool cand = false;
+        if (!((noin >> lane) & 1u)) {
+            vis = load_lw<W>(P.V + (size_t)u * W);
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                need.w[i] = active.w[i] & ~vis.w[i];
+                cand |= need.w[i] != 0;
+            }
+        }
+        uint32_t b = 0, e = 0;
+        if (cand) {
+            b = __ldg(g.cp + u);
+            e = __ldg(g.cp + u + 1);
+        }
+        LaneWord<W> acc_w;
+#pragma unroll
+        for (int i = 0; i < W; ++i) acc_w.w[i] = 0;
+        uint32_t scanned = 0;
+        if (cand && e - b <= 32) {
+            for (uint32_t p = b; p < e; ++p) {
+                const uint32_t v = __ldg(g.ri + p);
+                const LaneWord<W> f = load_lw<W>(Fc + (size_t)v * W);
+                bool done = true;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    acc_w.w[i] |= f.w[i];
+                    done &= (acc_w.w[i] & need.w[i]) == need.w[i];
+                }
+                ++scanned;
+                if (done) break;
+            }
+        }
+        unsigned big = __ballot_sync(kFull, cand && e - b > 32);
+        while (big) {
+            const int j = __ffs(big) - 1;
+            big &= big - 1;
+            const uint32_t bj = __shfl_sync(kFull, b, j), ej = __shfl_sync(kFull, e, j);
+            LaneWord<W> nj, aj;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                nj.w[i] = __shfl_sync(kFull, need.w[i], j);
+                aj.w[i] = 0;
+            }
+            uint32_t sc = 0;
+            for (uint32_t p0 = bj; p0 < ej; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                LaneWord<W> f;
+                if (p < ej) {
+                    f = load_lw<W>(Fc + (size_t)__ldg(g.ri + p) * W);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < W; ++i) f.w[i] = 0;
+                }
+                bool done = true;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    aj.w[i] |= warp_or_u64(f.w[i]);
+                    done &= (aj.w[i] & nj.w[i]) == nj.w[i];
+                }
+                sc += min(32u, ej - p0);
+                if (done) break;
+            }
+            if ((int)lane == j) {
+                acc_w = aj;
+                scanned += sc;
+            }
+        }
+        bool found = false;
+        if (cand) {
+            LaneWord<W> res;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                res.w[i] = acc_w.w[i] & need.w[i];
+                found |= res.w[i] != 0;
+            }
+            if (found) {
+                store_lw<W>(Fn + (size_t)u * W, res);
+                bool fresh = true;
+#pragma unroll
+                for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
+                count_discovered(g, u, fresh, acc);
+            }
+        }
+        acc.candidates += cand;
+        acc.scanned += scanned;
+        st.push(found, u);
+        if (st.full()) {
+            emit_list(st.buf, st.n, Rn, &qn->nitems);
+            st.n = 0;
+        }
+    }
+    emit_list(st.buf, st.n, Rn, &qn->nitems);
+    st.n = 0;
+}
+
+// ---- finalize: V |= F', lane counts, next-hop items, clear old frontier -------
+template <int W>
+__device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR,
+                               unsigned long long* Fn, bool touched_set, bool want_items,
+                               uint4* items_n, unsigned int* item_tail, bool count_lanes,
+                               unsigned long long* s_cnt, unsigned long long* active_n,
+                               uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
+                               uint32_t warp_gid, uint32_t nwarps) {
+    const uint32_t lane = lane_id();
+    const DevGraph& g = P.g;
+    LaneWord<W> act;
+    unsigned long long cnt[W][2];
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        act.w[i] = 0;
+        cnt[i][0] = cnt[i][1] = 0;
+    }
+    for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
+        const uint32_t idx = base + lane;
+        const bool valid = idx < nR;
+        uint32_t u = 0;
+        LaneWord<W> x;
+#pragma unroll
+        for (int i = 0; i < W; ++i) x.w[i] = 0;
+        bool expand = false;
+        if (valid) {
+            u = Rn[idx];
+            x = load_lw<W>(Fn + (size_t)u * W);
+            unsigned long long* vp = P.V + (size_t)u * W;
+            LaneWord<W> v = load_lw<W>(vp);
+            uint32_t pc = 0;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                v.w[i] |= x.w[i];
+                act.w[i] |= x.w[i];
+                pc += __popcll(x.w[i]);
+            }
+            store_lw<W>(vp, v);
+            if (touched_set) atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
+            if (clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
+            const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
+            acc.pairs += pc;
+            acc.pe += (unsigned long long)deg * pc;
+            expand = want_items && deg > 0;
+        }
+        if (count_lanes) {
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                if (__ballot_sync(kFull, x.w[i] != 0) == 0) continue;
+#pragma unroll 8
+                for (int bb = 0; bb < 64; ++bb) {
+                    const uint32_t c = __popc(__ballot_sync(kFull, (x.w[i] >> bb) & 1ULL));
+                    if ((uint32_t)(bb & 31) == lane) cnt[i][bb >> 5] += c;
+                }
+            }
+        }
+        if (want_items) {
+            st.push(expand, u);
+            if (st.full()) {
+                emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+                st.n = 0;
+            }
+        }
+    }
+    if (want_items) {
+        emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+        st.n = 0;
+    }
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+        const unsigned long long a = warp_or_u64(act.w[i]);
+        if (lane == 0 && a) atomicOr(active_n + i, a);
+    }
+    if (count_lanes) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            if (cnt[i][0]) atomicAdd(&s_cnt[i * 64 + lane], cnt[i][0]);
+            if (cnt[i][1]) atomicAdd(&s_cnt[i * 64 + 32 + lane], cnt[i][1]);
+        }
+    }
+}
+
+template <int W>
+__device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F, uint32_t gtid,
+                           uint32_t nthreads) {
+    LaneWord<W> z;
+#pragma unroll
+    for (int i = 0; i < W; ++i) z.w[i] = 0;
+    for (uint32_t i = gtid; i < n; i += nthreads) store_lw<W>(F + (size_t)R[i] * W, z);
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
+    // qctl[parity] fields in this engine:
+    //   nitems = |R| (discovery list tail), nfound = push items built for the
+    //   frontier, edges = sum of outdeg over R, pad = push-equivalent edges.
+    constexpr uint32_t LB = 64 * W;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ uint32_t s_stage[kWarps][kStageCap];
+    __shared__ unsigned long long s_cnt[LB];
+    const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
+    const uint32_t nthreads = gridDim.x * kBlock;
+    const uint32_t warp_gid = gtid >> 5;
+    const uint32_t nwarps = nthreads >> 5;
+    const DevGraph& g = P.g;
+    Acc acc;
+    acc.zero();
+    Stage<kStageCap> st{s_stage[threadIdx.x >> 5], 0};
+    const uint64_t nbatches = (P.nseeds + LB - 1) / LB;
+    const bool cumulative = P.mode == MGK_CUMULATIVE;
+
+    for (uint64_t bt = 0; bt < nbatches; ++bt) {
+        const uint32_t lanes = (uint32_t)min((uint64_t)LB, P.nseeds - bt * LB);
+        // ---- init ------------------------------------------------------------
+        for (uint32_t i = gtid; i < (P.k + 1) * LB; i += nthreads) P.lane_cnt[i] = 0;
+        if (gtid < 2 * W) P.active[gtid] = 0;
+        if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
+        if (gtid == 0) P.misc[0] = g.m;
+        grid.sync();
+        // ---- seeds: level-0 frontier -------------------------------------------
+        {
+            bool first = false;
+            uint32_t s = 0;
+            if (gtid < lanes) {
+                s = P.seeds[bt * LB + gtid];
+                const unsigned long long bit = 1ULL << (gtid & 63);
+                atomicOr(P.F0 + (size_t)s * W + (gtid >> 6), bit);
+                const uint32_t tb = 1u << (s & 31);
+                first = !(atomicOr(P.touched + (s >> 5), tb) & tb);
+                if (first) count_discovered(g, s, true, acc);
+            }
+            if (blockIdx.x * kBlock < lanes) {
+                st.push(first, s);
+                emit_list(st.buf, st.n, P.R0, &P.qctl[0].nitems);
+                st.n = 0;
+            }
+        }
+        block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], nullptr, &P.misc[0]);
+        grid.sync();
+        // ---- finalize level 0 (V |= F0, hop-1 items) ------------------------------
+        uint32_t nR = ld_volatile(&P.qctl[0].nitems);
+        bool pull = P.force_dir == 2;
+        if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+        __syncthreads();
+        finalize_phase<W>(P, P.R0, nR, P.F0, true, !pull, P.items0, &P.qctl[0].nfound, false,
+                          s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
+        acc.pairs = 0;  // the seeds themselves are never counted
+        block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
+        grid.sync();
+
+        uint64_t clog_used = nR;
+        uint32_t nR_prev = nR;
+        uint32_t hop = 1;
+        for (; hop <= P.k; ++hop) {
+            const uint32_t cur = (hop - 1) & 1, nxt = hop & 1;
+            QCtl* qc = &P.qctl[cur];
+            QCtl* qn = &P.qctl[nxt];  // zeroed by init (hop 1) or the previous finalize
+            unsigned long long* Fc = F_of(P, cur);
+            unsigned long long* Fn = F_of(P, nxt);
+            uint32_t* Rc = R_of(P, cur);
+            uint32_t* Rn = R_of(P, nxt);
+            unsigned long long t0 = 0;
+            if (gtid == 0) {
+                t0 = globaltimer();
+                atomicAdd(&P.lc[hop].runs, 1u);
+                if (pull) atomicAdd(&P.lc[hop].pull_runs, 1u);
+                atomicAdd(&P.lc[hop].union_edges, ld_volatile(&qc->edges));
+            }
+            if (gtid < W) P.active[nxt * W + gtid] = 0;  // rebuilt by this hop's finalize
+            // ---- expand ---------------------------------------------------------------
+            if (pull) {
+                LaneWord<W> act;
+#pragma unroll
+                for (int i = 0; i < W; ++i) act.w[i] = ld_volatile(P.active + cur * W + i);
+                pull_phase<W>(P, Fc, Fn, act, Rn, qn, acc, st, warp_gid, nwarps);
+            } else {
+                push_phase<W>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
+                              st, warp_gid, nwarps);
+            }
+            block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
+            grid.sync();
+            // ---- decide the next hop's direction (uniform) ---------------------------
+            nR = ld_volatile(&qn->nitems);
+            const unsigned long long mf = ld_volatile(&qn->edges);
+            const unsigned long long mu = ld_volatile(&P.misc[0]);
+            const bool was_pull = pull;
+            if (P.force_dir == 1) {
+                pull = false;
+            } else if (P.force_dir == 2) {
+                pull = true;
+            } else if (!pull) {
+                pull = mf * P.alpha > mu;
+            } else {
+                pull = (unsigned long long)nR * P.beta >= g.n;
+            }
+            const bool last = hop == P.k || nR == 0;
+            const bool count_lanes = cumulative || hop == P.k;
+            // ---- finalize -------------------------------------------------------------
+            if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+            if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
+            __syncthreads();
+            finalize_phase<W>(P, Rn, nR, Fn, !was_pull, !last && !pull, items_of(P, nxt),
+                              &qn->nfound, count_lanes, s_cnt, P.active + nxt * W, clog_used,
+                              acc, st, warp_gid, nwarps);
+            clear_list<W>(Rc, nR_prev, Fc, gtid, nthreads);
+            __syncthreads();
+            if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
+                atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
+            block_flush(acc, qn, qn, &P.lc[hop], hop < P.k ? &P.lc[hop + 1] : nullptr,
+                        &P.misc[0]);
+            grid.sync();
+            if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
+            clog_used += nR;
+            nR_prev = nR;
+            if (nR == 0) break;
+        }
+        // ---- answers ------------------------------------------------------------------
+        if (gtid < lanes) {
+            unsigned long long r = 0;
+            if (cumulative) {
+                for (uint32_t h = 1; h <= P.k; ++h) r += P.lane_cnt[h * LB + gtid];
+            } else {
+                r = P.lane_cnt[P.k * LB + gtid];
+            }
+            P.counts[bt * LB + gtid] = r;
+        }
+        // ---- clear V and the last frontier (state is all-zero between batches) ---------
+        const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
+        if (clog_used <= P.clog_cap) {
+            clear_list<W>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
+            clear_list<W>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
+        } else {
+            for (size_t i = gtid; i < (size_t)g.n * W; i += nthreads) {
+                P.V[i] = 0;
+                P.F0[i] = 0;
+                P.F1[i] = 0;
+            }
+        }
+        grid.sync();
+    }
+}
+
+template <int W>
+cudaError_t launch_w(Launch& L) {
+    static int blocks_per_sm = 0, num_sms = 0;
+    cudaError_t e;
+    if (blocks_per_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W>, kBlock,
+                                                                0)))
+            return e;
+        if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
+    }
+    const Graph* gr = L.g;
+    Workspace* ws = L.ws;
+    MSParams P;
+    P.g = gr->dg;
+    P.seeds = L.d_seeds;
+    P.nseeds = L.nseeds;
+    P.k = L.k;
+    P.mode = L.mode;
+    P.counts = L.d_counts;
+    P.V = ws->lv;
+    P.F0 = ws->lf[0];
+    P.F1 = ws->lf[1];
+    P.touched = ws->touched;
+    P.R0 = ws->rlog;
+    P.R1 = ws->rlog + gr->dg.n;
+    P.clog = ws->rlog + 2 * (size_t)gr->dg.n;
+    P.clog_cap = ws->rlog_cap - 2 * (uint64_t)gr->dg.n;
+    P.items0 = ws->ms_items[0];
+    P.items1 = ws->ms_items[1];
+    P.lane_cnt = ws->lane_cnt;
+    P.active = ws->active;
+    P.qctl = ws->qctl;
+    P.misc = ws->misc;
+    P.lc = ws->lc;
+    P.alpha = L.tuning.alpha;
+    P.beta = L.tuning.beta;
+    P.force_dir = L.tuning.force_dir;
+    L.grid = (uint32_t)(blocks_per_sm * num_sms);
+    L.block = kBlock;
+    void* args[] = {&P};
+    return cudaLaunchCooperativeKernel((const void*)ms_kernel<W>, dim3(L.grid), dim3(kBlock), args,
+                                       0, L.stream);
+}
+
+}  // namespace
+
+cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
+    if (ws->lanes_words >= W) return cudaSuccess;
+    cudaError_t e;
+    if (ws->lv) {  // grow: release the narrower buffers
+        cudaFree(ws->lv);
+        cudaFree(ws->lf[0]);
+        cudaFree(ws->lf[1]);
+        cudaFree(ws->lane_cnt);
+        cudaFree(ws->active);
+        ws->lv = ws->lf[0] = ws->lf[1] = ws->lane_cnt = ws->active = nullptr;
+    }
+    const DevGraph& g = gr->dg;
+    const size_t words = (size_t)g.n * W + 2;
+    for (unsigned long long** p : {&ws->lv, &ws->lf[0], &ws->lf[1]}) {
+        if ((e = cudaMalloc(p, words * 8))) return e;
+        if ((e = cudaMemset(*p, 0, words * 8))) return e;
+    }
+    if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
+    if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
+    ws->bytes += 3 * words * 8;
+    if (!ws->touched) {
+        if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;
+        if ((e = cudaMemset(ws->touched, 0, (size_t)(g.nwords + 1) * 4))) return e;
+        ws->rlog_cap = 4 * (uint64_t)g.n + 1024;
+        if ((e = cudaMalloc(&ws->rlog, ws->rlog_cap * 4))) return e;
+        const size_t items = (size_t)(g.m / kChunk + g.n + 64);
+        for (int i = 0; i < 2; ++i)
+            if ((e = cudaMalloc(&ws->ms_items[i], items * sizeof(uint4)))) return e;
+        ws->bytes += (size_t)(g.nwords + 1) * 4 + ws->rlog_cap * 4 + 2 * items * sizeof(uint4);
+    }
+    ws->lanes_words = W;
+    return cudaSuccess;
+}
+
+cudaError_t launch_lanes(Launch& L) {
+    int W = L.lanes_words;
+    cudaError_t e = ensure_lanes_ws(L.g, L.ws, W);
+    if (e) return e;
+    switch (W) {
+        case 1: return launch_w<1>(L);
+        case 2: return launch_w<2>(L);
+        case 4: return launch_w<4>(L);
+        case 8: return launch_w<8>(L);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace mgk

@@ -1,0 +1,249 @@
+"""The k-hop count path, mirroring the reference's interface.
+
+Reference (proj/core/include/matgraph/execute.hpp:52-68, execute.cpp:347-375):
+
+    struct KHopQuery { uint64 seed; uint32 k = 1; RelationRef relation = ANY;
+                       TraverseMode mode = Exact; };
+    BitVector     k_hop_frontier(const PropertyGraph&, const KHopQuery&);
+    std::uint64_t k_hop_count   (const PropertyGraph&, const KHopQuery&);
+
+Here the graph argument is a :class:`DeviceGraph` — the device-resident
+uint32 CSR + CSC of one relation matrix (what ``relation_matrix(rel)``
+returns in the reference, proj/core/src/graph.cpp:84-88) — and the work runs
+in the sm_100a kernels of libmgk.so through the C ABI. Errors mirror the
+reference's classes and texts (proj/core/include/matgraph/error.hpp:10-66):
+``ContractError("k-hop seed 99 is not an allocated node")`` etc.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import ENGINE_AUTO, ENGINE_LANES, ENGINE_SINGLE, MgkStats, MgkTuning
+
+K_MAX_HOPS = 32  # proj/core/include/matgraph/ast.hpp:15
+
+
+class Error(RuntimeError):
+    """matgraph::Error (error.hpp:10-14)."""
+
+
+class ContractError(Error):
+    """matgraph::ContractError (error.hpp:16-19)."""
+
+
+class HarnessError(Error):
+    """matgraph::HarnessError (error.hpp:62-65)."""
+
+
+class DeviceError(Error):
+    """A CUDA failure inside the engine (reported as matgraph::Error)."""
+
+
+def _raise(rc: int):
+    msg = _lib.last_error()
+    if rc == _lib.MGK_ECONTRACT:
+        raise ContractError(msg)
+    if rc == _lib.MGK_EHARNESS:
+        raise HarnessError(msg)
+    if rc == _lib.MGK_ERANGE:
+        raise ContractError(msg)
+    raise DeviceError(msg)
+
+
+def _check(rc: int):
+    if rc != _lib.MGK_OK:
+        _raise(rc)
+
+
+class TraverseMode(enum.IntEnum):
+    """proj/core/include/matgraph/plan.hpp:17."""
+    Exact = 0
+    Cumulative = 1
+
+
+@dataclass
+class KHopQuery:
+    """proj/core/include/matgraph/execute.hpp:53-58 (relation is chosen when the
+    DeviceGraph is built, as relation_matrix(rel) is in the reference)."""
+    seed: int = 0
+    k: int = 1
+    mode: TraverseMode = TraverseMode.Exact
+
+
+@dataclass
+class Tuning:
+    alpha: int = 15
+    beta: int = 24
+    force_dir: int = 0   # 0 auto, 1 push only, 2 pull only
+    lanes_words: int = 0  # 0 auto; else 1, 2, 4, 8 (x64 seeds per batch)
+
+
+class DeviceGraph:
+    """A relation matrix resident on one GPU (uint32 CSR + CSC + zero-in-degree bitmap)."""
+
+    def __init__(self, handle: int, node_count: int | None = None):
+        self._h = C.c_void_p(handle)
+        n, m, dev = C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(_lib.lib().mgk_graph_info(self._h, C.byref(n), C.byref(m), C.byref(dev)))
+        self.nrows, self.nnz, self.device = n.value, m.value, dev.value
+        # KHopQuery seeds are checked against node_count (execute.cpp:348); the
+        # store's capacity (matrix dimension) can be larger (graph.cpp:26).
+        self.node_count = self.nrows if node_count is None else int(node_count)
+
+    # -- construction ---------------------------------------------------------
+    @classmethod
+    def from_csr(cls, row_ptr, col_idx, device: int = 0, node_count: int | None = None):
+        """Upload a SparseMatrix-shaped CSR (uint64 like the reference, or uint32)."""
+        row_ptr = np.ascontiguousarray(row_ptr)
+        col_idx = np.ascontiguousarray(col_idx)
+        nrows = len(row_ptr) - 1
+        h = C.c_void_p()
+        L = _lib.lib()
+        if row_ptr.dtype == np.uint32 and col_idx.dtype == np.uint32:
+            ci = col_idx if len(col_idx) else np.zeros(1, np.uint32)
+            _check(L.mgk_graph_upload_u32(device, nrows, len(col_idx), row_ptr.ctypes.data,
+                                          ci.ctypes.data, C.byref(h)))
+        else:
+            rp = np.ascontiguousarray(row_ptr, np.uint64)
+            ci = np.ascontiguousarray(col_idx, np.uint64)
+            ci = ci if len(ci) else np.zeros(1, np.uint64)
+            _check(L.mgk_graph_upload(device, nrows, len(col_idx), rp.ctypes.data, ci.ctypes.data,
+                                      C.byref(h)))
+        return cls(h.value, node_count)
+
+    @classmethod
+    def from_edges(cls, src, dst, node_count: int, device: int = 0):
+        """build_bench_graph (bench.cpp:185-198) on the device: sort + dedup + CSR/CSC."""
+        src = np.ascontiguousarray(src, np.uint32)
+        dst = np.ascontiguousarray(dst, np.uint32)
+        h = C.c_void_p()
+        s = src if len(src) else np.zeros(1, np.uint32)
+        d = dst if len(dst) else np.zeros(1, np.uint32)
+        _check(_lib.lib().mgk_graph_from_edges(device, max(node_count, 1), len(src), s.ctypes.data,
+                                               d.ctypes.data, C.byref(h)))
+        return cls(h.value, node_count)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            _lib.lib().mgk_graph_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    # -- inspection -------------------------------------------------------------
+    def csr(self):
+        rp = np.zeros(self.nrows + 1, np.uint32)
+        ci = np.zeros(max(self.nnz, 1), np.uint32)
+        _check(_lib.lib().mgk_graph_download_csr(self._h, rp.ctypes.data, ci.ctypes.data))
+        return rp, ci[: self.nnz]
+
+    def csc(self):
+        cp = np.zeros(self.nrows + 1, np.uint32)
+        ri = np.zeros(max(self.nnz, 1), np.uint32)
+        _check(_lib.lib().mgk_graph_download_csc(self._h, cp.ctypes.data, ri.ctypes.data))
+        return cp, ri[: self.nnz]
+
+    def device_bytes(self) -> int:
+        return int(_lib.lib().mgk_graph_device_bytes(self._h))
+
+    def set_tuning(self, t: Tuning):
+        tt = MgkTuning(t.alpha, t.beta, t.force_dir, t.lanes_words)
+        _check(_lib.lib().mgk_graph_set_tuning(self._h, C.byref(tt)))
+
+    def get_tuning(self) -> Tuning:
+        tt = MgkTuning()
+        _check(_lib.lib().mgk_graph_get_tuning(self._h, C.byref(tt)))
+        return Tuning(tt.alpha, tt.beta, tt.force_dir, tt.lanes_words)
+
+    def _check_seed(self, seed: int):
+        if seed < 0 or seed >= self.node_count:
+            raise ContractError(f"k-hop seed {seed} is not an allocated node")
+
+
+def _check_k(k: int):
+    if k < 1 or k > K_MAX_HOPS:
+        raise ContractError(f"k-hop count {k} outside [1, {K_MAX_HOPS}]")
+
+
+def k_hop_count(graph: DeviceGraph, query: KHopQuery) -> int:
+    """execute.cpp:373-375 — number of vertices in k_hop_frontier(graph, query)."""
+    graph._check_seed(query.seed)
+    _check_k(query.k)
+    return int(k_hop_count_batch(graph, [query.seed], query.k, query.mode)[0])
+
+
+def k_hop_frontier(graph: DeviceGraph, query: KHopQuery) -> np.ndarray:
+    """execute.cpp:347-371 — sorted uint64 ids (exact: distance == k; cumulative: 1..k)."""
+    graph._check_seed(query.seed)
+    _check_k(query.k)
+    cap = max(graph.nrows, 1)
+    ids = np.zeros(cap, np.uint64)
+    n = C.c_uint64()
+    _check(_lib.lib().mgk_khop_frontier(graph.handle, int(query.seed), int(query.k),
+                                        int(query.mode), ids.ctypes.data, cap, C.byref(n)))
+    return ids[: n.value].copy()
+
+
+def k_hop_count_batch(graph: DeviceGraph, seeds, k: int, mode=TraverseMode.Exact,
+                      engine: int = ENGINE_AUTO, stats: bool = False):
+    """Batched k_hop_count: one count per seed, host buffers (additive API).
+
+    Seeds are validated in order exactly like k_hop_frontier's first check.
+    With stats=True returns (counts, stats_dict) with per-hop work counters.
+    """
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    for s in seeds:
+        if int(s) >= graph.node_count:
+            raise ContractError(f"k-hop seed {int(s)} is not an allocated node")
+    _check_k(k)
+    counts = np.zeros(max(len(seeds), 1), np.uint64)
+    st = MgkStats()
+    sp = seeds if len(seeds) else np.zeros(1, np.uint64)
+    _check(_lib.lib().mgk_khop_count_ex(graph.handle, sp.ctypes.data, len(seeds), int(k), int(mode),
+                                        int(engine), counts.ctypes.data,
+                                        C.byref(st) if stats else None))
+    counts = counts[: len(seeds)]
+    return (counts, st.to_dict()) if stats else counts
+
+
+def k_hop_count_device(graph: DeviceGraph, d_seeds_ptr: int, nseeds: int, k: int, mode: int,
+                       d_counts_ptr: int, stream_ptr: int = 0, engine: int = ENGINE_AUTO):
+    """Device-resident batch: uint32 seeds and uint64 counts already in HBM; async on stream."""
+    _check(_lib.lib().mgk_khop_count_device(graph.handle, C.c_void_p(d_seeds_ptr), nseeds, int(k),
+                                            int(mode), int(engine), C.c_void_p(d_counts_ptr),
+                                            C.c_void_p(stream_ptr)))
+
+
+def device_stats(graph: DeviceGraph, stream_ptr: int = 0) -> dict:
+    st = MgkStats()
+    _check(_lib.lib().mgk_khop_device_stats(graph.handle, C.c_void_p(stream_ptr), C.byref(st)))
+    return st.to_dict()
+
+
+def device_count() -> int:
+    return int(_lib.lib().mgk_device_count())
+
+
+__all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "TraverseMode", "KHopQuery",
+           "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
+           "k_hop_count_device", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "ENGINE_LANES", "K_MAX_HOPS"]
