@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""k-hop count benchmark (BASELINE.json metric) — one JSON line on rank 0.
+
+Workload (N=1): BASELINE.json configs[1] ("cfg2"): R-MAT (a=.57 b=.19 c=.19
+d=.05) over 2^22 ids until 67,108,864 unique directed edges remain, isolated
+ids dropped and survivors renumbered (2,412,345 vertices); 300 pick_seeds
+seeds; a step = k=1 and k=2 exact counts for all 300 seeds. Multi-GPU: each
+rank holds a replica and runs its own disjoint 300-seed shard of one master
+seed list (weak scaling, no collective on the data path).
+
+Arms:
+  default           our sm_100a engine (libmgk.so) — `value` is device-resident
+                    (seeds/counts in HBM, CUDA events on the launch stream, L2
+                    flushed between steps); `e2e` is the public host API
+                    (k_hop_count_batch: host seeds -> H2D -> kernels -> D2H).
+  --impl reference  the reference's own CPU k_hop_count (oracle/_ref, the
+                    unmodified matgraph core) on all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SEEDS_PER_RANK = 300
+KS = (1, 2)
+WORKLOAD = "cfg2"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def build_inputs(world: int, rank: int):
+    from paper_1905_01294_b200 import harness as H
+    t = time.time()
+    rp, ci = H.gen_csr(H.G2)
+    master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
+    seeds = master[rank * SEEDS_PER_RANK:(rank + 1) * SEEDS_PER_RANK]
+    log(f"[rank {rank}] G2: n={len(rp) - 1} m={len(ci)} generated in {time.time() - t:.1f}s")
+    return rp, ci, seeds
+
+
+def algo_bytes(st: dict) -> float:
+    """Algorithmic bytes of one traversal launch, from the
+    engine's own per-hop counters.
+
+    SINGLE (per-seed bitmaps; SURVEY.md §8(d) single-source model): per hop,
+    4 B per adjacency entry read (push: out-edges of the frontier; pull:
+    in-edges up to the first frontier hit) + 8 B row/col_ptr pair per opened
+    vertex (push: frontier vertices, pull: candidates) + 4 B per frontier id
+    read (push) + 4 B per discovered id written. Bitmaps are L2-resident and
+    not counted.
+    LANES (W x 64-bit lane words): 4 B per adjacency entry read + (8 + 8W) B per
+    expanded (push) / candidate (pull) vertex + 3 x 8W B per discovered vertex
+    (F' read, V read + write)."""
+    lv = st["levels"]
+    total = 0.0
+    if st["engine"] == "lanes":
+        W = st["lanes"] // 64
+        for h in range(1, len(lv)):
+            L = lv[h]
+            if not L["runs"]:
+                continue
+            expanded = L["candidates"] if L["pull_runs"] else lv[h - 1]["vertices"]
+            total += 4 * L["scanned"] + (8 + 8 * W) * expanded + 24 * W * L["vertices"]
+        return total
+    for h in range(1, len(lv)):
+        L = lv[h]
+        if not L["runs"]:
+            continue
+        prev = lv[h - 1]["frontier"] if h > 1 else st["batches"]
+        pushes = L["runs"] - L["pull_runs"]
+        push_share = pushes / L["runs"]
+        opened = L["candidates"] + prev * push_share
+        total += 4 * L["scanned"] + 8 * opened + 4 * prev * push_share + 4 * L["frontier"]
+    return total
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1905_01294_b200 import DeviceGraph, k_hop_count_batch, k_hop_count_device, device_stats
+    from paper_1905_01294_b200 import Tuning
+
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rp, ci, seeds = build_inputs(world, rank)
+    t = time.time()
+    g = DeviceGraph.from_csr(rp, ci, device=local)
+    if args.lanes_words:
+        g.set_tuning(Tuning(lanes_words=args.lanes_words))
+    log(f"[rank {rank}] uploaded ({g.device_bytes() / 2**20:.0f} MiB on device) in {time.time() - t:.1f}s")
+
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    d_seeds = torch.from_numpy(seeds.astype(np.int32)).cuda()
+    d_counts = {k: torch.zeros(len(seeds), dtype=torch.int64, device="cuda") for k in KS}
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    def step(evs=None):
+        for i, k in enumerate(KS):
+            if evs:
+                evs[2 * i].record(stream)
+            k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts[k].data_ptr(), sp)
+            if evs:
+                evs[2 * i + 1].record(stream)
+
+    # correctness against the host API before timing
+    for k in KS:
+        step()
+    torch.cuda.synchronize()
+    host_counts = {k: k_hop_count_batch(g, seeds, k, 0) for k in KS}
+    for k in KS:
+        assert (d_counts[k].cpu().numpy().astype(np.uint64) == host_counts[k]).all()
+
+    # ---- device-resident timed region --------------------------------------------
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    per_launch = {k: [] for k in KS}
+    step_ms = []
+    sampler = ClockSampler(local)
+    with sampler:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.fill_(1)  # L2 flush between steps, outside the events
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * len(KS))]
+            step(evs)
+            torch.cuda.synchronize()
+            t_k = [evs[2 * i].elapsed_time(evs[2 * i + 1]) for i in range(len(KS))]
+            for k, tk in zip(KS, t_k):
+                per_launch[k].append(tk)
+            step_ms.append(evs[0].elapsed_time(evs[-1]))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        total_ms = float(np.sum(step_ms))
+        # ---- e2e through the public host API ---------------------------------------
+        e2e_ms = []
+        for _ in range(max(3, args.warmup)):
+            for k in KS:
+                k_hop_count_batch(g, seeds, k, 0)
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for k in KS:
+                k_hop_count_batch(g, seeds, k, 0)
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e2e_total = float(np.sum(e2e_ms))
+    clocks = sampler.summary()
+
+    # stats of one launch per k (for GTEPS and the roofline)
+    stats = {}
+    for k in KS:
+        _, stats[k] = k_hop_count_batch(g, seeds, k, 0, stats=True)
+
+    if world > 1:
+        tt = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, e2e_total = float(tt[0]), float(tt[1])
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    q_per_step = len(seeds) * len(KS) * world
+    value = q_per_step * args.steps / (total_ms / 1e3)
+    edges_per_step = sum(sum(L["edges"] for L in stats[k]["levels"]) for k in KS) * world
+    dom = max(KS, key=lambda k: np.mean(per_launch[k]))
+    dom_ms = float(np.mean(per_launch[dom]))
+    ab = algo_bytes(stats[dom])
+    pk, pk_src = peaks()
+    achieved = ab / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(f"{WORKLOAD}_k{dom}")
+        except Exception:
+            traffic = None
+    cpu = cpu_baseline(rp, ci, seeds) if (world == 1 and not args.no_cpu) else None
+    line = {
+        "metric": "k-hop count queries/s (cfg2: 300 seeds x k=1,2 exact on the 2.4M/67M R-MAT graph)",
+        "value": value,
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32 ids / u64 lane words (integer)",
+        "data": "synthetic R-MAT, BASELINE.json configs[1] shape (seeded; stands in for Graph500 2.4M/67M)",
+        "config": {"workload": WORKLOAD, "graph": {"n": int(len(rp) - 1), "m": int(len(ci)),
+                                                      "rmat": [0.57, 0.19, 0.19, 0.05], "ids": "2^22 renumbered"},
+                   "seeds_per_rank": len(seeds), "ks": list(KS), "mode": "exact",
+                   "engine": stats[dom]["engine"], "lanes_per_batch": stats[dom]["lanes"],
+                   "l2": "flushed between steps (256 MiB write, outside the events)",
+                   "parallelism": f"seed-sharded graph replicas x{world}"},
+        "gteps": edges_per_step * args.steps / (total_ms / 1e3) / 1e9,
+        "per_k": {str(k): {"ms_per_launch": float(np.mean(per_launch[k])),
+                           "queries_per_s": len(seeds) * world / (float(np.mean(per_launch[k])) / 1e3),
+                           "push_equiv_edges": int(sum(L["edges"] for L in stats[k]["levels"])),
+                           "hops": [{"dir": "pull" if L["pull_runs"] else "push", "frontier": L["frontier"],
+                                     "vertices": L["vertices"], "scanned": L["scanned"],
+                                     "us": L["ns"] / 1e3} for L in stats[k]["levels"][1:]]}
+                  for k in KS},
+        "roofline": {"bound": "hbm", "kernel": (f"ms_kernel<W={stats[dom]['lanes'] // 64}>" if stats[dom]["engine"] == "lanes"
+                                                else "fr_kernel") + f" (k={dom})",
+                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "peak_source": pk_src,
+                     "algo_bytes_per_launch": ab, "traffic": traffic},
+        "cpu_baseline": cpu,
+        "e2e": {"value": q_per_step * args.steps / (e2e_total / 1e3), "unit": "queries/s",
+                "h2d_bytes_per_step": 4 * len(seeds) * len(KS), "d2h_bytes_per_step": 8 * len(seeds) * len(KS),
+                "ms_per_step": e2e_total / args.steps},
+        "gpu_launches": len(KS) * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def ref_graph(rp, ci):
+    import oracle
+    from paper_1905_01294_b200 import harness as H
+    R = oracle.Ref()
+    src, dst = H.csr_to_edges(rp, ci)
+    t = time.time()
+    g = R.build_bench_graph(src, dst, len(rp) - 1)
+    log(f"reference build_bench_graph: {time.time() - t:.1f}s")
+    return g
+
+
+def cpu_baseline(rp, ci, seeds, budget_s: float = 12.0):
+    """The reference's CPU k_hop_count (oracle/_ref) on this host, all threads,
+    on repeated passes of the same 300-seed x k=1,2 schedule (bounded sample)."""
+    import oracle
+    cores = os.cpu_count() or 1
+    try:
+        g = ref_graph(rp, ci)
+        kind = "reference"
+        run = lambda k: g.k_hop_count_many(seeds, k, 0, threads=cores)[1]
+    except Exception as e:  # reference library not built: the C port, 1 thread
+        log(f"cpu_baseline: reference unavailable ({e}); timing the C port")
+        P = oracle.Port()
+        rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
+        kind, cores = "port", 1
+
+        def run(k):
+            t0 = time.perf_counter()
+            for s in seeds:
+                P.khop_count(rp64, ci64, int(s), k, 0)
+            return time.perf_counter() - t0
+    passes, elapsed = 0, 0.0
+    while elapsed < budget_s and passes < 50:
+        elapsed += sum(run(k) for k in KS)
+        passes += 1
+    q = passes * len(seeds) * len(KS)
+    return {"value": q / elapsed, "unit": "queries/s", "cores": cores, "kind": kind,
+            "sample": f"{passes} pass(es) of {len(seeds)} seeds x k=1,2 exact on the same G2 graph "
+                      f"({elapsed:.1f}s of CPU wall time)"}
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_1905_01294_b200 import harness as H
+    rp, ci = H.gen_csr(H.G2)
+    seeds = H.pick_seeds(rp, SEEDS_PER_RANK, 1)
+    g = ref_graph(rp, ci)
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        for k in KS:
+            g.k_hop_count_many(seeds, k, 0, threads=cores)
+    times = []
+    for _ in range(args.steps):
+        times.append(sum(g.k_hop_count_many(seeds, k, 0, threads=cores)[1] for k in KS))
+    total = float(np.sum(times))
+    value = len(seeds) * len(KS) * args.steps / total
+    line = {
+        "metric": "k-hop count queries/s (cfg2: 300 seeds x k=1,2 exact on the 2.4M/67M R-MAT graph)",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64 ids (integer)",
+        "data": "synthetic R-MAT, BASELINE.json configs[1] shape (seeded)",
+        "config": {"workload": WORKLOAD, "graph": {"n": int(len(rp) - 1), "m": int(len(ci))},
+                   "seeds_per_rank": len(seeds), "ks": list(KS), "mode": "exact",
+                   "parallelism": f"{cores} host threads, one query per thread"},
+        "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} step(s) of {len(seeds)} seeds x k=1,2 on "
+                                   f"oracle/_ref (unmodified matgraph core, -O3, checks off)"},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lanes-words", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

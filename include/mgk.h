@@ -47,7 +47,7 @@ extern "C" {
 #define MGK_CUMULATIVE 1
 
 /* traversal engines */
-#define MGK_ENGINE_AUTO 0   /* 1 seed -> SINGLE, more -> LANES */
+#define MGK_ENGINE_AUTO 0   /* k <= 2 or one seed -> SINGLE, else LANES */
 #define MGK_ENGINE_SINGLE 1 /* bitmap direction-optimizing BFS, one seed at a time */
 #define MGK_ENGINE_LANES 2  /* bit-parallel multi-source: 64 seeds per uint64 lane word */
 
@@ -138,16 +138,17 @@ int mgk_khop_frontier(mgk_graph* g, uint64_t seed, uint32_t k, int mode, uint64_
                       uint64_t cap, uint64_t* n_out);
 
 /* Engine tuning knobs (0 keeps the default). alpha/beta: Beamer-style
- * push->pull when frontier edges > unexplored edges / alpha, pull->push when
- * frontier < n / beta. Mostly for experiments and tests that force a
- * direction: force_dir 0 auto, 1 push only, 2 pull only (pull needs hop >= 2
- * frontier state, so hop 1 always pushes). lanes_words: 64-lane words per
- * vertex in the LANES engine (1, 2, 4 or 8). */
+ * push->pull when frontier edges * alpha > unexplored in-edges, pull->push
+ * when frontier * beta < n (alpha for SINGLE, alpha_lanes for LANES).
+ * force_dir: 0 auto, 1 push only, 2 pull only (tests use it to pin both
+ * directions to the same answers). lanes_words: 64-lane words per vertex in
+ * the LANES engine (1, 2, 4 or 8; 0 = auto). */
 typedef struct mgk_tuning {
     uint32_t alpha;
     uint32_t beta;
     uint32_t force_dir;
     uint32_t lanes_words;
+    uint32_t alpha_lanes;
 } mgk_tuning;
 int mgk_graph_set_tuning(mgk_graph* g, const mgk_tuning* t);
 int mgk_graph_get_tuning(const mgk_graph* g, mgk_tuning* t);

@@ -86,9 +86,16 @@ cudaError_t create_ws(Graph* g, Workspace* ws, bool own_stream) {
 }
 
 void destroy_ws(Workspace* ws, bool own_stream) {
-    cudaFree(ws->visited);
-    for (auto* p : ws->fb) cudaFree(p);
-    for (auto* p : ws->ss_items) cudaFree(p);
+    cudaFree(ws->fr_V);
+    cudaFree(ws->fr_Fb);
+    for (auto* p : ws->fr_items) cudaFree(p);
+    cudaFree(ws->fr_log);
+    cudaFree(ws->fr_cnt);
+    cudaFree(ws->fr_mfs);
+    cudaFree(ws->fr_mus);
+    cudaFree(ws->fr_logcnt);
+    cudaFree(ws->fr_dirs);
+    cudaFree(ws->fr_ctl);
     cudaFree(ws->lv);
     cudaFree(ws->lf[0]);
     cudaFree(ws->lf[1]);
@@ -161,7 +168,7 @@ int check_query(const Graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t
 cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_t nseeds,
                        uint32_t k, int mode, int engine, unsigned long long* d_counts,
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
-                       int* W_out) {
+                       int* W_out, bool keep_result = false) {
     cudaError_t e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
     if (e) return e;
     if (nseeds == 0) return cudaSuccess;
@@ -175,7 +182,12 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.d_counts = d_counts;
     L.stream = stream;
     L.tuning = g->tuning;
-    if (engine == MGK_ENGINE_AUTO) engine = nseeds == 1 ? MGK_ENGINE_SINGLE : MGK_ENGINE_LANES;
+    L.keep_result = keep_result;
+    // AUTO: shallow hops touch little of the graph per seed, so independent
+    // per-seed bitmaps win; from 3 hops on, frontiers of different seeds
+    // overlap heavily and the 64-lane words share every adjacency pass.
+    if (engine == MGK_ENGINE_AUTO)
+        engine = (nseeds > 1 && k >= 3) ? MGK_ENGINE_LANES : MGK_ENGINE_SINGLE;
     *used_engine = engine;
     if (engine == MGK_ENGINE_SINGLE) {
         e = launch_single(L);
@@ -418,6 +430,7 @@ int mgk_graph_set_tuning(mgk_graph* h, const mgk_tuning* t) {
         return fail(MGK_ECONTRACT, "lanes_words must be 1, 2, 4 or 8");
     std::lock_guard<std::mutex> lk(h->g.mu);
     if (t->alpha) h->g.tuning.alpha = t->alpha;
+    if (t->alpha_lanes) h->g.tuning.alpha_lanes = t->alpha_lanes;
     if (t->beta) h->g.tuning.beta = t->beta;
     h->g.tuning.force_dir = t->force_dir;
     h->g.tuning.lanes_words = t->lanes_words;
@@ -427,6 +440,7 @@ int mgk_graph_set_tuning(mgk_graph* h, const mgk_tuning* t) {
 int mgk_graph_get_tuning(const mgk_graph* h, mgk_tuning* t) {
     if (!h || !t) return fail(MGK_ECONTRACT, "null argument");
     t->alpha = h->g.tuning.alpha;
+    t->alpha_lanes = h->g.tuning.alpha_lanes;
     t->beta = h->g.tuning.beta;
     t->force_dir = h->g.tuning.force_dir;
     t->lanes_words = h->g.tuning.lanes_words;
@@ -562,7 +576,7 @@ int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_
         uint32_t grid = 0, block = 0;
         int used = 0, W = 0;
         if ((e = run_engine(g, ws, ws->d_seeds, 1, k, mode, MGK_ENGINE_SINGLE, ws->d_counts, ws->stream,
-                            &grid, &block, &used, &W)))
+                            &grid, &block, &used, &W, true)))
             break;
         if ((e = cudaMalloc(&d_ids, (size_t)std::max<uint32_t>(g->dg.n, 1) * 8))) break;
         if ((e = cudaMalloc(&d_n, 8))) break;

@@ -79,11 +79,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 // appended with a ballot (no atomics); a global reservation is taken only
 // when the stage is nearly full or at the end of a phase, so a hot queue tail
 // sees one atomic per ~200 vertices instead of one per warp step.
-template <int CAP>
+template <int CAP, typename T = uint32_t>
 struct Stage {
-    uint32_t* buf;  // CAP entries in shared memory, private to this warp
-    uint32_t n;     // warp-uniform fill
-    __device__ __forceinline__ void push(bool pred, uint32_t v) {
+    T* buf;      // CAP entries in shared memory, private to this warp
+    uint32_t n;  // warp-uniform fill
+    __device__ __forceinline__ void push(bool pred, T v) {
         const unsigned m = __ballot_sync(kFull, pred);
         if (pred) buf[n + __popc(m & lanemask_lt())] = v;
         n += __popc(m);
@@ -158,6 +158,14 @@ __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, cons
         base += total;
     }
     __syncwarp();
+}
+
+// Items per warp iteration so that small work lists still spread over every
+// warp of the grid: a power of two in [1, 32].
+__device__ __forceinline__ uint32_t items_per_warp(uint32_t nitems, uint32_t nwarps) {
+    uint32_t g = 1;
+    while (g < 32 && (uint64_t)g * 2 * nwarps <= nitems) g <<= 1;
+    return g;
 }
 
 // Block-level accumulation of counters, flushed once per phase.

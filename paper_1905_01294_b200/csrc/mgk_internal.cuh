@@ -57,6 +57,7 @@ struct Tuning {
     uint32_t beta = 24;   // pull -> push when frontier vertices < n / beta
     uint32_t force_dir = 0;
     uint32_t lanes_words = 0;  // 0 = auto
+    uint32_t alpha_lanes = 2;  // LANES: a pull pass rarely exits early, so switch later
 };
 
 // Workspace for one in-flight call. Sized for the graph; reused across calls.
@@ -64,10 +65,20 @@ struct Workspace {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // single-source engine
-    uint32_t* visited = nullptr;
-    uint32_t* fb[3] = {nullptr, nullptr, nullptr};
-    uint2* ss_items[2] = {nullptr, nullptr};
+    // single-source engine (per-seed bitmaps, fr_slots seeds in flight)
+    uint32_t fr_slots = 0;
+    uint32_t* fr_V = nullptr;   // [S][nwords]
+    uint32_t* fr_Fb = nullptr;  // [3][S][nwords]
+    uint2* fr_items[2] = {nullptr, nullptr};
+    uint32_t fr_items_cap = 0;
+    unsigned long long* fr_log = nullptr;
+    uint32_t fr_log_cap = 0, fr_quota = 0;
+    uint32_t* fr_cnt = nullptr;
+    unsigned long long* fr_mfs = nullptr;
+    unsigned long long* fr_mus = nullptr;
+    uint32_t* fr_logcnt = nullptr;
+    uint8_t* fr_dirs = nullptr;
+    void* fr_ctl = nullptr;
     // lanes engine (allocated lazily for the widest W used)
     int lanes_words = 0;
     unsigned long long* lv = nullptr;     // V  [n * W]
@@ -122,6 +133,7 @@ struct Launch {
     cudaStream_t stream;
     Tuning tuning;
     int lanes_words;  // LANES engine only
+    bool keep_result = false;  // SINGLE: leave slot 0's bitmaps for k_hop_frontier
     uint32_t grid = 0, block = 0;  // out
 };
 

@@ -166,9 +166,10 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
                            uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    for (uint32_t base = warp_gid * 32; base < nitems; base += nwarps * 32) {
+    const uint32_t G = items_per_warp(nitems, nwarps);
+    for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
         const uint32_t idx = base + lane;
-        const uint4 it = idx < nitems ? items[idx] : make_uint4(0, 0, 0, 0);
+        const uint4 it = (lane < G && idx < nitems) ? items[idx] : make_uint4(0, 0, 0, 0);
         const uint32_t len = it.y - it.x;
         const uint32_t incl = warp_incl_scan(len);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
@@ -261,17 +262,26 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         for (int i = 0; i < W; ++i) acc_w.w[i] = 0;
         uint32_t scanned = 0;
         if (cand && e - b <= 32) {
-            for (uint32_t p = b; p < e; ++p) {
-                const uint32_t v = __ldg(g.ri + p);
-                const LaneWord<W> f = load_lw<W>(Fc + (size_t)v * W);
-                bool done = true;
+            uint32_t p = b;
+            bool done = false;
+            // two in-neighbours per step: their lane words are gathered together
+            for (; p + 2 <= e && !done; p += 2) {
+                const uint32_t v0 = __ldg(g.ri + p), v1 = __ldg(g.ri + p + 1);
+                const LaneWord<W> f0 = load_lw<W>(Fc + (size_t)v0 * W);
+                const LaneWord<W> f1 = load_lw<W>(Fc + (size_t)v1 * W);
+                done = true;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    acc_w.w[i] |= f.w[i];
+                    acc_w.w[i] |= f0.w[i] | f1.w[i];
                     done &= (acc_w.w[i] & need.w[i]) == need.w[i];
                 }
+                scanned += 2;
+            }
+            if (!done && p < e) {
+                const LaneWord<W> f = load_lw<W>(Fc + (size_t)__ldg(g.ri + p) * W);
+#pragma unroll
+                for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
-                if (done) break;
             }
         }
         unsigned big = __ballot_sync(kFull, cand && e - b > 32);
@@ -616,7 +626,7 @@ cudaError_t launch_w(Launch& L) {
     P.qctl = ws->qctl;
     P.misc = ws->misc;
     P.lc = ws->lc;
-    P.alpha = L.tuning.alpha;
+    P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
     L.grid = (uint32_t)(blocks_per_sm * num_sms);

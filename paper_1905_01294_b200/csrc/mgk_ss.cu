@@ -1,22 +1,26 @@
-// SINGLE engine: one seed at a time, bitmap state, direction-optimizing BFS.
+// SINGLE engine: independent single-source traversals with per-seed bitmap
+// state, up to S seeds in flight at once, direction-optimizing per seed.
 //
 // Replaces the per-query loop of k_hop_frontier (proj/core/src/execute.cpp:347-371)
 // and its vxm / ewise_union calls (proj/core/src/sparse.cpp:253-290, 365-377):
-//   * visited / frontier sets are bitmaps (n/8 bytes, L2-resident) instead of
-//     sorted uint64 vectors plus two dense char arrays zeroed every hop;
-//   * the masked vxm is a push pass over the frontier's out-edges (CSR) with
-//     atomicOr test-and-set on the visited bitmap, or a pull pass over the
-//     unvisited vertices' in-edges (CSC) that stops at the first frontier hit;
-//   * ewise_union is the same atomicOr, and nvals is a discovery counter.
-// All hops of all seeds run inside one persistent cooperative launch; hops are
-// separated by grid-wide barriers and every direction / early-exit decision is
-// taken on the device from counters all CTAs read after the barrier, so there
-// is no host round trip per hop.
+//   * each seed slot owns a visited bitmap and three rotating frontier bitmaps
+//     (n/8 bytes each) instead of sorted uint64 vectors plus two dense char
+//     arrays zeroed every hop;
+//   * the masked vxm is, per seed and per hop, either a push pass over the
+//     frontier's out-edges (CSR) with atomicOr test-and-set on the seed's
+//     visited bitmap, or a pull pass over the seed's unvisited vertices'
+//     in-edges (CSC) that stops at the first frontier hit (Beamer's
+//     direction optimization, decided per seed on the device);
+//   * ewise_union is the same atomicOr; nvals is a per-seed discovery counter.
+// All hops of all seeds run inside one persistent cooperative launch. Hops are
+// separated by grid-wide barriers; every decision is taken on the device from
+// counters all CTAs read after the barrier, so there is no host round trip.
 //
-// Push work items are (begin, end) slices of at most kChunk adjacency entries,
-// written when a vertex is discovered, so a 97K-degree hub is spread over
-// ~3K warp iterations instead of serialising one warp; each warp merges 32
-// items with a shuffle scan and reads the adjacency in coalesced runs.
+// Load balance: push work items are (begin, len<=32, seed) slices of CSR rows,
+// written when a vertex is discovered, so a 100K-degree hub is spread over
+// thousands of warps; the items of ALL in-flight seeds form one global list and
+// each warp takes 1..32 items per step (fewer when the list is short, so a
+// small hop still occupies every warp of the grid). The last hop only counts.
 #include "mgk_device.cuh"
 
 namespace mgk {
@@ -27,134 +31,275 @@ using namespace dev;
 constexpr int kBlock = 512;
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
+constexpr int kIlp = 4;
+constexpr uint32_t kMaxSlots = 512;
+constexpr unsigned long long kOverflowBit = 1ULL << 62;
+enum : uint8_t { kPush = 0, kPull = 1, kDead = 2 };
 
-struct SSParams {
+struct FRCtl {
+    unsigned int nitems[3];  // items for hop h: buffer h & 1, count nitems[h % 3]
+    unsigned int log_n;
+    unsigned int log_overflow;
+    unsigned int pad;
+    unsigned long long found[MGK_MAX_HOPS + 1];
+    unsigned long long last_which;  // frontier bitmap id of the final hop (frontier ids)
+};
+
+struct FRParams {
     DevGraph g;
     const uint32_t* seeds;
-    uint32_t nseeds;
+    uint64_t nseeds;
     uint32_t k;
     int mode;
     unsigned long long* counts;
-    uint32_t* visited;
-    uint32_t* fb0;
-    uint32_t* fb1;
-    uint32_t* fb2;
+    uint32_t S;
+    uint32_t* V;   // [S][nwords]
+    uint32_t* Fb;  // [3][S][nwords]
     uint2* items0;
     uint2* items1;
-    QCtl* qctl;                // [3], indexed by hop % 3
-    unsigned long long* misc;  // [0] unexplored in-edges, [1] final bitmap id, [2] last seed
+    uint32_t items_cap;
+    unsigned long long* logbuf;
+    uint32_t log_cap;
+    uint32_t* cnt;             // [(k+1)][S] discoveries per hop per seed
+    unsigned long long* mfs;   // [(k+1)][S] out-edges of those discoveries
+    unsigned long long* mus;   // [S] unexplored in-edges per seed
+    uint32_t* logcnt;          // [S]
+    uint8_t* dirs;             // [2][S]
+    FRCtl* ctl;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
+    uint32_t quota;  // per-seed log entries before the seed is cleared densely
+    uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
 };
 
-__device__ __forceinline__ uint32_t* fb_of(const SSParams& P, uint32_t i) {
-    return i == 0 ? P.fb0 : (i == 1 ? P.fb1 : P.fb2);
-}
-__device__ __forceinline__ uint2* items_of(const SSParams& P, uint32_t i) {
-    return (i & 1) ? P.items1 : P.items0;
-}
-
-// Per-thread counters of one phase, reduced per block and flushed once.
 struct Acc {
-    unsigned long long found, edges, indeg, scanned, candidates;
-    __device__ void zero() { found = edges = indeg = scanned = candidates = 0; }
+    unsigned long long found, scanned, candidates;
+    __device__ void zero() { found = scanned = candidates = 0; }
 };
 
-__device__ void block_flush(Acc& a, QCtl* q, LevelCounters* lc, unsigned long long* unexplored) {
-    __shared__ unsigned long long s[5];
-    if (threadIdx.x < 5) s[threadIdx.x] = 0;
+__device__ void block_flush(Acc& a, unsigned long long* found_total, LevelCounters* lc) {
+    __shared__ unsigned long long s[3];
+    if (threadIdx.x < 3) s[threadIdx.x] = 0;
     __syncthreads();
-    const unsigned long long f = warp_sum_u64(a.found), e = warp_sum_u64(a.edges),
-                             i = warp_sum_u64(a.indeg), sc = warp_sum_u64(a.scanned),
+    const unsigned long long f = warp_sum_u64(a.found), sc = warp_sum_u64(a.scanned),
                              c = warp_sum_u64(a.candidates);
     if (lane_id() == 0) {
         if (f) atomicAdd(&s[0], f);
-        if (e) atomicAdd(&s[1], e);
-        if (i) atomicAdd(&s[2], i);
-        if (sc) atomicAdd(&s[3], sc);
-        if (c) atomicAdd(&s[4], c);
+        if (sc) atomicAdd(&s[1], sc);
+        if (c) atomicAdd(&s[2], c);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         if (s[0]) {
-            atomicAdd(&q->nfound, (unsigned int)s[0]);
+            atomicAdd(found_total, s[0]);
             atomicAdd(&lc->frontier, s[0]);
             atomicAdd(&lc->vertices, s[0]);
         }
-        if (s[1]) atomicAdd(&q->edges, s[1]);
-        if (s[2]) {
-            atomicAdd(&q->indeg, s[2]);
-            atomicAdd(unexplored, 0ULL - s[2]);
-        }
-        if (s[3]) atomicAdd(&lc->scanned, s[3]);
-        if (s[4]) atomicAdd(&lc->candidates, s[4]);
+        if (s[1]) atomicAdd(&lc->scanned, s[1]);
+        if (s[2]) atomicAdd(&lc->candidates, s[2]);
     }
     __syncthreads();
     a.zero();
 }
 
-__device__ __forceinline__ void count_found(const DevGraph& g, uint32_t u, Acc& acc) {
-    acc.found += 1;
-    acc.edges += __ldg(g.rp + u + 1) - __ldg(g.rp + u);
-    acc.indeg += __ldg(g.cp + u + 1) - __ldg(g.cp + u);
+// Warp-wide: sum (a, b, c) over the lanes of each distinct slot and apply one
+// set of atomics per slot. Returns, per lane, the slot's pre-add logcnt.
+__device__ __forceinline__ uint32_t slot_commit(const FRParams& P, uint32_t hop, bool valid,
+                                                uint32_t slot, uint32_t deg, uint32_t indeg,
+                                                bool last) {
+    uint32_t old_log = 0;
+    unsigned pending = __ballot_sync(kFull, valid);
+    while (pending) {
+        const int leader = __ffs(pending) - 1;
+        const uint32_t s = __shfl_sync(kFull, slot, leader);
+        const bool mine = valid && slot == s;
+        const unsigned grp = __ballot_sync(kFull, mine);
+        const uint32_t n = __popc(grp);
+        unsigned long long d = mine ? deg : 0, i = mine ? indeg : 0;
+        if (!last) {
+            d = warp_sum_u64(d);
+            i = warp_sum_u64(i);
+        }
+        uint32_t ol = 0;
+        if ((int)lane_id() == leader) {
+            atomicAdd(&P.cnt[hop * P.S + s], n);
+            ol = atomicAdd(&P.logcnt[s], n);
+            if (!last) {
+                atomicAdd(&P.mfs[hop * P.S + s], d);
+                atomicAdd(&P.mus[s], 0ULL - i);
+            }
+        }
+        ol = __shfl_sync(kFull, ol, leader);
+        if (mine) old_log = ol;
+        pending &= ~grp;
+    }
+    return old_log;
 }
 
-// Push: expand the frontier's work items; test-and-set visited; stage the
-// newly discovered vertices and turn them into next-hop work items.
-__device__ void push_phase(const SSParams& P, const uint2* items, uint32_t nitems, uint32_t* fnext,
-                           uint2* items_next, QCtl* qn, Acc& acc, Stage<kStageCap>& st,
-                           uint32_t warp_gid, uint32_t nwarps) {
+// Warp-wide emission of n staged (slot << 32 | u) discoveries of `hop`:
+// per-seed counters, the cleanup log, and (unless this is the last hop) the
+// next hop's push items.
+__device__ void emit(const FRParams& P, uint32_t hop, bool last, const unsigned long long* buf,
+                     uint32_t n) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    for (uint32_t base = warp_gid * 32; base < nitems; base += nwarps * 32) {
-        const uint32_t idx = base + lane;
-        const uint2 it = idx < nitems ? items[idx] : make_uint2(0, 0);
-        const uint32_t len = it.y - it.x;
-        const uint32_t incl = warp_incl_scan(len);
+    unsigned int* nitems = &P.ctl->nitems[(hop + 1) % 3];
+    uint2* items = ((hop + 1) & 1) ? P.items1 : P.items0;
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        const bool valid = i < n;
+        uint32_t u = 0, slot = 0, b = 0, deg = 0, indeg = 0;
+        if (valid) {
+            const unsigned long long e = buf[i];
+            u = (uint32_t)e;
+            slot = (uint32_t)(e >> 32);
+            if (!last) {
+                b = __ldg(g.rp + u);
+                deg = __ldg(g.rp + u + 1) - b;
+                indeg = __ldg(g.cp + u + 1) - __ldg(g.cp + u);
+            }
+        }
+        const uint32_t old_log = slot_commit(P, hop, valid, slot, deg, indeg, last);
+        // cleanup log: entries of seeds still under their quota
+        const bool loggable = valid && old_log < P.quota;
+        const unsigned lm = __ballot_sync(kFull, loggable);
+        if (lm) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&P.ctl->log_n, (unsigned)__popc(lm));
+            base = __shfl_sync(kFull, base, 0);
+            if (loggable) {
+                const uint32_t at = base + __popc(lm & lanemask_lt());
+                if (at < P.log_cap) P.logbuf[at] = ((unsigned long long)slot << 32) | u;
+                else P.ctl->log_overflow = 1;
+            }
+        }
+        if (last) continue;
+        // next-hop push items
+        const uint32_t nit = (deg + kChunk - 1) / kChunk;
+        const uint32_t incl = warp_incl_scan(nit);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
-        const uint32_t off = it.x - (incl - len);
+        if (total == 0) continue;
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(nitems, total);
+        base = __shfl_sync(kFull, base, 31);
+        if ((uint64_t)base + total > P.items_cap) {
+            // out of item space: these seeds pull next hop (pull needs no items)
+            if (valid && deg) atomicOr(&P.mfs[hop * P.S + slot], kOverflowBit);
+            continue;
+        }
+        const uint32_t excl = incl - nit;
         for (uint32_t x0 = 0; x0 < total; x0 += 32) {
             const uint32_t x = x0 + lane;
-            const bool valid = x < total;
-            const uint32_t j = warp_owner(incl, valid ? x : total - 1);
-            const uint32_t pos = __shfl_sync(kFull, off, j) + x;
-            bool found = false;
-            uint32_t u = 0;
-            if (valid) {
-                u = __ldg(g.ci + pos);
-                const uint32_t w = u >> 5, bit = 1u << (u & 31);
-                if (!(ld_cg(P.visited + w) & bit)) {
-                    const uint32_t old = atomicOr(P.visited + w, bit);
-                    if (!(old & bit)) {
-                        found = true;
-                        atomicOr(fnext + w, bit);
-                        count_found(g, u, acc);
-                    }
-                }
-            }
-            acc.scanned += valid;
-            st.push(found, u);
-            if (st.full()) {
-                emit_items(g.rp, st.buf, st.n, items_next, &qn->nitems);
-                st.n = 0;
+            const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
+            const uint32_t bj = __shfl_sync(kFull, b, j);
+            const uint32_t dj = __shfl_sync(kFull, deg, j);
+            const uint32_t ej = __shfl_sync(kFull, excl, j);
+            const uint32_t sj = __shfl_sync(kFull, slot, j);
+            if (x < total) {
+                const uint32_t s = bj + (x - ej) * kChunk;
+                const uint32_t len = min(kChunk, bj + dj - s);
+                items[base + x] = make_uint2(s, (sj << 5) | (len - 1));
             }
         }
     }
-    emit_items(g.rp, st.buf, st.n, items_next, &qn->nitems);
-    st.n = 0;
+    __syncwarp();
 }
 
-// Pull: every unvisited vertex with in-edges scans its in-neighbours (CSC,
-// ascending) until one is in the current frontier. One warp owns one bitmap
-// word (32 vertices), so visited / next words are written without atomics.
-__device__ void pull_phase(const SSParams& P, const uint32_t* fcur, uint32_t* fnext, Acc& acc,
+__device__ __forceinline__ void stage_push(const FRParams& P, uint32_t hop, bool last,
+                                           Stage<kStageCap, unsigned long long>& st, bool found,
+                                           uint32_t slot, uint32_t u) {
+    st.push(found, ((unsigned long long)slot << 32) | u);
+    if (st.full()) {
+        emit(P, hop, last, st.buf, st.n);
+        st.n = 0;
+    }
+}
+
+// Push: expand the work items of seeds in push mode.
+__device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uint8_t* s_dir,
+                           Stage<kStageCap, unsigned long long>& st, Acc& acc, uint32_t warp_gid,
+                           uint32_t nwarps) {
+    const uint32_t lane = lane_id();
+    const DevGraph& g = P.g;
+    const uint32_t nw = g.nwords;
+    const uint32_t nitems = min(ld_volatile(&P.ctl->nitems[hop % 3]), P.items_cap);
+    const uint2* items = (hop & 1) ? P.items1 : P.items0;
+    const uint32_t fn = hop % 3;
+    const uint32_t G = items_per_warp(nitems, nwarps);
+    for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
+        const uint32_t idx = base + lane;
+        uint32_t len = 0, slot = 0, beg = 0;
+        if (lane < G && idx < nitems) {
+            const uint2 it = items[idx];
+            slot = it.y >> 5;
+            if (s_dir[slot] == kPush) {
+                len = (it.y & 31) + 1;
+                beg = it.x;
+            }
+        }
+        const uint32_t incl = warp_incl_scan(len);
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const uint32_t off = beg - (incl - len);
+        // kIlp edges per lane per step: all loads of a step are in flight together
+        for (uint32_t x0 = 0; x0 < total; x0 += 32 * kIlp) {
+            uint32_t u[kIlp], sj[kIlp], vis[kIlp];
+            bool valid[kIlp];
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r) {
+                const uint32_t x = x0 + r * 32 + lane;
+                valid[r] = x < total;
+                const uint32_t j = warp_owner(incl, valid[r] ? x : total - 1);
+                const uint32_t pos = __shfl_sync(kFull, off, j) + x;
+                sj[r] = __shfl_sync(kFull, slot, j);
+                u[r] = valid[r] ? __ldg(g.ci + pos) : 0;
+            }
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r)
+                vis[r] = valid[r] ? ld_cg(P.V + (size_t)sj[r] * nw + (u[r] >> 5)) : kFull;
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r) {
+                bool found = false;
+                const uint32_t bit = 1u << (u[r] & 31);
+                if (valid[r] && !(vis[r] & bit)) {
+                    const uint32_t old = atomicOr(P.V + (size_t)sj[r] * nw + (u[r] >> 5), bit);
+                    if (!(old & bit)) {
+                        found = true;
+                        if (!last || P.keep_result)
+                            atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * nw + (u[r] >> 5), bit);
+                    }
+                }
+                acc.scanned += valid[r];
+                acc.found += found;
+                stage_push(P, hop, last, st, found, sj[r], u[r]);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool fbit(const uint32_t* f, uint32_t v) {
+    return (f[v >> 5] >> (v & 31)) & 1u;
+}
+
+// Pull: for every seed in pull mode, every unvisited vertex with in-edges
+// scans its in-neighbours (CSC, ascending) until one is in the seed's
+// frontier. One warp owns one (seed, bitmap word) so V / F words are written
+// without atomics.
+__device__ void pull_phase(const FRParams& P, uint32_t hop, bool last, const uint16_t* s_pull,
+                           uint32_t npull, Stage<kStageCap, unsigned long long>& st, Acc& acc,
                            uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    for (uint32_t w = warp_gid; w < g.nwords; w += nwarps) {
-        const uint32_t vis = ld_cg(P.visited + w);
+    const uint32_t nw = g.nwords;
+    const uint64_t total = (uint64_t)npull * nw;
+    for (uint64_t t = warp_gid; t < total; t += nwarps) {
+        const uint32_t pi = (uint32_t)(t / nw);
+        const uint32_t w = (uint32_t)(t - (uint64_t)pi * nw);
+        const uint32_t slot = s_pull[pi];
+        uint32_t* vword = P.V + (size_t)slot * nw + w;
+        const uint32_t vis = *vword;
         const uint32_t done = vis | __ldg(g.no_in + w);
         if (done == kFull) continue;
+        const uint32_t* fcur = P.Fb + ((size_t)((hop - 1) % 3) * P.S + slot) * nw;
         const uint32_t u = w * 32 + lane;
         const bool cand = !((done >> lane) & 1u);
         uint32_t b = 0, e = 0;
@@ -165,12 +310,23 @@ __device__ void pull_phase(const SSParams& P, const uint32_t* fcur, uint32_t* fn
         bool found = false;
         uint32_t scanned = 0;
         if (cand && e - b <= 32) {
-            for (uint32_t p = b; p < e; ++p) {
-                const uint32_t v = __ldg(g.ri + p);
-                ++scanned;
-                if ((fcur[v >> 5] >> (v & 31)) & 1u) {
+            uint32_t p = b;
+            for (; p + 4 <= e; p += 4) {
+                const uint32_t v0 = __ldg(g.ri + p), v1 = __ldg(g.ri + p + 1),
+                               v2 = __ldg(g.ri + p + 2), v3 = __ldg(g.ri + p + 3);
+                scanned += 4;
+                if (fbit(fcur, v0) | fbit(fcur, v1) | fbit(fcur, v2) | fbit(fcur, v3)) {
                     found = true;
                     break;
+                }
+            }
+            if (!found) {
+                for (; p < e; ++p) {
+                    ++scanned;
+                    if (fbit(fcur, __ldg(g.ri + p))) {
+                        found = true;
+                        break;
+                    }
                 }
             }
         }
@@ -183,11 +339,7 @@ __device__ void pull_phase(const SSParams& P, const uint32_t* fcur, uint32_t* fn
             uint32_t sc = ej - bj;
             for (uint32_t p0 = bj; p0 < ej; p0 += 32) {
                 const uint32_t p = p0 + lane;
-                bool h = false;
-                if (p < ej) {
-                    const uint32_t v = __ldg(g.ri + p);
-                    h = (fcur[v >> 5] >> (v & 31)) & 1u;
-                }
+                const bool h = p < ej && fbit(fcur, __ldg(g.ri + p));
                 const unsigned hm = __ballot_sync(kFull, h);
                 if (hm) {
                     hit = true;
@@ -202,138 +354,190 @@ __device__ void pull_phase(const SSParams& P, const uint32_t* fcur, uint32_t* fn
         }
         acc.candidates += cand;
         acc.scanned += scanned;
+        acc.found += found;
         const unsigned fm = __ballot_sync(kFull, found);
         if (fm) {
             if (lane == 0) {
-                P.visited[w] = vis | fm;
-                fnext[w] = fm;
+                *vword = vis | fm;
+                if (!last || P.keep_result) P.Fb[((size_t)(hop % 3) * P.S + slot) * nw + w] = fm;
             }
-            if (found) count_found(g, u, acc);
         }
+        stage_push(P, hop, last, st, found, slot, u);
     }
 }
 
-// Re-derive push items from a frontier bitmap (after a pull hop).
-__device__ void compact_phase(const SSParams& P, const uint32_t* fcur, uint2* items, QCtl* q,
-                              Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
-    const uint32_t lane = lane_id();
-    for (uint32_t w = warp_gid; w < P.g.nwords; w += nwarps) {
-        const uint32_t bits = fcur[w];
-        if (bits == 0) continue;
-        st.push((bits >> lane) & 1u, w * 32 + lane);
-        if (st.full()) {
-            emit_items(P.g.rp, st.buf, st.n, items, &q->nitems);
-            st.n = 0;
-        }
-    }
-    emit_items(P.g.rp, st.buf, st.n, items, &q->nitems);
-    st.n = 0;
-}
-
-__global__ void __launch_bounds__(kBlock) ss_kernel(SSParams P) {
+__global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ uint32_t s_stage[kWarps][kStageCap];
+    __shared__ unsigned long long s_stage[kWarps][kStageCap];
+    __shared__ uint8_t s_dir[kMaxSlots];
+    __shared__ uint16_t s_list[kMaxSlots];
+    __shared__ uint32_t s_wcount[kWarps];
+    __shared__ uint32_t s_nlist;
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = gridDim.x * kBlock;
     const uint32_t warp_gid = gtid >> 5;
     const uint32_t nwarps = nthreads >> 5;
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
     const DevGraph& g = P.g;
+    const uint32_t nw = g.nwords;
+    const uint32_t S = P.S;
     Acc acc;
     acc.zero();
-    Stage<kStageCap> st{s_stage[threadIdx.x >> 5], 0};
+    Stage<kStageCap, unsigned long long> st{s_stage[wib], 0};
+    const uint64_t ngroups = (P.nseeds + S - 1) / S;
 
-    for (uint32_t qi = 0; qi < P.nseeds; ++qi) {
-        const uint32_t seed = P.seeds[qi];
-        // ---- init: clear state --------------------------------------------
-        for (uint32_t w = gtid; w < g.nwords; w += nthreads) {
-            P.visited[w] = 0;
-            P.fb0[w] = 0;
-            P.fb1[w] = 0;
-            P.fb2[w] = 0;
+    // block-wide ordered compaction of slots satisfying pred into s_list
+    auto compact = [&](bool pred) {
+        const unsigned m = __ballot_sync(kFull, pred);
+        if (lane == 0) s_wcount[wib] = __popc(m);
+        __syncthreads();
+        uint32_t off = 0, tot = 0;
+        for (uint32_t i = 0; i < kWarps; ++i) {
+            if (i < wib) off += s_wcount[i];
+            tot += s_wcount[i];
         }
-        if (gtid < 3) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
-        grid.sync();
-        if (warp_gid == 0) {
-            const bool me = lane_id() == 0;
-            if (me) {
-                P.visited[seed >> 5] = 1u << (seed & 31);
-                P.fb0[seed >> 5] = 1u << (seed & 31);
-                Acc a0;
-                a0.zero();
-                count_found(g, seed, a0);
-                P.qctl[0].nfound = 1;
-                P.qctl[0].edges = a0.edges;
-                P.qctl[0].indeg = a0.indeg;
-                P.misc[0] = g.m - a0.indeg;
-            }
-            st.push(me, seed);
-            emit_items(g.rp, st.buf, st.n, P.items0, &P.qctl[0].nitems);
-            st.n = 0;
-        }
-        grid.sync();
+        if (pred) s_list[off + __popc(m & lanemask_lt())] = (uint16_t)threadIdx.x;
+        if (threadIdx.x == 0) s_nlist = tot;
+        __syncthreads();
+    };
 
-        unsigned long long cum = 0, last = 1;
-        bool pull = false, items_ready = true;
-        uint32_t hop = 1;
-        for (; hop <= P.k; ++hop) {
-            const uint32_t cur = (hop - 1) % 3, nxt = hop % 3, clr = (hop + 1) % 3;
-            QCtl* qc = &P.qctl[cur];
-            QCtl* qn = &P.qctl[nxt];
-            const unsigned long long nf = ld_volatile(&qc->nfound);
-            const unsigned long long mf = ld_volatile(&qc->edges);
-            const unsigned long long mu = ld_volatile(&P.misc[0]);
-            if (P.force_dir == 1) {
-                pull = false;
-            } else if (P.force_dir == 2) {
-                pull = true;
-            } else if (!pull) {
-                pull = mf * P.alpha > mu;
-            } else {
-                pull = nf * P.beta >= g.n;
-            }
-            uint32_t* fcur = fb_of(P, cur);
-            uint32_t* fnext = fb_of(P, nxt);
-            uint32_t* fclr = fb_of(P, clr);
-            unsigned long long t0 = 0;
-            if (gtid == 0) {
-                t0 = globaltimer();
-                atomicAdd(&P.lc[hop].runs, 1u);
-                if (pull) atomicAdd(&P.lc[hop].pull_runs, 1u);
-                atomicAdd(&P.lc[hop].edges, mf);
-                atomicAdd(&P.lc[hop].union_edges, mf);
-            }
-            if (!pull && !items_ready) {
-                compact_phase(P, fcur, items_of(P, cur), qc, st, warp_gid, nwarps);
-                grid.sync();
-            }
-            for (uint32_t w = gtid; w < g.nwords; w += nthreads) fclr[w] = 0;
-            if (gtid == 0) P.qctl[clr] = QCtl{0, 0, 0, 0, 0};
-            if (pull) {
-                pull_phase(P, fcur, fnext, acc, warp_gid, nwarps);
-                items_ready = false;
-            } else {
-                push_phase(P, items_of(P, cur), ld_volatile(&qc->nitems), fnext, items_of(P, nxt),
-                           qn, acc, st, warp_gid, nwarps);
-                items_ready = true;
-            }
-            block_flush(acc, qn, &P.lc[hop], &P.misc[0]);
-            grid.sync();
-            if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
-            const unsigned long long found = ld_volatile(&qn->nfound);
-            cum += found;
-            last = found;
-            if (found == 0) break;
+    for (uint64_t grp = 0; grp < ngroups; ++grp) {
+        const uint32_t ns = (uint32_t)min((uint64_t)S, P.nseeds - grp * S);
+        // ---- init -------------------------------------------------------------
+        for (uint32_t i = gtid; i < (P.k + 1) * S; i += nthreads) {
+            P.cnt[i] = 0;
+            P.mfs[i] = 0;
+        }
+        for (uint32_t i = gtid; i < S; i += nthreads) {
+            P.logcnt[i] = 0;
+            P.dirs[i] = P.dirs[S + i] = kPush;
+            P.mus[i] = g.m;
         }
         if (gtid == 0) {
-            P.counts[qi] = P.mode == MGK_EXACT ? last : cum;
-            P.misc[1] = (last != 0 && hop > P.k) ? (P.k % 3) : 3ULL;
-            P.misc[2] = seed;
+            P.ctl->nitems[0] = P.ctl->nitems[1] = P.ctl->nitems[2] = 0;
+            P.ctl->log_n = 0;
+            P.ctl->log_overflow = 0;
+            for (int h = 0; h <= MGK_MAX_HOPS; ++h) P.ctl->found[h] = 0;
+        }
+        grid.sync();
+        // ---- seeds (hop 0) --------------------------------------------------------
+        {
+            bool me = gtid < ns;
+            uint32_t s = 0;
+            if (me) {
+                s = P.seeds[grp * S + gtid];
+                const uint32_t bit = 1u << (s & 31);
+                P.V[(size_t)gtid * nw + (s >> 5)] |= bit;
+                P.Fb[(size_t)gtid * nw + (s >> 5)] |= bit;
+            }
+            if (blockIdx.x * kBlock < ns) {
+                st.push(me, ((unsigned long long)gtid << 32) | s);
+                emit(P, 0, false, st.buf, st.n);
+                st.n = 0;
+            }
+            if (gtid == 0) P.ctl->found[0] = ns;
+        }
+        grid.sync();
+
+        uint32_t hop = 1;
+        for (; hop <= P.k; ++hop) {
+            const bool last = hop == P.k;
+            // ---- plan: per-seed direction (every block computes the same) ------------
+            bool pull_me = false;
+            if (threadIdx.x < kMaxSlots) {
+                uint8_t d = kDead;
+                const uint32_t slot = threadIdx.x;
+                if (slot < ns) {
+                    const unsigned long long nf = P.cnt[(hop - 1) * S + slot];
+                    const unsigned long long mf = P.mfs[(hop - 1) * S + slot];
+                    const unsigned long long mu = P.mus[slot];
+                    const uint8_t prev = P.dirs[((hop - 1) & 1) * S + slot];
+                    if (nf == 0) {
+                        d = kDead;
+                    } else if (P.force_dir == 1) {
+                        d = kPush;
+                    } else if (P.force_dir == 2 || (mf & kOverflowBit)) {
+                        d = kPull;
+                    } else if (prev == kPush) {
+                        d = mf * P.alpha > mu ? kPull : kPush;
+                    } else {
+                        d = nf * P.beta >= g.n ? kPull : kPush;
+                    }
+                    if (blockIdx.x == 0) {
+                        P.dirs[(hop & 1) * S + slot] = d == kDead ? prev : d;
+                        if (d != kDead) {
+                            atomicAdd(&P.lc[hop].runs, 1u);
+                            if (d == kPull) atomicAdd(&P.lc[hop].pull_runs, 1u);
+                            atomicAdd(&P.lc[hop].edges, mf & ~kOverflowBit);
+                            atomicAdd(&P.lc[hop].union_edges, mf & ~kOverflowBit);
+                        }
+                    }
+                }
+                s_dir[slot] = d;
+                pull_me = d == kPull;
+            }
+            compact(pull_me);
+            const uint32_t npull = s_nlist;
+            if (gtid == 0) P.ctl->nitems[(hop + 2) % 3] = 0;
+            unsigned long long t0 = 0;
+            if (gtid == 0) t0 = globaltimer();
+            // ---- expand -----------------------------------------------------------------
+            push_phase(P, hop, last, s_dir, st, acc, warp_gid, nwarps);
+            if (npull) pull_phase(P, hop, last, s_list, npull, st, acc, warp_gid, nwarps);
+            emit(P, hop, last, st.buf, st.n);
+            st.n = 0;
+            block_flush(acc, &P.ctl->found[hop], &P.lc[hop]);
+            grid.sync();
+            if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
+            if (ld_volatile(&P.ctl->found[hop]) == 0) break;
+        }
+        // ---- answers ----------------------------------------------------------------------
+        if (gtid < ns) {
+            unsigned long long r = 0;
+            if (P.mode == MGK_CUMULATIVE) {
+                for (uint32_t h = 1; h <= P.k; ++h) r += P.cnt[h * S + gtid];
+            } else {
+                r = P.cnt[P.k * S + gtid];
+            }
+            P.counts[grp * S + gtid] = r;
+        }
+        if (gtid == 0) P.ctl->last_which = (hop > P.k) ? (P.k % 3) : 3ULL;
+        // ---- cleanup: state back to all-zero -------------------------------------------------
+        const bool overflow = ld_volatile(&P.ctl->log_overflow) != 0;
+        const uint32_t nlog = min(ld_volatile(&P.ctl->log_n), P.log_cap);
+        bool dense_me = false;
+        if (threadIdx.x < kMaxSlots && threadIdx.x < ns)
+            dense_me = overflow || P.logcnt[threadIdx.x] > P.quota;
+        compact(dense_me);
+        const uint32_t ndense = s_nlist;
+        if (!P.keep_result) {
+            for (uint32_t i = gtid; i < nlog; i += nthreads) {
+                const unsigned long long e = P.logbuf[i];
+                const uint32_t slot = (uint32_t)(e >> 32), w = (uint32_t)e >> 5;
+                if (P.logcnt[slot] > P.quota || overflow) continue;
+                P.V[(size_t)slot * nw + w] = 0;
+                for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * nw + w] = 0;
+            }
+            const uint64_t dtotal = (uint64_t)ndense * nw;
+            for (uint64_t t = gtid; t < dtotal; t += nthreads) {
+                const uint32_t slot = s_list[t / nw];
+                const uint32_t w = (uint32_t)(t % nw);
+                P.V[(size_t)slot * nw + w] = 0;
+                for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * nw + w] = 0;
+            }
         }
         grid.sync();
     }
 }
 
-// ---- result ids (k_hop_frontier) ---------------------------------------------
+// Clears slot 0's bitmaps after a k_hop_frontier readback.
+__global__ void clear_slot0(uint32_t* V, uint32_t* Fb, uint32_t S, uint32_t nw) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
+        V[w] = 0;
+        for (int f = 0; f < 3; ++f) Fb[(size_t)f * S * nw + w] = 0;
+    }
+}
+
 __global__ void popc_words(const uint32_t* bits, uint32_t nwords, uint32_t drop, uint32_t* out) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwords) return;
@@ -356,20 +560,41 @@ __global__ void scatter_ids(const uint32_t* bits, uint32_t nwords, uint32_t drop
     }
 }
 
+uint32_t slots_for(const DevGraph& g) {
+    const uint64_t per_slot = 4ull * (g.nwords + 1) * 4;
+    const uint64_t budget = 4ull << 30;
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kMaxSlots, budget / per_slot));
+}
+
 }  // namespace
 
 cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
-    if (ws->visited) return cudaSuccess;
+    if (ws->fr_V) return cudaSuccess;
     const DevGraph& g = gr->dg;
-    const size_t wb = (size_t)(g.nwords + 1) * 4;
-    const size_t items = (size_t)(g.m / kChunk + g.n + 64);
+    const uint32_t S = slots_for(g);
+    const size_t bm = (size_t)S * g.nwords * 4 + 64;
     cudaError_t e;
-    if ((e = cudaMalloc(&ws->visited, wb))) return e;
-    for (int i = 0; i < 3; ++i)
-        if ((e = cudaMalloc(&ws->fb[i], wb))) return e;
+    if ((e = cudaMalloc(&ws->fr_V, bm))) return e;
+    if ((e = cudaMalloc(&ws->fr_Fb, 3 * bm))) return e;
+    if ((e = cudaMemset(ws->fr_V, 0, bm))) return e;
+    if ((e = cudaMemset(ws->fr_Fb, 0, 3 * bm))) return e;
+    const uint64_t want_items = (uint64_t)S * (g.m / kChunk + g.n) + 1024;
+    ws->fr_items_cap = (uint32_t)std::min<uint64_t>(want_items, 64ull << 20);
     for (int i = 0; i < 2; ++i)
-        if ((e = cudaMalloc(&ws->ss_items[i], items * sizeof(uint2)))) return e;
-    ws->bytes += 4 * wb + 2 * items * sizeof(uint2);
+        if ((e = cudaMalloc(&ws->fr_items[i], (size_t)ws->fr_items_cap * sizeof(uint2)))) return e;
+    ws->fr_quota = std::max<uint32_t>(64, g.nwords / 4);
+    ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * ws->fr_quota + 1024, 64ull << 20);
+    if ((e = cudaMalloc(&ws->fr_log, (size_t)ws->fr_log_cap * 8))) return e;
+    const size_t cs = (size_t)(MGK_MAX_HOPS + 1) * S;
+    if ((e = cudaMalloc(&ws->fr_cnt, cs * 4))) return e;
+    if ((e = cudaMalloc(&ws->fr_mfs, cs * 8))) return e;
+    if ((e = cudaMalloc(&ws->fr_mus, (size_t)S * 8))) return e;
+    if ((e = cudaMalloc(&ws->fr_logcnt, (size_t)S * 4))) return e;
+    if ((e = cudaMalloc(&ws->fr_dirs, (size_t)2 * S))) return e;
+    if ((e = cudaMalloc(&ws->fr_ctl, sizeof(FRCtl)))) return e;
+    ws->fr_slots = S;
+    ws->bytes += 4 * bm + 2 * (size_t)ws->fr_items_cap * 8 + (size_t)ws->fr_log_cap * 8 + cs * 12 +
+                 (size_t)S * 14 + sizeof(FRCtl);
     return cudaSuccess;
 }
 
@@ -383,33 +608,44 @@ cudaError_t launch_single(Launch& L) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ss_kernel, kBlock, 0)))
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, fr_kernel, kBlock, 0)))
             return e;
         if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
     }
-    SSParams P;
+    FRParams P;
     P.g = gr->dg;
     P.seeds = L.d_seeds;
-    P.nseeds = (uint32_t)L.nseeds;
+    P.nseeds = L.nseeds;
     P.k = L.k;
     P.mode = L.mode;
     P.counts = L.d_counts;
-    P.visited = ws->visited;
-    P.fb0 = ws->fb[0];
-    P.fb1 = ws->fb[1];
-    P.fb2 = ws->fb[2];
-    P.items0 = ws->ss_items[0];
-    P.items1 = ws->ss_items[1];
-    P.qctl = ws->qctl;
-    P.misc = ws->misc;
+    P.S = (uint32_t)std::min<uint64_t>(ws->fr_slots, L.nseeds);
+    P.V = ws->fr_V;
+    P.Fb = ws->fr_Fb;
+    P.items0 = ws->fr_items[0];
+    P.items1 = ws->fr_items[1];
+    P.items_cap = ws->fr_items_cap;
+    P.logbuf = ws->fr_log;
+    P.log_cap = ws->fr_log_cap;
+    P.cnt = ws->fr_cnt;
+    P.mfs = ws->fr_mfs;
+    P.mus = ws->fr_mus;
+    P.logcnt = ws->fr_logcnt;
+    P.dirs = ws->fr_dirs;
+    P.ctl = reinterpret_cast<FRCtl*>(ws->fr_ctl);
     P.lc = ws->lc;
     P.alpha = L.tuning.alpha;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
+    P.quota = ws->fr_quota;
+    P.keep_result = L.keep_result ? 1u : 0u;
+    // Fb is laid out [3][S_alloc][nw]; the kernel indexes it with P.S, so use
+    // the allocated slot count as the stride and cap the group size by it.
+    P.S = ws->fr_slots;
     L.grid = (uint32_t)(blocks_per_sm * num_sms);
     L.block = kBlock;
     void* args[] = {&P};
-    return cudaLaunchCooperativeKernel((const void*)ss_kernel, dim3(L.grid), dim3(kBlock), args, 0,
+    return cudaLaunchCooperativeKernel((const void*)fr_kernel, dim3(L.grid), dim3(kBlock), args, 0,
                                        L.stream);
 }
 
@@ -417,28 +653,32 @@ cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mo
                               unsigned long long* d_ids, unsigned long long* d_n, cudaStream_t s) {
     (void)k;
     const DevGraph& g = gr->dg;
+    const uint32_t nw = g.nwords;
+    FRCtl* ctl = reinterpret_cast<FRCtl*>(ws->fr_ctl);
     unsigned long long which = 0;
-    cudaError_t e = cudaMemcpyAsync(&which, ws->misc + 1, 8, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaMemcpyAsync(&which, &ctl->last_which, 8, cudaMemcpyDeviceToHost, s);
     if (e) return e;
     if ((e = cudaStreamSynchronize(s))) return e;
     const uint32_t* bits = nullptr;
     uint32_t drop = 0xFFFFFFFFu;
     if (mode == MGK_CUMULATIVE) {
-        bits = ws->visited;
+        bits = ws->fr_V;  // slot 0
         drop = seed;
     } else if (which < 3) {
-        bits = ws->fb[which];
-    } else {
-        return cudaMemsetAsync(d_n, 0, 8, s);
+        bits = ws->fr_Fb + (size_t)which * ws->fr_slots * nw;  // slot 0 of bitmap `which`
     }
-    // popcounts -> exclusive scan (+ total) -> scatter, all on the device.
-    uint32_t* offs = nullptr;
-    if ((e = cudaMallocAsync(&offs, (size_t)(g.nwords + 1) * 4, s))) return e;
-    const int tb = 256, nb = (int)((g.nwords + tb - 1) / tb);
-    popc_words<<<nb, tb, 0, s>>>(bits, g.nwords, drop, offs);
-    if ((e = exclusive_scan_u32(offs, g.nwords, d_n, s))) return e;
-    scatter_ids<<<nb, tb, 0, s>>>(bits, g.nwords, drop, offs, d_ids);
-    cudaFreeAsync(offs, s);
+    if (bits) {
+        uint32_t* offs = nullptr;
+        if ((e = cudaMallocAsync(&offs, (size_t)(nw + 1) * 4, s))) return e;
+        const int tb = 256, nb = (int)((nw + tb - 1) / tb);
+        popc_words<<<nb, tb, 0, s>>>(bits, nw, drop, offs);
+        if ((e = exclusive_scan_u32(offs, nw, d_n, s))) return e;
+        scatter_ids<<<nb, tb, 0, s>>>(bits, nw, drop, offs, d_ids);
+        cudaFreeAsync(offs, s);
+    } else {
+        if ((e = cudaMemsetAsync(d_n, 0, 8, s))) return e;
+    }
+    clear_slot0<<<148, 256, 0, s>>>(ws->fr_V, ws->fr_Fb, ws->fr_slots, nw);
     return cudaGetLastError();
 }
 

@@ -81,6 +81,7 @@ class Tuning:
     beta: int = 24
     force_dir: int = 0   # 0 auto, 1 push only, 2 pull only
     lanes_words: int = 0  # 0 auto; else 1, 2, 4, 8 (x64 seeds per batch)
+    alpha_lanes: int = 2
 
 
 class DeviceGraph:
@@ -166,13 +167,13 @@ class DeviceGraph:
         return int(_lib.lib().mgk_graph_device_bytes(self._h))
 
     def set_tuning(self, t: Tuning):
-        tt = MgkTuning(t.alpha, t.beta, t.force_dir, t.lanes_words)
+        tt = MgkTuning(t.alpha, t.beta, t.force_dir, t.lanes_words, t.alpha_lanes)
         _check(_lib.lib().mgk_graph_set_tuning(self._h, C.byref(tt)))
 
     def get_tuning(self) -> Tuning:
         tt = MgkTuning()
         _check(_lib.lib().mgk_graph_get_tuning(self._h, C.byref(tt)))
-        return Tuning(tt.alpha, tt.beta, tt.force_dir, tt.lanes_words)
+        return Tuning(tt.alpha, tt.beta, tt.force_dir, tt.lanes_words, tt.alpha_lanes)
 
     def _check_seed(self, seed: int):
         if seed < 0 or seed >= self.node_count:
