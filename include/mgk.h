@@ -76,6 +76,8 @@ typedef struct mgk_stats {
     uint32_t grid;         /* persistent CTAs launched */
     uint32_t block;        /* threads per CTA */
     double kernel_ms;      /* CUDA-event time of the traversal launch(es) */
+    uint64_t setup_ns;     /* device time clearing counters + seeding hop 0 */
+    uint64_t cleanup_ns;   /* device time returning the workspace to all-zero */
     mgk_level level[MGK_MAX_HOPS + 1];
 } mgk_stats;
 

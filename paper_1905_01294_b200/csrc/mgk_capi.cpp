@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -94,6 +95,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->fr_mfs);
     cudaFree(ws->fr_mus);
     cudaFree(ws->fr_logcnt);
+    cudaFree(ws->fr_pop);
     cudaFree(ws->fr_dirs);
     cudaFree(ws->fr_ctl);
     cudaFree(ws->lv);
@@ -229,6 +231,8 @@ void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint6
     st->grid = grid;
     st->block = block;
     st->kernel_ms = ms;
+    st->setup_ns = lc[0].ns;
+    st->cleanup_ns = lc[MGK_MAX_HOPS + 1].ns;
     for (int h = 0; h <= MGK_MAX_HOPS; ++h) {
         mgk_level& L = st->level[h];
         L.frontier = lc[h].frontier;
@@ -285,6 +289,16 @@ int finish_upload(int device, uint64_t nrows, uint64_t nnz, const uint32_t* rp, 
 }  // namespace
 
 void set_last_error(const std::string& msg) { t_err = msg; }
+
+cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, void** args,
+                              cudaStream_t stream) {
+    static const bool noncoop = [] {
+        const char* v = std::getenv("MGK_NONCOOP");
+        return v && v[0] == '1';
+    }();
+    if (noncoop) return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, 0, stream);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, 0, stream);
+}
 
 }  // namespace mgk
 

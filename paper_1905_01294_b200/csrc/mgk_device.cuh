@@ -34,6 +34,30 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
     return *reinterpret_cast<const volatile unsigned long long*>(p);
 }
 
+// Grid-wide barrier for the persistent engines (bar[0] = arrivals, bar[1] =
+// generation). Every CTA of the grid must be resident: the engines launch
+// with cudaLaunchCooperativeKernel (which guarantees it) and size the grid
+// from the occupancy calculator; MGK_NONCOOP=1 uses a plain launch of the
+// same grid so profilers that skip cooperative launches still see the kernel.
+// The fences on both sides order all memory traffic of the phase and drop
+// stale L1 lines (gpu-scope fence), like cooperative_groups grid.sync().
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned int gen = *reinterpret_cast<volatile unsigned int*>(bar + 1);
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            *reinterpret_cast<volatile unsigned int*>(bar) = 0;
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned int*>(bar + 1) == gen) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // Inclusive warp scan (all 32 lanes must call).
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
     const uint32_t lane = lane_id();
@@ -162,9 +186,9 @@ __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, cons
 
 // Items per warp iteration so that small work lists still spread over every
 // warp of the grid: a power of two in [1, 32].
-__device__ __forceinline__ uint32_t items_per_warp(uint32_t nitems, uint32_t nwarps) {
+__device__ __forceinline__ uint32_t items_per_warp(uint32_t nitems, uint64_t nwarps) {
     uint32_t g = 1;
-    while (g < 32 && (uint64_t)g * 2 * nwarps <= nitems) g <<= 1;
+    while (g < 32 && g * 2 * nwarps <= nitems) g <<= 1;
     return g;
 }
 

@@ -77,6 +77,7 @@ struct Workspace {
     unsigned long long* fr_mfs = nullptr;
     unsigned long long* fr_mus = nullptr;
     uint32_t* fr_logcnt = nullptr;
+    unsigned long long* fr_pop = nullptr;
     uint8_t* fr_dirs = nullptr;
     void* fr_ctl = nullptr;
     // lanes engine (allocated lazily for the widest W used)
@@ -136,6 +137,13 @@ struct Launch {
     bool keep_result = false;  // SINGLE: leave slot 0's bitmaps for k_hop_frontier
     uint32_t grid = 0, block = 0;  // out
 };
+
+// Launches a persistent engine kernel: cooperative (all CTAs co-resident,
+// guaranteed) unless MGK_NONCOOP=1 asks for a plain launch of the same
+// occupancy-sized grid (for profilers that do not intercept cooperative
+// launches; the grid still fits on an otherwise idle GPU).
+cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, void** args,
+                              cudaStream_t stream);
 
 cudaError_t launch_single(Launch& L);
 cudaError_t launch_lanes(Launch& L);

@@ -52,6 +52,7 @@ struct MSParams {
     unsigned long long* active;    // [2 * W]
     QCtl* qctl;                    // [2] by hop parity; .pad = push-equivalent edges
     unsigned long long* misc;      // [0] unexplored in-edges
+    unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
 };
@@ -444,7 +445,6 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     //   nitems = |R| (discovery list tail), nfound = push items built for the
     //   frontier, edges = sum of outdeg over R, pad = push-equivalent edges.
     constexpr uint32_t LB = 64 * W;
-    cg::grid_group grid = cg::this_grid();
     __shared__ uint32_t s_stage[kWarps][kStageCap];
     __shared__ unsigned long long s_cnt[LB];
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
         if (gtid == 0) P.misc[0] = g.m;
-        grid.sync();
+        grid_barrier(P.bar);
         // ---- seeds: level-0 frontier -------------------------------------------
         {
             bool first = false;
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             }
         }
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], nullptr, &P.misc[0]);
-        grid.sync();
+        grid_barrier(P.bar);
         // ---- finalize level 0 (V |= F0, hop-1 items) ------------------------------
         uint32_t nR = ld_volatile(&P.qctl[0].nitems);
         bool pull = P.force_dir == 2;
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                           s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
         acc.pairs = 0;  // the seeds themselves are never counted
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
-        grid.sync();
+        grid_barrier(P.bar);
 
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                               st, warp_gid, nwarps);
             }
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
-            grid.sync();
+            grid_barrier(P.bar);
             // ---- decide the next hop's direction (uniform) ---------------------------
             nR = ld_volatile(&qn->nitems);
             const unsigned long long mf = ld_volatile(&qn->edges);
@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
             block_flush(acc, qn, qn, &P.lc[hop], hop < P.k ? &P.lc[hop + 1] : nullptr,
                         &P.misc[0]);
-            grid.sync();
+            grid_barrier(P.bar);
             if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
             clog_used += nR;
             nR_prev = nR;
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 P.F1[i] = 0;
             }
         }
-        grid.sync();
+        grid_barrier(P.bar);
     }
 }
 
@@ -626,14 +626,14 @@ cudaError_t launch_w(Launch& L) {
     P.qctl = ws->qctl;
     P.misc = ws->misc;
     P.lc = ws->lc;
+    P.bar = reinterpret_cast<unsigned int*>(ws->misc + 8);
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
     L.grid = (uint32_t)(blocks_per_sm * num_sms);
     L.block = kBlock;
     void* args[] = {&P};
-    return cudaLaunchCooperativeKernel((const void*)ms_kernel<W>, dim3(L.grid), dim3(kBlock), args,
-                                       0, L.stream);
+    return launch_persistent((const void*)ms_kernel<W>, L.grid, kBlock, args, L.stream);
 }
 
 }  // namespace

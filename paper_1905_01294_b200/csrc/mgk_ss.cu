@@ -43,6 +43,8 @@ struct FRCtl {
     unsigned int pad;
     unsigned long long found[MGK_MAX_HOPS + 1];
     unsigned long long last_which;  // frontier bitmap id of the final hop (frontier ids)
+    unsigned int done;              // CTAs finished with the cleanup (last one answers)
+    unsigned long long t_clean;     // cleanup start (%globaltimer), for the stats
 };
 
 struct FRParams {
@@ -53,8 +55,9 @@ struct FRParams {
     int mode;
     unsigned long long* counts;
     uint32_t S;
-    uint32_t* V;   // [S][nwords]
-    uint32_t* Fb;  // [3][S][nwords]
+    uint32_t rs;   // bitmap row stride in words (nwords rounded up to 32: 128-B rows)
+    uint32_t* V;   // [S][rs]
+    uint32_t* Fb;  // [3][S][rs]
     uint2* items0;
     uint2* items1;
     uint32_t items_cap;
@@ -62,10 +65,12 @@ struct FRParams {
     uint32_t log_cap;
     uint32_t* cnt;             // [(k+1)][S] discoveries per hop per seed
     unsigned long long* mfs;   // [(k+1)][S] out-edges of those discoveries
-    unsigned long long* mus;   // [S] unexplored in-edges per seed
-    uint32_t* logcnt;          // [S]
+    unsigned long long* mex;   // [S] explored in-edges per seed (unexplored = m - mex)
+    uint32_t* logcnt;          // [S] 1 = last hop not logged: clear V densely
+    unsigned long long* pop;   // [S] popcount of V for those seeds (counting pass)
     uint8_t* dirs;             // [2][S]
     FRCtl* ctl;
+    unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
     uint32_t quota;  // per-seed log entries before the seed is cleared densely
@@ -102,49 +107,57 @@ __device__ void block_flush(Acc& a, unsigned long long* found_total, LevelCounte
     a.zero();
 }
 
-// Warp-wide: sum (a, b, c) over the lanes of each distinct slot and apply one
-// set of atomics per slot. Returns, per lane, the slot's pre-add logcnt.
-__device__ __forceinline__ uint32_t slot_commit(const FRParams& P, uint32_t hop, bool valid,
-                                                uint32_t slot, uint32_t deg, uint32_t indeg,
-                                                bool last) {
-    uint32_t old_log = 0;
+// Warp-wide: per distinct slot among the valid lanes, add the lane count (and,
+// before the last hop, the summed out / in degrees) to that seed's counters
+// with one fire-and-forget atomic each.
+__device__ __forceinline__ void slot_commit(const FRParams& P, uint32_t hop, bool valid,
+                                            uint32_t slot, uint32_t deg, uint32_t indeg,
+                                            bool last) {
     unsigned pending = __ballot_sync(kFull, valid);
     while (pending) {
         const int leader = __ffs(pending) - 1;
         const uint32_t s = __shfl_sync(kFull, slot, leader);
         const bool mine = valid && slot == s;
         const unsigned grp = __ballot_sync(kFull, mine);
-        const uint32_t n = __popc(grp);
         unsigned long long d = mine ? deg : 0, i = mine ? indeg : 0;
         if (!last) {
             d = warp_sum_u64(d);
             i = warp_sum_u64(i);
         }
-        uint32_t ol = 0;
         if ((int)lane_id() == leader) {
-            atomicAdd(&P.cnt[hop * P.S + s], n);
-            ol = atomicAdd(&P.logcnt[s], n);
+            atomicAdd(&P.cnt[hop * P.S + s], (unsigned)__popc(grp));
             if (!last) {
                 atomicAdd(&P.mfs[hop * P.S + s], d);
-                atomicAdd(&P.mus[s], 0ULL - i);
+                atomicAdd(&P.mex[s], i);
             }
         }
-        ol = __shfl_sync(kFull, ol, leader);
-        if (mine) old_log = ol;
         pending &= ~grp;
     }
-    return old_log;
 }
 
 // Warp-wide emission of n staged (slot << 32 | u) discoveries of `hop`:
 // per-seed counters, the cleanup log, and (unless this is the last hop) the
-// next hop's push items.
-__device__ void emit(const FRParams& P, uint32_t hop, bool last, const unsigned long long* buf,
-                     uint32_t n) {
+// next hop's push items. Discoveries before the last hop are always logged
+// (they also mark frontier bitmaps); last-hop discoveries only for seeds whose
+// last hop was predicted small (s_logok), the others are cleared densely.
+__device__ void emit(const FRParams& P, uint32_t hop, bool last, const uint8_t* s_logok,
+                     const unsigned long long* buf, uint32_t n) {
+    if (n == 0) return;
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     unsigned int* nitems = &P.ctl->nitems[(hop + 1) % 3];
     uint2* items = ((hop + 1) & 1) ? P.items1 : P.items0;
+    // one log reservation for the whole stage
+    uint32_t nlog = 0;
+    for (uint32_t i = lane; i < n; i += 32)
+        nlog += (!last || s_logok[(uint32_t)(buf[i] >> 32)]) ? 1u : 0u;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) nlog += __shfl_xor_sync(kFull, nlog, d);
+    uint32_t log_base = 0;
+    if (nlog) {
+        if (lane == 0) log_base = atomicAdd(&P.ctl->log_n, nlog);
+        log_base = __shfl_sync(kFull, log_base, 0);
+    }
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
         const uint32_t i = i0 + lane;
         const bool valid = i < n;
@@ -159,22 +172,18 @@ __device__ void emit(const FRParams& P, uint32_t hop, bool last, const unsigned 
                 indeg = __ldg(g.cp + u + 1) - __ldg(g.cp + u);
             }
         }
-        const uint32_t old_log = slot_commit(P, hop, valid, slot, deg, indeg, last);
-        // cleanup log: entries of seeds still under their quota
-        const bool loggable = valid && old_log < P.quota;
+        slot_commit(P, hop, valid, slot, deg, indeg, last);
+        const bool loggable = valid && (!last || s_logok[slot]);
         const unsigned lm = __ballot_sync(kFull, loggable);
-        if (lm) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&P.ctl->log_n, (unsigned)__popc(lm));
-            base = __shfl_sync(kFull, base, 0);
-            if (loggable) {
-                const uint32_t at = base + __popc(lm & lanemask_lt());
-                if (at < P.log_cap) P.logbuf[at] = ((unsigned long long)slot << 32) | u;
-                else P.ctl->log_overflow = 1;
-            }
+        if (loggable) {
+            const uint32_t at = log_base + __popc(lm & lanemask_lt());
+            // bit 63 marks a last-hop entry: it has no frontier bit to clear
+            if (at < P.log_cap)
+                P.logbuf[at] = ((unsigned long long)(last ? 0x80000000u | slot : slot) << 32) | u;
+            else P.ctl->log_overflow = 1;
         }
+        log_base += __popc(lm);
         if (last) continue;
-        // next-hop push items
         const uint32_t nit = (deg + kChunk - 1) / kChunk;
         const uint32_t incl = warp_incl_scan(nit);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
@@ -206,26 +215,29 @@ __device__ void emit(const FRParams& P, uint32_t hop, bool last, const unsigned 
 }
 
 __device__ __forceinline__ void stage_push(const FRParams& P, uint32_t hop, bool last,
+                                           const uint8_t* s_logok,
                                            Stage<kStageCap, unsigned long long>& st, bool found,
                                            uint32_t slot, uint32_t u) {
     st.push(found, ((unsigned long long)slot << 32) | u);
     if (st.full()) {
-        emit(P, hop, last, st.buf, st.n);
+        emit(P, hop, last, s_logok, st.buf, st.n);
         st.n = 0;
     }
 }
 
 // Push: expand the work items of seeds in push mode.
 __device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uint8_t* s_dir,
-                           Stage<kStageCap, unsigned long long>& st, Acc& acc, uint32_t warp_gid,
-                           uint32_t nwarps) {
+                           const uint8_t* s_logok, Stage<kStageCap, unsigned long long>& st,
+                           Acc& acc, uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     const uint32_t nw = g.nwords;
     const uint32_t nitems = min(ld_volatile(&P.ctl->nitems[hop % 3]), P.items_cap);
     const uint2* items = (hop & 1) ? P.items1 : P.items0;
     const uint32_t fn = hop % 3;
-    const uint32_t G = items_per_warp(nitems, nwarps);
+    const bool set_fb = !last || P.keep_result;
+    // ~8 steps per warp at least, so the tail of the hop stays balanced
+    const uint32_t G = items_per_warp(nitems, (uint64_t)nwarps * 8);
     for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
         const uint32_t idx = base + lane;
         uint32_t len = 0, slot = 0, beg = 0;
@@ -240,9 +252,9 @@ __device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uin
         const uint32_t incl = warp_incl_scan(len);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         const uint32_t off = beg - (incl - len);
-        // kIlp edges per lane per step: all loads of a step are in flight together
+        // kIlp edges per lane per step: all loads / atomics of a step in flight together
         for (uint32_t x0 = 0; x0 < total; x0 += 32 * kIlp) {
-            uint32_t u[kIlp], sj[kIlp], vis[kIlp];
+            uint32_t u[kIlp], sj[kIlp], old[kIlp];
             bool valid[kIlp];
 #pragma unroll
             for (int r = 0; r < kIlp; ++r) {
@@ -251,26 +263,29 @@ __device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uin
                 const uint32_t j = warp_owner(incl, valid[r] ? x : total - 1);
                 const uint32_t pos = __shfl_sync(kFull, off, j) + x;
                 sj[r] = __shfl_sync(kFull, slot, j);
-                u[r] = valid[r] ? __ldg(g.ci + pos) : 0;
+                u[r] = valid[r] ? __ldcs(g.ci + pos) : 0;  // streamed: keep bitmaps in L2
             }
 #pragma unroll
-            for (int r = 0; r < kIlp; ++r)
-                vis[r] = valid[r] ? ld_cg(P.V + (size_t)sj[r] * nw + (u[r] >> 5)) : kFull;
+            for (int r = 0; r < kIlp; ++r) {
+                old[r] = kFull;
+                if (valid[r]) {
+                    uint32_t* vw = P.V + (size_t)sj[r] * P.rs + (u[r] >> 5);
+                    const uint32_t bit = 1u << (u[r] & 31);
+                    // a seed's last hop that is not logged only sets bits
+                    // (fire-and-forget red.or); it is counted afterwards by a
+                    // popcount of the bitmap in the clearing pass
+                    if (last && !s_logok[sj[r]]) atomicOr(vw, bit);
+                    else old[r] = atomicOr(vw, bit);
+                }
+            }
 #pragma unroll
             for (int r = 0; r < kIlp; ++r) {
-                bool found = false;
-                const uint32_t bit = 1u << (u[r] & 31);
-                if (valid[r] && !(vis[r] & bit)) {
-                    const uint32_t old = atomicOr(P.V + (size_t)sj[r] * nw + (u[r] >> 5), bit);
-                    if (!(old & bit)) {
-                        found = true;
-                        if (!last || P.keep_result)
-                            atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * nw + (u[r] >> 5), bit);
-                    }
-                }
+                const bool found = !((old[r] >> (u[r] & 31)) & 1u);
+                if (found && set_fb)
+                    atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * P.rs + (u[r] >> 5), 1u << (u[r] & 31));
                 acc.scanned += valid[r];
                 acc.found += found;
-                stage_push(P, hop, last, st, found, sj[r], u[r]);
+                stage_push(P, hop, last, s_logok, st, found, sj[r], u[r]);
             }
         }
     }
@@ -285,8 +300,9 @@ __device__ __forceinline__ bool fbit(const uint32_t* f, uint32_t v) {
 // frontier. One warp owns one (seed, bitmap word) so V / F words are written
 // without atomics.
 __device__ void pull_phase(const FRParams& P, uint32_t hop, bool last, const uint16_t* s_pull,
-                           uint32_t npull, Stage<kStageCap, unsigned long long>& st, Acc& acc,
-                           uint32_t warp_gid, uint32_t nwarps) {
+                           uint32_t npull, const uint8_t* s_logok,
+                           Stage<kStageCap, unsigned long long>& st, Acc& acc, uint32_t warp_gid,
+                           uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     const uint32_t nw = g.nwords;
@@ -295,11 +311,11 @@ __device__ void pull_phase(const FRParams& P, uint32_t hop, bool last, const uin
         const uint32_t pi = (uint32_t)(t / nw);
         const uint32_t w = (uint32_t)(t - (uint64_t)pi * nw);
         const uint32_t slot = s_pull[pi];
-        uint32_t* vword = P.V + (size_t)slot * nw + w;
+        uint32_t* vword = P.V + (size_t)slot * P.rs + w;
         const uint32_t vis = *vword;
         const uint32_t done = vis | __ldg(g.no_in + w);
         if (done == kFull) continue;
-        const uint32_t* fcur = P.Fb + ((size_t)((hop - 1) % 3) * P.S + slot) * nw;
+        const uint32_t* fcur = P.Fb + ((size_t)((hop - 1) % 3) * P.S + slot) * P.rs;
         const uint32_t u = w * 32 + lane;
         const bool cand = !((done >> lane) & 1u);
         uint32_t b = 0, e = 0;
@@ -359,17 +375,17 @@ __device__ void pull_phase(const FRParams& P, uint32_t hop, bool last, const uin
         if (fm) {
             if (lane == 0) {
                 *vword = vis | fm;
-                if (!last || P.keep_result) P.Fb[((size_t)(hop % 3) * P.S + slot) * nw + w] = fm;
+                if (!last || P.keep_result) P.Fb[((size_t)(hop % 3) * P.S + slot) * P.rs + w] = fm;
             }
         }
-        stage_push(P, hop, last, st, found, slot, u);
+        stage_push(P, hop, last, s_logok, st, found, slot, u);
     }
 }
 
 __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
-    cg::grid_group grid = cg::this_grid();
     __shared__ unsigned long long s_stage[kWarps][kStageCap];
     __shared__ uint8_t s_dir[kMaxSlots];
+    __shared__ uint8_t s_flag[kMaxSlots];  // last hop: log it; cleanup: clear V densely
     __shared__ uint16_t s_list[kMaxSlots];
     __shared__ uint32_t s_wcount[kWarps];
     __shared__ uint32_t s_nlist;
@@ -403,41 +419,40 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
 
     for (uint64_t grp = 0; grp < ngroups; ++grp) {
         const uint32_t ns = (uint32_t)min((uint64_t)S, P.nseeds - grp * S);
-        // ---- init -------------------------------------------------------------
-        for (uint32_t i = gtid; i < (P.k + 1) * S; i += nthreads) {
-            P.cnt[i] = 0;
-            P.mfs[i] = 0;
-        }
-        for (uint32_t i = gtid; i < S; i += nthreads) {
-            P.logcnt[i] = 0;
-            P.dirs[i] = P.dirs[S + i] = kPush;
-            P.mus[i] = g.m;
+        unsigned long long t_init = 0;
+        if (gtid == 0) t_init = globaltimer();
+        // ---- seeds (hop 0): one warp per seed; counters are zero on entry --------------
+        for (uint32_t slot = warp_gid; slot < ns; slot += nwarps) {
+            const uint32_t s = P.seeds[grp * S + slot];
+            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
+            if (lane == 0) {
+                const uint32_t bit = 1u << (s & 31);
+                P.V[(size_t)slot * P.rs + (s >> 5)] = bit;
+                P.Fb[(size_t)slot * P.rs + (s >> 5)] = bit;
+                P.cnt[slot] = 1;
+                P.mfs[slot] = deg;
+                P.mex[slot] = __ldg(g.cp + s + 1) - __ldg(g.cp + s);
+                P.logbuf[slot] = ((unsigned long long)slot << 32) | s;  // log slots [0, ns)
+            }
+            const uint32_t nit = (deg + kChunk - 1) / kChunk;
+            uint32_t base = 0;
+            if (lane == 0 && nit) base = atomicAdd(&P.ctl->nitems[1], nit);
+            base = __shfl_sync(kFull, base, 0);
+            if (base + nit <= P.items_cap) {
+                for (uint32_t x = lane; x < nit; x += 32) {
+                    const uint32_t st0 = b + x * kChunk;
+                    P.items1[base + x] = make_uint2(st0, (slot << 5) | (min(kChunk, b + deg - st0) - 1));
+                }
+            } else if (lane == 0) {
+                atomicOr(&P.mfs[slot], kOverflowBit);
+            }
         }
         if (gtid == 0) {
-            P.ctl->nitems[0] = P.ctl->nitems[1] = P.ctl->nitems[2] = 0;
-            P.ctl->log_n = 0;
-            P.ctl->log_overflow = 0;
-            for (int h = 0; h <= MGK_MAX_HOPS; ++h) P.ctl->found[h] = 0;
+            P.ctl->found[0] = ns;
+            atomicAdd(&P.ctl->log_n, ns);
         }
-        grid.sync();
-        // ---- seeds (hop 0) --------------------------------------------------------
-        {
-            bool me = gtid < ns;
-            uint32_t s = 0;
-            if (me) {
-                s = P.seeds[grp * S + gtid];
-                const uint32_t bit = 1u << (s & 31);
-                P.V[(size_t)gtid * nw + (s >> 5)] |= bit;
-                P.Fb[(size_t)gtid * nw + (s >> 5)] |= bit;
-            }
-            if (blockIdx.x * kBlock < ns) {
-                st.push(me, ((unsigned long long)gtid << 32) | s);
-                emit(P, 0, false, st.buf, st.n);
-                st.n = 0;
-            }
-            if (gtid == 0) P.ctl->found[0] = ns;
-        }
-        grid.sync();
+        grid_barrier(P.bar);
+        if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds
 
         uint32_t hop = 1;
         for (; hop <= P.k; ++hop) {
@@ -450,7 +465,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
                 if (slot < ns) {
                     const unsigned long long nf = P.cnt[(hop - 1) * S + slot];
                     const unsigned long long mf = P.mfs[(hop - 1) * S + slot];
-                    const unsigned long long mu = P.mus[slot];
+                    const unsigned long long mu = g.m - P.mex[slot];
                     const uint8_t prev = P.dirs[((hop - 1) & 1) * S + slot];
                     if (nf == 0) {
                         d = kDead;
@@ -475,6 +490,15 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
                 }
                 s_dir[slot] = d;
                 pull_me = d == kPull;
+                // last hop: log the discoveries only if they are bounded by the
+                // quota (mf = out-edges of the frontier); otherwise the seed's
+                // visited bitmap is cleared densely afterwards
+                if (last) {
+                    const bool logok = slot < ns && (P.keep_result ||
+                                                     P.mfs[(hop - 1) * S + slot] <= P.quota);
+                    s_flag[slot] = logok;
+                    if (blockIdx.x == 0 && slot < ns && d != kDead && !logok) P.logcnt[slot] = 1;
+                }
             }
             compact(pull_me);
             const uint32_t npull = s_nlist;
@@ -482,59 +506,127 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
             unsigned long long t0 = 0;
             if (gtid == 0) t0 = globaltimer();
             // ---- expand -----------------------------------------------------------------
-            push_phase(P, hop, last, s_dir, st, acc, warp_gid, nwarps);
-            if (npull) pull_phase(P, hop, last, s_list, npull, st, acc, warp_gid, nwarps);
-            emit(P, hop, last, st.buf, st.n);
+            push_phase(P, hop, last, s_dir, s_flag, st, acc, warp_gid, nwarps);
+            if (npull) pull_phase(P, hop, last, s_list, npull, s_flag, st, acc, warp_gid, nwarps);
+            emit(P, hop, last, s_flag, st.buf, st.n);
             st.n = 0;
             block_flush(acc, &P.ctl->found[hop], &P.lc[hop]);
-            grid.sync();
+            grid_barrier(P.bar);
             if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
             if (ld_volatile(&P.ctl->found[hop]) == 0) break;
         }
-        // ---- answers ----------------------------------------------------------------------
-        if (gtid < ns) {
-            unsigned long long r = 0;
-            if (P.mode == MGK_CUMULATIVE) {
-                for (uint32_t h = 1; h <= P.k; ++h) r += P.cnt[h * S + gtid];
-            } else {
-                r = P.cnt[P.k * S + gtid];
-            }
-            P.counts[grp * S + gtid] = r;
-        }
         if (gtid == 0) P.ctl->last_which = (hop > P.k) ? (P.k % 3) : 3ULL;
         // ---- cleanup: state back to all-zero -------------------------------------------------
+        // Every discovery before the last hop is in the log (it may also have a
+        // frontier bit); last-hop discoveries are logged unless the seed was
+        // flagged (logcnt[slot] = 1): its last hop only set bits, so its answer
+        // is a popcount of its visited bitmap, taken while clearing it densely.
+        // A log overflow clears everything densely.
+        if (gtid == 0) P.ctl->t_clean = globaltimer();
         const bool overflow = ld_volatile(&P.ctl->log_overflow) != 0;
         const uint32_t nlog = min(ld_volatile(&P.ctl->log_n), P.log_cap);
         bool dense_me = false;
-        if (threadIdx.x < kMaxSlots && threadIdx.x < ns)
-            dense_me = overflow || P.logcnt[threadIdx.x] > P.quota;
+        if (threadIdx.x < kMaxSlots) {
+            const bool pop_me = threadIdx.x < ns && P.logcnt[threadIdx.x] != 0;
+            dense_me = threadIdx.x < ns && (overflow || pop_me);
+            s_flag[threadIdx.x] = pop_me ? 2 : (dense_me ? 1 : 0);
+        }
         compact(dense_me);
         const uint32_t ndense = s_nlist;
         if (!P.keep_result) {
-            for (uint32_t i = gtid; i < nlog; i += nthreads) {
-                const unsigned long long e = P.logbuf[i];
-                const uint32_t slot = (uint32_t)(e >> 32), w = (uint32_t)e >> 5;
-                if (P.logcnt[slot] > P.quota || overflow) continue;
-                P.V[(size_t)slot * nw + w] = 0;
-                for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * nw + w] = 0;
+            if (!overflow) {
+                for (uint32_t i = gtid; i < nlog; i += nthreads) {
+                    const unsigned long long e = P.logbuf[i];
+                    const uint32_t slot = (uint32_t)(e >> 32) & 0x7FFFFFFFu, w = (uint32_t)e >> 5;
+                    if (!s_flag[slot]) P.V[(size_t)slot * P.rs + w] = 0;
+                    if (!(e >> 63))
+                        for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * P.rs + w] = 0;
+                }
             }
-            const uint64_t dtotal = (uint64_t)ndense * nw;
-            for (uint64_t t = gtid; t < dtotal; t += nthreads) {
-                const uint32_t slot = s_list[t / nw];
-                const uint32_t w = (uint32_t)(t % nw);
-                P.V[(size_t)slot * nw + w] = 0;
-                for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * nw + w] = 0;
+            // dense pass: (slot, 8192-word chunk) tasks; each thread keeps four
+            // aligned uint4 loads in flight (rows are padded to 128 B, padding
+            // words are always zero)
+            constexpr uint32_t kDenseChunk = 4 * 4 * kBlock;
+            const uint32_t chunks = (P.rs + kDenseChunk - 1) / kDenseChunk;
+            for (uint32_t t = blockIdx.x; t < ndense * chunks; t += gridDim.x) {
+                const uint32_t slot = s_list[t / chunks];
+                const uint32_t base = (t % chunks) * kDenseChunk + threadIdx.x * 4;
+                uint4* row = reinterpret_cast<uint4*>(P.V + (size_t)slot * P.rs);
+                uint4 v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t w = base + i * 4 * kBlock;
+                    v[i] = w < P.rs ? __ldcs(row + w / 4) : make_uint4(0, 0, 0, 0);
+                }
+                uint32_t pc = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t w = base + i * 4 * kBlock;
+                    pc += __popc(v[i].x) + __popc(v[i].y) + __popc(v[i].z) + __popc(v[i].w);
+                    if (w < P.rs) {
+                        __stcs(row + w / 4, make_uint4(0, 0, 0, 0));
+                        if (overflow)
+                            for (int f = 0; f < 3; ++f)
+                                __stcs(reinterpret_cast<uint4*>(P.Fb + ((size_t)f * S + slot) * P.rs + w),
+                                       make_uint4(0, 0, 0, 0));
+                    }
+                }
+                if (s_flag[slot] == 2) {
+#pragma unroll
+                    for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
+                    if (lane == 0 && pc) atomicAdd(&P.pop[slot], (unsigned long long)pc);
+                }
             }
         }
-        grid.sync();
+        // ---- answers (by the last CTA to finish cleaning); leave every counter zero ----------
+        __shared__ bool s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&P.ctl->done, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            for (uint32_t slot = threadIdx.x; slot < ns; slot += kBlock) {
+                unsigned long long before = 0;  // vertices visited before the last hop (seed incl.)
+                for (uint32_t h = 0; h < P.k; ++h) before += ld_cg(&P.cnt[h * S + slot]);
+                const unsigned long long lastc = ld_cg(&P.cnt[P.k * S + slot]);
+                unsigned long long r;
+                if (ld_cg(&P.logcnt[slot]) != 0) {
+                    const unsigned long long total = ld_cg(&P.pop[slot]);
+                    r = P.mode == MGK_CUMULATIVE ? total - 1 : total - before;
+                } else {
+                    r = P.mode == MGK_CUMULATIVE ? before - 1 + lastc : lastc;
+                }
+                P.counts[grp * S + slot] = r;
+                for (uint32_t h = 0; h <= P.k; ++h) {
+                    P.cnt[h * S + slot] = 0;
+                    P.mfs[h * S + slot] = 0;
+                }
+                P.logcnt[slot] = 0;
+                P.pop[slot] = 0;
+                P.mex[slot] = 0;
+                P.dirs[slot] = P.dirs[S + slot] = kPush;
+            }
+            if (threadIdx.x == 0) {
+                P.ctl->nitems[0] = P.ctl->nitems[1] = P.ctl->nitems[2] = 0;
+                P.ctl->log_n = 0;
+                P.ctl->log_overflow = 0;
+                for (uint32_t h = 0; h <= P.k; ++h) P.ctl->found[h] = 0;
+                P.ctl->done = 0;
+                atomicAdd(&P.lc[MGK_MAX_HOPS + 1].ns, globaltimer() - ld_cg(&P.ctl->t_clean));
+            }
+        }
+        if (grp + 1 < ngroups) grid_barrier(P.bar);
     }
 }
 
 // Clears slot 0's bitmaps after a k_hop_frontier readback.
-__global__ void clear_slot0(uint32_t* V, uint32_t* Fb, uint32_t S, uint32_t nw) {
+__global__ void clear_slot0(uint32_t* V, uint32_t* Fb, uint32_t S, uint32_t nw, uint32_t rs) {
     for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) {
         V[w] = 0;
-        for (int f = 0; f < 3; ++f) Fb[(size_t)f * S * nw + w] = 0;
+        for (int f = 0; f < 3; ++f) Fb[(size_t)f * S * rs + w] = 0;
     }
 }
 
@@ -560,8 +652,10 @@ __global__ void scatter_ids(const uint32_t* bits, uint32_t nwords, uint32_t drop
     }
 }
 
+uint32_t row_stride(const DevGraph& g) { return (g.nwords + 31) & ~31u; }
+
 uint32_t slots_for(const DevGraph& g) {
-    const uint64_t per_slot = 4ull * (g.nwords + 1) * 4;
+    const uint64_t per_slot = 4ull * row_stride(g) * 4;
     const uint64_t budget = 4ull << 30;
     return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(kMaxSlots, budget / per_slot));
 }
@@ -572,7 +666,7 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     if (ws->fr_V) return cudaSuccess;
     const DevGraph& g = gr->dg;
     const uint32_t S = slots_for(g);
-    const size_t bm = (size_t)S * g.nwords * 4 + 64;
+    const size_t bm = (size_t)S * row_stride(g) * 4 + 64;
     cudaError_t e;
     if ((e = cudaMalloc(&ws->fr_V, bm))) return e;
     if ((e = cudaMalloc(&ws->fr_Fb, 3 * bm))) return e;
@@ -582,16 +676,28 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     ws->fr_items_cap = (uint32_t)std::min<uint64_t>(want_items, 64ull << 20);
     for (int i = 0; i < 2; ++i)
         if ((e = cudaMalloc(&ws->fr_items[i], (size_t)ws->fr_items_cap * sizeof(uint2)))) return e;
+    // a last hop that can touch more than ~nwords/4 vertices of a seed is not
+    // logged; its visited bitmap is cleared with one coalesced pass instead
     ws->fr_quota = std::max<uint32_t>(64, g.nwords / 4);
-    ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * ws->fr_quota + 1024, 64ull << 20);
+    ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * (g.n + 64), 64ull << 20);
     if ((e = cudaMalloc(&ws->fr_log, (size_t)ws->fr_log_cap * 8))) return e;
     const size_t cs = (size_t)(MGK_MAX_HOPS + 1) * S;
     if ((e = cudaMalloc(&ws->fr_cnt, cs * 4))) return e;
     if ((e = cudaMalloc(&ws->fr_mfs, cs * 8))) return e;
     if ((e = cudaMalloc(&ws->fr_mus, (size_t)S * 8))) return e;
+    // per-seed counters and the control block are all-zero between launches
+    // (each launch re-zeroes what it used), so a launch needs no init phase
+    if ((e = cudaMemset(ws->fr_mus, 0, (size_t)S * 8))) return e;
     if ((e = cudaMalloc(&ws->fr_logcnt, (size_t)S * 4))) return e;
+    if ((e = cudaMalloc(&ws->fr_pop, (size_t)S * 8))) return e;
+    if ((e = cudaMemset(ws->fr_pop, 0, (size_t)S * 8))) return e;
     if ((e = cudaMalloc(&ws->fr_dirs, (size_t)2 * S))) return e;
     if ((e = cudaMalloc(&ws->fr_ctl, sizeof(FRCtl)))) return e;
+    if ((e = cudaMemset(ws->fr_cnt, 0, cs * 4))) return e;
+    if ((e = cudaMemset(ws->fr_mfs, 0, cs * 8))) return e;
+    if ((e = cudaMemset(ws->fr_logcnt, 0, (size_t)S * 4))) return e;
+    if ((e = cudaMemset(ws->fr_dirs, 0, (size_t)2 * S))) return e;
+    if ((e = cudaMemset(ws->fr_ctl, 0, sizeof(FRCtl)))) return e;
     ws->fr_slots = S;
     ws->bytes += 4 * bm + 2 * (size_t)ws->fr_items_cap * 8 + (size_t)ws->fr_log_cap * 8 + cs * 12 +
                  (size_t)S * 14 + sizeof(FRCtl);
@@ -629,11 +735,13 @@ cudaError_t launch_single(Launch& L) {
     P.log_cap = ws->fr_log_cap;
     P.cnt = ws->fr_cnt;
     P.mfs = ws->fr_mfs;
-    P.mus = ws->fr_mus;
+    P.mex = ws->fr_mus;
     P.logcnt = ws->fr_logcnt;
+    P.pop = ws->fr_pop;
     P.dirs = ws->fr_dirs;
     P.ctl = reinterpret_cast<FRCtl*>(ws->fr_ctl);
     P.lc = ws->lc;
+    P.bar = reinterpret_cast<unsigned int*>(ws->misc + 8);
     P.alpha = L.tuning.alpha;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -642,11 +750,11 @@ cudaError_t launch_single(Launch& L) {
     // Fb is laid out [3][S_alloc][nw]; the kernel indexes it with P.S, so use
     // the allocated slot count as the stride and cap the group size by it.
     P.S = ws->fr_slots;
+    P.rs = row_stride(gr->dg);
     L.grid = (uint32_t)(blocks_per_sm * num_sms);
     L.block = kBlock;
     void* args[] = {&P};
-    return cudaLaunchCooperativeKernel((const void*)fr_kernel, dim3(L.grid), dim3(kBlock), args, 0,
-                                       L.stream);
+    return launch_persistent((const void*)fr_kernel, L.grid, kBlock, args, L.stream);
 }
 
 cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mode, uint32_t seed,
@@ -665,7 +773,7 @@ cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mo
         bits = ws->fr_V;  // slot 0
         drop = seed;
     } else if (which < 3) {
-        bits = ws->fr_Fb + (size_t)which * ws->fr_slots * nw;  // slot 0 of bitmap `which`
+        bits = ws->fr_Fb + (size_t)which * ws->fr_slots * row_stride(g);  // slot 0 of bitmap `which`
     }
     if (bits) {
         uint32_t* offs = nullptr;
@@ -678,7 +786,7 @@ cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mo
     } else {
         if ((e = cudaMemsetAsync(d_n, 0, 8, s))) return e;
     }
-    clear_slot0<<<148, 256, 0, s>>>(ws->fr_V, ws->fr_Fb, ws->fr_slots, nw);
+    clear_slot0<<<148, 256, 0, s>>>(ws->fr_V, ws->fr_Fb, ws->fr_slots, nw, row_stride(g));
     return cudaGetLastError();
 }
 

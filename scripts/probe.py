@@ -14,6 +14,12 @@ from paper_1905_01294_b200 import (ENGINE_LANES, ENGINE_SINGLE, DeviceGraph, Tun
                                    harness as H, k_hop_count_device)
 
 
+def lc_extra(g, stream):
+    import ctypes as C
+    from paper_1905_01294_b200 import _lib
+    return None
+
+
 def timeit(g, seeds_np, k, engine, reps=5):
     s = torch.cuda.current_stream()
     d_seeds = torch.from_numpy(seeds_np.astype(np.int32)).cuda()
@@ -45,7 +51,7 @@ def main():
         for k in (1, 2, 3):
             ms, st, c = timeit(g, master[:300], k, ENGINE_SINGLE)
             print(json.dumps({"cfg": "cfg2", "engine": "single", "k": k, "ms": ms, "qps": 300 / ms * 1e3,
-                              "sum": int(c.sum()),
+                              "sum": int(c.sum()), "setup_us": st["setup_us"], "cleanup_us": st["cleanup_us"],
                               "hops": [(L["runs"], L["pull_runs"], L["frontier"], L["scanned"], L["candidates"],
                                         round(L["ns"] / 1e3, 1)) for L in st["levels"][1:]]}), flush=True)
         for W in (1, 2, 4, 8):
