@@ -90,6 +90,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->fr_V);
     cudaFree(ws->fr_Fb);
     for (auto* p : ws->fr_items) cudaFree(p);
+    for (auto* p : ws->fr_big) cudaFree(p);
     cudaFree(ws->fr_log);
     cudaFree(ws->fr_cnt);
     cudaFree(ws->fr_mfs);

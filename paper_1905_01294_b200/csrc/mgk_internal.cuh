@@ -71,6 +71,8 @@ struct Workspace {
     uint32_t* fr_Fb = nullptr;  // [3][S][nwords]
     uint2* fr_items[2] = {nullptr, nullptr};
     uint32_t fr_items_cap = 0;
+    uint2* fr_big[2] = {nullptr, nullptr};
+    uint32_t fr_big_cap = 0;
     unsigned long long* fr_log = nullptr;
     uint32_t fr_log_cap = 0, fr_quota = 0;
     uint32_t* fr_cnt = nullptr;

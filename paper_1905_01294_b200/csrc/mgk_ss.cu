@@ -21,6 +21,8 @@
 // thousands of warps; the items of ALL in-flight seeds form one global list and
 // each warp takes 1..32 items per step (fewer when the list is short, so a
 // small hop still occupies every warp of the grid). The last hop only counts.
+#include <cstdlib>
+
 #include "mgk_device.cuh"
 
 namespace mgk {
@@ -32,12 +34,14 @@ constexpr int kBlock = 512;
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
 constexpr int kIlp = 4;
+constexpr uint32_t kBigChunk = 1024;  // rows longer than this become 1024-entry big items
 constexpr uint32_t kMaxSlots = 512;
 constexpr unsigned long long kOverflowBit = 1ULL << 62;
 enum : uint8_t { kPush = 0, kPull = 1, kDead = 2 };
 
 struct FRCtl {
     unsigned int nitems[3];  // items for hop h: buffer h & 1, count nitems[h % 3]
+    unsigned int nbig[3];    // big items (1024-entry slices of rows longer than 1024)
     unsigned int log_n;
     unsigned int log_overflow;
     unsigned int pad;
@@ -45,15 +49,17 @@ struct FRCtl {
     unsigned long long last_which;  // frontier bitmap id of the final hop (frontier ids)
     unsigned int done;              // CTAs finished with the cleanup (last one answers)
     unsigned long long t_clean;     // cleanup start (%globaltimer), for the stats
+    unsigned long long t_last;      // start of the last hop expanded (its end = fr_finish start)
+    unsigned int last_hop;          // last hop expanded by fr_kernel
 };
 
 struct FRParams {
     DevGraph g;
-    const uint32_t* seeds;
-    uint64_t nseeds;
+    const uint32_t* seeds;  // this group's seeds (ns of them)
+    uint32_t ns;
     uint32_t k;
     int mode;
-    unsigned long long* counts;
+    unsigned long long* counts;  // this group's answers
     uint32_t S;
     uint32_t rs;   // bitmap row stride in words (nwords rounded up to 32: 128-B rows)
     uint32_t* V;   // [S][rs]
@@ -61,6 +67,9 @@ struct FRParams {
     uint2* items0;
     uint2* items1;
     uint32_t items_cap;
+    uint2* big0;  // {begin, slot << 10 | (len - 1)}, len <= kBigChunk
+    uint2* big1;
+    uint32_t big_cap;
     unsigned long long* logbuf;
     uint32_t log_cap;
     uint32_t* cnt;             // [(k+1)][S] discoveries per hop per seed
@@ -135,6 +144,75 @@ __device__ __forceinline__ void slot_commit(const FRParams& P, uint32_t hop, boo
     }
 }
 
+// Warp-wide: push work items for the next hop (hop + 1) for each lane's row
+// (b, deg) of seed `slot`. Rows up to kBigChunk entries become <= 32-entry
+// items (each warp step of the next hop merges up to 32 of them); longer rows
+// become kBigChunk-entry big items (one warp step each), so one warp never
+// writes more than ~32 items per discovered vertex.
+__device__ void emit_row_items(const FRParams& P, uint32_t hop, bool valid, uint32_t slot,
+                               uint32_t b, uint32_t deg) {
+    const uint32_t lane = lane_id();
+    const bool big = valid && deg > kBigChunk;
+    const uint32_t par = (hop + 1) & 1, cidx = (hop + 1) % 3;
+    // small items
+    {
+        const uint32_t nit = (valid && !big) ? (deg + kChunk - 1) / kChunk : 0;
+        const uint32_t incl = warp_incl_scan(nit);
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        if (total) {
+            uint32_t base = 0;
+            if (lane == 31) base = atomicAdd(&P.ctl->nitems[cidx], total);
+            base = __shfl_sync(kFull, base, 31);
+            if ((uint64_t)base + total > P.items_cap) {
+                // out of item space: these seeds pull next hop (pull needs no items)
+                if (nit) atomicOr(&P.mfs[hop * P.S + slot], kOverflowBit);
+            } else {
+                uint2* items = par ? P.items1 : P.items0;
+                const uint32_t excl = incl - nit;
+                for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+                    const uint32_t x = x0 + lane;
+                    const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
+                    const uint32_t bj = __shfl_sync(kFull, b, j);
+                    const uint32_t dj = __shfl_sync(kFull, deg, j);
+                    const uint32_t ej = __shfl_sync(kFull, excl, j);
+                    const uint32_t sj = __shfl_sync(kFull, slot, j);
+                    if (x < total) {
+                        const uint32_t s = bj + (x - ej) * kChunk;
+                        items[base + x] = make_uint2(s, (sj << 5) | (min(kChunk, bj + dj - s) - 1));
+                    }
+                }
+            }
+        }
+    }
+    // big items
+    const unsigned bigmask = __ballot_sync(kFull, big);
+    if (!bigmask) return;
+    const uint32_t nbg = big ? (deg + kBigChunk - 1) / kBigChunk : 0;
+    const uint32_t incl = warp_incl_scan(nbg);
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(&P.ctl->nbig[cidx], total);
+    base = __shfl_sync(kFull, base, 31);
+    if ((uint64_t)base + total > P.big_cap) {
+        if (nbg) atomicOr(&P.mfs[hop * P.S + slot], kOverflowBit);
+        return;
+    }
+    uint2* bigs = par ? P.big1 : P.big0;
+    const uint32_t excl = incl - nbg;
+    for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+        const uint32_t x = x0 + lane;
+        const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
+        const uint32_t bj = __shfl_sync(kFull, b, j);
+        const uint32_t dj = __shfl_sync(kFull, deg, j);
+        const uint32_t ej = __shfl_sync(kFull, excl, j);
+        const uint32_t sj = __shfl_sync(kFull, slot, j);
+        if (x < total) {
+            const uint32_t s = bj + (x - ej) * kBigChunk;
+            bigs[base + x] = make_uint2(s, (sj << 10) | (min(kBigChunk, bj + dj - s) - 1));
+        }
+    }
+}
+
 // Warp-wide emission of n staged (slot << 32 | u) discoveries of `hop`:
 // per-seed counters, the cleanup log, and (unless this is the last hop) the
 // next hop's push items. Discoveries before the last hop are always logged
@@ -145,8 +223,6 @@ __device__ void emit(const FRParams& P, uint32_t hop, bool last, const uint8_t* 
     if (n == 0) return;
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    unsigned int* nitems = &P.ctl->nitems[(hop + 1) % 3];
-    uint2* items = ((hop + 1) & 1) ? P.items1 : P.items0;
     // one log reservation for the whole stage
     uint32_t nlog = 0;
     for (uint32_t i = lane; i < n; i += 32)
@@ -184,32 +260,7 @@ __device__ void emit(const FRParams& P, uint32_t hop, bool last, const uint8_t* 
         }
         log_base += __popc(lm);
         if (last) continue;
-        const uint32_t nit = (deg + kChunk - 1) / kChunk;
-        const uint32_t incl = warp_incl_scan(nit);
-        const uint32_t total = __shfl_sync(kFull, incl, 31);
-        if (total == 0) continue;
-        uint32_t base = 0;
-        if (lane == 31) base = atomicAdd(nitems, total);
-        base = __shfl_sync(kFull, base, 31);
-        if ((uint64_t)base + total > P.items_cap) {
-            // out of item space: these seeds pull next hop (pull needs no items)
-            if (valid && deg) atomicOr(&P.mfs[hop * P.S + slot], kOverflowBit);
-            continue;
-        }
-        const uint32_t excl = incl - nit;
-        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
-            const uint32_t x = x0 + lane;
-            const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
-            const uint32_t bj = __shfl_sync(kFull, b, j);
-            const uint32_t dj = __shfl_sync(kFull, deg, j);
-            const uint32_t ej = __shfl_sync(kFull, excl, j);
-            const uint32_t sj = __shfl_sync(kFull, slot, j);
-            if (x < total) {
-                const uint32_t s = bj + (x - ej) * kChunk;
-                const uint32_t len = min(kChunk, bj + dj - s);
-                items[base + x] = make_uint2(s, (sj << 5) | (len - 1));
-            }
-        }
+        emit_row_items(P, hop, valid, slot, b, deg);
     }
     __syncwarp();
 }
@@ -225,36 +276,79 @@ __device__ __forceinline__ void stage_push(const FRParams& P, uint32_t hop, bool
     }
 }
 
+// Visit kIlp adjacency entries per lane (targets u of seeds sj): test-and-set
+// the seed's visited bit; new vertices go to the frontier bitmap and the stage.
+__device__ __forceinline__ void visit_edges(const FRParams& P, uint32_t hop, bool last,
+                                            const uint8_t* s_logok,
+                                            Stage<kStageCap, unsigned long long>& st, Acc& acc,
+                                            const uint32_t (&u)[kIlp], const uint32_t (&sj)[kIlp],
+                                            const bool (&valid)[kIlp]) {
+    const uint32_t fn = hop % 3;
+    const bool set_fb = !last || P.keep_result;
+    uint32_t old[kIlp];
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+        old[r] = kFull;
+        if (valid[r]) {
+            uint32_t* vw = P.V + (size_t)sj[r] * P.rs + (u[r] >> 5);
+            const uint32_t bit = 1u << (u[r] & 31);
+            // a seed's last hop that is not logged only sets bits
+            // (fire-and-forget red.or); it is counted afterwards by a
+            // popcount of the bitmap in the clearing pass
+            if (last && !s_logok[sj[r]]) atomicOr(vw, bit);
+            else old[r] = atomicOr(vw, bit);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kIlp; ++r) {
+        const bool found = !((old[r] >> (u[r] & 31)) & 1u);
+        if (found && set_fb)
+            atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * P.rs + (u[r] >> 5), 1u << (u[r] & 31));
+        acc.scanned += valid[r];
+        acc.found += found;
+        stage_push(P, hop, last, s_logok, st, found, sj[r], u[r]);
+    }
+}
+
 // Push: expand the work items of seeds in push mode.
 __device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uint8_t* s_dir,
                            const uint8_t* s_logok, Stage<kStageCap, unsigned long long>& st,
                            Acc& acc, uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    const uint32_t nw = g.nwords;
-    const uint32_t nitems = min(ld_volatile(&P.ctl->nitems[hop % 3]), P.items_cap);
+    const uint32_t nsmall = min(ld_volatile(&P.ctl->nitems[hop % 3]), P.items_cap);
+    const uint32_t nbig = min(ld_volatile(&P.ctl->nbig[hop % 3]), P.big_cap);
     const uint2* items = (hop & 1) ? P.items1 : P.items0;
-    const uint32_t fn = hop % 3;
-    const bool set_fb = !last || P.keep_result;
+    const uint2* bigs = (hop & 1) ? P.big1 : P.big0;
+    // a big item (<= 1024 entries) is consumed as 32 virtual <= 32-entry items
+    const uint32_t nitems = nsmall + nbig * 32;
     // ~8 steps per warp at least, so the tail of the hop stays balanced
     const uint32_t G = items_per_warp(nitems, (uint64_t)nwarps * 8);
     for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
         const uint32_t idx = base + lane;
         uint32_t len = 0, slot = 0, beg = 0;
         if (lane < G && idx < nitems) {
-            const uint2 it = items[idx];
-            slot = it.y >> 5;
-            if (s_dir[slot] == kPush) {
+            if (idx < nsmall) {
+                const uint2 it = items[idx];
+                slot = it.y >> 5;
                 len = (it.y & 31) + 1;
                 beg = it.x;
+            } else {
+                const uint32_t v = idx - nsmall, sub = (v & 31) * kChunk;
+                const uint2 it = bigs[v >> 5];
+                slot = it.y >> 10;
+                const uint32_t blen = (it.y & 1023) + 1;
+                len = sub < blen ? min(kChunk, blen - sub) : 0;
+                beg = it.x + sub;
             }
+            if (s_dir[slot] != kPush) len = 0;
         }
         const uint32_t incl = warp_incl_scan(len);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         const uint32_t off = beg - (incl - len);
         // kIlp edges per lane per step: all loads / atomics of a step in flight together
         for (uint32_t x0 = 0; x0 < total; x0 += 32 * kIlp) {
-            uint32_t u[kIlp], sj[kIlp], old[kIlp];
+            uint32_t u[kIlp], sj[kIlp];
             bool valid[kIlp];
 #pragma unroll
             for (int r = 0; r < kIlp; ++r) {
@@ -265,28 +359,7 @@ __device__ void push_phase(const FRParams& P, uint32_t hop, bool last, const uin
                 sj[r] = __shfl_sync(kFull, slot, j);
                 u[r] = valid[r] ? __ldcs(g.ci + pos) : 0;  // streamed: keep bitmaps in L2
             }
-#pragma unroll
-            for (int r = 0; r < kIlp; ++r) {
-                old[r] = kFull;
-                if (valid[r]) {
-                    uint32_t* vw = P.V + (size_t)sj[r] * P.rs + (u[r] >> 5);
-                    const uint32_t bit = 1u << (u[r] & 31);
-                    // a seed's last hop that is not logged only sets bits
-                    // (fire-and-forget red.or); it is counted afterwards by a
-                    // popcount of the bitmap in the clearing pass
-                    if (last && !s_logok[sj[r]]) atomicOr(vw, bit);
-                    else old[r] = atomicOr(vw, bit);
-                }
-            }
-#pragma unroll
-            for (int r = 0; r < kIlp; ++r) {
-                const bool found = !((old[r] >> (u[r] & 31)) & 1u);
-                if (found && set_fb)
-                    atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * P.rs + (u[r] >> 5), 1u << (u[r] & 31));
-                acc.scanned += valid[r];
-                acc.found += found;
-                stage_push(P, hop, last, s_logok, st, found, sj[r], u[r]);
-            }
+            visit_edges(P, hop, last, s_logok, st, acc, u, sj, valid);
         }
     }
 }
@@ -400,7 +473,6 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     Acc acc;
     acc.zero();
     Stage<kStageCap, unsigned long long> st{s_stage[wib], 0};
-    const uint64_t ngroups = (P.nseeds + S - 1) / S;
 
     // block-wide ordered compaction of slots satisfying pred into s_list
     auto compact = [&](bool pred) {
@@ -417,208 +489,239 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
         __syncthreads();
     };
 
-    for (uint64_t grp = 0; grp < ngroups; ++grp) {
-        const uint32_t ns = (uint32_t)min((uint64_t)S, P.nseeds - grp * S);
-        unsigned long long t_init = 0;
-        if (gtid == 0) t_init = globaltimer();
-        // ---- seeds (hop 0): one warp per seed; counters are zero on entry --------------
-        for (uint32_t slot = warp_gid; slot < ns; slot += nwarps) {
-            const uint32_t s = P.seeds[grp * S + slot];
-            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
-            if (lane == 0) {
-                const uint32_t bit = 1u << (s & 31);
-                P.V[(size_t)slot * P.rs + (s >> 5)] = bit;
-                P.Fb[(size_t)slot * P.rs + (s >> 5)] = bit;
-                P.cnt[slot] = 1;
-                P.mfs[slot] = deg;
-                P.mex[slot] = __ldg(g.cp + s + 1) - __ldg(g.cp + s);
-                P.logbuf[slot] = ((unsigned long long)slot << 32) | s;  // log slots [0, ns)
-            }
-            const uint32_t nit = (deg + kChunk - 1) / kChunk;
-            uint32_t base = 0;
-            if (lane == 0 && nit) base = atomicAdd(&P.ctl->nitems[1], nit);
-            base = __shfl_sync(kFull, base, 0);
-            if (base + nit <= P.items_cap) {
-                for (uint32_t x = lane; x < nit; x += 32) {
-                    const uint32_t st0 = b + x * kChunk;
-                    P.items1[base + x] = make_uint2(st0, (slot << 5) | (min(kChunk, b + deg - st0) - 1));
+    const uint32_t ns = P.ns;
+    unsigned long long t_init = 0;
+    if (gtid == 0) t_init = globaltimer();
+    // ---- seeds (hop 0): one warp per seed; counters are zero on entry --------------
+    for (uint32_t slot = warp_gid; slot < ns; slot += nwarps) {
+        const uint32_t s = P.seeds[slot];
+        const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
+        if (lane == 0) {
+            const uint32_t bit = 1u << (s & 31);
+            P.V[(size_t)slot * P.rs + (s >> 5)] = bit;
+            P.Fb[(size_t)slot * P.rs + (s >> 5)] = bit;
+            P.cnt[slot] = 1;
+            P.mfs[slot] = deg;
+            P.mex[slot] = __ldg(g.cp + s + 1) - __ldg(g.cp + s);
+            P.logbuf[slot] = ((unsigned long long)slot << 32) | s;  // log slots [0, ns)
+        }
+        emit_row_items(P, 0, lane == 0, slot, b, deg);
+    }
+    if (gtid == 0) {
+        P.ctl->found[0] = ns;
+        atomicAdd(&P.ctl->log_n, ns);
+    }
+    grid_barrier(P.bar);
+    if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds
+
+    uint32_t hop = 1;
+    for (; hop <= P.k; ++hop) {
+        const bool last = hop == P.k;
+        // ---- plan: per-seed direction (every block computes the same) ------------
+        bool pull_me = false;
+        if (threadIdx.x < kMaxSlots) {
+            uint8_t d = kDead;
+            const uint32_t slot = threadIdx.x;
+            if (slot < ns) {
+                const unsigned long long nf = P.cnt[(hop - 1) * S + slot];
+                const unsigned long long mf = P.mfs[(hop - 1) * S + slot];
+                const unsigned long long mu = g.m - P.mex[slot];
+                const uint8_t prev = P.dirs[((hop - 1) & 1) * S + slot];
+                if (nf == 0) {
+                    d = kDead;
+                } else if (P.force_dir == 1) {
+                    d = kPush;
+                } else if (P.force_dir == 2 || (mf & kOverflowBit)) {
+                    d = kPull;
+                } else if (prev == kPush) {
+                    d = mf * P.alpha > mu ? kPull : kPush;
+                } else {
+                    d = nf * P.beta >= g.n ? kPull : kPush;
                 }
-            } else if (lane == 0) {
-                atomicOr(&P.mfs[slot], kOverflowBit);
+                if (blockIdx.x == 0) {
+                    P.dirs[(hop & 1) * S + slot] = d == kDead ? prev : d;
+                    if (d != kDead) {
+                        atomicAdd(&P.lc[hop].runs, 1u);
+                        if (d == kPull) atomicAdd(&P.lc[hop].pull_runs, 1u);
+                        atomicAdd(&P.lc[hop].edges, mf & ~kOverflowBit);
+                        atomicAdd(&P.lc[hop].union_edges, mf & ~kOverflowBit);
+                    }
+                }
+            }
+            s_dir[slot] = d;
+            pull_me = d == kPull;
+            // last hop: log the discoveries only if they are bounded by the
+            // quota (mf = out-edges of the frontier); otherwise the seed's
+            // visited bitmap is cleared densely afterwards
+            if (last) {
+                const bool logok = slot < ns && (P.keep_result ||
+                                                 P.mfs[(hop - 1) * S + slot] <= P.quota);
+                s_flag[slot] = logok;
+                if (blockIdx.x == 0 && slot < ns && d != kDead && !logok) P.logcnt[slot] = 1;
             }
         }
-        if (gtid == 0) {
-            P.ctl->found[0] = ns;
-            atomicAdd(&P.ctl->log_n, ns);
+        compact(pull_me);
+        const uint32_t npull = s_nlist;
+        if (gtid == 0) P.ctl->nitems[(hop + 2) % 3] = P.ctl->nbig[(hop + 2) % 3] = 0;
+        unsigned long long t0 = 0;
+        if (gtid == 0) t0 = globaltimer();
+        // Frontier bitmaps rotate over 3 buffers and are only cleared at the end:
+        // stale bits of F_{h-3} are harmless to pull (an unvisited vertex at hop
+        // h has no in-neighbour at distance <= h-2), but k_hop_frontier reads
+        // F_k back, so in that mode the buffer of F_{h-2} is cleared here
+        // (hop h reads F_{h-1}, writes F_h; the next write is after a barrier).
+        if (P.keep_result)
+            for (uint32_t w = gtid; w < nw; w += nthreads)
+                P.Fb[(size_t)((hop + 1) % 3) * S * P.rs + w] = 0;
+        // ---- expand -----------------------------------------------------------------
+        push_phase(P, hop, last, s_dir, s_flag, st, acc, warp_gid, nwarps);
+        if (npull) pull_phase(P, hop, last, s_list, npull, s_flag, st, acc, warp_gid, nwarps);
+        emit(P, hop, last, s_flag, st.buf, st.n);
+        st.n = 0;
+        block_flush(acc, &P.ctl->found[hop], &P.lc[hop]);
+        if (last) {  // the kernel boundary orders the last hop before fr_finish
+            if (gtid == 0) P.ctl->t_last = t0;
+            ++hop;  // all k hops completed
+            break;
         }
         grid_barrier(P.bar);
-        if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds
+        if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
+        if (ld_volatile(&P.ctl->found[hop]) == 0) break;
+    }
+    if (gtid == 0) {
+        P.ctl->last_hop = hop > P.k ? P.k : hop;
+        P.ctl->last_which = (hop > P.k) ? (P.k % 3) : 3ULL;
+    }
+}
 
-        uint32_t hop = 1;
-        for (; hop <= P.k; ++hop) {
-            const bool last = hop == P.k;
-            // ---- plan: per-seed direction (every block computes the same) ------------
-            bool pull_me = false;
-            if (threadIdx.x < kMaxSlots) {
-                uint8_t d = kDead;
-                const uint32_t slot = threadIdx.x;
-                if (slot < ns) {
-                    const unsigned long long nf = P.cnt[(hop - 1) * S + slot];
-                    const unsigned long long mf = P.mfs[(hop - 1) * S + slot];
-                    const unsigned long long mu = g.m - P.mex[slot];
-                    const uint8_t prev = P.dirs[((hop - 1) & 1) * S + slot];
-                    if (nf == 0) {
-                        d = kDead;
-                    } else if (P.force_dir == 1) {
-                        d = kPush;
-                    } else if (P.force_dir == 2 || (mf & kOverflowBit)) {
-                        d = kPull;
-                    } else if (prev == kPush) {
-                        d = mf * P.alpha > mu ? kPull : kPush;
-                    } else {
-                        d = nf * P.beta >= g.n ? kPull : kPush;
-                    }
-                    if (blockIdx.x == 0) {
-                        P.dirs[(hop & 1) * S + slot] = d == kDead ? prev : d;
-                        if (d != kDead) {
-                            atomicAdd(&P.lc[hop].runs, 1u);
-                            if (d == kPull) atomicAdd(&P.lc[hop].pull_runs, 1u);
-                            atomicAdd(&P.lc[hop].edges, mf & ~kOverflowBit);
-                            atomicAdd(&P.lc[hop].union_edges, mf & ~kOverflowBit);
-                        }
-                    }
-                }
-                s_dir[slot] = d;
-                pull_me = d == kPull;
-                // last hop: log the discoveries only if they are bounded by the
-                // quota (mf = out-edges of the frontier); otherwise the seed's
-                // visited bitmap is cleared densely afterwards
-                if (last) {
-                    const bool logok = slot < ns && (P.keep_result ||
-                                                     P.mfs[(hop - 1) * S + slot] <= P.quota);
-                    s_flag[slot] = logok;
-                    if (blockIdx.x == 0 && slot < ns && d != kDead && !logok) P.logcnt[slot] = 1;
-                }
-            }
-            compact(pull_me);
-            const uint32_t npull = s_nlist;
-            if (gtid == 0) P.ctl->nitems[(hop + 2) % 3] = 0;
-            unsigned long long t0 = 0;
-            if (gtid == 0) t0 = globaltimer();
-            // ---- expand -----------------------------------------------------------------
-            push_phase(P, hop, last, s_dir, s_flag, st, acc, warp_gid, nwarps);
-            if (npull) pull_phase(P, hop, last, s_list, npull, s_flag, st, acc, warp_gid, nwarps);
-            emit(P, hop, last, s_flag, st.buf, st.n);
-            st.n = 0;
-            block_flush(acc, &P.ctl->found[hop], &P.lc[hop]);
-            grid_barrier(P.bar);
-            if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
-            if (ld_volatile(&P.ctl->found[hop]) == 0) break;
-        }
-        if (gtid == 0) P.ctl->last_which = (hop > P.k) ? (P.k % 3) : 3ULL;
-        // ---- cleanup: state back to all-zero -------------------------------------------------
-        // Every discovery before the last hop is in the log (it may also have a
-        // frontier bit); last-hop discoveries are logged unless the seed was
-        // flagged (logcnt[slot] = 1): its last hop only set bits, so its answer
-        // is a popcount of its visited bitmap, taken while clearing it densely.
-        // A log overflow clears everything densely.
-        if (gtid == 0) P.ctl->t_clean = globaltimer();
-        const bool overflow = ld_volatile(&P.ctl->log_overflow) != 0;
-        const uint32_t nlog = min(ld_volatile(&P.ctl->log_n), P.log_cap);
-        bool dense_me = false;
-        if (threadIdx.x < kMaxSlots) {
-            const bool pop_me = threadIdx.x < ns && P.logcnt[threadIdx.x] != 0;
-            dense_me = threadIdx.x < ns && (overflow || pop_me);
-            s_flag[threadIdx.x] = pop_me ? 2 : (dense_me ? 1 : 0);
-        }
-        compact(dense_me);
-        const uint32_t ndense = s_nlist;
-        if (!P.keep_result) {
-            if (!overflow) {
-                for (uint32_t i = gtid; i < nlog; i += nthreads) {
-                    const unsigned long long e = P.logbuf[i];
-                    const uint32_t slot = (uint32_t)(e >> 32) & 0x7FFFFFFFu, w = (uint32_t)e >> 5;
-                    if (!s_flag[slot]) P.V[(size_t)slot * P.rs + w] = 0;
-                    if (!(e >> 63))
-                        for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * P.rs + w] = 0;
-                }
-            }
-            // dense pass: (slot, 8192-word chunk) tasks; each thread keeps four
-            // aligned uint4 loads in flight (rows are padded to 128 B, padding
-            // words are always zero)
-            constexpr uint32_t kDenseChunk = 4 * 4 * kBlock;
-            const uint32_t chunks = (P.rs + kDenseChunk - 1) / kDenseChunk;
-            for (uint32_t t = blockIdx.x; t < ndense * chunks; t += gridDim.x) {
-                const uint32_t slot = s_list[t / chunks];
-                const uint32_t base = (t % chunks) * kDenseChunk + threadIdx.x * 4;
-                uint4* row = reinterpret_cast<uint4*>(P.V + (size_t)slot * P.rs);
-                uint4 v[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t w = base + i * 4 * kBlock;
-                    v[i] = w < P.rs ? __ldcs(row + w / 4) : make_uint4(0, 0, 0, 0);
-                }
-                uint32_t pc = 0;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint32_t w = base + i * 4 * kBlock;
-                    pc += __popc(v[i].x) + __popc(v[i].y) + __popc(v[i].z) + __popc(v[i].w);
-                    if (w < P.rs) {
-                        __stcs(row + w / 4, make_uint4(0, 0, 0, 0));
-                        if (overflow)
-                            for (int f = 0; f < 3; ++f)
-                                __stcs(reinterpret_cast<uint4*>(P.Fb + ((size_t)f * S + slot) * P.rs + w),
-                                       make_uint4(0, 0, 0, 0));
-                    }
-                }
-                if (s_flag[slot] == 2) {
-#pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
-                    if (lane == 0 && pc) atomicAdd(&P.pop[slot], (unsigned long long)pc);
-                }
-            }
-        }
-        // ---- answers (by the last CTA to finish cleaning); leave every counter zero ----------
-        __shared__ bool s_last;
+// Second launch of a group: return the workspace to all-zero and write the
+// answers. Every discovery before the last hop is in the log (it may also have
+// a frontier bit); last-hop discoveries are logged unless the seed was flagged
+// (logcnt[slot] = 1): its last hop only set bits, so its answer is a popcount
+// of its visited bitmap, taken while clearing it densely. A log overflow
+// clears everything densely. The last CTA to finish writes the answers and
+// re-zeroes the per-seed counters and the control block.
+constexpr int kFinBlock = 512;
+__global__ void __launch_bounds__(kFinBlock) fr_finish(FRParams P) {
+    __shared__ uint8_t s_flag[kMaxSlots];
+    __shared__ uint16_t s_list[kMaxSlots];
+    __shared__ uint32_t s_wcount[kFinBlock / 32];
+    __shared__ uint32_t s_nlist;
+    __shared__ bool s_last;
+    const uint32_t gtid = blockIdx.x * kFinBlock + threadIdx.x;
+    const uint32_t nthreads = gridDim.x * kFinBlock;
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+    const uint32_t S = P.S, ns = P.ns;
+    if (gtid == 0) {
+        const unsigned long long now = globaltimer();
+        P.ctl->t_clean = now;
+        const uint32_t lh = P.ctl->last_hop;
+        if (lh == P.k) atomicAdd(&P.lc[lh].ns, now - P.ctl->t_last);
+    }
+    const bool overflow = ld_volatile(&P.ctl->log_overflow) != 0;
+    const uint32_t nlog = min(ld_volatile(&P.ctl->log_n), P.log_cap);
+    bool dense_me = false;
+    if (threadIdx.x < kMaxSlots) {
+        const bool pop_me = threadIdx.x < ns && P.logcnt[threadIdx.x] != 0;
+        dense_me = threadIdx.x < ns && (overflow || pop_me);
+        s_flag[threadIdx.x] = pop_me ? 2 : (dense_me ? 1 : 0);
+    }
+    {
+        const unsigned m = __ballot_sync(kFull, dense_me);
+        if (lane == 0) s_wcount[wib] = __popc(m);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            s_last = atomicAdd(&P.ctl->done, 1u) == gridDim.x - 1;
+        uint32_t off = 0, tot = 0;
+        for (uint32_t i = 0; i < kFinBlock / 32; ++i) {
+            if (i < wib) off += s_wcount[i];
+            tot += s_wcount[i];
         }
+        if (dense_me) s_list[off + __popc(m & lanemask_lt())] = (uint16_t)threadIdx.x;
+        if (threadIdx.x == 0) s_nlist = tot;
         __syncthreads();
-        if (s_last) {
-            __threadfence();
-            for (uint32_t slot = threadIdx.x; slot < ns; slot += kBlock) {
-                unsigned long long before = 0;  // vertices visited before the last hop (seed incl.)
-                for (uint32_t h = 0; h < P.k; ++h) before += ld_cg(&P.cnt[h * S + slot]);
-                const unsigned long long lastc = ld_cg(&P.cnt[P.k * S + slot]);
-                unsigned long long r;
-                if (ld_cg(&P.logcnt[slot]) != 0) {
-                    const unsigned long long total = ld_cg(&P.pop[slot]);
-                    r = P.mode == MGK_CUMULATIVE ? total - 1 : total - before;
-                } else {
-                    r = P.mode == MGK_CUMULATIVE ? before - 1 + lastc : lastc;
-                }
-                P.counts[grp * S + slot] = r;
-                for (uint32_t h = 0; h <= P.k; ++h) {
-                    P.cnt[h * S + slot] = 0;
-                    P.mfs[h * S + slot] = 0;
-                }
-                P.logcnt[slot] = 0;
-                P.pop[slot] = 0;
-                P.mex[slot] = 0;
-                P.dirs[slot] = P.dirs[S + slot] = kPush;
-            }
-            if (threadIdx.x == 0) {
-                P.ctl->nitems[0] = P.ctl->nitems[1] = P.ctl->nitems[2] = 0;
-                P.ctl->log_n = 0;
-                P.ctl->log_overflow = 0;
-                for (uint32_t h = 0; h <= P.k; ++h) P.ctl->found[h] = 0;
-                P.ctl->done = 0;
-                atomicAdd(&P.lc[MGK_MAX_HOPS + 1].ns, globaltimer() - ld_cg(&P.ctl->t_clean));
+    }
+    const uint32_t ndense = s_nlist;
+    if (!P.keep_result) {
+        if (!overflow) {
+            for (uint32_t i = gtid; i < nlog; i += nthreads) {
+                const unsigned long long e = P.logbuf[i];
+                const uint32_t slot = (uint32_t)(e >> 32) & 0x7FFFFFFFu, w = (uint32_t)e >> 5;
+                if (!s_flag[slot]) P.V[(size_t)slot * P.rs + w] = 0;
+                if (!(e >> 63))
+                    for (int f = 0; f < 3; ++f) P.Fb[((size_t)f * S + slot) * P.rs + w] = 0;
             }
         }
-        if (grp + 1 < ngroups) grid_barrier(P.bar);
+        // dense pass: (slot, 8192-word chunk) tasks; each thread keeps four
+        // aligned uint4 loads in flight (rows are padded to 128 B, padding
+        // words are always zero)
+        constexpr uint32_t kDenseChunk = 4 * 4 * kFinBlock;
+        const uint32_t chunks = (P.rs + kDenseChunk - 1) / kDenseChunk;
+        for (uint32_t t = blockIdx.x; t < ndense * chunks; t += gridDim.x) {
+            const uint32_t slot = s_list[t / chunks];
+            const uint32_t base = (t % chunks) * kDenseChunk + threadIdx.x * 4;
+            uint4* row = reinterpret_cast<uint4*>(P.V + (size_t)slot * P.rs);
+            uint4 v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t w = base + i * 4 * kFinBlock;
+                v[i] = w < P.rs ? __ldcs(row + w / 4) : make_uint4(0, 0, 0, 0);
+            }
+            uint32_t pc = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t w = base + i * 4 * kFinBlock;
+                pc += __popc(v[i].x) + __popc(v[i].y) + __popc(v[i].z) + __popc(v[i].w);
+                if (w < P.rs) {
+                    __stcs(row + w / 4, make_uint4(0, 0, 0, 0));
+                    if (overflow)
+                        for (int f = 0; f < 3; ++f)
+                            __stcs(reinterpret_cast<uint4*>(P.Fb + ((size_t)f * S + slot) * P.rs + w),
+                                   make_uint4(0, 0, 0, 0));
+                }
+            }
+            if (s_flag[slot] == 2) {
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
+                if (lane == 0 && pc) atomicAdd(&P.pop[slot], (unsigned long long)pc);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&P.ctl->done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (uint32_t slot = threadIdx.x; slot < ns; slot += kFinBlock) {
+        unsigned long long before = 0;  // vertices visited before the last hop (seed incl.)
+        for (uint32_t h = 0; h < P.k; ++h) before += ld_cg(&P.cnt[h * S + slot]);
+        const unsigned long long lastc = ld_cg(&P.cnt[P.k * S + slot]);
+        unsigned long long r;
+        if (ld_cg(&P.logcnt[slot]) != 0) {
+            const unsigned long long total = ld_cg(&P.pop[slot]);
+            r = P.mode == MGK_CUMULATIVE ? total - 1 : total - before;
+        } else {
+            r = P.mode == MGK_CUMULATIVE ? before - 1 + lastc : lastc;
+        }
+        P.counts[slot] = r;
+        for (uint32_t h = 0; h <= P.k; ++h) {
+            P.cnt[h * S + slot] = 0;
+            P.mfs[h * S + slot] = 0;
+        }
+        P.logcnt[slot] = 0;
+        P.pop[slot] = 0;
+        P.mex[slot] = 0;
+        P.dirs[slot] = P.dirs[S + slot] = kPush;
+    }
+    if (threadIdx.x == 0) {
+        P.ctl->nitems[0] = P.ctl->nitems[1] = P.ctl->nitems[2] = 0;
+        P.ctl->nbig[0] = P.ctl->nbig[1] = P.ctl->nbig[2] = 0;
+        P.ctl->log_n = 0;
+        P.ctl->log_overflow = 0;
+        for (uint32_t h = 0; h <= P.k; ++h) P.ctl->found[h] = 0;
+        P.ctl->done = 0;
+        atomicAdd(&P.lc[MGK_MAX_HOPS + 1].ns, globaltimer() - ld_cg(&P.ctl->t_clean));
     }
 }
 
@@ -676,9 +779,15 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     ws->fr_items_cap = (uint32_t)std::min<uint64_t>(want_items, 64ull << 20);
     for (int i = 0; i < 2; ++i)
         if ((e = cudaMalloc(&ws->fr_items[i], (size_t)ws->fr_items_cap * sizeof(uint2)))) return e;
+    const uint64_t want_big = (uint64_t)S * (g.m / kBigChunk + 64) + 1024;
+    ws->fr_big_cap = (uint32_t)std::min<uint64_t>(want_big, 16ull << 20);
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaMalloc(&ws->fr_big[i], (size_t)ws->fr_big_cap * sizeof(uint2)))) return e;
     // a last hop that can touch more than ~nwords/4 vertices of a seed is not
     // logged; its visited bitmap is cleared with one coalesced pass instead
-    ws->fr_quota = std::max<uint32_t>(64, g.nwords / 4);
+    uint32_t qdiv = 4;
+    if (const char* q = std::getenv("MGK_QUOTA_DIV")) qdiv = std::max(1, std::atoi(q));
+    ws->fr_quota = std::max<uint32_t>(64, g.nwords / qdiv);
     ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * (g.n + 64), 64ull << 20);
     if ((e = cudaMalloc(&ws->fr_log, (size_t)ws->fr_log_cap * 8))) return e;
     const size_t cs = (size_t)(MGK_MAX_HOPS + 1) * S;
@@ -699,6 +808,7 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     if ((e = cudaMemset(ws->fr_dirs, 0, (size_t)2 * S))) return e;
     if ((e = cudaMemset(ws->fr_ctl, 0, sizeof(FRCtl)))) return e;
     ws->fr_slots = S;
+    ws->bytes += 2 * (size_t)ws->fr_big_cap * 8;
     ws->bytes += 4 * bm + 2 * (size_t)ws->fr_items_cap * 8 + (size_t)ws->fr_log_cap * 8 + cs * 12 +
                  (size_t)S * 14 + sizeof(FRCtl);
     return cudaSuccess;
@@ -718,19 +828,24 @@ cudaError_t launch_single(Launch& L) {
             return e;
         if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
     }
+    static int fin_blocks = 0;
+    if (fin_blocks == 0) {
+        int per_sm = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fr_finish, kFinBlock, 0))) return e;
+        fin_blocks = std::max(1, per_sm) * num_sms;
+    }
     FRParams P;
     P.g = gr->dg;
-    P.seeds = L.d_seeds;
-    P.nseeds = L.nseeds;
     P.k = L.k;
     P.mode = L.mode;
-    P.counts = L.d_counts;
-    P.S = (uint32_t)std::min<uint64_t>(ws->fr_slots, L.nseeds);
     P.V = ws->fr_V;
     P.Fb = ws->fr_Fb;
     P.items0 = ws->fr_items[0];
     P.items1 = ws->fr_items[1];
     P.items_cap = ws->fr_items_cap;
+    P.big0 = ws->fr_big[0];
+    P.big1 = ws->fr_big[1];
+    P.big_cap = ws->fr_big_cap;
     P.logbuf = ws->fr_log;
     P.log_cap = ws->fr_log_cap;
     P.cnt = ws->fr_cnt;
@@ -747,14 +862,23 @@ cudaError_t launch_single(Launch& L) {
     P.force_dir = L.tuning.force_dir;
     P.quota = ws->fr_quota;
     P.keep_result = L.keep_result ? 1u : 0u;
-    // Fb is laid out [3][S_alloc][nw]; the kernel indexes it with P.S, so use
-    // the allocated slot count as the stride and cap the group size by it.
+    // bitmaps are laid out [S_alloc][rs] ([3][S_alloc][rs] for Fb): S is the
+    // allocated slot count (the stride); a group holds up to S seeds
     P.S = ws->fr_slots;
     P.rs = row_stride(gr->dg);
     L.grid = (uint32_t)(blocks_per_sm * num_sms);
     L.block = kBlock;
-    void* args[] = {&P};
-    return launch_persistent((const void*)fr_kernel, L.grid, kBlock, args, L.stream);
+    // one group of up to S seeds per (traverse, finish) launch pair
+    for (uint64_t g0 = 0; g0 < L.nseeds; g0 += P.S) {
+        P.ns = (uint32_t)std::min<uint64_t>(P.S, L.nseeds - g0);
+        P.seeds = L.d_seeds + g0;
+        P.counts = L.d_counts + g0;
+        void* args[] = {&P};
+        if ((e = launch_persistent((const void*)fr_kernel, L.grid, kBlock, args, L.stream))) return e;
+        fr_finish<<<fin_blocks, kFinBlock, 0, L.stream>>>(P);
+        if ((e = cudaGetLastError())) return e;
+    }
+    return cudaSuccess;
 }
 
 cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mode, uint32_t seed,

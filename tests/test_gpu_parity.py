@@ -205,3 +205,20 @@ def test_g2_properties(g2):
     assert (k_hop_count_batch(g, seeds[perm], 3, 0) == ex[2][perm]).all()
     single = k_hop_count_batch(g, seeds[:4], 6, 1, engine=ENGINE_SINGLE)
     assert (single == cum6[:4]).all()
+
+
+@pytest.mark.parametrize("force", [0, 1, 2])
+def test_frontier_ids_deep(port, g1, force):
+    """k_hop_frontier's sorted ids (exact and cumulative) at depth, every direction."""
+    rp, ci, g = g1
+    rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
+    try:
+        g.set_tuning(Tuning(force_dir=force))
+        for s in H.pick_seeds(rp, 4, 21):
+            for k in (2, 3, 4, 6):
+                for mode in (0, 1):
+                    want = port.khop_frontier(rp64, ci64, int(s), k, mode)
+                    got = k_hop_frontier(g, KHopQuery(int(s), k, TraverseMode(mode)))
+                    assert np.array_equal(got, want), (int(s), k, mode, force)
+    finally:
+        g.set_tuning(Tuning())
