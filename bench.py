@@ -262,7 +262,7 @@ def run_ours(args):
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{WORKLOAD}_k{dom}")
+            traffic = json.loads(tf.read_text()).get(f"{WORKLOAD}_k{dom}", {}).get("total")
         except Exception:
             traffic = None
     cpu = cpu_baseline(rp, ci, seeds) if (world == 1 and not args.no_cpu) else None
@@ -294,7 +294,7 @@ def run_ours(args):
                                      "us": L["ns"] / 1e3} for L in stats[k]["levels"][1:]]}
                   for k in KS},
         "roofline": {"bound": "hbm", "kernel": (f"ms_kernel<W={stats[dom]['lanes'] // 64}>" if stats[dom]["engine"] == "lanes"
-                                                else "fr_kernel") + f" (k={dom})",
+                                                else "fr_kernel + fr_finish") + f" (k={dom} call)",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "peak_source": pk_src,
                      "algo_bytes_per_launch": ab, "traffic": traffic},
@@ -302,7 +302,7 @@ def run_ours(args):
         "e2e": {"value": q_per_step * args.steps / (e2e_total / 1e3), "unit": "queries/s",
                 "h2d_bytes_per_step": 4 * len(seeds) * len(KS), "d2h_bytes_per_step": 8 * len(seeds) * len(KS),
                 "ms_per_step": e2e_total / args.steps},
-        "gpu_launches": len(KS) * args.steps,
+        "gpu_launches": sum(stats[k]["launches"] for k in KS) * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
@@ -390,8 +390,8 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lanes-words", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

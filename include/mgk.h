@@ -75,6 +75,8 @@ typedef struct mgk_stats {
     uint32_t hops;         /* deepest hop expanded by any run */
     uint32_t grid;         /* persistent CTAs launched */
     uint32_t block;        /* threads per CTA */
+    uint32_t launches;     /* kernel launches the call made */
+    uint32_t pad;
     double kernel_ms;      /* CUDA-event time of the traversal launch(es) */
     uint64_t setup_ns;     /* device time clearing counters + seeding hop 0 */
     uint64_t cleanup_ns;   /* device time returning the workspace to all-zero */

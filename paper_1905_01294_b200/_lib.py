@@ -27,6 +27,7 @@ class MgkLevel(C.Structure):
 class MgkStats(C.Structure):
     _fields_ = [("engine", C.c_uint32), ("lanes", C.c_uint32), ("batches", C.c_uint32),
                 ("hops", C.c_uint32), ("grid", C.c_uint32), ("block", C.c_uint32),
+                ("launches", C.c_uint32), ("pad", C.c_uint32),
                 ("kernel_ms", C.c_double), ("setup_ns", C.c_uint64), ("cleanup_ns", C.c_uint64),
                 ("level", MgkLevel * (MAX_HOPS + 1))]
 
@@ -37,7 +38,8 @@ class MgkStats(C.Structure):
             levels.append({k: getattr(L, k) for k, _ in MgkLevel._fields_})
         return {"engine": {1: "single", 2: "lanes"}.get(self.engine, str(self.engine)),
                 "lanes": self.lanes, "batches": self.batches, "hops": self.hops,
-                "grid": self.grid, "block": self.block, "kernel_ms": self.kernel_ms,
+                "grid": self.grid, "block": self.block, "launches": self.launches,
+                "kernel_ms": self.kernel_ms,
                 "setup_us": self.setup_ns / 1e3, "cleanup_us": self.cleanup_ns / 1e3,
                 "levels": levels}
 

@@ -224,13 +224,17 @@ cudaError_t ensure_staging(Workspace* ws, uint64_t nseeds) {
 }
 
 void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint64_t nseeds,
-                uint32_t grid, uint32_t block, float ms) {
+                uint32_t grid, uint32_t block, float ms, uint32_t slots) {
     std::memset(st, 0, sizeof *st);
     st->engine = (uint32_t)engine;
     st->lanes = engine == MGK_ENGINE_LANES ? 64u * (uint32_t)W : 1u;
     st->batches = (uint32_t)(engine == MGK_ENGINE_LANES ? (nseeds + st->lanes - 1) / st->lanes : nseeds);
     st->grid = grid;
     st->block = block;
+    // SINGLE: a (traverse, finish) launch pair per group of `slots` seeds; LANES: one launch
+    st->launches = nseeds == 0 ? 0
+                   : engine == MGK_ENGINE_LANES ? 1u
+                                                : 2u * (uint32_t)((nseeds + slots - 1) / std::max(1u, slots));
     st->kernel_ms = ms;
     st->setup_ns = lc[0].ns;
     st->cleanup_ns = lc[MGK_MAX_HOPS + 1].ns;
@@ -501,7 +505,7 @@ int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint
             cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
             LevelCounters lc[MGK_MAX_HOPS + 2];
             if ((e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost))) break;
-            fill_stats(stats, lc, used, W, nseeds, grid, block, ms);
+            fill_stats(stats, lc, used, W, nseeds, grid, block, ms, ws->fr_slots);
         }
     } while (0);
     release_ws(g, ws);
@@ -566,7 +570,8 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     LevelCounters lc[MGK_MAX_HOPS + 2];
     cudaError_t e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
     if (e) return fail_cuda(e, "stats");
-    fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f);
+    fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f,
+               ws->fr_slots);
     return MGK_OK;
 }
 
