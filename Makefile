@@ -13,11 +13,28 @@ CPP     := $(CSRC)/mgk_capi.cpp $(CSRC)/mgk_host.cpp
 OBJS    := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU)) $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP))
 HDRS    := include/mgk.h $(CSRC)/mgk_internal.cuh $(CSRC)/mgk_device.cuh
 LIB     := $(PKG)/lib/libmgk.so
+DROPIN  := $(PKG)/lib/libmatgraph_b200.so
+CPPTEST := build/test_dropin
+CXXFLAGS_DROPIN := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude
 
-.PHONY: all lib oracle ref clean
-all: lib oracle
+.PHONY: all lib dropin cpptest oracle ref clean
+all: lib dropin oracle cpptest
 
 lib: $(LIB)
+
+# C++ drop-in (namespace matgraph) over the C ABI; rpath finds libmgk.so beside it
+dropin: $(DROPIN)
+$(DROPIN): $(CSRC)/dropin/matgraph_b200.cpp include/matgraph_b200/khop.hpp include/mgk.h $(LIB)
+	g++ $(CXXFLAGS_DROPIN) -shared -o $@ $< -L$(PKG)/lib -lmgk -Wl,-rpath,'$$ORIGIN'
+
+# the drop-in's C++ tests (linked with the C oracle as the checker)
+cpptest: $(CPPTEST)
+$(CPPTEST): tests/cpp/test_dropin.cpp tests/cpp/mini_test.hpp include/matgraph_b200/khop.hpp $(DROPIN) oracle/khop_oracle.c
+	@mkdir -p build
+	gcc -std=c11 -O2 -fPIC -c -o build/khop_oracle.o oracle/khop_oracle.c
+	g++ $(CXXFLAGS_DROPIN) -Itests/cpp -o $@ tests/cpp/test_dropin.cpp build/khop_oracle.o \
+	    -L$(PKG)/lib -lmatgraph_b200 -lmgk -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)

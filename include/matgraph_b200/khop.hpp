@@ -1,0 +1,237 @@
+// matgraph_b200: the C++ drop-in for the reference's k-hop count path.
+//
+// Signature-compatible with the reference (namespace matgraph) for every
+// symbol on the path, so a caller of
+//   proj/core/include/matgraph/execute.hpp:52-68  (KHopQuery, k_hop_frontier, k_hop_count)
+//   proj/core/include/matgraph/graph.hpp:20-124   (RelationRef, PropertyGraph load API)
+//   proj/core/include/matgraph/bench.hpp:16-156   (RMAT, build_bench_graph, pick_seeds,
+//                                                  summarize, run_khop_benchmark, CSV)
+//   proj/core/include/matgraph/error.hpp:10-66    (Error, ContractError, HarnessError)
+// recompiles against this header unchanged. The traversal runs on a B200
+// through the C ABI of include/mgk.h; the relation matrix is uploaded once per
+// (relation, flush state) and cached like the reference caches its transpose
+// (graph.cpp:90-102). Not on the path (and not provided): labels, property
+// maps, the Cypher executor, the server, snapshots, mxm.
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+struct mgk_graph;
+
+namespace matgraph {
+
+// ---- errors (error.hpp:10-66) ----------------------------------------------------
+class Error : public std::runtime_error {
+public:
+    explicit Error(const std::string& message) : std::runtime_error(message) {}
+};
+class ContractError : public Error {
+    using Error::Error;
+};
+class HarnessError : public Error {
+    using Error::Error;
+};
+
+inline constexpr std::uint32_t kMaxHops = 32;  // ast.hpp:15
+
+enum class TraverseMode : std::uint8_t { Exact, Cumulative };  // plan.hpp:17
+
+// ---- sparse types (sparse.hpp:13-43, 83-134), the subset the path reads -----------
+class BitVector {
+public:
+    BitVector() = default;
+    explicit BitVector(std::uint64_t dimension) : dimension_(dimension) {}
+    static BitVector from_sorted(std::uint64_t dimension, std::vector<std::uint64_t> indices);
+    std::uint64_t dimension() const noexcept { return dimension_; }
+    std::uint64_t nvals() const noexcept { return indices_.size(); }
+    bool empty() const noexcept { return indices_.empty(); }
+    std::span<const std::uint64_t> indices() const noexcept { return indices_; }
+    friend bool operator==(const BitVector&, const BitVector&) = default;
+
+private:
+    std::uint64_t dimension_ = 0;
+    std::vector<std::uint64_t> indices_;
+};
+
+class SparseMatrix {
+public:
+    SparseMatrix() = default;
+    SparseMatrix(std::uint64_t nrows, std::uint64_t ncols)
+        : nrows_(nrows), ncols_(ncols), row_ptr_(nrows + 1, 0) {}
+    static SparseMatrix from_parts(std::uint64_t nrows, std::uint64_t ncols,
+                                   std::vector<std::uint64_t> row_ptr,
+                                   std::vector<std::uint64_t> col_idx);
+    std::uint64_t nrows() const noexcept { return nrows_; }
+    std::uint64_t ncols() const noexcept { return ncols_; }
+    std::uint64_t nvals() const noexcept { return col_idx_.size(); }
+    std::span<const std::uint64_t> row_ptr() const noexcept { return row_ptr_; }
+    std::span<const std::uint64_t> col_idx() const noexcept { return col_idx_; }
+    std::span<const std::uint64_t> row(std::uint64_t r) const;
+
+private:
+    std::uint64_t nrows_ = 0, ncols_ = 0;
+    std::vector<std::uint64_t> row_ptr_ = {0};
+    std::vector<std::uint64_t> col_idx_;
+};
+
+std::uint64_t nvals(const SparseMatrix& m);
+std::uint64_t nvals(const BitVector& v);
+
+// ---- graph store (graph.hpp:20-124), load API + matrix access ---------------------
+struct RelationRef {
+    std::optional<std::string> name;  // nullopt = ANY
+    RelationRef() = default;
+    RelationRef(std::string n) : name(std::move(n)) {}
+    RelationRef(std::string_view n) : name(std::string(n)) {}
+    RelationRef(const char* n) : name(std::string(n)) {}
+    static RelationRef any() { return {}; }
+    bool is_any() const noexcept { return !name.has_value(); }
+    friend bool operator==(const RelationRef&, const RelationRef&) = default;
+};
+
+// A relation matrix resident on one GPU (owning handle of the C ABI graph).
+class DeviceMatrix {
+public:
+    explicit DeviceMatrix(mgk_graph* h) : h_(h) {}
+    ~DeviceMatrix();
+    DeviceMatrix(const DeviceMatrix&) = delete;
+    DeviceMatrix& operator=(const DeviceMatrix&) = delete;
+    mgk_graph* handle() const noexcept { return h_; }
+
+private:
+    mgk_graph* h_;
+};
+
+class PropertyGraph {
+public:
+    explicit PropertyGraph(std::uint64_t initial_capacity = 16);
+    PropertyGraph(PropertyGraph&&) noexcept = default;
+    PropertyGraph& operator=(PropertyGraph&&) noexcept = default;
+    PropertyGraph(const PropertyGraph&) = delete;
+    PropertyGraph& operator=(const PropertyGraph&) = delete;
+
+    /// Allocates the next node id (labels / properties are not stored: the
+    /// k-hop path never reads them).
+    std::uint64_t create_node(const std::vector<std::string>& labels = {});
+    /// Records a directed typed edge (graph.cpp:54-82 contract and messages).
+    void create_edge(std::uint64_t src, const std::string& relation, std::uint64_t dst);
+
+    std::uint64_t node_count() const noexcept { return node_count_; }
+    std::uint64_t capacity() const noexcept { return capacity_; }
+
+    /// Flushes pending edges; unknown names yield the empty matrix (graph.cpp:84-88).
+    const SparseMatrix& relation_matrix(const RelationRef& rel = RelationRef::any()) const;
+    /// The matrix on `device` (uploaded on first use, cached until the next
+    /// flush that changes it; mutex-guarded like transposed_matrix).
+    const DeviceMatrix& device_matrix(const RelationRef& rel = RelationRef::any(),
+                                      int device = 0) const;
+    std::vector<std::string> relation_names() const;
+    /// Sort + dedup pending pairs into the CSR of each relation and ANY
+    /// (graph.cpp:167-215); drops device caches of changed matrices.
+    void flush() const;
+
+private:
+    struct Slot {
+        SparseMatrix matrix;
+        std::vector<std::pair<std::uint64_t, std::uint64_t>> pending;
+        std::map<int, std::shared_ptr<DeviceMatrix>> device;
+    };
+    void grow_to(std::uint64_t needed);
+    const Slot* find_slot(const RelationRef& rel) const;
+    static void flush_slot(Slot& slot, std::uint64_t dim);
+
+    std::uint64_t capacity_ = 0;
+    std::uint64_t node_count_ = 0;
+    mutable std::map<std::string, Slot, std::less<>> relations_;
+    mutable Slot any_;
+    mutable Slot empty_;
+    mutable std::unique_ptr<std::mutex> device_mutex_;
+};
+
+// ---- the k-hop kernel (execute.hpp:52-68) ------------------------------------------
+struct KHopQuery {
+    std::uint64_t seed = 0;
+    std::uint32_t k = 1;
+    RelationRef relation = RelationRef::any();
+    TraverseMode mode = TraverseMode::Exact;
+};
+
+/// Masked BFS from the seed (execute.cpp:347-371), on the GPU.
+BitVector k_hop_frontier(const PropertyGraph& graph, const KHopQuery& query);
+/// nvals(k_hop_frontier(graph, query)) (execute.cpp:373-375), on the GPU.
+std::uint64_t k_hop_count(const PropertyGraph& graph, const KHopQuery& query);
+/// Additive API: one k_hop_count per seed in one device call (bit-exact per seed).
+std::vector<std::uint64_t> k_hop_count_batch(const PropertyGraph& graph,
+                                             std::span<const std::uint64_t> seeds, std::uint32_t k,
+                                             const RelationRef& relation = RelationRef::any(),
+                                             TraverseMode mode = TraverseMode::Exact);
+
+// ---- benchmark harness (bench.hpp:16-156) -------------------------------------------
+struct RmatParams {
+    std::uint32_t scale = 14;
+    std::uint32_t edge_factor = 16;
+    double a = 0.57, b = 0.19, c = 0.19, d = 0.05;
+    std::uint64_t rng_seed = 1;
+    std::uint64_t node_count() const noexcept { return std::uint64_t{1} << scale; }
+    std::uint64_t edge_count() const noexcept { return std::uint64_t{edge_factor} << scale; }
+    void validate() const;
+};
+
+struct EdgeTuple {
+    std::uint32_t src = 0;
+    std::uint32_t dst = 0;
+    friend bool operator==(const EdgeTuple&, const EdgeTuple&) = default;
+};
+using EdgeList = std::vector<EdgeTuple>;
+
+inline constexpr std::string_view kBenchRelation = "EDGE";
+
+EdgeList rmat_generate(const RmatParams& params);
+PropertyGraph build_bench_graph(const EdgeList& edges, std::uint64_t node_count);
+std::vector<std::uint64_t> pick_seeds(const PropertyGraph& graph, std::size_t n,
+                                      std::uint64_t rng_seed);
+
+struct SeedRun {
+    std::uint64_t seed = 0;
+    std::uint64_t count = 0;
+    std::int64_t elapsed_us = 0;
+};
+struct SectionStats {
+    double mean_us = 0.0, median_us = 0.0, p99_us = 0.0, mean_count = 0.0;
+};
+SectionStats summarize(const std::vector<SeedRun>& runs);
+struct KHopSection {
+    std::uint32_t k = 0;
+    std::vector<SeedRun> runs;
+    SectionStats stats;
+};
+struct KHopReport {
+    TraverseMode mode = TraverseMode::Exact;
+    std::vector<KHopSection> sections;
+};
+struct BenchSchedule {
+    std::vector<std::uint32_t> ks;
+    std::vector<std::size_t> seeds_per_k;
+    TraverseMode mode = TraverseMode::Exact;
+    std::uint64_t rng_seed = 1;
+    void validate() const;
+};
+/// bench.cpp:311-343: sequential per-query timing like the reference
+/// (batched = true issues one device call per section instead and spreads its
+/// wall time over the section's seeds).
+KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule,
+                              bool batched = false);
+std::string report_csv_string(const KHopReport& report);
+void report_csv(const KHopReport& report, const std::filesystem::path& path);
+
+}  // namespace matgraph

@@ -1,0 +1,247 @@
+// The C++ drop-in (namespace matgraph, include/matgraph_b200/khop.hpp) run
+// against the reference's own test cases for the k-hop path and against the
+// CPU oracle (oracle/khop_oracle.c, linked as the checker).
+//   proj/tests/test_execute.cpp:32-47, 104-139   k-hop known answers and errors
+//   proj/tests/test_bench.cpp:33-349              harness pieces, oracle agreement
+//   proj/tests/acceptance/acceptance_main.cpp:53-88  c1 (20 RMAT graphs x 50 seeds)
+// `test_dropin --cpu` runs only the cases that need no GPU.
+#include <cstdint>
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "matgraph_b200/khop.hpp"
+#include "mini_test.hpp"
+
+extern "C" {  // oracle/khop_oracle.c (checker only)
+typedef struct orc_adj orc_adj;
+orc_adj* orc_adj_new(uint64_t n, uint64_t m, const uint32_t* src, const uint32_t* dst);
+void orc_adj_free(orc_adj* g);
+uint64_t orc_bfs_count(const orc_adj* g, uint64_t seed, uint32_t k, int mode);
+}
+
+using namespace matgraph;
+
+namespace {
+
+PropertyGraph path4() {  // 0 -> 1 -> 2 -> 3 over relation R
+    PropertyGraph g;
+    for (int i = 0; i < 4; ++i) g.create_node({});
+    for (std::uint64_t i = 0; i < 3; ++i) g.create_edge(i, "R", i + 1);
+    return g;
+}
+
+PropertyGraph triangle() {  // 0 -> 1 -> 2 -> 0 over relation R
+    PropertyGraph g;
+    for (int i = 0; i < 3; ++i) g.create_node({});
+    g.create_edge(0, "R", 1);
+    g.create_edge(1, "R", 2);
+    g.create_edge(2, "R", 0);
+    return g;
+}
+
+struct Oracle {  // BfsOracle semantics over the raw edge list
+    orc_adj* h;
+    Oracle(const EdgeList& e, std::uint64_t n) {
+        std::vector<uint32_t> s, d;
+        for (auto& t : e) {
+            s.push_back(t.src);
+            d.push_back(t.dst);
+        }
+        if (s.empty()) {
+            s.push_back(0);
+            d.push_back(0);
+        }
+        h = orc_adj_new(n, e.size(), s.data(), d.data());
+    }
+    ~Oracle() { orc_adj_free(h); }
+    std::uint64_t count(std::uint64_t seed, std::uint32_t k, TraverseMode m) const {
+        return orc_bfs_count(h, seed, k, m == TraverseMode::Exact ? 0 : 1);
+    }
+};
+
+}  // namespace
+
+// ---- proj/tests/test_execute.cpp ------------------------------------------------------------
+GPU_TEST_CASE("k-hop counts match the masked-BFS definition") {  // test_execute.cpp:104-120
+    PropertyGraph path = path4();
+    PropertyGraph tri = triangle();
+    CHECK(k_hop_count(path, {.seed = 0, .k = 2, .mode = TraverseMode::Exact}) == 1);
+    const auto frontier = k_hop_frontier(path, {.seed = 0, .k = 2});
+    CHECK(std::vector<std::uint64_t>(frontier.indices().begin(), frontier.indices().end()) ==
+          std::vector<std::uint64_t>{2});
+    CHECK(k_hop_count(path, {.seed = 3, .k = 1, .mode = TraverseMode::Exact}) == 0);
+    CHECK(k_hop_count(path, {.seed = 0, .k = 6, .mode = TraverseMode::Cumulative}) == 3);
+    CHECK(k_hop_count(tri, {.seed = 0, .k = 3, .mode = TraverseMode::Exact}) == 0);
+    CHECK(k_hop_count(tri, {.seed = 0, .k = 3, .mode = TraverseMode::Cumulative}) == 2);
+}
+
+GPU_TEST_CASE("k-hop respects the relation filter") {  // test_execute.cpp:122-129
+    PropertyGraph g = path4();
+    g.create_edge(0, "S", 3);
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1, .relation = "R"}) == 1);
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1, .relation = RelationRef::any()}) == 2);
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1, .relation = "S"}) == 1);
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1, .relation = "NONE"}) == 0);
+}
+
+TEST_CASE("k-hop rejects out-of-range seeds and hop counts") {  // test_execute.cpp:131-139
+    PropertyGraph g = path4();
+    CHECK_THROWS_WITH_AS(k_hop_count(g, {.seed = 99, .k = 1}), "k-hop seed 99 is not an allocated node",
+                         ContractError);
+    CHECK_THROWS_WITH_AS(k_hop_count(g, {.seed = 0, .k = 0}), "k-hop count 0 outside [1, 32]", ContractError);
+    CHECK_THROWS_WITH_AS(k_hop_count(g, {.seed = 0, .k = 33}), "k-hop count 33 outside [1, 32]",
+                         ContractError);
+}
+
+GPU_TEST_CASE("a cached device matrix is dropped when new edges arrive") {
+    PropertyGraph g = path4();
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1}) == 1);
+    g.create_edge(0, "R", 2);  // pending until the next read flushes it
+    CHECK(k_hop_count(g, {.seed = 0, .k = 1}) == 2);
+    CHECK(k_hop_count(g, {.seed = 0, .k = 2, .mode = TraverseMode::Exact}) == 1);
+}
+
+// ---- proj/tests/test_bench.cpp --------------------------------------------------------------
+TEST_CASE("rmat generation is deterministic and in bounds") {  // test_bench.cpp:33-50
+    RmatParams params;
+    params.scale = 8;
+    params.rng_seed = 42;
+    const EdgeList first = rmat_generate(params);
+    REQUIRE(first.size() == params.edge_count());
+    CHECK(first == rmat_generate(params));
+    params.rng_seed = 43;
+    CHECK(rmat_generate(params) != first);
+    for (const auto& e : first) REQUIRE(e.src < 256 && e.dst < 256);
+}
+
+TEST_CASE("rmat parameters are validated") {  // test_bench.cpp:66-79
+    RmatParams params;
+    params.scale = 25;
+    CHECK_THROWS_WITH_AS(params.validate(), "RMAT scale 25 exceeds the cap of 24", ContractError);
+    params.scale = 10;
+    params.a = -0.1;
+    params.b = 0.57 + 0.19 + 0.1 - 0.05;
+    CHECK_THROWS_WITH_AS(params.validate(), "RMAT quadrant probabilities must be non-negative", ContractError);
+}
+
+TEST_CASE("the bench graph carries one edge relation and collapses duplicates") {  // :81-91
+    const EdgeList edges = {{0, 1}, {1, 2}, {1, 2}, {2, 0}};
+    PropertyGraph g = build_bench_graph(edges, 4);
+    CHECK(g.node_count() == 4);
+    CHECK(g.relation_names() == std::vector<std::string>{std::string(kBenchRelation)});
+    CHECK(g.relation_matrix("EDGE").nvals() == 3);
+    CHECK_THROWS_WITH_AS(build_bench_graph({{5, 9}}, 4), "edge (5, 9) outside the 4-node range", ContractError);
+}
+
+TEST_CASE("seed picking is deterministic and sticks to source nodes") {  // :93-102
+    RmatParams params;
+    params.scale = 7;
+    PropertyGraph g = build_bench_graph(rmat_generate(params), params.node_count());
+    const auto seeds = pick_seeds(g, 50, 9);
+    CHECK(seeds == pick_seeds(g, 50, 9));
+    CHECK(seeds != pick_seeds(g, 50, 10));
+    CHECK(std::set<std::uint64_t>(seeds.begin(), seeds.end()).size() == seeds.size());
+    for (auto s : seeds) CHECK_FALSE(g.relation_matrix().row(s).empty());
+}
+
+TEST_CASE("seed picking fails loudly when too few nodes qualify") {  // :104-113
+    PropertyGraph g = build_bench_graph({{0, 1}}, 3);
+    CHECK(pick_seeds(g, 1, 1) == std::vector<std::uint64_t>{0});
+    CHECK_THROWS_WITH_AS(pick_seeds(g, 2, 1), "need 2 seeds but only 1 nodes have out-degree >= 1",
+                         HarnessError);
+}
+
+GPU_TEST_CASE("the oracle agrees with the k-hop counter on rmat graphs") {  // :115-138
+    RmatParams params;
+    params.scale = 6;
+    params.rng_seed = 3;
+    const EdgeList edges = rmat_generate(params);
+    PropertyGraph g = build_bench_graph(edges, params.node_count());
+    Oracle oracle(edges, params.node_count());
+    for (std::uint64_t seed : pick_seeds(g, 20, 5))
+        for (std::uint32_t k : {1u, 2u, 3u, 6u})
+            for (TraverseMode mode : {TraverseMode::Exact, TraverseMode::Cumulative})
+                CHECK(k_hop_count(g, {.seed = seed, .k = k, .relation = std::string(kBenchRelation),
+                                      .mode = mode}) == oracle.count(seed, k, mode));
+}
+
+TEST_CASE("summary statistics match hand-computed values") {  // :148-168
+    std::vector<SeedRun> runs = {{0, 2, 10}, {1, 4, 30}, {2, 6, 20}, {3, 8, 40}};
+    const SectionStats s = summarize(runs);
+    CHECK(s.mean_us == 25.0);
+    CHECK(s.median_us == 25.0);
+    CHECK(s.p99_us == 40.0);
+    CHECK(s.mean_count == 5.0);
+    CHECK(summarize({{0, 0, 1}, {1, 0, 100}, {2, 0, 2}}).median_us == 2.0);
+    CHECK_THROWS_WITH_AS(summarize({}), "cannot summarize an empty run list", ContractError);
+}
+
+TEST_CASE("schedules validate their shape before any work starts") {  // :170-188
+    BenchSchedule schedule;
+    schedule.ks = {1, 2};
+    schedule.seeds_per_k = {10};
+    CHECK_THROWS_WITH_AS(schedule.validate(), "schedule pairs 2 hop counts with 1 seed counts", ContractError);
+    schedule.seeds_per_k = {10, 0};
+    CHECK_THROWS_WITH_AS(schedule.validate(), "seed count for k=2 must be at least 1", ContractError);
+    schedule.ks = {0, 2};
+    schedule.seeds_per_k = {10, 10};
+    CHECK_THROWS_WITH_AS(schedule.validate(), "hop count 0 outside [1, 32]", ContractError);
+}
+
+TEST_CASE("reports serialize with fixed headers and one row per unit") {  // :190-209
+    KHopReport empty;
+    CHECK(report_csv_string(empty) == "k,seed,count,elapsed_us\nk,n_seeds,mean_us,median_us,p99_us,mean_count\n");
+    KHopReport report;
+    report.sections.push_back({2, {{5, 7, 10}, {6, 9, 20}}, summarize({{5, 7, 10}, {6, 9, 20}})});
+    CHECK(report_csv_string(report) ==
+          "k,seed,count,elapsed_us\n2,5,7,10\n2,6,9,20\n"
+          "k,n_seeds,mean_us,median_us,p99_us,mean_count\n2,2,15,15,20,8\n");
+}
+
+GPU_TEST_CASE("benchmark counts agree with the oracle in both modes") {  // :295-317
+    RmatParams params;
+    params.scale = 6;
+    params.rng_seed = 11;
+    const EdgeList edges = rmat_generate(params);
+    PropertyGraph g = build_bench_graph(edges, params.node_count());
+    Oracle oracle(edges, params.node_count());
+    for (TraverseMode mode : {TraverseMode::Exact, TraverseMode::Cumulative})
+        for (bool batched : {false, true}) {
+            BenchSchedule schedule;
+            schedule.ks = {1, 2, 6};
+            schedule.seeds_per_k = {10, 10, 10};
+            schedule.mode = mode;
+            const KHopReport report = run_khop_benchmark(g, schedule, batched);
+            for (const auto& section : report.sections)
+                for (const auto& run : section.runs)
+                    CHECK(run.count == oracle.count(run.seed, section.k, mode));
+        }
+}
+
+// ---- acceptance c1 --------------------------------------------------------------------------
+GPU_TEST_CASE("c1: 8000 k-hop counts equal the BFS oracle") {  // acceptance_main.cpp:53-88
+    std::uint64_t agreements = 0, mismatches = 0;
+    for (std::uint64_t rng_seed = 1; rng_seed <= 20; ++rng_seed) {
+        RmatParams params;
+        params.scale = static_cast<std::uint32_t>(6 + (rng_seed - 1) % 7);
+        params.rng_seed = rng_seed;
+        const EdgeList edges = rmat_generate(params);
+        PropertyGraph graph = build_bench_graph(edges, params.node_count());
+        Oracle oracle(edges, params.node_count());
+        const auto seeds = pick_seeds(graph, 50, rng_seed);
+        for (std::uint32_t k : {1u, 2u, 3u, 6u})
+            for (TraverseMode mode : {TraverseMode::Exact, TraverseMode::Cumulative}) {
+                const auto got = k_hop_count_batch(graph, seeds, k, std::string(kBenchRelation), mode);
+                for (std::size_t i = 0; i < seeds.size(); ++i)
+                    (got[i] == oracle.count(seeds[i], k, mode) ? agreements : mismatches) += 1;
+            }
+    }
+    CHECK(mismatches == 0);
+    CHECK(agreements == 8000);
+}
+
+int main(int argc, char** argv) { return mini::run(argc, argv); }
