@@ -107,13 +107,44 @@ def dist_env():
             int(os.environ.get("WORLD_SIZE", 1)))
 
 
-def build_inputs(world: int, rank: int):
+def seed_shard(master, rank: int, world: int, per_rank: int):
+    """Rank r's disjoint shard of the master seed list (weak scaling)."""
+    assert len(master) >= per_rank * world
+    return master[rank * per_rank:(rank + 1) * per_rank]
+
+
+def build_inputs(world: int, rank: int, dist=None, device=None):
+    """G2 CSR + this rank's seeds. With world > 1 rank 0 generates the graph and
+    the master seed list and broadcasts them (NCCL over NVLink): load-time
+    replication, not on the timed path."""
     from paper_1905_01294_b200 import harness as H
     t = time.time()
-    rp, ci = H.gen_csr(H.G2)
-    master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
-    seeds = master[rank * SEEDS_PER_RANK:(rank + 1) * SEEDS_PER_RANK]
-    log(f"[rank {rank}] G2: n={len(rp) - 1} m={len(ci)} generated in {time.time() - t:.1f}s")
+    if world == 1 or dist is None:
+        rp, ci = H.gen_csr(H.G2)
+        master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
+    else:
+        import torch
+        if rank == 0:
+            rp, ci = H.gen_csr(H.G2)
+            master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
+            meta = torch.tensor([len(rp), len(ci)], dtype=torch.int64, device=device)
+        else:
+            meta = torch.zeros(2, dtype=torch.int64, device=device)
+        dist.broadcast(meta, 0)
+        n1, m = int(meta[0]), int(meta[1])
+        trp = torch.from_numpy(rp.view(np.int32)).to(device) if rank == 0 else \
+            torch.empty(n1, dtype=torch.int32, device=device)
+        tci = torch.from_numpy(ci.view(np.int32)).to(device) if rank == 0 else \
+            torch.empty(m, dtype=torch.int32, device=device)
+        tms = torch.from_numpy(master.view(np.int64)).to(device) if rank == 0 else \
+            torch.empty(SEEDS_PER_RANK * world, dtype=torch.int64, device=device)
+        for tt in (trp, tci, tms):
+            dist.broadcast(tt, 0)
+        rp = trp.cpu().numpy().view(np.uint32)
+        ci = tci.cpu().numpy().view(np.uint32)
+        master = tms.cpu().numpy().view(np.uint64)
+    seeds = seed_shard(master, rank, world, SEEDS_PER_RANK)
+    log(f"[rank {rank}] G2: n={len(rp) - 1} m={len(ci)} ready in {time.time() - t:.1f}s")
     return rp, ci, seeds
 
 
@@ -164,7 +195,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rp, ci, seeds = build_inputs(world, rank)
+    rp, ci, seeds = build_inputs(world, rank, dist if world > 1 else None, torch.device("cuda", local))
     t = time.time()
     g = DeviceGraph.from_csr(rp, ci, device=local)
     if args.lanes_words:
