@@ -158,9 +158,10 @@ def algo_bytes(st: dict) -> float:
     vertex (push: frontier vertices, pull: candidates) + 4 B per frontier id
     read (push) + 4 B per discovered id written. Bitmaps are L2-resident and
     not counted.
-    LANES (W x 64-bit lane words): 4 B per adjacency entry read + (8 + 8W) B per
-    expanded (push) / candidate (pull) vertex + 3 x 8W B per discovered vertex
-    (F' read, V read + write)."""
+    LANES (W x 64-bit lane words): (4 + 8W) B per adjacency entry read (the
+    index and the neighbour's lane word) + (8 + 8W) B per expanded (push) /
+    candidate (pull) vertex + 3 x 8W B per discovered vertex (F' read, V read +
+    write)."""
     lv = st["levels"]
     total = 0.0
     if st["engine"] == "lanes":
@@ -170,7 +171,7 @@ def algo_bytes(st: dict) -> float:
             if not L["runs"]:
                 continue
             expanded = L["candidates"] if L["pull_runs"] else lv[h - 1]["vertices"]
-            total += 4 * L["scanned"] + (8 + 8 * W) * expanded + 24 * W * L["vertices"]
+            total += (4 + 8 * W) * L["scanned"] + (8 + 8 * W) * expanded + 24 * W * L["vertices"]
         return total
     for h in range(1, len(lv)):
         L = lv[h]
@@ -182,6 +183,69 @@ def algo_bytes(st: dict) -> float:
         opened = L["candidates"] + prev * push_share
         total += 4 * L["scanned"] + 8 * opened + 4 * prev * push_share + 4 * L["frontier"]
     return total
+
+
+def hop_bytes(st: dict, h: int) -> float:
+    """algo_bytes restricted to hop h (same model)."""
+    one = dict(st)
+    lv = st["levels"]
+    one["levels"] = [dict(L, runs=0) if i not in (h - 1, h) else (L if i == h else dict(L, runs=0))
+                     for i, L in enumerate(lv)]
+    return algo_bytes(one)
+
+
+def run_extras(g, rp, world, rank, dist, stream, flush, torch):
+    """BASELINE.json configs[2] (cfg3: 10 seeds, k=3,6) and configs[4] (cfg5:
+    65,536 seeds in 64-lane words, k=1,2,3,6; seed batches split across
+    ranks), on the already-resident G2. Device-resident, CUDA-event timed, L2
+    flushed before each call; per-hop device time from the engine's
+    %globaltimer stamps gives each frontier-expansion phase's achieved bytes/s."""
+    from paper_1905_01294_b200 import harness as H, k_hop_count_device, device_stats
+    import numpy as np
+    out = {}
+    sp = stream.cuda_stream
+    pk, _ = peaks()
+    master = H.pick_seeds(rp, 65536, 1)
+    plans = [("cfg3", master[:10], (3, 6), 3), ("cfg5", master, (1, 2, 3, 6), 1)]
+    for name, seeds_all, ks, reps in plans:
+        per = (len(seeds_all) + world - 1) // world if name == "cfg5" else len(seeds_all)
+        seeds = seeds_all[rank * per:(rank + 1) * per] if name == "cfg5" else seeds_all
+        d_seeds = torch.from_numpy(np.ascontiguousarray(seeds).astype(np.int32)).cuda()
+        d_counts = torch.zeros(len(seeds), dtype=torch.int64, device="cuda")
+        sec = {"seeds": int(len(seeds_all)), "seeds_per_rank": int(len(seeds)), "k": {}}
+        for k in ks:
+            k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+            times = []
+            for _ in range(reps):
+                flush.fill_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+            ms = float(np.median(times))
+            st = device_stats(g, sp)
+            if world > 1:
+                t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                ms = float(t[0])
+            edges = sum(L["edges"] for L in st["levels"]) * world
+            hops = []
+            for h in range(1, len(st["levels"])):
+                L = st["levels"][h]
+                if not L["runs"] or not L["ns"]:
+                    continue
+                b = hop_bytes(st, h)
+                hops.append({"hop": h, "dir": "pull" if L["pull_runs"] else "push", "scanned": L["scanned"],
+                             "us": L["ns"] / 1e3, "algo_GBps": b / L["ns"],
+                             "frac_of_peak": b / L["ns"] / pk["hbm_gbs"]})
+            sec["k"][str(k)] = {"ms": ms, "queries_per_s": len(seeds) * world / (ms / 1e3),
+                                "gteps": edges / (ms / 1e3) / 1e9, "engine": st["engine"],
+                                "lanes_per_batch": st["lanes"], "hops": hops,
+                                "count_sum": int(d_counts.sum().item())}
+        out[name] = sec
+    return out
 
 
 def run_ours(args):
@@ -275,6 +339,9 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, e2e_total = float(tt[0]), float(tt[1])
 
+    # BASELINE configs[2] / [4] on the same resident graph (every rank takes part)
+    extras = None if args.no_extras else run_extras(g, rp, world, rank, dist, stream, flush, torch)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -335,6 +402,7 @@ def run_ours(args):
                 "ms_per_step": e2e_total / args.steps},
         "gpu_launches": sum(stats[k]["launches"] for k in KS) * args.steps,
         "clocks": clocks,
+        "extra_configs": extras,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -426,6 +494,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lanes-words", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 / cfg5 sections")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -72,6 +72,23 @@ __global__ void no_in_bitmap(const uint32_t* cp, uint32_t n, uint32_t nwords, ui
     }
 }
 
+// in-degree > kHeavyIn: count kHeavyChunk tasks; mark in the pull skip mask
+__global__ void heavy_count(const uint32_t* cp, uint32_t n, uint32_t* cnt, uint32_t* skip) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const uint32_t d = cp[u + 1] - cp[u];
+        const bool heavy = d > kHeavyIn;
+        cnt[u] = heavy ? (d + kHeavyChunk - 1) / kHeavyChunk : 0;
+        if (heavy) atomicOr(skip + (u >> 5), 1u << (u & 31));
+    }
+}
+
+__global__ void heavy_fill(const uint32_t* cp, uint32_t n, const uint32_t* off, uint2* tasks) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const uint32_t c = off[u + 1] - off[u];
+        for (uint32_t i = 0; i < c; ++i) tasks[off[u] + i] = make_uint2(u, cp[u] + i * kHeavyChunk);
+    }
+}
+
 __global__ void pack_edges(const uint32_t* src, const uint32_t* dst, uint64_t m, uint32_t n,
                            unsigned long long* keys, unsigned int* bad) {
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
@@ -116,6 +133,48 @@ cudaError_t radix_sort_keys(unsigned long long*& keys, unsigned long long*& alt,
     return cudaSuccess;
 }
 
+cudaError_t build_heavy(Graph* g, cudaStream_t s);
+
+// (col << 32 | row) sorted keys -> (col << 32 | ~outdeg(row)) keys + row values
+__global__ void make_deg_keys(unsigned long long* keys, uint32_t* vals, uint64_t m,
+                              const uint32_t* rp) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long k = keys[p];
+        const uint32_t row = (uint32_t)k;
+        const uint32_t deg = rp[row + 1] - rp[row];
+        keys[p] = (k & 0xFFFFFFFF00000000ull) | (0xFFFFFFFFu - deg);
+        vals[p] = row;
+    }
+}
+
+// Order every in-neighbour list by descending out-degree (ties: ascending id,
+// the radix sort is stable). Pull passes OR / test in-neighbours in list order
+// and stop at the first hit (SINGLE) or once every needed lane is covered
+// (LANES); hubs sit in most frontiers, so putting them first ends scans early.
+// The list is a set, so results do not depend on the order.
+cudaError_t order_in_lists(Graph* g, unsigned long long*& keys, unsigned long long*& alt, cudaStream_t s) {
+    const uint64_t m = g->dg.m;
+    const uint32_t n = g->dg.n;
+    uint32_t *vals = nullptr, *valt = nullptr;
+    MGK_TRY(cudaMallocAsync(&vals, m * 4, s));
+    MGK_TRY(cudaMallocAsync(&valt, m * 4, s));
+    make_deg_keys<<<blocks_for(m), kTB, 0, s>>>(keys, vals, m, g->rp);
+    MGK_TRY(cudaGetLastError());
+    cub::DoubleBuffer<unsigned long long> dk(keys, alt);
+    cub::DoubleBuffer<uint32_t> dv(vals, valt);
+    size_t tmp = 0;
+    MGK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int64_t)m, 0, 32 + key_bits(n), s));
+    void* t = nullptr;
+    MGK_TRY(cudaMallocAsync(&t, tmp, s));
+    MGK_TRY(cub::DeviceRadixSort::SortPairs(t, tmp, dk, dv, (int64_t)m, 0, 32 + key_bits(n), s));
+    MGK_TRY(cudaMemcpyAsync(g->ri, dv.Current(), m * 4, cudaMemcpyDeviceToDevice, s));
+    MGK_TRY(cudaFreeAsync(t, s));
+    MGK_TRY(cudaFreeAsync(vals, s));
+    MGK_TRY(cudaFreeAsync(valt, s));
+    return cudaSuccess;
+}
+
 // Given device CSR (rp, ci) fill CSC (cp, ri) and the no_in bitmap.
 cudaError_t build_csc(Graph* g, cudaStream_t s) {
     const uint32_t n = g->dg.n;
@@ -128,13 +187,41 @@ cudaError_t build_csc(Graph* g, cudaStream_t s) {
         fill_cols<<<blocks_for(m), kTB, 0, s>>>(g->ci, m, keys);
         MGK_TRY(radix_sort_keys(keys, alt, m, 32 + key_bits(n), s));
         keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
+        MGK_TRY(order_in_lists(g, keys, alt, s));
         MGK_TRY(cudaFreeAsync(keys, s));
         MGK_TRY(cudaFreeAsync(alt, s));
     } else {
         MGK_TRY(cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s));
     }
     no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
-    return cudaGetLastError();
+    MGK_TRY(cudaGetLastError());
+    return build_heavy(g, s);
+}
+
+// pull_skip = no_in | heavy, and the heavy task list (prefix sum of chunk counts)
+cudaError_t build_heavy(Graph* g, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    MGK_TRY(cudaMemcpyAsync(g->pull_skip, g->no_in, (size_t)(g->dg.nwords + 1) * 4,
+                            cudaMemcpyDeviceToDevice, s));
+    uint32_t* cnt = nullptr;
+    MGK_TRY(cudaMallocAsync(&cnt, (size_t)(n + 1) * 4, s));
+    heavy_count<<<blocks_for(n), kTB, 0, s>>>(g->cp, n, cnt, g->pull_skip);
+    MGK_TRY(cudaGetLastError());
+    unsigned long long* d_total = nullptr;
+    MGK_TRY(cudaMallocAsync(&d_total, 8, s));
+    MGK_TRY(exclusive_scan_u32(cnt, n, d_total, s));
+    unsigned long long total = 0;
+    MGK_TRY(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, s));
+    MGK_TRY(cudaStreamSynchronize(s));
+    g->dg.nheavy = (uint32_t)total;
+    MGK_TRY(cudaMalloc(&g->heavy, (size_t)std::max<unsigned long long>(total, 1) * sizeof(uint2)));
+    g->dg.heavy = g->heavy;
+    g->bytes += (size_t)std::max<unsigned long long>(total, 1) * sizeof(uint2);
+    if (total) heavy_fill<<<blocks_for(n), kTB, 0, s>>>(g->cp, n, cnt, g->heavy);
+    MGK_TRY(cudaGetLastError());
+    MGK_TRY(cudaFreeAsync(cnt, s));
+    MGK_TRY(cudaFreeAsync(d_total, s));
+    return cudaSuccess;
 }
 
 cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
@@ -147,12 +234,14 @@ cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
     MGK_TRY(cudaMalloc(&g->cp, (size_t)(n + 1) * 4));
     MGK_TRY(cudaMalloc(&g->ri, mp * 4));
     MGK_TRY(cudaMalloc(&g->no_in, (size_t)(g->dg.nwords + 1) * 4));
-    g->bytes = 2 * (size_t)(n + 1) * 4 + 2 * mp * 4 + (size_t)(g->dg.nwords + 1) * 4;
+    MGK_TRY(cudaMalloc(&g->pull_skip, (size_t)(g->dg.nwords + 1) * 4));
+    g->bytes = 2 * (size_t)(n + 1) * 4 + 2 * mp * 4 + 2 * (size_t)(g->dg.nwords + 1) * 4;
     g->dg.rp = g->rp;
     g->dg.ci = g->ci;
     g->dg.cp = g->cp;
     g->dg.ri = g->ri;
     g->dg.no_in = g->no_in;
+    g->dg.pull_skip = g->pull_skip;
     return cudaSuccess;
 }
 
@@ -264,11 +353,13 @@ cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const
             swap_halves<<<blocks_for(m), kTB, 0, s>>>(keys, m);
             if ((e = radix_sort_keys(keys, alt, m, 32 + key_bits(n), s))) break;
             keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
+            if ((e = order_in_lists(g, keys, alt, s))) break;
         } else {
             if ((e = cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s))) break;
         }
         no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
         if ((e = cudaGetLastError())) break;
+        if ((e = build_heavy(g, s))) break;
         e = cudaStreamSynchronize(s);
     } while (0);
     if (keys) cudaFreeAsync(keys, s);
@@ -288,7 +379,10 @@ void free_device_graph(Graph* g) {
     cudaFree(g->cp);
     cudaFree(g->ri);
     cudaFree(g->no_in);
-    g->rp = g->ci = g->cp = g->ri = g->no_in = nullptr;
+    cudaFree(g->pull_skip);
+    cudaFree(g->heavy);
+    g->rp = g->ci = g->cp = g->ri = g->no_in = g->pull_skip = nullptr;
+    g->heavy = nullptr;
 }
 
 }  // namespace mgk

@@ -27,7 +27,14 @@ struct DevGraph {
     const uint32_t* cp = nullptr;     // col_ptr[n+1] (CSC)
     const uint32_t* ri = nullptr;     // row_idx[m], ascending per column
     const uint32_t* no_in = nullptr;  // bitmap: zero in-degree (and padding ids >= n)
+    // pull load balance: vertices with in-degree > kHeavyIn are scanned as
+    // kHeavyChunk-entry tasks spread over the grid instead of by one warp
+    const uint32_t* pull_skip = nullptr;  // no_in | heavy: what the per-word pull pass skips
+    const uint2* heavy = nullptr;         // {vertex, first CSC entry} per task
+    uint32_t nheavy = 0;
 };
+constexpr uint32_t kHeavyIn = 1024;
+constexpr uint32_t kHeavyChunk = 1024;
 
 // Per-level device counters, mirrored into mgk_level on the host.
 struct LevelCounters {
@@ -116,6 +123,8 @@ struct Graph {
     uint32_t* cp = nullptr;
     uint32_t* ri = nullptr;
     uint32_t* no_in = nullptr;
+    uint32_t* pull_skip = nullptr;
+    uint2* heavy = nullptr;
     uint64_t bytes = 0;
     Tuning tuning;
     std::mutex mu;

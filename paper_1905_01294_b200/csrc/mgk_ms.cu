@@ -231,6 +231,52 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
 }
 
 // ---- pull expand -------------------------------------------------------------
+// Vertices are split by in-degree: <= 32 in-edges are scanned by one thread
+// (two lane-word gathers in flight per step), 33..kHeavyIn by the word's warp
+// cooperatively (each lane ORs its own stride, one warp reduction per 256
+// entries for the early-exit test), and > kHeavyIn as kHeavyChunk-entry tasks
+// spread over the whole grid (DevGraph::heavy), so no hub serialises a warp.
+template <int W>
+__device__ __forceinline__ LaneWord<W> warp_or_lw(LaneWord<W> a) {
+#pragma unroll
+    for (int i = 0; i < W; ++i) a.w[i] = warp_or_u64(a.w[i]);
+    return a;
+}
+
+template <int W>
+__device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>& need) {
+    bool done = true;
+#pragma unroll
+    for (int i = 0; i < W; ++i) done &= (acc.w[i] & need.w[i]) == need.w[i];
+    return done;
+}
+
+// Warp-wide: OR of the lane words of in-neighbours ri[b..e), stopping early
+// once `need` is covered. Returns the OR (all lanes) and the entries read.
+template <int W>
+__device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
+                                                       uint32_t b, uint32_t e, const LaneWord<W>& need,
+                                                       uint32_t& scanned) {
+    const uint32_t lane = lane_id();
+    LaneWord<W> acc;
+#pragma unroll
+    for (int i = 0; i < W; ++i) acc.w[i] = 0;
+    scanned = 0;
+    for (uint32_t p0 = b; p0 < e; p0 += 256) {
+        const uint32_t pe = min(e, p0 + 256);
+#pragma unroll 2
+        for (uint32_t p = p0 + lane; p < pe; p += 32) {
+            const LaneWord<W> f = load_lw<W>(Fc + (size_t)__ldg(P.g.ri + p) * W);
+#pragma unroll
+            for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
+        }
+        scanned += pe - p0;
+        acc = warp_or_lw<W>(acc);
+        if (covers<W>(acc, need)) break;
+    }
+    return acc;
+}
+
 template <int W>
 __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
@@ -238,14 +284,14 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     for (uint32_t w = warp_gid; w < g.nwords; w += nwarps) {
-        const uint32_t noin = __ldg(g.no_in + w);
-        if (noin == kFull) continue;
+        const uint32_t skip = __ldg(g.pull_skip + w);
+        if (skip == kFull) continue;
         const uint32_t u = w * 32 + lane;
         LaneWord<W> need, vis;
 #pragma unroll
         for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
         bool cand = false;
-        if (!((noin >> lane) & 1u)) {
+        if (!((skip >> lane) & 1u)) {
             vis = load_lw<W>(P.V + (size_t)u * W);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
@@ -265,17 +311,13 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         if (cand && e - b <= 32) {
             uint32_t p = b;
             bool done = false;
-            // two in-neighbours per step: their lane words are gathered together
             for (; p + 2 <= e && !done; p += 2) {
                 const uint32_t v0 = __ldg(g.ri + p), v1 = __ldg(g.ri + p + 1);
                 const LaneWord<W> f0 = load_lw<W>(Fc + (size_t)v0 * W);
                 const LaneWord<W> f1 = load_lw<W>(Fc + (size_t)v1 * W);
-                done = true;
 #pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    acc_w.w[i] |= f0.w[i] | f1.w[i];
-                    done &= (acc_w.w[i] & need.w[i]) == need.w[i];
-                }
+                for (int i = 0; i < W; ++i) acc_w.w[i] |= f0.w[i] | f1.w[i];
+                done = covers<W>(acc_w, need);
                 scanned += 2;
             }
             if (!done && p < e) {
@@ -285,36 +327,16 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 ++scanned;
             }
         }
-        unsigned big = __ballot_sync(kFull, cand && e - b > 32);
-        while (big) {
-            const int j = __ffs(big) - 1;
-            big &= big - 1;
-            const uint32_t bj = __shfl_sync(kFull, b, j), ej = __shfl_sync(kFull, e, j);
-            LaneWord<W> nj, aj;
+        unsigned mid = __ballot_sync(kFull, cand && e - b > 32);
+        while (mid) {
+            const int j = __ffs(mid) - 1;
+            mid &= mid - 1;
+            LaneWord<W> nj;
 #pragma unroll
-            for (int i = 0; i < W; ++i) {
-                nj.w[i] = __shfl_sync(kFull, need.w[i], j);
-                aj.w[i] = 0;
-            }
+            for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i], j);
             uint32_t sc = 0;
-            for (uint32_t p0 = bj; p0 < ej; p0 += 32) {
-                const uint32_t p = p0 + lane;
-                LaneWord<W> f;
-                if (p < ej) {
-                    f = load_lw<W>(Fc + (size_t)__ldg(g.ri + p) * W);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < W; ++i) f.w[i] = 0;
-                }
-                bool done = true;
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    aj.w[i] |= warp_or_u64(f.w[i]);
-                    done &= (aj.w[i] & nj.w[i]) == nj.w[i];
-                }
-                sc += min(32u, ej - p0);
-                if (done) break;
-            }
+            const LaneWord<W> aj = warp_pull_range<W>(P, Fc, __shfl_sync(kFull, b, j),
+                                                      __shfl_sync(kFull, e, j), nj, sc);
             if ((int)lane == j) {
                 acc_w = aj;
                 scanned += sc;
@@ -344,6 +366,54 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             st.n = 0;
         }
     }
+    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step
+    for (uint32_t t = warp_gid; t < g.nheavy; t += nwarps) {
+        const uint2 task = __ldg(g.heavy + t);
+        const uint32_t u = task.x;
+        const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
+        LaneWord<W> need;
+        bool cand = false;
+#pragma unroll
+        for (int i = 0; i < W; ++i) {
+            need.w[i] = active.w[i] & ~vis.w[i];
+            cand |= need.w[i] != 0;
+        }
+        bool first = false;
+        if (cand) {
+            const uint32_t e = min(task.y + kHeavyChunk, __ldg(g.cp + u + 1));
+            uint32_t sc = 0;
+            const LaneWord<W> aj = warp_pull_range<W>(P, Fc, task.y, e, need, sc);
+            if (lane == 0) {
+                acc.scanned += sc;
+                acc.candidates += task.y == __ldg(g.cp + u);
+                bool any = false;
+                unsigned long long* fn = Fn + (size_t)u * W;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    const unsigned long long r = aj.w[i] & need.w[i];
+                    if (r) {
+                        atomicOr(fn + i, r);
+                        any = true;
+                    }
+                }
+                if (any) {  // several chunks of one vertex: the first one enqueues it
+                    const uint32_t bit = 1u << (u & 31);
+                    first = !(atomicOr(P.touched + (u >> 5), bit) & bit);
+                    if (first) {
+                        bool fresh = true;
+#pragma unroll
+                        for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
+                        count_discovered(g, u, fresh, acc);
+                    }
+                }
+            }
+        }
+        st.push(first, u);
+        if (st.full()) {
+            emit_list(st.buf, st.n, Rn, &qn->nitems);
+            st.n = 0;
+        }
+    }
     emit_list(st.buf, st.n, Rn, &qn->nitems);
     st.n = 0;
 }
@@ -359,11 +429,11 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     LaneWord<W> act;
-    unsigned long long cnt[W][2];
+    uint32_t cnt_lo[W], cnt_hi[W];
 #pragma unroll
     for (int i = 0; i < W; ++i) {
         act.w[i] = 0;
-        cnt[i][0] = cnt[i][1] = 0;
+        cnt_lo[i] = cnt_hi[i] = 0;
     }
     for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
         const uint32_t idx = base + lane;
@@ -386,7 +456,11 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
                 pc += __popcll(x.w[i]);
             }
             store_lw<W>(vp, v);
-            if (touched_set) atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
+            // push levels set a touched bit per discovery; pull levels only for
+            // heavy vertices (discovered vertices in pull_skip are heavy: a
+            // zero-in-degree vertex is never discovered)
+            if (touched_set || ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u))
+                atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
             if (clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
             const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
             acc.pairs += pc;
@@ -394,13 +468,20 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             expand = want_items && deg > 0;
         }
         if (count_lanes) {
+            // column popcounts: lane l accumulates bit l (cnt_lo) and bit 32+l
+            // (cnt_hi) of each lane word over the warp's 32 entries
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 if (__ballot_sync(kFull, x.w[i] != 0) == 0) continue;
-#pragma unroll 8
-                for (int bb = 0; bb < 64; ++bb) {
-                    const uint32_t c = __popc(__ballot_sync(kFull, (x.w[i] >> bb) & 1ULL));
-                    if ((uint32_t)(bb & 31) == lane) cnt[i][bb >> 5] += c;
+                const uint32_t lo = (uint32_t)x.w[i], hi = (uint32_t)(x.w[i] >> 32);
+#pragma unroll
+                for (int bb = 0; bb < 32; ++bb) {
+                    const uint32_t c0 = __popc(__ballot_sync(kFull, (lo >> bb) & 1u));
+                    const uint32_t c1 = __popc(__ballot_sync(kFull, (hi >> bb) & 1u));
+                    if ((uint32_t)bb == lane) {
+                        cnt_lo[i] += c0;
+                        cnt_hi[i] += c1;
+                    }
                 }
             }
         }
@@ -424,8 +505,8 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
     if (count_lanes) {
 #pragma unroll
         for (int i = 0; i < W; ++i) {
-            if (cnt[i][0]) atomicAdd(&s_cnt[i * 64 + lane], cnt[i][0]);
-            if (cnt[i][1]) atomicAdd(&s_cnt[i * 64 + 32 + lane], cnt[i][1]);
+            if (cnt_lo[i]) atomicAdd(&s_cnt[i * 64 + lane], (unsigned long long)cnt_lo[i]);
+            if (cnt_hi[i]) atomicAdd(&s_cnt[i * 64 + 32 + lane], (unsigned long long)cnt_hi[i]);
         }
     }
 }

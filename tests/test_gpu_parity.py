@@ -95,14 +95,25 @@ def test_frontier_pins(port, pins):
         assert got.tolist() == f["ids"]
 
 
-def test_csc_is_transpose(port):
+@pytest.mark.parametrize("via", ["edges", "csr"])
+def test_csc_is_transpose(port, via):
+    """CSC = transpose (sparse.cpp:379-403) as sets per column; each in-list is
+    ordered by descending out-degree of the in-neighbour (ties ascending id)."""
     src, dst = port.rmat_generate(10, rng_seed=3)
-    g = DeviceGraph.from_edges(src, dst, 1 << 10)
+    n = 1 << 10
+    g = DeviceGraph.from_edges(src, dst, n)
     rp, ci = g.csr()
+    if via == "csr":
+        g = DeviceGraph.from_csr(rp, ci)
     cp, ri = g.csc()
-    # transpose by the oracle: CSR of (dst, src)
-    trp, tci = port.build_csr(1 << 10, ci, H.csr_to_edges(rp, ci)[0])
-    assert (cp == trp).all() and (ri == tci).all()
+    trp, tci = port.build_csr(n, ci, H.csr_to_edges(rp, ci)[0])
+    assert (cp == trp).all()
+    deg = np.diff(rp.astype(np.int64))
+    for c in range(n):
+        seg = ri[cp[c]:cp[c + 1]].astype(np.int64)
+        assert sorted(seg.tolist()) == tci[trp[c]:trp[c + 1]].tolist()
+        want = sorted(seg.tolist(), key=lambda r: (-deg[r], r))
+        assert seg.tolist() == want
 
 
 # ---- config 1 (scale 16, 300 seeds) and direction/lane variants ----------------------------
