@@ -103,6 +103,13 @@ int mgk_graph_upload_u32(int device, uint64_t nrows, uint64_t nnz, const uint32_
  * < nrows (build_bench_graph's ContractError, bench.cpp:189-193). */
 int mgk_graph_from_edges(int device, uint64_t nrows, uint64_t nedges, const uint32_t* src,
                          const uint32_t* dst, mgk_graph** out);
+/* Generate a BASELINE.json bench graph directly on the device: the same edge
+ * set and ids as mgk_gen_rmat_csr below (same chunked mt19937_64 stream,
+ * first `target_unique` distinct non-loop edges, same seeded relabelling),
+ * with sort / dedup / CSR / CSC on the GPU. Download with
+ * mgk_graph_download_csr. (BASELINE cfg4: 1.47B edges in seconds.) */
+int mgk_graph_gen_rmat(int device, uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                       uint64_t rng_seed, uint64_t target_unique, int relabel, mgk_graph** out);
 int mgk_graph_free(mgk_graph* g);
 int mgk_graph_info(const mgk_graph* g, uint64_t* nrows, uint64_t* nnz, int* device);
 /* Copy the device CSR back (uint32; either pointer may be NULL). */

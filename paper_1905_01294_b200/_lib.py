@@ -56,6 +56,8 @@ SIGNATURES = [
     ("mgk_graph_upload", _int, [_int, _u64, _u64, _vp, _vp, C.POINTER(_vp)]),
     ("mgk_graph_upload_u32", _int, [_int, _u64, _u64, _vp, _vp, C.POINTER(_vp)]),
     ("mgk_graph_from_edges", _int, [_int, _u64, _u64, _vp, _vp, C.POINTER(_vp)]),
+    ("mgk_graph_gen_rmat", _int, [_int, _u32, _u32, C.c_double, C.c_double, C.c_double, _u64, _u64, _int,
+                                  C.POINTER(_vp)]),
     ("mgk_graph_free", _int, [_vp]),
     ("mgk_graph_info", _int, [_vp, _u64p, _u64p, C.POINTER(_int)]),
     ("mgk_graph_download_csr", _int, [_vp, _vp, _vp]),

@@ -389,6 +389,35 @@ int mgk_graph_from_edges(int device, uint64_t nrows, uint64_t nedges, const uint
     return MGK_OK;
 }
 
+int mgk_graph_gen_rmat(int device, uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                       uint64_t rng_seed, uint64_t target_unique, int relabel, mgk_graph** out) {
+    if (!out) return fail(MGK_ECONTRACT, "null argument");
+    if (scale < 1 || scale > 31) return fail(MGK_ECONTRACT, "RMAT scale must be in [1, 31]");
+    if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0 + 1e-9)
+        return fail(MGK_ECONTRACT, "RMAT quadrant probabilities must be non-negative and sum to at most 1");
+    if (relabel < 0 || relabel > 2) return fail(MGK_ECONTRACT, "relabel must be 0, 1 or 2");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MGK_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(MGK_ECONTRACT, "device %d out of range", device);
+    DeviceGuard dg(device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = device;
+    cudaError_t e = build_device_graph_generated(&h->g, scale, edge_factor, a, b, c, rng_seed, target_unique,
+                                                 relabel);
+    if (e) {
+        free_device_graph(&h->g);
+        delete h;
+        return e == cudaErrorInvalidValue ? fail(MGK_ERANGE, "generated graph exceeds uint32 indices")
+                                          : fail_cuda(e, "graph generation");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
 int mgk_graph_free(mgk_graph* h) {
     if (!h) return MGK_OK;
     DeviceGuard dg(h->g.device);

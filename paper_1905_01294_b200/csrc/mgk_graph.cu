@@ -268,6 +268,31 @@ cudaError_t exclusive_scan_u32(uint32_t* data, uint32_t n, unsigned long long* t
     return cudaSuccess;
 }
 
+cudaError_t graph_from_sorted_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt,
+                                   uint64_t m, cudaStream_t s);
+
+cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge_factor, double a,
+                                         double b, double c, uint64_t rng_seed, uint64_t target,
+                                         int relabel) {
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    uint64_t m = 0, n = 0;
+    cudaError_t e = gen_rmat_device(scale, edge_factor, a, b, c, rng_seed, target, relabel, &keys, &m, &n, s);
+    if (!e && (n >= 0xFFFFFFFFull || m >= 0xFFFFFFFFull)) e = cudaErrorInvalidValue;
+    if (!e) e = cudaMallocAsync(&alt, std::max<uint64_t>(m, 1) * 8, s);
+    if (!e) {
+        g->dg.n = (uint32_t)n;
+        e = graph_from_sorted_keys(g, keys, alt, m, s);
+    }
+    if (!e) e = cudaStreamSynchronize(s);
+    if (keys) cudaFreeAsync(keys, s);
+    if (alt) cudaFreeAsync(alt, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e;
+}
+
 cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h_ci) {
     const uint32_t n = g->dg.n;
     const uint64_t m = g->dg.m;
@@ -280,6 +305,28 @@ cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
     return e;
+}
+
+// CSR + CSC + pull metadata from sorted unique (src << 32 | dst) keys; `alt`
+// is a scratch buffer of the same size. Keys are consumed (reordered).
+cudaError_t graph_from_sorted_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt,
+                                   uint64_t m, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    g->dg.m = m;
+    MGK_TRY(alloc_graph(g, n, m));
+    if (m) {
+        keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->rp, g->ci);
+        swap_halves<<<blocks_for(m), kTB, 0, s>>>(keys, m);
+        MGK_TRY(radix_sort_keys(keys, alt, m, 32 + key_bits(n), s));
+        keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
+        MGK_TRY(order_in_lists(g, keys, alt, s));
+    } else {
+        MGK_TRY(cudaMemsetAsync(g->rp, 0, (size_t)(n + 1) * 4, s));
+        MGK_TRY(cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s));
+    }
+    no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
+    MGK_TRY(cudaGetLastError());
+    return build_heavy(g, s);
 }
 
 cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const uint32_t* h_dst,
@@ -341,25 +388,7 @@ cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const
             e = cudaErrorInvalidValue;
             break;
         }
-        g->dg.m = m;
-        if ((e = alloc_graph(g, n, m))) break;
-        if (m) {
-            keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->rp, g->ci);
-        } else {
-            if ((e = cudaMemsetAsync(g->rp, 0, (size_t)(n + 1) * 4, s))) break;
-        }
-        // CSC: swap halves, sort again
-        if (m) {
-            swap_halves<<<blocks_for(m), kTB, 0, s>>>(keys, m);
-            if ((e = radix_sort_keys(keys, alt, m, 32 + key_bits(n), s))) break;
-            keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
-            if ((e = order_in_lists(g, keys, alt, s))) break;
-        } else {
-            if ((e = cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s))) break;
-        }
-        no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
-        if ((e = cudaGetLastError())) break;
-        if ((e = build_heavy(g, s))) break;
+        if ((e = graph_from_sorted_keys(g, keys, alt, m, s))) break;
         e = cudaStreamSynchronize(s);
     } while (0);
     if (keys) cudaFreeAsync(keys, s);

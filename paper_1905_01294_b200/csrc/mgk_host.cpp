@@ -27,6 +27,7 @@
 
 namespace mgk {
 void set_last_error(const std::string& msg);  // mgk_capi.cpp
+void seeded_perm(uint64_t live, uint64_t rng_seed, std::vector<uint32_t>& perm);  // mgk_gen.cu
 }
 
 namespace {
@@ -249,16 +250,9 @@ int gen_graph(uint32_t scale, uint32_t edge_factor, double a, double b, double c
         } else {
             for (uint64_t v = 0; v < ids; ++v) map[v] = (uint32_t)v;
         }
-        // seeded Fisher-Yates over the live ids
-        std::vector<uint32_t> perm(live);
-        for (uint64_t i = 0; i < live; ++i) perm[i] = (uint32_t)i;
-        std::mt19937_64 rng(splitmix64(rng_seed ^ 0x5DEECE66DULL));
-        for (uint64_t i = live; i > 1; --i) {
-            const uint64_t max = UINT64_MAX, bound = i, limit = max - max % bound;
-            uint64_t r = rng();
-            while (r >= limit) r = rng();
-            std::swap(perm[i - 1], perm[r % bound]);
-        }
+        // seeded Fisher-Yates over the live ids (shared with the device generator)
+        std::vector<uint32_t> perm;
+        mgk::seeded_perm(live, rng_seed, perm);
         par(nt, S.size(), [&](uint64_t x, uint64_t y, unsigned) {
             for (uint64_t i = x; i < y; ++i) {
                 const uint64_t s = perm[map[S[i] >> 32]], d = perm[map[S[i] & 0xFFFFFFFFu]];

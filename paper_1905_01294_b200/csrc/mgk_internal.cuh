@@ -174,6 +174,15 @@ cudaError_t ensure_lanes_ws(const Graph* g, Workspace* ws, int W);
 cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h_ci);
 cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const uint32_t* h_dst,
                                           uint64_t nedges);
+cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge_factor, double a,
+                                         double b, double c, uint64_t rng_seed, uint64_t target,
+                                         int relabel);
 void free_device_graph(Graph* g);
+
+// device R-MAT generator (mgk_gen.cu) and its host-drawn relabel permutation
+cudaError_t gen_rmat_device(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                            uint64_t rng_seed, uint64_t target, int relabel, unsigned long long** d_keys,
+                            uint64_t* m_out, uint64_t* n_out, cudaStream_t s);
+void seeded_perm(uint64_t live, uint64_t rng_seed, std::vector<uint32_t>& perm);
 
 }  // namespace mgk

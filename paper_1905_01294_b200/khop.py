@@ -129,6 +129,15 @@ class DeviceGraph:
                                                d.ctypes.data, C.byref(h)))
         return cls(h.value, node_count)
 
+    @classmethod
+    def generate(cls, spec, device: int = 0):
+        """A harness.GraphSpec bench graph generated on the device (same graph
+        as harness.gen_csr(spec), built with sort/dedup/CSR/CSC on the GPU)."""
+        h = C.c_void_p()
+        _check(_lib.lib().mgk_graph_gen_rmat(device, spec.scale, spec.edge_factor, spec.a, spec.b, spec.c,
+                                             spec.rng_seed, spec.target_unique, spec.relabel, C.byref(h)))
+        return cls(h.value)
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             _lib.lib().mgk_graph_free(self._h)

@@ -233,3 +233,25 @@ def test_frontier_ids_deep(port, g1, force):
                     assert np.array_equal(got, want), (int(s), k, mode, force)
     finally:
         g.set_tuning(Tuning())
+
+
+@pytest.mark.parametrize("spec", [
+    H.GraphSpec("a", scale=10, edge_factor=8, target_unique=0, relabel=0, rng_seed=3),
+    H.GraphSpec("b", scale=12, edge_factor=8, target_unique=20000, relabel=2, rng_seed=5),
+    H.GraphSpec("c", scale=14, edge_factor=4, target_unique=0, relabel=1, rng_seed=9),
+    H.G1,
+], ids=lambda s: s.name)
+def test_device_generator_equals_host(spec):
+    """mgk_graph_gen_rmat (GPU) builds exactly the CSR of mgk_gen_rmat_csr (host)."""
+    rp, ci = H.gen_csr(spec)
+    g = DeviceGraph.generate(spec)
+    drp, dci = g.csr()
+    assert g.nrows == len(rp) - 1
+    assert np.array_equal(drp, rp) and np.array_equal(dci, ci)
+
+
+def test_device_generator_g2(g2):
+    rp, ci, _ = g2
+    g = DeviceGraph.generate(H.G2)
+    drp, dci = g.csr()
+    assert np.array_equal(drp, rp) and np.array_equal(dci, ci)
