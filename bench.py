@@ -194,7 +194,7 @@ def hop_bytes(st: dict, h: int) -> float:
     return algo_bytes(one)
 
 
-def run_extras(g, rp, world, rank, dist, stream, flush, torch):
+def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True):
     """BASELINE.json configs[2] (cfg3: 10 seeds, k=3,6) and configs[4] (cfg5:
     65,536 seeds in 64-lane words, k=1,2,3,6; seed batches split across
     ranks), on the already-resident G2. Device-resident, CUDA-event timed, L2
@@ -206,26 +206,43 @@ def run_extras(g, rp, world, rank, dist, stream, flush, torch):
     sp = stream.cuda_stream
     pk, _ = peaks()
     master = H.pick_seeds(rp, 65536, 1)
-    plans = [("cfg3", master[:10], (3, 6), 3), ("cfg5", master, (1, 2, 3, 6), 1)]
-    for name, seeds_all, ks, reps in plans:
-        per = (len(seeds_all) + world - 1) // world if name == "cfg5" else len(seeds_all)
-        seeds = seeds_all[rank * per:(rank + 1) * per] if name == "cfg5" else seeds_all
+    plans = [("cfg3", g, master[:10], (3, 6), 3, False), ("cfg5", g, master, (1, 2, 3, 6), 1, True)]
+    if with_cfg4:
+        # configs[3]: G4 (2^26 ids, 1.47B edges) generated on each rank's GPU
+        from paper_1905_01294_b200 import DeviceGraph
+        t = time.time()
+        g4 = DeviceGraph.generate(H.G4, device=torch.cuda.current_device())
+        rp4, _ = g4.csr()
+        m4 = H.pick_seeds(rp4, 300, 1)
+        log(f"[rank {rank}] G4: n={g4.nrows} m={g4.nnz} built on the GPU in {time.time() - t:.1f}s")
+        plans.append(("cfg4", g4, m4, (1, 2), 3, True))
+        plans.append(("cfg4", g4, m4[:10], (3, 6), 3, True))
+    for name, gg, seeds_all, ks, reps, split in plans:
+        per = (len(seeds_all) + world - 1) // world if split else len(seeds_all)
+        seeds = seeds_all[rank * per:(rank + 1) * per] if split else seeds_all
+        if len(seeds) == 0:
+            seeds = seeds_all[:1]
         d_seeds = torch.from_numpy(np.ascontiguousarray(seeds).astype(np.int32)).cuda()
         d_counts = torch.zeros(len(seeds), dtype=torch.int64, device="cuda")
-        sec = {"seeds": int(len(seeds_all)), "seeds_per_rank": int(len(seeds)), "k": {}}
+        sec = out.get(name) or {"seeds": {}, "seeds_per_rank": {}, "k": {}}
+        if name == "cfg4":
+            sec["graph"] = {"n": int(gg.nrows), "m": int(gg.nnz), "ids": "2^26 renumbered",
+                            "rmat": [0.57, 0.19, 0.19, 0.05], "built": "on the GPU (mgk_graph_gen_rmat)"}
         for k in ks:
-            k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+            sec["seeds"][str(k)] = int(len(seeds_all))
+            sec["seeds_per_rank"][str(k)] = int(len(seeds))
+            k_hop_count_device(gg, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
             times = []
             for _ in range(reps):
                 flush.fill_(1)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+                k_hop_count_device(gg, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 times.append(e0.elapsed_time(e1))
             ms = float(np.median(times))
-            st = device_stats(g, sp)
+            st = device_stats(gg, sp)
             if world > 1:
                 t = torch.tensor([ms], dtype=torch.float64, device="cuda")
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -240,7 +257,8 @@ def run_extras(g, rp, world, rank, dist, stream, flush, torch):
                 hops.append({"hop": h, "dir": "pull" if L["pull_runs"] else "push", "scanned": L["scanned"],
                              "us": L["ns"] / 1e3, "algo_GBps": b / L["ns"],
                              "frac_of_peak": b / L["ns"] / pk["hbm_gbs"]})
-            sec["k"][str(k)] = {"ms": ms, "queries_per_s": len(seeds) * world / (ms / 1e3),
+            nq = len(seeds_all) if split else len(seeds) * world
+            sec["k"][str(k)] = {"ms": ms, "queries_per_s": nq / (ms / 1e3),
                                 "gteps": edges / (ms / 1e3) / 1e9, "engine": st["engine"],
                                 "lanes_per_batch": st["lanes"], "hops": hops,
                                 "count_sum": int(d_counts.sum().item())}
@@ -340,7 +358,8 @@ def run_ours(args):
         total_ms, e2e_total = float(tt[0]), float(tt[1])
 
     # BASELINE configs[2] / [4] on the same resident graph (every rank takes part)
-    extras = None if args.no_extras else run_extras(g, rp, world, rank, dist, stream, flush, torch)
+    extras = None if args.no_extras else run_extras(g, rp, world, rank, dist, stream, flush, torch,
+                                                    with_cfg4=not args.no_cfg4)
 
     if rank != 0:
         if world > 1:
@@ -494,7 +513,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lanes-words", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 / cfg5 sections")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 / cfg4 / cfg5 sections")
+    ap.add_argument("--no-cfg4", action="store_true", help="skip the 1.47B-edge cfg4 section")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
