@@ -176,6 +176,18 @@ std::vector<std::uint64_t> k_hop_count_batch(const PropertyGraph& graph,
                                              const RelationRef& relation = RelationRef::any(),
                                              TraverseMode mode = TraverseMode::Exact);
 
+/// walk_targets (execute.cpp:43-60): sorted ids whose shortest nonempty walk
+/// from `src` has length in [min, max] (visited starts empty, so `src` itself
+/// appears on a cycle) — the VarLenTraverse step of MATCH (a)-[*min..max]->(b).
+std::vector<std::uint64_t> walk_targets(const PropertyGraph& graph, std::uint64_t src,
+                                        std::uint32_t min, std::uint32_t max,
+                                        const RelationRef& relation = RelationRef::any());
+/// |walk_targets| for many sources in one device call.
+std::vector<std::uint64_t> walk_count_batch(const PropertyGraph& graph,
+                                            std::span<const std::uint64_t> sources, std::uint32_t min,
+                                            std::uint32_t max,
+                                            const RelationRef& relation = RelationRef::any());
+
 // ---- benchmark harness (bench.hpp:16-156) -------------------------------------------
 struct RmatParams {
     std::uint32_t scale = 14;

@@ -148,6 +148,18 @@ int mgk_khop_device_stats(mgk_graph* g, void* stream, mgk_stats* stats);
 int mgk_khop_frontier(mgk_graph* g, uint64_t seed, uint32_t k, int mode, uint64_t* ids,
                       uint64_t cap, uint64_t* n_out);
 
+/* walk_targets (execute.cpp:43-60, the Cypher VarLenTraverse step behind
+ * MATCH (a)-[*min..max]->(b)): the same masked traversal but with the visited
+ * set starting EMPTY, so the source itself is reached again on a cycle;
+ * counts / sorted ids of the union of levels min..max. Window checks follow
+ * the Cypher parser (cypher.cpp:356-392): "hop minimum must be at least 1",
+ * "hop count {h} exceeds the cap of 32", "hop maximum {max} is less than
+ * minimum {min}"; an unallocated source is MGK_ECONTRACT. */
+int mgk_walk_count(mgk_graph* g, const uint64_t* sources, uint64_t nsources, uint32_t min_hops,
+                   uint32_t max_hops, int engine, uint64_t* counts);
+int mgk_walk_targets(mgk_graph* g, uint64_t source, uint32_t min_hops, uint32_t max_hops, uint64_t* ids,
+                     uint64_t cap, uint64_t* n_out);
+
 /* Engine tuning knobs (0 keeps the default). alpha/beta: Beamer-style
  * push->pull when frontier edges * alpha > unexplored in-edges, pull->push
  * when frontier * beta < n (alpha for SINGLE, alpha_lanes for LANES).

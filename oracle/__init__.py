@@ -64,6 +64,9 @@ class Port:
         L.orc_khop_frontier.restype = C.c_uint64
         L.orc_khop_frontier.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_int,
                                         C.c_void_p]
+        L.orc_walk_targets.restype = C.c_uint64
+        L.orc_walk_targets.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                       C.c_void_p]
         L.orc_khop_work.restype = C.c_uint64
         L.orc_khop_work.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_void_p,
                                     C.POINTER(C.c_uint32)]
@@ -108,6 +111,13 @@ class Port:
     def khop_count(self, row_ptr, col_idx, seed, k, mode):
         n = len(row_ptr) - 1
         return int(self.lib.orc_khop_frontier(n, row_ptr, _c64(col_idx), seed, k, mode, None))
+
+    def walk_targets(self, row_ptr, col_idx, src, lo, hi):
+        """execute.cpp:43-60: sorted union of walk levels lo..hi (nothing pre-visited)."""
+        n = len(row_ptr) - 1
+        out = np.zeros(max(n, 1), np.uint64)
+        cnt = self.lib.orc_walk_targets(n, row_ptr, _c64(col_idx), src, lo, hi, out.ctypes.data)
+        return out[:cnt].copy()
 
     def khop_work(self, row_ptr, col_idx, seed, k):
         """(E(s,k), level sizes [|F_0|..|F_L|]) — SURVEY.md §8(d)."""
@@ -174,6 +184,7 @@ class Ref:
         L.ref_k_hop_count_many.argtypes = [vp, vp, u64, u32, C.c_int, C.c_int, vp,
                                            C.POINTER(C.c_double)]
         L.ref_pick_seeds.argtypes = [vp, u64, u64, vp]
+        L.ref_cypher.argtypes = [vp, C.c_char_p, C.c_char_p, u64, C.POINTER(u64)]
         L.ref_rmat_generate.argtypes = [u32, u32, C.c_double, C.c_double, C.c_double, C.c_double,
                                         u64, vp, vp, C.POINTER(u64)]
         L.ref_bfs_oracle_new.restype = vp
@@ -272,6 +283,14 @@ class RefGraph:
         out = np.zeros(max(n, 1), np.uint64)
         self.ref._check(self.ref.lib.ref_pick_seeds(self.h, n, rng_seed, out.ctypes.data))
         return out[:n].copy()
+
+    def cypher(self, text):
+        """The reference's own executor: the result table's wire text."""
+        n = C.c_uint64()
+        self.ref._check(self.ref.lib.ref_cypher(self.h, text.encode(), None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.ref._check(self.ref.lib.ref_cypher(self.h, text.encode(), buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
 
 
 class RefBfs:

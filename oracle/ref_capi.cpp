@@ -22,6 +22,8 @@
 #include <vector>
 
 #include "matgraph/bench.hpp"
+#include "matgraph/cypher.hpp"
+#include "matgraph/plan.hpp"
 #include "matgraph/error.hpp"
 #include "matgraph/execute.hpp"
 #include "matgraph/graph.hpp"
@@ -168,6 +170,24 @@ int ref_k_hop_count_many(void* g, const uint64_t* seeds, uint64_t nseeds, uint32
     *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (status != 0) g_err = first_err;
     return status;
+}
+
+// Runs a Cypher query through the reference's parse -> plan -> execute
+// (proj/core/src/cypher.cpp, plan.cpp, execute.cpp:342-345) and returns the
+// table's wire text (to_string). Used to pin walk_targets (VarLenTraverse).
+int ref_cypher(void* g, const char* text, char* out, uint64_t cap, uint64_t* n) {
+    try {
+        auto& graph = *static_cast<PropertyGraph*>(g);
+        const std::string t = matgraph_ref::to_string(
+            matgraph_ref::execute(matgraph_ref::plan(matgraph_ref::parse(text), graph), graph));
+        *n = t.size();
+        if (out && cap) {
+            const uint64_t k = std::min<uint64_t>(cap - 1, t.size());
+            std::memcpy(out, t.data(), k);
+            out[k] = 0;
+        }
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
 }
 
 // ---- harness pieces -------------------------------------------------------------

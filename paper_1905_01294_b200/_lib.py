@@ -68,6 +68,8 @@ SIGNATURES = [
     ("mgk_khop_count_device", _int, [_vp, _vp, _u64, _u32, _int, _int, _vp, _vp]),
     ("mgk_khop_device_stats", _int, [_vp, _vp, C.POINTER(MgkStats)]),
     ("mgk_khop_frontier", _int, [_vp, _u64, _u32, _int, _vp, _u64, _u64p]),
+    ("mgk_walk_count", _int, [_vp, _vp, _u64, _u32, _u32, _int, _vp]),
+    ("mgk_walk_targets", _int, [_vp, _u64, _u32, _u32, _vp, _u64, _u64p]),
     ("mgk_graph_set_tuning", _int, [_vp, C.POINTER(MgkTuning)]),
     ("mgk_graph_get_tuning", _int, [_vp, C.POINTER(MgkTuning)]),
     ("mgk_last_error", C.c_char_p, []),

@@ -269,6 +269,27 @@ std::vector<std::uint64_t> k_hop_count_batch(const PropertyGraph& graph,
     return counts;
 }
 
+std::vector<std::uint64_t> walk_targets(const PropertyGraph& graph, std::uint64_t src, std::uint32_t min,
+                                        std::uint32_t max, const RelationRef& relation) {
+    const DeviceMatrix& dm = graph.device_matrix(relation);
+    std::vector<std::uint64_t> ids(graph.capacity());
+    std::uint64_t n = 0;
+    const int rc = mgk_walk_targets(dm.handle(), src, min, max, ids.data(), ids.size(), &n);
+    if (rc != MGK_OK) throw_mgk(rc);
+    ids.resize(n);
+    return ids;
+}
+
+std::vector<std::uint64_t> walk_count_batch(const PropertyGraph& graph, std::span<const std::uint64_t> sources,
+                                            std::uint32_t min, std::uint32_t max, const RelationRef& relation) {
+    const DeviceMatrix& dm = graph.device_matrix(relation);
+    std::vector<std::uint64_t> counts(sources.size());
+    const int rc = mgk_walk_count(dm.handle(), sources.data(), sources.size(), min, max, MGK_ENGINE_AUTO,
+                                  counts.data());
+    if (rc != MGK_OK) throw_mgk(rc);
+    return counts;
+}
+
 // ---- harness -----------------------------------------------------------------------------
 void RmatParams::validate() const {  // bench.cpp:96-105
     if (scale > 24) throw ContractError(fmt("RMAT scale %u exceeds the cap of 24", scale));

@@ -99,6 +99,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->fr_pop);
     cudaFree(ws->fr_dirs);
     cudaFree(ws->fr_ctl);
+    cudaFree(ws->fr_snap);
     cudaFree(ws->lv);
     cudaFree(ws->lf[0]);
     cudaFree(ws->lf[1]);
@@ -168,10 +169,20 @@ int check_query(const Graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t
     return MGK_OK;
 }
 
+// The hop window a call counts: k_hop exact = [k, k], cumulative = [1, k]
+// (seed pre-visited, execute.cpp:357-370); walk_targets = [min, max] with the
+// visited set starting empty (execute.cpp:43-60).
+struct Span {
+    uint32_t lo, hi;
+    bool seed_visited;
+};
+Span span_of(uint32_t k, int mode) { return Span{mode == MGK_EXACT ? k : 1u, k, true}; }
+
 cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_t nseeds,
-                       uint32_t k, int mode, int engine, unsigned long long* d_counts,
+                       Span span, int engine, unsigned long long* d_counts,
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
                        int* W_out, bool keep_result = false) {
+    const uint32_t k = span.hi;
     cudaError_t e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
     if (e) return e;
     if (nseeds == 0) return cudaSuccess;
@@ -181,7 +192,8 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.d_seeds = d_seeds;
     L.nseeds = nseeds;
     L.k = k;
-    L.mode = mode;
+    L.min_hop = span.lo;
+    L.seed_visited = span.seed_visited ? 1u : 0u;
     L.d_counts = d_counts;
     L.stream = stream;
     L.tuning = g->tuning;
@@ -495,15 +507,15 @@ int mgk_graph_get_tuning(const mgk_graph* h, mgk_tuning* t) {
     return MGK_OK;
 }
 
-int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
-                      int engine, uint64_t* counts, mgk_stats* stats) {
-    if (!h) return fail(MGK_ECONTRACT, "null graph");
-    if (nseeds && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
-    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
-    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+}  // extern "C"
+
+namespace mgk {
+namespace {
+// Counts of a batch of seeds over the hop window `span` (host buffers).
+int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, int engine,
+               uint64_t* counts, mgk_stats* stats, const char* what) {
     Graph* g = &h->g;
-    int rc = check_query(g, seeds, nseeds, k);
-    if (rc) return rc;
+    int rc = MGK_OK;
     if (nseeds >= 0xFFFFFFFFull) return fail(MGK_ECONTRACT, "too many seeds");
     DeviceGuard dg(g->device);
     Workspace* ws = acquire_ws(g, &rc);
@@ -522,7 +534,7 @@ int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint
     do {
         if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
         if ((e = cudaEventRecord(ws->ev0, ws->stream))) break;
-        if ((e = run_engine(g, ws, ws->d_seeds, nseeds, k, mode, engine, ws->d_counts, ws->stream,
+        if ((e = run_engine(g, ws, ws->d_seeds, nseeds, span, engine, ws->d_counts, ws->stream,
                             &grid, &block, &used, &W)))
             break;
         if ((e = cudaEventRecord(ws->ev1, ws->stream))) break;
@@ -538,7 +550,44 @@ int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint
         }
     } while (0);
     release_ws(g, ws);
-    return e ? fail_cuda(e, "k-hop count") : MGK_OK;
+    return e ? fail_cuda(e, what) : MGK_OK;
+}
+
+// walk_targets' window checks, with the Cypher parser's messages (cypher.cpp:356-392)
+int check_walk(const Graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t lo, uint32_t hi) {
+    for (uint64_t i = 0; i < nseeds; ++i)
+        if (seeds[i] >= g->dg.n)
+            return fail(MGK_ECONTRACT, "walk source %llu is not an allocated node", (unsigned long long)seeds[i]);
+    if (lo < 1) return fail(MGK_ECONTRACT, "hop minimum must be at least 1");
+    if (hi > MGK_MAX_HOPS) return fail(MGK_ECONTRACT, "hop count %u exceeds the cap of %d", hi, MGK_MAX_HOPS);
+    if (hi < lo) return fail(MGK_ECONTRACT, "hop maximum %u is less than minimum %u", hi, lo);
+    return MGK_OK;
+}
+}  // namespace
+}  // namespace mgk
+
+extern "C" {
+
+int mgk_khop_count_ex(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
+                      int engine, uint64_t* counts, mgk_stats* stats) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (nseeds && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+    int rc = check_query(&h->g, seeds, nseeds, k);
+    if (rc) return rc;
+    return count_impl(h, seeds, nseeds, span_of(k, mode), engine, counts, stats, "k-hop count");
+}
+
+int mgk_walk_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t min_hops,
+                   uint32_t max_hops, int engine, uint64_t* counts) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (nseeds && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
+    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+    int rc = check_walk(&h->g, seeds, nseeds, min_hops, max_hops);
+    if (rc) return rc;
+    return count_impl(h, seeds, nseeds, Span{min_hops, max_hops, false}, engine, counts, nullptr,
+                      "walk count");
 }
 
 int mgk_khop_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
@@ -576,7 +625,7 @@ int mgk_khop_count_device(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds
     }
     uint32_t grid = 0, block = 0;
     int used = 0, W = 0;
-    cudaError_t e = run_engine(g, ws, d_seeds, nseeds, k, mode, engine,
+    cudaError_t e = run_engine(g, ws, d_seeds, nseeds, span_of(k, mode), engine,
                                reinterpret_cast<unsigned long long*>(d_counts), s, &grid, &block, &used, &W);
     ws->misc_engine = used;
     ws->misc_W = W;
@@ -604,13 +653,14 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     return MGK_OK;
 }
 
-int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_t* ids, uint64_t cap,
-                      uint64_t* n_out) {
-    if (!h || !n_out || (cap && !ids)) return fail(MGK_ECONTRACT, "null argument");
-    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+}  // extern "C"
+
+namespace mgk {
+namespace {
+int ids_impl(mgk_graph* h, uint64_t seed, Span span, uint64_t* ids, uint64_t cap, uint64_t* n_out,
+             const char* what) {
     Graph* g = &h->g;
-    int rc = check_query(g, &seed, 1, k);
-    if (rc) return rc;
+    int rc = MGK_OK;
     DeviceGuard dg(g->device);
     Workspace* ws = acquire_ws(g, &rc);
     if (!ws) return rc;
@@ -619,17 +669,17 @@ int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_
     unsigned long long* d_n = nullptr;
     do {
         if (e) break;
-        uint32_t s32 = (uint32_t)seed;
-        reinterpret_cast<uint32_t*>(ws->h_pinned)[0] = s32;
+        reinterpret_cast<uint32_t*>(ws->h_pinned)[0] = (uint32_t)seed;
         if ((e = cudaMemcpyAsync(ws->d_seeds, ws->h_pinned, 4, cudaMemcpyHostToDevice, ws->stream))) break;
         uint32_t grid = 0, block = 0;
         int used = 0, W = 0;
-        if ((e = run_engine(g, ws, ws->d_seeds, 1, k, mode, MGK_ENGINE_SINGLE, ws->d_counts, ws->stream,
-                            &grid, &block, &used, &W, true)))
+        if ((e = run_engine(g, ws, ws->d_seeds, 1, span, MGK_ENGINE_SINGLE, ws->d_counts, ws->stream, &grid,
+                            &block, &used, &W, true)))
             break;
         if ((e = cudaMalloc(&d_ids, (size_t)std::max<uint32_t>(g->dg.n, 1) * 8))) break;
         if ((e = cudaMalloc(&d_n, 8))) break;
-        if ((e = single_result_ids(g, ws, k, mode, s32, d_ids, d_n, ws->stream))) break;
+        if ((e = single_result_ids(g, ws, span.lo, span.seed_visited, (uint32_t)seed, d_ids, d_n, ws->stream)))
+            break;
         unsigned long long n = 0;
         if ((e = cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, ws->stream))) break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;
@@ -640,7 +690,28 @@ int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_
     cudaFree(d_ids);
     cudaFree(d_n);
     release_ws(g, ws);
-    return e ? fail_cuda(e, "k-hop frontier") : MGK_OK;
+    return e ? fail_cuda(e, what) : MGK_OK;
+}
+}  // namespace
+}  // namespace mgk
+
+extern "C" {
+
+int mgk_khop_frontier(mgk_graph* h, uint64_t seed, uint32_t k, int mode, uint64_t* ids, uint64_t cap,
+                      uint64_t* n_out) {
+    if (!h || !n_out || (cap && !ids)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    int rc = check_query(&h->g, &seed, 1, k);
+    if (rc) return rc;
+    return ids_impl(h, seed, span_of(k, mode), ids, cap, n_out, "k-hop frontier");
+}
+
+int mgk_walk_targets(mgk_graph* h, uint64_t seed, uint32_t min_hops, uint32_t max_hops, uint64_t* ids,
+                     uint64_t cap, uint64_t* n_out) {
+    if (!h || !n_out || (cap && !ids)) return fail(MGK_ECONTRACT, "null argument");
+    int rc = check_walk(&h->g, &seed, 1, min_hops, max_hops);
+    if (rc) return rc;
+    return ids_impl(h, seed, Span{min_hops, max_hops, false}, ids, cap, n_out, "walk targets");
 }
 
 }  // extern "C"

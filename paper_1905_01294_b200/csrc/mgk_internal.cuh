@@ -89,6 +89,7 @@ struct Workspace {
     unsigned long long* fr_pop = nullptr;
     uint8_t* fr_dirs = nullptr;
     void* fr_ctl = nullptr;
+    uint32_t* fr_snap = nullptr;  // keep_result: slot 0's visited bitmap after hop min-1
     // lanes engine (allocated lazily for the widest W used)
     int lanes_words = 0;
     unsigned long long* lv = nullptr;     // V  [n * W]
@@ -139,8 +140,9 @@ struct Launch {
     Workspace* ws;
     const uint32_t* d_seeds;
     uint64_t nseeds;
-    uint32_t k;
-    int mode;
+    uint32_t k;             // max hop
+    uint32_t min_hop;       // count hops [min_hop, k]
+    uint32_t seed_visited;  // 1 for k_hop_*, 0 for walk_targets
     unsigned long long* d_counts;
     cudaStream_t stream;
     Tuning tuning;
@@ -158,9 +160,11 @@ cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, voi
 
 cudaError_t launch_single(Launch& L);
 cudaError_t launch_lanes(Launch& L);
-// Compacts the final result bitmap of the last single-seed run into sorted ids.
-cudaError_t single_result_ids(const Graph* g, Workspace* ws, uint32_t k, int mode, uint32_t seed,
-                              unsigned long long* d_ids, unsigned long long* d_n, cudaStream_t s);
+// Sorted ids of the last single-seed keep_result run: visited \ (visited
+// after hop min-1), i.e. the union of the levels in the window.
+cudaError_t single_result_ids(const Graph* g, Workspace* ws, uint32_t min_hop, bool seed_visited,
+                              uint32_t seed, unsigned long long* d_ids, unsigned long long* d_n,
+                              cudaStream_t s);
 
 // In-place exclusive scan of data[0..n) (data must hold n+1 entries); *total
 // (device) receives the sum.

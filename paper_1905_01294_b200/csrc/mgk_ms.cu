@@ -35,8 +35,9 @@ struct MSParams {
     DevGraph g;
     const uint32_t* seeds;
     uint64_t nseeds;
-    uint32_t k;
-    int mode;
+    uint32_t k;             // max hop
+    uint32_t min_hop;       // answer = sum over hops [min_hop, k] of each lane's |F_h|
+    uint32_t seed_visited;  // 0: walk_targets semantics (the seed is not pre-visited)
     unsigned long long* counts;
     unsigned long long* V;
     unsigned long long* F0;
@@ -421,7 +422,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
 // ---- finalize: V |= F', lane counts, next-hop items, clear old frontier -------
 template <int W>
 __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR,
-                               unsigned long long* Fn, bool touched_set, bool want_items,
+                               unsigned long long* Fn, bool mark_visited, bool touched_set, bool want_items,
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
@@ -451,7 +452,7 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             uint32_t pc = 0;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
-                v.w[i] |= x.w[i];
+                if (mark_visited) v.w[i] |= x.w[i];
                 act.w[i] |= x.w[i];
                 pc += __popcll(x.w[i]);
             }
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     acc.zero();
     Stage<kStageCap> st{s_stage[threadIdx.x >> 5], 0};
     const uint64_t nbatches = (P.nseeds + LB - 1) / LB;
-    const bool cumulative = P.mode == MGK_CUMULATIVE;
+
 
     for (uint64_t bt = 0; bt < nbatches; ++bt) {
         const uint32_t lanes = (uint32_t)min((uint64_t)LB, P.nseeds - bt * LB);
@@ -572,7 +573,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         bool pull = P.force_dir == 2;
         if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
         __syncthreads();
-        finalize_phase<W>(P, P.R0, nR, P.F0, true, !pull, P.items0, &P.qctl[0].nfound, false,
+        finalize_phase<W>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull, P.items0, &P.qctl[0].nfound, false,
                           s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
         acc.pairs = 0;  // the seeds themselves are never counted
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
@@ -624,12 +625,12 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 pull = (unsigned long long)nR * P.beta >= g.n;
             }
             const bool last = hop == P.k || nR == 0;
-            const bool count_lanes = cumulative || hop == P.k;
+            const bool count_lanes = hop >= P.min_hop;
             // ---- finalize -------------------------------------------------------------
             if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
-            finalize_phase<W>(P, Rn, nR, Fn, !was_pull, !last && !pull, items_of(P, nxt),
+            finalize_phase<W>(P, Rn, nR, Fn, true, !was_pull, !last && !pull, items_of(P, nxt),
                               &qn->nfound, count_lanes, s_cnt, P.active + nxt * W, clog_used,
                               acc, st, warp_gid, nwarps);
             clear_list<W>(Rc, nR_prev, Fc, gtid, nthreads);
@@ -647,11 +648,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         // ---- answers ------------------------------------------------------------------
         if (gtid < lanes) {
             unsigned long long r = 0;
-            if (cumulative) {
-                for (uint32_t h = 1; h <= P.k; ++h) r += P.lane_cnt[h * LB + gtid];
-            } else {
-                r = P.lane_cnt[P.k * LB + gtid];
-            }
+            for (uint32_t h = P.min_hop; h <= P.k; ++h) r += P.lane_cnt[h * LB + gtid];
             P.counts[bt * LB + gtid] = r;
         }
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
@@ -690,7 +687,8 @@ cudaError_t launch_w(Launch& L) {
     P.seeds = L.d_seeds;
     P.nseeds = L.nseeds;
     P.k = L.k;
-    P.mode = L.mode;
+    P.min_hop = L.min_hop;
+    P.seed_visited = L.seed_visited;
     P.counts = L.d_counts;
     P.V = ws->lv;
     P.F0 = ws->lf[0];

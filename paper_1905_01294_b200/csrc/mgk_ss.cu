@@ -57,8 +57,9 @@ struct FRParams {
     DevGraph g;
     const uint32_t* seeds;  // this group's seeds (ns of them)
     uint32_t ns;
-    uint32_t k;
-    int mode;
+    uint32_t k;          // max hop
+    uint32_t min_hop;    // answer = sum of |F_h| for h in [min_hop, k]
+    uint32_t seed_visited;  // 1: k_hop_* (seed pre-visited); 0: walk_targets (visited starts empty)
     unsigned long long* counts;  // this group's answers
     uint32_t S;
     uint32_t rs;   // bitmap row stride in words (nwords rounded up to 32: 128-B rows)
@@ -82,6 +83,7 @@ struct FRParams {
     unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
+    uint32_t* snap;  // keep_result: slot 0's visited bitmap after hop min_hop - 1
     uint32_t quota;  // per-seed log entries before the seed is cleared densely
     uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
 };
@@ -498,11 +500,11 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
         const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
         if (lane == 0) {
             const uint32_t bit = 1u << (s & 31);
-            P.V[(size_t)slot * P.rs + (s >> 5)] = bit;
+            if (P.seed_visited) P.V[(size_t)slot * P.rs + (s >> 5)] = bit;
             P.Fb[(size_t)slot * P.rs + (s >> 5)] = bit;
             P.cnt[slot] = 1;
             P.mfs[slot] = deg;
-            P.mex[slot] = __ldg(g.cp + s + 1) - __ldg(g.cp + s);
+            P.mex[slot] = P.seed_visited ? __ldg(g.cp + s + 1) - __ldg(g.cp + s) : 0;
             P.logbuf[slot] = ((unsigned long long)slot << 32) | s;  // log slots [0, ns)
         }
         emit_row_items(P, 0, lane == 0, slot, b, deg);
@@ -514,6 +516,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     grid_barrier(P.bar);
     if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds
 
+    bool snapped = false;
     uint32_t hop = 1;
     for (; hop <= P.k; ++hop) {
         const bool last = hop == P.k;
@@ -587,7 +590,14 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
         grid_barrier(P.bar);
         if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
         if (ld_volatile(&P.ctl->found[hop]) == 0) break;
+        if (P.keep_result && hop + 1 == P.min_hop) {  // visited up to hop min-1
+            for (uint32_t w = gtid; w < nw; w += nthreads) P.snap[w] = P.V[w];
+            snapped = true;
+            grid_barrier(P.bar);
+        }
     }
+    if (P.keep_result && P.min_hop >= 2 && !snapped)  // stopped before hop min-1: nothing in the window
+        for (uint32_t w = gtid; w < nw; w += nthreads) P.snap[w] = P.V[w];
     if (gtid == 0) {
         P.ctl->last_hop = hop > P.k ? P.k : hop;
         P.ctl->last_which = (hop > P.k) ? (P.k % 3) : 3ULL;
@@ -694,16 +704,17 @@ __global__ void __launch_bounds__(kFinBlock) fr_finish(FRParams P) {
     if (!s_last) return;
     __threadfence();
     for (uint32_t slot = threadIdx.x; slot < ns; slot += kFinBlock) {
-        unsigned long long before = 0;  // vertices visited before the last hop (seed incl.)
-        for (uint32_t h = 0; h < P.k; ++h) before += ld_cg(&P.cnt[h * S + slot]);
-        const unsigned long long lastc = ld_cg(&P.cnt[P.k * S + slot]);
-        unsigned long long r;
-        if (ld_cg(&P.logcnt[slot]) != 0) {
-            const unsigned long long total = ld_cg(&P.pop[slot]);
-            r = P.mode == MGK_CUMULATIVE ? total - 1 : total - before;
-        } else {
-            r = P.mode == MGK_CUMULATIVE ? before - 1 + lastc : lastc;
+        // cnt[0] = 1 (the seed frontier); cnt[h] = |F_h| for the hops counted
+        // by discovery; a flagged seed's last hop is popcount(V) minus the rest
+        unsigned long long before = 0, r = 0;  // discoveries at hops 1..k-1
+        for (uint32_t h = 1; h < P.k; ++h) {
+            const unsigned long long c = ld_cg(&P.cnt[h * S + slot]);
+            before += c;
+            if (h >= P.min_hop) r += c;
         }
+        unsigned long long lastc = ld_cg(&P.cnt[P.k * S + slot]);
+        if (ld_cg(&P.logcnt[slot]) != 0) lastc = ld_cg(&P.pop[slot]) - before - P.seed_visited;
+        if (P.k >= P.min_hop) r += lastc;
         P.counts[slot] = r;
         for (uint32_t h = 0; h <= P.k; ++h) {
             P.cnt[h * S + slot] = 0;
@@ -733,19 +744,20 @@ __global__ void clear_slot0(uint32_t* V, uint32_t* Fb, uint32_t S, uint32_t nw, 
     }
 }
 
-__global__ void popc_words(const uint32_t* bits, uint32_t nwords, uint32_t drop, uint32_t* out) {
+__global__ void popc_words(const uint32_t* bits, const uint32_t* sub, uint32_t nwords, uint32_t drop,
+                           uint32_t* out) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwords) return;
-    uint32_t x = bits[w];
+    uint32_t x = bits[w] & (sub ? ~sub[w] : kFull);
     if ((drop >> 5) == w) x &= ~(1u << (drop & 31));
     out[w] = __popc(x);
 }
 
-__global__ void scatter_ids(const uint32_t* bits, uint32_t nwords, uint32_t drop,
+__global__ void scatter_ids(const uint32_t* bits, const uint32_t* sub, uint32_t nwords, uint32_t drop,
                             const uint32_t* offs, unsigned long long* ids) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwords) return;
-    uint32_t x = bits[w];
+    uint32_t x = bits[w] & (sub ? ~sub[w] : kFull);
     if ((drop >> 5) == w) x &= ~(1u << (drop & 31));
     uint32_t o = offs[w];
     while (x) {
@@ -802,6 +814,7 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     if ((e = cudaMemset(ws->fr_pop, 0, (size_t)S * 8))) return e;
     if ((e = cudaMalloc(&ws->fr_dirs, (size_t)2 * S))) return e;
     if ((e = cudaMalloc(&ws->fr_ctl, sizeof(FRCtl)))) return e;
+    if ((e = cudaMalloc(&ws->fr_snap, (size_t)row_stride(g) * 4))) return e;
     if ((e = cudaMemset(ws->fr_cnt, 0, cs * 4))) return e;
     if ((e = cudaMemset(ws->fr_mfs, 0, cs * 8))) return e;
     if ((e = cudaMemset(ws->fr_logcnt, 0, (size_t)S * 4))) return e;
@@ -837,7 +850,8 @@ cudaError_t launch_single(Launch& L) {
     FRParams P;
     P.g = gr->dg;
     P.k = L.k;
-    P.mode = L.mode;
+    P.min_hop = L.min_hop;
+    P.seed_visited = L.seed_visited;
     P.V = ws->fr_V;
     P.Fb = ws->fr_Fb;
     P.items0 = ws->fr_items[0];
@@ -862,6 +876,7 @@ cudaError_t launch_single(Launch& L) {
     P.force_dir = L.tuning.force_dir;
     P.quota = ws->fr_quota;
     P.keep_result = L.keep_result ? 1u : 0u;
+    P.snap = ws->fr_snap;
     // bitmaps are laid out [S_alloc][rs] ([3][S_alloc][rs] for Fb): S is the
     // allocated slot count (the stride); a group holds up to S seeds
     P.S = ws->fr_slots;
@@ -881,35 +896,23 @@ cudaError_t launch_single(Launch& L) {
     return cudaSuccess;
 }
 
-cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t k, int mode, uint32_t seed,
-                              unsigned long long* d_ids, unsigned long long* d_n, cudaStream_t s) {
-    (void)k;
+cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t min_hop, bool seed_visited,
+                              uint32_t seed, unsigned long long* d_ids, unsigned long long* d_n,
+                              cudaStream_t s) {
     const DevGraph& g = gr->dg;
     const uint32_t nw = g.nwords;
-    FRCtl* ctl = reinterpret_cast<FRCtl*>(ws->fr_ctl);
-    unsigned long long which = 0;
-    cudaError_t e = cudaMemcpyAsync(&which, &ctl->last_which, 8, cudaMemcpyDeviceToHost, s);
-    if (e) return e;
-    if ((e = cudaStreamSynchronize(s))) return e;
-    const uint32_t* bits = nullptr;
-    uint32_t drop = 0xFFFFFFFFu;
-    if (mode == MGK_CUMULATIVE) {
-        bits = ws->fr_V;  // slot 0
-        drop = seed;
-    } else if (which < 3) {
-        bits = ws->fr_Fb + (size_t)which * ws->fr_slots * row_stride(g);  // slot 0 of bitmap `which`
-    }
-    if (bits) {
-        uint32_t* offs = nullptr;
-        if ((e = cudaMallocAsync(&offs, (size_t)(nw + 1) * 4, s))) return e;
-        const int tb = 256, nb = (int)((nw + tb - 1) / tb);
-        popc_words<<<nb, tb, 0, s>>>(bits, nw, drop, offs);
-        if ((e = exclusive_scan_u32(offs, nw, d_n, s))) return e;
-        scatter_ids<<<nb, tb, 0, s>>>(bits, nw, drop, offs, d_ids);
-        cudaFreeAsync(offs, s);
-    } else {
-        if ((e = cudaMemsetAsync(d_n, 0, 8, s))) return e;
-    }
+    // window [min_hop, k] = visited \ visited-after-hop-(min_hop - 1); for
+    // min_hop = 1 that is visited minus the pre-visited seed (if any)
+    const uint32_t* sub = min_hop >= 2 ? ws->fr_snap : nullptr;
+    const uint32_t drop = (min_hop < 2 && seed_visited) ? seed : 0xFFFFFFFFu;
+    uint32_t* offs = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync(&offs, (size_t)(nw + 1) * 4, s))) return e;
+    const int tb = 256, nb = (int)((nw + tb - 1) / tb);
+    popc_words<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, offs);
+    if ((e = exclusive_scan_u32(offs, nw, d_n, s))) return e;
+    scatter_ids<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, offs, d_ids);
+    cudaFreeAsync(offs, s);
     clear_slot0<<<148, 256, 0, s>>>(ws->fr_V, ws->fr_Fb, ws->fr_slots, nw, row_stride(g));
     return cudaGetLastError();
 }

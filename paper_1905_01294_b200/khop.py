@@ -235,6 +235,29 @@ def k_hop_count_batch(graph: DeviceGraph, seeds, k: int, mode=TraverseMode.Exact
     return (counts, st.to_dict()) if stats else counts
 
 
+def walk_count_batch(graph: DeviceGraph, sources, min_hops: int, max_hops: int,
+                     engine: int = ENGINE_AUTO):
+    """|walk_targets(src, min, max)| per source (execute.cpp:43-60): the
+    VarLenTraverse step of MATCH (a)-[*min..max]->(b) — visited starts empty,
+    so the source itself is counted when a cycle returns to it."""
+    src = np.ascontiguousarray(sources, np.uint64)
+    counts = np.zeros(max(len(src), 1), np.uint64)
+    sp = src if len(src) else np.zeros(1, np.uint64)
+    _check(_lib.lib().mgk_walk_count(graph.handle, sp.ctypes.data, len(src), int(min_hops), int(max_hops),
+                                     int(engine), counts.ctypes.data))
+    return counts[: len(src)]
+
+
+def walk_targets(graph: DeviceGraph, source: int, min_hops: int, max_hops: int) -> np.ndarray:
+    """execute.cpp:43-60 walk_targets: sorted ids of walk levels min..max."""
+    cap = max(graph.nrows, 1)
+    ids = np.zeros(cap, np.uint64)
+    n = C.c_uint64()
+    _check(_lib.lib().mgk_walk_targets(graph.handle, int(source), int(min_hops), int(max_hops),
+                                       ids.ctypes.data, cap, C.byref(n)))
+    return ids[: n.value].copy()
+
+
 def k_hop_count_device(graph: DeviceGraph, d_seeds_ptr: int, nseeds: int, k: int, mode: int,
                        d_counts_ptr: int, stream_ptr: int = 0, engine: int = ENGINE_AUTO):
     """Device-resident batch: uint32 seeds and uint64 counts already in HBM; async on stream."""
@@ -255,5 +278,5 @@ def device_count() -> int:
 
 __all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
-           "k_hop_count_device", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "k_hop_count_device", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

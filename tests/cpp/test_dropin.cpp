@@ -5,6 +5,7 @@
 //   proj/tests/test_bench.cpp:33-349              harness pieces, oracle agreement
 //   proj/tests/acceptance/acceptance_main.cpp:53-88  c1 (20 RMAT graphs x 50 seeds)
 // `test_dropin --cpu` runs only the cases that need no GPU.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <filesystem>
@@ -103,6 +104,31 @@ GPU_TEST_CASE("a cached device matrix is dropped when new edges arrive") {
     g.create_edge(0, "R", 2);  // pending until the next read flushes it
     CHECK(k_hop_count(g, {.seed = 0, .k = 1}) == 2);
     CHECK(k_hop_count(g, {.seed = 0, .k = 2, .mode = TraverseMode::Exact}) == 1);
+}
+
+GPU_TEST_CASE("anchored variable-length walks agree with the in-process k-hop counts") {
+    // test_execute.cpp:141-173: MATCH (a {id: S})-[*k..k]->(b) WHERE b.id <> S and
+    // [*1..k] equal k_hop_count exact / cumulative; walk_targets (execute.cpp:43-60)
+    // starts with nothing visited, so S is dropped by the WHERE term.
+    PropertyGraph graphs[] = {path4(), triangle()};
+    for (PropertyGraph& g : graphs) {
+        for (std::uint64_t seed = 0; seed < g.node_count(); ++seed) {
+            for (std::uint32_t k = 1; k <= 4; ++k) {
+                auto without_seed = [&](std::vector<std::uint64_t> ids) {
+                    return std::count_if(ids.begin(), ids.end(), [&](std::uint64_t v) { return v != seed; });
+                };
+                CHECK(without_seed(walk_targets(g, seed, k, k, "R")) ==
+                      (long)k_hop_count(g, {.seed = seed, .k = k, .relation = "R", .mode = TraverseMode::Exact}));
+                CHECK(without_seed(walk_targets(g, seed, 1, k, "R")) ==
+                      (long)k_hop_count(g, {.seed = seed, .k = k, .relation = "R", .mode = TraverseMode::Cumulative}));
+            }
+        }
+    }
+    PropertyGraph tri = triangle();  // 0 -> 1 -> 2 -> 0: the source returns at hop 3
+    CHECK(walk_targets(tri, 0, 3, 3, "R") == std::vector<std::uint64_t>{0});
+    const std::uint64_t srcs[] = {0, 1, 2};
+    CHECK(walk_count_batch(tri, srcs, 1, 3, "R") == std::vector<std::uint64_t>({3, 3, 3}));
+    CHECK_THROWS_WITH_AS(walk_targets(tri, 0, 0, 2, "R"), "hop minimum must be at least 1", ContractError);
 }
 
 // ---- proj/tests/test_bench.cpp --------------------------------------------------------------

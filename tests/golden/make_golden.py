@@ -18,6 +18,9 @@ through oracle/ref_capi.cpp:
   with a SHA-256 of each generated edge list and of its flushed CSR.
 * harness_pins.json — rmat_generate / pick_seeds pins (proj/tests/
   test_bench.cpp:33-113 shapes) and a few sorted k_hop_frontier id lists.
+* walk_pins.json — walk_targets (execute.cpp:43-60, the VarLenTraverse step)
+  through the reference's own Cypher executor: counts and ids of
+  MATCH (a {id: S})-[*min..max]->(b) on RMAT graphs and a cycle with a loop.
 
 The GPU box never runs this script (no /root/reference there); it only reads
 the committed JSON.
@@ -158,10 +161,41 @@ def harness_pins(R: oracle.Ref) -> dict:
     return pins
 
 
+def walk_pins(R: oracle.Ref) -> dict:
+    """walk_targets (execute.cpp:43-60) through the reference's Cypher executor:
+    MATCH (a {id: S})-[*min..max]->(b) RETURN count(b) / RETURN b."""
+    ranges = ((1, 1), (1, 2), (2, 2), (1, 3), (2, 4), (3, 3), (3, 6), (1, 32))
+    out = {"ranges": [list(r) for r in ranges], "graphs": []}
+    for scale, rng in ((6, 3), (7, 8), (8, 2), (9, 17)):
+        src, dst = R.rmat_generate(scale, rng_seed=rng)
+        g = R.build_bench_graph(src, dst, 1 << scale)
+        seeds = [int(s) for s in g.pick_seeds(6, rng)]
+        cases = []
+        for s in seeds:
+            for lo, hi in ranges:
+                cnt = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN count(b)")
+                ids = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN b")
+                cases.append({"seed": s, "min": lo, "max": hi, "count": int(cnt.split("\n")[1]),
+                              "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t]})
+        out["graphs"].append({"scale": scale, "rng_seed": rng, "cases": cases})
+    # the seed reappears on a cycle; a self-loop keeps a walk alive (test_execute.cpp:89-97)
+    edges = [[0, 1], [1, 2], [2, 0], [1, 1], [2, 3]]
+    g = R.build_bench_graph(np.array([e[0] for e in edges], np.uint32),
+                            np.array([e[1] for e in edges], np.uint32), 4)
+    tl = []
+    for s in range(4):
+        for lo, hi in ((1, 1), (1, 3), (2, 2), (3, 3), (2, 5)):
+            ids = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN b")
+            tl.append({"seed": s, "min": lo, "max": hi,
+                       "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t]})
+    out["cycle_loop"] = {"edges": edges, "node_count": 4, "cases": tl}
+    return out
+
+
 def main() -> None:
     R = oracle.Ref()
     for name, fn in (("known_answers", known_answers), ("c1_sweep", c1_sweep),
-                     ("harness_pins", harness_pins)):
+                     ("harness_pins", harness_pins), ("walk_pins", walk_pins)):
         data = fn(R)
         data["_generated_by"] = "tests/golden/make_golden.py from oracle/_ref (reference core)"
         (OUT / f"{name}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")

@@ -255,3 +255,50 @@ def test_device_generator_g2(g2):
     g = DeviceGraph.generate(H.G2)
     drp, dci = g.csr()
     assert np.array_equal(drp, rp) and np.array_equal(dci, ci)
+
+
+# ---- walk_targets (execute.cpp:43-60): the Cypher variable-length route -------------------
+@pytest.mark.parametrize("engine", [ENGINE_SINGLE, ENGINE_LANES])
+def test_walk_pins(port, engine):
+    """Counts and ids of MATCH (a {id: S})-[*min..max]->(b) from the reference's
+    own executor (tests/golden/walk_pins.json)."""
+    from conftest import load_golden
+    from paper_1905_01294_b200 import walk_count_batch, walk_targets
+    w = load_golden("walk_pins")
+    for gd in w["graphs"]:
+        src, dst = port.rmat_generate(gd["scale"], rng_seed=gd["rng_seed"])
+        g = DeviceGraph.from_edges(src, dst, 1 << gd["scale"])
+        by_range = {}
+        for c in gd["cases"]:
+            by_range.setdefault((c["min"], c["max"]), []).append(c)
+        for (lo, hi), cases in by_range.items():
+            seeds = [c["seed"] for c in cases]
+            got = walk_count_batch(g, seeds, lo, hi, engine=engine)
+            assert got.tolist() == [c["count"] for c in cases], (lo, hi)
+            if engine == ENGINE_SINGLE:
+                for c in cases[:3]:
+                    assert walk_targets(g, c["seed"], lo, hi).tolist() == c["ids"], c
+    cl = w["cycle_loop"]
+    e = np.array(cl["edges"], np.uint32)
+    g = DeviceGraph.from_edges(e[:, 0], e[:, 1], cl["node_count"])
+    for c in cl["cases"]:
+        assert walk_count_batch(g, [c["seed"]], c["min"], c["max"], engine=engine).tolist() == [len(c["ids"])]
+        assert walk_targets(g, c["seed"], c["min"], c["max"]).tolist() == c["ids"], c
+
+
+def test_walk_cfg1_and_messages(port, g1):
+    from paper_1905_01294_b200 import walk_count_batch, walk_targets
+    rp, ci, g = g1
+    rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
+    seeds = H.pick_seeds(rp, 64, 4)
+    for lo, hi in ((1, 2), (2, 3), (3, 6), (1, 6)):
+        want = [len(port.walk_targets(rp64, ci64, int(s), lo, hi)) for s in seeds]
+        for eng in (ENGINE_SINGLE, ENGINE_LANES):
+            assert walk_count_batch(g, seeds, lo, hi, engine=eng).tolist() == want, (lo, hi, eng)
+        assert np.array_equal(walk_targets(g, int(seeds[0]), lo, hi),
+                              port.walk_targets(rp64, ci64, int(seeds[0]), lo, hi))
+    for (lo, hi), msg in (((0, 2), "hop minimum must be at least 1"),
+                          ((1, 33), "hop count 33 exceeds the cap of 32"),
+                          ((4, 2), "hop maximum 2 is less than minimum 4")):
+        with pytest.raises(ContractError, match=msg):
+            walk_count_batch(g, seeds[:1], lo, hi)

@@ -113,3 +113,20 @@ def test_port_matches_reference_library(port):
         for k in (1, 2, 3, 6, 32):
             for mode in (0, 1):
                 assert port.khop_count(rp, ci, int(s), k, mode) == g.k_hop_count(int(s), k, mode)
+
+
+def test_walk_pins(port):
+    """walk_targets restated (oracle) vs the reference's Cypher executor."""
+    from conftest import load_golden
+    w = load_golden("walk_pins")
+    for gd in w["graphs"]:
+        src, dst = port.rmat_generate(gd["scale"], rng_seed=gd["rng_seed"])
+        rp, ci = port.build_csr(1 << gd["scale"], src, dst)
+        for c in gd["cases"]:
+            got = port.walk_targets(rp, ci, c["seed"], c["min"], c["max"])
+            assert got.tolist() == c["ids"] and len(got) == c["count"], c
+    cl = w["cycle_loop"]
+    e = np.array(cl["edges"], np.uint32)
+    rp, ci = port.build_csr(cl["node_count"], e[:, 0], e[:, 1])
+    for c in cl["cases"]:
+        assert port.walk_targets(rp, ci, c["seed"], c["min"], c["max"]).tolist() == c["ids"], c
