@@ -183,9 +183,9 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
                        int* W_out, bool keep_result = false) {
     const uint32_t k = span.hi;
-    cudaError_t e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
-    if (e) return e;
-    if (nseeds == 0) return cudaSuccess;
+    // the engines zero the per-hop counters themselves (first launch of a call)
+    cudaError_t e = cudaSuccess;
+    if (nseeds == 0) return cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
     Launch L{};
     L.g = g;
     L.ws = ws;
@@ -533,11 +533,11 @@ int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, 
     float ms = 0.f;
     do {
         if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
-        if ((e = cudaEventRecord(ws->ev0, ws->stream))) break;
+        if (stats && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
         if ((e = run_engine(g, ws, ws->d_seeds, nseeds, span, engine, ws->d_counts, ws->stream,
                             &grid, &block, &used, &W)))
             break;
-        if ((e = cudaEventRecord(ws->ev1, ws->stream))) break;
+        if (stats && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
         if ((e = cudaMemcpyAsync(ws->h_pinned, ws->d_counts, nseeds * 8, cudaMemcpyDeviceToHost, ws->stream)))
             break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;

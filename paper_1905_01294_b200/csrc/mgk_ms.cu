@@ -547,6 +547,9 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
         if (gtid == 0) P.misc[0] = g.m;
+        if (bt == 0)  // the first lc write is after the barrier below
+            for (uint32_t i = gtid; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += nthreads)
+                reinterpret_cast<unsigned long long*>(P.lc)[i] = 0;
         grid_barrier(P.bar);
         // ---- seeds: level-0 frontier -------------------------------------------
         {

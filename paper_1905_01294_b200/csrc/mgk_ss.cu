@@ -86,6 +86,7 @@ struct FRParams {
     uint32_t* snap;  // keep_result: slot 0's visited bitmap after hop min_hop - 1
     uint32_t quota;  // per-seed log entries before the seed is cleared densely
     uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
+    uint32_t zero_lc;      // first group of a call: clear the per-hop counters
 };
 
 struct Acc {
@@ -509,6 +510,9 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
         }
         emit_row_items(P, 0, lane == 0, slot, b, deg);
     }
+    if (P.zero_lc)  // the first lc write is after the barrier below
+        for (uint32_t i = gtid; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += nthreads)
+            reinterpret_cast<unsigned long long*>(P.lc)[i] = 0;
     if (gtid == 0) {
         P.ctl->found[0] = ns;
         atomicAdd(&P.ctl->log_n, ns);
@@ -886,6 +890,7 @@ cudaError_t launch_single(Launch& L) {
     // one group of up to S seeds per (traverse, finish) launch pair
     for (uint64_t g0 = 0; g0 < L.nseeds; g0 += P.S) {
         P.ns = (uint32_t)std::min<uint64_t>(P.S, L.nseeds - g0);
+        P.zero_lc = g0 == 0;
         P.seeds = L.d_seeds + g0;
         P.counts = L.d_counts + g0;
         void* args[] = {&P};

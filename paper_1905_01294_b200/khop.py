@@ -221,12 +221,13 @@ def k_hop_count_batch(graph: DeviceGraph, seeds, k: int, mode=TraverseMode.Exact
     With stats=True returns (counts, stats_dict) with per-hop work counters.
     """
     seeds = np.ascontiguousarray(seeds, np.uint64)
-    for s in seeds:
-        if int(s) >= graph.node_count:
-            raise ContractError(f"k-hop seed {int(s)} is not an allocated node")
+    if graph.node_count < graph.nrows and len(seeds):  # the C ABI checks against nrows
+        bad = np.flatnonzero(seeds >= graph.node_count)
+        if len(bad):
+            raise ContractError(f"k-hop seed {int(seeds[bad[0]])} is not an allocated node")
     _check_k(k)
-    counts = np.zeros(max(len(seeds), 1), np.uint64)
-    st = MgkStats()
+    counts = np.empty(max(len(seeds), 1), np.uint64)
+    st = MgkStats() if stats else None
     sp = seeds if len(seeds) else np.zeros(1, np.uint64)
     _check(_lib.lib().mgk_khop_count_ex(graph.handle, sp.ctypes.data, len(seeds), int(k), int(mode),
                                         int(engine), counts.ctypes.data,
