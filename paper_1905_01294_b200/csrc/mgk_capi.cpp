@@ -185,7 +185,10 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     const uint32_t k = span.hi;
     // the engines zero the per-hop counters themselves (first launch of a call)
     cudaError_t e = cudaSuccess;
-    if (nseeds == 0) return cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
+    if (nseeds == 0) {
+        ws->last_launches = 0;
+        return cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), stream);
+    }
     Launch L{};
     L.g = g;
     L.ws = ws;
@@ -214,6 +217,7 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     }
     *grid = L.grid;
     *block = L.block;
+    ws->last_launches = e ? 0 : L.launches;
     return e;
 }
 
@@ -236,17 +240,14 @@ cudaError_t ensure_staging(Workspace* ws, uint64_t nseeds) {
 }
 
 void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint64_t nseeds,
-                uint32_t grid, uint32_t block, float ms, uint32_t slots) {
+                uint32_t grid, uint32_t block, float ms, uint32_t launches) {
     std::memset(st, 0, sizeof *st);
     st->engine = (uint32_t)engine;
     st->lanes = engine == MGK_ENGINE_LANES ? 64u * (uint32_t)W : 1u;
     st->batches = (uint32_t)(engine == MGK_ENGINE_LANES ? (nseeds + st->lanes - 1) / st->lanes : nseeds);
     st->grid = grid;
     st->block = block;
-    // SINGLE: a (traverse, finish) launch pair per group of `slots` seeds; LANES: one launch
-    st->launches = nseeds == 0 ? 0
-                   : engine == MGK_ENGINE_LANES ? 1u
-                                                : 2u * (uint32_t)((nseeds + slots - 1) / std::max(1u, slots));
+    st->launches = launches;
     st->kernel_ms = ms;
     st->setup_ns = lc[0].ns;
     st->cleanup_ns = lc[MGK_MAX_HOPS + 1].ns;
@@ -467,18 +468,14 @@ uint64_t mgk_graph_device_bytes(const mgk_graph* h) {
 int mgk_graph_download_csr(const mgk_graph* h, uint32_t* row_ptr, uint32_t* col_idx) {
     if (!h) return fail(MGK_ECONTRACT, "null graph");
     DeviceGuard dg(h->g.device);
-    cudaError_t e = cudaSuccess;
-    if (row_ptr) e = cudaMemcpy(row_ptr, h->g.rp, (size_t)(h->g.dg.n + 1) * 4, cudaMemcpyDeviceToHost);
-    if (!e && col_idx && h->g.dg.m) e = cudaMemcpy(col_idx, h->g.ci, h->g.dg.m * 4, cudaMemcpyDeviceToHost);
+    cudaError_t e = download_graph(&h->g, row_ptr, col_idx, nullptr, nullptr);
     return e ? fail_cuda(e, "download") : MGK_OK;
 }
 
 int mgk_graph_download_csc(const mgk_graph* h, uint32_t* col_ptr, uint32_t* row_idx) {
     if (!h) return fail(MGK_ECONTRACT, "null graph");
     DeviceGuard dg(h->g.device);
-    cudaError_t e = cudaSuccess;
-    if (col_ptr) e = cudaMemcpy(col_ptr, h->g.cp, (size_t)(h->g.dg.n + 1) * 4, cudaMemcpyDeviceToHost);
-    if (!e && row_idx && h->g.dg.m) e = cudaMemcpy(row_idx, h->g.ri, h->g.dg.m * 4, cudaMemcpyDeviceToHost);
+    cudaError_t e = download_graph(&h->g, nullptr, nullptr, col_ptr, row_idx);
     return e ? fail_cuda(e, "download") : MGK_OK;
 }
 
@@ -546,7 +543,7 @@ int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, 
             cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
             LevelCounters lc[MGK_MAX_HOPS + 2];
             if ((e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost))) break;
-            fill_stats(stats, lc, used, W, nseeds, grid, block, ms, ws->fr_slots);
+            fill_stats(stats, lc, used, W, nseeds, grid, block, ms, ws->last_launches);
         }
     } while (0);
     release_ws(g, ws);
@@ -649,7 +646,7 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     cudaError_t e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
     if (e) return fail_cuda(e, "stats");
     fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f,
-               ws->fr_slots);
+               ws->last_launches);
     return MGK_OK;
 }
 
@@ -682,6 +679,8 @@ int ids_impl(mgk_graph* h, uint64_t seed, Span span, uint64_t* ids, uint64_t cap
             break;
         unsigned long long n = 0;
         if ((e = cudaMemcpyAsync(&n, d_n, 8, cudaMemcpyDeviceToHost, ws->stream))) break;
+        if ((e = cudaStreamSynchronize(ws->stream))) break;
+        if ((e = ids_to_external(g, d_ids, n, ws->stream))) break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;
         *n_out = n;
         const uint64_t take = std::min<uint64_t>(n, cap);

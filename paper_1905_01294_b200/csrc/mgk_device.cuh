@@ -15,6 +15,11 @@ namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// device id of an external vertex id (locality relabelling; identity if none)
+__device__ __forceinline__ uint32_t dev_id(const DevGraph& g, uint32_t x) {
+    return g.perm ? __ldg(g.perm + x) : x;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -10,6 +10,7 @@
 // transpose. A zero-in-degree bitmap lets the pull pass skip vertices that
 // can never be reached.
 #include <cub/cub.cuh>
+#include <cstdlib>
 
 #include "mgk_internal.cuh"
 
@@ -46,6 +47,16 @@ __global__ void fill_cols(const uint32_t* ci, uint64_t m, unsigned long long* ke
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
          p += (uint64_t)gridDim.x * blockDim.x)
         keys[p] |= (unsigned long long)ci[p] << 32;
+}
+
+// keys[p] = col << 32 | row in CSR order: flags a row whose entries are not
+// strictly ascending (a duplicate or unsorted entry)
+__global__ void rows_strict_check(const unsigned long long* keys, uint64_t m, unsigned int* bad) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p + 1 < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long a = keys[p], b = keys[p + 1];
+        if ((uint32_t)a == (uint32_t)b && (a >> 32) >= (b >> 32)) *bad = 1;
+    }
 }
 
 // sorted (major << 32 | minor) keys -> ptr[n+1] over the major ids and the
@@ -112,6 +123,37 @@ __global__ void swap_halves(unsigned long long* keys, uint64_t m) {
         const unsigned long long k = keys[p];
         keys[p] = (k << 32) | (k >> 32);
     }
+}
+
+// ((~indeg) << 32 | v): ascending order = descending in-degree, ties by id
+__global__ void indeg_keys(const uint32_t* cp, uint32_t n, unsigned long long* keys) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        keys[v] = ((unsigned long long)(0xFFFFFFFFu - (cp[v + 1] - cp[v])) << 32) | v;
+}
+
+__global__ void perm_from_sorted(const unsigned long long* keys, uint32_t n, uint32_t* perm, uint32_t* inv) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = (uint32_t)keys[i];
+        inv[i] = v;
+        perm[v] = (uint32_t)i;
+    }
+}
+
+// keys[p] = row (expand_rows) -> map[row] << 32 | map[ci[p]]
+__global__ void map_edge_keys(unsigned long long* keys, const uint32_t* ci, const uint32_t* map, uint64_t m) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < m;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t row = (uint32_t)keys[p];
+        keys[p] = ((unsigned long long)map[row] << 32) | map[ci[p]];
+    }
+}
+
+__global__ void map_ids(unsigned long long* ids, uint64_t n, const uint32_t* map) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        ids[i] = map[ids[i]];
 }
 
 int key_bits(uint32_t n) {
@@ -185,6 +227,17 @@ cudaError_t build_csc(Graph* g, cudaStream_t s) {
         MGK_TRY(cudaMallocAsync(&alt, m * 8, s));
         expand_rows<<<blocks_for(m), kTB, 0, s>>>(g->rp, n, m, keys);
         fill_cols<<<blocks_for(m), kTB, 0, s>>>(g->ci, m, keys);
+        {
+            unsigned int* bad = nullptr;
+            unsigned int h_bad = 1;
+            MGK_TRY(cudaMallocAsync(&bad, 4, s));
+            MGK_TRY(cudaMemsetAsync(bad, 0, 4, s));
+            rows_strict_check<<<blocks_for(m), kTB, 0, s>>>(keys, m, bad);
+            MGK_TRY(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, s));
+            MGK_TRY(cudaFreeAsync(bad, s));
+            MGK_TRY(cudaStreamSynchronize(s));
+            g->dg.rows_unique = h_bad ? 0u : 1u;
+        }
         MGK_TRY(radix_sort_keys(keys, alt, m, 32 + key_bits(n), s));
         keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->cp, g->ri);
         MGK_TRY(order_in_lists(g, keys, alt, s));
@@ -192,6 +245,7 @@ cudaError_t build_csc(Graph* g, cudaStream_t s) {
         MGK_TRY(cudaFreeAsync(alt, s));
     } else {
         MGK_TRY(cudaMemsetAsync(g->cp, 0, (size_t)(n + 1) * 4, s));
+        g->dg.rows_unique = 1;
     }
     no_in_bitmap<<<blocks_for(g->dg.nwords), kTB, 0, s>>>(g->cp, n, g->dg.nwords, g->no_in);
     MGK_TRY(cudaGetLastError());
@@ -271,6 +325,73 @@ cudaError_t exclusive_scan_u32(uint32_t* data, uint32_t n, unsigned long long* t
 cudaError_t graph_from_sorted_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt,
                                    uint64_t m, cudaStream_t s);
 
+// (map[src] << 32 | map[dst]) of every CSR entry of g, sorted; keys/alt are
+// allocated here (m entries each)
+cudaError_t mapped_sorted_keys(const Graph* g, const uint32_t* map, unsigned long long*& keys,
+                               unsigned long long*& alt, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    const uint64_t m = g->dg.m;
+    MGK_TRY(cudaMallocAsync(&keys, m * 8, s));
+    MGK_TRY(cudaMallocAsync(&alt, m * 8, s));
+    expand_rows<<<blocks_for(m), kTB, 0, s>>>(g->rp, n, m, keys);
+    map_edge_keys<<<blocks_for(m), kTB, 0, s>>>(keys, g->ci, map, m);
+    MGK_TRY(cudaGetLastError());
+    return radix_sort_keys(keys, alt, m, 32 + key_bits(n), s);
+}
+
+// Locality relabelling (opt-in, MGK_RELABEL=1 at load): device ids by
+// descending in-degree (ties by id), so the bits of popular targets share
+// words and 128-B lines. Counts are invariant; seeds are mapped through perm
+// on the device and returned ids through inv. Measured on G2:
+// the dense hops of k >= 3 get faster (SINGLE k=3 27.5 -> 18.0 ms), but the
+// k = 2 last hop gets 1.8x slower -- every seed's atomics now converge on the
+// same few hot words, which serialise in their L2 slice -- so it is off by
+// default. Needs duplicate-free rows (the rebuild goes through sorted keys).
+cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    const uint64_t m = g->dg.m;
+    const char* on = std::getenv("MGK_RELABEL");
+    if (!g->dg.rows_unique || m == 0 || n < 2 || !(on && on[0] == '1')) return cudaSuccess;
+    uint32_t *perm = nullptr, *inv = nullptr;
+    MGK_TRY(cudaMalloc(&perm, (size_t)n * 4));
+    MGK_TRY(cudaMalloc(&inv, (size_t)n * 4));
+    {
+        unsigned long long *kv = nullptr, *ka = nullptr;
+        MGK_TRY(cudaMallocAsync(&kv, (size_t)n * 8, s));
+        MGK_TRY(cudaMallocAsync(&ka, (size_t)n * 8, s));
+        indeg_keys<<<blocks_for(n), kTB, 0, s>>>(g->cp, n, kv);
+        MGK_TRY(radix_sort_keys(kv, ka, n, 64, s));
+        perm_from_sorted<<<blocks_for(n), kTB, 0, s>>>(kv, n, perm, inv);
+        MGK_TRY(cudaGetLastError());
+        MGK_TRY(cudaFreeAsync(kv, s));
+        MGK_TRY(cudaFreeAsync(ka, s));
+    }
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    MGK_TRY(mapped_sorted_keys(g, perm, keys, alt, s));
+    MGK_TRY(cudaStreamSynchronize(s));
+    Graph old;
+    old.rp = g->rp, old.ci = g->ci, old.cp = g->cp, old.ri = g->ri;
+    old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy;
+    g->heavy = nullptr;
+    cudaError_t e = graph_from_sorted_keys(g, keys, alt, m, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    cudaFreeAsync(keys, s);
+    cudaFreeAsync(alt, s);
+    cudaStreamSynchronize(s);
+    free_device_graph(&old);
+    if (e) {
+        cudaFree(perm);
+        cudaFree(inv);
+        return e;
+    }
+    g->perm = perm;
+    g->inv = inv;
+    g->dg.perm = perm;
+    g->dg.inv = inv;
+    g->bytes += 2 * (size_t)n * 4;
+    return cudaSuccess;
+}
+
 cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge_factor, double a,
                                          double b, double c, uint64_t rng_seed, uint64_t target,
                                          int relabel) {
@@ -288,6 +409,10 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
     if (!e) e = cudaStreamSynchronize(s);
     if (keys) cudaFreeAsync(keys, s);
     if (alt) cudaFreeAsync(alt, s);
+    keys = alt = nullptr;
+    if (!e) e = locality_relabel(g, s);
+    if (keys) cudaFreeAsync(keys, s);
+    if (alt) cudaFreeAsync(alt, s);
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
     return e;
@@ -303,6 +428,7 @@ cudaError_t build_device_graph(Graph* g, const uint32_t* h_rp, const uint32_t* h
     if (m) MGK_TRY(cudaMemcpyAsync(g->ci, h_ci, m * 4, cudaMemcpyHostToDevice, s));
     cudaError_t e = build_csc(g, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = locality_relabel(g, s);
     cudaStreamDestroy(s);
     return e;
 }
@@ -314,6 +440,7 @@ cudaError_t graph_from_sorted_keys(Graph* g, unsigned long long*& keys, unsigned
     const uint32_t n = g->dg.n;
     g->dg.m = m;
     MGK_TRY(alloc_graph(g, n, m));
+    g->dg.rows_unique = 1;  // sorted unique keys
     if (m) {
         keys_to_csr<<<blocks_for(m + 1), kTB, 0, s>>>(keys, m, n, g->rp, g->ci);
         swap_halves<<<blocks_for(m), kTB, 0, s>>>(keys, m);
@@ -398,8 +525,53 @@ cudaError_t build_device_graph_from_edges(Graph* g, const uint32_t* h_src, const
     if (keep) cudaFreeAsync(keep, s);
     if (bad) cudaFreeAsync(bad, s);
     cudaStreamSynchronize(s);
+    keys = alt = nullptr;
+    if (!e) e = locality_relabel(g, s);
     cudaStreamDestroy(s);
     return e;
+}
+
+cudaError_t download_graph(const Graph* g, uint32_t* h_rp, uint32_t* h_ci, uint32_t* h_cp, uint32_t* h_ri) {
+    const uint32_t n = g->dg.n;
+    const uint64_t m = g->dg.m;
+    auto copy_out = [&](const Graph* src) -> cudaError_t {
+        if (h_rp) MGK_TRY(cudaMemcpy(h_rp, src->rp, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost));
+        if (h_ci && m) MGK_TRY(cudaMemcpy(h_ci, src->ci, m * 4, cudaMemcpyDeviceToHost));
+        if (h_cp) MGK_TRY(cudaMemcpy(h_cp, src->cp, (size_t)(n + 1) * 4, cudaMemcpyDeviceToHost));
+        if (h_ri && m) MGK_TRY(cudaMemcpy(h_ri, src->ri, m * 4, cudaMemcpyDeviceToHost));
+        return cudaSuccess;
+    };
+    if (!g->inv) return copy_out(g);
+    // relabelled: rebuild the external-id graph (same CSC ordering rules) once
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    Graph tmp;
+    tmp.dg.n = n;
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    cudaError_t e = mapped_sorted_keys(g, g->inv, keys, alt, s);
+    if (!e) e = graph_from_sorted_keys(&tmp, keys, alt, m, s);
+    if (!e) e = cudaStreamSynchronize(s);
+    if (!e) e = copy_out(&tmp);
+    if (keys) cudaFreeAsync(keys, s);
+    if (alt) cudaFreeAsync(alt, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    free_device_graph(&tmp);
+    return e;
+}
+
+cudaError_t ids_to_external(const Graph* g, unsigned long long* d_ids, uint64_t n, cudaStream_t s) {
+    if (!g->inv || n == 0) return cudaSuccess;
+    map_ids<<<blocks_for(n), kTB, 0, s>>>(d_ids, n, g->inv);
+    MGK_TRY(cudaGetLastError());
+    unsigned long long* alt = nullptr;
+    MGK_TRY(cudaMallocAsync(&alt, n * 8, s));
+    unsigned long long* keys = d_ids;
+    MGK_TRY(radix_sort_keys(keys, alt, n, key_bits(g->dg.n), s));
+    if (keys != d_ids) MGK_TRY(cudaMemcpyAsync(d_ids, keys, n * 8, cudaMemcpyDeviceToDevice, s));
+    // radix_sort_keys swaps the pointers when the result landed in alt
+    MGK_TRY(cudaFreeAsync(keys == d_ids ? alt : keys, s));
+    return cudaSuccess;
 }
 
 void free_device_graph(Graph* g) {
@@ -410,8 +582,12 @@ void free_device_graph(Graph* g) {
     cudaFree(g->no_in);
     cudaFree(g->pull_skip);
     cudaFree(g->heavy);
+    cudaFree(g->perm);
+    cudaFree(g->inv);
     g->rp = g->ci = g->cp = g->ri = g->no_in = g->pull_skip = nullptr;
     g->heavy = nullptr;
+    g->perm = g->inv = nullptr;
+    g->dg.perm = g->dg.inv = nullptr;
 }
 
 }  // namespace mgk

@@ -32,6 +32,13 @@ struct DevGraph {
     const uint32_t* pull_skip = nullptr;  // no_in | heavy: what the per-word pull pass skips
     const uint2* heavy = nullptr;         // {vertex, first CSC entry} per task
     uint32_t nheavy = 0;
+    // every CSR row strictly ascending (no duplicate entries): hop 1 from a
+    // seed is then its row minus the seed itself, with no test-and-set
+    uint32_t rows_unique = 0;
+    // locality relabelling (ids by descending in-degree): device id of an
+    // external id (perm) and back (inv); null = identity
+    const uint32_t* perm = nullptr;
+    const uint32_t* inv = nullptr;
 };
 constexpr uint32_t kHeavyIn = 1024;
 constexpr uint32_t kHeavyChunk = 1024;
@@ -113,6 +120,7 @@ struct Workspace {
     // last device-path launch (mgk_khop_device_stats)
     int misc_engine = 0, misc_W = 0;
     uint32_t misc_grid = 0, misc_block = 0;
+    uint32_t last_launches = 0;  // engine kernels of the last call
     uint64_t misc_nseeds = 0;
 };
 
@@ -126,6 +134,8 @@ struct Graph {
     uint32_t* no_in = nullptr;
     uint32_t* pull_skip = nullptr;
     uint2* heavy = nullptr;
+    uint32_t* perm = nullptr;
+    uint32_t* inv = nullptr;
     uint64_t bytes = 0;
     Tuning tuning;
     std::mutex mu;
@@ -149,6 +159,7 @@ struct Launch {
     int lanes_words;  // LANES engine only
     bool keep_result = false;  // SINGLE: leave slot 0's bitmaps for k_hop_frontier
     uint32_t grid = 0, block = 0;  // out
+    uint32_t launches = 0;         // out: engine kernels launched
 };
 
 // Launches a persistent engine kernel: cooperative (all CTAs co-resident,
@@ -182,6 +193,10 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
                                          double b, double c, uint64_t rng_seed, uint64_t target,
                                          int relabel);
 void free_device_graph(Graph* g);
+// CSR / CSC in external ids into host buffers (un-relabelled when relabelled)
+cudaError_t download_graph(const Graph* g, uint32_t* h_rp, uint32_t* h_ci, uint32_t* h_cp, uint32_t* h_ri);
+// device ids (scattered from a bitmap) -> external ids, ascending
+cudaError_t ids_to_external(const Graph* g, unsigned long long* d_ids, uint64_t n, cudaStream_t s);
 
 // device R-MAT generator (mgk_gen.cu) and its host-drawn relabel permutation
 cudaError_t gen_rmat_device(uint32_t scale, uint32_t edge_factor, double a, double b, double c,

@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             bool first = false;
             uint32_t s = 0;
             if (gtid < lanes) {
-                s = P.seeds[bt * LB + gtid];
+                s = dev_id(g, P.seeds[bt * LB + gtid]);
                 const unsigned long long bit = 1ULL << (gtid & 63);
                 atomicOr(P.F0 + (size_t)s * W + (gtid >> 6), bit);
                 const uint32_t tb = 1u << (s & 31);
@@ -715,6 +715,7 @@ cudaError_t launch_w(Launch& L) {
     L.grid = (uint32_t)(blocks_per_sm * num_sms);
     L.block = kBlock;
     void* args[] = {&P};
+    L.launches = 1;
     return launch_persistent((const void*)ms_kernel<W>, L.grid, kBlock, args, L.stream);
 }
 

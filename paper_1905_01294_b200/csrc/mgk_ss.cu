@@ -36,6 +36,7 @@ constexpr int kStageCap = 256;
 constexpr int kIlp = 4;
 constexpr uint32_t kBigChunk = 1024;  // rows longer than this become 1024-entry big items
 constexpr uint32_t kMaxSlots = 512;
+constexpr uint32_t kSeedChunk = 32;  // fused hop 1: seed-row entries per warp task
 constexpr unsigned long long kOverflowBit = 1ULL << 62;
 enum : uint8_t { kPush = 0, kPull = 1, kDead = 2 };
 
@@ -87,6 +88,7 @@ struct FRParams {
     uint32_t quota;  // per-seed log entries before the seed is cleared densely
     uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
     uint32_t zero_lc;      // first group of a call: clear the per-hop counters
+    uint32_t fuse1;        // rows unique, seed pre-visited, k >= 2: hop 1 = the seed rows
 };
 
 struct Acc {
@@ -495,9 +497,84 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     const uint32_t ns = P.ns;
     unsigned long long t_init = 0;
     if (gtid == 0) t_init = globaltimer();
+    if (P.fuse1) {
+        // ---- seeds and hop 1 in one phase: with duplicate-free rows, F_1 of a
+        // seed is its row minus the seed, so every entry is a discovery and the
+        // bits are set fire-and-forget. Tasks are kSeedChunk-entry slices of
+        // the seed rows (a hub seed is spread over many warps).
+        __shared__ uint32_t s_pref[kMaxSlots];
+        __shared__ uint32_t s_ntask, s_logbase;
+        // the seed log entries get their own reservation (hop-1 emits run concurrently)
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) s_logbase = atomicAdd(&P.ctl->log_n, ns);
+            __syncthreads();
+        }
+        uint32_t c = 0;
+        if (threadIdx.x < ns) {
+            const uint32_t sd = dev_id(g, P.seeds[threadIdx.x]);
+            const uint32_t b = __ldg(g.rp + sd), deg = __ldg(g.rp + sd + 1) - b;
+            c = (deg + kSeedChunk - 1) / kSeedChunk;
+            if (blockIdx.x == 0) {  // hop 0: the seed itself
+                const uint32_t slot = threadIdx.x;
+                const uint32_t bit = 1u << (sd & 31);
+                atomicOr(P.V + (size_t)slot * P.rs + (sd >> 5), bit);
+                P.Fb[(size_t)slot * P.rs + (sd >> 5)] = bit;
+                P.cnt[slot] = 1;
+                P.mfs[slot] = deg;
+                if (s_logbase + slot < P.log_cap)
+                    P.logbuf[s_logbase + slot] = ((unsigned long long)slot << 32) | sd;
+                else P.ctl->log_overflow = 1;
+                // mex gets the seed's in-degree plus (in emit) its discoveries'
+                atomicAdd(&P.mex[slot], (unsigned long long)(__ldg(g.cp + sd + 1) - __ldg(g.cp + sd)));
+            }
+        }
+        {
+            const uint32_t incl = warp_incl_scan(c);
+            if (lane == 31) s_wcount[wib] = incl;
+            __syncthreads();
+            uint32_t off = 0, tot = 0;
+            for (uint32_t i = 0; i < kWarps; ++i) {
+                if (i < wib) off += s_wcount[i];
+                tot += s_wcount[i];
+            }
+            if (threadIdx.x < kMaxSlots) s_pref[threadIdx.x] = off + incl - c;
+            if (threadIdx.x == 0) s_ntask = tot;
+            __syncthreads();
+        }
+        const uint32_t ntask = s_ntask;
+        for (uint32_t t = warp_gid; t < ntask; t += nwarps) {
+            uint32_t lo = 0, hi = ns;  // last slot with s_pref <= t
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_pref[mid] <= t) lo = mid;
+                else hi = mid;
+            }
+            const uint32_t slot = lo;
+            const uint32_t sd = dev_id(g, P.seeds[slot]);
+            const uint32_t b = __ldg(g.rp + sd), deg = __ldg(g.rp + sd + 1) - b;
+            const uint32_t beg = (t - s_pref[slot]) * kSeedChunk;
+            const uint32_t len = min(kSeedChunk, deg - beg);
+            uint32_t* vrow = P.V + (size_t)slot * P.rs;
+            uint32_t* frow = P.Fb + ((size_t)1 * S + slot) * P.rs;
+            for (uint32_t i0 = 0; i0 < len; i0 += 32) {
+                const uint32_t i = i0 + lane;
+                const uint32_t u = i < len ? __ldg(g.ci + b + beg + i) : sd;
+                const bool found = u != sd;
+                if (found) {
+                    atomicOr(vrow + (u >> 5), 1u << (u & 31));
+                    atomicOr(frow + (u >> 5), 1u << (u & 31));
+                }
+                acc.scanned += i < len;
+                acc.found += found;
+                stage_push(P, 1, false, s_flag, st, found, slot, u);
+            }
+        }
+        emit(P, 1, false, s_flag, st.buf, st.n);
+        st.n = 0;
+    }
     // ---- seeds (hop 0): one warp per seed; counters are zero on entry --------------
-    for (uint32_t slot = warp_gid; slot < ns; slot += nwarps) {
-        const uint32_t s = P.seeds[slot];
+    for (uint32_t slot = warp_gid; slot < (P.fuse1 ? 0u : ns); slot += nwarps) {
+        const uint32_t s = dev_id(g, P.seeds[slot]);
         const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
         if (lane == 0) {
             const uint32_t bit = 1u << (s & 31);
@@ -515,13 +592,23 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
             reinterpret_cast<unsigned long long*>(P.lc)[i] = 0;
     if (gtid == 0) {
         P.ctl->found[0] = ns;
-        atomicAdd(&P.ctl->log_n, ns);
+        if (!P.fuse1) atomicAdd(&P.ctl->log_n, ns);
     }
     grid_barrier(P.bar);
-    if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds
+    if (gtid == 0) atomicAdd(&P.lc[0].ns, globaltimer() - t_init);  // seeds (+ hop 1 if fused)
+    if (P.fuse1) {  // hop 1's counters, now that lc is zeroed
+        block_flush(acc, &P.ctl->found[1], &P.lc[1]);
+        if (blockIdx.x == 0 && threadIdx.x < ns) {
+            const uint32_t sd = dev_id(g, P.seeds[threadIdx.x]);
+            const uint32_t deg = __ldg(g.rp + sd + 1) - __ldg(g.rp + sd);
+            atomicAdd(&P.lc[1].runs, 1u);
+            atomicAdd(&P.lc[1].edges, (unsigned long long)deg);
+            atomicAdd(&P.lc[1].union_edges, (unsigned long long)deg);
+        }
+    }
 
     bool snapped = false;
-    uint32_t hop = 1;
+    uint32_t hop = P.fuse1 ? 2 : 1;
     for (; hop <= P.k; ++hop) {
         const bool last = hop == P.k;
         // ---- plan: per-seed direction (every block computes the same) ------------
@@ -748,19 +835,22 @@ __global__ void clear_slot0(uint32_t* V, uint32_t* Fb, uint32_t S, uint32_t nw, 
     }
 }
 
+// `drop` is an external id (mapped to its device id here); ~0 = none
 __global__ void popc_words(const uint32_t* bits, const uint32_t* sub, uint32_t nwords, uint32_t drop,
-                           uint32_t* out) {
+                           const uint32_t* perm, uint32_t* out) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwords) return;
+    if (perm && drop != 0xFFFFFFFFu) drop = perm[drop];
     uint32_t x = bits[w] & (sub ? ~sub[w] : kFull);
     if ((drop >> 5) == w) x &= ~(1u << (drop & 31));
     out[w] = __popc(x);
 }
 
 __global__ void scatter_ids(const uint32_t* bits, const uint32_t* sub, uint32_t nwords, uint32_t drop,
-                            const uint32_t* offs, unsigned long long* ids) {
+                            const uint32_t* perm, const uint32_t* offs, unsigned long long* ids) {
     const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= nwords) return;
+    if (perm && drop != 0xFFFFFFFFu) drop = perm[drop];
     uint32_t x = bits[w] & (sub ? ~sub[w] : kFull);
     if ((drop >> 5) == w) x &= ~(1u << (drop & 31));
     uint32_t o = offs[w];
@@ -831,9 +921,78 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     return cudaSuccess;
 }
 
+// k = 1 on duplicate-free rows: |F_1| = deg(s) - [s in row(s)] (binary search
+// of the ascending row). No bitmap is touched, so there is nothing to clean up.
+constexpr int kK1Block = 512;
+__global__ void __launch_bounds__(kK1Block) k1_kernel(DevGraph g, const uint32_t* seeds, uint64_t ns,
+                                                      unsigned long long* counts, LevelCounters* lc,
+                                                      uint32_t zero_lc) {
+    __shared__ unsigned long long s_acc[3];
+    const unsigned long long t0 = globaltimer();
+    if (zero_lc)  // single-block launch: nothing else writes lc
+        for (uint32_t i = threadIdx.x; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += blockDim.x)
+            reinterpret_cast<unsigned long long*>(lc)[i] = 0;
+    if (threadIdx.x < 3) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long f = 0, sc = 0, nrun = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t sd = dev_id(g, seeds[i]);
+        const uint32_t b = __ldg(g.rp + sd), e = __ldg(g.rp + sd + 1);
+        uint32_t lo = b, hi = e;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(g.ci + mid) < sd) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t self = (lo < e && __ldg(g.ci + lo) == sd) ? 1u : 0u;
+        const uint32_t c = e - b - self;
+        counts[i] = c;
+        f += c;
+        sc += e - b;
+        nrun += 1;
+    }
+    f = warp_sum_u64(f);
+    sc = warp_sum_u64(sc);
+    nrun = warp_sum_u64(nrun);
+    if (lane_id() == 0) {
+        if (f) atomicAdd(&s_acc[0], f);
+        if (sc) atomicAdd(&s_acc[1], sc);
+        if (nrun) atomicAdd(&s_acc[2], nrun);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(&lc[1].frontier, s_acc[0]);
+        atomicAdd(&lc[1].vertices, s_acc[0]);
+        atomicAdd(&lc[1].scanned, s_acc[1]);
+        atomicAdd(&lc[1].edges, s_acc[1]);
+        atomicAdd(&lc[1].union_edges, s_acc[1]);
+        atomicAdd(&lc[1].runs, (unsigned)s_acc[2]);
+        if (blockIdx.x == 0) atomicAdd(&lc[1].ns, globaltimer() - t0);
+    }
+}
+
+bool fuse_disabled() {
+    static const bool off = std::getenv("MGK_NO_FUSE1") != nullptr;
+    return off;
+}
+
 cudaError_t launch_single(Launch& L) {
     const Graph* gr = L.g;
     Workspace* ws = L.ws;
+    if (gr->dg.rows_unique && L.k == 1 && L.seed_visited && !L.keep_result && !fuse_disabled()) {
+        const uint64_t want = (L.nseeds + kK1Block - 1) / kK1Block;
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(want, 148ull * 8);
+        cudaError_t e = cudaSuccess;
+        if (grid > 1 && (e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), L.stream)))
+            return e;
+        k1_kernel<<<grid, kK1Block, 0, L.stream>>>(gr->dg, L.d_seeds, L.nseeds, L.d_counts, ws->lc,
+                                                  grid == 1 ? 1u : 0u);
+        L.grid = grid;
+        L.block = kK1Block;
+        L.launches = 1;
+        return cudaGetLastError();
+    }
     cudaError_t e = ensure_single_ws(gr, ws);
     if (e) return e;
     static int blocks_per_sm = 0, num_sms = 0;
@@ -880,6 +1039,8 @@ cudaError_t launch_single(Launch& L) {
     P.force_dir = L.tuning.force_dir;
     P.quota = ws->fr_quota;
     P.keep_result = L.keep_result ? 1u : 0u;
+    P.fuse1 = (gr->dg.rows_unique && L.seed_visited && L.k >= 2 && !L.keep_result && !fuse_disabled())
+                  ? 1u : 0u;
     P.snap = ws->fr_snap;
     // bitmaps are laid out [S_alloc][rs] ([3][S_alloc][rs] for Fb): S is the
     // allocated slot count (the stride); a group holds up to S seeds
@@ -897,6 +1058,7 @@ cudaError_t launch_single(Launch& L) {
         if ((e = launch_persistent((const void*)fr_kernel, L.grid, kBlock, args, L.stream))) return e;
         fr_finish<<<fin_blocks, kFinBlock, 0, L.stream>>>(P);
         if ((e = cudaGetLastError())) return e;
+        L.launches += 2;
     }
     return cudaSuccess;
 }
@@ -914,9 +1076,9 @@ cudaError_t single_result_ids(const Graph* gr, Workspace* ws, uint32_t min_hop, 
     cudaError_t e;
     if ((e = cudaMallocAsync(&offs, (size_t)(nw + 1) * 4, s))) return e;
     const int tb = 256, nb = (int)((nw + tb - 1) / tb);
-    popc_words<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, offs);
+    popc_words<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, g.perm, offs);
     if ((e = exclusive_scan_u32(offs, nw, d_n, s))) return e;
-    scatter_ids<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, offs, d_ids);
+    scatter_ids<<<nb, tb, 0, s>>>(ws->fr_V, sub, nw, drop, g.perm, offs, d_ids);
     cudaFreeAsync(offs, s);
     clear_slot0<<<148, 256, 0, s>>>(ws->fr_V, ws->fr_Fb, ws->fr_slots, nw, row_stride(g));
     return cudaGetLastError();

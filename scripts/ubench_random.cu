@@ -10,7 +10,7 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
     return x;
 }
 
-template <int ILP, int MODE>  // MODE 0 atomicOr w/ return, 1 red (no return), 2 load, 3 load+cond atomic
+template <int ILP, int MODE>  // MODE 0 atomicOr w/ return, 1 red (no return), 2 load, 3 load+cond atomic, 4 st.b32, 5 st 32 B
 __global__ void kern(uint32_t* bits, uint32_t nwords, uint32_t iters, uint32_t* sink) {
     uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     uint32_t acc = 0;
@@ -24,6 +24,12 @@ __global__ void kern(uint32_t* bits, uint32_t nwords, uint32_t iters, uint32_t* 
             const uint32_t bit = 1u << (idx[r] & 31);
             if (MODE == 0) v[r] = atomicOr(bits + idx[r], bit);
             else if (MODE == 1) { atomicOr(bits + idx[r], bit); v[r] = 0; }
+            else if (MODE == 4) { bits[idx[r]] = 0; v[r] = 0; }
+            else if (MODE == 5) {
+                asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(bits + (idx[r] & ~7u)),
+                             "r"(0u) : "memory");
+                v[r] = 0;
+            }
             else v[r] = __ldcg(bits + idx[r]);
         }
         if (MODE == 3) {
@@ -69,6 +75,10 @@ int main() {
         run<4, 2>("ld.cg", bits, nwords, 296, 512, sink);
         run<8, 2>("ld.cg", bits, nwords, 296, 512, sink);
         run<4, 2>("ld.cg", bits, nwords, 148 * 4, 512, sink);
+        run<4, 4>("st.b32 zero", bits, nwords, 296, 512, sink);
+        run<4, 4>("st.b32 zero", bits, nwords, 148 * 4, 512, sink);
+        run<4, 5>("st.v8 sector zero", bits, nwords, 296, 512, sink);
+        run<4, 5>("st.v8 sector zero", bits, nwords, 148 * 4, 512, sink);
         cudaMemset(bits, 0, (size_t)nwords * 4);
         run<4, 3>("ld+cond atomic", bits, nwords, 296, 512, sink);
         cudaFree(bits);

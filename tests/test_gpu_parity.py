@@ -302,3 +302,34 @@ def test_walk_cfg1_and_messages(port, g1):
                           ((4, 2), "hop maximum 2 is less than minimum 4")):
         with pytest.raises(ContractError, match=msg):
             walk_count_batch(g, seeds[:1], lo, hi)
+
+
+# ---- opt-in locality relabelling (MGK_RELABEL=1): ids stay external at the boundary -----
+def test_relabelled_layout(port, g1, monkeypatch):
+    """The in-degree relabelled device layout answers exactly like the
+    external-id layout: counts (both engines, both modes), frontier and walk
+    ids (mapped back and sorted), and the downloaded CSR / CSC."""
+    from paper_1905_01294_b200 import walk_count_batch, walk_targets
+    rp, ci, g0 = g1
+    monkeypatch.setenv("MGK_RELABEL", "1")
+    g = DeviceGraph.from_csr(rp, ci)
+    monkeypatch.delenv("MGK_RELABEL")
+    rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
+    drp, dci = g.csr()
+    assert np.array_equal(drp, rp) and np.array_equal(dci, ci)
+    cp0, ri0 = g0.csc()
+    cp1, ri1 = g.csc()
+    assert np.array_equal(cp0, cp1) and np.array_equal(ri0, ri1)
+    seeds = H.pick_seeds(rp, 300, 11)
+    for mode in (0, 1):
+        for k in (1, 2, 3, 6):
+            want = oracle_counts(port, rp, ci, seeds, k, mode)
+            for eng in (ENGINE_SINGLE, ENGINE_LANES):
+                assert k_hop_count_batch(g, seeds, k, mode, engine=eng).tolist() == want, (mode, k, eng)
+    for s in seeds[:4]:
+        for k, mode in ((1, 0), (2, 0), (3, 1)):
+            want = port.khop_frontier(rp64, ci64, int(s), k, mode)
+            assert np.array_equal(k_hop_frontier(g, KHopQuery(int(s), k, TraverseMode(mode))), want)
+        assert np.array_equal(walk_targets(g, int(s), 2, 3), port.walk_targets(rp64, ci64, int(s), 2, 3))
+    assert walk_count_batch(g, seeds[:50], 1, 3).tolist() == \
+        [len(port.walk_targets(rp64, ci64, int(s), 1, 3)) for s in seeds[:50]]
