@@ -131,6 +131,20 @@ int mgk_khop_count(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_
 int mgk_khop_count_ex(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
                       int engine, uint64_t* counts, mgk_stats* stats);
 
+/* ---- multi-GPU: seed-sharded replicas, no collective ----------
+ * mgk_graph_replicate copies a device graph to `device` (cudaMemcpyPeer over
+ * NVLink / NVSwitch when the devices differ; a plain device copy otherwise):
+ * load-time replication instead of re-uploading from the host.
+ * mgk_khop_count_multi answers one batch over nreplicas replicas of the same
+ * graph: the seeds are split into contiguous shards, one host thread and the
+ * replica's own stream per shard, each writing a disjoint range of counts.
+ * Same validation and messages as mgk_khop_count (checked once, in seed order,
+ * before any device work). Replaces the "mgk_khop_count_multi_gpu" entry
+ * SURVEY §8(b) lists; the reference has no multi-device path. */
+int mgk_graph_replicate(const mgk_graph* src, int device, mgk_graph** out);
+int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64_t* seeds, uint64_t nseeds,
+                         uint32_t k, int mode, uint64_t* counts);
+
 /* Device-resident variant: d_seeds (uint32) and d_counts (uint64) are DEVICE
  * pointers on the graph's device; work is enqueued on `stream`
  * (a cudaStream_t, NULL = legacy default) and returns without synchronizing.

@@ -592,6 +592,64 @@ int mgk_khop_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_
     return mgk_khop_count_ex(h, seeds, nseeds, k, mode, MGK_ENGINE_AUTO, counts, nullptr);
 }
 
+int mgk_graph_replicate(const mgk_graph* src, int device, mgk_graph** out) {
+    if (!src || !out) return fail(MGK_ECONTRACT, "null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MGK_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(MGK_ECONTRACT, "device %d out of range [0, %d)", device, ndev);
+    DeviceGuard dg(device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = device;
+    cudaError_t e = replicate_device_graph(&src->g, &h->g);
+    if (e) {
+        free_device_graph(&h->g);
+        delete h;
+        return fail_cuda(e, "graph replicate");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
+int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64_t* seeds, uint64_t nseeds,
+                         uint32_t k, int mode, uint64_t* counts) {
+    if (!replicas || nreplicas < 1) return fail(MGK_ECONTRACT, "no replicas");
+    for (int i = 0; i < nreplicas; ++i) {
+        if (!replicas[i]) return fail(MGK_ECONTRACT, "null graph");
+        if (replicas[i]->g.dg.n != replicas[0]->g.dg.n || replicas[i]->g.dg.m != replicas[0]->g.dg.m)
+            return fail(MGK_ECONTRACT, "replica %d is not a copy of replica 0", i);
+    }
+    if (nseeds && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    int rc = check_query(&replicas[0]->g, seeds, nseeds, k);
+    if (rc) return rc;
+    // contiguous shards, one host thread (and the replica's own stream) each;
+    // no collective: every shard writes a disjoint range of `counts`
+    const Span span = span_of(k, mode);
+    std::vector<int> rcs(nreplicas, MGK_OK);
+    std::vector<std::string> errs(nreplicas);
+    auto run = [&](int i) {
+        const uint64_t a = nseeds * (uint64_t)i / nreplicas, b = nseeds * (uint64_t)(i + 1) / nreplicas;
+        if (b == a) return;
+        rcs[i] = count_impl(replicas[i], seeds + a, b - a, span, MGK_ENGINE_AUTO, counts + a, nullptr,
+                            "k-hop count");
+        if (rcs[i]) errs[i] = t_err;
+    };
+    std::vector<std::thread> ts;
+    for (int i = 1; i < nreplicas; ++i) ts.emplace_back(run, i);
+    run(0);
+    for (auto& t : ts) t.join();
+    for (int i = 0; i < nreplicas; ++i)
+        if (rcs[i]) {
+            t_err = errs[i];
+            return rcs[i];
+        }
+    return MGK_OK;
+}
+
 int mgk_khop_count_device(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
                           int mode, int engine, uint64_t* d_counts, void* stream) {
     if (!h) return fail(MGK_ECONTRACT, "null graph");

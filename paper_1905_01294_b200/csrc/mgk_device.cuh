@@ -15,6 +15,23 @@ namespace cg = cooperative_groups;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// L2 evict-last policy for the per-seed bitmaps: their lines should outlive
+// the streamed adjacency (loaded evict-first) until the cleanup pass.
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void red_or_keep(uint32_t* p, uint32_t v, unsigned long long pol) {
+    asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_or_keep(uint32_t* p, uint32_t v, unsigned long long pol) {
+    uint32_t old;
+    asm volatile("atom.global.or.L2::cache_hint.b32 %0, [%1], %2, %3;"
+                 : "=r"(old) : "l"(p), "r"(v), "l"(pol) : "memory");
+    return old;
+}
+
 // device id of an external vertex id (locality relabelling; identity if none)
 __device__ __forceinline__ uint32_t dev_id(const DevGraph& g, uint32_t x) {
     return g.perm ? __ldg(g.perm + x) : x;

@@ -574,6 +574,51 @@ cudaError_t ids_to_external(const Graph* g, unsigned long long* d_ids, uint64_t 
     return cudaSuccess;
 }
 
+// A copy of src's device arrays on dst->device (peer copies over NVLink when
+// the devices differ): load-time replication for seed-sharded multi-GPU runs.
+cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
+    const uint32_t n = src->dg.n;
+    const uint64_t m = src->dg.m;
+    int can = 0;
+    if (dst->device != src->device &&
+        cudaDeviceCanAccessPeer(&can, dst->device, src->device) == cudaSuccess && can) {
+        if (cudaDeviceEnablePeerAccess(src->device, 0) != cudaSuccess) cudaGetLastError();
+    }
+    MGK_TRY(alloc_graph(dst, n, m));
+    dst->dg = src->dg;
+    dst->dg.rp = dst->rp;
+    dst->dg.ci = dst->ci;
+    dst->dg.cp = dst->cp;
+    dst->dg.ri = dst->ri;
+    dst->dg.no_in = dst->no_in;
+    dst->dg.pull_skip = dst->pull_skip;
+    const size_t mp = (size_t)std::max<uint64_t>(m, 1);
+    const size_t nh = (size_t)std::max<uint32_t>(src->dg.nheavy, 1);
+    MGK_TRY(cudaMalloc(&dst->heavy, nh * sizeof(uint2)));
+    dst->dg.heavy = dst->heavy;
+    dst->bytes = src->bytes;
+    dst->tuning = src->tuning;
+    auto cp = [&](void* d, const void* s, size_t b) {
+        return cudaMemcpyPeer(d, dst->device, s, src->device, b);
+    };
+    MGK_TRY(cp(dst->rp, src->rp, (size_t)(n + 1) * 4));
+    MGK_TRY(cp(dst->ci, src->ci, mp * 4));
+    MGK_TRY(cp(dst->cp, src->cp, (size_t)(n + 1) * 4));
+    MGK_TRY(cp(dst->ri, src->ri, mp * 4));
+    MGK_TRY(cp(dst->no_in, src->no_in, (size_t)(src->dg.nwords + 1) * 4));
+    MGK_TRY(cp(dst->pull_skip, src->pull_skip, (size_t)(src->dg.nwords + 1) * 4));
+    MGK_TRY(cp(dst->heavy, src->heavy, nh * sizeof(uint2)));
+    if (src->perm) {
+        MGK_TRY(cudaMalloc(&dst->perm, (size_t)n * 4));
+        MGK_TRY(cudaMalloc(&dst->inv, (size_t)n * 4));
+        MGK_TRY(cp(dst->perm, src->perm, (size_t)n * 4));
+        MGK_TRY(cp(dst->inv, src->inv, (size_t)n * 4));
+    }
+    dst->dg.perm = dst->perm;
+    dst->dg.inv = dst->inv;
+    return cudaDeviceSynchronize();
+}
+
 void free_device_graph(Graph* g) {
     cudaFree(g->rp);
     cudaFree(g->ci);

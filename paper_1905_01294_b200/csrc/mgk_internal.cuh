@@ -193,6 +193,7 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
                                          double b, double c, uint64_t rng_seed, uint64_t target,
                                          int relabel);
 void free_device_graph(Graph* g);
+cudaError_t replicate_device_graph(const Graph* src, Graph* dst);
 // CSR / CSC in external ids into host buffers (un-relabelled when relabelled)
 cudaError_t download_graph(const Graph* g, uint32_t* h_rp, uint32_t* h_ci, uint32_t* h_cp, uint32_t* h_ri);
 // device ids (scattered from a bitmap) -> external ids, ascending

@@ -290,6 +290,7 @@ __device__ __forceinline__ void visit_edges(const FRParams& P, uint32_t hop, boo
                                             const bool (&valid)[kIlp]) {
     const uint32_t fn = hop % 3;
     const bool set_fb = !last || P.keep_result;
+    const unsigned long long pol = l2_keep_policy();
     uint32_t old[kIlp];
 #pragma unroll
     for (int r = 0; r < kIlp; ++r) {
@@ -300,15 +301,15 @@ __device__ __forceinline__ void visit_edges(const FRParams& P, uint32_t hop, boo
             // a seed's last hop that is not logged only sets bits
             // (fire-and-forget red.or); it is counted afterwards by a
             // popcount of the bitmap in the clearing pass
-            if (last && !s_logok[sj[r]]) atomicOr(vw, bit);
-            else old[r] = atomicOr(vw, bit);
+            if (last && !s_logok[sj[r]]) red_or_keep(vw, bit, pol);
+            else old[r] = atom_or_keep(vw, bit, pol);
         }
     }
 #pragma unroll
     for (int r = 0; r < kIlp; ++r) {
         const bool found = !((old[r] >> (u[r] & 31)) & 1u);
         if (found && set_fb)
-            atomicOr(P.Fb + ((size_t)fn * P.S + sj[r]) * P.rs + (u[r] >> 5), 1u << (u[r] & 31));
+            red_or_keep(P.Fb + ((size_t)fn * P.S + sj[r]) * P.rs + (u[r] >> 5), 1u << (u[r] & 31), pol);
         acc.scanned += valid[r];
         acc.found += found;
         stage_push(P, hop, last, s_logok, st, found, sj[r], u[r]);

@@ -138,6 +138,13 @@ class DeviceGraph:
                                              spec.rng_seed, spec.target_unique, spec.relabel, C.byref(h)))
         return cls(h.value)
 
+    def replicate(self, device: int):
+        """A copy of this device graph on `device` (peer copy over NVLink when
+        it is another GPU): load-time replication for k_hop_count_multi."""
+        h = C.c_void_p()
+        _check(_lib.lib().mgk_graph_replicate(self.handle, device, C.byref(h)))
+        return DeviceGraph(h.value, self.node_count)
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             _lib.lib().mgk_graph_free(self._h)
@@ -259,6 +266,29 @@ def walk_targets(graph: DeviceGraph, source: int, min_hops: int, max_hops: int) 
     return ids[: n.value].copy()
 
 
+def k_hop_count_multi(replicas, seeds, k: int, mode=TraverseMode.Exact):
+    """One batch over replicas of the same graph (e.g. one per GPU, made with
+    DeviceGraph.replicate): contiguous seed shards, one host thread per
+    replica, no collective. Same answers and errors as
+    k_hop_count_batch."""
+    reps = list(replicas)
+    if not reps:
+        raise ContractError("no replicas")
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    node_count = reps[0].node_count
+    if node_count < reps[0].nrows and len(seeds):
+        bad = np.flatnonzero(seeds >= node_count)
+        if len(bad):
+            raise ContractError(f"k-hop seed {int(seeds[bad[0]])} is not an allocated node")
+    _check_k(k)
+    counts = np.empty(max(len(seeds), 1), np.uint64)
+    handles = (C.c_void_p * len(reps))(*[r.handle for r in reps])
+    sp = seeds if len(seeds) else np.zeros(1, np.uint64)
+    _check(_lib.lib().mgk_khop_count_multi(handles, len(reps), sp.ctypes.data, len(seeds), int(k), int(mode),
+                                           counts.ctypes.data))
+    return counts[: len(seeds)]
+
+
 def k_hop_count_device(graph: DeviceGraph, d_seeds_ptr: int, nseeds: int, k: int, mode: int,
                        d_counts_ptr: int, stream_ptr: int = 0, engine: int = ENGINE_AUTO):
     """Device-resident batch: uint32 seeds and uint64 counts already in HBM; async on stream."""
@@ -279,5 +309,5 @@ def device_count() -> int:
 
 __all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
-           "k_hop_count_device", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "k_hop_count_device", "k_hop_count_multi", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

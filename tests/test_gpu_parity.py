@@ -333,3 +333,28 @@ def test_relabelled_layout(port, g1, monkeypatch):
         assert np.array_equal(walk_targets(g, int(s), 2, 3), port.walk_targets(rp64, ci64, int(s), 2, 3))
     assert walk_count_batch(g, seeds[:50], 1, 3).tolist() == \
         [len(port.walk_targets(rp64, ci64, int(s), 1, 3)) for s in seeds[:50]]
+
+
+# ---- multi-GPU entry: seed-sharded replicas ------------------------------
+def test_replicas_and_multi(port, g1):
+    """mgk_graph_replicate + mgk_khop_count_multi. This box has one GPU, so the
+    replicas all live on device 0; the sharding, per-replica streams and
+    threads are the same code a multi-GPU node runs."""
+    from paper_1905_01294_b200 import k_hop_count_multi
+    rp, ci, g = g1
+    reps = [g, g.replicate(0), g.replicate(0)]
+    drp, dci = reps[2].csr()
+    assert np.array_equal(drp, rp) and np.array_equal(dci, ci)
+    seeds = H.pick_seeds(rp, 301, 5)
+    for k in (1, 2, 3):
+        for mode in (0, 1):
+            want = k_hop_count_batch(g, seeds, k, mode)
+            assert want.tolist() == oracle_counts(port, rp, ci, seeds[:40], k, mode) + want.tolist()[40:]
+            for nrep in (1, 2, 3):
+                assert k_hop_count_multi(reps[:nrep], seeds, k, mode).tolist() == want.tolist(), (k, mode, nrep)
+    assert k_hop_count_multi(reps, seeds[:2], 2).tolist() == k_hop_count_batch(g, seeds[:2], 2).tolist()
+    assert k_hop_count_multi(reps, [], 2).tolist() == []
+    with pytest.raises(ContractError, match="k-hop seed 99999999 is not an allocated node"):
+        k_hop_count_multi(reps, [int(seeds[0]), 99999999], 2)
+    with pytest.raises(ContractError, match=r"k-hop count 0 outside \[1, 32\]"):
+        k_hop_count_multi(reps, seeds, 0)
