@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define MGK_ABI_VERSION 1
+#define MGK_ABI_VERSION 2
 
 /* status codes */
 #define MGK_OK 0
@@ -186,6 +186,7 @@ typedef struct mgk_tuning {
     uint32_t force_dir;
     uint32_t lanes_words;
     uint32_t alpha_lanes;
+    uint32_t alpha_last;  /* SINGLE, last hop: push -> pull when frontier edges * alpha_last > unexplored */
 } mgk_tuning;
 int mgk_graph_set_tuning(mgk_graph* g, const mgk_tuning* t);
 int mgk_graph_get_tuning(const mgk_graph* g, mgk_tuning* t);

@@ -46,7 +46,7 @@ class MgkStats(C.Structure):
 
 class MgkTuning(C.Structure):
     _fields_ = [("alpha", C.c_uint32), ("beta", C.c_uint32), ("force_dir", C.c_uint32),
-                ("lanes_words", C.c_uint32), ("alpha_lanes", C.c_uint32)]
+                ("lanes_words", C.c_uint32), ("alpha_lanes", C.c_uint32), ("alpha_last", C.c_uint32)]
 
 
 # (name, restype, argtypes) for every symbol include/mgk.h declares

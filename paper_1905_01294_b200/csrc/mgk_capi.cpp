@@ -488,6 +488,7 @@ int mgk_graph_set_tuning(mgk_graph* h, const mgk_tuning* t) {
     std::lock_guard<std::mutex> lk(h->g.mu);
     if (t->alpha) h->g.tuning.alpha = t->alpha;
     if (t->alpha_lanes) h->g.tuning.alpha_lanes = t->alpha_lanes;
+    if (t->alpha_last) h->g.tuning.alpha_last = t->alpha_last;
     if (t->beta) h->g.tuning.beta = t->beta;
     h->g.tuning.force_dir = t->force_dir;
     h->g.tuning.lanes_words = t->lanes_words;
@@ -498,6 +499,7 @@ int mgk_graph_get_tuning(const mgk_graph* h, mgk_tuning* t) {
     if (!h || !t) return fail(MGK_ECONTRACT, "null argument");
     t->alpha = h->g.tuning.alpha;
     t->alpha_lanes = h->g.tuning.alpha_lanes;
+    t->alpha_last = h->g.tuning.alpha_last;
     t->beta = h->g.tuning.beta;
     t->force_dir = h->g.tuning.force_dir;
     t->lanes_words = h->g.tuning.lanes_words;

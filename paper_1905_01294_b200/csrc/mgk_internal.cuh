@@ -67,11 +67,15 @@ struct QCtl {
 };
 
 struct Tuning {
-    uint32_t alpha = 15;  // push -> pull when frontier edges > unexplored in-edges / alpha
+    uint32_t alpha = 4;   // push -> pull when frontier edges > unexplored in-edges / alpha
     uint32_t beta = 24;   // pull -> push when frontier vertices < n / beta
     uint32_t force_dir = 0;
     uint32_t lanes_words = 0;  // 0 = auto
     uint32_t alpha_lanes = 2;  // LANES: a pull pass rarely exits early, so switch later
+    // SINGLE's last hop only counts: a push is one fire-and-forget red.or per
+    // edge, a pull must settle every unvisited vertex, so pull only when the
+    // frontier's out-edges exceed the whole unexplored in-edge set
+    uint32_t alpha_last = 1;
 };
 
 // Workspace for one in-flight call. Sized for the graph; reused across calls.

@@ -83,7 +83,7 @@ struct FRParams {
     FRCtl* ctl;
     unsigned int* bar;
     LevelCounters* lc;
-    uint32_t alpha, beta, force_dir;
+    uint32_t alpha, beta, force_dir, alpha_last;
     uint32_t* snap;  // keep_result: slot 0's visited bitmap after hop min_hop - 1
     uint32_t quota;  // per-seed log entries before the seed is cleared densely
     uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
@@ -624,12 +624,14 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
                 const uint8_t prev = P.dirs[((hop - 1) & 1) * S + slot];
                 if (nf == 0) {
                     d = kDead;
+                } else if (mf & kOverflowBit) {  // the item list overflowed: pull needs no items
+                    d = kPull;
                 } else if (P.force_dir == 1) {
                     d = kPush;
-                } else if (P.force_dir == 2 || (mf & kOverflowBit)) {
+                } else if (P.force_dir == 2) {
                     d = kPull;
                 } else if (prev == kPush) {
-                    d = mf * P.alpha > mu ? kPull : kPush;
+                    d = mf * (last ? P.alpha_last : P.alpha) > mu ? kPull : kPush;
                 } else {
                     d = nf * P.beta >= g.n ? kPull : kPush;
                 }
@@ -1038,6 +1040,7 @@ cudaError_t launch_single(Launch& L) {
     P.alpha = L.tuning.alpha;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
+    P.alpha_last = L.tuning.alpha_last;
     P.quota = ws->fr_quota;
     P.keep_result = L.keep_result ? 1u : 0u;
     P.fuse1 = (gr->dg.rows_unique && L.seed_visited && L.k >= 2 && !L.keep_result && !fuse_disabled())

@@ -77,11 +77,12 @@ class KHopQuery:
 
 @dataclass
 class Tuning:
-    alpha: int = 15
+    alpha: int = 4
     beta: int = 24
     force_dir: int = 0   # 0 auto, 1 push only, 2 pull only
     lanes_words: int = 0  # 0 auto; else 1, 2, 4, 8 (x64 seeds per batch)
     alpha_lanes: int = 2
+    alpha_last: int = 1
 
 
 class DeviceGraph:
@@ -183,13 +184,13 @@ class DeviceGraph:
         return int(_lib.lib().mgk_graph_device_bytes(self._h))
 
     def set_tuning(self, t: Tuning):
-        tt = MgkTuning(t.alpha, t.beta, t.force_dir, t.lanes_words, t.alpha_lanes)
+        tt = MgkTuning(t.alpha, t.beta, t.force_dir, t.lanes_words, t.alpha_lanes, t.alpha_last)
         _check(_lib.lib().mgk_graph_set_tuning(self._h, C.byref(tt)))
 
     def get_tuning(self) -> Tuning:
         tt = MgkTuning()
         _check(_lib.lib().mgk_graph_get_tuning(self._h, C.byref(tt)))
-        return Tuning(tt.alpha, tt.beta, tt.force_dir, tt.lanes_words, tt.alpha_lanes)
+        return Tuning(tt.alpha, tt.beta, tt.force_dir, tt.lanes_words, tt.alpha_lanes, tt.alpha_last)
 
     def _check_seed(self, seed: int):
         if seed < 0 or seed >= self.node_count:

@@ -31,7 +31,7 @@ def test_header_symbols_exported():
 
 def test_abi_version_and_no_gpu_is_loud():
     L = _lib.lib()
-    assert L.mgk_abi_version() == 1
+    assert L.mgk_abi_version() == 2
     if L.mgk_device_count() == 0:
         h = C.c_void_p()
         rp = np.array([0, 0], np.uint32)

@@ -218,6 +218,21 @@ def test_g2_properties(g2):
     assert (single == cum6[:4]).all()
 
 
+def test_g2_single_directions_at_depth(g2):
+    """300 seeds x k=6 in the SINGLE engine: the push item lists overflow (the
+    engine then pulls those seeds, even when push is forced) and every
+    direction policy gives the same answers."""
+    rp, ci, g = g2
+    seeds = H.pick_seeds(rp, 300, 1)
+    want = k_hop_count_batch(g, seeds, 6, 0, engine=ENGINE_LANES)
+    try:
+        for t in (Tuning(), Tuning(force_dir=1), Tuning(force_dir=2), Tuning(alpha=60, alpha_last=60)):
+            g.set_tuning(t)
+            assert (k_hop_count_batch(g, seeds, 6, 0, engine=ENGINE_SINGLE) == want).all(), t
+    finally:
+        g.set_tuning(Tuning())
+
+
 @pytest.mark.parametrize("force", [0, 1, 2])
 def test_frontier_ids_deep(port, g1, force):
     """k_hop_frontier's sorted ids (exact and cumulative) at depth, every direction."""
