@@ -41,6 +41,7 @@ extern "C" {
 #define MGK_ECUDA 3     /* CUDA runtime / launch failure (matgraph::Error) */
 #define MGK_ENOMEM 4    /* device or host allocation failed */
 #define MGK_ERANGE 5    /* graph exceeds uint32 device indices (n or nnz >= 2^32) */
+#define MGK_ESNAPSHOT 6 /* malformed GRAPHSNAP1 text (SnapshotError): "snapshot parse error at line N: ..." */
 
 /* TraverseMode, proj/core/include/matgraph/plan.hpp:17 */
 #define MGK_EXACT 0
@@ -110,6 +111,20 @@ int mgk_graph_from_edges(int device, uint64_t nrows, uint64_t nedges, const uint
  * mgk_graph_download_csr. (BASELINE cfg4: 1.47B edges in seconds.) */
 int mgk_graph_gen_rmat(int device, uint32_t scale, uint32_t edge_factor, double a, double b, double c,
                        uint64_t rng_seed, uint64_t target_unique, int relabel, mgk_graph** out);
+/* GRAPHSNAP1 load (snapshot_from_string / snapshot_load, snapshot.cpp:162-259,
+ * then relation_matrix): the text is parsed on the GPU, one thread per line,
+ * and the edges of `relation` (NULL = ANY) become the device CSR + CSC. The
+ * matrix dimension is the store's capacity max(NODES, 16) (graph.cpp:15-30);
+ * *node_count receives NODES (seeds are checked against it by callers, like
+ * KHopQuery against node_count). Labels and properties are validated, not
+ * kept. A malformed text fails with MGK_ESNAPSHOT and the reference's exact
+ * SnapshotError message; a missing file with "cannot open '<path>' for reading".
+ * mgk_snapshot_check runs the same grammar on the host only (no GPU). */
+int mgk_graph_load_snapshot(int device, const char* text, uint64_t len, const char* relation,
+                            mgk_graph** out, uint64_t* node_count);
+int mgk_graph_load_snapshot_file(int device, const char* path, const char* relation, mgk_graph** out,
+                                 uint64_t* node_count);
+int mgk_snapshot_check(const char* text, uint64_t len, uint64_t* node_count, uint64_t* edge_count);
 int mgk_graph_free(mgk_graph* g);
 int mgk_graph_info(const mgk_graph* g, uint64_t* nrows, uint64_t* nnz, int* device);
 /* Copy the device CSR back (uint32; either pointer may be NULL). */
@@ -215,6 +230,13 @@ int mgk_gen_rmat_csr(uint32_t scale, uint32_t edge_factor, double a, double b, d
  * "need {n} seeds but only {e} nodes have out-degree >= 1" when short. */
 int mgk_pick_seeds_csr(uint64_t nrows, const uint32_t* row_ptr, uint64_t n, uint64_t rng_seed,
                        uint64_t* out);
+/* snapshot_to_string (snapshot.cpp:127-160) of a one-relation graph given as a
+ * CSR over node_count nodes without labels, each node carrying {"id": i} when
+ * id_props != 0 (exactly what build_bench_graph stores, bench.cpp:185-198):
+ * byte-identical to the reference writer for such graphs. Call with out=NULL
+ * for the size. Host only (multi-threaded). */
+int mgk_snapshot_write_csr(uint64_t node_count, const uint32_t* row_ptr, const uint32_t* col_idx,
+                           const char* relation, int id_props, char* out, uint64_t cap, uint64_t* n_out);
 
 #ifdef __cplusplus
 }

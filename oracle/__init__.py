@@ -187,6 +187,10 @@ class Ref:
         L.ref_cypher.argtypes = [vp, C.c_char_p, C.c_char_p, u64, C.POINTER(u64)]
         L.ref_rmat_generate.argtypes = [u32, u32, C.c_double, C.c_double, C.c_double, C.c_double,
                                         u64, vp, vp, C.POINTER(u64)]
+        L.ref_graph_create_node_full.argtypes = [vp, C.c_char_p, C.c_char_p]
+        L.ref_graph_create_edge_props.argtypes = [vp, u64, C.c_char_p, u64, C.c_char_p]
+        L.ref_snapshot_parse.argtypes = [C.c_char_p, u64, C.POINTER(vp)]
+        L.ref_snapshot_to_string.argtypes = [vp, C.c_char_p, u64, C.POINTER(u64)]
         L.ref_bfs_oracle_new.restype = vp
         L.ref_bfs_oracle_new.argtypes = [vp, vp, u64, u64]
         L.ref_bfs_oracle_count.argtypes = [vp, u64, u32, C.c_int, C.POINTER(u64)]
@@ -206,6 +210,12 @@ class Ref:
         h = C.c_void_p()
         self._check(self.lib.ref_build_bench_graph(src.ctypes.data, dst.ctypes.data, len(src),
                                                    node_count, C.byref(h)))
+        return RefGraph(self, h.value)
+
+    def snapshot_parse(self, text: bytes):
+        """snapshot_from_string (snapshot.cpp:162-231); raises RefError with its message."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_snapshot_parse(text, len(text), C.byref(h)))
         return RefGraph(self, h.value)
 
     def rmat_generate(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, d=0.05, rng_seed=1):
@@ -239,8 +249,23 @@ class RefGraph:
     def create_nodes(self, count):
         self.ref._check(self.ref.lib.ref_graph_create_nodes(self.h, count))
 
-    def create_edge(self, src, relation, dst):
-        self.ref._check(self.ref.lib.ref_graph_create_edge(self.h, src, relation.encode(), dst))
+    def create_edge(self, src, relation, dst, props=""):
+        if props:
+            self.ref._check(self.ref.lib.ref_graph_create_edge_props(self.h, src, relation.encode(), dst,
+                                                                     props.encode()))
+        else:
+            self.ref._check(self.ref.lib.ref_graph_create_edge(self.h, src, relation.encode(), dst))
+
+    def create_node(self, labels="", props=""):
+        self.ref._check(self.ref.lib.ref_graph_create_node_full(self.h, labels.encode(), props.encode()))
+
+    def snapshot(self) -> bytes:
+        """snapshot_to_string (snapshot.cpp:127-160): the reference's canonical text."""
+        n = C.c_uint64()
+        self.ref._check(self.ref.lib.ref_snapshot_to_string(self.h, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        self.ref._check(self.ref.lib.ref_snapshot_to_string(self.h, buf, n.value + 1, C.byref(n)))
+        return buf.raw[: n.value]
 
     @property
     def node_count(self):

@@ -10,6 +10,7 @@
 //   pick_seeds             proj/core/src/bench.cpp:200-218
 //   rmat_generate          proj/core/src/bench.cpp:107-137
 //   BfsOracle::count       proj/core/src/bench.cpp:233-259
+//   snapshot_from_string / snapshot_to_string   proj/core/src/snapshot.cpp:127-231
 // Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
 // --impl reference) may load this library.
 #include <atomic>
@@ -27,6 +28,7 @@
 #include "matgraph/error.hpp"
 #include "matgraph/execute.hpp"
 #include "matgraph/graph.hpp"
+#include "matgraph/snapshot.hpp"
 
 using matgraph_ref::PropertyGraph;
 
@@ -87,6 +89,50 @@ int ref_build_bench_graph(const uint32_t* src, const uint32_t* dst, uint64_t m,
     try {
         auto edges = to_edges(src, dst, m);
         *out = new PropertyGraph(matgraph_ref::build_bench_graph(edges, node_count));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// A node with labels ("a,b" or "") and a <props> field in snapshot encoding.
+int ref_graph_create_node_full(void* g, const char* labels_csv, const char* props_field) {
+    try {
+        std::vector<std::string> labels;
+        std::string csv(labels_csv);
+        size_t start = 0;
+        while (!csv.empty()) {
+            const size_t pos = csv.find(',', start);
+            labels.push_back(csv.substr(start, pos == std::string::npos ? std::string::npos : pos - start));
+            if (pos == std::string::npos) break;
+            start = pos + 1;
+        }
+        static_cast<PropertyGraph*>(g)->create_node(labels, matgraph_ref::decode_props(props_field));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+int ref_graph_create_edge_props(void* g, uint64_t src, const char* relation, uint64_t dst,
+                                const char* props_field) {
+    try {
+        static_cast<PropertyGraph*>(g)->create_edge(src, relation, dst, matgraph_ref::decode_props(props_field));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// snapshot_from_string over text[0, len) (text[len] must be readable: the
+// reference may peek one byte past a props item, see make_golden.py).
+int ref_snapshot_parse(const char* text, uint64_t len, void** out) {
+    try {
+        *out = new PropertyGraph(matgraph_ref::snapshot_from_string(std::string_view(text, len)));
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// snapshot_to_string: size first (out may be NULL), then the bytes.
+int ref_snapshot_to_string(void* g, char* out, uint64_t cap, uint64_t* n) {
+    try {
+        const std::string s = matgraph_ref::snapshot_to_string(*static_cast<PropertyGraph*>(g));
+        *n = s.size();
+        if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }

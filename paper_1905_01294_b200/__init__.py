@@ -5,7 +5,8 @@ include/mgk.h); this package is the Python host mirror of the reference's
 interface (proj/core/include/matgraph/execute.hpp, bench.hpp). See DESIGN.md.
 """
 from .khop import (  # noqa: F401
-    ENGINE_AUTO, ENGINE_LANES, ENGINE_SINGLE, K_MAX_HOPS, ContractError, DeviceError, DeviceGraph,
+    ENGINE_AUTO, ENGINE_LANES, ENGINE_SINGLE, K_MAX_HOPS, ContractError, DeviceError, DeviceGraph, SnapshotError,
+    snapshot_check,
     Error, HarnessError, KHopQuery, TraverseMode, Tuning, device_count, device_stats, k_hop_count,
     k_hop_count_batch, k_hop_count_device, k_hop_count_multi, k_hop_frontier, walk_count_batch, walk_targets)
 

@@ -13,7 +13,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libmgk.so"
 
-MGK_OK, MGK_ECONTRACT, MGK_EHARNESS, MGK_ECUDA, MGK_ENOMEM, MGK_ERANGE = range(6)
+MGK_OK, MGK_ECONTRACT, MGK_EHARNESS, MGK_ECUDA, MGK_ENOMEM, MGK_ERANGE, MGK_ESNAPSHOT = range(7)
 ENGINE_AUTO, ENGINE_SINGLE, ENGINE_LANES = 0, 1, 2
 MAX_HOPS = 32
 
@@ -58,6 +58,9 @@ SIGNATURES = [
     ("mgk_graph_from_edges", _int, [_int, _u64, _u64, _vp, _vp, C.POINTER(_vp)]),
     ("mgk_graph_gen_rmat", _int, [_int, _u32, _u32, C.c_double, C.c_double, C.c_double, _u64, _u64, _int,
                                   C.POINTER(_vp)]),
+    ("mgk_graph_load_snapshot", _int, [_int, C.c_char_p, _u64, C.c_char_p, C.POINTER(_vp), _u64p]),
+    ("mgk_graph_load_snapshot_file", _int, [_int, C.c_char_p, C.c_char_p, C.POINTER(_vp), _u64p]),
+    ("mgk_snapshot_check", _int, [C.c_char_p, _u64, _u64p, _u64p]),
     ("mgk_graph_free", _int, [_vp]),
     ("mgk_graph_info", _int, [_vp, _u64p, _u64p, C.POINTER(_int)]),
     ("mgk_graph_download_csr", _int, [_vp, _vp, _vp]),
@@ -80,6 +83,7 @@ SIGNATURES = [
     ("mgk_gen_rmat_csr", _int, [_u32, _u32, C.c_double, C.c_double, C.c_double, _u64, _u64, _int,
                                 _int, _u64p, _u64p, _vp, _vp]),
     ("mgk_pick_seeds_csr", _int, [_u64, _vp, _u64, _u64, _vp]),
+    ("mgk_snapshot_write_csr", _int, [_u64, _vp, _vp, C.c_char_p, _int, _vp, _u64, _u64p]),
 ]
 
 _lib = None

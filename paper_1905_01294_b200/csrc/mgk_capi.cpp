@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <new>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
@@ -429,6 +430,59 @@ int mgk_graph_gen_rmat(int device, uint32_t scale, uint32_t edge_factor, double 
     }
     *out = h;
     return MGK_OK;
+}
+
+int mgk_snapshot_check(const char* text, uint64_t len, uint64_t* node_count, uint64_t* edge_count) {
+    if ((!text && len) || !node_count || !edge_count) return fail(MGK_ECONTRACT, "null argument");
+    std::optional<std::string> err;
+    try {
+        err = snap::check_all(std::string_view(text ? text : "", len), node_count, edge_count);
+    } catch (const std::bad_alloc&) {
+        return fail(MGK_ENOMEM, "out of host memory");
+    }
+    if (err) return fail(MGK_ESNAPSHOT, "%s", err->c_str());
+    return MGK_OK;
+}
+
+int mgk_graph_load_snapshot(int device, const char* text, uint64_t len, const char* relation,
+                            mgk_graph** out, uint64_t* node_count) {
+    if (!out || !node_count || (!text && len)) return fail(MGK_ECONTRACT, "null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MGK_ECUDA, "no CUDA device available");
+    }
+    if (device < 0 || device >= ndev) return fail(MGK_ECONTRACT, "device %d out of range [0, %d)", device, ndev);
+    DeviceGuard dg(device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = device;
+    std::string err;
+    cudaError_t e = snap::load_to_graph(&h->g, text ? text : "", len, relation, node_count, &err);
+    if (e || !err.empty()) {
+        free_device_graph(&h->g);
+        delete h;
+        if (!err.empty()) return fail(MGK_ESNAPSHOT, "%s", err.c_str());
+        return e == cudaErrorInvalidValue ? fail(MGK_ERANGE, "graph exceeds uint32 device indices")
+                                          : fail_cuda(e, "snapshot load");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
+int mgk_graph_load_snapshot_file(int device, const char* path, const char* relation, mgk_graph** out,
+                                 uint64_t* node_count) {
+    if (!path) return fail(MGK_ECONTRACT, "null argument");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(MGK_ESNAPSHOT, "cannot open '%s' for reading", path);
+    std::string text;
+    char buf[1 << 16];
+    size_t got = 0;
+    while ((got = std::fread(buf, 1, sizeof buf, f)) > 0) text.append(buf, got);
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad) return fail(MGK_ESNAPSHOT, "failed reading snapshot from '%s'", path);
+    return mgk_graph_load_snapshot(device, text.data(), text.size(), relation, out, node_count);
 }
 
 int mgk_graph_free(mgk_graph* h) {

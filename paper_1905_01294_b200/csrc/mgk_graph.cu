@@ -619,6 +619,36 @@ cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
     return cudaDeviceSynchronize();
 }
 
+// sort + unique (src << 32 | dst) keys, then CSR + CSC (keys/alt: m entries each, consumed)
+cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
+                            cudaStream_t s) {
+    uint64_t mu = 0;
+    if (m) {
+        MGK_TRY(radix_sort_keys(keys, alt, m, 32 + key_bits(g->dg.n), s));
+        uint32_t* keep = nullptr;
+        unsigned long long* d_num = nullptr;
+        MGK_TRY(cudaMallocAsync(&keep, m * 4, s));
+        MGK_TRY(cudaMallocAsync(&d_num, 8, s));
+        mark_unique<<<blocks_for(m), kTB, 0, s>>>(keys, m, keep);
+        size_t tmp = 0;
+        MGK_TRY(cub::DeviceSelect::Flagged(nullptr, tmp, keys, keep, alt, d_num, (int64_t)m, s));
+        void* t = nullptr;
+        MGK_TRY(cudaMallocAsync(&t, tmp, s));
+        MGK_TRY(cub::DeviceSelect::Flagged(t, tmp, keys, keep, alt, d_num, (int64_t)m, s));
+        unsigned long long h_num = 0;
+        MGK_TRY(cudaMemcpyAsync(&h_num, d_num, 8, cudaMemcpyDeviceToHost, s));
+        MGK_TRY(cudaStreamSynchronize(s));
+        cudaFreeAsync(t, s);
+        cudaFreeAsync(d_num, s);
+        cudaFreeAsync(keep, s);
+        std::swap(keys, alt);
+        mu = h_num;
+    }
+    if (mu >= 0xFFFFFFFFull) return cudaErrorInvalidValue;
+    MGK_TRY(graph_from_sorted_keys(g, keys, alt, mu, s));
+    return cudaStreamSynchronize(s);
+}
+
 void free_device_graph(Graph* g) {
     cudaFree(g->rp);
     cudaFree(g->ci);

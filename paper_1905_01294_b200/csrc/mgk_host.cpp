@@ -347,4 +347,81 @@ int mgk_pick_seeds_csr(uint64_t nrows, const uint32_t* row_ptr, uint64_t n, uint
     return MGK_OK;
 }
 
+int mgk_snapshot_write_csr(uint64_t node_count, const uint32_t* row_ptr, const uint32_t* col_idx,
+                           const char* relation, int id_props, char* out, uint64_t cap, uint64_t* n_out) {
+    if (!row_ptr || !relation || !n_out || (cap && !out)) {
+        mgk::set_last_error("null argument");
+        return MGK_ECONTRACT;
+    }
+    // per-row byte counts (node line + its edge lines), then a prefix sum, so
+    // every thread can format its rows in place
+    const std::string rel(relation);
+    auto digits = [](uint64_t v) {
+        int d = 1;
+        while (v >= 10) v /= 10, ++d;
+        return (uint64_t)d;
+    };
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<uint64_t> node_bytes(node_count + 1, 0), edge_bytes(node_count + 1, 0);
+    auto par = [&](auto&& f) {
+        std::vector<std::thread> ts;
+        const uint64_t step = (node_count + nt - 1) / nt;
+        for (unsigned t = 0; t < nt; ++t) {
+            const uint64_t a = t * step, b = std::min<uint64_t>(node_count, a + step);
+            if (a < b) ts.emplace_back([&f, a, b] { f(a, b); });
+        }
+        for (auto& t : ts) t.join();
+    };
+    par([&](uint64_t a, uint64_t b) {
+        for (uint64_t v = a; v < b; ++v) {
+            const uint64_t dv = digits(v);
+            node_bytes[v] = dv + 2 + (id_props ? 5 + dv : 0) + 1;  // "v\t\tid:i:v\n"
+            uint64_t eb = 0;
+            for (uint32_t p = row_ptr[v]; p < row_ptr[v + 1]; ++p)
+                eb += dv + 1 + rel.size() + 1 + digits(col_idx[p]) + 2;  // "v\tREL\tu\t\n"
+            edge_bytes[v] = eb;
+        }
+    });
+    const std::string head = "GRAPHSNAP1\nNODES " + std::to_string(node_count) + "\n";
+    const std::string mid = "EDGES " + std::to_string(node_count ? (uint64_t)row_ptr[node_count] : 0) + "\n";
+    uint64_t nb = 0, eb = 0;
+    for (uint64_t v = 0; v < node_count; ++v) {
+        const uint64_t x = node_bytes[v], y = edge_bytes[v];
+        node_bytes[v] = nb, edge_bytes[v] = eb;
+        nb += x, eb += y;
+    }
+    const uint64_t total = head.size() + nb + mid.size() + eb;
+    *n_out = total;
+    if (!out) return MGK_OK;
+    if (cap < total) {
+        mgk::set_last_error("output buffer too small");
+        return MGK_ECONTRACT;
+    }
+    std::memcpy(out, head.data(), head.size());
+    char* nodes = out + head.size();
+    std::memcpy(nodes + nb, mid.data(), mid.size());
+    char* edges = nodes + nb + mid.size();
+    par([&](uint64_t a, uint64_t b) {
+        char num[24];
+        for (uint64_t v = a; v < b; ++v) {
+            const int dv = snprintf(num, sizeof num, "%llu", (unsigned long long)v);
+            char* p = nodes + node_bytes[v];
+            std::memcpy(p, num, dv), p += dv;
+            *p++ = '\t', *p++ = '\t';
+            if (id_props) std::memcpy(p, "id:i:", 5), p += 5, std::memcpy(p, num, dv), p += dv;
+            *p++ = '\n';
+            char* q = edges + edge_bytes[v];
+            for (uint32_t e = row_ptr[v]; e < row_ptr[v + 1]; ++e) {
+                std::memcpy(q, num, dv), q += dv;
+                *q++ = '\t';
+                std::memcpy(q, rel.data(), rel.size()), q += rel.size();
+                *q++ = '\t';
+                q += snprintf(q, 24, "%u", col_idx[e]);
+                *q++ = '\t', *q++ = '\n';
+            }
+        }
+    });
+    return MGK_OK;
+}
+
 }  // extern "C"

@@ -6,7 +6,9 @@
 #include <cstdint>
 #include <memory>
 #include <mutex>
+#include <optional>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "mgk.h"
@@ -198,6 +200,19 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
                                          int relabel);
 void free_device_graph(Graph* g);
 cudaError_t replicate_device_graph(const Graph* src, Graph* dst);
+// sort + unique (src << 32 | dst) keys into g (g->dg.n set; keys/alt hold m
+// entries each and are consumed); cudaErrorInvalidValue if >= 2^32 remain
+cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
+                            cudaStream_t s);
+cudaError_t locality_relabel(Graph* g, cudaStream_t s);
+
+// GRAPHSNAP1 (mgk_snapshot.cu): the reference's grammar checked sequentially on
+// the host, and the GPU loader (empty *err on success)
+namespace snap {
+std::optional<std::string> check_all(std::string_view text, uint64_t* n_out, uint64_t* m_out);
+cudaError_t load_to_graph(Graph* g, const char* text, uint64_t len, const char* relation, uint64_t* node_count,
+                          std::string* err);
+}  // namespace snap
 // CSR / CSC in external ids into host buffers (un-relabelled when relabelled)
 cudaError_t download_graph(const Graph* g, uint32_t* h_rp, uint32_t* h_ci, uint32_t* h_cp, uint32_t* h_ri);
 // device ids (scattered from a bitmap) -> external ids, ascending

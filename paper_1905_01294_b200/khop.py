@@ -44,6 +44,10 @@ class DeviceError(Error):
     """A CUDA failure inside the engine (reported as matgraph::Error)."""
 
 
+class SnapshotError(Error):
+    """matgraph::SnapshotError (error.hpp:52-61): malformed GRAPHSNAP1 text."""
+
+
 def _raise(rc: int):
     msg = _lib.last_error()
     if rc == _lib.MGK_ECONTRACT:
@@ -52,6 +56,8 @@ def _raise(rc: int):
         raise HarnessError(msg)
     if rc == _lib.MGK_ERANGE:
         raise ContractError(msg)
+    if rc == _lib.MGK_ESNAPSHOT:
+        raise SnapshotError(msg)
     raise DeviceError(msg)
 
 
@@ -138,6 +144,22 @@ class DeviceGraph:
         _check(_lib.lib().mgk_graph_gen_rmat(device, spec.scale, spec.edge_factor, spec.a, spec.b, spec.c,
                                              spec.rng_seed, spec.target_unique, spec.relabel, C.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def from_snapshot(cls, text=None, path=None, relation: str | None = None, device: int = 0):
+        """GRAPHSNAP1 text (bytes) or file -> the device matrix of `relation`
+        (None = ANY), parsed on the GPU (snapshot.cpp:162-259 + relation_matrix).
+        node_count = the snapshot's NODES; malformed input raises SnapshotError
+        with the reference's message."""
+        h = C.c_void_p()
+        n = C.c_uint64()
+        rel = relation.encode() if relation is not None else None
+        if path is not None:
+            _check(_lib.lib().mgk_graph_load_snapshot_file(device, str(path).encode(), rel, C.byref(h), C.byref(n)))
+        else:
+            text = bytes(text)
+            _check(_lib.lib().mgk_graph_load_snapshot(device, text, len(text), rel, C.byref(h), C.byref(n)))
+        return cls(h.value, n.value)
 
     def replicate(self, device: int):
         """A copy of this device graph on `device` (peer copy over NVLink when
@@ -267,6 +289,14 @@ def walk_targets(graph: DeviceGraph, source: int, min_hops: int, max_hops: int) 
     return ids[: n.value].copy()
 
 
+def snapshot_check(text: bytes):
+    """The GRAPHSNAP1 grammar on the host only (no GPU): (NODES, EDGES) or SnapshotError."""
+    text = bytes(text)
+    n, m = C.c_uint64(), C.c_uint64()
+    _check(_lib.lib().mgk_snapshot_check(text, len(text), C.byref(n), C.byref(m)))
+    return n.value, m.value
+
+
 def k_hop_count_multi(replicas, seeds, k: int, mode=TraverseMode.Exact):
     """One batch over replicas of the same graph (e.g. one per GPU, made with
     DeviceGraph.replicate): contiguous seed shards, one host thread per
@@ -308,7 +338,7 @@ def device_count() -> int:
     return int(_lib.lib().mgk_device_count())
 
 
-__all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "TraverseMode", "KHopQuery",
+__all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
            "k_hop_count_device", "k_hop_count_multi", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

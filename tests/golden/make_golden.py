@@ -18,6 +18,10 @@ through oracle/ref_capi.cpp:
   with a SHA-256 of each generated edge list and of its flushed CSR.
 * harness_pins.json — rmat_generate / pick_seeds pins (proj/tests/
   test_bench.cpp:33-113 shapes) and a few sorted k_hop_frontier id lists.
+* snapshot_pins.json — GRAPHSNAP1 texts (snapshot.cpp) parsed by the
+  reference's snapshot_from_string: node count and relation CSRs of valid
+  texts (some written by the reference's own snapshot_to_string), and the
+  exact SnapshotError message of malformed ones.
 * walk_pins.json — walk_targets (execute.cpp:43-60, the VarLenTraverse step)
   through the reference's own Cypher executor: counts and ids of
   MATCH (a {id: S})-[*min..max]->(b) on RMAT graphs and a cycle with a loop.
@@ -192,10 +196,111 @@ def walk_pins(R: oracle.Ref) -> dict:
     return out
 
 
+def snapshot_pins(R: oracle.Ref) -> dict:
+    """GRAPHSNAP1 (snapshot.cpp:127-231) through the reference parser/writer."""
+    def csrs(g, rels):
+        out = {}
+        for r in rels:
+            rp, ci = g.relation_csr(r)
+            out["ANY" if r is None else r] = {"row_ptr": [int(x) for x in rp], "col_idx": [int(x) for x in ci]}
+        return out
+
+    valid, errors = [], []
+    # 1. written by the reference: labels, every property type, two relations,
+    #    a re-created edge (props overwritten), a self-loop
+    g = R.graph(4)
+    g.create_node("Person", "name:s:Ann%20Lee;age:i:31;score:f:1.5")
+    g.create_node("Person,Admin", "ok:b:true;w:f:-0.25")
+    g.create_node("", "")
+    g.create_node("City", "big:f:1e10;t:s:a%3Bb%3Ac%25")
+    g.create_node("", "inf:f:inf")
+    for e in ((0, "KNOWS", 1, ""), (1, "KNOWS", 2, "since:i:2001"), (2, "LIKES", 0, ""), (0, "LIKES", 3, "w:f:0.5"),
+              (3, "KNOWS", 3, ""), (1, "KNOWS", 2, "since:i:2002"), (4, "LIKES", 1, "")):
+        g.create_edge(*e)
+    t1 = g.snapshot()
+    rels = [None, "KNOWS", "LIKES", "NOPE"]
+    valid.append({"name": "writer_props_labels", "text": t1.decode(), "node_count": 5,
+                  "csr": csrs(R.snapshot_parse(t1), rels)})
+    # 2. hand-written: non-canonical order, duplicate lines, exotic literals the
+    #    GPU fast path leaves to the host, blank trailing lines, no final newline
+    t2 = ("GRAPHSNAP1\nNODES 6\n0\t\tx:f:.5\n1\tA\t\n2\t\ty:f:5.;z:i:-0\n3\t\t\n4\t\tq:s:\n5\t\t\n"
+          "EDGES 9\n5\tR\t0\t\n0\tS\t1\t\n0\tR\t1\t\n0\tR\t1\tw:f:INF\n3\tR\t3\t\n2\tS\t4\tk:b:false\n"
+          "4\tR\t2\t\n1\tR\t0\tk:i:-9223372036854775808\n0000002\tS\t0005\t\n\n\n").encode()
+    valid.append({"name": "hand_unordered", "text": t2.decode(), "node_count": 6,
+                  "csr": csrs(R.snapshot_parse(t2), [None, "R", "S", "T"])})
+    t3 = b"GRAPHSNAP1\nNODES 0\nEDGES 0"
+    valid.append({"name": "empty_graph", "text": t3.decode(), "node_count": 0,
+                  "csr": csrs(R.snapshot_parse(t3), [None])})
+    t4 = b"GRAPHSNAP1\nNODES 20\n" + b"".join(b"%d\t\t\n" % i for i in range(20)) + b"EDGES 2\n19\tE\t0\t\n0\tE\t19\t"
+    valid.append({"name": "no_final_newline", "text": t4.decode(), "node_count": 20,
+                  "csr": csrs(R.snapshot_parse(t4), [None, "E"])})
+    # 3. a bench graph written by the reference (scale 9 RMAT, "EDGE" + ANY)
+    src, dst = R.rmat_generate(9, rng_seed=5)
+    bg = R.build_bench_graph(src, dst, 1 << 9)
+    tb = bg.snapshot()
+    pg = R.snapshot_parse(tb)
+    rp, ci = pg.relation_csr(None)
+    bench = {"scale": 9, "rng_seed": 5, "text_sha256": hashlib.sha256(tb).hexdigest(), "bytes": len(tb),
+             "node_count": pg.node_count, "any_csr_sha256": sha(rp, ci),
+             "edge_csr_sha256": sha(*pg.relation_csr("EDGE")),
+             "counts_k2": [pg.k_hop_count(int(s), 2) for s in pg.pick_seeds(8, 1)],
+             "seeds": [int(s) for s in pg.pick_seeds(8, 1)]}
+    # 4. malformed texts: the reference's exact message
+    H = b"GRAPHSNAP1\nNODES 3\n0\t\t\n1\tA,B\tx:i:5\n2\t\t\n"
+    bad = {
+        "empty": b"", "header_crlf": H.replace(b"\n", b"\r\n") + b"EDGES 0\r\n",
+        "header_space": b"GRAPHSNAP1 \nNODES 0\nEDGES 0\n", "no_nodes_line": b"GRAPHSNAP1",
+        "nodes_word": b"GRAPHSNAP1\nNODE 3\n", "nodes_plus": b"GRAPHSNAP1\nNODES +1\n0\t\t\nEDGES 0\n",
+        "nodes_huge": b"GRAPHSNAP1\nNODES 99999999999999999999\n",
+        "nodes_eof": b"GRAPHSNAP1\nNODES 3\n0\t\t\n", "node_fields": b"GRAPHSNAP1\nNODES 1\n0\t\nEDGES 0\n",
+        "node_id_bad": b"GRAPHSNAP1\nNODES 1\nx\t\t\nEDGES 0\n",
+        "node_id_order": b"GRAPHSNAP1\nNODES 2\n0\t\t\n0\t\t\nEDGES 0\n",
+        "label_empty": b"GRAPHSNAP1\nNODES 1\n0\tA,\t\nEDGES 0\n",
+        "label_digit": b"GRAPHSNAP1\nNODES 1\n0\t1A\tq\nEDGES 0\n",
+        "label_bad_props_ok": b"GRAPHSNAP1\nNODES 1\n0\tA-B\tk:i:1\nEDGES 0\n",
+        "no_edges_line": H, "edges_word": H + b"EDGE 1\n", "edges_count": H + b"EDGES x\n",
+        "edges_eof": H + b"EDGES 3\n0\tR\t1\t\n", "edge_fields": H + b"EDGES 1\n0\tR\t1\n",
+        "edge_fields5": H + b"EDGES 1\n0\tR\t1\t\t\n",
+        "edge_src_props": H + b"EDGES 1\nx\tR\t1\tq\n", "edge_src_dst": H + b"EDGES 1\nx\tR\ty\t\n",
+        "edge_range_rel": H + b"EDGES 1\n9\t1R\t1\t\n", "edge_dst_range": H + b"EDGES 1\n0\tR\t3\t\n",
+        "edge_rel_bad": H + b"EDGES 1\n0\tR-S\t1\t\n", "edge_rel_empty": H + b"EDGES 1\n0\t\t1\t\n",
+        "edge_later_line": H + b"EDGES 3\n0\tR\t1\t\n1\tR\t2\t\n2\tR\t0\tk:b:yes\n",
+        "trailing": H + b"EDGES 0\n\nx\n",
+        "item_short": H.replace(b"x:i:5", b"x:i") + b"EDGES 0\n",
+        "item_empty_value": H.replace(b"x:i:5", b"x:i:") + b"EDGES 0\n",
+        "item_empty": H.replace(b"x:i:5", b"x:i:5;") + b"EDGES 0\n",
+        "item_nocolon": H.replace(b"x:i:5", b"abc") + b"EDGES 0\n",
+        "item_double_colon": H.replace(b"x:i:5", b"x::5") + b"EDGES 0\n",
+        "key_bad": H.replace(b"x:i:5", b"1x:i:5") + b"EDGES 0\n",
+        "type_bad": H.replace(b"x:i:5", b"x:z:1") + b"EDGES 0\n",
+        "int_plus": H.replace(b"x:i:5", b"x:i:+5") + b"EDGES 0\n",
+        "int_space": H.replace(b"x:i:5", b"x:i: 5") + b"EDGES 0\n",
+        "int_overflow": H.replace(b"x:i:5", b"x:i:9223372036854775808") + b"EDGES 0\n",
+        "float_plus": H.replace(b"x:i:5", b"x:f:+5") + b"EDGES 0\n",
+        "float_hex": H.replace(b"x:i:5", b"x:f:0x1p3") + b"EDGES 0\n",
+        "float_big": H.replace(b"x:i:5", b"x:f:1e400") + b"EDGES 0\n",
+        "float_tiny": H.replace(b"x:i:5", b"x:f:1e-400") + b"EDGES 0\n",
+        "float_exp": H.replace(b"x:i:5", b"x:f:5e") + b"EDGES 0\n",
+        "bool_case": H.replace(b"x:i:5", b"x:b:True") + b"EDGES 0\n",
+        "pct_trunc": H.replace(b"x:i:5", b"x:s:a%2") + b"EDGES 0\n",
+        "pct_trunc0": H.replace(b"x:i:5", b"x:s:%") + b"EDGES 0\n",
+        "pct_bad": H.replace(b"x:i:5", b"x:s:a%zz") + b"EDGES 0\n",
+        "two_errors_first_wins": H.replace(b"x:i:5", b"x:f:+1") + b"EDGES 1\nx\tR\t1\t\n",
+    }
+    for name, text in bad.items():
+        try:
+            R.snapshot_parse(text)
+            raise SystemExit(f"snapshot case {name} unexpectedly parsed")
+        except oracle.RefError as e:
+            errors.append({"name": name, "text": text.decode(), "error": str(e)})
+    return {"valid": valid, "bench": bench, "errors": errors}
+
+
 def main() -> None:
     R = oracle.Ref()
     for name, fn in (("known_answers", known_answers), ("c1_sweep", c1_sweep),
-                     ("harness_pins", harness_pins), ("walk_pins", walk_pins)):
+                     ("harness_pins", harness_pins), ("walk_pins", walk_pins),
+                     ("snapshot_pins", snapshot_pins)):
         data = fn(R)
         data["_generated_by"] = "tests/golden/make_golden.py from oracle/_ref (reference core)"
         (OUT / f"{name}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")
