@@ -194,7 +194,44 @@ def hop_bytes(st: dict, h: int) -> float:
     return algo_bytes(one)
 
 
-def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True):
+def snapshot_load(rp, ci, torch):
+    """GRAPHSNAP1 text of G2 (byte-identical to the
+    reference writer) loaded into a device graph by the GPU parser, wall clock
+    from host bytes to a ready CSR + CSC; beside it the reference's own
+    snapshot_from_string on the G1 text (a bounded sample, one thread)."""
+    from paper_1905_01294_b200 import DeviceGraph, harness as H
+    t = time.time()
+    text = H.snapshot_text(rp, ci)
+    t_write = time.time() - t
+    times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gs = DeviceGraph.from_snapshot(text)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    drp, dci = gs.csr()
+    ok = bool(np.array_equal(drp, rp) and np.array_equal(dci, ci))
+    del gs
+    sec = {"graph": "G2", "bytes": len(text), "write_s": t_write, "gpu_s": float(np.median(times)),
+           "gpu_GBps": len(text) / float(np.median(times)) / 1e9, "csr_matches": ok}
+    try:
+        import oracle
+        R = oracle.Ref()
+        rp1, ci1 = H.gen_csr(H.G1)
+        t1 = H.snapshot_text(rp1, ci1)
+        t0 = time.perf_counter()
+        R.snapshot_parse(t1)
+        el = time.perf_counter() - t0
+        sec["reference"] = {"bytes": len(t1), "s": el, "GBps": len(t1) / el / 1e9,
+                            "sample": "G1 snapshot text, reference snapshot_from_string (1 thread, full store)"}
+    except Exception as e:  # reference library not built
+        sec["reference"] = {"unavailable": str(e)[:120]}
+    del text
+    return sec
+
+
+def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True, ci=None):
     """BASELINE.json configs[2] (cfg3: 10 seeds, k=3,6) and configs[4] (cfg5:
     65,536 seeds in 64-lane words, k=1,2,3,6; seed batches split across
     ranks), on the already-resident G2. Device-resident, CUDA-event timed, L2
@@ -263,6 +300,8 @@ def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True):
                                 "lanes_per_batch": st["lanes"], "hops": hops,
                                 "count_sum": int(d_counts.sum().item())}
         out[name] = sec
+    if rank == 0 and ci is not None:
+        out["snapshot_load"] = snapshot_load(rp, ci, torch)
     return out
 
 
@@ -359,7 +398,7 @@ def run_ours(args):
 
     # BASELINE configs[2] / [4] on the same resident graph (every rank takes part)
     extras = None if args.no_extras else run_extras(g, rp, world, rank, dist, stream, flush, torch,
-                                                    with_cfg4=not args.no_cfg4)
+                                                    with_cfg4=not args.no_cfg4, ci=ci)
 
     if rank != 0:
         if world > 1:
