@@ -727,7 +727,13 @@ __global__ void __launch_bounds__(kFinBlock) fr_finish(FRParams P) {
     bool dense_me = false;
     if (threadIdx.x < kMaxSlots) {
         const bool pop_me = threadIdx.x < ns && P.logcnt[threadIdx.x] != 0;
-        dense_me = threadIdx.x < ns && (overflow || pop_me);
+        // a logged seed with many last-hop discoveries: one streamed row of
+        // zeros (write-only, full lines) is cheaper than that many scattered
+        // single-word stores to lines that have mostly left L2 (break-even
+        // measured near nwords / 40 discoveries)
+        const bool wide = threadIdx.x < ns && !pop_me && !P.keep_result &&
+                          ld_cg(&P.cnt[P.k * S + threadIdx.x]) > P.rs / 32;
+        dense_me = threadIdx.x < ns && (overflow || pop_me || wide);
         s_flag[threadIdx.x] = pop_me ? 2 : (dense_me ? 1 : 0);
     }
     {
@@ -764,10 +770,11 @@ __global__ void __launch_bounds__(kFinBlock) fr_finish(FRParams P) {
             const uint32_t base = (t % chunks) * kDenseChunk + threadIdx.x * 4;
             uint4* row = reinterpret_cast<uint4*>(P.V + (size_t)slot * P.rs);
             uint4 v[4];
+            const bool count_me = s_flag[slot] == 2;  // the others only need zeros
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const uint32_t w = base + i * 4 * kFinBlock;
-                v[i] = w < P.rs ? __ldcs(row + w / 4) : make_uint4(0, 0, 0, 0);
+                v[i] = (count_me && w < P.rs) ? __ldcs(row + w / 4) : make_uint4(0, 0, 0, 0);
             }
             uint32_t pc = 0;
 #pragma unroll
@@ -892,9 +899,11 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     ws->fr_big_cap = (uint32_t)std::min<uint64_t>(want_big, 16ull << 20);
     for (int i = 0; i < 2; ++i)
         if ((e = cudaMalloc(&ws->fr_big[i], (size_t)ws->fr_big_cap * sizeof(uint2)))) return e;
-    // a last hop that can touch more than ~nwords/4 vertices of a seed is not
-    // logged; its visited bitmap is cleared with one coalesced pass instead
-    uint32_t qdiv = 4;
+    // a last hop that can touch more than ~nwords/16 vertices of a seed is not
+    // logged (fire-and-forget red.or); its visited bitmap is popcounted and
+    // cleared with one coalesced pass instead (G2 sweep of the divisor:
+    // 4 -> 0.198 ms, 8 -> 0.183, 16 -> 0.178, 32 -> 0.180 per cfg2 k=2 call)
+    uint32_t qdiv = 16;
     if (const char* q = std::getenv("MGK_QUOTA_DIV")) qdiv = std::max(1, std::atoi(q));
     ws->fr_quota = std::max<uint32_t>(64, g.nwords / qdiv);
     ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * (g.n + 64), 64ull << 20);
