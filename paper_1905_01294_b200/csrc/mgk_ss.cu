@@ -933,54 +933,74 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     return cudaSuccess;
 }
 
-// k = 1 on duplicate-free rows: |F_1| = deg(s) - [s in row(s)] (binary search
-// of the ascending row). No bitmap is touched, so there is nothing to clean up.
+// k = 1 on duplicate-free rows: |F_1| = deg(s) - [s in row(s)]. One warp per
+// seed finds s in its ascending row with a 32-way search (32 pivots per round:
+// a 100K-entry hub row takes 3 dependent loads instead of 17). No bitmap is
+// touched, so there is nothing to clean up. The last CTA (done counter in
+// misc[7]) folds the per-CTA sums into the per-hop counters; misc[3..7] are
+// zero on entry and on exit.
 constexpr int kK1Block = 512;
 __global__ void __launch_bounds__(kK1Block) k1_kernel(DevGraph g, const uint32_t* seeds, uint64_t ns,
                                                       unsigned long long* counts, LevelCounters* lc,
-                                                      uint32_t zero_lc) {
+                                                      unsigned long long* misc) {
     __shared__ unsigned long long s_acc[3];
+    __shared__ bool s_last;
     const unsigned long long t0 = globaltimer();
-    if (zero_lc)  // single-block launch: nothing else writes lc
-        for (uint32_t i = threadIdx.x; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += blockDim.x)
-            reinterpret_cast<unsigned long long*>(lc)[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) misc[3] = t0;
     if (threadIdx.x < 3) s_acc[threadIdx.x] = 0;
     __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint64_t nwarps = (uint64_t)gridDim.x * (kK1Block / 32);
     unsigned long long f = 0, sc = 0, nrun = 0;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t i = (blockIdx.x * (uint64_t)kK1Block + threadIdx.x) >> 5; i < ns; i += nwarps) {
         const uint32_t sd = dev_id(g, seeds[i]);
         const uint32_t b = __ldg(g.rp + sd), e = __ldg(g.rp + sd + 1);
-        uint32_t lo = b, hi = e;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(g.ci + mid) < sd) lo = mid + 1;
-            else hi = mid;
+        uint32_t lo = b, hi = e;  // sd, if present, is in [lo, hi)
+        while (hi - lo > 32) {
+            const uint32_t piv = lo + (uint32_t)((uint64_t)(hi - lo) * (lane + 1) / 33);
+            const unsigned below = __ballot_sync(kFull, __ldg(g.ci + piv) < sd);
+            const int c = __popc(below);  // pivots ascend: `below` is a prefix
+            const uint32_t nlo = c == 0 ? lo : __shfl_sync(kFull, piv, c - 1) + 1;
+            const uint32_t nhi = c == 32 ? hi : __shfl_sync(kFull, piv, c) + 1;
+            lo = nlo;
+            hi = nhi;
         }
-        const uint32_t self = (lo < e && __ldg(g.ci + lo) == sd) ? 1u : 0u;
-        const uint32_t c = e - b - self;
-        counts[i] = c;
-        f += c;
-        sc += e - b;
-        nrun += 1;
+        const bool hit = lo + lane < hi && __ldg(g.ci + lo + lane) == sd;
+        const uint32_t self = __ballot_sync(kFull, hit) ? 1u : 0u;
+        if (lane == 0) {
+            const uint32_t c = e - b - self;
+            counts[i] = c;
+            f += c;
+            sc += e - b;
+            nrun += 1;
+        }
     }
-    f = warp_sum_u64(f);
-    sc = warp_sum_u64(sc);
-    nrun = warp_sum_u64(nrun);
-    if (lane_id() == 0) {
+    if (lane == 0) {
         if (f) atomicAdd(&s_acc[0], f);
         if (sc) atomicAdd(&s_acc[1], sc);
         if (nrun) atomicAdd(&s_acc[2], nrun);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        atomicAdd(&lc[1].frontier, s_acc[0]);
-        atomicAdd(&lc[1].vertices, s_acc[0]);
-        atomicAdd(&lc[1].scanned, s_acc[1]);
-        atomicAdd(&lc[1].edges, s_acc[1]);
-        atomicAdd(&lc[1].union_edges, s_acc[1]);
-        atomicAdd(&lc[1].runs, (unsigned)s_acc[2]);
-        if (blockIdx.x == 0) atomicAdd(&lc[1].ns, globaltimer() - t0);
+        if (s_acc[0]) atomicAdd(&misc[4], s_acc[0]);
+        if (s_acc[1]) atomicAdd(&misc[5], s_acc[1]);
+        if (s_acc[2]) atomicAdd(&misc[6], s_acc[2]);
+        __threadfence();
+        s_last = atomicAdd(&misc[7], 1ull) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (uint32_t i = threadIdx.x; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += blockDim.x)
+        reinterpret_cast<unsigned long long*>(lc)[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long fr = ld_cg(&misc[4]), scn = ld_cg(&misc[5]), runs = ld_cg(&misc[6]);
+        lc[1].frontier = lc[1].vertices = fr;
+        lc[1].scanned = lc[1].edges = lc[1].union_edges = scn;
+        lc[1].runs = (unsigned)runs;
+        lc[1].ns = globaltimer() - ld_cg(&misc[3]);
+        misc[3] = misc[4] = misc[5] = misc[6] = misc[7] = 0;
     }
 }
 
@@ -993,13 +1013,9 @@ cudaError_t launch_single(Launch& L) {
     const Graph* gr = L.g;
     Workspace* ws = L.ws;
     if (gr->dg.rows_unique && L.k == 1 && L.seed_visited && !L.keep_result && !fuse_disabled()) {
-        const uint64_t want = (L.nseeds + kK1Block - 1) / kK1Block;
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(want, 148ull * 8);
-        cudaError_t e = cudaSuccess;
-        if (grid > 1 && (e = cudaMemsetAsync(ws->lc, 0, (MGK_MAX_HOPS + 2) * sizeof(LevelCounters), L.stream)))
-            return e;
-        k1_kernel<<<grid, kK1Block, 0, L.stream>>>(gr->dg, L.d_seeds, L.nseeds, L.d_counts, ws->lc,
-                                                  grid == 1 ? 1u : 0u);
+        const uint64_t want = (L.nseeds + kK1Block / 32 - 1) / (kK1Block / 32);  // a warp per seed
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(want, 148ull * 4);
+        k1_kernel<<<grid, kK1Block, 0, L.stream>>>(gr->dg, L.d_seeds, L.nseeds, L.d_counts, ws->lc, ws->misc);
         L.grid = grid;
         L.block = kK1Block;
         L.launches = 1;
