@@ -179,10 +179,18 @@ struct Span {
 };
 Span span_of(uint32_t k, int mode) { return Span{mode == MGK_EXACT ? k : 1u, k, true}; }
 
+// AUTO: shallow hops touch little of the graph per seed, so independent
+// per-seed bitmaps win; from 3 hops on, frontiers of different seeds
+// overlap heavily and the 64-lane words share every adjacency pass.
+int resolve_engine(int engine, uint64_t nseeds, uint32_t k) {
+    if (engine != MGK_ENGINE_AUTO) return engine;
+    return (nseeds > 1 && k >= 3) ? MGK_ENGINE_LANES : MGK_ENGINE_SINGLE;
+}
+
 cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_t nseeds,
                        Span span, int engine, unsigned long long* d_counts,
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
-                       int* W_out, bool keep_result = false) {
+                       int* W_out, bool keep_result = false, const uint32_t* h_seeds = nullptr) {
     const uint32_t k = span.hi;
     // the engines zero the per-hop counters themselves (first launch of a call)
     cudaError_t e = cudaSuccess;
@@ -202,11 +210,9 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.stream = stream;
     L.tuning = g->tuning;
     L.keep_result = keep_result;
-    // AUTO: shallow hops touch little of the graph per seed, so independent
-    // per-seed bitmaps win; from 3 hops on, frontiers of different seeds
-    // overlap heavily and the 64-lane words share every adjacency pass.
-    if (engine == MGK_ENGINE_AUTO)
-        engine = (nseeds > 1 && k >= 3) ? MGK_ENGINE_LANES : MGK_ENGINE_SINGLE;
+    L.host_io = h_seeds != nullptr;
+    L.h_seeds = h_seeds;
+    engine = resolve_engine(engine, nseeds, k);
     *used_engine = engine;
     if (engine == MGK_ENGINE_SINGLE) {
         e = launch_single(L);
@@ -235,7 +241,12 @@ cudaError_t ensure_staging(Workspace* ws, uint64_t nseeds) {
     cudaError_t e;
     if ((e = cudaMalloc(&ws->d_seeds, cap * 4))) return e;
     if ((e = cudaMalloc(&ws->d_counts, cap * 8))) return e;
-    if ((e = cudaMallocHost(&ws->h_pinned, cap * 8))) return e;
+    // mapped: the SINGLE engine reads the seeds and writes the counts in place
+    if ((e = cudaHostAlloc(&ws->h_pinned, cap * 12, cudaHostAllocMapped | cudaHostAllocPortable))) return e;
+    ws->h_seeds = reinterpret_cast<uint32_t*>(ws->h_pinned);
+    ws->h_counts = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws->h_pinned) + cap * 4);
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->h_seeds_dev), ws->h_seeds, 0))) return e;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&ws->h_counts_dev), ws->h_counts, 0))) return e;
     ws->seeds_cap = cap;
     return cudaSuccess;
 }
@@ -578,23 +589,32 @@ int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, 
         release_ws(g, ws);
         return fail_cuda(e, "staging");
     }
-    // seeds: host uint64 -> pinned uint32 -> device (inside the caller's timing)
-    uint32_t* hs = reinterpret_cast<uint32_t*>(ws->h_pinned);
+    // seeds: host uint64 -> pinned, device-mapped uint32 (inside the caller's timing)
+    uint32_t* hs = ws->h_seeds;
     for (uint64_t i = 0; i < nseeds; ++i) hs[i] = (uint32_t)seeds[i];
+    // SINGLE reads the seeds over the bus (k = 1) or carries each group's
+    // seeds in its launch, and writes the counts straight into the mapped
+    // buffer: no copy operations on the stream. LANES stages through HBM.
+    const int eng = resolve_engine(engine, nseeds, span.hi);
+    const bool host_io = eng == MGK_ENGINE_SINGLE;
     uint32_t grid = 0, block = 0;
     int used = 0, W = 0;
     float ms = 0.f;
     do {
-        if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
+        if (!host_io &&
+            (e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream)))
+            break;
         if (stats && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
-        if ((e = run_engine(g, ws, ws->d_seeds, nseeds, span, engine, ws->d_counts, ws->stream,
-                            &grid, &block, &used, &W)))
+        if ((e = run_engine(g, ws, host_io ? ws->h_seeds_dev : ws->d_seeds, nseeds, span, eng,
+                            host_io ? ws->h_counts_dev : ws->d_counts, ws->stream, &grid, &block, &used, &W,
+                            false, host_io ? hs : nullptr)))
             break;
         if (stats && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
-        if ((e = cudaMemcpyAsync(ws->h_pinned, ws->d_counts, nseeds * 8, cudaMemcpyDeviceToHost, ws->stream)))
+        if (!host_io && (e = cudaMemcpyAsync(ws->h_counts, ws->d_counts, nseeds * 8, cudaMemcpyDeviceToHost,
+                                             ws->stream)))
             break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;
-        std::memcpy(counts, ws->h_pinned, nseeds * 8);
+        std::memcpy(counts, ws->h_counts, nseeds * 8);
         if (stats) {
             cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
             LevelCounters lc[MGK_MAX_HOPS + 2];

@@ -120,7 +120,11 @@ struct Workspace {
     uint32_t* d_seeds = nullptr;             // staging for host calls
     unsigned long long* d_counts = nullptr;
     uint64_t seeds_cap = 0;
-    uint64_t* h_pinned = nullptr;            // pinned host staging (seeds/counts)
+    uint64_t* h_pinned = nullptr;            // pinned, device-mapped host staging:
+    uint32_t* h_seeds = nullptr;             //   [seeds_cap] uint32 seeds (device-readable)
+    unsigned long long* h_counts = nullptr;  //   [seeds_cap] uint64 counts (device-writable)
+    uint32_t* h_seeds_dev = nullptr;         // device addresses of the two regions
+    unsigned long long* h_counts_dev = nullptr;
     uint64_t h_pinned_cap = 0;
     uint64_t bytes = 0;
     // last device-path launch (mgk_khop_device_stats)
@@ -164,6 +168,11 @@ struct Launch {
     Tuning tuning;
     int lanes_words;  // LANES engine only
     bool keep_result = false;  // SINGLE: leave slot 0's bitmaps for k_hop_frontier
+    // d_seeds / d_counts are mapped pinned HOST memory (host calls, SINGLE):
+    // each group's seeds then travel inside its launch and the answers are
+    // written straight to the host buffer (no copy operations)
+    bool host_io = false;
+    const uint32_t* h_seeds = nullptr;  // host view of d_seeds when host_io
     uint32_t grid = 0, block = 0;  // out
     uint32_t launches = 0;         // out: engine kernels launched
 };

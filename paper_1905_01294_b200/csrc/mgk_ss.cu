@@ -22,6 +22,7 @@
 // each warp takes 1..32 items per step (fewer when the list is short, so a
 // small hop still occupies every warp of the grid). The last hop only counts.
 #include <cstdlib>
+#include <cstring>
 
 #include "mgk_device.cuh"
 
@@ -89,7 +90,13 @@ struct FRParams {
     uint32_t keep_result;  // one seed, bitmaps kept for k_hop_frontier
     uint32_t zero_lc;      // first group of a call: clear the per-hop counters
     uint32_t fuse1;        // rows unique, seed pre-visited, k >= 2: hop 1 = the seed rows
+    // host calls: this group's seeds travel inside the launch (seeds == nullptr)
+    uint32_t inline_seeds[kMaxSlots];
 };
+
+__device__ __forceinline__ uint32_t seed_at(const FRParams& P, uint32_t i) {
+    return P.seeds ? P.seeds[i] : P.inline_seeds[i];
+}
 
 struct Acc {
     unsigned long long found, scanned, candidates;
@@ -512,7 +519,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
         }
         uint32_t c = 0;
         if (threadIdx.x < ns) {
-            const uint32_t sd = dev_id(g, P.seeds[threadIdx.x]);
+            const uint32_t sd = dev_id(g, seed_at(P, threadIdx.x));
             const uint32_t b = __ldg(g.rp + sd), deg = __ldg(g.rp + sd + 1) - b;
             c = (deg + kSeedChunk - 1) / kSeedChunk;
             if (blockIdx.x == 0) {  // hop 0: the seed itself
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
                 else hi = mid;
             }
             const uint32_t slot = lo;
-            const uint32_t sd = dev_id(g, P.seeds[slot]);
+            const uint32_t sd = dev_id(g, seed_at(P, slot));
             const uint32_t b = __ldg(g.rp + sd), deg = __ldg(g.rp + sd + 1) - b;
             const uint32_t beg = (t - s_pref[slot]) * kSeedChunk;
             const uint32_t len = min(kSeedChunk, deg - beg);
@@ -575,7 +582,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     }
     // ---- seeds (hop 0): one warp per seed; counters are zero on entry --------------
     for (uint32_t slot = warp_gid; slot < (P.fuse1 ? 0u : ns); slot += nwarps) {
-        const uint32_t s = dev_id(g, P.seeds[slot]);
+        const uint32_t s = dev_id(g, seed_at(P, slot));
         const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
         if (lane == 0) {
             const uint32_t bit = 1u << (s & 31);
@@ -600,7 +607,7 @@ __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
     if (P.fuse1) {  // hop 1's counters, now that lc is zeroed
         block_flush(acc, &P.ctl->found[1], &P.lc[1]);
         if (blockIdx.x == 0 && threadIdx.x < ns) {
-            const uint32_t sd = dev_id(g, P.seeds[threadIdx.x]);
+            const uint32_t sd = dev_id(g, seed_at(P, threadIdx.x));
             const uint32_t deg = __ldg(g.rp + sd + 1) - __ldg(g.rp + sd);
             atomicAdd(&P.lc[1].runs, 1u);
             atomicAdd(&P.lc[1].edges, (unsigned long long)deg);
@@ -1081,7 +1088,12 @@ cudaError_t launch_single(Launch& L) {
     for (uint64_t g0 = 0; g0 < L.nseeds; g0 += P.S) {
         P.ns = (uint32_t)std::min<uint64_t>(P.S, L.nseeds - g0);
         P.zero_lc = g0 == 0;
-        P.seeds = L.d_seeds + g0;
+        if (L.host_io) {  // this group's seeds ride in the launch parameters
+            P.seeds = nullptr;
+            std::memcpy(P.inline_seeds, L.h_seeds + g0, (size_t)P.ns * 4);
+        } else {
+            P.seeds = L.d_seeds + g0;
+        }
         P.counts = L.d_counts + g0;
         void* args[] = {&P};
         if ((e = launch_persistent((const void*)fr_kernel, L.grid, kBlock, args, L.stream))) return e;
