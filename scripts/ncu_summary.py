@@ -105,6 +105,16 @@ def launches(csv_path, out_md):
              "", "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{n}` | {c} | {t:.1f} | {100 * t / total:.1f}% |")
+    # the timed step only: engine kernels (graph build and setup launches run
+    # before the timed region)
+    eng = OrderedDict((n, v) for n, v in agg.items()
+                      if any(t in n for t in ("fr_kernel", "fr_finish", "k1_kernel", "ms_kernel")))
+    et = sum(v[1] for v in eng.values())
+    if et:
+        lines += ["", "timed-step engine kernels only (share of their sum):", "",
+                  "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+        for n, (c, t) in sorted(eng.items(), key=lambda x: -x[1][1]):
+            lines.append(f"| `{n}` | {c} | {t:.1f} | {t / c:.1f} | {100 * t / et:.1f}% |")
     lines += ["", "| # | kernel | grid | block | us |", "|---|---|---|---|---|"]
     for r in rows:
         n = r["Kernel Name"].split("(")[0][-50:]
