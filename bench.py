@@ -231,6 +231,40 @@ def snapshot_load(rp, ci, torch):
     return sec
 
 
+def mxm_section(torch):
+    """A x A of a scale-14 R-MAT graph (bool_or_and and plus_times) through the
+    GPU mxm (host CSR in, host CSR out, wall clock) beside the reference's own
+    mxm (one thread) on the same operands."""
+    from paper_1905_01294_b200 import harness as H, mxm
+    spec = H.GraphSpec("M14", scale=14, edge_factor=16, relabel=1)
+    rp, ci = H.gen_csr(spec)
+    n = len(rp) - 1
+    A = (n, n, rp.astype(np.uint64), ci.astype(np.uint64), None)
+    sec = {"graph": "scale-14 R-MAT (G1 recipe)", "nnz_a": int(len(ci))}
+    try:
+        import oracle
+        R = oracle.Ref()
+    except Exception as e:
+        R = None
+        sec["reference"] = {"unavailable": str(e)[:120]}
+    for name, sr in (("bool_or_and", 0), ("plus_times", 1)):
+        mxm(A, A, sr)  # warm
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            c = mxm(A, A, sr)
+            ts.append(time.perf_counter() - t0)
+        ent = {"nnz_c": int(len(c[3])), "gpu_s": float(np.median(ts))}
+        if R is not None:
+            t0 = time.perf_counter()
+            r = R.mxm(A, A, sr)
+            ent["reference_s"] = time.perf_counter() - t0
+            ent["matches_reference"] = bool(np.array_equal(r[2], c[2]) and np.array_equal(r[3], c[3]) and
+                                            (r[4] is None or np.array_equal(r[4], c[4])))
+        sec[name] = ent
+    return sec
+
+
 def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True, ci=None):
     """BASELINE.json configs[2] (cfg3: 10 seeds, k=3,6) and configs[4] (cfg5:
     65,536 seeds in 64-lane words, k=1,2,3,6; seed batches split across
@@ -302,6 +336,7 @@ def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True, c
         out[name] = sec
     if rank == 0 and ci is not None:
         out["snapshot_load"] = snapshot_load(rp, ci, torch)
+        out["mxm"] = mxm_section(torch)
     return out
 
 

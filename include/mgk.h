@@ -55,6 +55,7 @@ extern "C" {
 #define MGK_MAX_HOPS 32 /* kMaxHops, proj/core/include/matgraph/ast.hpp:15 */
 
 typedef struct mgk_graph mgk_graph;
+typedef struct mgk_matrix mgk_matrix; /* a host CSR result (mgk_mxm) */
 
 /* Per-level work counters of one call (summed over seeds / batches). */
 typedef struct mgk_level {
@@ -159,6 +160,29 @@ int mgk_khop_count_ex(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint
 int mgk_graph_replicate(const mgk_graph* src, int device, mgk_graph** out);
 int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64_t* seeds, uint64_t nseeds,
                          uint32_t k, int mode, uint64_t* counts);
+
+/* ---- semiring matrix product ----------------------------
+ * mxm (sparse.cpp:292-363): C = A (+.*) B over bool_or_and (structural
+ * result), plus_times or min_plus (int64 values; a NULL value array is a
+ * structural operand multiplying as all-ones), optionally restricted to the
+ * pattern of a structural mask (m_row_ptr NULL = no mask). Computed on the GPU
+ * (expand / radix sort / reduce in row chunks); columns come out ascending per
+ * row and values are bit-identical to the reference (wrapping int64).
+ * Errors (MGK_ECONTRACT, the reference's text):
+ *   "mxm: inner dimensions disagree ({}x{} times {}x{})"
+ *   "mxm: mask shape {}x{} != result shape {}x{}"
+ * The result is a handle: query sizes, download, free. Like from_parts, a
+ * valued product with no entries reports valued = 0. */
+#define MGK_SEMIRING_BOOL_OR_AND 0
+#define MGK_SEMIRING_PLUS_TIMES 1
+#define MGK_SEMIRING_MIN_PLUS 2
+int mgk_mxm(int device, uint64_t a_nrows, uint64_t a_ncols, const uint64_t* a_row_ptr, const uint64_t* a_col_idx,
+            const int64_t* a_vals, uint64_t b_nrows, uint64_t b_ncols, const uint64_t* b_row_ptr,
+            const uint64_t* b_col_idx, const int64_t* b_vals, int semiring, uint64_t m_nrows, uint64_t m_ncols,
+            const uint64_t* m_row_ptr, const uint64_t* m_col_idx, mgk_matrix** out);
+int mgk_matrix_info(const mgk_matrix* m, uint64_t* nrows, uint64_t* ncols, uint64_t* nnz, int* valued);
+int mgk_matrix_download(const mgk_matrix* m, uint64_t* row_ptr, uint64_t* col_idx, int64_t* vals);
+int mgk_matrix_free(mgk_matrix* m);
 
 /* Device-resident variant: d_seeds (uint32) and d_counts (uint64) are DEVICE
  * pointers on the graph's device; work is enqueued on `stream`

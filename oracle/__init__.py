@@ -67,6 +67,9 @@ class Port:
         L.orc_walk_targets.restype = C.c_uint64
         L.orc_walk_targets.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_uint32,
                                        C.c_void_p]
+        vp = C.c_void_p
+        L.orc_mxm.restype = C.c_uint64
+        L.orc_mxm.argtypes = [C.c_uint64, vp, vp, vp, C.c_uint64, vp, vp, vp, C.c_int, vp, vp, vp, vp, vp]
         L.orc_khop_work.restype = C.c_uint64
         L.orc_khop_work.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_void_p,
                                     C.POINTER(C.c_uint32)]
@@ -126,6 +129,39 @@ class Port:
         L = C.c_uint32(0)
         e = self.lib.orc_khop_work(n, row_ptr, _c64(col_idx), seed, k, sizes.ctypes.data, C.byref(L))
         return int(e), sizes[: L.value + 1].copy()
+
+
+def _csr_args(m):
+    """(nrows, ncols, row_ptr, col_idx, vals|None) -> contiguous arrays kept alive by the caller."""
+    nr, nc, rp, ci, v = m
+    rp = np.ascontiguousarray(rp, np.uint64)
+    ci = _c64(ci)
+    v = None if v is None else (np.ascontiguousarray(v, np.int64) if len(v) else np.zeros(1, np.int64))
+    return int(nr), int(nc), rp, ci, v
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _port_mxm(self, a, b, semiring=0, mask=None):
+    """sparse.cpp:292-363 restated (oracle/khop_oracle.c orc_mxm). Matrices are
+    (nrows, ncols, row_ptr, col_idx, vals|None); returns the same tuple."""
+    an, ac, arp, aci, av = _csr_args(a)
+    bn, bc, brp, bci, bv = _csr_args(b)
+    mrp = mci = None
+    if mask is not None:
+        _, _, mrp, mci, _ = _csr_args(mask)
+    args = (an, _ptr(arp), _ptr(aci), _ptr(av), bc, _ptr(brp), _ptr(bci), _ptr(bv), semiring, _ptr(mrp), _ptr(mci))
+    nnz = self.lib.orc_mxm(*args, None, None, None)
+    rp = np.zeros(an + 1, np.uint64)
+    ci = np.zeros(max(nnz, 1), np.uint64)
+    vals = np.zeros(max(nnz, 1), np.int64)
+    self.lib.orc_mxm(*args, rp.ctypes.data, ci.ctypes.data, vals.ctypes.data)
+    return an, bc, rp, ci[:nnz].copy(), (vals[:nnz].copy() if semiring != 0 and nnz else None)
+
+
+Port.mxm = _port_mxm
 
 
 def _c64(a):
@@ -191,6 +227,8 @@ class Ref:
         L.ref_graph_create_edge_props.argtypes = [vp, u64, C.c_char_p, u64, C.c_char_p]
         L.ref_snapshot_parse.argtypes = [C.c_char_p, u64, C.POINTER(vp)]
         L.ref_snapshot_to_string.argtypes = [vp, C.c_char_p, u64, C.POINTER(u64)]
+        L.ref_mxm.argtypes = [u64, u64, vp, vp, vp, u64, u64, vp, vp, vp, C.c_int, u64, u64, vp, vp,
+                              C.POINTER(u64), C.POINTER(C.c_int), vp, vp, vp]
         L.ref_bfs_oracle_new.restype = vp
         L.ref_bfs_oracle_new.argtypes = [vp, vp, u64, u64]
         L.ref_bfs_oracle_count.argtypes = [vp, u64, u32, C.c_int, C.POINTER(u64)]
@@ -211,6 +249,26 @@ class Ref:
         self._check(self.lib.ref_build_bench_graph(src.ctypes.data, dst.ctypes.data, len(src),
                                                    node_count, C.byref(h)))
         return RefGraph(self, h.value)
+
+    def mxm(self, a, b, semiring=0, mask=None):
+        """The reference's mxm over from_parts operands; returns
+        (nrows, ncols, row_ptr, col_idx, vals|None)."""
+        an, ac, arp, aci, av = _csr_args(a)
+        bn, bc, brp, bci, bv = _csr_args(b)
+        mn = mc = 0
+        mrp = mci = None
+        if mask is not None:
+            mn, mc, mrp, mci, _ = _csr_args(mask)
+        nnz, valued = C.c_uint64(), C.c_int()
+        args = (an, ac, _ptr(arp), _ptr(aci), _ptr(av), bn, bc, _ptr(brp), _ptr(bci), _ptr(bv), semiring,
+                mn, mc, _ptr(mrp), _ptr(mci), C.byref(nnz), C.byref(valued))
+        self._check(self.lib.ref_mxm(*args, None, None, None))
+        rp = np.zeros(an + 1, np.uint64)
+        ci = np.zeros(max(nnz.value, 1), np.uint64)
+        vals = np.zeros(max(nnz.value, 1), np.int64)
+        self._check(self.lib.ref_mxm(*args, rp.ctypes.data, ci.ctypes.data, vals.ctypes.data))
+        n = nnz.value
+        return an, bc, rp, ci[:n].copy(), (vals[:n].copy() if valued.value else None)
 
     def snapshot_parse(self, text: bytes):
         """snapshot_from_string (snapshot.cpp:162-231); raises RefError with its message."""

@@ -11,6 +11,7 @@
 //   rmat_generate          proj/core/src/bench.cpp:107-137
 //   BfsOracle::count       proj/core/src/bench.cpp:233-259
 //   snapshot_from_string / snapshot_to_string   proj/core/src/snapshot.cpp:127-231
+//   mxm                    proj/core/src/sparse.cpp:292-363
 // Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
 // --impl reference) may load this library.
 #include <atomic>
@@ -29,6 +30,7 @@
 #include "matgraph/execute.hpp"
 #include "matgraph/graph.hpp"
 #include "matgraph/snapshot.hpp"
+#include "matgraph/sparse.hpp"
 
 using matgraph_ref::PropertyGraph;
 
@@ -133,6 +135,39 @@ int ref_snapshot_to_string(void* g, char* out, uint64_t cap, uint64_t* n) {
         const std::string s = matgraph_ref::snapshot_to_string(*static_cast<PropertyGraph*>(g));
         *n = s.size();
         if (out && cap >= s.size()) std::memcpy(out, s.data(), s.size());
+        return 0;
+    } catch (const std::exception& e) { return fail(e); }
+}
+
+// mxm over from_parts operands (vals NULL = structural). Two calls: out
+// arrays NULL -> *nnz and *valued; then the CSR (+ values when valued).
+int ref_mxm(uint64_t a_nrows, uint64_t a_ncols, const uint64_t* a_rp, const uint64_t* a_ci, const int64_t* a_vals,
+            uint64_t b_nrows, uint64_t b_ncols, const uint64_t* b_rp, const uint64_t* b_ci, const int64_t* b_vals,
+            int semiring, uint64_t m_nrows, uint64_t m_ncols, const uint64_t* m_rp, const uint64_t* m_ci,
+            uint64_t* nnz, int* valued, uint64_t* out_rp, uint64_t* out_ci, int64_t* out_vals) {
+    try {
+        using matgraph_ref::SparseMatrix;
+        auto make = [](uint64_t nr, uint64_t nc, const uint64_t* rp, const uint64_t* ci, const int64_t* v) {
+            std::vector<uint64_t> r(rp, rp + nr + 1), c(ci, ci + rp[nr]);
+            std::vector<int64_t> vv;
+            if (v) vv.assign(v, v + rp[nr]);
+            return SparseMatrix::from_parts(nr, nc, std::move(r), std::move(c), std::move(vv));
+        };
+        const SparseMatrix a = make(a_nrows, a_ncols, a_rp, a_ci, a_vals);
+        const SparseMatrix b = make(b_nrows, b_ncols, b_rp, b_ci, b_vals);
+        const matgraph_ref::Semiring& sr = semiring == 0 ? matgraph_ref::Semiring::bool_or_and()
+                                         : semiring == 1 ? matgraph_ref::Semiring::plus_times()
+                                                         : matgraph_ref::Semiring::min_plus();
+        SparseMatrix mask;
+        if (m_rp) mask = make(m_nrows, m_ncols, m_rp, m_ci, nullptr);
+        const SparseMatrix c = matgraph_ref::mxm(a, b, sr, m_rp ? &mask : nullptr);
+        *nnz = c.nvals();
+        *valued = c.valued() ? 1 : 0;
+        if (out_rp) std::memcpy(out_rp, c.row_ptr().data(), (c.nrows() + 1) * 8);
+        if (out_ci && c.nvals()) std::memcpy(out_ci, c.col_idx().data(), c.nvals() * 8);
+        if (out_vals && c.valued() && c.nvals())
+            for (uint64_t r = 0, p = 0; r < c.nrows(); ++r)
+                for (int64_t v : c.row_values(r)) out_vals[p++] = v;
         return 0;
     } catch (const std::exception& e) { return fail(e); }
 }

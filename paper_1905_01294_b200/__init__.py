@@ -6,7 +6,7 @@ interface (proj/core/include/matgraph/execute.hpp, bench.hpp). See DESIGN.md.
 """
 from .khop import (  # noqa: F401
     ENGINE_AUTO, ENGINE_LANES, ENGINE_SINGLE, K_MAX_HOPS, ContractError, DeviceError, DeviceGraph, SnapshotError,
-    snapshot_check,
+    snapshot_check, mxm, SEMIRING_BOOL_OR_AND, SEMIRING_PLUS_TIMES, SEMIRING_MIN_PLUS,
     Error, HarnessError, KHopQuery, TraverseMode, Tuning, device_count, device_stats, k_hop_count,
     k_hop_count_batch, k_hop_count_device, k_hop_count_multi, k_hop_frontier, walk_count_batch, walk_targets)
 

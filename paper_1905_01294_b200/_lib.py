@@ -62,6 +62,11 @@ SIGNATURES = [
     ("mgk_graph_load_snapshot_file", _int, [_int, C.c_char_p, C.c_char_p, C.POINTER(_vp), _u64p]),
     ("mgk_snapshot_check", _int, [C.c_char_p, _u64, _u64p, _u64p]),
     ("mgk_graph_free", _int, [_vp]),
+    ("mgk_mxm", _int, [_int, _u64, _u64, _vp, _vp, _vp, _u64, _u64, _vp, _vp, _vp, _int, _u64, _u64, _vp, _vp,
+                       C.POINTER(_vp)]),
+    ("mgk_matrix_info", _int, [_vp, _u64p, _u64p, _u64p, C.POINTER(_int)]),
+    ("mgk_matrix_download", _int, [_vp, _vp, _vp, _vp]),
+    ("mgk_matrix_free", _int, [_vp]),
     ("mgk_graph_info", _int, [_vp, _u64p, _u64p, C.POINTER(_int)]),
     ("mgk_graph_download_csr", _int, [_vp, _vp, _vp]),
     ("mgk_graph_download_csc", _int, [_vp, _vp, _vp]),

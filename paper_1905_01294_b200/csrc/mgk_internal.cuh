@@ -222,6 +222,18 @@ std::optional<std::string> check_all(std::string_view text, uint64_t* n_out, uin
 cudaError_t load_to_graph(Graph* g, const char* text, uint64_t len, const char* relation, uint64_t* node_count,
                           std::string* err);
 }  // namespace snap
+
+// semiring mxm (mgk_mxm.cu): host CSR operands (validated by the caller)
+namespace mx {
+struct DevIn {
+    uint64_t nrows = 0, ncols = 0;
+    const uint64_t* rp = nullptr;
+    const uint64_t* ci = nullptr;
+    const int64_t* vals = nullptr;  // null = structural
+};
+cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const DevIn* mask, uint64_t max_chunk,
+                mgk_matrix* out);
+}  // namespace mx
 // CSR / CSC in external ids into host buffers (un-relabelled when relabelled)
 cudaError_t download_graph(const Graph* g, uint32_t* h_rp, uint32_t* h_ci, uint32_t* h_cp, uint32_t* h_ri);
 // device ids (scattered from a bitmap) -> external ids, ascending

@@ -289,6 +289,42 @@ def walk_targets(graph: DeviceGraph, source: int, min_hops: int, max_hops: int) 
     return ids[: n.value].copy()
 
 
+SEMIRING_BOOL_OR_AND, SEMIRING_PLUS_TIMES, SEMIRING_MIN_PLUS = 0, 1, 2  # sparse.hpp:54-66
+
+
+def mxm(a, b, semiring: int = SEMIRING_BOOL_OR_AND, mask=None, device: int = 0):
+    """mxm (sparse.cpp:292-363) on the GPU. Matrices are (nrows, ncols,
+    row_ptr, col_idx, vals|None) host tuples (vals None = structural);
+    returns the same shape (vals None for a structural / empty result)."""
+    def args(m):
+        nr, nc, rp, ci, v = m
+        rp = np.ascontiguousarray(rp, np.uint64)
+        ci = np.ascontiguousarray(ci, np.uint64) if len(ci) else np.zeros(1, np.uint64)
+        v = None if v is None else (np.ascontiguousarray(v, np.int64) if len(v) else np.zeros(1, np.int64))
+        return int(nr), int(nc), rp, ci, v
+    an, ac, arp, aci, av = args(a)
+    bn, bc, brp, bci, bv = args(b)
+    mn = mc = 0
+    mrp = mci = None
+    if mask is not None:
+        mn, mc, mrp, mci, _ = args(mask)
+    ptr = lambda x: None if x is None else x.ctypes.data  # noqa: E731
+    h = C.c_void_p()
+    _check(_lib.lib().mgk_mxm(device, an, ac, ptr(arp), ptr(aci), ptr(av), bn, bc, ptr(brp), ptr(bci), ptr(bv),
+                              int(semiring), mn, mc, ptr(mrp), ptr(mci), C.byref(h)))
+    try:
+        nr, nc, nnz, valued = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(_lib.lib().mgk_matrix_info(h, C.byref(nr), C.byref(nc), C.byref(nnz), C.byref(valued)))
+        rp = np.empty(nr.value + 1, np.uint64)
+        ci = np.empty(nnz.value, np.uint64)
+        vals = np.empty(nnz.value, np.int64) if valued.value else None
+        _check(_lib.lib().mgk_matrix_download(h, rp.ctypes.data, ci.ctypes.data if nnz.value else None,
+                                              vals.ctypes.data if vals is not None and nnz.value else None))
+    finally:
+        _lib.lib().mgk_matrix_free(h)
+    return nr.value, nc.value, rp, ci, vals
+
+
 def snapshot_check(text: bytes):
     """The GRAPHSNAP1 grammar on the host only (no GPU): (NODES, EDGES) or SnapshotError."""
     text = bytes(text)
@@ -338,7 +374,8 @@ def device_count() -> int:
     return int(_lib.lib().mgk_device_count())
 
 
-__all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "TraverseMode", "KHopQuery",
+__all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "mxm",
+           "SEMIRING_BOOL_OR_AND", "SEMIRING_PLUS_TIMES", "SEMIRING_MIN_PLUS", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
            "k_hop_count_device", "k_hop_count_multi", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

@@ -22,6 +22,10 @@ through oracle/ref_capi.cpp:
   reference's snapshot_from_string: node count and relation CSRs of valid
   texts (some written by the reference's own snapshot_to_string), and the
   exact SnapshotError message of malformed ones.
+* mxm_pins.json — mxm (sparse.cpp:292-363) over the three semirings, with
+  and without masks: hand examples (test_sparse.cpp:165-243 shapes), a seeded
+  random sweep of small matrices, RMAT graph products (SHA-256 of the result),
+  and the dimension error texts.
 * walk_pins.json — walk_targets (execute.cpp:43-60, the VarLenTraverse step)
   through the reference's own Cypher executor: counts and ids of
   MATCH (a {id: S})-[*min..max]->(b) on RMAT graphs and a cycle with a loop.
@@ -296,11 +300,93 @@ def snapshot_pins(R: oracle.Ref) -> dict:
     return {"valid": valid, "bench": bench, "errors": errors}
 
 
+def mxm_pins(R: oracle.Ref) -> dict:
+    """mxm through the reference (from_parts operands, vals None = structural)."""
+    def enc(m):
+        nr, nc, rp, ci, v = m
+        return {"nrows": int(nr), "ncols": int(nc), "row_ptr": [int(x) for x in rp],
+                "col_idx": [int(x) for x in ci], "vals": None if v is None else [int(x) for x in v]}
+
+    def from_dense(p, v, valued):
+        nr, nc = p.shape
+        rp = [0]
+        ci, vals = [], []
+        for i in range(nr):
+            for j in range(nc):
+                if p[i, j]:
+                    ci.append(j)
+                    vals.append(int(v[i, j]))
+            rp.append(len(ci))
+        return (nr, nc, np.array(rp, np.uint64), np.array(ci, np.uint64),
+                np.array(vals, np.int64) if valued else None)
+
+    cases = []
+
+    def add(name, a, b, sr, mask=None):
+        c = R.mxm(a, b, sr, mask)
+        cases.append({"name": name, "semiring": sr, "a": enc(a), "b": enc(b),
+                      "mask": None if mask is None else enc(mask), "c": enc(c)})
+
+    path = (4, 4, np.array([0, 1, 2, 3, 3], np.uint64), np.array([1, 2, 3], np.uint64), None)
+    add("path_squared", path, path, 0)
+    add("path_squared_masked", path, path, 0, (4, 4, np.array([0, 1, 1, 1, 1]), np.array([2]), None))
+    add("plus_times_2x2", (2, 2, np.array([0, 2, 3]), np.array([0, 1, 1]), np.array([1, 2, 3])),
+        (2, 2, np.array([0, 1, 3]), np.array([0, 0, 1]), np.array([4, 5, 6])), 1)
+    add("min_plus_3x3", (3, 3, np.array([0, 2, 3, 3]), np.array([1, 2, 2]), np.array([5, 9, 2])),
+        (3, 3, np.array([0, 2, 3, 3]), np.array([1, 2, 2]), np.array([5, 9, 2])), 2)
+    pat = (3, 3, np.array([0, 1, 2, 2]), np.array([1, 2]), None)
+    add("structural_plus_times", pat, pat, 1)
+    add("empty_valued", (2, 2, np.array([0, 0, 0]), np.array([]), np.array([], np.int64)),
+        (2, 2, np.array([0, 1, 1]), np.array([0]), np.array([3])), 1)
+    add("wraparound", (1, 1, np.array([0, 1]), np.array([0]), np.array([2 ** 62])),
+        (1, 2, np.array([0, 2]), np.array([0, 1]), np.array([4, -(2 ** 63)])), 1)
+    rng = np.random.default_rng(202)
+    for trial in range(150):
+        m, k, n = (int(x) for x in rng.integers(1, 21, 3))
+        sr = trial % 3
+        dens = (0.02, 0.1, 0.35)[(trial // 3) % 3]
+        valued = sr != 0
+        pa = rng.random((m, k)) < dens
+        pb = rng.random((k, n)) < dens
+        va = rng.integers(-50, 50, (m, k))
+        vb = rng.integers(-50, 50, (k, n))
+        mask = None
+        if trial % 4 == 0:
+            pm = rng.random((m, n)) < 0.5
+            mask = from_dense(pm, pm, False)
+        add(f"random_{trial}", from_dense(pa, va, valued), from_dense(pb, vb, valued), sr, mask)
+    out = {"cases": cases, "graphs": []}
+    for scale, rng_seed in ((9, 2), (10, 7)):
+        src, dst = R.rmat_generate(scale, rng_seed=rng_seed)
+        g = R.build_bench_graph(src, dst, 1 << scale)
+        rp, ci = g.relation_csr(None)
+        A = (len(rp) - 1, len(rp) - 1, rp, ci, None)
+        ent = {"scale": scale, "rng_seed": rng_seed}
+        for key, sr, mask in (("bool", 0, None), ("plus_times", 1, None), ("min_plus", 2, None),
+                              ("bool_masked_by_A", 0, A)):
+            c = R.mxm(A, A, sr, mask)
+            ent[key] = {"nnz": int(len(c[3])),
+                        "sha256": sha(c[2], c[3], c[4] if c[4] is not None else np.zeros(0, np.int64))}
+        out["graphs"].append(ent)
+    errs = []
+    for a, b, mask in (((2, 3), (4, 2), None), ((5, 4), (4, 6), (5, 5)), ((3, 3), (3, 3), (2, 3))):
+        A = (a[0], a[1], np.zeros(a[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        B = (b[0], b[1], np.zeros(b[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        M = None if mask is None else (mask[0], mask[1], np.zeros(mask[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        try:
+            R.mxm(A, B, 0, M)
+            raise SystemExit("mxm dimension case unexpectedly passed")
+        except oracle.RefError as e:
+            errs.append({"a": list(a), "b": list(b), "mask": None if mask is None else list(mask), "error": str(e)})
+    out["errors"] = errs
+    return out
+
+
 def main() -> None:
     R = oracle.Ref()
     for name, fn in (("known_answers", known_answers), ("c1_sweep", c1_sweep),
                      ("harness_pins", harness_pins), ("walk_pins", walk_pins),
-                     ("snapshot_pins", snapshot_pins)):
+                     ("snapshot_pins", snapshot_pins), ("mxm_pins", mxm_pins)):
         data = fn(R)
         data["_generated_by"] = "tests/golden/make_golden.py from oracle/_ref (reference core)"
         (OUT / f"{name}.json").write_text(json.dumps(data, separators=(",", ":")) + "\n")
