@@ -46,6 +46,27 @@ inline constexpr std::uint32_t kMaxHops = 32;  // ast.hpp:15
 
 enum class TraverseMode : std::uint8_t { Exact, Cumulative };  // plan.hpp:17
 
+// ---- semirings (sparse.hpp:45-67) -------------------------------------------------
+enum class BinaryOp : std::uint8_t { BoolOr, BoolAnd, Plus, Times, Min };
+std::int64_t apply(BinaryOp op, std::int64_t lhs, std::int64_t rhs);
+struct Semiring {
+    BinaryOp add_op = BinaryOp::BoolOr;
+    BinaryOp mul_op = BinaryOp::BoolAnd;
+    std::int64_t add_identity = 0;
+    static const Semiring& bool_or_and();
+    static const Semiring& plus_times();
+    static const Semiring& min_plus();
+    bool is_boolean() const noexcept { return add_op == BinaryOp::BoolOr; }
+    friend bool operator==(const Semiring&, const Semiring&) = default;
+};
+
+struct MatrixTuple {  // sparse.hpp:69-75
+    std::uint64_t row = 0;
+    std::uint64_t col = 0;
+    std::int64_t value = 1;
+    friend bool operator==(const MatrixTuple&, const MatrixTuple&) = default;
+};
+
 // ---- sparse types (sparse.hpp:13-43, 83-134), the subset the path reads -----------
 class BitVector {
 public:
@@ -68,24 +89,41 @@ public:
     SparseMatrix() = default;
     SparseMatrix(std::uint64_t nrows, std::uint64_t ncols)
         : nrows_(nrows), ncols_(ncols), row_ptr_(nrows + 1, 0) {}
+    /// Valued when `vals` is non-empty (one int64 per entry), like the reference.
     static SparseMatrix from_parts(std::uint64_t nrows, std::uint64_t ncols,
                                    std::vector<std::uint64_t> row_ptr,
-                                   std::vector<std::uint64_t> col_idx);
+                                   std::vector<std::uint64_t> col_idx,
+                                   std::vector<std::int64_t> vals = {});
     std::uint64_t nrows() const noexcept { return nrows_; }
     std::uint64_t ncols() const noexcept { return ncols_; }
     std::uint64_t nvals() const noexcept { return col_idx_.size(); }
+    bool has_values() const noexcept { return valued_; }
+    bool valued() const noexcept { return valued_; }
     std::span<const std::uint64_t> row_ptr() const noexcept { return row_ptr_; }
     std::span<const std::uint64_t> col_idx() const noexcept { return col_idx_; }
+    std::span<const std::int64_t> values() const noexcept { return vals_; }
     std::span<const std::uint64_t> row(std::uint64_t r) const;
+    std::span<const std::int64_t> row_values(std::uint64_t r) const;
+    bool contains(std::uint64_t r, std::uint64_t c) const;
+    /// (row, col, value) in row-major order; value 1 for a structural matrix.
+    std::vector<MatrixTuple> extract_tuples() const;
 
 private:
     std::uint64_t nrows_ = 0, ncols_ = 0;
+    bool valued_ = false;
     std::vector<std::uint64_t> row_ptr_ = {0};
     std::vector<std::uint64_t> col_idx_;
+    std::vector<std::int64_t> vals_;
 };
 
 std::uint64_t nvals(const SparseMatrix& m);
 std::uint64_t nvals(const BitVector& v);
+
+/// mxm (sparse.cpp:292-363) computed on the GPU (mgk_mxm): C = A (+.*) B,
+/// restricted to the pattern of `mask` when given. Same results and messages
+/// as the reference ("mxm: inner dimensions disagree ...", "mxm: mask shape ...").
+SparseMatrix mxm(const SparseMatrix& a, const SparseMatrix& b,
+                 const Semiring& semiring = Semiring::bool_or_and(), const SparseMatrix* mask = nullptr);
 
 // ---- graph store (graph.hpp:20-124), load API + matrix access ---------------------
 struct RelationRef {

@@ -79,15 +79,96 @@ BitVector BitVector::from_sorted(std::uint64_t dimension, std::vector<std::uint6
 
 SparseMatrix SparseMatrix::from_parts(std::uint64_t nrows, std::uint64_t ncols,
                                       std::vector<std::uint64_t> row_ptr,
-                                      std::vector<std::uint64_t> col_idx) {
+                                      std::vector<std::uint64_t> col_idx,
+                                      std::vector<std::int64_t> vals) {
     if (row_ptr.size() != nrows + 1 || row_ptr.front() != 0 || row_ptr.back() != col_idx.size())
         throw Error("SparseMatrix invariant violated: row_ptr shape");
+    if (!vals.empty() && vals.size() != col_idx.size())
+        throw Error("SparseMatrix invariant violated: value count");
     SparseMatrix m;
     m.nrows_ = nrows;
     m.ncols_ = ncols;
+    m.valued_ = !vals.empty();
     m.row_ptr_ = std::move(row_ptr);
     m.col_idx_ = std::move(col_idx);
+    m.vals_ = std::move(vals);
     return m;
+}
+
+std::span<const std::int64_t> SparseMatrix::row_values(std::uint64_t r) const {
+    if (r >= nrows_)
+        throw ContractError(fmt("row %llu out of range for %llux%llu matrix", (unsigned long long)r,
+                                (unsigned long long)nrows_, (unsigned long long)ncols_));
+    if (!valued_) return {};
+    return std::span(vals_).subspan(row_ptr_[r], row_ptr_[r + 1] - row_ptr_[r]);
+}
+
+bool SparseMatrix::contains(std::uint64_t r, std::uint64_t c) const {
+    const auto cols = row(r);
+    return std::binary_search(cols.begin(), cols.end(), c);
+}
+
+std::vector<MatrixTuple> SparseMatrix::extract_tuples() const {
+    std::vector<MatrixTuple> out;
+    out.reserve(col_idx_.size());
+    for (std::uint64_t r = 0; r < nrows_; ++r)
+        for (std::uint64_t p = row_ptr_[r]; p < row_ptr_[r + 1]; ++p)
+            out.push_back({r, col_idx_[p], valued_ ? vals_[p] : 1});
+    return out;
+}
+
+// ---- semirings (sparse.cpp:69-93) --------------------------------------------------
+std::int64_t apply(BinaryOp op, std::int64_t lhs, std::int64_t rhs) {
+    switch (op) {
+        case BinaryOp::BoolOr: return (lhs != 0 || rhs != 0) ? 1 : 0;
+        case BinaryOp::BoolAnd: return (lhs != 0 && rhs != 0) ? 1 : 0;
+        case BinaryOp::Plus: return (std::int64_t)((std::uint64_t)lhs + (std::uint64_t)rhs);
+        case BinaryOp::Times: return (std::int64_t)((std::uint64_t)lhs * (std::uint64_t)rhs);
+        case BinaryOp::Min: return lhs < rhs ? lhs : rhs;
+    }
+    throw ContractError("unknown binary operator");
+}
+
+const Semiring& Semiring::bool_or_and() {
+    static const Semiring s{BinaryOp::BoolOr, BinaryOp::BoolAnd, 0};
+    return s;
+}
+const Semiring& Semiring::plus_times() {
+    static const Semiring s{BinaryOp::Plus, BinaryOp::Times, 0};
+    return s;
+}
+const Semiring& Semiring::min_plus() {
+    static const Semiring s{BinaryOp::Min, BinaryOp::Plus, INT64_MAX};
+    return s;
+}
+
+SparseMatrix mxm(const SparseMatrix& a, const SparseMatrix& b, const Semiring& semiring,
+                 const SparseMatrix* mask) {
+    int code = -1;
+    if (semiring == Semiring::bool_or_and()) code = MGK_SEMIRING_BOOL_OR_AND;
+    else if (semiring == Semiring::plus_times()) code = MGK_SEMIRING_PLUS_TIMES;
+    else if (semiring == Semiring::min_plus()) code = MGK_SEMIRING_MIN_PLUS;
+    if (code < 0) throw ContractError("mxm: unsupported semiring");
+    const std::uint64_t zero = 0;
+    auto ci = [&](const SparseMatrix& m) { return m.nvals() ? m.col_idx().data() : &zero; };
+    auto vals = [&](const SparseMatrix& m) -> const std::int64_t* {
+        return m.valued() && m.nvals() ? m.values().data() : nullptr;
+    };
+    mgk_matrix* h = nullptr;
+    const int rc = mgk_mxm(0, a.nrows(), a.ncols(), a.row_ptr().data(), ci(a), vals(a), b.nrows(), b.ncols(),
+                           b.row_ptr().data(), ci(b), vals(b), code, mask ? mask->nrows() : 0,
+                           mask ? mask->ncols() : 0, mask ? mask->row_ptr().data() : nullptr,
+                           mask ? ci(*mask) : nullptr, &h);
+    if (rc == MGK_ECONTRACT || rc == MGK_ERANGE) throw ContractError(mgk_last_error());
+    if (rc) throw Error(mgk_last_error());
+    std::uint64_t nr = 0, nc = 0, nnz = 0;
+    int valued = 0;
+    mgk_matrix_info(h, &nr, &nc, &nnz, &valued);
+    std::vector<std::uint64_t> rp(nr + 1), c(nnz);
+    std::vector<std::int64_t> v(valued ? nnz : 0);
+    mgk_matrix_download(h, rp.data(), c.data(), valued ? v.data() : nullptr);
+    mgk_matrix_free(h);
+    return SparseMatrix::from_parts(nr, nc, std::move(rp), std::move(c), std::move(v));
 }
 
 std::span<const std::uint64_t> SparseMatrix::row(std::uint64_t r) const {

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
+#include <random>
 #include <set>
 #include <string>
 #include <vector>
@@ -22,6 +23,10 @@ typedef struct orc_adj orc_adj;
 orc_adj* orc_adj_new(uint64_t n, uint64_t m, const uint32_t* src, const uint32_t* dst);
 void orc_adj_free(orc_adj* g);
 uint64_t orc_bfs_count(const orc_adj* g, uint64_t seed, uint32_t k, int mode);
+uint64_t orc_mxm(uint64_t a_nrows, const uint64_t* a_rp, const uint64_t* a_ci, const int64_t* a_vals,
+                 uint64_t b_ncols, const uint64_t* b_rp, const uint64_t* b_ci, const int64_t* b_vals,
+                 int semiring, const uint64_t* m_rp, const uint64_t* m_ci,
+                 uint64_t* out_rp, uint64_t* out_ci, int64_t* out_vals);
 }
 
 using namespace matgraph;
@@ -268,6 +273,101 @@ GPU_TEST_CASE("c1: 8000 k-hop counts equal the BFS oracle") {  // acceptance_mai
     }
     CHECK(mismatches == 0);
     CHECK(agreements == 8000);
+}
+
+// ---- mxm (proj/tests/test_sparse.cpp:165-243 shapes) --------------------------------------
+namespace {
+SparseMatrix build(std::uint64_t nr, std::uint64_t nc, std::vector<MatrixTuple> t, bool valued) {
+    std::sort(t.begin(), t.end(), [](const MatrixTuple& x, const MatrixTuple& y) {
+        return x.row != y.row ? x.row < y.row : x.col < y.col;
+    });
+    std::vector<std::uint64_t> rp(nr + 1, 0), ci;
+    std::vector<std::int64_t> v;
+    for (auto& x : t) {
+        ++rp[x.row + 1];
+        ci.push_back(x.col);
+        if (valued) v.push_back(x.value);
+    }
+    for (std::uint64_t i = 0; i < nr; ++i) rp[i + 1] += rp[i];
+    return SparseMatrix::from_parts(nr, nc, std::move(rp), std::move(ci), std::move(v));
+}
+
+SparseMatrix oracle_mxm(const SparseMatrix& a, const SparseMatrix& b, int sr, const SparseMatrix* mask) {
+    auto vals = [](const SparseMatrix& m) { return m.valued() ? m.values().data() : nullptr; };
+    const std::uint64_t nnz = orc_mxm(a.nrows(), a.row_ptr().data(), a.col_idx().data(), vals(a), b.ncols(),
+                                      b.row_ptr().data(), b.col_idx().data(), vals(b), sr,
+                                      mask ? mask->row_ptr().data() : nullptr,
+                                      mask ? mask->col_idx().data() : nullptr, nullptr, nullptr, nullptr);
+    std::vector<std::uint64_t> rp(a.nrows() + 1), ci(nnz);
+    std::vector<std::int64_t> v(nnz);
+    orc_mxm(a.nrows(), a.row_ptr().data(), a.col_idx().data(), vals(a), b.ncols(), b.row_ptr().data(),
+            b.col_idx().data(), vals(b), sr, mask ? mask->row_ptr().data() : nullptr,
+            mask ? mask->col_idx().data() : nullptr, rp.data(), ci.data(), v.data());
+    if (sr == 0 || nnz == 0) v.clear();
+    return SparseMatrix::from_parts(a.nrows(), b.ncols(), std::move(rp), std::move(ci), std::move(v));
+}
+}  // namespace
+
+GPU_TEST_CASE("mxm hand examples") {
+    const SparseMatrix path = build(4, 4, {{0, 1}, {1, 2}, {2, 3}}, false);
+    const SparseMatrix two = mxm(path, path);
+    CHECK(nvals(two) == 2);
+    CHECK(two.contains(0, 2));
+    CHECK(two.contains(1, 3));
+    CHECK(!two.valued());
+    const SparseMatrix a = build(2, 2, {{0, 0, 1}, {0, 1, 2}, {1, 1, 3}}, true);
+    const SparseMatrix b = build(2, 2, {{0, 0, 4}, {1, 0, 5}, {1, 1, 6}}, true);
+    const auto t = mxm(a, b, Semiring::plus_times()).extract_tuples();
+    REQUIRE(t.size() == 4);
+    CHECK(t[0] == (MatrixTuple{0, 0, 14}));
+    CHECK(t[1] == (MatrixTuple{0, 1, 12}));
+    CHECK(t[2] == (MatrixTuple{1, 0, 15}));
+    CHECK(t[3] == (MatrixTuple{1, 1, 18}));
+    const SparseMatrix d = build(3, 3, {{0, 1, 5}, {1, 2, 2}, {0, 2, 9}}, true);
+    const auto dist = mxm(d, d, Semiring::min_plus()).extract_tuples();
+    REQUIRE(dist.size() == 1);
+    CHECK(dist[0] == (MatrixTuple{0, 2, 7}));
+    CHECK_THROWS_WITH_AS(mxm(a, build(3, 3, {}, false)), "mxm: inner dimensions disagree (2x2 times 3x3)",
+                         ContractError);
+    const SparseMatrix pattern = build(3, 3, {{0, 1}, {1, 2}}, false);
+    const auto counted = mxm(pattern, pattern, Semiring::plus_times()).extract_tuples();
+    REQUIRE(counted.size() == 1);
+    CHECK(counted[0] == (MatrixTuple{0, 2, 1}));
+}
+
+GPU_TEST_CASE("mxm mask restricts the result pattern") {
+    const SparseMatrix path = build(4, 4, {{0, 1}, {1, 2}, {2, 3}}, false);
+    const SparseMatrix mask = build(4, 4, {{0, 2}}, false);
+    const SparseMatrix two = mxm(path, path, Semiring::bool_or_and(), &mask);
+    CHECK(nvals(two) == 1);
+    CHECK(two.contains(0, 2));
+    const SparseMatrix bad = build(3, 4, {}, false);
+    CHECK_THROWS_WITH_AS(mxm(path, path, Semiring::bool_or_and(), &bad),
+                         "mxm: mask shape 3x4 != result shape 4x4", ContractError);
+}
+
+GPU_TEST_CASE("mxm agrees with the C oracle across semirings") {
+    std::mt19937_64 rng(202);
+    const Semiring* rings[] = {&Semiring::bool_or_and(), &Semiring::plus_times(), &Semiring::min_plus()};
+    for (int trial = 0; trial < 90; ++trial) {
+        const std::uint64_t m = 1 + rng() % 20, k = 1 + rng() % 20, n = 1 + rng() % 20;
+        const int sr = trial % 3;
+        const double dens[] = {0.02, 0.1, 0.35};
+        const double d = dens[(trial / 3) % 3];
+        auto rand_t = [&](std::uint64_t nr, std::uint64_t nc, double p) {
+            std::vector<MatrixTuple> t;
+            for (std::uint64_t i = 0; i < nr; ++i)
+                for (std::uint64_t j = 0; j < nc; ++j)
+                    if ((double)(rng() >> 11) * 0x1.0p-53 < p) t.push_back({i, j, (std::int64_t)(rng() % 101) - 50});
+            return t;
+        };
+        const SparseMatrix a = build(m, k, rand_t(m, k, d), sr != 0), b = build(k, n, rand_t(k, n, d), sr != 0);
+        const SparseMatrix mask = build(m, n, rand_t(m, n, 0.5), false);
+        const SparseMatrix* mp = trial % 4 == 0 ? &mask : nullptr;
+        const SparseMatrix got = mxm(a, b, *rings[sr], mp), want = oracle_mxm(a, b, sr, mp);
+        CHECK(got.extract_tuples() == want.extract_tuples());
+        CHECK(got.valued() == want.valued());
+    }
 }
 
 int main(int argc, char** argv) { return mini::run(argc, argv); }
