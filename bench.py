@@ -348,9 +348,17 @@ def run_ours(args):
     from paper_1905_01294_b200 import Tuning
 
     rank, local, world = dist_env()
+    # MGK_BENCH_DRYRUN=1: functional check of the multi-rank path on a box with
+    # fewer GPUs than ranks (gloo, ranks share devices; its numbers mean nothing)
+    dry = os.environ.get("MGK_BENCH_DRYRUN") == "1"
+    if dry:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if dry:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rp, ci, seeds = build_inputs(world, rank, dist if world > 1 else None, torch.device("cuda", local))
     t = time.time()
     g = DeviceGraph.from_csr(rp, ci, device=local)

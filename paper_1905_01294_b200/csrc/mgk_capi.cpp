@@ -84,7 +84,8 @@ cudaError_t create_ws(Graph* g, Workspace* ws, bool own_stream) {
     if ((e = cudaMemset(ws->qctl, 0, 4 * sizeof(QCtl)))) return e;
     if ((e = cudaMemset(ws->misc, 0, 16 * 8))) return e;
     ws->bytes += 4 * sizeof(QCtl) + 128 + (MGK_MAX_HOPS + 2) * sizeof(LevelCounters);
-    return cudaSuccess;
+    // legacy-stream memsets do not order non-blocking streams: finish them now
+    return cudaStreamSynchronize(0);
 }
 
 void destroy_ws(Workspace* ws, bool own_stream) {

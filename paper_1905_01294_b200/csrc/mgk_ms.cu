@@ -752,7 +752,8 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
         ws->bytes += (size_t)(g.nwords + 1) * 4 + ws->rlog_cap * 4 + 2 * items * sizeof(uint4);
     }
     ws->lanes_words = W;
-    return cudaSuccess;
+    // zero state complete before the first launch on a non-blocking stream
+    return cudaStreamSynchronize(0);
 }
 
 cudaError_t launch_lanes(Launch& L) {

@@ -937,7 +937,10 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     ws->bytes += 2 * (size_t)ws->fr_big_cap * 8;
     ws->bytes += 4 * bm + 2 * (size_t)ws->fr_items_cap * 8 + (size_t)ws->fr_log_cap * 8 + cs * 12 +
                  (size_t)S * 14 + sizeof(FRCtl);
-    return cudaSuccess;
+    // the memsets above run on the legacy stream, which does not order work on
+    // the non-blocking streams the engines launch on: the zero state must be
+    // complete before the first traversal (recycled allocations are not zero)
+    return cudaStreamSynchronize(0);
 }
 
 // k = 1 on duplicate-free rows: |F_1| = deg(s) - [s in row(s)]. One warp per

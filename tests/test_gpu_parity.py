@@ -373,3 +373,17 @@ def test_replicas_and_multi(port, g1):
         k_hop_count_multi(reps, [int(seeds[0]), 99999999], 2)
     with pytest.raises(ContractError, match=r"k-hop count 0 outside \[1, 32\]"):
         k_hop_count_multi(reps, seeds, 0)
+
+
+def test_two_processes_share_one_gpu():
+    """Regression: workspace zeroing ran on the legacy stream, unordered with
+    the engines' non-blocking streams; with another process on the GPU the
+    first traversal could start on recycled, non-zero bitmaps."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    worker = Path(__file__).resolve().parent / "helpers" / "share_worker.py"
+    procs = [subprocess.Popen([sys.executable, str(worker)], stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+                              text=True) for _ in range(2)]
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    assert all(p.returncode == 0 for p in procs), outs
