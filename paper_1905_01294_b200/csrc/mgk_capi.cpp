@@ -778,7 +778,9 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     if (!ws) return fail(MGK_ECONTRACT, "no device-path call was made on this stream");
     DeviceGuard dg(h->g.device);
     LevelCounters lc[MGK_MAX_HOPS + 2];
-    cudaError_t e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
+    // the counters of the last call enqueued on this stream: wait for it
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (!e) e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
     if (e) return fail_cuda(e, "stats");
     fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f,
                ws->last_launches);

@@ -480,6 +480,8 @@ cudaError_t load_to_graph(Graph* g, const char* text, uint64_t len, const char* 
         SNAP_TRY(cub::DeviceSelect::If(tmp, tb2, it, d_nl, d_cnt, (int64_t)len, pred, s));
         cudaFreeAsync(tmp, s);
         tmp = nullptr;
+        // host_line below reads d_nl with plain (legacy-stream) copies
+        SNAP_TRY(cudaStreamSynchronize(s));
     }
     L = nnl + ((len > 0 && text[len - 1] != '\n') ? 1 : 0);
     SNAP_TRY(cudaMalloc(&suspect, std::max<uint64_t>(L, 1)));
@@ -567,8 +569,10 @@ cudaError_t load_to_graph(Graph* g, const char* text, uint64_t len, const char* 
                 const unsigned long long key = ((unsigned long long)src << 32) | dst;
                 const uint8_t kp = (!relation || rel == relation) ? 1 : 0;
                 const uint64_t j = idx - edges_idx - 1;
-                SNAP_TRY(cudaMemcpy(keys + j, &key, 8, cudaMemcpyHostToDevice));
-                SNAP_TRY(cudaMemcpy(keep + j, &kp, 1, cudaMemcpyHostToDevice));
+                // on s: ordered before the compaction below
+                SNAP_TRY(cudaMemcpyAsync(keys + j, &key, 8, cudaMemcpyHostToDevice, s));
+                SNAP_TRY(cudaMemcpyAsync(keep + j, &kp, 1, cudaMemcpyHostToDevice, s));
+                SNAP_TRY(cudaStreamSynchronize(s));  // key / kp live on this stack frame
             }
         }
     }
