@@ -192,7 +192,7 @@ int mgk_matrix_free(mgk_matrix* m);
  * and serialize on that stream. */
 int mgk_khop_count_device(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
                           int mode, int engine, uint64_t* d_counts, void* stream);
-/* Work counters of the last device-path call on `stream` (synchronize first;
+/* Work counters of the last device-path call on `stream` (waits for that stream;
  * kernel_ms is 0 on this path — time it with your own events). */
 int mgk_khop_device_stats(mgk_graph* g, void* stream, mgk_stats* stats);
 
