@@ -387,3 +387,17 @@ def test_two_processes_share_one_gpu():
                               text=True) for _ in range(2)]
     outs = [p.communicate(timeout=600)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
+
+
+def test_concurrent_host_calls_on_one_graph(g1):
+    """The reference's server runs queries from several worker threads against
+    one graph (server.cpp:75-76): calls are reentrant (own workspace and
+    stream each) and answer exactly like sequential calls."""
+    from concurrent.futures import ThreadPoolExecutor
+    rp, ci, g = g1
+    jobs = [(H.pick_seeds(rp, 50 + 7 * i, 100 + i), 1 + i % 4, i % 2) for i in range(16)]
+    want = [k_hop_count_batch(g, s, k, m).tolist() for s, k, m in jobs]
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        for _ in range(3):
+            got = list(ex.map(lambda j: k_hop_count_batch(g, j[0], j[1], j[2]).tolist(), jobs))
+            assert got == want
