@@ -31,12 +31,19 @@
 
 #include "mgk_internal.cuh"
 
+// The result stays on the device until the caller downloads it (one copy,
+// straight into the caller's arrays); row_ptr is small and kept on the host.
 struct mgk_matrix {
-    uint64_t nrows = 0, ncols = 0;
+    int device = 0;
+    uint64_t nrows = 0, ncols = 0, nnz = 0;
     bool valued = false;
     std::vector<uint64_t> row_ptr;
-    std::vector<uint64_t> col_idx;
-    std::vector<int64_t> vals;
+    unsigned long long* d_col = nullptr;  // [nnz] (uint64 columns)
+    long long* d_vals = nullptr;          // [nnz] when valued
+    ~mgk_matrix() {
+        cudaFree(d_col);
+        cudaFree(d_vals);
+    }
 };
 
 namespace mgk {
@@ -159,6 +166,21 @@ __global__ void mark_first(const unsigned long long* keys, uint64_t n, uint8_t* 
         keep[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
 }
 
+// first output position of every row present in the sorted keys
+__global__ void row_firsts(const unsigned long long* keys, uint64_t n, unsigned long long* first) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long r = keys[x] >> 32;
+        if (x == 0 || (keys[x - 1] >> 32) != r) first[r] = x;
+    }
+}
+
+__global__ void keys_to_cols(unsigned long long* keys, uint64_t n) {
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        keys[x] &= 0xFFFFFFFFull;
+}
+
 int bits_for(uint64_t n) {
     int b = 1;
     while (b < 32 && (1ull << b) < n) ++b;
@@ -170,7 +192,6 @@ int bits_for(uint64_t n) {
 // 0 ok; cudaError_t on device failure
 cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const DevIn* mask,
                 uint64_t max_chunk, mgk_matrix* out) {
-    (void)device;
     const int add_op = semiring == 0 ? kBoolOr : semiring == 1 ? kPlus : kMin;
     const int mul_op = semiring == 0 ? kBoolAnd : semiring == 1 ? kTimes : kPlus;
     const bool valued = semiring != 0;
@@ -184,13 +205,44 @@ cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const 
     unsigned long long* d_num = nullptr;
     void* tmp = nullptr;
     std::vector<unsigned long long> h_off;
-    std::vector<unsigned long long> h_keys;
-    std::vector<long long> h_vals;
+    // device output: reduced (row << 32 | col) keys and values of all chunks, in order
+    unsigned long long* okeys = nullptr;
+    long long* ovals = nullptr;
+    uint64_t on = 0, ocap = 0;
+    unsigned long long* first = nullptr;
+    auto reserve = [&](uint64_t need) -> cudaError_t {
+        if (need <= ocap) return cudaSuccess;
+        const uint64_t nc = std::max<uint64_t>({need, 2 * ocap, 1ull << 20});
+        unsigned long long* nk = nullptr;
+        long long* nv = nullptr;
+        cudaError_t r = cudaMalloc(&nk, nc * 8);
+        if (!r && valued) r = cudaMalloc(&nv, nc * 8);
+        if (!r && on) r = cudaMemcpyAsync(nk, okeys, on * 8, cudaMemcpyDeviceToDevice, s);
+        if (!r && on && valued) r = cudaMemcpyAsync(nv, ovals, on * 8, cudaMemcpyDeviceToDevice, s);
+        if (!r) r = cudaStreamSynchronize(s);
+        if (r) {
+            cudaFree(nk);
+            cudaFree(nv);
+            return r;
+        }
+        cudaFree(okeys);
+        cudaFree(ovals);
+        okeys = nk;
+        ovals = nv;
+        ocap = nc;
+        return cudaSuccess;
+    };
+    auto append = [&](const unsigned long long* k, const long long* v, uint64_t n) -> cudaError_t {
+        cudaError_t r = reserve(on + n);
+        if (!r && n) r = cudaMemcpyAsync(okeys + on, k, n * 8, cudaMemcpyDeviceToDevice, s);
+        if (!r && n && valued) r = cudaMemcpyAsync(ovals + on, v, n * 8, cudaMemcpyDeviceToDevice, s);
+        on += n;
+        return r;
+    };
+    out->device = device;
     out->nrows = a.nrows;
     out->ncols = b.ncols;
     out->row_ptr.assign(a.nrows + 1, 0);
-    out->col_idx.clear();
-    out->vals.clear();
     MX_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     MX_TRY(upload(A, a.nrows, a.ncols, a.rp, a.ci, valued ? a.vals : nullptr, s));
     MX_TRY(upload(B, b.nrows, b.ncols, b.rp, b.ci, valued ? b.vals : nullptr, s));
@@ -236,7 +288,7 @@ cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const 
             // product range of the chunk, cut into pieces of <= cap products
             // (a piece may start or end inside an A entry's B row)
             const unsigned long long T0 = h_off[a.rp[r0]], T1 = h_off[a.rp[r1]];
-            const size_t chunk_start = h_keys.size();
+            const uint64_t chunk_start = on;
             int pieces = 0;
             for (unsigned long long t0 = T0; t0 < T1;) {
                 ++pieces;
@@ -284,11 +336,7 @@ cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const 
                             MX_TRY(cudaMemcpyAsync(&nun, d_num, 8, cudaMemcpyDeviceToHost, s));
                             MX_TRY(cudaStreamSynchronize(s));
                             nu = nun;
-                            const size_t at = h_keys.size();
-                            h_keys.resize(at + nu);
-                            h_vals.resize(at + nu);
-                            MX_TRY(cudaMemcpy(h_keys.data() + at, ukeys, nu * 8, cudaMemcpyDeviceToHost));
-                            MX_TRY(cudaMemcpy(h_vals.data() + at, uvals, nu * 8, cudaMemcpyDeviceToHost));
+                            MX_TRY(append(ukeys, uvals, nu));
                         } else {
                             cub::DoubleBuffer<unsigned long long> dk(kalt, keys);
                             size_t tb3 = 0;
@@ -310,65 +358,73 @@ cudaError_t run(int device, const DevIn& a, const DevIn& b, int semiring, const 
                             MX_TRY(cudaMemcpyAsync(&nun, d_num, 8, cudaMemcpyDeviceToHost, s));
                             MX_TRY(cudaStreamSynchronize(s));
                             nu = nun;
-                            const size_t at = h_keys.size();
-                            h_keys.resize(at + nu);
-                            MX_TRY(cudaMemcpy(h_keys.data() + at, other, nu * 8, cudaMemcpyDeviceToHost));
+                            MX_TRY(append(other, nullptr, nu));
                         }
                     }
                 }
                 t0 = t1;
             }
             if (pieces > 1) {
-                // one row wider than a chunk: its pieces overlap in columns; merge them
-                std::vector<std::pair<unsigned long long, long long>> kv(h_keys.size() - chunk_start);
-                for (size_t x = 0; x < kv.size(); ++x)
-                    kv[x] = {h_keys[chunk_start + x], valued ? h_vals[chunk_start + x] : 0};
+                // one row wider than a chunk: its pieces overlap in columns;
+                // merge them on the host (rare) and write the row back
+                const uint64_t ns = on - chunk_start;
+                std::vector<unsigned long long> hk(ns);
+                std::vector<long long> hv(valued ? ns : 0);
+                MX_TRY(cudaStreamSynchronize(s));
+                MX_TRY(cudaMemcpy(hk.data(), okeys + chunk_start, ns * 8, cudaMemcpyDeviceToHost));
+                if (valued) MX_TRY(cudaMemcpy(hv.data(), ovals + chunk_start, ns * 8, cudaMemcpyDeviceToHost));
+                std::vector<std::pair<unsigned long long, long long>> kv(ns);
+                for (size_t x = 0; x < ns; ++x) kv[x] = {hk[x], valued ? hv[x] : 0};
                 std::stable_sort(kv.begin(), kv.end(),
                                  [](const auto& l, const auto& r) { return l.first < r.first; });
-                h_keys.resize(chunk_start);
-                if (valued) h_vals.resize(chunk_start);
+                hk.clear();
+                hv.clear();
                 for (size_t x = 0; x < kv.size(); ++x) {
                     if (x && kv[x].first == kv[x - 1].first) {
-                        if (valued) h_vals.back() = apply(add_op, h_vals.back(), kv[x].second);
+                        if (valued) hv.back() = apply(add_op, hv.back(), kv[x].second);
                         continue;
                     }
-                    h_keys.push_back(kv[x].first);
-                    if (valued) h_vals.push_back(kv[x].second);
+                    hk.push_back(kv[x].first);
+                    if (valued) hv.push_back(kv[x].second);
                 }
+                MX_TRY(cudaMemcpy(okeys + chunk_start, hk.data(), hk.size() * 8, cudaMemcpyHostToDevice));
+                if (valued) MX_TRY(cudaMemcpy(ovals + chunk_start, hv.data(), hv.size() * 8, cudaMemcpyHostToDevice));
+                on = chunk_start + hk.size();
             }
             r0 = r1;
         }
     }
-    {
-        // keys are (row, col) ascending across chunks: CSR (host threads; the
-        // row starts come from the sorted keys, so no counting pass is needed)
-        const size_t nk = h_keys.size();
-        out->col_idx.resize(nk);
-        const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        std::vector<std::thread> ts;
-        for (unsigned t = 0; t < nt; ++t)
-            ts.emplace_back([&, t] {
-                const size_t x0 = nk * t / nt, x1 = nk * (t + 1) / nt;
-                for (size_t x = x0; x < x1; ++x) out->col_idx[x] = (uint32_t)h_keys[x];
-            });
-        for (auto& th : ts) th.join();
-        // row_ptr[i] = first key position with row >= i
-        size_t x = 0;
-        for (uint64_t i = 0; i <= a.nrows; ++i) {
-            while (x < nk && (h_keys[x] >> 32) < i) ++x;
-            out->row_ptr[i] = x;
-        }
+    // keys are (row, col) ascending across chunks: row starts from the keys,
+    // then the keys become the column array in place
+    MX_TRY(cudaMallocAsync(&first, (a.nrows + 1) * 8, s));
+    MX_TRY(cudaMemsetAsync(first, 0xFF, (a.nrows + 1) * 8, s));
+    if (on) {
+        row_firsts<<<blocks_for(on), kTB, 0, s>>>(okeys, on, first);
+        keys_to_cols<<<blocks_for(on), kTB, 0, s>>>(okeys, on);
+        MX_TRY(cudaGetLastError());
     }
-    out->vals.assign(h_vals.begin(), h_vals.end());
-    out->valued = valued && !out->vals.empty();  // from_parts: valued = !vals.empty()
+    MX_TRY(cudaMemcpyAsync(out->row_ptr.data(), first, (a.nrows + 1) * 8, cudaMemcpyDeviceToHost, s));
+    MX_TRY(cudaStreamSynchronize(s));
+    out->row_ptr[a.nrows] = on;  // rows without entries start where the next row starts
+    for (uint64_t i2 = a.nrows; i2-- > 0;)
+        out->row_ptr[i2] = std::min<uint64_t>(out->row_ptr[i2], out->row_ptr[i2 + 1]);
+    out->nnz = on;
+    out->valued = valued && on > 0;  // from_parts: valued = !vals.empty()
+    out->d_col = okeys;
+    out->d_vals = valued ? ovals : nullptr;
+    if (!valued) cudaFree(ovals);
+    okeys = nullptr;
+    ovals = nullptr;
 done:
     if (tmp) cudaFreeAsync(tmp, s);
     if (s) cudaStreamSynchronize(s);
     release(A);
     release(B);
     release(M);
+    cudaFree(okeys);  // only on an error path (ownership moved to `out` otherwise)
+    cudaFree(ovals);
     for (void* pz : {(void*)cnt, (void*)off, (void*)arow, (void*)keys, (void*)kalt, (void*)ukeys, (void*)vals,
-                     (void*)valt, (void*)uvals, (void*)keep, (void*)d_num})
+                     (void*)valt, (void*)uvals, (void*)keep, (void*)d_num, (void*)first})
         if (pz) cudaFreeAsync(pz, s);
     if (s) {
         cudaStreamSynchronize(s);
@@ -459,7 +515,7 @@ int mgk_matrix_info(const mgk_matrix* m, uint64_t* nrows, uint64_t* ncols, uint6
     if (!m) return fail_code(MGK_ECONTRACT, "null matrix");
     if (nrows) *nrows = m->nrows;
     if (ncols) *ncols = m->ncols;
-    if (nnz) *nnz = m->col_idx.size();
+    if (nnz) *nnz = m->nnz;
     if (valued) *valued = m->valued ? 1 : 0;
     return MGK_OK;
 }
@@ -467,13 +523,24 @@ int mgk_matrix_info(const mgk_matrix* m, uint64_t* nrows, uint64_t* ncols, uint6
 int mgk_matrix_download(const mgk_matrix* m, uint64_t* row_ptr, uint64_t* col_idx, int64_t* vals) {
     if (!m) return fail_code(MGK_ECONTRACT, "null matrix");
     if (row_ptr) std::memcpy(row_ptr, m->row_ptr.data(), m->row_ptr.size() * 8);
-    if (col_idx && !m->col_idx.empty()) std::memcpy(col_idx, m->col_idx.data(), m->col_idx.size() * 8);
-    if (vals && !m->vals.empty()) std::memcpy(vals, m->vals.data(), m->vals.size() * 8);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    cudaError_t e = cudaSuccess;
+    if (col_idx && m->nnz) e = cudaMemcpy(col_idx, m->d_col, m->nnz * 8, cudaMemcpyDeviceToHost);
+    if (!e && vals && m->valued && m->nnz) e = cudaMemcpy(vals, m->d_vals, m->nnz * 8, cudaMemcpyDeviceToHost);
+    cudaSetDevice(prev);
+    if (e) return fail_code(MGK_ECUDA, std::string("mxm download: ") + cudaGetErrorString(e));
     return MGK_OK;
 }
 
 int mgk_matrix_free(mgk_matrix* m) {
+    if (!m) return MGK_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
     delete m;
+    cudaSetDevice(prev);
     return MGK_OK;
 }
 
