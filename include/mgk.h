@@ -147,6 +147,13 @@ int mgk_khop_count(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_
 int mgk_khop_count_ex(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
                       int engine, uint64_t* counts, mgk_stats* stats);
 
+/* Several hop counts for one seed list in one call (the harness's sections
+ * over one master seed list, bench.cpp:311-343): counts[j * nseeds + i] is
+ * k_hop_count(seeds[i], ks[j]). All windows are enqueued back to back and
+ * answered with one synchronisation. Checked like mgk_khop_count, per k. */
+int mgk_khop_count_ks(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, const uint32_t* ks, uint32_t nks,
+                      int mode, uint64_t* counts);
+
 /* ---- multi-GPU: seed-sharded replicas, no collective ----------
  * mgk_graph_replicate copies a device graph to `device` (cudaMemcpyPeer over
  * NVLink / NVSwitch when the devices differ; a plain device copy otherwise):

@@ -577,15 +577,18 @@ int mgk_graph_get_tuning(const mgk_graph* h, mgk_tuning* t) {
 namespace mgk {
 namespace {
 // Counts of a batch of seeds over the hop window `span` (host buffers).
-int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, int engine,
-               uint64_t* counts, mgk_stats* stats, const char* what) {
+// Counts of a batch of seeds over several hop windows (host buffers): all
+// windows are enqueued on the workspace's stream and answered with one
+// synchronisation; counts[w * nseeds + i] is window w of seed i.
+int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const Span* spans, uint32_t nspans,
+                     int engine, uint64_t* counts, mgk_stats* stats, const char* what) {
     Graph* g = &h->g;
     int rc = MGK_OK;
     if (nseeds >= 0xFFFFFFFFull) return fail(MGK_ECONTRACT, "too many seeds");
     DeviceGuard dg(g->device);
     Workspace* ws = acquire_ws(g, &rc);
     if (!ws) return rc;
-    cudaError_t e = ensure_staging(ws, nseeds);
+    cudaError_t e = ensure_staging(ws, std::max<uint64_t>(nseeds * nspans, 1));
     if (e) {
         release_ws(g, ws);
         return fail_cuda(e, "staging");
@@ -596,27 +599,33 @@ int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, 
     // SINGLE reads the seeds over the bus (k = 1) or carries each group's
     // seeds in its launch, and writes the counts straight into the mapped
     // buffer: no copy operations on the stream. LANES stages through HBM.
-    const int eng = resolve_engine(engine, nseeds, span.hi);
-    const bool host_io = eng == MGK_ENGINE_SINGLE;
     uint32_t grid = 0, block = 0;
     int used = 0, W = 0;
     float ms = 0.f;
+    bool seeds_on_device = false;
     do {
-        if (!host_io &&
-            (e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream)))
-            break;
-        if (stats && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
-        if ((e = run_engine(g, ws, host_io ? ws->h_seeds_dev : ws->d_seeds, nseeds, span, eng,
-                            host_io ? ws->h_counts_dev : ws->d_counts, ws->stream, &grid, &block, &used, &W,
-                            false, host_io ? hs : nullptr)))
-            break;
-        if (stats && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
-        if (!host_io && (e = cudaMemcpyAsync(ws->h_counts, ws->d_counts, nseeds * 8, cudaMemcpyDeviceToHost,
-                                             ws->stream)))
-            break;
+        for (uint32_t w = 0; w < nspans && !e; ++w) {
+            const int eng = resolve_engine(engine, nseeds, spans[w].hi);
+            const bool host_io = eng == MGK_ENGINE_SINGLE;
+            if (!host_io && !seeds_on_device) {
+                if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
+                seeds_on_device = true;
+            }
+            const bool last = w + 1 == nspans;
+            if (stats && last && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
+            if ((e = run_engine(g, ws, host_io ? ws->h_seeds_dev : ws->d_seeds, nseeds, spans[w], eng,
+                                (host_io ? ws->h_counts_dev : ws->d_counts) + w * nseeds, ws->stream, &grid,
+                                &block, &used, &W, false, host_io ? hs : nullptr)))
+                break;
+            if (stats && last && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
+            if (!host_io && (e = cudaMemcpyAsync(ws->h_counts + w * nseeds, ws->d_counts + w * nseeds,
+                                                 nseeds * 8, cudaMemcpyDeviceToHost, ws->stream)))
+                break;
+        }
+        if (e) break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;
-        std::memcpy(counts, ws->h_counts, nseeds * 8);
-        if (stats) {
+        std::memcpy(counts, ws->h_counts, nseeds * nspans * 8);
+        if (stats) {  // the last window's counters
             cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
             LevelCounters lc[MGK_MAX_HOPS + 2];
             if ((e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost))) break;
@@ -625,6 +634,11 @@ int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, 
     } while (0);
     release_ws(g, ws);
     return e ? fail_cuda(e, what) : MGK_OK;
+}
+
+int count_impl(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, Span span, int engine,
+               uint64_t* counts, mgk_stats* stats, const char* what) {
+    return count_impl_multi(h, seeds, nseeds, &span, 1, engine, counts, stats, what);
 }
 
 // walk_targets' window checks, with the Cypher parser's messages (cypher.cpp:356-392)
@@ -667,6 +681,21 @@ int mgk_walk_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_
 int mgk_khop_count(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, uint32_t k, int mode,
                    uint64_t* counts) {
     return mgk_khop_count_ex(h, seeds, nseeds, k, mode, MGK_ENGINE_AUTO, counts, nullptr);
+}
+
+int mgk_khop_count_ks(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const uint32_t* ks, uint32_t nks,
+                      int mode, uint64_t* counts) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if ((nseeds && !seeds) || (nks && !ks) || (nseeds && nks && !counts)) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    std::vector<Span> spans(nks);
+    for (uint32_t w = 0; w < nks; ++w) {  // execute.cpp:348-354 per query: the seed, then k
+        int rc = check_query(&h->g, seeds, nseeds, ks[w]);
+        if (rc) return rc;
+        spans[w] = span_of(ks[w], mode);
+    }
+    if (nks == 0) return MGK_OK;
+    return count_impl_multi(h, seeds, nseeds, spans.data(), nks, MGK_ENGINE_AUTO, counts, nullptr, "k-hop count");
 }
 
 int mgk_graph_replicate(const mgk_graph* src, int device, mgk_graph** out) {

@@ -333,6 +333,25 @@ def snapshot_check(text: bytes):
     return n.value, m.value
 
 
+def k_hop_count_sections(graph: DeviceGraph, seeds, ks, mode=TraverseMode.Exact):
+    """k_hop_count for every seed at every k in `ks`, one call (the
+    harness's sections over one master seed list, bench.cpp:311-343):
+    returns uint64 counts of shape (len(ks), len(seeds))."""
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    ks = np.ascontiguousarray(ks, np.uint32)
+    if graph.node_count < graph.nrows and len(seeds):  # the C ABI checks against nrows
+        bad = np.flatnonzero(seeds >= graph.node_count)
+        if len(bad):
+            raise ContractError(f"k-hop seed {int(seeds[bad[0]])} is not an allocated node")
+    for k in ks:
+        _check_k(int(k))
+    counts = np.empty((len(ks), len(seeds)), np.uint64)
+    if len(ks) and len(seeds):
+        _check(_lib.lib().mgk_khop_count_ks(graph.handle, seeds.ctypes.data, len(seeds), ks.ctypes.data, len(ks),
+                                            int(mode), counts.ctypes.data))
+    return counts
+
+
 def k_hop_count_multi(replicas, seeds, k: int, mode=TraverseMode.Exact):
     """One batch over replicas of the same graph (e.g. one per GPU, made with
     DeviceGraph.replicate): contiguous seed shards, one host thread per
@@ -377,5 +396,5 @@ def device_count() -> int:
 __all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "mxm",
            "SEMIRING_BOOL_OR_AND", "SEMIRING_PLUS_TIMES", "SEMIRING_MIN_PLUS", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
-           "k_hop_count_device", "k_hop_count_multi", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "k_hop_count_device", "k_hop_count_multi", "k_hop_count_sections", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

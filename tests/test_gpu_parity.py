@@ -401,3 +401,20 @@ def test_concurrent_host_calls_on_one_graph(g1):
         for _ in range(3):
             got = list(ex.map(lambda j: k_hop_count_batch(g, j[0], j[1], j[2]).tolist(), jobs))
             assert got == want
+
+
+def test_sections_in_one_call(port, g1):
+    """mgk_khop_count_ks: several k for one seed list in one call (SINGLE and
+    LANES windows mixed) equals one call per k; errors in the reference order."""
+    from paper_1905_01294_b200 import k_hop_count_sections
+    rp, ci, g = g1
+    seeds = H.pick_seeds(rp, 300, 2)
+    for mode in (0, 1):
+        ks = [1, 2, 3, 6, 2]
+        got = k_hop_count_sections(g, seeds, ks, mode)
+        assert got.shape == (len(ks), len(seeds))
+        for j, k in enumerate(ks):
+            assert got[j].tolist() == k_hop_count_batch(g, seeds, k, mode).tolist(), (mode, k)
+    assert k_hop_count_sections(g, seeds[:1], [2], 0)[0].tolist() == oracle_counts(port, rp, ci, seeds[:1], 2, 0)
+    with pytest.raises(ContractError, match=r"k-hop count 40 outside \[1, 32\]"):
+        k_hop_count_sections(g, seeds, [1, 40], 0)
