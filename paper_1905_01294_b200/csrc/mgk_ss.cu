@@ -906,11 +906,12 @@ cudaError_t ensure_single_ws(const Graph* gr, Workspace* ws) {
     ws->fr_big_cap = (uint32_t)std::min<uint64_t>(want_big, 16ull << 20);
     for (int i = 0; i < 2; ++i)
         if ((e = cudaMalloc(&ws->fr_big[i], (size_t)ws->fr_big_cap * sizeof(uint2)))) return e;
-    // a last hop that can touch more than ~nwords/16 vertices of a seed is not
-    // logged (fire-and-forget red.or); its visited bitmap is popcounted and
-    // cleared with one coalesced pass instead (G2 sweep of the divisor:
-    // 4 -> 0.198 ms, 8 -> 0.183, 16 -> 0.178, 32 -> 0.180 per cfg2 k=2 call)
-    uint32_t qdiv = 16;
+    // a last hop that can touch more than ~nwords/256 vertices of a seed is
+    // not logged (fire-and-forget red.or); its visited bitmap is popcounted
+    // and cleared with one coalesced pass instead. Sweep of the divisor (cfg2
+    // k=2 call on G2 / cfg4 k=2 on G4): 16 -> 0.179 / 1.51 ms, 64 -> 0.173 /
+    // 1.39, 256 -> 0.169 / 1.41, 1024 -> 0.169 / 1.44
+    uint32_t qdiv = 256;
     if (const char* q = std::getenv("MGK_QUOTA_DIV")) qdiv = std::max(1, std::atoi(q));
     ws->fr_quota = std::max<uint32_t>(64, g.nwords / qdiv);
     ws->fr_log_cap = (uint32_t)std::min<uint64_t>((uint64_t)S * (g.n + 64), 64ull << 20);
