@@ -3,6 +3,7 @@
 // per-edge visited test). nvcc -O3 -gencode arch=compute_100a,code=sm_100a
 #include <cstdio>
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t hash32(uint32_t x) {
@@ -59,7 +60,26 @@ void run(const char* name, uint32_t* bits, uint32_t nwords, int blocks, int thre
            ops / ms / 1e6);
 }
 
-int main() {
+int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "--red-sweep") {  // the red.or ceiling over configurations
+        for (size_t mb : {8ul, 16ul, 32ul, 64ul, 90ul}) {
+            const uint32_t nwords = (uint32_t)(mb * 1024 * 1024 / 4);
+            uint32_t *bits, *sink;
+            cudaMalloc(&bits, (size_t)nwords * 4);
+            cudaMalloc(&sink, 4);
+            cudaMemset(bits, 0, (size_t)nwords * 4);
+            printf("== %zu MB array\n", mb);
+            for (int blocks : {296, 592, 1184})
+                for (int threads : {256, 512, 1024}) {
+                    run<4, 1>("red.or", bits, nwords, blocks, threads, sink);
+                    run<8, 1>("red.or", bits, nwords, blocks, threads, sink);
+                    run<16, 1>("red.or", bits, nwords, blocks, threads, sink);
+                }
+            cudaFree(bits);
+            cudaFree(sink);
+        }
+        return 0;
+    }
     for (size_t mb : {1ul, 16ul, 90ul, 512ul}) {
         const uint32_t nwords = (uint32_t)(mb * 1024 * 1024 / 4);
         uint32_t *bits, *sink;
