@@ -788,8 +788,12 @@ __global__ void __launch_bounds__(kFinBlock) fr_finish(FRParams P) {
             for (int i = 0; i < 4; ++i) {
                 const uint32_t w = base + i * 4 * kFinBlock;
                 pc += __popc(v[i].x) + __popc(v[i].y) + __popc(v[i].z) + __popc(v[i].w);
+                // a popcounted row is only written where it holds bits (a row
+                // of a small seed is almost all zero already); rows cleared
+                // without reading them are written whole
+                const bool dirty = !count_me || (v[i].x | v[i].y | v[i].z | v[i].w) != 0;
                 if (w < P.rs) {
-                    __stcs(row + w / 4, make_uint4(0, 0, 0, 0));
+                    if (dirty) __stcs(row + w / 4, make_uint4(0, 0, 0, 0));
                     if (overflow)
                         for (int f = 0; f < 3; ++f)
                             __stcs(reinterpret_cast<uint4*>(P.Fb + ((size_t)f * S + slot) * P.rs + w),
