@@ -87,3 +87,33 @@ def test_generator_raw_mode_counts():
     rp, ci = H.gen_csr(spec)
     assert len(rp) - 1 == 1024
     assert 0 < len(ci) <= 4096
+
+
+def test_mxm_validation_before_device_work(tmp_path):
+    """mgk_mxm checks shapes with the reference's messages (sparse.cpp:294-301)
+    before touching a device, so these run without a GPU."""
+    from conftest import load_golden
+    from paper_1905_01294_b200 import mxm
+    for e in load_golden("mxm_pins")["errors"]:
+        a, b, m = e["a"], e["b"], e["mask"]
+        A = (a[0], a[1], np.zeros(a[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        B = (b[0], b[1], np.zeros(b[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        M = None if m is None else (m[0], m[1], np.zeros(m[0] + 1, np.uint64), np.zeros(0, np.uint64), None)
+        with pytest.raises(ContractError) as ex:
+            mxm(A, B, 0, M)
+        assert str(ex.value) == e["error"]
+    A = (2, 2, np.array([0, 1, 1], np.uint64), np.array([5], np.uint64), None)
+    with pytest.raises(ContractError, match="mxm: A column out of range"):
+        mxm(A, A)
+    with pytest.raises(ContractError, match="unknown semiring 7"):
+        mxm(A, A, 7)
+
+
+def test_snapshot_writer_and_checker_round_trip():
+    """Host-only: the bench-graph writer's text passes the exact grammar and
+    reports its own node / edge counts."""
+    from paper_1905_01294_b200 import snapshot_check
+    rp, ci = H.gen_csr(H.GraphSpec("S10", scale=10, edge_factor=8, relabel=1))
+    text = H.snapshot_text(rp, ci, relation="KNOWS")
+    assert snapshot_check(text) == (len(rp) - 1, len(ci))
+    assert text.startswith(b"GRAPHSNAP1\nNODES ")
