@@ -278,13 +278,34 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
     return acc;
 }
 
+// Warp-level dynamic work split: chunk c = warp_gid first, then chunks
+// nwarps, nwarps + 1, ... handed out by one atomic counter, so warps that
+// finish early take over the tail instead of idling at the next barrier.
+struct ChunkGrab {
+    unsigned long long* ctr;
+    uint32_t nchunks, chunk;
+    uint32_t c;
+    __device__ ChunkGrab(unsigned long long* counter, uint32_t total, uint32_t chunk_len, uint32_t warp_gid)
+        : ctr(counter), nchunks((total + chunk_len - 1) / chunk_len), chunk(chunk_len), c(warp_gid) {}
+    __device__ bool valid() const { return c < nchunks; }
+    __device__ void advance(uint32_t nwarps) {
+        uint32_t n = 0;
+        if (lane_id() == 0) n = (uint32_t)atomicAdd(ctr, 1ull);
+        c = __shfl_sync(kFull, n, 0) + nwarps;
+    }
+};
+
 template <int W>
 __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    for (uint32_t w = warp_gid; w < g.nwords; w += nwarps) {
+    // candidate words in chunks of kWordChunk, spread dynamically (misc[1])
+    constexpr uint32_t kWordChunk = 8;
+    ChunkGrab words(&P.misc[1], g.nwords, kWordChunk, warp_gid);
+    for (; words.valid(); words.advance(nwarps))
+    for (uint32_t w = words.c * kWordChunk; w < min(g.nwords, (words.c + 1) * kWordChunk); ++w) {
         const uint32_t skip = __ldg(g.pull_skip + w);
         if (skip == kFull) continue;
         const uint32_t u = w * 32 + lane;
@@ -367,8 +388,10 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             st.n = 0;
         }
     }
-    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step
-    for (uint32_t t = warp_gid; t < g.nheavy; t += nwarps) {
+    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step (misc[2])
+    ChunkGrab tasks(&P.misc[2], g.nheavy, 1, warp_gid);
+    for (; tasks.valid(); tasks.advance(nwarps)) {
+        const uint32_t t = tasks.c;
         const uint2 task = __ldg(g.heavy + t);
         const uint32_t u = task.x;
         const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
@@ -546,7 +569,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         for (uint32_t i = gtid; i < (P.k + 1) * LB; i += nthreads) P.lane_cnt[i] = 0;
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
-        if (gtid == 0) P.misc[0] = g.m;
+        if (gtid == 0) {
+            P.misc[0] = g.m;
+            P.misc[1] = P.misc[2] = 0;  // pull work counters
+        }
         if (bt == 0)  // the first lc write is after the barrier below
             for (uint32_t i = gtid; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += nthreads)
                 reinterpret_cast<unsigned long long*>(P.lc)[i] = 0;
@@ -618,6 +644,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             const unsigned long long mf = ld_volatile(&qn->edges);
             const unsigned long long mu = ld_volatile(&P.misc[0]);
             const bool was_pull = pull;
+            if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
             if (P.force_dir == 1) {
                 pull = false;
             } else if (P.force_dir == 2) {
