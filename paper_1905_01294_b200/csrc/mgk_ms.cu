@@ -301,11 +301,12 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
-    // candidate words in chunks of kWordChunk, spread dynamically (misc[1])
-    constexpr uint32_t kWordChunk = 8;
-    ChunkGrab words(&P.misc[1], g.nwords, kWordChunk, warp_gid);
+    // candidate words in chunks, spread dynamically (misc[1]); about 8
+    // chunks per warp, at least 8 words each, so the counter stays cold
+    const uint32_t wchunk = max(8u, g.nwords / (nwarps * 8));
+    ChunkGrab words(&P.misc[1], g.nwords, wchunk, warp_gid);
     for (; words.valid(); words.advance(nwarps))
-    for (uint32_t w = words.c * kWordChunk; w < min(g.nwords, (words.c + 1) * kWordChunk); ++w) {
+    for (uint32_t w = words.c * wchunk; w < min(g.nwords, (words.c + 1) * wchunk); ++w) {
         const uint32_t skip = __ldg(g.pull_skip + w);
         if (skip == kFull) continue;
         const uint32_t u = w * 32 + lane;
@@ -388,10 +389,12 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             st.n = 0;
         }
     }
-    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step (misc[2])
-    ChunkGrab tasks(&P.misc[2], g.nheavy, 1, warp_gid);
-    for (; tasks.valid(); tasks.advance(nwarps)) {
-        const uint32_t t = tasks.c;
+    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step,
+    // handed out in chunks of about an eighth of a warp's share (misc[2])
+    const uint32_t tchunk = max(1u, g.nheavy / (nwarps * 8));
+    ChunkGrab tasks(&P.misc[2], g.nheavy, tchunk, warp_gid);
+    for (; tasks.valid(); tasks.advance(nwarps))
+    for (uint32_t t = tasks.c * tchunk; t < min(g.nheavy, (tasks.c + 1) * tchunk); ++t) {
         const uint2 task = __ldg(g.heavy + t);
         const uint32_t u = task.x;
         const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
