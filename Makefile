@@ -8,7 +8,7 @@ CSRC    := $(PKG)/csrc
 BUILD   := build
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -Wall \
            -Iinclude -I$(CSRC) --expt-relaxed-constexpr
-CU      := $(CSRC)/mgk_graph.cu $(CSRC)/mgk_ss.cu $(CSRC)/mgk_ms.cu $(CSRC)/mgk_gen.cu $(CSRC)/mgk_snapshot.cu $(CSRC)/mgk_mxm.cu
+CU      := $(CSRC)/mgk_graph.cu $(CSRC)/mgk_ss.cu $(CSRC)/mgk_k2.cu $(CSRC)/mgk_ms.cu $(CSRC)/mgk_gen.cu $(CSRC)/mgk_snapshot.cu $(CSRC)/mgk_mxm.cu
 CPP     := $(CSRC)/mgk_capi.cpp $(CSRC)/mgk_host.cpp
 OBJS    := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU)) $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.o,$(CPP))
 HDRS    := include/mgk.h $(CSRC)/mgk_internal.cuh $(CSRC)/mgk_device.cuh

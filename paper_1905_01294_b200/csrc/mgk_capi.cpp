@@ -102,6 +102,21 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->fr_dirs);
     cudaFree(ws->fr_ctl);
     cudaFree(ws->fr_snap);
+    cudaFree(ws->k2_w);
+    cudaFree(ws->k2_acc);
+    cudaFree(ws->k2_f1);
+    cudaFree(ws->k2_stage);
+    cudaFree(ws->k2_misc);
+    cudaFree(ws->k2_bounds);
+    cudaFree(ws->k2_first);
+    cudaFree(ws->k2_cuts);
+    cudaFree(ws->k2_f1off);
+    cudaFree(ws->k2_f1v);
+    cudaFree(ws->k2_f1rb);
+    cudaFree(ws->k2_f1d);
+    cudaFree(ws->k2_f1win);
+    cudaFree(ws->k2_wt);
+    cudaFree(ws->k2_tasks);
     cudaFree(ws->lv);
     cudaFree(ws->lf[0]);
     cudaFree(ws->lf[1]);
@@ -329,6 +344,16 @@ cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, voi
     }();
     if (noncoop) return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, 0, stream);
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, 0, stream);
+}
+
+cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block, void** args, size_t smem,
+                                   cudaStream_t stream) {
+    static const bool noncoop = [] {
+        const char* v = std::getenv("MGK_NONCOOP");
+        return v && v[0] == '1';
+    }();
+    if (noncoop) return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, stream);
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, smem, stream);
 }
 
 }  // namespace mgk

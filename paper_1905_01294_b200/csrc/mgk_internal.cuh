@@ -103,6 +103,28 @@ struct Workspace {
     uint8_t* fr_dirs = nullptr;
     void* fr_ctl = nullptr;
     uint32_t* fr_snap = nullptr;  // keep_result: slot 0's visited bitmap after hop min-1
+    // k = 2 on-chip path (mgk_k2.cu)
+    unsigned long long* k2_w = nullptr;    // [cap + 1] per-seed work, scanned
+    unsigned long long* k2_acc = nullptr;  // [cap] popcounts (zero between launches)
+    uint32_t* k2_f1 = nullptr;             // [cap] |F1|
+    uint64_t k2_cap = 0;
+    uint32_t* k2_stage = nullptr;          // slices of seeds cut by a group boundary
+    size_t k2_stage_bytes = 0;
+    unsigned long long* k2_misc = nullptr;
+    unsigned long long* k2_bounds = nullptr;
+    uint32_t* k2_first = nullptr;
+    uint4* k2_cuts = nullptr;
+    uint32_t k2_groups = 0;
+    uint32_t* k2_f1off = nullptr;           // [cap] per seed
+    uint32_t* k2_f1v = nullptr;             // [k2_f1cap] F1 rows of the seeds
+    uint32_t* k2_f1rb = nullptr;
+    uint32_t* k2_f1d = nullptr;
+    uint64_t k2_f1cap = 0;
+    uint32_t* k2_f1win = nullptr;           // [cap] per seed
+    unsigned long long* k2_wt = nullptr;    // window totals
+    uint64_t k2_wtcap = 0;
+    uint2* k2_tasks = nullptr;              // phase-0 tasks
+    uint64_t k2_taskcap = 0;
     // lanes engine (allocated lazily for the widest W used)
     int lanes_words = 0;
     unsigned long long* lv = nullptr;     // V  [n * W]
@@ -183,8 +205,13 @@ struct Launch {
 // launches; the grid still fits on an otherwise idle GPU).
 cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, void** args,
                               cudaStream_t stream);
+cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block, void** args, size_t smem,
+                                   cudaStream_t stream);
 
 cudaError_t launch_single(Launch& L);
+// SINGLE, k = 2 counts with the visited sets in shared memory (mgk_k2.cu)
+bool k2_eligible(const Launch& L);
+cudaError_t launch_k2(Launch& L);
 cudaError_t launch_lanes(Launch& L);
 // Sorted ids of the last single-seed keep_result run: visited \ (visited
 // after hop min-1), i.e. the union of the levels in the window.

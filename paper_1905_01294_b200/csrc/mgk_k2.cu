@@ -1,0 +1,688 @@
+// SINGLE engine, 2-hop counts with the visited set in SHARED memory.
+//
+// For k = 2 on duplicate-free rows (k_hop_count exact / cumulative,
+// proj/core/src/execute.cpp:347-375) the answer of seed s is a set size:
+//   B(s) = {s} u F1 u N(F1),  F1 = row(s) \ {s}
+//   exact |F2| = |B| - 1 - |F1|,  cumulative |F1 u F2| = |B| - 1
+// (the masked vxm of hop 2, sparse.cpp:253-290, unioned with visited). The
+// general engine (mgk_ss.cu) builds B in a per-seed bitmap in L2 with one
+// fire-and-forget red.or per adjacency entry, which runs at the L2 atomic
+// ceiling (~200 G/s on this B200), and then popcounts and clears the bitmaps.
+// Shared-memory atomics on a random word run at ~777 G/s over the chip
+// (scripts/ubench_smem.cu; DSMEM atomics across a cluster only at ~185 G/s),
+// so here B lives on chip: the vertex range is split into R slices of at most
+// ~200 KB of bits, and R CTAs ("a group") hold one slice of one seed's B each.
+//
+// One persistent cooperative launch, four phases separated by grid barriers:
+//   0. warp per seed: |F1| and the hop-2 work w(s) = sum of deg(F1)
+//   1. CTA 0: exclusive scan of w over the seeds (the "work line")
+//   2. group g takes the g-th equal slice of the work line: for every seed
+//      segment in it, the R CTAs of the group stream that part of the F1 rows
+//      (the same adjacency entries; each keeps the targets in its vertex range)
+//      and set bits with shared-memory atomics; a seed wholly inside the
+//      group is popcounted on chip, a seed cut by a group boundary writes its
+//      slice of B to a staging area (coalesced)
+//   3. cut seeds: OR of their staged slices, popcounted by all CTAs
+//   4. answers (and the per-seed accumulators back to zero)
+// Nothing in global memory is touched per adjacency entry except the entry
+// itself; the adjacency is streamed once from HBM (the R CTAs of a group read
+// the same lines close together, the repeats hit L2).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
+#include "mgk_device.cuh"
+
+namespace mgk {
+namespace {
+
+using namespace dev;
+
+constexpr int kK2Block = 1024;
+constexpr int kK2Warps = kK2Block / 32;
+constexpr uint32_t kK2Win = 2048;   // F1 rows per prefix window (2 per thread)
+constexpr uint32_t kK2Task = 256;   // F1 rows per phase-0 task (8 per lane)
+constexpr uint32_t kK2Inline = 512;
+constexpr uint32_t kK2MaxR = 4;
+constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
+constexpr int kK2Ilp = 16;  // adjacency entries in flight per lane
+// smem besides the bitmap: window prefix (u64) + row begins (u32) + scratch
+constexpr uint32_t kK2Fixed = (kK2Win + 1) * 8 + kK2Win * 4 + 1024;
+
+struct K2Params {
+    DevGraph g;
+    const uint32_t* seeds;  // nullptr: inline_seeds
+    uint64_t ns;
+    unsigned long long* counts;
+    uint32_t cumulative;
+    uint32_t R;       // vertex slices per seed (CTAs per group)
+    uint32_t rbits;   // vertices per slice (multiple of 128)
+    uint32_t rwords;  // rbits / 32
+    uint32_t ngroups;
+    unsigned long long* w;    // [ns + 1] hop-2 entries per seed -> the work line (scanned)
+    unsigned long long* acc;  // [ns] popcounts (zero between launches)
+    uint32_t* f1;             // [ns] |F1|
+    uint32_t* stage;          // [ngroups][2][R][rwords]
+    LevelCounters* lc;
+    unsigned int* bar;
+    // [0..2] timestamps, [4] cut seeds, [5..7] allocators of the F1 rows, the
+    // window totals and the phase-0 tasks (zero between launches)
+    unsigned long long* misc;
+    unsigned long long* bounds;  // [ngroups + 1] group slices of the work line
+    uint32_t* first;             // [ngroups] first seed of each group
+    uint4* cuts;                 // [ngroups] {seed, first group, last group, 0} of the cut seeds
+    // the seeds' F1 rows (phase 0): vertex, CSR row begin, length (0 for the
+    // seed itself); per seed its first row (kNoF1: scratch ran out) and its
+    // first 2048-row window total
+    uint32_t* f1off;  // [ns]
+    uint32_t* f1win;  // [ns]
+    uint32_t* f1v;
+    uint32_t* f1rb;
+    uint32_t* f1d;
+    uint64_t f1cap;
+    unsigned long long* wt;  // window totals
+    uint64_t wtcap;
+    uint2* tasks;            // {seed, 256-row block}
+    uint64_t taskcap;
+    unsigned long long seedcost;  // work-line units charged per seed (its fixed cost)
+    uint32_t inline_seeds[kK2Inline];
+};
+
+__device__ __forceinline__ uint32_t k2_seed(const K2Params& P, uint64_t i) {
+    return dev_id(P.g, P.seeds ? P.seeds[i] : P.inline_seeds[i]);
+}
+
+// first offset of group g on the work line [0, W): floor(W * g / G) without
+// a 128-bit product (W = q G + r)
+__device__ __forceinline__ unsigned long long group_lo(unsigned long long W, uint32_t g, uint32_t G) {
+    return (W / G) * g + (W % G) * g / G;
+}
+
+// block-wide exclusive scan of one u64 per thread; returns the block total
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* out,
+                                                              unsigned long long* s_warp) {
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+    unsigned long long x = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long t = __shfl_up_sync(kFull, x, d);
+        if (lane >= (uint32_t)d) x += t;
+    }
+    if (lane == 31) s_warp[wib] = x;
+    __syncthreads();
+    if (wib == 0) {
+        unsigned long long y = s_warp[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned long long t = __shfl_up_sync(kFull, y, d);
+            if (lane >= (uint32_t)d) y += t;
+        }
+        s_warp[lane] = y;  // inclusive warp totals
+    }
+    __syncthreads();
+    const unsigned long long before = wib ? s_warp[wib - 1] : 0;
+    *out = before + x - v;
+    const unsigned long long total = s_warp[kK2Warps - 1];
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t bit) {
+    asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + word * 4), "r"(bit));
+}
+
+__global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
+    extern __shared__ __align__(16) unsigned char k2_smem[];
+    uint32_t* bm = reinterpret_cast<uint32_t*>(k2_smem);
+    unsigned long long* pre = reinterpret_cast<unsigned long long*>(k2_smem + (size_t)P.rwords * 4);
+    uint32_t* rbeg = reinterpret_cast<uint32_t*>(pre + kK2Win + 1);
+    unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(rbeg + kK2Win);  // [32]
+    unsigned long long* s_misc = s_warp + 32;                                         // [8]
+    const DevGraph& g = P.g;
+    const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+    const uint32_t nthreads = gridDim.x * kK2Block;
+    const uint32_t gtid = blockIdx.x * kK2Block + threadIdx.x;
+    const uint64_t nwarps = (uint64_t)gridDim.x * kK2Warps;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * kK2Warps + wib;
+    const uint32_t bm_base = (uint32_t)__cvta_generic_to_shared(bm);
+    const unsigned long long t0 = globaltimer();
+
+    // ---- phase 0a: per seed, reserve its F1 rows, window totals and tasks -----------
+    for (uint32_t i = threadIdx.x; i < P.rwords; i += kK2Block) bm[i] = 0;
+    if (blockIdx.x == 0)
+        for (uint32_t i = threadIdx.x; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += kK2Block)
+            reinterpret_cast<unsigned long long*>(P.lc)[i] = 0;
+    for (uint64_t i = gwarp; i < P.ns; i += nwarps) {
+        const uint32_t s = k2_seed(P, i);
+        const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
+        const uint32_t nwin = (deg + kK2Win - 1) / kK2Win, nt = (deg + kK2Task - 1) / kK2Task;
+        unsigned long long off = 0, ow = 0, ot = 0;
+        if (lane == 0) {
+            off = atomicAdd(&P.misc[5], (unsigned long long)deg);
+            ow = atomicAdd(&P.misc[6], (unsigned long long)nwin);
+            ot = atomicAdd(&P.misc[7], (unsigned long long)nt);
+        }
+        off = __shfl_sync(kFull, off, 0);
+        ow = __shfl_sync(kFull, ow, 0);
+        ot = __shfl_sync(kFull, ot, 0);
+        const bool ok = off + deg <= P.f1cap && ow + nwin <= P.wtcap && ot + nt <= P.taskcap;
+        for (uint32_t q = lane; q < nt; q += 32)
+            if (ot + q < P.taskcap) P.tasks[ot + q] = make_uint2(ok ? (uint32_t)i : kNoF1, q);
+        if (ok) {
+            for (uint32_t q = lane; q < nwin; q += 32) P.wt[ow + q] = 0;
+            if (lane == 0) {
+                P.f1off[i] = (uint32_t)off;
+                P.f1win[i] = (uint32_t)ow;
+                P.w[i] = 0;
+                P.f1[i] = 0;
+            }
+        } else {  // scratch exhausted (huge batches of hubs): this warp sums the rows itself
+            unsigned long long wsum = 0;
+            uint32_t nf = 0;
+            for (uint32_t j = b + lane; j < b + deg; j += 32) {
+                const uint32_t v = __ldg(g.ci + j);
+                if (v != s) {
+                    wsum += __ldg(g.rp + v + 1) - __ldg(g.rp + v);
+                    ++nf;
+                }
+            }
+            wsum = warp_sum_u64(wsum);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) nf += __shfl_xor_sync(kFull, nf, d);
+            if (lane == 0) {
+                P.f1off[i] = kNoF1;
+                P.w[i] = wsum;
+                P.f1[i] = nf;
+            }
+        }
+    }
+    grid_barrier(P.bar);
+
+    // ---- phase 0b: tasks of 256 F1 rows: vertex, row begin, row length --------------
+    {
+        const uint64_t ntask = min(ld_cg(&P.misc[7]), (unsigned long long)P.taskcap);
+        for (uint64_t t = gwarp; t < ntask; t += nwarps) {
+            const uint2 tk = __ldcg(P.tasks + t);
+            if (tk.x == kNoF1) continue;
+            const uint32_t s = k2_seed(P, tk.x);
+            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
+            const uint32_t off = ld_cg(P.f1off + tk.x);
+            const uint32_t j0 = tk.y * kK2Task;
+            uint32_t v[kK2Task / 32], rb[kK2Task / 32], re[kK2Task / 32];
+#pragma unroll
+            for (int r = 0; r < (int)(kK2Task / 32); ++r) {
+                const uint32_t j = j0 + lane + 32 * r;
+                v[r] = j < deg ? __ldg(g.ci + b + j) : s;
+            }
+#pragma unroll
+            for (int r = 0; r < (int)(kK2Task / 32); ++r) {
+                rb[r] = __ldg(g.rp + v[r]);
+                re[r] = __ldg(g.rp + v[r] + 1);
+            }
+            unsigned long long sum = 0;
+            uint32_t nf = 0;
+#pragma unroll
+            for (int r = 0; r < (int)(kK2Task / 32); ++r) {
+                const uint32_t j = j0 + lane + 32 * r;
+                const uint32_t d = v[r] != s ? re[r] - rb[r] : 0;
+                if (j < deg) {
+                    P.f1v[off + j] = v[r];
+                    P.f1rb[off + j] = rb[r];
+                    P.f1d[off + j] = d;
+                    sum += d;
+                    nf += v[r] != s;
+                }
+            }
+            sum = warp_sum_u64(sum);
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) nf += __shfl_xor_sync(kFull, nf, d);
+            if (lane == 0) {
+                if (sum) {
+                    atomicAdd(&P.w[tk.x], sum);
+                    atomicAdd(&P.wt[ld_cg(P.f1win + tk.x) + j0 / kK2Win], sum);
+                }
+                if (nf) atomicAdd(&P.f1[tk.x], nf);
+            }
+        }
+    }
+    grid_barrier(P.bar);
+
+    // ---- phase 1 (CTA 0): the work line (w + seedcost per seed with work), the
+    // group slices, each group's first seed, and the seeds cut by a group
+    // boundary. Thread t owns a chunk of seeds and finds the boundaries inside
+    // them arithmetically (no searches through global memory)
+    if (blockIdx.x == 0) {
+        const uint32_t G = P.ngroups;
+        const uint64_t per = (P.ns + kK2Block - 1) / kK2Block;
+        const uint64_t i0 = min((uint64_t)threadIdx.x * per, P.ns), i1 = min(i0 + per, P.ns);
+        unsigned long long part = 0;
+        for (uint64_t i = i0; i < i1; ++i) {
+            const unsigned long long v = ld_cg(P.w + i);
+            part += v ? v + P.seedcost : 0;
+        }
+        unsigned long long base;
+        const unsigned long long total = block_excl_scan(part, &base, s_warp);
+        unsigned int* s_ncut = reinterpret_cast<unsigned int*>(s_misc);
+        if (threadIdx.x == 0) *s_ncut = 0;
+        __syncthreads();
+        // smallest b in [0, G] with group_lo(b) > x (>= x when ge); group_lo(G) = total
+        auto first_group = [&](unsigned long long x, bool ge) {
+            uint32_t lo = 0, hi = G;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) / 2;
+                const unsigned long long gm = group_lo(total, mid, G);
+                if (ge ? gm >= x : gm > x) hi = mid; else lo = mid + 1;
+            }
+            return lo;
+        };
+        for (uint64_t i = i0; i < i1; ++i) {
+            const unsigned long long v0 = ld_cg(P.w + i);
+            const unsigned long long v = v0 ? v0 + P.seedcost : 0, ws = base, we = base + v;
+            P.w[i] = ws;
+            base = we;
+            if (v == 0) continue;
+            const uint32_t b0 = first_group(ws, true), bA = first_group(ws, false), bB = first_group(we, true);
+            for (uint32_t bb = b0; bb < bB && bb < G; ++bb) P.first[bb] = (uint32_t)i;
+            if (bA < bB) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bA - 1, bB - 1, 0);
+        }
+        for (uint32_t t = threadIdx.x; t <= G; t += kK2Block) P.bounds[t] = group_lo(total, t, G);
+        if (threadIdx.x == 0) P.w[P.ns] = total;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            P.misc[4] = *s_ncut;
+            P.misc[0] = globaltimer();
+        }
+    }
+    grid_barrier(P.bar);
+
+    // ---- phase 2: group slices of the work line -----------------------------------
+    const unsigned long long W = ld_cg(P.w + P.ns);
+    const uint32_t G = P.ngroups, R = P.R;
+    const uint32_t grp = blockIdx.x / R, rr = blockIdx.x % R;
+    const uint32_t rlo = rr * P.rbits;
+    const unsigned long long glo = W ? ld_cg(P.bounds + grp) : 0, ghi = W ? ld_cg(P.bounds + grp + 1) : 0;
+    if (glo < ghi) {
+        for (uint64_t i = ld_cg(P.first + grp); i < P.ns; ++i) {
+            const unsigned long long ws = ld_cg(P.w + i), we = ld_cg(P.w + i + 1);
+            if (ws >= ghi) break;
+            if (we == ws) continue;
+            // this group's part of the seed: on the work line, then in adjacency
+            // entries (the first seedcost units of a seed carry no entries)
+            const unsigned long long a2 = max(glo, ws) - ws, z2 = min(ghi, we) - ws;
+            const unsigned long long a = a2 > P.seedcost ? a2 - P.seedcost : 0;
+            const unsigned long long z = z2 > P.seedcost ? z2 - P.seedcost : 0;
+            const uint32_t s = k2_seed(P, i);
+            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
+            const uint32_t off = ld_cg(P.f1off + i);
+            const uint32_t ow = off != kNoF1 ? ld_cg(P.f1win + i) : 0;
+            const bool v1 = a2 == 0;  // the part holding offset 0 also holds {s} u F1
+            if (v1 && threadIdx.x == 0 && s - rlo < P.rbits) smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
+            unsigned long long wbase = 0;  // seed-local entry offset of the current window
+            uint32_t j0 = 0;
+            for (uint32_t k = 0; j0 < deg && wbase < z; j0 += kK2Win, ++k) {
+                const uint32_t wl = min(kK2Win, deg - j0);
+                if (off != kNoF1 && !v1) {
+                    const unsigned long long wk = ld_cg(P.wt + ow + k);
+                    if (wbase + wk <= a) {  // the whole window lies before this part
+                        wbase += wk;
+                        continue;
+                    }
+                }
+                unsigned long long d2[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t t = threadIdx.x * 2 + h;
+                    d2[h] = 0;
+                    if (t < wl) {
+                        uint32_t v;
+                        if (off != kNoF1) {
+                            v = v1 ? ld_cg(P.f1v + off + j0 + t) : 0;
+                            rbeg[t] = ld_cg(P.f1rb + off + j0 + t);
+                            d2[h] = ld_cg(P.f1d + off + j0 + t);
+                        } else {
+                            v = __ldg(g.ci + b + j0 + t);
+                            const uint32_t rb = __ldg(g.rp + v);
+                            rbeg[t] = rb;
+                            if (v != s) d2[h] = __ldg(g.rp + v + 1) - rb;
+                        }
+                        if (v1 && v - rlo < P.rbits) smem_or(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
+                    }
+                }
+                unsigned long long ex;
+                const unsigned long long wtot = block_excl_scan(d2[0] + d2[1], &ex, s_warp);
+                pre[threadIdx.x * 2] = wbase + ex;
+                pre[threadIdx.x * 2 + 1] = wbase + ex + d2[0];
+                if (threadIdx.x == 0) pre[wl] = wbase + wtot;
+                __syncthreads();
+                const unsigned long long x0 = max(a, wbase), x1 = min(z, wbase + wtot);
+                if (x0 < x1) {
+                    // warp q takes [xs, xe) of the window's part as one flat
+                    // stream: lane l reads entries xb + l + 32 j (coalesced within
+                    // a row), each lane walking its own row cursor; the next
+                    // block's loads are issued before this block's atomics
+                    const unsigned long long span = x1 - x0;
+                    const unsigned long long xs = x0 + span * wib / kK2Warps;
+                    const unsigned long long xe = x0 + span * (wib + 1) / kK2Warps;
+                    if (xs < xe) {
+                        uint32_t lo = 0, hi = wl;  // last row t with pre[t] <= xs
+                        while (hi - lo > 1) {
+                            const uint32_t mid = (lo + hi) / 2;
+                            if (pre[mid] <= xs) lo = mid; else hi = mid;
+                        }
+                        uint32_t tl = lo, rb = rbeg[lo];
+                        unsigned long long cur = pre[lo], nxt = pre[lo + 1];
+                        // addresses first (row cursor), then all loads back to
+                        // back (unconditional: a lane past the end re-reads its
+                        // last valid entry), then the atomics: no load waits on
+                        // a branch, so kK2Ilp loads per lane are in flight
+                        uint32_t last = rb + (uint32_t)(xs - cur);
+                        for (unsigned long long xb = xs; xb < xe; xb += 32 * kK2Ilp) {
+                            uint32_t idx[kK2Ilp];
+                            uint32_t valid = 0;
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) {
+                                const unsigned long long x = xb + lane + 32 * q;
+                                if (x < xe) {
+                                    while (nxt <= x) {
+                                        ++tl;
+                                        cur = nxt;
+                                        nxt = pre[tl + 1];
+                                        rb = rbeg[tl];
+                                    }
+                                    last = rb + (uint32_t)(x - cur);
+                                    valid |= 1u << q;
+                                }
+                                idx[q] = last;
+                            }
+                            uint32_t u[kK2Ilp];
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) u[q] = __ldg(g.ci + idx[q]);
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) {
+                                const uint32_t t = u[q] - rlo;
+                                if (((valid >> q) & 1u) && t < P.rbits) smem_or(bm_base, t >> 5, 1u << (t & 31));
+                            }
+                        }
+                    }
+                }
+                wbase += wtot;
+                __syncthreads();  // pre / rbeg are rewritten by the next window
+            }
+            if (v1)  // F1 rows in windows the loop did not reach
+                for (uint32_t j = j0 + threadIdx.x; j < deg; j += kK2Block) {
+                    const uint32_t v = (off != kNoF1 ? ld_cg(P.f1v + off + j) : __ldg(g.ci + b + j)) - rlo;
+                    if (v < P.rbits) smem_or(bm_base, v >> 5, 1u << (v & 31));
+                }
+            __syncthreads();
+            // the slice is complete: popcount it (whole seed) or stage it (cut seed)
+            const bool whole = ws >= glo && we <= ghi;
+            uint4* bm4 = reinterpret_cast<uint4*>(bm);
+            const uint32_t n4 = P.rwords / 4;
+            if (whole) {
+                uint32_t pc = 0;
+                for (uint32_t q = threadIdx.x; q < n4; q += kK2Block) {
+                    const uint4 x = bm4[q];
+                    if (x.x | x.y | x.z | x.w) {
+                        pc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+                        bm4[q] = make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
+                if (lane == 0 && pc) atomicAdd(&P.acc[i], (unsigned long long)pc);
+            } else {
+                const uint32_t slot = ws < glo ? 0 : 1;
+                uint4* dst = reinterpret_cast<uint4*>(P.stage + ((size_t)(grp * 2 + slot) * R + rr) * P.rwords);
+                for (uint32_t q = threadIdx.x; q < n4; q += kK2Block) {
+                    const uint4 x = bm4[q];
+                    __stcg(dst + q, x);
+                    if (x.x | x.y | x.z | x.w) bm4[q] = make_uint4(0, 0, 0, 0);
+                }
+            }
+            __syncthreads();
+        }
+    }
+    grid_barrier(P.bar);
+    if (gtid == 0) P.misc[1] = globaltimer();
+
+    // ---- phase 3: cut seeds = OR of their staged slices ----------------------------
+    // tasks: (cut seed, slice, 4096-word block)
+    {
+        constexpr uint32_t kBlk = 4 * kK2Block;
+        const uint32_t nblk = (P.rwords + kBlk - 1) / kBlk;
+        const uint32_t ntask = (uint32_t)ld_cg(P.misc + 4) * R * nblk;
+        for (uint32_t t = blockIdx.x; t < ntask; t += gridDim.x) {
+            const uint4 c = __ldcg(P.cuts + t / (R * nblk));
+            const uint32_t r = (t / nblk) % R, blk = t % nblk;
+            const uint64_t i = c.x;
+            uint32_t pc = 0;
+            const uint32_t q = blk * kBlk / 4 + threadIdx.x;
+            if (q < P.rwords / 4) {
+                // the seed starts inside group c.y (its slot 1) and runs through
+                // the first slot of the groups after it; with W >= G no group
+                // is empty, otherwise empty groups (no slice written) are skipped
+                uint4 o = make_uint4(0, 0, 0, 0);
+                const bool sparse = W < G;
+                for (uint32_t g0 = c.y; g0 <= c.z; g0 += 4) {
+                    uint4 y[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t gg = g0 + k;
+                        y[k] = make_uint4(0, 0, 0, 0);
+                        if (gg <= c.z && (!sparse || ld_cg(P.bounds + gg) != ld_cg(P.bounds + gg + 1)))
+                            y[k] = __ldcg(reinterpret_cast<const uint4*>(
+                                              P.stage + ((size_t)(gg * 2 + (gg == c.y ? 1 : 0)) * R + r) * P.rwords) + q);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        o.x |= y[k].x; o.y |= y[k].y; o.z |= y[k].z; o.w |= y[k].w;
+                    }
+                }
+                pc = __popc(o.x) + __popc(o.y) + __popc(o.z) + __popc(o.w);
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
+            if (lane == 0 && pc) atomicAdd(&P.acc[i], (unsigned long long)pc);
+        }
+    }
+    grid_barrier(P.bar);
+    if (gtid == 0) P.misc[2] = globaltimer();
+
+    // ---- phase 4: answers and the per-hop counters ---------------------------------
+    unsigned long long f1s = 0, f2s = 0, d1 = 0, e2 = 0, runs = 0;
+    for (uint64_t i = gtid; i < P.ns; i += nthreads) {
+        const unsigned long long nf = ld_cg(P.f1 + i);
+        const unsigned long long len = ld_cg(P.w + i + 1) - ld_cg(P.w + i);
+        const unsigned long long pop = len ? ld_cg(P.acc + i) : 1 + nf;  // |B|
+        const unsigned long long ex = pop - 1 - nf;
+        P.counts[i] = P.cumulative ? pop - 1 : ex;
+        if (len) P.acc[i] = 0;
+        const uint32_t s = k2_seed(P, i);
+        f1s += nf;
+        f2s += ex;
+        d1 += __ldg(g.rp + s + 1) - __ldg(g.rp + s);
+        e2 += len ? len - P.seedcost : 0;
+        runs += nf != 0;
+    }
+    f1s = warp_sum_u64(f1s);
+    f2s = warp_sum_u64(f2s);
+    d1 = warp_sum_u64(d1);
+    e2 = warp_sum_u64(e2);
+    runs = warp_sum_u64(runs);
+    if (lane == 0 && (f1s | d1 | runs)) {
+        atomicAdd(&P.lc[1].frontier, f1s);
+        atomicAdd(&P.lc[1].vertices, f1s);
+        atomicAdd(&P.lc[1].scanned, d1);
+        atomicAdd(&P.lc[1].edges, d1);
+        atomicAdd(&P.lc[1].union_edges, d1);
+        atomicAdd(&P.lc[2].frontier, f2s);
+        atomicAdd(&P.lc[2].vertices, f2s);
+        atomicAdd(&P.lc[2].scanned, e2);
+        atomicAdd(&P.lc[2].edges, e2);
+        atomicAdd(&P.lc[2].union_edges, e2);
+        atomicAdd(&P.lc[2].runs, (unsigned)runs);
+    }
+    if (gtid == 0) {
+        P.lc[1].runs = (unsigned)P.ns;
+        P.misc[5] = P.misc[6] = P.misc[7] = 0;  // allocators (every CTA is past phase 2)
+        const unsigned long long now = globaltimer();
+        P.lc[0].ns = ld_cg(&P.misc[0]) - t0;                  // phases 0-1
+        P.lc[2].ns = ld_cg(&P.misc[2]) - ld_cg(&P.misc[0]);  // slices + merge
+        P.lc[MGK_MAX_HOPS + 1].ns = now - ld_cg(&P.misc[2]);
+        P.lc[0].candidates = ld_cg(&P.misc[1]) - ld_cg(&P.misc[0]);  // DIAG: slices alone (ns)
+    }
+}
+
+}  // namespace
+
+// Eligible: k = 2 counts with the seed pre-visited (k_hop exact/cumulative),
+// duplicate-free rows, no forced direction, and a bitmap that fits R <= 4
+// slices of shared memory. MGK_NO_K2SMEM=1 keeps every call on fr_kernel.
+bool k2_eligible(const Launch& L) {
+    static const bool off = std::getenv("MGK_NO_K2SMEM") != nullptr;
+    if (off || L.k != 2 || !L.seed_visited || L.keep_result || !L.g->dg.rows_unique) return false;
+    if (L.tuning.force_dir != 0 || L.nseeds == 0) return false;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const uint64_t maxw = ((uint64_t)optin - kK2Fixed) / 4 / 4 * 4;
+    const uint64_t nw = L.g->dg.nwords;
+    return (nw + maxw - 1) / maxw <= kK2MaxR;
+}
+
+cudaError_t launch_k2(Launch& L) {
+    const Graph* gr = L.g;
+    Workspace* ws = L.ws;
+    cudaError_t e;
+    int dev = 0, optin = 0, nsm = 0;
+    if ((e = cudaGetDevice(&dev))) return e;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t maxw = (uint32_t)(((uint64_t)optin - kK2Fixed) / 4 / 4 * 4);
+    const uint32_t nw = gr->dg.nwords;
+    const uint32_t R = (nw + maxw - 1) / maxw;
+    // slices of equal size, 128 vertices (4 x uint4 words) aligned
+    const uint32_t rbits = (uint32_t)((((uint64_t)gr->dg.n + R - 1) / R + 127) / 128 * 128);
+    const uint32_t rwords = rbits / 32;
+    const size_t smem = (size_t)rwords * 4 + kK2Fixed;
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        if ((e = cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
+            return e;
+        smem_set = smem;
+    }
+    int per_sm = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_kernel, kK2Block, smem))) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const uint32_t grid = (uint32_t)(per_sm * nsm) / R * R;
+    const uint32_t G = grid / R;
+    // workspace: per-seed arrays (grow with the batch) and the staging area
+    const uint64_t ns = L.nseeds;
+    if (ws->k2_cap < ns) {
+        for (void* p : {(void*)ws->k2_w, (void*)ws->k2_acc, (void*)ws->k2_f1, (void*)ws->k2_f1off,
+                        (void*)ws->k2_f1win, (void*)ws->k2_wt, (void*)ws->k2_tasks})
+            cudaFree(p);
+        ws->k2_w = ws->k2_acc = ws->k2_wt = nullptr;
+        ws->k2_f1 = ws->k2_f1off = ws->k2_f1win = nullptr;
+        ws->k2_tasks = nullptr;
+        ws->k2_cap = 0;
+        const uint64_t cap = std::max<uint64_t>(ns, 1024);
+        // window totals and tasks: at most one partial window / task per seed
+        // beyond the F1 rows' own count
+        const uint64_t rows = std::min<uint64_t>(gr->dg.m + 1024, 8ull << 20);
+        ws->k2_wtcap = cap + rows / kK2Win + 1;
+        ws->k2_taskcap = cap + rows / kK2Task + 1;
+        if ((e = cudaMalloc(&ws->k2_w, (cap + 1) * 8))) return e;
+        if ((e = cudaMalloc(&ws->k2_acc, cap * 8))) return e;
+        if ((e = cudaMalloc(&ws->k2_f1, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_f1off, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_f1win, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_wt, ws->k2_wtcap * 8))) return e;
+        if ((e = cudaMalloc(&ws->k2_tasks, ws->k2_taskcap * 8))) return e;
+        if ((e = cudaMemset(ws->k2_acc, 0, cap * 8))) return e;
+        if ((e = cudaStreamSynchronize(0))) return e;  // zero state before the first launch
+        ws->k2_cap = cap;
+        ws->bytes += cap * 28 + 8 + ws->k2_wtcap * 8 + ws->k2_taskcap * 8;
+    }
+    const size_t stage = (size_t)G * 2 * R * rwords * 4;
+    if (ws->k2_stage_bytes < stage) {
+        cudaFree(ws->k2_stage);
+        ws->k2_stage = nullptr;
+        ws->k2_stage_bytes = 0;
+        if ((e = cudaMalloc(&ws->k2_stage, stage))) return e;
+        ws->k2_stage_bytes = stage;
+        ws->bytes += stage;
+    }
+    if (!ws->k2_f1v) {  // F1 rows of a call's seeds: up to min(m + 1024, 8M) entries
+        uint64_t cap = std::min<uint64_t>(gr->dg.m + 1024, 8ull << 20);
+        if (const char* c = std::getenv("MGK_K2_F1CAP")) cap = std::max<uint64_t>(1, std::strtoull(c, nullptr, 10));
+        if ((e = cudaMalloc(&ws->k2_f1v, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_f1rb, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_f1d, cap * 4))) return e;
+        ws->k2_f1cap = cap;
+        ws->bytes += cap * 12;
+    }
+    if (ws->k2_groups < G) {
+        cudaFree(ws->k2_bounds);
+        cudaFree(ws->k2_first);
+        cudaFree(ws->k2_cuts);
+        ws->k2_groups = 0;
+        if ((e = cudaMalloc(&ws->k2_bounds, (size_t)(G + 1) * 8))) return e;
+        if ((e = cudaMalloc(&ws->k2_first, (size_t)G * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_cuts, (size_t)G * 16))) return e;
+        ws->k2_groups = G;
+    }
+    if (!ws->k2_misc) {
+        if ((e = cudaMalloc(&ws->k2_misc, 64))) return e;
+        if ((e = cudaMemset(ws->k2_misc, 0, 64))) return e;
+        if ((e = cudaStreamSynchronize(0))) return e;
+    }
+    K2Params Q;  // ~2 KB with the inline seeds; the launch copies it
+    Q.g = gr->dg;
+    Q.ns = ns;
+    Q.counts = L.d_counts;
+    Q.cumulative = L.min_hop <= 1 ? 1u : 0u;
+    Q.R = R;
+    Q.rbits = rbits;
+    Q.rwords = rwords;
+    Q.ngroups = G;
+    Q.w = ws->k2_w;
+    Q.acc = ws->k2_acc;
+    Q.f1 = ws->k2_f1;
+    Q.stage = ws->k2_stage;
+    Q.lc = ws->lc;
+    Q.bar = reinterpret_cast<unsigned int*>(ws->misc + 8);
+    Q.misc = ws->k2_misc;
+    Q.bounds = ws->k2_bounds;
+    Q.first = ws->k2_first;
+    Q.cuts = ws->k2_cuts;
+    Q.f1off = ws->k2_f1off;
+    Q.f1win = ws->k2_f1win;
+    Q.f1v = ws->k2_f1v;
+    Q.f1rb = ws->k2_f1rb;
+    Q.f1d = ws->k2_f1d;
+    Q.f1cap = ws->k2_f1cap;
+    Q.wt = ws->k2_wt;
+    Q.wtcap = ws->k2_wtcap;
+    Q.tasks = ws->k2_tasks;
+    Q.taskcap = ws->k2_taskcap;
+    static const unsigned long long seedcost = [] {
+        const char* c = std::getenv("MGK_K2_SEEDCOST");
+        return c ? std::strtoull(c, nullptr, 10) : 16384ull;
+    }();
+    Q.seedcost = seedcost;
+    if (L.host_io && ns <= kK2Inline) {
+        Q.seeds = nullptr;
+        std::memcpy(Q.inline_seeds, L.h_seeds, (size_t)ns * 4);
+    } else {
+        Q.seeds = L.d_seeds;
+    }
+    void* args[] = {&Q};
+    if ((e = launch_persistent_smem((const void*)k2_kernel, grid, kK2Block, args, smem, L.stream))) return e;
+    L.grid = grid;
+    L.block = kK2Block;
+    L.launches = 1;
+    return cudaSuccess;
+}
+
+}  // namespace mgk

@@ -1027,6 +1027,7 @@ bool fuse_disabled() {
 cudaError_t launch_single(Launch& L) {
     const Graph* gr = L.g;
     Workspace* ws = L.ws;
+    if (k2_eligible(L)) return launch_k2(L);
     if (gr->dg.rows_unique && L.k == 1 && L.seed_visited && !L.keep_result && !fuse_disabled()) {
         const uint64_t want = (L.nseeds + kK1Block / 32 - 1) / (kK1Block / 32);  // a warp per seed
         const uint32_t grid = (uint32_t)std::min<uint64_t>(want, 148ull * 4);

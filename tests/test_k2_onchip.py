@@ -1,0 +1,49 @@
+"""The k = 2 on-chip path (mgk_k2.cu: per-seed visited sets in shared memory)
+against the oracle, including the cases it handles specially: seeds cut over
+several CTA groups (hubs), a work line shorter than the group count, the F1
+scratch running out, isolated seeds and self loops."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1905_01294_b200 import ENGINE_SINGLE, DeviceGraph, Tuning, harness as H, k_hop_count_batch
+
+pytestmark = pytest.mark.gpu
+WORKER = Path(__file__).resolve().parent / "helpers" / "k2_worker.py"
+
+
+@pytest.mark.parametrize("env", [
+    {},                                                # defaults
+    {"MGK_K2_SEEDCOST": "0"},                          # pure entry split: many cut seeds
+    {"MGK_K2_SEEDCOST": "0", "MGK_K2_F1CAP": "64"},    # F1 scratch runs out: in-kernel prefixes
+    {"MGK_K2_SEEDCOST": "100000000"},                  # one seed per group at most
+    {"MGK_NO_K2SMEM": "1"},                            # the L2-bitmap engine (fr_kernel)
+], ids=["default", "cost0", "f1cap", "cost_huge", "no_onchip"])
+def test_k2_paths_against_oracle(env):
+    p = subprocess.run([sys.executable, str(WORKER)], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=900)
+    assert p.returncode == 0, p.stdout + p.stderr
+
+
+def test_k2_stats_and_agreement(port):
+    rp, ci = H.gen_csr(H.G1)
+    g = DeviceGraph.from_csr(rp, ci)
+    seeds = H.pick_seeds(rp, 2000, 3)  # several seeds per group
+    counts, st = k_hop_count_batch(g, seeds, 2, 0, stats=True)
+    assert st["launches"] == 1 and st["block"] == 1024
+    assert st["levels"][2]["frontier"] == int(counts.sum())
+    rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
+    e = sum(port.khop_work(rp64, ci64, int(s), 2)[0] for s in seeds)
+    assert st["levels"][1]["edges"] + st["levels"][2]["edges"] == e
+    # forced directions run the general engine: same answers
+    for d in (1, 2):
+        g.set_tuning(Tuning(force_dir=d))
+        assert k_hop_count_batch(g, seeds, 2, 0, engine=ENGINE_SINGLE).tolist() == counts.tolist()
+    g.set_tuning(Tuning())
+    cum = k_hop_count_batch(g, seeds, 2, 1)
+    one = k_hop_count_batch(g, seeds, 1, 0)
+    assert (cum == counts + one).all()
