@@ -110,7 +110,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->k2_bounds);
     cudaFree(ws->k2_first);
     cudaFree(ws->k2_cuts);
-    cudaFree(ws->k2_f1off);
+    cudaFree(ws->k2_sinfo);
     cudaFree(ws->k2_f1v);
     cudaFree(ws->k2_f1rb);
     cudaFree(ws->k2_f1d);

@@ -115,7 +115,7 @@ struct Workspace {
     uint32_t* k2_first = nullptr;
     uint4* k2_cuts = nullptr;
     uint32_t k2_groups = 0;
-    uint32_t* k2_f1off = nullptr;           // [cap] per seed
+    uint4* k2_sinfo = nullptr;              // [cap] per seed
     uint32_t* k2_f1v = nullptr;             // [k2_f1cap] F1 rows of the seeds
     uint32_t* k2_f1rb = nullptr;
     uint32_t* k2_f1d = nullptr;

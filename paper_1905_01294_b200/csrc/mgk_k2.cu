@@ -47,7 +47,7 @@ constexpr uint32_t kK2MaxR = 4;
 constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
 constexpr int kK2Ilp = 16;  // adjacency entries in flight per lane
 // smem besides the bitmap: window prefix (u64) + row begins (u32) + scratch
-constexpr uint32_t kK2Fixed = (kK2Win + 1) * 8 + kK2Win * 4 + 1024;
+constexpr uint32_t kK2Fixed = (kK2Win + 2) * 4 + kK2Win * 4 + kK2Win * 8 + 1024;
 
 struct K2Params {
     DevGraph g;
@@ -74,7 +74,7 @@ struct K2Params {
     // the seeds' F1 rows (phase 0): vertex, CSR row begin, length (0 for the
     // seed itself); per seed its first row (kNoF1: scratch ran out) and its
     // first 2048-row window total
-    uint32_t* f1off;  // [ns]
+    uint4* sinfo;     // [ns] {device seed id, CSR row begin, degree, first F1 row or kNoF1}
     uint32_t* f1win;  // [ns]
     uint32_t* f1v;
     uint32_t* f1rb;
@@ -127,6 +127,12 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
     return total;
 }
 
+// one row-cursor step (asm volatile: the load stays inside the cursor loop
+// instead of being re-issued after it for every entry)
+__device__ __forceinline__ void ld_rinfo(uint32_t base, uint32_t t, uint32_t& nxt, uint32_t& dl) {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nxt), "=r"(dl) : "r"(base + t * 8));
+}
+
 __device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t bit) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + word * 4), "r"(bit));
 }
@@ -134,9 +140,14 @@ __device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t b
 __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
     uint32_t* bm = reinterpret_cast<uint32_t*>(k2_smem);
-    unsigned long long* pre = reinterpret_cast<unsigned long long*>(k2_smem + (size_t)P.rwords * 4);
-    uint32_t* rbeg = reinterpret_cast<uint32_t*>(pre + kK2Win + 1);
-    unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(rbeg + kK2Win);  // [32]
+    // window prefix of the row lengths, relative to the window start (a window's
+    // rows are distinct vertices, so its total is <= m < 2^32)
+    uint32_t* pre = reinterpret_cast<uint32_t*>(k2_smem + (size_t)P.rwords * 4);
+    uint32_t* rbeg = pre + kK2Win + 2;
+    // rinfo[t] = {pre[t + 1], rbeg[t] - pre[t]}: one 64-bit load advances a row
+    // cursor (entry x of the window lives at col_idx[x + rinfo[t].y])
+    uint2* rinfo = reinterpret_cast<uint2*>(rbeg + kK2Win);
+    unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(rinfo + kK2Win);  // [32]
     unsigned long long* s_misc = s_warp + 32;                                         // [8]
     const DevGraph& g = P.g;
     const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
@@ -168,10 +179,10 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         const bool ok = off + deg <= P.f1cap && ow + nwin <= P.wtcap && ot + nt <= P.taskcap;
         for (uint32_t q = lane; q < nt; q += 32)
             if (ot + q < P.taskcap) P.tasks[ot + q] = make_uint2(ok ? (uint32_t)i : kNoF1, q);
+        if (lane == 0) P.sinfo[i] = make_uint4(s, b, deg, ok ? (uint32_t)off : kNoF1);
         if (ok) {
             for (uint32_t q = lane; q < nwin; q += 32) P.wt[ow + q] = 0;
             if (lane == 0) {
-                P.f1off[i] = (uint32_t)off;
                 P.f1win[i] = (uint32_t)ow;
                 P.w[i] = 0;
                 P.f1[i] = 0;
@@ -190,7 +201,6 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) nf += __shfl_xor_sync(kFull, nf, d);
             if (lane == 0) {
-                P.f1off[i] = kNoF1;
                 P.w[i] = wsum;
                 P.f1[i] = nf;
             }
@@ -204,9 +214,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         for (uint64_t t = gwarp; t < ntask; t += nwarps) {
             const uint2 tk = __ldcg(P.tasks + t);
             if (tk.x == kNoF1) continue;
-            const uint32_t s = k2_seed(P, tk.x);
-            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
-            const uint32_t off = ld_cg(P.f1off + tk.x);
+            const uint4 si = __ldcg(P.sinfo + tk.x);
+            const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
             const uint32_t j0 = tk.y * kK2Task;
             uint32_t v[kK2Task / 32], rb[kK2Task / 32], re[kK2Task / 32];
 #pragma unroll
@@ -311,10 +320,9 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             const unsigned long long a2 = max(glo, ws) - ws, z2 = min(ghi, we) - ws;
             const unsigned long long a = a2 > P.seedcost ? a2 - P.seedcost : 0;
             const unsigned long long z = z2 > P.seedcost ? z2 - P.seedcost : 0;
-            const uint32_t s = k2_seed(P, i);
-            const uint32_t b = __ldg(g.rp + s), deg = __ldg(g.rp + s + 1) - b;
-            const uint32_t off = ld_cg(P.f1off + i);
-            const uint32_t ow = off != kNoF1 ? ld_cg(P.f1win + i) : 0;
+            const uint4 si = __ldcg(P.sinfo + i);
+            const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
+            const uint32_t ow = ld_cg(P.f1win + i);  // meaningful only when off != kNoF1
             const bool v1 = a2 == 0;  // the part holding offset 0 also holds {s} u F1
             if (v1 && threadIdx.x == 0 && s - rlo < P.rbits) smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
             unsigned long long wbase = 0;  // seed-local entry offset of the current window
@@ -350,49 +358,68 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                 }
                 unsigned long long ex;
                 const unsigned long long wtot = block_excl_scan(d2[0] + d2[1], &ex, s_warp);
-                pre[threadIdx.x * 2] = wbase + ex;
-                pre[threadIdx.x * 2 + 1] = wbase + ex + d2[0];
-                if (threadIdx.x == 0) pre[wl] = wbase + wtot;
+                pre[threadIdx.x * 2] = (uint32_t)ex;
+                pre[threadIdx.x * 2 + 1] = (uint32_t)(ex + d2[0]);
+                if (threadIdx.x == 0) pre[wl] = (uint32_t)wtot;
+                __syncthreads();
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t t = threadIdx.x * 2 + h;
+                    if (t < wl) rinfo[t] = make_uint2(pre[t + 1], rbeg[t] - pre[t]);
+                }
                 __syncthreads();
                 const unsigned long long x0 = max(a, wbase), x1 = min(z, wbase + wtot);
                 if (x0 < x1) {
                     // warp q takes [xs, xe) of the window's part as one flat
                     // stream: lane l reads entries xb + l + 32 j (coalesced within
-                    // a row), each lane walking its own row cursor; the next
-                    // block's loads are issued before this block's atomics
-                    const unsigned long long span = x1 - x0;
-                    const unsigned long long xs = x0 + span * wib / kK2Warps;
-                    const unsigned long long xe = x0 + span * (wib + 1) / kK2Warps;
+                    // a row), each lane walking its own row cursor. All offsets
+                    // are window-relative u32. Full blocks run without bounds
+                    // checks; addresses first, then the loads back to back, then
+                    // the atomics, so kK2Ilp loads per lane are in flight
+                    const uint32_t X0 = (uint32_t)(x0 - wbase), span = (uint32_t)(x1 - x0);
+                    const uint32_t xs = X0 + (uint32_t)((unsigned long long)span * wib / kK2Warps);
+                    const uint32_t xe = X0 + (uint32_t)((unsigned long long)span * (wib + 1) / kK2Warps);
                     if (xs < xe) {
                         uint32_t lo = 0, hi = wl;  // last row t with pre[t] <= xs
                         while (hi - lo > 1) {
                             const uint32_t mid = (lo + hi) / 2;
                             if (pre[mid] <= xs) lo = mid; else hi = mid;
                         }
-                        uint32_t tl = lo, rb = rbeg[lo];
-                        unsigned long long cur = pre[lo], nxt = pre[lo + 1];
-                        // addresses first (row cursor), then all loads back to
-                        // back (unconditional: a lane past the end re-reads its
-                        // last valid entry), then the atomics: no load waits on
-                        // a branch, so kK2Ilp loads per lane are in flight
-                        uint32_t last = rb + (uint32_t)(xs - cur);
-                        for (unsigned long long xb = xs; xb < xe; xb += 32 * kK2Ilp) {
+                        uint32_t tl = lo, nxt = rinfo[lo].x, dl = rinfo[lo].y;
+                        const uint32_t ri_base = (uint32_t)__cvta_generic_to_shared(rinfo);
+                        uint32_t xb = xs;
+                        for (; xb + 32 * kK2Ilp <= xe; xb += 32 * kK2Ilp) {
+                            uint32_t idx[kK2Ilp];
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) {
+                                const uint32_t x = xb + lane + 32 * q;
+                                while (nxt <= x) {
+                                    ++tl;
+                                    ld_rinfo(ri_base, tl, nxt, dl);
+                                }
+                                idx[q] = x + dl;
+                            }
+                            uint32_t u[kK2Ilp];
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) u[q] = __ldg(g.ci + idx[q]);
+#pragma unroll
+                            for (int q = 0; q < kK2Ilp; ++q) {
+                                const uint32_t t = u[q] - rlo;
+                                if (t < P.rbits) smem_or(bm_base, t >> 5, 1u << (t & 31));
+                            }
+                        }
+                        if (xb < xe) {  // tail (< 32 * kK2Ilp entries): one masked block
                             uint32_t idx[kK2Ilp];
                             uint32_t valid = 0;
 #pragma unroll
                             for (int q = 0; q < kK2Ilp; ++q) {
-                                const unsigned long long x = xb + lane + 32 * q;
-                                if (x < xe) {
-                                    while (nxt <= x) {
-                                        ++tl;
-                                        cur = nxt;
-                                        nxt = pre[tl + 1];
-                                        rb = rbeg[tl];
-                                    }
-                                    last = rb + (uint32_t)(x - cur);
-                                    valid |= 1u << q;
+                                const uint32_t x = min(xb + lane + 32 * q, xe - 1);
+                                valid |= (xb + lane + 32 * q < xe ? 1u : 0u) << q;
+                                while (nxt <= x) {
+                                    ++tl;
+                                    ld_rinfo(ri_base, tl, nxt, dl);
                                 }
-                                idx[q] = last;
+                                idx[q] = x + dl;
                             }
                             uint32_t u[kK2Ilp];
 #pragma unroll
@@ -420,12 +447,12 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             const uint32_t n4 = P.rwords / 4;
             if (whole) {
                 uint32_t pc = 0;
+#pragma unroll 4
                 for (uint32_t q = threadIdx.x; q < n4; q += kK2Block) {
                     const uint4 x = bm4[q];
-                    if (x.x | x.y | x.z | x.w) {
-                        pc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-                        bm4[q] = make_uint4(0, 0, 0, 0);
-                    }
+                    const uint32_t c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+                    pc += c;
+                    if (c) bm4[q] = make_uint4(0, 0, 0, 0);
                 }
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
@@ -497,10 +524,9 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         const unsigned long long ex = pop - 1 - nf;
         P.counts[i] = P.cumulative ? pop - 1 : ex;
         if (len) P.acc[i] = 0;
-        const uint32_t s = k2_seed(P, i);
         f1s += nf;
         f2s += ex;
-        d1 += __ldg(g.rp + s + 1) - __ldg(g.rp + s);
+        d1 += __ldcg(P.sinfo + i).z;
         e2 += len ? len - P.seedcost : 0;
         runs += nf != 0;
     }
@@ -579,11 +605,12 @@ cudaError_t launch_k2(Launch& L) {
     // workspace: per-seed arrays (grow with the batch) and the staging area
     const uint64_t ns = L.nseeds;
     if (ws->k2_cap < ns) {
-        for (void* p : {(void*)ws->k2_w, (void*)ws->k2_acc, (void*)ws->k2_f1, (void*)ws->k2_f1off,
+        for (void* p : {(void*)ws->k2_w, (void*)ws->k2_acc, (void*)ws->k2_f1, (void*)ws->k2_sinfo,
                         (void*)ws->k2_f1win, (void*)ws->k2_wt, (void*)ws->k2_tasks})
             cudaFree(p);
         ws->k2_w = ws->k2_acc = ws->k2_wt = nullptr;
-        ws->k2_f1 = ws->k2_f1off = ws->k2_f1win = nullptr;
+        ws->k2_f1 = ws->k2_f1win = nullptr;
+        ws->k2_sinfo = nullptr;
         ws->k2_tasks = nullptr;
         ws->k2_cap = 0;
         const uint64_t cap = std::max<uint64_t>(ns, 1024);
@@ -595,7 +622,7 @@ cudaError_t launch_k2(Launch& L) {
         if ((e = cudaMalloc(&ws->k2_w, (cap + 1) * 8))) return e;
         if ((e = cudaMalloc(&ws->k2_acc, cap * 8))) return e;
         if ((e = cudaMalloc(&ws->k2_f1, cap * 4))) return e;
-        if ((e = cudaMalloc(&ws->k2_f1off, cap * 4))) return e;
+        if ((e = cudaMalloc(&ws->k2_sinfo, cap * 16))) return e;
         if ((e = cudaMalloc(&ws->k2_f1win, cap * 4))) return e;
         if ((e = cudaMalloc(&ws->k2_wt, ws->k2_wtcap * 8))) return e;
         if ((e = cudaMalloc(&ws->k2_tasks, ws->k2_taskcap * 8))) return e;
@@ -656,7 +683,7 @@ cudaError_t launch_k2(Launch& L) {
     Q.bounds = ws->k2_bounds;
     Q.first = ws->k2_first;
     Q.cuts = ws->k2_cuts;
-    Q.f1off = ws->k2_f1off;
+    Q.sinfo = ws->k2_sinfo;
     Q.f1win = ws->k2_f1win;
     Q.f1v = ws->k2_f1v;
     Q.f1rb = ws->k2_f1rb;
@@ -668,9 +695,11 @@ cudaError_t launch_k2(Launch& L) {
     Q.taskcap = ws->k2_taskcap;
     static const unsigned long long seedcost = [] {
         const char* c = std::getenv("MGK_K2_SEEDCOST");
-        return c ? std::strtoull(c, nullptr, 10) : 16384ull;
+        return c ? std::strtoull(c, nullptr, 10) : 0ull;
     }();
-    Q.seedcost = seedcost;
+    // a seed's fixed cost in adjacency-entry units: its slice sweep (~rwords)
+    // plus the per-seed setup (measured on G2: ~60K entries-equivalent)
+    Q.seedcost = seedcost ? seedcost : 24576ull + rwords;
     if (L.host_io && ns <= kK2Inline) {
         Q.seeds = nullptr;
         std::memcpy(Q.inline_seeds, L.h_seeds, (size_t)ns * 4);

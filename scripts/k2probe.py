@@ -1,10 +1,21 @@
-import sys, numpy as np
-sys.path.insert(0, '.')
-from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch
+"""Timing breakdown of the cfg2 k=2 call (G2, 300 seeds): kernel ms, setup
+(phases 0-1), slices (phase 2), slices + merge, answers; min over 10 calls."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch  # noqa: E402
+
 rp, ci = H.gen_csr(H.G2)
 g = DeviceGraph.from_csr(rp, ci)
-seeds = H.pick_seeds(rp, 300, 1)
-for _ in range(3):
+seeds = H.pick_seeds(rp, int(sys.argv[1]) if len(sys.argv) > 1 else 300, 1)
+rows = []
+for _ in range(12):
     c, st = k_hop_count_batch(g, seeds, 2, 0, stats=True)
-print({k: st[k] for k in st if k != 'levels'})
-for h in range(3): print(h, st['levels'][h])
+    L = st["levels"]
+    rows.append((st["kernel_ms"] * 1e3, L[0]["ns"] / 1e3, L[0]["candidates"] / 1e3, L[2]["ns"] / 1e3,
+                 st["cleanup_us"]))
+rows = rows[2:]
+best = min(rows)
+print("k2 call us %.1f | setup %.1f | slices %.1f | slices+merge %.1f | answers %.1f  (median call %.1f)"
+      % (*best, sorted(r[0] for r in rows)[len(rows) // 2]))
