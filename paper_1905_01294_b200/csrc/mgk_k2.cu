@@ -291,10 +291,20 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             base = we;
             if (v == 0) continue;
             const uint32_t b0 = first_group(ws, true), bA = first_group(ws, false), bB = first_group(we, true);
-            for (uint32_t bb = b0; bb < bB && bb < G; ++bb) P.first[bb] = (uint32_t)i;
-            if (bA < bB) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bA - 1, bB - 1, 0);
+            // a boundary inside a small seed moves to the nearer end of it: the
+            // seed is not cut (no staged slices, no merge) and the groups on
+            // both sides change size by at most 1/16
+            const bool small = v * 8 < total / G;
+            for (uint32_t bb = b0; bb < bB && bb < G; ++bb) {
+                const unsigned long long x = group_lo(total, bb, G);
+                const bool to_end = small && x > ws && we - x < x - ws;
+                P.bounds[bb] = small ? (to_end ? we : ws) : x;
+                P.first[bb] = (uint32_t)i + (to_end ? 1u : 0u);
+            }
+            if (!small && bA < bB) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bA - 1, bB - 1, 0);
         }
-        for (uint32_t t = threadIdx.x; t <= G; t += kK2Block) P.bounds[t] = group_lo(total, t, G);
+        for (uint32_t t = threadIdx.x; t <= G; t += kK2Block)  // boundaries no seed holds
+            if (group_lo(total, t, G) >= total) P.bounds[t] = total;
         if (threadIdx.x == 0) P.w[P.ns] = total;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -489,7 +499,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                 // the first slot of the groups after it; with W >= G no group
                 // is empty, otherwise empty groups (no slice written) are skipped
                 uint4 o = make_uint4(0, 0, 0, 0);
-                const bool sparse = W < G;
+                const bool sparse = W < G;  // (snapped boundaries never empty a group inside a cut seed)
                 for (uint32_t g0 = c.y; g0 <= c.z; g0 += 4) {
                     uint4 y[4];
 #pragma unroll
