@@ -85,6 +85,7 @@ struct K2Params {
     uint2* tasks;            // {seed, 256-row block}
     uint64_t taskcap;
     unsigned long long seedcost;  // work-line units charged per seed (its fixed cost)
+    uint32_t snapdiv;  // group boundaries within (group size / snapdiv) of a seed edge move to it
     uint32_t inline_seeds[kK2Inline];
 };
 
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         const unsigned long long total = block_excl_scan(part, &base, s_warp);
         unsigned int* s_ncut = reinterpret_cast<unsigned int*>(s_misc);
         if (threadIdx.x == 0) *s_ncut = 0;
+        const unsigned long long snap = total / G / P.snapdiv;
         __syncthreads();
         // smallest b in [0, G] with group_lo(b) > x (>= x when ge); group_lo(G) = total
         auto first_group = [&](unsigned long long x, bool ge) {
@@ -290,18 +292,27 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             P.w[i] = ws;
             base = we;
             if (v == 0) continue;
-            const uint32_t b0 = first_group(ws, true), bA = first_group(ws, false), bB = first_group(we, true);
-            // a boundary inside a small seed moves to the nearer end of it: the
-            // seed is not cut (no staged slices, no merge) and the groups on
-            // both sides change size by at most 1/16
-            const bool small = v * 8 < total / G;
+            const uint32_t b0 = first_group(ws, true), bB = first_group(we, true);
+            // a boundary within `snap` of a seed edge moves to that edge: the
+            // seed is not cut there (no staged slices, no merge) at the price of
+            // groups that differ in size by up to 2 snap
+            bool cut = false;
+            uint32_t bfirst = 0, blast = 0;
             for (uint32_t bb = b0; bb < bB && bb < G; ++bb) {
                 const unsigned long long x = group_lo(total, bb, G);
-                const bool to_end = small && x > ws && we - x < x - ws;
-                P.bounds[bb] = small ? (to_end ? we : ws) : x;
+                const bool to_start = x - ws <= snap, to_end = !to_start && we - x <= snap;
+                P.bounds[bb] = to_start ? ws : (to_end ? we : x);
                 P.first[bb] = (uint32_t)i + (to_end ? 1u : 0u);
+                if (!to_start && !to_end) {
+                    if (!cut) bfirst = bb;
+                    blast = bb;
+                    cut = true;
+                }
             }
-            if (!small && bA < bB) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bA - 1, bB - 1, 0);
+            // the seed's parts: from the group holding its start (the one before
+            // its first unsnapped boundary) to the one before the first boundary
+            // at or after its end
+            if (cut) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bfirst - 1, blast, 0);
         }
         for (uint32_t t = threadIdx.x; t <= G; t += kK2Block)  // boundaries no seed holds
             if (group_lo(total, t, G) >= total) P.bounds[t] = total;
@@ -710,6 +721,11 @@ cudaError_t launch_k2(Launch& L) {
     // a seed's fixed cost in adjacency-entry units: its slice sweep (~rwords)
     // plus the per-seed setup (measured on G2: ~60K entries-equivalent)
     Q.seedcost = seedcost ? seedcost : 24576ull + rwords;
+    static const unsigned long long snapdiv = [] {
+        const char* c = std::getenv("MGK_K2_SNAP");
+        return c ? std::max<unsigned long long>(1, std::strtoull(c, nullptr, 10)) : 8ull;
+    }();
+    Q.snapdiv = (uint32_t)snapdiv;
     if (L.host_io && ns <= kK2Inline) {
         Q.seeds = nullptr;
         std::memcpy(Q.inline_seeds, L.h_seeds, (size_t)ns * 4);

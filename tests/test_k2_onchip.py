@@ -21,8 +21,10 @@ WORKER = Path(__file__).resolve().parent / "helpers" / "k2_worker.py"
     {"MGK_K2_SEEDCOST": "0"},                          # pure entry split: many cut seeds
     {"MGK_K2_SEEDCOST": "0", "MGK_K2_F1CAP": "64"},    # F1 scratch runs out: in-kernel prefixes
     {"MGK_K2_SEEDCOST": "100000000"},                  # one seed per group at most
+    {"MGK_K2_SNAP": "1"},                              # boundaries snap to seed edges a whole group away
+    {"MGK_K2_SNAP": "1000000", "MGK_K2_SEEDCOST": "0"},  # (almost) no snapping
     {"MGK_NO_K2SMEM": "1"},                            # the L2-bitmap engine (fr_kernel)
-], ids=["default", "cost0", "f1cap", "cost_huge", "no_onchip"])
+], ids=["default", "cost0", "f1cap", "cost_huge", "snap_wide", "snap_none", "no_onchip"])
 def test_k2_paths_against_oracle(env):
     p = subprocess.run([sys.executable, str(WORKER)], env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=900)
