@@ -257,12 +257,17 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     }
     grid_barrier(P.bar);
 
-    // ---- phase 1 (CTA 0): the work line (w + seedcost per seed with work), the
-    // group slices, each group's first seed, and the seeds cut by a group
-    // boundary. Thread t owns a chunk of seeds and finds the boundaries inside
-    // them arithmetically (no searches through global memory)
-    if (blockIdx.x == 0) {
-        const uint32_t G = P.ngroups;
+    // ---- phase 1 (every CTA, no barrier after it): the work line (w + seedcost
+    // per seed with work), this CTA's group slice and its first seed. Thread t
+    // owns a chunk of seeds and finds the group boundaries inside them
+    // arithmetically. CTA 0 also records every boundary and the cut seeds for
+    // the merge (read after the next grid barrier)
+    const uint32_t G = P.ngroups, R = P.R;
+    const uint32_t grp = blockIdx.x / R, rr = blockIdx.x % R;
+    unsigned long long W;
+    {
+        unsigned long long* s_b = s_misc;  // [0] group start, [1] group end, [2] first seed, [3] its ws
+        unsigned int* s_ncut = reinterpret_cast<unsigned int*>(s_misc + 4);
         const uint64_t per = (P.ns + kK2Block - 1) / kK2Block;
         const uint64_t i0 = min((uint64_t)threadIdx.x * per, P.ns), i1 = min(i0 + per, P.ns);
         unsigned long long part = 0;
@@ -272,27 +277,33 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         }
         unsigned long long base;
         const unsigned long long total = block_excl_scan(part, &base, s_warp);
-        unsigned int* s_ncut = reinterpret_cast<unsigned int*>(s_misc);
+        W = total;
         if (threadIdx.x == 0) *s_ncut = 0;
         const unsigned long long snap = total / G / P.snapdiv;
+        // boundaries no seed holds (the end of the work line)
+        if (threadIdx.x < 2 && group_lo(total, grp + threadIdx.x, G) >= total) {
+            s_b[threadIdx.x] = total;
+            if (threadIdx.x == 0) s_b[2] = P.ns;
+        }
+        if (blockIdx.x == 0)
+            for (uint32_t t = threadIdx.x; t <= G; t += kK2Block)
+                if (group_lo(total, t, G) >= total) P.bounds[t] = total;
         __syncthreads();
-        // smallest b in [0, G] with group_lo(b) > x (>= x when ge); group_lo(G) = total
-        auto first_group = [&](unsigned long long x, bool ge) {
+        // smallest b in [0, G] with group_lo(b) >= x; group_lo(G) = total
+        auto first_group = [&](unsigned long long x) {
             uint32_t lo = 0, hi = G;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) / 2;
-                const unsigned long long gm = group_lo(total, mid, G);
-                if (ge ? gm >= x : gm > x) hi = mid; else lo = mid + 1;
+                if (group_lo(total, mid, G) >= x) hi = mid; else lo = mid + 1;
             }
             return lo;
         };
         for (uint64_t i = i0; i < i1; ++i) {
             const unsigned long long v0 = ld_cg(P.w + i);
             const unsigned long long v = v0 ? v0 + P.seedcost : 0, ws = base, we = base + v;
-            P.w[i] = ws;
             base = we;
             if (v == 0) continue;
-            const uint32_t b0 = first_group(ws, true), bB = first_group(we, true);
+            const uint32_t b0 = first_group(ws), bB = first_group(we);
             // a boundary within `snap` of a seed edge moves to that edge: the
             // seed is not cut there (no staged slices, no merge) at the price of
             // groups that differ in size by up to 2 snap
@@ -301,8 +312,18 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             for (uint32_t bb = b0; bb < bB && bb < G; ++bb) {
                 const unsigned long long x = group_lo(total, bb, G);
                 const bool to_start = x - ws <= snap, to_end = !to_start && we - x <= snap;
-                P.bounds[bb] = to_start ? ws : (to_end ? we : x);
-                P.first[bb] = (uint32_t)i + (to_end ? 1u : 0u);
+                const unsigned long long bnd = to_start ? ws : (to_end ? we : x);
+                const uint32_t fs = (uint32_t)i + (to_end ? 1u : 0u);
+                if (bb == grp) {
+                    s_b[0] = bnd;
+                    s_b[2] = fs;
+                    s_b[3] = to_end ? we : ws;
+                }
+                if (bb == grp + 1) s_b[1] = bnd;
+                if (blockIdx.x == 0) {
+                    P.bounds[bb] = bnd;
+                    P.first[bb] = fs;
+                }
                 if (!to_start && !to_end) {
                     if (!cut) bfirst = bb;
                     blast = bb;
@@ -312,28 +333,25 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             // the seed's parts: from the group holding its start (the one before
             // its first unsnapped boundary) to the one before the first boundary
             // at or after its end
-            if (cut) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bfirst - 1, blast, 0);
+            if (cut && blockIdx.x == 0) P.cuts[atomicAdd(s_ncut, 1u)] = make_uint4((uint32_t)i, bfirst - 1, blast, 0);
         }
-        for (uint32_t t = threadIdx.x; t <= G; t += kK2Block)  // boundaries no seed holds
-            if (group_lo(total, t, G) >= total) P.bounds[t] = total;
-        if (threadIdx.x == 0) P.w[P.ns] = total;
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
             P.misc[4] = *s_ncut;
             P.misc[0] = globaltimer();
         }
     }
-    grid_barrier(P.bar);
 
     // ---- phase 2: group slices of the work line -----------------------------------
-    const unsigned long long W = ld_cg(P.w + P.ns);
-    const uint32_t G = P.ngroups, R = P.R;
-    const uint32_t grp = blockIdx.x / R, rr = blockIdx.x % R;
     const uint32_t rlo = rr * P.rbits;
-    const unsigned long long glo = W ? ld_cg(P.bounds + grp) : 0, ghi = W ? ld_cg(P.bounds + grp + 1) : 0;
+    const unsigned long long glo = W ? s_misc[0] : 0, ghi = W ? s_misc[1] : 0;
+    const uint64_t ifirst = s_misc[2];
+    unsigned long long wnext = s_misc[3];  // work-line start of seed ifirst
     if (glo < ghi) {
-        for (uint64_t i = ld_cg(P.first + grp); i < P.ns; ++i) {
-            const unsigned long long ws = ld_cg(P.w + i), we = ld_cg(P.w + i + 1);
+        for (uint64_t i = ifirst; i < P.ns; ++i) {
+            const unsigned long long v0 = ld_cg(P.w + i);
+            const unsigned long long ws = wnext, we = ws + (v0 ? v0 + P.seedcost : 0);
+            wnext = we;
             if (ws >= ghi) break;
             if (we == ws) continue;
             // this group's part of the seed: on the work line, then in adjacency
@@ -358,35 +376,36 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     }
                 }
                 unsigned long long d2[2];
+                uint32_t rb2[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t t = threadIdx.x * 2 + h;
                     d2[h] = 0;
+                    rb2[h] = 0;
                     if (t < wl) {
                         uint32_t v;
                         if (off != kNoF1) {
                             v = v1 ? ld_cg(P.f1v + off + j0 + t) : 0;
-                            rbeg[t] = ld_cg(P.f1rb + off + j0 + t);
+                            rb2[h] = ld_cg(P.f1rb + off + j0 + t);
                             d2[h] = ld_cg(P.f1d + off + j0 + t);
                         } else {
                             v = __ldg(g.ci + b + j0 + t);
-                            const uint32_t rb = __ldg(g.rp + v);
-                            rbeg[t] = rb;
-                            if (v != s) d2[h] = __ldg(g.rp + v + 1) - rb;
+                            rb2[h] = __ldg(g.rp + v);
+                            if (v != s) d2[h] = __ldg(g.rp + v + 1) - rb2[h];
                         }
                         if (v1 && v - rlo < P.rbits) smem_or(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
                     }
                 }
                 unsigned long long ex;
                 const unsigned long long wtot = block_excl_scan(d2[0] + d2[1], &ex, s_warp);
-                pre[threadIdx.x * 2] = (uint32_t)ex;
-                pre[threadIdx.x * 2 + 1] = (uint32_t)(ex + d2[0]);
-                if (threadIdx.x == 0) pre[wl] = (uint32_t)wtot;
-                __syncthreads();
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const uint32_t t = threadIdx.x * 2 + h;
-                    if (t < wl) rinfo[t] = make_uint2(pre[t + 1], rbeg[t] - pre[t]);
+                {
+                    const uint32_t p0 = (uint32_t)ex, p1 = (uint32_t)(ex + d2[0]), p2 = (uint32_t)(ex + d2[0] + d2[1]);
+                    const uint32_t t = threadIdx.x * 2;
+                    pre[t] = p0;
+                    pre[t + 1] = p1;
+                    if (t < wl) rinfo[t] = make_uint2(p1, rb2[0] - p0);
+                    if (t + 1 < wl) rinfo[t + 1] = make_uint2(p2, rb2[1] - p1);
+                    if (threadIdx.x == 0) pre[wl] = (uint32_t)wtot;
                 }
                 __syncthreads();
                 const unsigned long long x0 = max(a, wbase), x1 = min(z, wbase + wtot);
@@ -540,7 +559,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     unsigned long long f1s = 0, f2s = 0, d1 = 0, e2 = 0, runs = 0;
     for (uint64_t i = gtid; i < P.ns; i += nthreads) {
         const unsigned long long nf = ld_cg(P.f1 + i);
-        const unsigned long long len = ld_cg(P.w + i + 1) - ld_cg(P.w + i);
+        const unsigned long long raw = ld_cg(P.w + i), len = raw ? raw + P.seedcost : 0;
         const unsigned long long pop = len ? ld_cg(P.acc + i) : 1 + nf;  // |B|
         const unsigned long long ex = pop - 1 - nf;
         P.counts[i] = P.cumulative ? pop - 1 : ex;
