@@ -164,6 +164,11 @@ def algo_bytes(st: dict) -> float:
     write)."""
     lv = st["levels"]
     total = 0.0
+    if st.get("path") == "smem_k2":
+        # k = 2 with the visited sets on chip: the seeds' row pointers, their
+        # rows (F1 ids) with each F1 vertex's row-pointer pair, and every hop-2
+        # adjacency entry once from HBM (the R slice CTAs' repeats hit L2)
+        return 8 * st["batches"] + 12 * lv[1]["scanned"] + 4 * lv[2]["scanned"]
     if st["engine"] == "lanes":
         W = st["lanes"] // 64
         for h in range(1, len(lv)):
@@ -462,7 +467,8 @@ def run_ours(args):
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(f"{WORKLOAD}_k{dom}", {}).get("total")
+            key = f"{WORKLOAD}_k{dom}" + ("_smem" if stats[dom].get("path") == "smem_k2" else "")
+            traffic = json.loads(tf.read_text()).get(key, {}).get("total")
         except Exception:
             traffic = None
     # the dominant call's last hop is one random 32-bit atomic per scanned edge
@@ -472,7 +478,7 @@ def run_ours(args):
     lv = stats[dom]["levels"]
     hops = [h for h in range(1, len(lv)) if lv[h]["runs"]]
     ub = ROOT / "profiles" / "ubench_atomics.json"
-    if stats[dom]["engine"] == "single" and hops and ub.exists():
+    if stats[dom]["engine"] == "single" and stats[dom].get("path") != "smem_k2" and hops and ub.exists():
         last = lv[hops[-1]]
         if last["ns"] and not last["pull_runs"]:
             gops = last["scanned"] / last["ns"]
@@ -483,6 +489,21 @@ def run_ours(args):
             l2_atomic = {"hop": hops[-1], "atomics": last["scanned"], "us": last["ns"] / 1e3,
                          "achieved_gops": gops, "ceiling_gops": ceil, "frac": gops / ceil,
                          "ceiling_source": "profiles/ubench_atomics.json: fastest measured red.or (L2-resident array, best launch shape)"}
+    # the on-chip k = 2 path: every hop-2 adjacency entry is streamed by the R
+    # CTAs holding the seed's vertex slices and set with a shared-memory atomic;
+    # its ceiling is the measured stream + smem-atomic rate of that pattern
+    onchip = None
+    us_ = ROOT / "profiles" / "ubench_smem.json"
+    if stats[dom].get("path") == "smem_k2" and len(lv) > 2 and lv[2]["ns"] and us_.exists():
+        u = json.loads(us_.read_text())
+        R = 2  # G2: the visited set spans two 150 KB slices
+        reads = R * lv[2]["scanned"]
+        got = reads / lv[2]["ns"]
+        ceil = u["stream_ids_from_dram_then_smem_red_or"]["sorted_runs_ilp16"]
+        onchip = {"hop": 2, "entries": lv[2]["scanned"], "slice_ctas": R, "entry_reads": reads,
+                  "us": lv[2]["ns"] / 1e3, "achieved_g_reads": got, "ceiling_g_reads": ceil, "frac": got / ceil,
+                  "ceiling_source": "profiles/ubench_smem.json: ids streamed from HBM + shared-memory red.or, "
+                                    "R=2 filter, sorted runs, one 1024-thread CTA per SM"}
     cpu = cpu_baseline(rp, ci, seeds) if (world == 1 and not args.no_cpu) else None
     line = {
         "metric": "k-hop count queries/s (cfg2: 300 seeds x k=1,2 exact on the 2.4M/67M R-MAT graph)",
@@ -512,10 +533,12 @@ def run_ours(args):
                                      "us": L["ns"] / 1e3} for L in stats[k]["levels"][1:]]}
                   for k in KS},
         "roofline": {"bound": "hbm", "kernel": (f"ms_kernel<W={stats[dom]['lanes'] // 64}>" if stats[dom]["engine"] == "lanes"
+                                                else "k2_kernel" if stats[dom].get("path") == "smem_k2"
                                                 else "fr_kernel + fr_finish") + f" (k={dom} call)",
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "peak_source": pk_src,
-                     "algo_bytes_per_launch": ab, "traffic": traffic, "l2_atomic": l2_atomic},
+                     "algo_bytes_per_launch": ab, "traffic": traffic, "l2_atomic": l2_atomic,
+                     "onchip": onchip},
         "cpu_baseline": cpu,
         "e2e": {"value": q_per_step * args.steps / (e2e_total / 1e3), "unit": "queries/s",
                 "h2d_bytes_per_step": 4 * len(seeds), "d2h_bytes_per_step": 8 * len(seeds) * len(KS),

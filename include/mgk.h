@@ -78,7 +78,8 @@ typedef struct mgk_stats {
     uint32_t grid;         /* persistent CTAs launched */
     uint32_t block;        /* threads per CTA */
     uint32_t launches;     /* kernel launches the call made */
-    uint32_t pad;
+    uint32_t path;         /* SINGLE: 0 = per-seed bitmaps in L2 (fr_kernel), 1 = k = 2 with the
+                              visited sets in shared memory (k2_kernel) */
     double kernel_ms;      /* CUDA-event time of the traversal launch(es) */
     uint64_t setup_ns;     /* device time clearing counters + seeding hop 0 */
     uint64_t cleanup_ns;   /* device time returning the workspace to all-zero */

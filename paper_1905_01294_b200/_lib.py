@@ -27,7 +27,7 @@ class MgkLevel(C.Structure):
 class MgkStats(C.Structure):
     _fields_ = [("engine", C.c_uint32), ("lanes", C.c_uint32), ("batches", C.c_uint32),
                 ("hops", C.c_uint32), ("grid", C.c_uint32), ("block", C.c_uint32),
-                ("launches", C.c_uint32), ("pad", C.c_uint32),
+                ("launches", C.c_uint32), ("path", C.c_uint32),
                 ("kernel_ms", C.c_double), ("setup_ns", C.c_uint64), ("cleanup_ns", C.c_uint64),
                 ("level", MgkLevel * (MAX_HOPS + 1))]
 
@@ -39,6 +39,7 @@ class MgkStats(C.Structure):
         return {"engine": {1: "single", 2: "lanes"}.get(self.engine, str(self.engine)),
                 "lanes": self.lanes, "batches": self.batches, "hops": self.hops,
                 "grid": self.grid, "block": self.block, "launches": self.launches,
+                "path": {0: "l2_bitmaps", 1: "smem_k2"}.get(self.path, str(self.path)),
                 "kernel_ms": self.kernel_ms,
                 "setup_us": self.setup_ns / 1e3, "cleanup_us": self.cleanup_ns / 1e3,
                 "levels": levels}

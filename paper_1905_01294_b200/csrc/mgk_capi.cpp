@@ -241,6 +241,7 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     *grid = L.grid;
     *block = L.block;
     ws->last_launches = e ? 0 : L.launches;
+    ws->last_path = L.path;
     return e;
 }
 
@@ -268,8 +269,9 @@ cudaError_t ensure_staging(Workspace* ws, uint64_t nseeds) {
 }
 
 void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint64_t nseeds,
-                uint32_t grid, uint32_t block, float ms, uint32_t launches) {
+                uint32_t grid, uint32_t block, float ms, uint32_t launches, uint32_t path) {
     std::memset(st, 0, sizeof *st);
+    st->path = path;
     st->engine = (uint32_t)engine;
     st->lanes = engine == MGK_ENGINE_LANES ? 64u * (uint32_t)W : 1u;
     st->batches = (uint32_t)(engine == MGK_ENGINE_LANES ? (nseeds + st->lanes - 1) / st->lanes : nseeds);
@@ -654,7 +656,7 @@ int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const
             cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
             LevelCounters lc[MGK_MAX_HOPS + 2];
             if ((e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost))) break;
-            fill_stats(stats, lc, used, W, nseeds, grid, block, ms, ws->last_launches);
+            fill_stats(stats, lc, used, W, nseeds, grid, block, ms, ws->last_launches, ws->last_path);
         }
     } while (0);
     release_ws(g, ws);
@@ -837,7 +839,7 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     if (!e) e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
     if (e) return fail_cuda(e, "stats");
     fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f,
-               ws->last_launches);
+               ws->last_launches, ws->last_path);
     return MGK_OK;
 }
 

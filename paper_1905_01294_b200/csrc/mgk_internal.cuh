@@ -153,6 +153,7 @@ struct Workspace {
     int misc_engine = 0, misc_W = 0;
     uint32_t misc_grid = 0, misc_block = 0;
     uint32_t last_launches = 0;  // engine kernels of the last call
+    uint32_t last_path = 0;      // mgk_stats.path of the last call
     uint64_t misc_nseeds = 0;
 };
 
@@ -197,6 +198,7 @@ struct Launch {
     const uint32_t* h_seeds = nullptr;  // host view of d_seeds when host_io
     uint32_t grid = 0, block = 0;  // out
     uint32_t launches = 0;         // out: engine kernels launched
+    uint32_t path = 0;             // out: 1 = the shared-memory k = 2 path
 };
 
 // Launches a persistent engine kernel: cooperative (all CTAs co-resident,

@@ -756,6 +756,7 @@ cudaError_t launch_k2(Launch& L) {
     L.grid = grid;
     L.block = kK2Block;
     L.launches = 1;
+    L.path = 1;
     return cudaSuccess;
 }
 

@@ -108,7 +108,7 @@ def launches(csv_path, out_md):
     # the timed step only: engine kernels (graph build and setup launches run
     # before the timed region)
     eng = OrderedDict((n, v) for n, v in agg.items()
-                      if any(t in n for t in ("fr_kernel", "fr_finish", "k1_kernel", "ms_kernel")))
+                      if any(t in n for t in ("fr_kernel", "fr_finish", "k1_kernel", "k2_kernel", "ms_kernel")))
     et = sum(v[1] for v in eng.values())
     if et:
         lines += ["", "timed-step engine kernels only (share of their sum):", "",
