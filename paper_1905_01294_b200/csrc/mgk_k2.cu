@@ -98,6 +98,12 @@ __device__ __forceinline__ uint32_t k2_seed(const K2Params& P, uint64_t i) {
 __device__ __forceinline__ unsigned long long group_lo(unsigned long long W, uint32_t g, uint32_t G) {
     return (W / G) * g + (W % G) * g / G;
 }
+// the same with W / G and W % G precomputed (r g < G^2 fits 32 bits)
+struct GroupLine {
+    unsigned long long q;
+    uint32_t r, G;
+    __device__ __forceinline__ unsigned long long lo(uint32_t g) const { return q * g + (r * g) / G; }
+};
 
 // block-wide exclusive scan of one u64 per thread; returns the block total
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v, unsigned long long* out,
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         }
     }
     grid_barrier(P.bar);
+    if (gtid == 0) P.misc[8] = globaltimer();
 
     // ---- phase 0b: tasks of 256 F1 rows: vertex, row begin, row length --------------
     {
@@ -257,6 +264,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     }
     grid_barrier(P.bar);
 
+    if (gtid == 0) P.misc[9] = globaltimer();
     // ---- phase 1 (every CTA, no barrier after it): the work line (w + seedcost
     // per seed with work), this CTA's group slice and its first seed. Thread t
     // owns a chunk of seeds and finds the group boundaries inside them
@@ -280,21 +288,22 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         W = total;
         if (threadIdx.x == 0) *s_ncut = 0;
         const unsigned long long snap = total / G / P.snapdiv;
+        const GroupLine gl{total / G, (uint32_t)(total % G), G};
         // boundaries no seed holds (the end of the work line)
-        if (threadIdx.x < 2 && group_lo(total, grp + threadIdx.x, G) >= total) {
+        if (threadIdx.x < 2 && gl.lo(grp + threadIdx.x) >= total) {
             s_b[threadIdx.x] = total;
             if (threadIdx.x == 0) s_b[2] = P.ns;
         }
         if (blockIdx.x == 0)
             for (uint32_t t = threadIdx.x; t <= G; t += kK2Block)
-                if (group_lo(total, t, G) >= total) P.bounds[t] = total;
+                if (gl.lo(t) >= total) P.bounds[t] = total;
         __syncthreads();
         // smallest b in [0, G] with group_lo(b) >= x; group_lo(G) = total
         auto first_group = [&](unsigned long long x) {
             uint32_t lo = 0, hi = G;
             while (lo < hi) {
                 const uint32_t mid = (lo + hi) / 2;
-                if (group_lo(total, mid, G) >= x) hi = mid; else lo = mid + 1;
+                if (gl.lo(mid) >= x) hi = mid; else lo = mid + 1;
             }
             return lo;
         };
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             bool cut = false;
             uint32_t bfirst = 0, blast = 0;
             for (uint32_t bb = b0; bb < bB && bb < G; ++bb) {
-                const unsigned long long x = group_lo(total, bb, G);
+                const unsigned long long x = gl.lo(bb);
                 const bool to_start = x - ws <= snap, to_end = !to_start && we - x <= snap;
                 const unsigned long long bnd = to_start ? ws : (to_end ? we : x);
                 const uint32_t fs = (uint32_t)i + (to_end ? 1u : 0u);
@@ -596,6 +605,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         P.lc[2].ns = ld_cg(&P.misc[2]) - ld_cg(&P.misc[0]);  // slices + merge
         P.lc[MGK_MAX_HOPS + 1].ns = now - ld_cg(&P.misc[2]);
         P.lc[0].candidates = ld_cg(&P.misc[1]) - ld_cg(&P.misc[0]);  // DIAG: slices alone (ns)
+        P.lc[0].frontier = ld_cg(&P.misc[8]) - t0;                    // DIAG: 0a + barrier
+        P.lc[0].vertices = ld_cg(&P.misc[9]) - ld_cg(&P.misc[8]);     // DIAG: 0b + barrier
     }
 }
 
@@ -700,8 +711,8 @@ cudaError_t launch_k2(Launch& L) {
         ws->k2_groups = G;
     }
     if (!ws->k2_misc) {
-        if ((e = cudaMalloc(&ws->k2_misc, 64))) return e;
-        if ((e = cudaMemset(ws->k2_misc, 0, 64))) return e;
+        if ((e = cudaMalloc(&ws->k2_misc, 128))) return e;
+        if ((e = cudaMemset(ws->k2_misc, 0, 128))) return e;
         if ((e = cudaStreamSynchronize(0))) return e;
     }
     K2Params Q;  // ~2 KB with the inline seeds; the launch copies it

@@ -14,8 +14,8 @@ for _ in range(12):
     c, st = k_hop_count_batch(g, seeds, 2, 0, stats=True)
     L = st["levels"]
     rows.append((st["kernel_ms"] * 1e3, L[0]["ns"] / 1e3, L[0]["candidates"] / 1e3, L[2]["ns"] / 1e3,
-                 st["cleanup_us"]))
+                 st["cleanup_us"], L[0]["frontier"] / 1e3, L[0]["vertices"] / 1e3))
 rows = rows[2:]
 best = min(rows)
-print("k2 call us %.1f | setup %.1f | slices %.1f | slices+merge %.1f | answers %.1f  (median call %.1f)"
-      % (*best, sorted(r[0] for r in rows)[len(rows) // 2]))
+print("k2 call us %.1f | setup %.1f | slices %.1f | slices+merge %.1f | answers %.1f | (0a+bar %.1f 0b+bar %.1f)"
+      "  (median call %.1f)" % (*best, sorted(r[0] for r in rows)[len(rows) // 2]))
