@@ -200,6 +200,13 @@ int mgk_matrix_free(mgk_matrix* m);
  * and serialize on that stream. */
 int mgk_khop_count_device(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
                           int mode, int engine, uint64_t* d_counts, void* stream);
+/* Device-path sections (the harness's k sections over one seed list,
+ * bench.cpp:311-343, device-resident like mgk_khop_count_device): the answers
+ * for ks[j] go to d_counts[j * nseeds + i]. A k = 1 section is answered by the
+ * k = 2 launch when that one runs on the on-chip path (|F1| is part of it).
+ * k is checked like mgk_khop_count_device; seeds are not. */
+int mgk_khop_count_device_ks(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, const uint32_t* ks,
+                             uint32_t nks, int mode, uint64_t* d_counts, void* stream);
 /* Work counters of the last device-path call on `stream` (waits for that stream;
  * kernel_ms is 0 on this path — time it with your own events). */
 int mgk_khop_device_stats(mgk_graph* g, void* stream, mgk_stats* stats);

@@ -206,7 +206,8 @@ int resolve_engine(int engine, uint64_t nseeds, uint32_t k) {
 cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_t nseeds,
                        Span span, int engine, unsigned long long* d_counts,
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
-                       int* W_out, bool keep_result = false, const uint32_t* h_seeds = nullptr) {
+                       int* W_out, bool keep_result = false, const uint32_t* h_seeds = nullptr,
+                       unsigned long long* d_counts1 = nullptr) {
     const uint32_t k = span.hi;
     // the engines zero the per-hop counters themselves (first launch of a call)
     cudaError_t e = cudaSuccess;
@@ -223,6 +224,7 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.min_hop = span.lo;
     L.seed_visited = span.seed_visited ? 1u : 0u;
     L.d_counts = d_counts;
+    L.d_counts1 = d_counts1;
     L.stream = stream;
     L.tuning = g->tuning;
     L.keep_result = keep_result;
@@ -607,6 +609,25 @@ namespace {
 // Counts of a batch of seeds over several hop windows (host buffers): all
 // windows are enqueued on the workspace's stream and answered with one
 // synchronisation; counts[w * nseeds + i] is window w of seed i.
+// A k = 1 section (seed pre-visited) of a call that also has a k = 2 section
+// taking the on-chip path is answered by that launch (|F1| is a by-product of
+// it): fused[w] = the k = 2 section answering section w, or -1.
+std::vector<int> plan_k1_fusion(const Graph* g, uint64_t nseeds, const Span* spans, uint32_t n, int engine) {
+    std::vector<int> fused(n, -1);
+    int k2 = -1;
+    for (uint32_t w = 0; w < n && k2 < 0; ++w)
+        if (spans[w].hi == 2 && spans[w].seed_visited && resolve_engine(engine, nseeds, 2) == MGK_ENGINE_SINGLE &&
+            k2_takes(g, nseeds, spans[w].lo))
+            k2 = (int)w;
+    if (k2 < 0) return fused;
+    for (uint32_t w = 0; w < n; ++w)
+        if (spans[w].hi == 1 && spans[w].seed_visited) {
+            fused[w] = k2;
+            break;  // one k = 1 output per launch
+        }
+    return fused;
+}
+
 int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const Span* spans, uint32_t nspans,
                      int engine, uint64_t* counts, mgk_stats* stats, const char* what) {
     Graph* g = &h->g;
@@ -630,19 +651,29 @@ int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const
     int used = 0, W = 0;
     float ms = 0.f;
     bool seeds_on_device = false;
+    const std::vector<int> fused = plan_k1_fusion(g, nseeds, spans, nspans, engine);
+    int k1_of = -1;  // the section a fused k = 2 launch also answers
+    uint32_t last_run = 0;
+    for (uint32_t w = 0; w < nspans; ++w) {
+        if (fused[w] >= 0) k1_of = (int)w;
+        else last_run = w;
+    }
     do {
         for (uint32_t w = 0; w < nspans && !e; ++w) {
+            if (fused[w] >= 0) continue;  // answered by the k = 2 launch
             const int eng = resolve_engine(engine, nseeds, spans[w].hi);
             const bool host_io = eng == MGK_ENGINE_SINGLE;
             if (!host_io && !seeds_on_device) {
                 if ((e = cudaMemcpyAsync(ws->d_seeds, hs, nseeds * 4, cudaMemcpyHostToDevice, ws->stream))) break;
                 seeds_on_device = true;
             }
-            const bool last = w + 1 == nspans;
+            const bool last = w == last_run;
+            unsigned long long* out = host_io ? ws->h_counts_dev : ws->d_counts;
+            unsigned long long* out1 = (k1_of >= 0 && fused[k1_of] == (int)w) ? out + k1_of * nseeds : nullptr;
             if (stats && last && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
             if ((e = run_engine(g, ws, host_io ? ws->h_seeds_dev : ws->d_seeds, nseeds, spans[w], eng,
-                                (host_io ? ws->h_counts_dev : ws->d_counts) + w * nseeds, ws->stream, &grid,
-                                &block, &used, &W, false, host_io ? hs : nullptr)))
+                                out + w * nseeds, ws->stream, &grid, &block, &used, &W, false,
+                                host_io ? hs : nullptr, out1)))
                 break;
             if (stats && last && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
             if (!host_io && (e = cudaMemcpyAsync(ws->h_counts + w * nseeds, ws->d_counts + w * nseeds,
@@ -783,44 +814,96 @@ int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64
     return MGK_OK;
 }
 
-int mgk_khop_count_device(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
-                          int mode, int engine, uint64_t* d_counts, void* stream) {
-    if (!h) return fail(MGK_ECONTRACT, "null graph");
-    if (k < 1 || k > MGK_MAX_HOPS) return fail(MGK_ECONTRACT, "k-hop count %u outside [1, %d]", k, MGK_MAX_HOPS);
-    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
-    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+}  // extern "C"
+
+namespace mgk {
+namespace {
+// the workspace of a caller's stream (created on first use)
+Workspace* stream_workspace(mgk_graph* h, cudaStream_t s, int* rc) {
     Graph* g = &h->g;
-    DeviceGuard dg(g->device);
-    cudaStream_t s = (cudaStream_t)stream;
     Workspace* ws = nullptr;
     {
         std::lock_guard<std::mutex> lk(g->mu);
         auto it = h->stream_ws.find(s);
         if (it != h->stream_ws.end()) ws = it->second;
     }
+    if (ws) return ws;
+    ws = new (std::nothrow) Workspace();
     if (!ws) {
-        ws = new (std::nothrow) Workspace();
-        if (!ws) return fail(MGK_ENOMEM, "out of host memory");
-        cudaError_t e = create_ws(g, ws, false);
-        if (e) {
-            destroy_ws(ws, false);
-            delete ws;
-            return fail_cuda(e, "workspace");
-        }
-        ws->stream = s;
-        std::lock_guard<std::mutex> lk(g->mu);
-        h->stream_ws[s] = ws;
+        *rc = fail(MGK_ENOMEM, "out of host memory");
+        return nullptr;
     }
+    cudaError_t e = create_ws(g, ws, false);
+    if (e) {
+        destroy_ws(ws, false);
+        delete ws;
+        *rc = fail_cuda(e, "workspace");
+        return nullptr;
+    }
+    ws->stream = s;
+    std::lock_guard<std::mutex> lk(g->mu);
+    h->stream_ws[s] = ws;
+    return ws;
+}
+
+// device-path sections: spans[w]'s answers at d_counts + w * nseeds
+int count_device_multi(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, const Span* spans, uint32_t nspans,
+                       int engine, uint64_t* d_counts, void* stream) {
+    Graph* g = &h->g;
+    DeviceGuard dg(g->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = MGK_OK;
+    Workspace* ws = stream_workspace(h, s, &rc);
+    if (!ws) return rc;
+    const std::vector<int> fused = plan_k1_fusion(g, nseeds, spans, nspans, engine);
+    int k1_of = -1;
+    for (uint32_t w = 0; w < nspans; ++w)
+        if (fused[w] >= 0) k1_of = (int)w;
+    auto* out = reinterpret_cast<unsigned long long*>(d_counts);
     uint32_t grid = 0, block = 0;
     int used = 0, W = 0;
-    cudaError_t e = run_engine(g, ws, d_seeds, nseeds, span_of(k, mode), engine,
-                               reinterpret_cast<unsigned long long*>(d_counts), s, &grid, &block, &used, &W);
+    cudaError_t e = cudaSuccess;
+    for (uint32_t w = 0; w < nspans && !e; ++w) {
+        if (fused[w] >= 0) continue;  // answered by the k = 2 launch
+        unsigned long long* out1 = (k1_of >= 0 && fused[k1_of] == (int)w) ? out + k1_of * nseeds : nullptr;
+        e = run_engine(g, ws, d_seeds, nseeds, spans[w], engine, out + w * nseeds, s, &grid, &block, &used, &W, false,
+                       nullptr, out1);
+    }
     ws->misc_engine = used;
     ws->misc_W = W;
     ws->misc_grid = grid;
     ws->misc_block = block;
     ws->misc_nseeds = nseeds;
     return e ? fail_cuda(e, "k-hop count (device)") : MGK_OK;
+}
+}  // namespace
+}  // namespace mgk
+
+extern "C" {
+
+int mgk_khop_count_device(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
+                          int mode, int engine, uint64_t* d_counts, void* stream) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (k < 1 || k > MGK_MAX_HOPS) return fail(MGK_ECONTRACT, "k-hop count %u outside [1, %d]", k, MGK_MAX_HOPS);
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    if (engine < MGK_ENGINE_AUTO || engine > MGK_ENGINE_LANES) return fail(MGK_ECONTRACT, "unknown engine %d", engine);
+    const Span sp = span_of(k, mode);
+    return count_device_multi(h, d_seeds, nseeds, &sp, 1, engine, d_counts, stream);
+}
+
+int mgk_khop_count_device_ks(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, const uint32_t* ks,
+                             uint32_t nks, int mode, uint64_t* d_counts, void* stream) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (nks && !ks) return fail(MGK_ECONTRACT, "null argument");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    std::vector<Span> spans(nks);
+    for (uint32_t w = 0; w < nks; ++w) {
+        if (ks[w] < 1 || ks[w] > MGK_MAX_HOPS)
+            return fail(MGK_ECONTRACT, "k-hop count %u outside [1, %d]", ks[w], MGK_MAX_HOPS);
+        spans[w] = span_of(ks[w], mode);
+    }
+    if (nks == 0) return MGK_OK;
+    return count_device_multi(h, d_seeds, nseeds, spans.data(), nks, MGK_ENGINE_AUTO, d_counts, stream);
 }
 
 int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {

@@ -187,6 +187,7 @@ struct Launch {
     uint32_t min_hop;       // count hops [min_hop, k]
     uint32_t seed_visited;  // 1 for k_hop_*, 0 for walk_targets
     unsigned long long* d_counts;
+    unsigned long long* d_counts1 = nullptr;  // on-chip k = 2 only: also the k = 1 answers
     cudaStream_t stream;
     Tuning tuning;
     int lanes_words;  // LANES engine only
@@ -213,6 +214,9 @@ cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block
 cudaError_t launch_single(Launch& L);
 // SINGLE, k = 2 counts with the visited sets in shared memory (mgk_k2.cu)
 bool k2_eligible(const Launch& L);
+// would a k = 2 k_hop count of nseeds seeds on g take the on-chip path? (it can
+// then also return the k = 1 answers of the same seeds: Launch::d_counts1)
+bool k2_takes(const Graph* g, uint64_t nseeds, uint32_t min_hop);
 cudaError_t launch_k2(Launch& L);
 cudaError_t launch_lanes(Launch& L);
 // Sorted ids of the last single-seed keep_result run: visited \ (visited

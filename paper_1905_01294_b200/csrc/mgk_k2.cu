@@ -54,6 +54,7 @@ struct K2Params {
     const uint32_t* seeds;  // nullptr: inline_seeds
     uint64_t ns;
     unsigned long long* counts;
+    unsigned long long* counts1;  // optional: the same seeds' k = 1 answers (|F1|)
     uint32_t cumulative;
     uint32_t R;       // vertex slices per seed (CTAs per group)
     uint32_t rbits;   // vertices per slice (multiple of 128)
@@ -572,6 +573,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         const unsigned long long pop = len ? ld_cg(P.acc + i) : 1 + nf;  // |B|
         const unsigned long long ex = pop - 1 - nf;
         P.counts[i] = P.cumulative ? pop - 1 : ex;
+        if (P.counts1) P.counts1[i] = nf;  // k = 1, exact = cumulative
         if (len) P.acc[i] = 0;
         f1s += nf;
         f2s += ex;
@@ -625,6 +627,17 @@ bool k2_eligible(const Launch& L) {
     const uint64_t maxw = ((uint64_t)optin - kK2Fixed) / 4 / 4 * 4;
     const uint64_t nw = L.g->dg.nwords;
     return (nw + maxw - 1) / maxw <= kK2MaxR;
+}
+
+bool k2_takes(const Graph* g, uint64_t nseeds, uint32_t min_hop) {
+    Launch L{};
+    L.g = g;
+    L.nseeds = nseeds;
+    L.k = 2;
+    L.min_hop = min_hop;
+    L.seed_visited = 1;
+    L.tuning = g->tuning;
+    return k2_eligible(L);
 }
 
 cudaError_t launch_k2(Launch& L) {
@@ -719,6 +732,7 @@ cudaError_t launch_k2(Launch& L) {
     Q.g = gr->dg;
     Q.ns = ns;
     Q.counts = L.d_counts;
+    Q.counts1 = L.d_counts1;
     Q.cumulative = L.min_hop <= 1 ? 1u : 0u;
     Q.R = R;
     Q.rbits = rbits;

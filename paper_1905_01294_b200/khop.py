@@ -383,6 +383,16 @@ def k_hop_count_device(graph: DeviceGraph, d_seeds_ptr: int, nseeds: int, k: int
                                             C.c_void_p(stream_ptr)))
 
 
+def k_hop_count_device_sections(graph: DeviceGraph, d_seeds_ptr: int, nseeds: int, ks, mode: int,
+                                d_counts_ptr: int, stream_ptr: int = 0):
+    """Device-resident sections: the answers for ks[j] at d_counts[j * nseeds + i]
+    (uint64), async on stream. A k = 1 section rides on the on-chip k = 2 launch."""
+    ks = np.ascontiguousarray(ks, np.uint32)
+    _check(_lib.lib().mgk_khop_count_device_ks(graph.handle, C.c_void_p(d_seeds_ptr), nseeds, ks.ctypes.data,
+                                               len(ks), int(mode), C.c_void_p(d_counts_ptr),
+                                               C.c_void_p(stream_ptr)))
+
+
 def device_stats(graph: DeviceGraph, stream_ptr: int = 0) -> dict:
     st = MgkStats()
     _check(_lib.lib().mgk_khop_device_stats(graph.handle, C.c_void_p(stream_ptr), C.byref(st)))
@@ -396,5 +406,5 @@ def device_count() -> int:
 __all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "mxm",
            "SEMIRING_BOOL_OR_AND", "SEMIRING_PLUS_TIMES", "SEMIRING_MIN_PLUS", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
-           "k_hop_count_device", "k_hop_count_multi", "k_hop_count_sections", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "k_hop_count_device", "k_hop_count_device_sections", "k_hop_count_multi", "k_hop_count_sections", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]

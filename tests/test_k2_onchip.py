@@ -49,3 +49,29 @@ def test_k2_stats_and_agreement(port):
     cum = k_hop_count_batch(g, seeds, 2, 1)
     one = k_hop_count_batch(g, seeds, 1, 0)
     assert (cum == counts + one).all()
+
+
+def test_sections_share_the_k2_launch():
+    """k = 1 sections answered by the on-chip k = 2 launch (|F1| is part of it):
+    host and device sections agree with separate per-k calls, in any order,
+    with and without other sections, and when the fusion does not apply."""
+    import torch
+    from paper_1905_01294_b200 import k_hop_count_device_sections, k_hop_count_sections
+    rp, ci = H.gen_csr(H.G1)
+    g = DeviceGraph.from_csr(rp, ci)
+    seeds = H.pick_seeds(rp, 700, 4)
+    for mode in (0, 1):
+        ref = {k: k_hop_count_batch(g, seeds, k, mode, engine=ENGINE_SINGLE if k < 3 else 0) for k in (1, 2, 3)}
+        for ks in ([1, 2], [2, 1], [1, 2, 3], [3, 1, 2], [1], [2], [1, 1, 2]):
+            got = k_hop_count_sections(g, seeds, ks, mode)
+            assert all((got[j] == ref[k]).all() for j, k in enumerate(ks)), (mode, ks)
+            d_seeds = torch.from_numpy(seeds.astype(np.int32)).cuda()
+            d_counts = torch.zeros(len(ks) * len(seeds), dtype=torch.int64, device="cuda")
+            k_hop_count_device_sections(g, d_seeds.data_ptr(), len(seeds), ks, mode, d_counts.data_ptr(),
+                                        torch.cuda.current_stream().cuda_stream)
+            torch.cuda.synchronize()
+            dc = d_counts.cpu().numpy().astype(np.uint64).reshape(len(ks), len(seeds))
+            assert all((dc[j] == ref[k]).all() for j, k in enumerate(ks)), ("device", mode, ks)
+    g.set_tuning(Tuning(force_dir=1))  # general engine for k = 2: no fusion, same answers
+    got = k_hop_count_sections(g, seeds, [1, 2], 0)
+    assert (got[0] == k_hop_count_batch(g, seeds, 1, 0)).all() and (got[1] == k_hop_count_batch(g, seeds, 2, 0)).all()
