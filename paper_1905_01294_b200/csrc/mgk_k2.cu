@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "mgk_device.cuh"
 
@@ -617,13 +618,35 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 // Eligible: k = 2 counts with the seed pre-visited (k_hop exact/cumulative),
 // duplicate-free rows, no forced direction, and a bitmap that fits R <= 4
 // slices of shared memory. MGK_NO_K2SMEM=1 keeps every call on fr_kernel.
+// Per-device launch facts, looked up once (the host work between a caller's
+// events and the launch is part of the measured call)
+struct K2Device {
+    int optin = 0, nsm = 0;
+    size_t smem_set = 0;  // dynamic smem the kernel attribute allows
+    size_t occ_smem = 0;  // occupancy cached for this smem size
+    int occ = 0;
+};
+K2Device& k2_device() {
+    static std::mutex mu;
+    static K2Device devs[64];
+    static bool ready[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 63;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!ready[dev]) {
+        cudaDeviceGetAttribute(&devs[dev].optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&devs[dev].nsm, cudaDevAttrMultiProcessorCount, dev);
+        ready[dev] = true;
+    }
+    return devs[dev];
+}
+
 bool k2_eligible(const Launch& L) {
     static const bool off = std::getenv("MGK_NO_K2SMEM") != nullptr;
     if (off || L.k != 2 || !L.seed_visited || L.keep_result || !L.g->dg.rows_unique) return false;
     if (L.tuning.force_dir != 0 || L.nseeds == 0) return false;
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int optin = k2_device().optin;
     const uint64_t maxw = ((uint64_t)optin - kK2Fixed) / 4 / 4 * 4;
     const uint64_t nw = L.g->dg.nwords;
     return (nw + maxw - 1) / maxw <= kK2MaxR;
@@ -644,10 +667,8 @@ cudaError_t launch_k2(Launch& L) {
     const Graph* gr = L.g;
     Workspace* ws = L.ws;
     cudaError_t e;
-    int dev = 0, optin = 0, nsm = 0;
-    if ((e = cudaGetDevice(&dev))) return e;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    K2Device& kd = k2_device();
+    const int optin = kd.optin, nsm = kd.nsm;
     const uint32_t maxw = (uint32_t)(((uint64_t)optin - kK2Fixed) / 4 / 4 * 4);
     const uint32_t nw = gr->dg.nwords;
     const uint32_t R = (nw + maxw - 1) / maxw;
@@ -655,14 +676,18 @@ cudaError_t launch_k2(Launch& L) {
     const uint32_t rbits = (uint32_t)((((uint64_t)gr->dg.n + R - 1) / R + 127) / 128 * 128);
     const uint32_t rwords = rbits / 32;
     const size_t smem = (size_t)rwords * 4 + kK2Fixed;
-    static size_t smem_set = 0;
-    if (smem > smem_set) {
+    if (smem > kd.smem_set) {  // per device (the attribute is per context)
         if ((e = cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
             return e;
-        smem_set = smem;
+        kd.smem_set = smem;
     }
-    int per_sm = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_kernel, kK2Block, smem))) return e;
+    if (kd.occ_smem != smem) {
+        int per_sm = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_kernel, kK2Block, smem))) return e;
+        kd.occ = per_sm;
+        kd.occ_smem = smem;
+    }
+    const int per_sm = kd.occ;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint32_t grid = (uint32_t)(per_sm * nsm) / R * R;
     const uint32_t G = grid / R;
