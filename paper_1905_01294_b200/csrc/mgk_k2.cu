@@ -56,7 +56,8 @@ struct K2Params {
     uint64_t ns;
     unsigned long long* counts;
     unsigned long long* counts1;  // optional: the same seeds' k = 1 answers (|F1|)
-    uint32_t cumulative;
+    uint32_t cumulative;  // window starts at hop 1 (k_hop cumulative; walks [1, 2])
+    uint32_t walk;        // walk_targets: the visited set starts empty (no seed bit; s in F1 if a self loop)
     uint32_t R;       // vertex slices per seed (CTAs per group)
     uint32_t rbits;   // vertices per slice (multiple of 128)
     uint32_t rwords;  // rbits / 32
@@ -87,7 +88,8 @@ struct K2Params {
     uint2* tasks;            // {seed, 256-row block}
     uint64_t taskcap;
     unsigned long long seedcost;  // work-line units charged per seed (its fixed cost)
-    uint32_t snapdiv;  // group boundaries within (group size / snapdiv) of a seed edge move to it
+    uint32_t snapdiv;
+    uint32_t diag;  // MGK_K2_DIAG=1: phase timings in level 0 of the stats  // group boundaries within (group size / snapdiv) of a seed edge move to it
     uint32_t inline_seeds[kK2Inline];
 };
 
@@ -201,7 +203,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             uint32_t nf = 0;
             for (uint32_t j = b + lane; j < b + deg; j += 32) {
                 const uint32_t v = __ldg(g.ci + j);
-                if (v != s) {
+                if (v != s || P.walk) {
                     wsum += __ldg(g.rp + v + 1) - __ldg(g.rp + v);
                     ++nf;
                 }
@@ -243,13 +245,14 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 #pragma unroll
             for (int r = 0; r < (int)(kK2Task / 32); ++r) {
                 const uint32_t j = j0 + lane + 32 * r;
-                const uint32_t d = v[r] != s ? re[r] - rb[r] : 0;
+                const bool in_f1 = v[r] != s || P.walk;
+                const uint32_t d = in_f1 ? re[r] - rb[r] : 0;
                 if (j < deg) {
                     P.f1v[off + j] = v[r];
                     P.f1rb[off + j] = rb[r];
                     P.f1d[off + j] = d;
                     sum += d;
-                    nf += v[r] != s;
+                    nf += in_f1;
                 }
             }
             sum = warp_sum_u64(sum);
@@ -374,7 +377,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
             const uint32_t ow = ld_cg(P.f1win + i);  // meaningful only when off != kNoF1
             const bool v1 = a2 == 0;  // the part holding offset 0 also holds {s} u F1
-            if (v1 && threadIdx.x == 0 && s - rlo < P.rbits) smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
+            if (v1 && !P.walk && threadIdx.x == 0 && s - rlo < P.rbits)
+                smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
             unsigned long long wbase = 0;  // seed-local entry offset of the current window
             uint32_t j0 = 0;
             for (uint32_t k = 0; j0 < deg && wbase < z; j0 += kK2Win, ++k) {
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                         } else {
                             v = __ldg(g.ci + b + j0 + t);
                             rb2[h] = __ldg(g.rp + v);
-                            if (v != s) d2[h] = __ldg(g.rp + v + 1) - rb2[h];
+                            if (v != s || P.walk) d2[h] = __ldg(g.rp + v + 1) - rb2[h];
                         }
                         if (v1 && v - rlo < P.rbits) smem_or(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
                     }
@@ -571,9 +575,10 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     for (uint64_t i = gtid; i < P.ns; i += nthreads) {
         const unsigned long long nf = ld_cg(P.f1 + i);
         const unsigned long long raw = ld_cg(P.w + i), len = raw ? raw + P.seedcost : 0;
-        const unsigned long long pop = len ? ld_cg(P.acc + i) : 1 + nf;  // |B|
-        const unsigned long long ex = pop - 1 - nf;
-        P.counts[i] = P.cumulative ? pop - 1 : ex;
+        // |B| = |{s} u F1 u N(F1)| (walks: |F1 u N(F1)|)
+        const unsigned long long own = P.walk ? 0 : 1, pop = len ? ld_cg(P.acc + i) : own + nf;
+        const unsigned long long ex = pop - own - nf;  // level 2
+        P.counts[i] = P.cumulative ? pop - own : ex;
         if (P.counts1) P.counts1[i] = nf;  // k = 1, exact = cumulative
         if (len) P.acc[i] = 0;
         f1s += nf;
@@ -607,15 +612,18 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         P.lc[0].ns = ld_cg(&P.misc[0]) - t0;                  // phases 0-1
         P.lc[2].ns = ld_cg(&P.misc[2]) - ld_cg(&P.misc[0]);  // slices + merge
         P.lc[MGK_MAX_HOPS + 1].ns = now - ld_cg(&P.misc[2]);
-        P.lc[0].candidates = ld_cg(&P.misc[1]) - ld_cg(&P.misc[0]);  // DIAG: slices alone (ns)
-        P.lc[0].frontier = ld_cg(&P.misc[8]) - t0;                    // DIAG: 0a + barrier
-        P.lc[0].vertices = ld_cg(&P.misc[9]) - ld_cg(&P.misc[8]);     // DIAG: 0b + barrier
+        if (P.diag) {  // MGK_K2_DIAG=1: phase timings (ns) in level 0 (scripts/k2probe.py)
+            P.lc[0].candidates = ld_cg(&P.misc[1]) - ld_cg(&P.misc[0]);  // slices alone
+            P.lc[0].frontier = ld_cg(&P.misc[8]) - t0;                    // phase 0a + barrier
+            P.lc[0].vertices = ld_cg(&P.misc[9]) - ld_cg(&P.misc[8]);     // phase 0b + barrier
+        }
     }
 }
 
 }  // namespace
 
-// Eligible: k = 2 counts with the seed pre-visited (k_hop exact/cumulative),
+// Eligible: k = 2 counts (k_hop exact / cumulative, or walk_targets windows
+// [1, 2] / [2, 2]: the same set with the visited set starting empty),
 // duplicate-free rows, no forced direction, and a bitmap that fits R <= 4
 // slices of shared memory. MGK_NO_K2SMEM=1 keeps every call on fr_kernel.
 // Per-device launch facts, looked up once (the host work between a caller's
@@ -644,7 +652,7 @@ K2Device& k2_device() {
 
 bool k2_eligible(const Launch& L) {
     static const bool off = std::getenv("MGK_NO_K2SMEM") != nullptr;
-    if (off || L.k != 2 || !L.seed_visited || L.keep_result || !L.g->dg.rows_unique) return false;
+    if (off || L.k != 2 || L.min_hop < 1 || L.keep_result || !L.g->dg.rows_unique) return false;
     if (L.tuning.force_dir != 0 || L.nseeds == 0) return false;
     const int optin = k2_device().optin;
     const uint64_t maxw = ((uint64_t)optin - kK2Fixed) / 4 / 4 * 4;
@@ -759,6 +767,7 @@ cudaError_t launch_k2(Launch& L) {
     Q.counts = L.d_counts;
     Q.counts1 = L.d_counts1;
     Q.cumulative = L.min_hop <= 1 ? 1u : 0u;
+    Q.walk = L.seed_visited ? 0u : 1u;
     Q.R = R;
     Q.rbits = rbits;
     Q.rwords = rwords;
@@ -795,6 +804,8 @@ cudaError_t launch_k2(Launch& L) {
         return c ? std::max<unsigned long long>(1, std::strtoull(c, nullptr, 10)) : 8ull;
     }();
     Q.snapdiv = (uint32_t)snapdiv;
+    static const uint32_t diag = std::getenv("MGK_K2_DIAG") != nullptr ? 1u : 0u;
+    Q.diag = diag;
     if (L.host_io && ns <= kK2Inline) {
         Q.seeds = nullptr;
         std::memcpy(Q.inline_seeds, L.h_seeds, (size_t)ns * 4);

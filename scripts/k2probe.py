@@ -1,7 +1,10 @@
 """Timing breakdown of the cfg2 k=2 call (G2, 300 seeds): kernel ms, setup
 (phases 0-1), slices (phase 2), slices + merge, answers; min over 10 calls."""
+import os
 import sys
 from pathlib import Path
+
+os.environ.setdefault("MGK_K2_DIAG", "1")  # phase timings in level 0 of the stats
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch  # noqa: E402

@@ -9,7 +9,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import oracle  # noqa: E402  (the checker)
-from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch  # noqa: E402
+from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch, walk_count_batch  # noqa: E402
 
 port = oracle.Port()
 bad = 0
@@ -25,6 +25,12 @@ def check(rp, ci, seeds, label):
         if got != want:
             bad += 1
             print(label, "mode", mode, "mismatch at", [i for i, (a, b) in enumerate(zip(got, want)) if a != b][:10])
+    for lo in (1, 2):  # walk_targets windows [1, 2] and [2, 2]: nothing pre-visited
+        want = [len(port.walk_targets(rp64, ci64, int(s), lo, 2)) for s in seeds]
+        got = walk_count_batch(g, seeds, lo, 2).tolist()
+        if got != want:
+            bad += 1
+            print(label, "walk", lo, "mismatch at", [i for i, (a, b) in enumerate(zip(got, want)) if a != b][:10])
 
 
 rp, ci = H.gen_csr(H.G1)

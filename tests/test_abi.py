@@ -40,6 +40,23 @@ def test_abi_version_and_no_gpu_is_loud():
         assert "no CUDA device" in _lib.last_error()
 
 
+def test_device_sections_validation_before_device_work():
+    """mgk_khop_count_device_ks checks its arguments before touching the graph."""
+    L = _lib.lib()
+    ks = np.array([1, 2], np.uint32)
+    assert L.mgk_khop_count_device_ks(None, None, 0, ks.ctypes.data, 2, 0, None, None) == _lib.MGK_ECONTRACT
+    assert "null graph" in _lib.last_error()
+    fake = C.c_void_p(8)  # never dereferenced: every case below fails first
+    assert L.mgk_khop_count_device_ks(fake, None, 0, None, 2, 0, None, None) == _lib.MGK_ECONTRACT
+    assert "null argument" in _lib.last_error()
+    assert L.mgk_khop_count_device_ks(fake, None, 0, ks.ctypes.data, 2, 7, None, None) == _lib.MGK_ECONTRACT
+    assert "unknown traverse mode 7" in _lib.last_error()
+    for bad in (0, 33):
+        kb = np.array([1, bad], np.uint32)
+        assert L.mgk_khop_count_device_ks(fake, None, 0, kb.ctypes.data, 2, 0, None, None) == _lib.MGK_ECONTRACT
+        assert f"k-hop count {bad} outside [1, 32]" in _lib.last_error()
+
+
 def test_upload_validation_messages():
     L = _lib.lib()
     h = C.c_void_p()
