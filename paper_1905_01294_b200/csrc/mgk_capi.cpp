@@ -114,6 +114,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->k2_f1v);
     cudaFree(ws->k2_f1rb);
     cudaFree(ws->k2_f1d);
+    cudaFree(ws->k2_f1sp);
     cudaFree(ws->k2_f1win);
     cudaFree(ws->k2_wt);
     cudaFree(ws->k2_tasks);

@@ -659,6 +659,9 @@ void free_device_graph(Graph* g) {
     cudaFree(g->heavy);
     cudaFree(g->perm);
     cudaFree(g->inv);
+    cudaFree(g->k2_split);
+    g->k2_split = nullptr;
+    g->k2_split_bits = g->k2_split_R = 0;
     g->rp = g->ci = g->cp = g->ri = g->no_in = g->pull_skip = nullptr;
     g->heavy = nullptr;
     g->perm = g->inv = nullptr;

@@ -119,6 +119,8 @@ struct Workspace {
     uint32_t* k2_f1v = nullptr;             // [k2_f1cap] F1 rows of the seeds
     uint32_t* k2_f1rb = nullptr;
     uint32_t* k2_f1d = nullptr;
+    uint32_t* k2_f1sp = nullptr;            // [k2_f1cap][R-1] slice splits within each F1 row
+    uint32_t k2_f1sp_R = 0;
     uint64_t k2_f1cap = 0;
     uint32_t* k2_f1win = nullptr;           // [cap] per seed
     unsigned long long* k2_wt = nullptr;    // window totals
@@ -170,6 +172,10 @@ struct Graph {
     uint32_t* perm = nullptr;
     uint32_t* inv = nullptr;
     uint64_t bytes = 0;
+    // on-chip k = 2: per vertex, where its (ascending) row crosses each bitmap
+    // slice boundary ([n][R-1] absolute col_idx positions), built on first use
+    uint32_t* k2_split = nullptr;
+    uint32_t k2_split_bits = 0, k2_split_R = 0;
     Tuning tuning;
     std::mutex mu;
     std::vector<std::unique_ptr<Workspace>> free_ws;

@@ -47,8 +47,9 @@ constexpr uint32_t kK2Inline = 512;
 constexpr uint32_t kK2MaxR = 4;
 constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
 constexpr int kK2Ilp = 16;  // adjacency entries in flight per lane
-// smem besides the bitmap: window prefix (u64) + row begins (u32) + scratch
-constexpr uint32_t kK2Fixed = (kK2Win + 2) * 4 + kK2Win * 4 + kK2Win * 8 + 1024;
+// smem besides the bitmap: the window's slice and combined prefixes, each row's
+// slice start, the row cursors, and scratch
+constexpr uint32_t kK2Fixed = 2 * (kK2Win + 2) * 4 + kK2Win * 4 + kK2Win * 8 + 1024;
 
 struct K2Params {
     DevGraph g;
@@ -82,6 +83,8 @@ struct K2Params {
     uint32_t* f1v;
     uint32_t* f1rb;
     uint32_t* f1d;
+    uint32_t* f1sp;         // [f1cap][R-1] where each F1 row enters slices 1..R-1 (offsets in the row)
+    const uint32_t* split;  // graph: [n][R-1] absolute positions of the same
     uint64_t f1cap;
     unsigned long long* wt;  // window totals
     uint64_t wtcap;
@@ -148,16 +151,36 @@ __device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t b
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + word * 4), "r"(bit));
 }
 
+// Where each row crosses the slice boundaries r * rbits (rows ascend): the
+// CTA holding slice r streams only [split r-1, split r) of every F1 row.
+__global__ void k2_split_kernel(DevGraph g, uint32_t R, uint32_t rbits, uint32_t* out) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
+        const uint32_t b = g.rp[v], e = g.rp[v + 1];
+        for (uint32_t r = 1; r < R; ++r) {
+            const uint32_t bound = r * rbits;
+            uint32_t lo = b, hi = e;  // first position with col >= bound
+            while (lo < hi) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (g.ci[mid] < bound) lo = mid + 1; else hi = mid;
+            }
+            out[(size_t)v * (R - 1) + r - 1] = lo;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
     uint32_t* bm = reinterpret_cast<uint32_t*>(k2_smem);
     // window prefix of the row lengths, relative to the window start (a window's
     // rows are distinct vertices, so its total is <= m < 2^32)
+    // pre: the window's prefix of this slice's row lengths; prec: of the whole
+    // rows (the work line's unit); srow: where each row enters this slice
     uint32_t* pre = reinterpret_cast<uint32_t*>(k2_smem + (size_t)P.rwords * 4);
-    uint32_t* rbeg = pre + kK2Win + 2;
-    // rinfo[t] = {pre[t + 1], rbeg[t] - pre[t]}: one 64-bit load advances a row
-    // cursor (entry x of the window lives at col_idx[x + rinfo[t].y])
-    uint2* rinfo = reinterpret_cast<uint2*>(rbeg + kK2Win);
+    uint32_t* prec = pre + kK2Win + 2;
+    uint32_t* srow = prec + kK2Win + 2;
+    // rinfo[t] = {pre[t + 1], (row start + srow[t]) - pre[t]}: one 64-bit load
+    // advances a row cursor (slice entry x lives at col_idx[x + rinfo[t].y])
+    uint2* rinfo = reinterpret_cast<uint2*>(srow + kK2Win);
     unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(rinfo + kK2Win);  // [32]
     unsigned long long* s_misc = s_warp + 32;                                         // [8]
     const DevGraph& g = P.g;
@@ -229,7 +252,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             const uint4 si = __ldcg(P.sinfo + tk.x);
             const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
             const uint32_t j0 = tk.y * kK2Task;
-            uint32_t v[kK2Task / 32], rb[kK2Task / 32], re[kK2Task / 32];
+            uint32_t v[kK2Task / 32], rb[kK2Task / 32], re[kK2Task / 32], sp1[kK2Task / 32];
 #pragma unroll
             for (int r = 0; r < (int)(kK2Task / 32); ++r) {
                 const uint32_t j = j0 + lane + 32 * r;
@@ -239,6 +262,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             for (int r = 0; r < (int)(kK2Task / 32); ++r) {
                 rb[r] = __ldg(g.rp + v[r]);
                 re[r] = __ldg(g.rp + v[r] + 1);
+                // R = 2 (the usual case): the one split, loaded with the row bounds
+                sp1[r] = P.R == 2 ? __ldg(P.split + v[r]) : 0;
             }
             unsigned long long sum = 0;
             uint32_t nf = 0;
@@ -251,6 +276,12 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     P.f1v[off + j] = v[r];
                     P.f1rb[off + j] = rb[r];
                     P.f1d[off + j] = d;
+                    if (P.R == 2)
+                        P.f1sp[off + j] = in_f1 ? sp1[r] - rb[r] : 0;
+                    else
+                        for (uint32_t q = 0; q + 1 < P.R; ++q)
+                            P.f1sp[(size_t)(off + j) * (P.R - 1) + q] =
+                                in_f1 ? __ldg(P.split + (size_t)v[r] * (P.R - 1) + q) - rb[r] : 0;
                     sum += d;
                     nf += in_f1;
                 }
@@ -390,37 +421,62 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                         continue;
                     }
                 }
-                unsigned long long d2[2];
-                uint32_t rb2[2];
+                // per row: whole length d, this slice's part [sr, sr + lr)
+                uint32_t d2[2], rb2[2], sr2[2], lr2[2];
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const uint32_t t = threadIdx.x * 2 + h;
-                    d2[h] = 0;
-                    rb2[h] = 0;
+                    d2[h] = rb2[h] = sr2[h] = lr2[h] = 0;
                     if (t < wl) {
-                        uint32_t v;
+                        uint32_t v, lo = 0, hi = 0xFFFFFFFFu;
                         if (off != kNoF1) {
                             v = v1 ? ld_cg(P.f1v + off + j0 + t) : 0;
                             rb2[h] = ld_cg(P.f1rb + off + j0 + t);
                             d2[h] = ld_cg(P.f1d + off + j0 + t);
+                            const uint32_t* sp = P.f1sp + (size_t)(off + j0 + t) * (P.R - 1);
+                            if (rr > 0) lo = ld_cg(sp + rr - 1);
+                            if (rr + 1 < P.R) hi = ld_cg(sp + rr);
                         } else {
                             v = __ldg(g.ci + b + j0 + t);
                             rb2[h] = __ldg(g.rp + v);
-                            if (v != s || P.walk) d2[h] = __ldg(g.rp + v + 1) - rb2[h];
+                            if (v != s || P.walk) {
+                                d2[h] = __ldg(g.rp + v + 1) - rb2[h];
+                                const uint32_t* sp = P.split + (size_t)v * (P.R - 1);
+                                if (rr > 0) lo = __ldg(sp + rr - 1) - rb2[h];
+                                if (rr + 1 < P.R) hi = __ldg(sp + rr) - rb2[h];
+                            }
                         }
+                        sr2[h] = min(lo, d2[h]);
+                        lr2[h] = min(hi, d2[h]) - sr2[h];
                         if (v1 && v - rlo < P.rbits) smem_or(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
                     }
                 }
-                unsigned long long ex;
-                const unsigned long long wtot = block_excl_scan(d2[0] + d2[1], &ex, s_warp);
+                // one scan of (whole << 32 | slice): both prefixes (a window's
+                // rows are distinct vertices, so each sum is <= m < 2^32)
+                unsigned long long exp;
+                const unsigned long long tot =
+                    block_excl_scan(((unsigned long long)(d2[0] + d2[1]) << 32) | (lr2[0] + lr2[1]), &exp, s_warp);
+                const unsigned long long wtot = tot >> 32;
                 {
-                    const uint32_t p0 = (uint32_t)ex, p1 = (uint32_t)(ex + d2[0]), p2 = (uint32_t)(ex + d2[0] + d2[1]);
+                    const uint32_t c0 = (uint32_t)(exp >> 32), p0 = (uint32_t)exp;
+                    const uint32_t p1 = p0 + lr2[0], p2 = p1 + lr2[1];
                     const uint32_t t = threadIdx.x * 2;
                     pre[t] = p0;
                     pre[t + 1] = p1;
-                    if (t < wl) rinfo[t] = make_uint2(p1, rb2[0] - p0);
-                    if (t + 1 < wl) rinfo[t + 1] = make_uint2(p2, rb2[1] - p1);
-                    if (threadIdx.x == 0) pre[wl] = (uint32_t)wtot;
+                    prec[t] = c0;
+                    prec[t + 1] = c0 + d2[0];
+                    if (t < wl) {
+                        srow[t] = sr2[0];
+                        rinfo[t] = make_uint2(p1, rb2[0] + sr2[0] - p0);
+                    }
+                    if (t + 1 < wl) {
+                        srow[t + 1] = sr2[1];
+                        rinfo[t + 1] = make_uint2(p2, rb2[1] + sr2[1] - p1);
+                    }
+                    if (threadIdx.x == 0) {
+                        pre[wl] = (uint32_t)tot;
+                        prec[wl] = (uint32_t)wtot;
+                    }
                 }
                 __syncthreads();
                 const unsigned long long x0 = max(a, wbase), x1 = min(z, wbase + wtot);
@@ -431,7 +487,20 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     // are window-relative u32. Full blocks run without bounds
                     // checks; addresses first, then the loads back to back, then
                     // the atomics, so kK2Ilp loads per lane are in flight
-                    const uint32_t X0 = (uint32_t)(x0 - wbase), span = (uint32_t)(x1 - x0);
+                    // the part in whole-row units -> this slice's entries
+                    auto to_slice = [&](uint32_t X) -> uint32_t {
+                        if (X == 0) return 0;
+                        if (X >= (uint32_t)wtot) return pre[wl];
+                        uint32_t lo = 0, hi = wl;  // last row t with prec[t] <= X
+                        while (hi - lo > 1) {
+                            const uint32_t mid = (lo + hi) / 2;
+                            if (prec[mid] <= X) lo = mid; else hi = mid;
+                        }
+                        const uint32_t o = X - prec[lo], sr = srow[lo], lr = pre[lo + 1] - pre[lo];
+                        return pre[lo] + (o <= sr ? 0 : min(o - sr, lr));
+                    };
+                    const uint32_t X0 = to_slice((uint32_t)(x0 - wbase)), X1 = to_slice((uint32_t)(x1 - wbase));
+                    const uint32_t span = X1 - X0;
                     const uint32_t xs = X0 + (uint32_t)((unsigned long long)span * wib / kK2Warps);
                     const uint32_t xe = X0 + (uint32_t)((unsigned long long)span * (wib + 1) / kK2Warps);
                     if (xs < xe) {
@@ -737,6 +806,21 @@ cudaError_t launch_k2(Launch& L) {
         ws->k2_stage_bytes = stage;
         ws->bytes += stage;
     }
+    if (R > 1 && (!gr->k2_split || gr->k2_split_bits != rbits || gr->k2_split_R != R)) {
+        // slice crossings of every row, once per graph (the first on-chip call)
+        Graph* gm = const_cast<Graph*>(gr);
+        std::lock_guard<std::mutex> lk(gm->mu);
+        if (!gm->k2_split || gm->k2_split_bits != rbits || gm->k2_split_R != R) {
+            cudaFree(gm->k2_split);
+            gm->k2_split = nullptr;
+            if ((e = cudaMalloc(&gm->k2_split, (size_t)gm->dg.n * (R - 1) * 4))) return e;
+            k2_split_kernel<<<nsm * 8, 256, 0, L.stream>>>(gm->dg, R, rbits, gm->k2_split);
+            if ((e = cudaStreamSynchronize(L.stream))) return e;
+            gm->k2_split_bits = rbits;
+            gm->k2_split_R = R;
+            gm->bytes += (size_t)gm->dg.n * (R - 1) * 4;
+        }
+    }
     if (!ws->k2_f1v) {  // F1 rows of a call's seeds: up to min(m + 1024, 8M) entries
         uint64_t cap = std::min<uint64_t>(gr->dg.m + 1024, 8ull << 20);
         if (const char* c = std::getenv("MGK_K2_F1CAP")) cap = std::max<uint64_t>(1, std::strtoull(c, nullptr, 10));
@@ -744,7 +828,15 @@ cudaError_t launch_k2(Launch& L) {
         if ((e = cudaMalloc(&ws->k2_f1rb, cap * 4))) return e;
         if ((e = cudaMalloc(&ws->k2_f1d, cap * 4))) return e;
         ws->k2_f1cap = cap;
+        ws->k2_f1sp_R = 0;
         ws->bytes += cap * 12;
+    }
+    if (R > 1 && ws->k2_f1sp_R < R) {
+        cudaFree(ws->k2_f1sp);
+        ws->k2_f1sp = nullptr;
+        if ((e = cudaMalloc(&ws->k2_f1sp, (size_t)ws->k2_f1cap * (R - 1) * 4))) return e;
+        ws->k2_f1sp_R = R;
+        ws->bytes += (size_t)ws->k2_f1cap * (R - 1) * 4;
     }
     if (ws->k2_groups < G) {
         cudaFree(ws->k2_bounds);
@@ -787,6 +879,8 @@ cudaError_t launch_k2(Launch& L) {
     Q.f1v = ws->k2_f1v;
     Q.f1rb = ws->k2_f1rb;
     Q.f1d = ws->k2_f1d;
+    Q.f1sp = ws->k2_f1sp;
+    Q.split = gr->k2_split;
     Q.f1cap = ws->k2_f1cap;
     Q.wt = ws->k2_wt;
     Q.wtcap = ws->k2_wtcap;
