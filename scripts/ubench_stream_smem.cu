@@ -93,6 +93,12 @@ int main(int argc, char** argv) {
     // "CSR rows": runs of 2048 sorted ids (a row of degree 2048 over N ids)
     for (uint64_t i = 0; i < n; i += 2048) std::sort(h.begin() + i, h.begin() + std::min(n, i + 2048));
     cudaMemcpy(d_sorted, h.data(), n * 4, cudaMemcpyHostToDevice);
+    // every id in the CTA's slice (each read ends in an atomic): ids mod half, sorted runs
+    uint32_t* d_inrange;
+    if (cudaMalloc(&d_inrange, n * 4)) return 1;
+    for (auto& x : h) x %= half;
+    for (uint64_t i = 0; i < n; i += 2048) std::sort(h.begin() + i, h.begin() + std::min(n, i + 2048));
+    cudaMemcpy(d_inrange, h.data(), n * 4, cudaMemcpyHostToDevice);
     const uint32_t nbits = half;
     run<8, 0>("loads only (random)", d_rand, n, nbits, 0, half, sink);
     run<8, 1>("loads+atoms random R=2", d_rand, n, nbits, 0, half, sink);
@@ -102,5 +108,7 @@ int main(int argc, char** argv) {
     run<16, 1>("loads+atoms random R=2", d_rand, n, nbits, 0, half, sink);
     run<16, 1>("loads+atoms rows R=2", d_sorted, n, nbits, 0, half, sink);
     run<4, 1>("loads+atoms random R=2", d_rand, n, nbits, 0, half, sink);
+    run<16, 1>("loads+atoms rows all-kept", d_inrange, n, nbits, 0, half, sink);
+    run<8, 1>("loads+atoms rows all-kept", d_inrange, n, nbits, 0, half, sink);
     return 0;
 }
