@@ -125,7 +125,7 @@ struct Workspace {
     uint32_t* k2_f1win = nullptr;           // [cap] per seed
     unsigned long long* k2_wt = nullptr;    // window totals
     uint64_t k2_wtcap = 0;
-    uint2* k2_tasks = nullptr;              // phase-0 tasks
+    uint4* k2_tasks = nullptr;              // phase-0 tasks
     uint64_t k2_taskcap = 0;
     // lanes engine (allocated lazily for the widest W used)
     int lanes_words = 0;

@@ -88,7 +88,7 @@ struct K2Params {
     uint64_t f1cap;
     unsigned long long* wt;  // window totals
     uint64_t wtcap;
-    uint2* tasks;            // {seed, 256-row block}
+    uint4* tasks;            // {seed, CSR position of the block, output position, window total slot}
     uint64_t taskcap;
     unsigned long long seedcost;  // work-line units charged per seed (its fixed cost)
     uint32_t snapdiv;
@@ -212,7 +212,9 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
         ot = __shfl_sync(kFull, ot, 0);
         const bool ok = off + deg <= P.f1cap && ow + nwin <= P.wtcap && ot + nt <= P.taskcap;
         for (uint32_t q = lane; q < nt; q += 32)
-            if (ot + q < P.taskcap) P.tasks[ot + q] = make_uint2(ok ? (uint32_t)i : kNoF1, q);
+            if (ot + q < P.taskcap)
+                P.tasks[ot + q] = make_uint4(ok ? (uint32_t)i : kNoF1, b + q * kK2Task, (uint32_t)off + q * kK2Task,
+                                             (uint32_t)ow + q * kK2Task / kK2Win);
         if (lane == 0) P.sinfo[i] = make_uint4(s, b, deg, ok ? (uint32_t)off : kNoF1);
         if (ok) {
             for (uint32_t q = lane; q < nwin; q += 32) P.wt[ow + q] = 0;
@@ -247,17 +249,20 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     {
         const uint64_t ntask = min(ld_cg(&P.misc[7]), (unsigned long long)P.taskcap);
         for (uint64_t t = gwarp; t < ntask; t += nwarps) {
-            const uint2 tk = __ldcg(P.tasks + t);
+            const uint4 tk = __ldcg(P.tasks + t);
             if (tk.x == kNoF1) continue;
-            const uint4 si = __ldcg(P.sinfo + tk.x);
-            const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
-            const uint32_t j0 = tk.y * kK2Task;
+            // the block's entries and the seed's record load together (the
+            // entries are clamped to col_idx and masked once deg is known)
             uint32_t v[kK2Task / 32], rb[kK2Task / 32], re[kK2Task / 32], sp1[kK2Task / 32];
 #pragma unroll
-            for (int r = 0; r < (int)(kK2Task / 32); ++r) {
-                const uint32_t j = j0 + lane + 32 * r;
-                v[r] = j < deg ? __ldg(g.ci + b + j) : s;
-            }
+            for (int r = 0; r < (int)(kK2Task / 32); ++r)
+                v[r] = __ldg(g.ci + min((unsigned long long)tk.y + lane + 32 * r, (unsigned long long)g.m - 1));
+            const uint4 si = __ldcg(P.sinfo + tk.x);
+            const uint32_t s = si.x, b = si.y, deg = si.z;
+            const uint32_t j0 = tk.y - b, off = tk.z - j0;
+#pragma unroll
+            for (int r = 0; r < (int)(kK2Task / 32); ++r)
+                if (j0 + lane + 32 * r >= deg) v[r] = s;
 #pragma unroll
             for (int r = 0; r < (int)(kK2Task / 32); ++r) {
                 rb[r] = __ldg(g.rp + v[r]);
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             if (lane == 0) {
                 if (sum) {
                     atomicAdd(&P.w[tk.x], sum);
-                    atomicAdd(&P.wt[ld_cg(P.f1win + tk.x) + j0 / kK2Win], sum);
+                    atomicAdd(&P.wt[tk.w], sum);
                 }
                 if (nf) atomicAdd(&P.f1[tk.x], nf);
             }
@@ -791,11 +796,11 @@ cudaError_t launch_k2(Launch& L) {
         if ((e = cudaMalloc(&ws->k2_sinfo, cap * 16))) return e;
         if ((e = cudaMalloc(&ws->k2_f1win, cap * 4))) return e;
         if ((e = cudaMalloc(&ws->k2_wt, ws->k2_wtcap * 8))) return e;
-        if ((e = cudaMalloc(&ws->k2_tasks, ws->k2_taskcap * 8))) return e;
+        if ((e = cudaMalloc(&ws->k2_tasks, ws->k2_taskcap * 16))) return e;
         if ((e = cudaMemset(ws->k2_acc, 0, cap * 8))) return e;
         if ((e = cudaStreamSynchronize(0))) return e;  // zero state before the first launch
         ws->k2_cap = cap;
-        ws->bytes += cap * 28 + 8 + ws->k2_wtcap * 8 + ws->k2_taskcap * 8;
+        ws->bytes += cap * 28 + 8 + ws->k2_wtcap * 8 + ws->k2_taskcap * 16;
     }
     const size_t stage = (size_t)G * 2 * R * rwords * 4;
     if (ws->k2_stage_bytes < stage) {
