@@ -39,9 +39,9 @@ namespace {
 
 using namespace dev;
 
-constexpr int kK2Block = 1024;
+constexpr int kK2Block = 768;  // 80 registers, no spills (1024 threads spilled at 64)
 constexpr int kK2Warps = kK2Block / 32;
-constexpr uint32_t kK2Win = 2048;   // F1 rows per prefix window (2 per thread)
+constexpr uint32_t kK2Win = 2 * kK2Block;  // F1 rows per prefix window (2 per thread)
 constexpr uint32_t kK2Task = 256;   // F1 rows per phase-0 task (8 per lane)
 constexpr uint32_t kK2Inline = 512;
 constexpr uint32_t kK2MaxR = 4;

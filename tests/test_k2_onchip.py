@@ -36,7 +36,7 @@ def test_k2_stats_and_agreement(port):
     g = DeviceGraph.from_csr(rp, ci)
     seeds = H.pick_seeds(rp, 2000, 3)  # several seeds per group
     counts, st = k_hop_count_batch(g, seeds, 2, 0, stats=True)
-    assert st["launches"] == 1 and st["block"] == 1024
+    assert st["launches"] == 1 and st["path"] == "smem_k2"
     assert st["levels"][2]["frontier"] == int(counts.sum())
     rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
     e = sum(port.khop_work(rp64, ci64, int(s), 2)[0] for s in seeds)
