@@ -49,7 +49,8 @@ constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
 constexpr int kK2Ilp = 16;  // adjacency entries in flight per lane
 // smem besides the bitmap: the window's slice and combined prefixes, each row's
 // slice start, the row cursors, and scratch
-constexpr uint32_t kK2Fixed = 2 * (kK2Win + 2) * 4 + kK2Win * 4 + kK2Win * 8 + 1024;
+constexpr uint32_t kK2Stg = 512;  // rows of the next seed's first window staged during a sweep
+constexpr uint32_t kK2Fixed = 2 * (kK2Win + 2) * 4 + kK2Win * 4 + kK2Win * 8 + 4 * kK2Stg * 4 + 1024;
 
 struct K2Params {
     DevGraph g;
@@ -147,6 +148,16 @@ __device__ __forceinline__ void ld_rinfo(uint32_t base, uint32_t t, uint32_t& nx
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nxt), "=r"(dl) : "r"(base + t * 8));
 }
 
+// asynchronous global -> shared copies (nothing held in registers meanwhile)
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t bit) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + word * 4), "r"(bit));
 }
@@ -181,7 +192,9 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     // rinfo[t] = {pre[t + 1], (row start + srow[t]) - pre[t]}: one 64-bit load
     // advances a row cursor (slice entry x lives at col_idx[x + rinfo[t].y])
     uint2* rinfo = reinterpret_cast<uint2*>(srow + kK2Win);
-    unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(rinfo + kK2Win);  // [32]
+    // the next seed's first window, copied in (cp.async) during this seed's sweep
+    uint32_t* stg = reinterpret_cast<uint32_t*>(rinfo + kK2Win);  // [4][kK2Stg]: rb, d, split, v
+    unsigned long long* s_warp = reinterpret_cast<unsigned long long*>(stg + 4 * kK2Stg);  // [32]
     unsigned long long* s_misc = s_warp + 32;                                         // [8]
     const DevGraph& g = P.g;
     const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
@@ -397,26 +410,53 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     const unsigned long long glo = W ? s_misc[0] : 0, ghi = W ? s_misc[1] : 0;
     const uint64_t ifirst = s_misc[2];
     unsigned long long wnext = s_misc[3];  // work-line start of seed ifirst
+    // seed records {sinfo, w, f1win} prefetched into slots (i & 1), and the
+    // next seed's first window staged during this seed's sweep
+    unsigned long long* s_rec = s_misc + 8;  // [2][4]
+    uint64_t rec_i = ~0ull;                  // seed whose record is in slot rec_i & 1
+    bool staged = false;                     // seed rec_i's first window is in stg
     if (glo < ghi) {
         for (uint64_t i = ifirst; i < P.ns; ++i) {
-            const unsigned long long v0 = ld_cg(P.w + i);
+            unsigned long long v0;
+            uint4 si;
+            uint32_t ow;
+            if (i == rec_i) {
+                const unsigned long long* r = s_rec + (i & 1) * 4;
+                const uint2 x0 = *reinterpret_cast<const uint2*>(r), x1 = *reinterpret_cast<const uint2*>(r + 1);
+                si = make_uint4(x0.x, x0.y, x1.x, x1.y);
+                v0 = r[2];
+                ow = (uint32_t)r[3];
+            } else {
+                v0 = ld_cg(P.w + i);
+                si = __ldcg(P.sinfo + i);
+                ow = ld_cg(P.f1win + i);  // meaningful only when si.w != kNoF1
+                staged = false;
+            }
             const unsigned long long ws = wnext, we = ws + (v0 ? v0 + P.seedcost : 0);
             wnext = we;
             if (ws >= ghi) break;
             if (we == ws) continue;
+            const bool have_next = i + 1 < P.ns && we < ghi;
+            if (have_next && threadIdx.x == 0) {  // the next record, into the other slot
+                const uint32_t d = (uint32_t)__cvta_generic_to_shared(s_rec + ((i + 1) & 1) * 4);
+                cp_async8(d, P.sinfo + i + 1);
+                cp_async8(d + 8, reinterpret_cast<const char*>(P.sinfo + i + 1) + 8);
+                cp_async8(d + 16, P.w + i + 1);
+                cp_async4(d + 24, P.f1win + i + 1);
+                cp_async_commit();
+            }
             // this group's part of the seed: on the work line, then in adjacency
             // entries (the first seedcost units of a seed carry no entries)
             const unsigned long long a2 = max(glo, ws) - ws, z2 = min(ghi, we) - ws;
             const unsigned long long a = a2 > P.seedcost ? a2 - P.seedcost : 0;
             const unsigned long long z = z2 > P.seedcost ? z2 - P.seedcost : 0;
-            const uint4 si = __ldcg(P.sinfo + i);
             const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
-            const uint32_t ow = ld_cg(P.f1win + i);  // meaningful only when off != kNoF1
             const bool v1 = a2 == 0;  // the part holding offset 0 also holds {s} u F1
             if (v1 && !P.walk && threadIdx.x == 0 && s - rlo < P.rbits)
                 smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
             unsigned long long wbase = 0;  // seed-local entry offset of the current window
             uint32_t j0 = 0;
+            if (staged) cp_async_wait_all();  // this thread's staged rows
             for (uint32_t k = 0; j0 < deg && wbase < z; j0 += kK2Win, ++k) {
                 const uint32_t wl = min(kK2Win, deg - j0);
                 if (off != kNoF1 && !v1) {
@@ -434,7 +474,15 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     d2[h] = rb2[h] = sr2[h] = lr2[h] = 0;
                     if (t < wl) {
                         uint32_t v, lo = 0, hi = 0xFFFFFFFFu;
-                        if (off != kNoF1) {
+                        if (k == 0 && staged) {  // copied in during the last sweep (this thread's rows)
+                            v = stg[3 * kK2Stg + t];
+                            rb2[h] = stg[t];
+                            d2[h] = stg[kK2Stg + t];
+                            if (P.R == 2) {
+                                if (rr > 0) lo = stg[2 * kK2Stg + t];
+                                else hi = stg[2 * kK2Stg + t];
+                            }
+                        } else if (off != kNoF1) {
                             v = v1 ? ld_cg(P.f1v + off + j0 + t) : 0;
                             rb2[h] = ld_cg(P.f1rb + off + j0 + t);
                             d2[h] = ld_cg(P.f1d + off + j0 + t);
@@ -569,7 +617,33 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     const uint32_t v = (off != kNoF1 ? ld_cg(P.f1v + off + j) : __ldg(g.ci + b + j)) - rlo;
                     if (v < P.rbits) smem_or(bm_base, v >> 5, 1u << (v & 31));
                 }
+            if (have_next && threadIdx.x == 0) cp_async_wait_all();  // the next record
             __syncthreads();
+            // the next seed's first window starts copying in now (it starts in
+            // this group: its work-line start is this seed's end)
+            staged = false;
+            if (have_next) {
+                const unsigned long long* r = s_rec + ((i + 1) & 1) * 4;
+                const uint2 x1 = *reinterpret_cast<const uint2*>(r + 1);
+                const uint32_t noff = x1.y, ndeg = x1.x;
+                if (r[2] != 0 && noff != kNoF1 && P.R <= 2 && ndeg <= kK2Stg) {
+                    const uint32_t wl = ndeg;
+                    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(stg);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t t = threadIdx.x * 2 + h;
+                        if (t < wl) {
+                            cp_async4(sb + t * 4, P.f1rb + noff + t);
+                            cp_async4(sb + (kK2Stg + t) * 4, P.f1d + noff + t);
+                            if (P.R == 2) cp_async4(sb + (2 * kK2Stg + t) * 4, P.f1sp + noff + t);
+                            cp_async4(sb + (3 * kK2Stg + t) * 4, P.f1v + noff + t);
+                        }
+                    }
+                    cp_async_commit();
+                    staged = true;
+                }
+                rec_i = i + 1;
+            }
             // the slice is complete: popcount it (whole seed) or stage it (cut seed)
             const bool whole = ws >= glo && we <= ghi;
             uint4* bm4 = reinterpret_cast<uint4*>(bm);
