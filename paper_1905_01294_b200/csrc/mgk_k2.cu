@@ -44,7 +44,7 @@ constexpr int kK2Warps = kK2Block / 32;
 constexpr uint32_t kK2Win = 2 * kK2Block;  // F1 rows per prefix window (2 per thread)
 constexpr uint32_t kK2Task = 256;   // F1 rows per phase-0 task (8 per lane)
 constexpr uint32_t kK2Inline = 512;
-constexpr uint32_t kK2MaxR = 4;
+constexpr uint32_t kK2MaxR = 64;  // slices per seed (G4: 26, so 5 groups)
 constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
 constexpr int kK2Ilp = 16;  // adjacency entries in flight per lane
 // smem besides the bitmap: the window's slice and combined prefixes, each row's
@@ -294,12 +294,9 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     P.f1v[off + j] = v[r];
                     P.f1rb[off + j] = rb[r];
                     P.f1d[off + j] = d;
-                    if (P.R == 2)
-                        P.f1sp[off + j] = in_f1 ? sp1[r] - rb[r] : 0;
-                    else
-                        for (uint32_t q = 0; q + 1 < P.R; ++q)
-                            P.f1sp[(size_t)(off + j) * (P.R - 1) + q] =
-                                in_f1 ? __ldg(P.split + (size_t)v[r] * (P.R - 1) + q) - rb[r] : 0;
+                    // R = 2: the one split per row; R > 2 reads the graph's
+                    // split array in phase 2 (R - 1 words per row would not pay)
+                    if (P.R == 2) P.f1sp[off + j] = in_f1 ? sp1[r] - rb[r] : 0;
                     sum += d;
                     nf += in_f1;
                 }
@@ -483,12 +480,17 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                                 else hi = stg[2 * kK2Stg + t];
                             }
                         } else if (off != kNoF1) {
-                            v = v1 ? ld_cg(P.f1v + off + j0 + t) : 0;
+                            v = (v1 || P.R > 2) ? ld_cg(P.f1v + off + j0 + t) : 0;
                             rb2[h] = ld_cg(P.f1rb + off + j0 + t);
                             d2[h] = ld_cg(P.f1d + off + j0 + t);
-                            const uint32_t* sp = P.f1sp + (size_t)(off + j0 + t) * (P.R - 1);
-                            if (rr > 0) lo = ld_cg(sp + rr - 1);
-                            if (rr + 1 < P.R) hi = ld_cg(sp + rr);
+                            if (P.R == 2) {
+                                const uint32_t sp = ld_cg(P.f1sp + off + j0 + t);
+                                if (rr > 0) lo = sp; else hi = sp;
+                            } else if (P.R > 2 && d2[h]) {  // this slice's crossings of row v
+                                const uint32_t* sp = P.split + (size_t)v * (P.R - 1);
+                                if (rr > 0) lo = __ldg(sp + rr - 1) - rb2[h];
+                                if (rr + 1 < P.R) hi = __ldg(sp + rr) - rb2[h];
+                            }
                         } else {
                             v = __ldg(g.ci + b + j0 + t);
                             rb2[h] = __ldg(g.rp + v);
@@ -798,12 +800,23 @@ K2Device& k2_device() {
     return devs[dev];
 }
 
+// bitmap words one CTA can hold (MGK_K2_SLICE_WORDS caps it, for tests of many slices)
+uint32_t k2_max_words(int optin) {
+    static const long cap = [] {
+        const char* c = std::getenv("MGK_K2_SLICE_WORDS");
+        return c ? std::atol(c) : 0L;
+    }();
+    uint32_t w = (uint32_t)(((uint64_t)optin - kK2Fixed) / 4 / 4 * 4);
+    if (cap >= 4 && (uint32_t)cap < w) w = (uint32_t)cap / 4 * 4;
+    return w;
+}
+
 bool k2_eligible(const Launch& L) {
     static const bool off = std::getenv("MGK_NO_K2SMEM") != nullptr;
     if (off || L.k != 2 || L.min_hop < 1 || L.keep_result || !L.g->dg.rows_unique) return false;
     if (L.tuning.force_dir != 0 || L.nseeds == 0) return false;
     const int optin = k2_device().optin;
-    const uint64_t maxw = ((uint64_t)optin - kK2Fixed) / 4 / 4 * 4;
+    const uint64_t maxw = k2_max_words(optin);
     const uint64_t nw = L.g->dg.nwords;
     return (nw + maxw - 1) / maxw <= kK2MaxR;
 }
@@ -825,7 +838,7 @@ cudaError_t launch_k2(Launch& L) {
     cudaError_t e;
     K2Device& kd = k2_device();
     const int optin = kd.optin, nsm = kd.nsm;
-    const uint32_t maxw = (uint32_t)(((uint64_t)optin - kK2Fixed) / 4 / 4 * 4);
+    const uint32_t maxw = k2_max_words(optin);
     const uint32_t nw = gr->dg.nwords;
     const uint32_t R = (nw + maxw - 1) / maxw;
     // slices of equal size, 128 vertices (4 x uint4 words) aligned
@@ -910,12 +923,12 @@ cudaError_t launch_k2(Launch& L) {
         ws->k2_f1sp_R = 0;
         ws->bytes += cap * 12;
     }
-    if (R > 1 && ws->k2_f1sp_R < R) {
+    if (R == 2 && ws->k2_f1sp_R < 2) {
         cudaFree(ws->k2_f1sp);
         ws->k2_f1sp = nullptr;
-        if ((e = cudaMalloc(&ws->k2_f1sp, (size_t)ws->k2_f1cap * (R - 1) * 4))) return e;
-        ws->k2_f1sp_R = R;
-        ws->bytes += (size_t)ws->k2_f1cap * (R - 1) * 4;
+        if ((e = cudaMalloc(&ws->k2_f1sp, (size_t)ws->k2_f1cap * 4))) return e;
+        ws->k2_f1sp_R = 2;
+        ws->bytes += (size_t)ws->k2_f1cap * 4;
     }
     if (ws->k2_groups < G) {
         cudaFree(ws->k2_bounds);

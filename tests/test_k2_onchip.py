@@ -23,8 +23,11 @@ WORKER = Path(__file__).resolve().parent / "helpers" / "k2_worker.py"
     {"MGK_K2_SEEDCOST": "100000000"},                  # one seed per group at most
     {"MGK_K2_SNAP": "1"},                              # boundaries snap to seed edges a whole group away
     {"MGK_K2_SNAP": "1000000", "MGK_K2_SEEDCOST": "0"},  # (almost) no snapping
+    {"MGK_K2_SLICE_WORDS": "256"},                     # G1 in 8 slices (the split array path, R > 2)
+    {"MGK_K2_SLICE_WORDS": "1024", "MGK_K2_SEEDCOST": "0"},  # G1 in 2 slices
     {"MGK_NO_K2SMEM": "1"},                            # the L2-bitmap engine (fr_kernel)
-], ids=["default", "cost0", "f1cap", "cost_huge", "snap_wide", "snap_none", "no_onchip"])
+], ids=["default", "cost0", "f1cap", "cost_huge", "snap_wide", "snap_none", "r8", "r2",
+                      "no_onchip"])
 def test_k2_paths_against_oracle(env):
     p = subprocess.run([sys.executable, str(WORKER)], env={**os.environ, **env}, capture_output=True,
                        text=True, timeout=900)
