@@ -984,7 +984,10 @@ cudaError_t launch_k2(Launch& L) {
     }();
     // a seed's fixed cost in adjacency-entry units: its slice sweep (~rwords)
     // plus the per-seed setup (measured on G2: ~60K entries-equivalent)
-    Q.seedcost = seedcost ? seedcost : 24576ull + rwords;
+    // per slice CTA a seed costs ~12K cycles of setup plus its slice sweep; in
+    // whole-row entry units (a CTA streams 1/R of a seed's entries) that is
+    // R x (12288 + rwords / 2): G2 (R = 2) ~62K, G4 (R = 26) ~870K, measured
+    Q.seedcost = seedcost ? seedcost : (unsigned long long)R * (12288ull + rwords / 2);
     static const unsigned long long snapdiv = [] {
         const char* c = std::getenv("MGK_K2_SNAP");
         return c ? std::max<unsigned long long>(1, std::strtoull(c, nullptr, 10)) : 8ull;
