@@ -4,29 +4,32 @@
 // proj/core/src/execute.cpp:347-375) the answer of seed s is a set size:
 //   B(s) = {s} u F1 u N(F1),  F1 = row(s) \ {s}
 //   exact |F2| = |B| - 1 - |F1|,  cumulative |F1 u F2| = |B| - 1
-// (the masked vxm of hop 2, sparse.cpp:253-290, unioned with visited). The
-// general engine (mgk_ss.cu) builds B in a per-seed bitmap in L2 with one
-// fire-and-forget red.or per adjacency entry, which runs at the L2 atomic
-// ceiling (~200 G/s on this B200), and then popcounts and clears the bitmaps.
-// Shared-memory atomics on a random word run at ~777 G/s over the chip
-// (scripts/ubench_smem.cu; DSMEM atomics across a cluster only at ~185 G/s),
-// so here B lives on chip: the vertex range is split into R slices of at most
-// ~200 KB of bits, and R CTAs ("a group") hold one slice of one seed's B each.
+// (the masked vxm of hop 2, sparse.cpp:253-290, unioned with visited);
+// walk_targets windows [1, 2] / [2, 2] are the same set without the seed bit
+// (execute.cpp:43-60). The general engine (mgk_ss.cu) builds B in a per-seed
+// bitmap in L2 with one red.or per adjacency entry, at the L2 atomic ceiling
+// (~200 G/s on this B200). Shared-memory atomics on a random word run at
+// ~777 G/s over the chip (scripts/ubench_smem.cu; DSMEM atomics across a
+// cluster only at ~185 G/s), so here B lives on chip: the vertex range is cut
+// into R slices of at most ~175 KB of bits, and R CTAs ("a group", one
+// 768-thread CTA per SM) hold one slice of one seed's B each. Rows ascend, so
+// a per-vertex array of slice crossings lets each CTA stream only its part of
+// every F1 row: each adjacency entry is read once, by the CTA owning its
+// target.
 //
-// One persistent cooperative launch, four phases separated by grid barriers:
-//   0. warp per seed: |F1| and the hop-2 work w(s) = sum of deg(F1)
-//   1. CTA 0: exclusive scan of w over the seeds (the "work line")
-//   2. group g takes the g-th equal slice of the work line: for every seed
-//      segment in it, the R CTAs of the group stream that part of the F1 rows
-//      (the same adjacency entries; each keeps the targets in its vertex range)
-//      and set bits with shared-memory atomics; a seed wholly inside the
-//      group is popcounted on chip, a seed cut by a group boundary writes its
-//      slice of B to a staging area (coalesced)
-//   3. cut seeds: OR of their staged slices, popcounted by all CTAs
-//   4. answers (and the per-seed accumulators back to zero)
-// Nothing in global memory is touched per adjacency entry except the entry
-// itself; the adjacency is streamed once from HBM (the R CTAs of a group read
-// the same lines close together, the repeats hit L2).
+// One persistent cooperative launch:
+//   0a. warp per seed: reserve its F1 rows, window totals and 256-row tasks
+//   0b. tasks: each F1 row's vertex, row begin, length and slice crossings;
+//       per seed w(s) = sum of deg(F1)                            (barrier)
+//   1. every CTA: the "work line" (w + a per-seed cost, scanned) and its
+//      group's equal slice of it; boundaries near a seed edge snap to it
+//   2. per seed part: window prefixes in shared memory, a flat entry stream
+//      per warp (16 loads in flight per lane), red.shared.or into the slice;
+//      a whole seed is popcounted on chip, a seed cut by a group boundary
+//      stages its slice (coalesced); the next seed's record and first window
+//      arrive by cp.async during the sweep                         (barrier)
+//   3. cut seeds: OR of their staged slices, popcounted by all CTAs (barrier)
+//   4. answers (+ the k = 1 answers of a fused section), accumulators reset
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
