@@ -81,7 +81,7 @@ struct K2Params {
     uint4* cuts;                 // [ngroups] {seed, first group, last group, 0} of the cut seeds
     // the seeds' F1 rows (phase 0): vertex, CSR row begin, length (0 for the
     // seed itself); per seed its first row (kNoF1: scratch ran out) and its
-    // first 2048-row window total
+    // first window total (windows of kK2Win rows)
     uint4* sinfo;     // [ns] {device seed id, CSR row begin, degree, first F1 row or kNoF1}
     uint32_t* f1win;  // [ns]
     uint32_t* f1v;
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     }
                 }
                 wbase += wtot;
-                __syncthreads();  // pre / rbeg are rewritten by the next window
+                __syncthreads();  // pre / prec / srow / rinfo are rewritten by the next window
             }
             if (v1)  // F1 rows in windows the loop did not reach
                 for (uint32_t j = j0 + threadIdx.x; j < deg; j += kK2Block) {
