@@ -61,21 +61,40 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 // with cudaLaunchCooperativeKernel (which guarantees it) and size the grid
 // from the occupancy calculator; MGK_NONCOOP=1 uses a plain launch of the
 // same grid so profilers that skip cooperative launches still see the kernel.
-// The fences on both sides order all memory traffic of the phase and drop
-// stale L1 lines (gpu-scope fence), like cooperative_groups grid.sync().
+// Each CTA reads the generation once per launch (grid_barrier_init, before its
+// first arrival, so no barrier can complete before the read); a barrier is
+// then one release-add per CTA and an acquire spin on the generation — the
+// release / acquire pair orders every thread's memory traffic of the phase
+// (through the CTA barriers on both sides), like cooperative_groups grid.sync().
+static __shared__ unsigned int s_bar_gen;
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void grid_barrier_init(unsigned int* bar) {
+    if (threadIdx.x == 0) s_bar_gen = ld_acquire_gpu(bar + 1);
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned int gen = *reinterpret_cast<volatile unsigned int*>(bar + 1);
-        __threadfence();
-        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-            *reinterpret_cast<volatile unsigned int*>(bar) = 0;
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
+        const unsigned int gen = s_bar_gen;
+        unsigned int old;
+        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
+            // an acquire here too: the last arriver's SM must also drop stale
+            // L1 lines before the next phase reads what other SMs wrote
+            (void)ld_acquire_gpu(bar + 1);
         } else {
-            while (*reinterpret_cast<volatile unsigned int*>(bar + 1) == gen) __nanosleep(20);
+            while (ld_acquire_gpu(bar + 1) == gen) {
+            }
         }
-        __threadfence();
+        s_bar_gen = gen + 1;
     }
     __syncthreads();
 }

@@ -184,6 +184,7 @@ __global__ void k2_split_kernel(DevGraph g, uint32_t R, uint32_t rbits, uint32_t
 
 __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
+    grid_barrier_init(P.bar);
     uint32_t* bm = reinterpret_cast<uint32_t*>(k2_smem);
     // window prefix of the row lengths, relative to the window start (a window's
     // rows are distinct vertices, so its total is <= m < 2^32)

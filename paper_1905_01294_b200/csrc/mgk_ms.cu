@@ -549,6 +549,7 @@ __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F,
 
 template <int W>
 __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
+    grid_barrier_init(P.bar);
     // qctl[parity] fields in this engine:
     //   nitems = |R| (discovery list tail), nfound = push items built for the
     //   frontier, edges = sum of outdeg over R, pad = push-equivalent edges.

@@ -469,6 +469,7 @@ __device__ void pull_phase(const FRParams& P, uint32_t hop, bool last, const uin
 }
 
 __global__ void __launch_bounds__(kBlock) fr_kernel(FRParams P) {
+    grid_barrier_init(P.bar);
     __shared__ unsigned long long s_stage[kWarps][kStageCap];
     __shared__ uint8_t s_dir[kMaxSlots];
     __shared__ uint8_t s_flag[kMaxSlots];  // last hop: log it; cleanup: clear V densely
