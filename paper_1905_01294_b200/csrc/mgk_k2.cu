@@ -18,7 +18,7 @@
 // target.
 //
 // One persistent cooperative launch:
-//   0a. warp per seed: reserve its F1 rows, window totals and 64-row tasks
+//   0a. warp per seed: reserve its F1 rows, window totals and 32-row tasks
 //   0b. tasks: each F1 row's vertex, row begin, length and slice crossings;
 //       per seed w(s) = sum of deg(F1)                            (barrier)
 //   1. every CTA: the "work line" (w + a per-seed cost, scanned) and its
@@ -45,7 +45,7 @@ using namespace dev;
 constexpr int kK2Block = 768;  // 80 registers, no spills (1024 threads spilled at 64)
 constexpr int kK2Warps = kK2Block / 32;
 constexpr uint32_t kK2Win = 2 * kK2Block;  // F1 rows per prefix window (2 per thread)
-constexpr uint32_t kK2Task = 64;   // F1 rows per phase-0 task (2 per lane)
+constexpr uint32_t kK2Task = 32;   // F1 rows per phase-0 task (1 per lane)
 constexpr uint32_t kK2Inline = 512;
 constexpr uint32_t kK2MaxR = 64;  // slices per seed (G4: 26, so 5 groups)
 constexpr uint32_t kNoF1 = 0xFFFFFFFFu;
