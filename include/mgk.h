@@ -195,8 +195,9 @@ int mgk_matrix_free(mgk_matrix* m);
 /* Device-resident variant: d_seeds (uint32) and d_counts (uint64) are DEVICE
  * pointers on the graph's device; work is enqueued on `stream`
  * (a cudaStream_t, NULL = legacy default) and returns without synchronizing.
- * Seeds are NOT range-checked on this path (the caller owns them; use
- * mgk_khop_count for checked calls). Calls on one stream share one workspace
+ * Seeds are not range-checked on the host on this path (the caller owns
+ * them): the kernels flag a seed >= nrows instead, reported by
+ * mgk_khop_device_check / mgk_khop_device_stats (see there). Calls on one stream share one workspace
  * and serialize on that stream. */
 int mgk_khop_count_device(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, uint32_t k,
                           int mode, int engine, uint64_t* d_counts, void* stream);
@@ -207,9 +208,34 @@ int mgk_khop_count_device(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds
  * k is checked like mgk_khop_count_device; seeds are not. */
 int mgk_khop_count_device_ks(mgk_graph* g, const uint32_t* d_seeds, uint64_t nseeds, const uint32_t* ks,
                              uint32_t nks, int mode, uint64_t* d_counts, void* stream);
+/* The harness's whole schedule in one call (run_khop_benchmark,
+ * bench.cpp:311-343, with one master seed list sized by the largest request):
+ * section j = k_hop_count(seeds[i], ks[j]) for i < nseeds_per_k[j] (a prefix
+ * of the master list, like pick_seeds' prefix-stable list). counts holds the
+ * sections back to back: section j starts at sum_{j' < j} nseeds_per_k[j'].
+ * Checks: the schedule first (bench.cpp:297-309: "hop count {k} outside [1,
+ * 32]", "seed count for k={k} must be at least 1"), then every query like
+ * mgk_khop_count. Consecutive sections with equal seed counts share launches:
+ * a k = 1 section rides on the on-chip k = 2 launch, and LANES sections of the
+ * same seeds (e.g. k = 3 and k = 6) share one traversal, each answered from
+ * its own hops' per-lane counts. The _device_ variant takes device seeds /
+ * counts and a stream like mgk_khop_count_device (no host-side seed check). */
+int mgk_khop_count_schedule(mgk_graph* g, const uint64_t* seeds, const uint64_t* nseeds_per_k, const uint32_t* ks,
+                            uint32_t nks, int mode, uint64_t* counts);
+int mgk_khop_count_device_schedule(mgk_graph* g, const uint32_t* d_seeds, const uint64_t* nseeds_per_k,
+                                   const uint32_t* ks, uint32_t nks, int mode, uint64_t* d_counts, void* stream);
+
 /* Work counters of the last device-path call on `stream` (waits for that stream;
- * kernel_ms is 0 on this path — time it with your own events). */
+ * kernel_ms is 0 on this path — time it with your own events). Also performs
+ * the check of mgk_khop_device_check. */
 int mgk_khop_device_stats(mgk_graph* g, void* stream, mgk_stats* stats);
+/* Waits for `stream` and reports the device path's seed check: when any
+ * device-path call on this graph since the last check met a seed >= nrows,
+ * returns MGK_ECONTRACT (the reference's "not an allocated node" contract,
+ * execute.cpp:348-351) and clears the flag. Such a seed is read as vertex 0
+ * on the device (no out-of-bounds access); the answers of that call are
+ * undefined. */
+int mgk_khop_device_check(mgk_graph* g, void* stream);
 
 /* k_hop_frontier (execute.cpp:347-371): the sorted ids of the result set.
  * Writes min(*n_out, cap) ids; *n_out = total. Same checks as above. */

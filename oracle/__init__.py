@@ -74,6 +74,18 @@ class Port:
         L.orc_khop_work.argtypes = [C.c_uint64, _u64p, _u64p, C.c_uint64, C.c_uint32, C.c_void_p,
                                     C.POINTER(C.c_uint32)]
 
+        L.orc_gen_bench_csr.restype = C.c_int
+        L.orc_gen_bench_csr.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                        C.c_uint64, C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                        C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]
+        L.orc_free.argtypes = [C.c_void_p]
+        L.orc_set_threads.argtypes = [C.c_uint]
+        L.orc_pick_seeds_u32.restype = C.c_int
+        L.orc_pick_seeds_u32.argtypes = [C.c_uint64, _u32p, C.c_uint64, C.c_uint64, _u64p, C.POINTER(C.c_uint64)]
+        L.orc_khop_many.restype = None
+        L.orc_khop_many.argtypes = [C.c_uint64, _u32p, _u32p, _u64p, C.c_uint64, C.c_uint32, C.c_uint,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+
     def rmat_generate(self, scale, edge_factor=16, a=0.57, b=0.19, c=0.19, rng_seed=1):
         m = self.lib.orc_rmat_generate(scale, edge_factor, a, b, c, rng_seed, None, None)
         src = np.empty(m, np.uint32)
@@ -130,6 +142,60 @@ class Port:
         e = self.lib.orc_khop_work(n, row_ptr, _c64(col_idx), seed, k, sizes.ctypes.data, C.byref(L))
         return int(e), sizes[: L.value + 1].copy()
 
+
+    # ---- bench scale (oracle/bench_oracle.c) ---------------------------------
+    def gen_bench_csr(self, scale, edge_factor=16, target_unique=0, relabel=1, a=0.57, b=0.19, c=0.19,
+                      rng_seed=1):
+        """The BASELINE.json bench graph as a uint32 CSR (row_ptr, col_idx):
+        the chunked R-MAT stream's first `target_unique` distinct non-loop
+        edges, relabelled (bench_oracle.c orc_gen_bench_csr)."""
+        n, m = C.c_uint64(), C.c_uint64()
+        prp, pci = C.c_void_p(), C.c_void_p()
+        rc = self.lib.orc_gen_bench_csr(scale, edge_factor, a, b, c, rng_seed, target_unique, relabel,
+                                        C.byref(n), C.byref(m), C.byref(prp), C.byref(pci))
+        if rc != 0:
+            raise MemoryError("orc_gen_bench_csr failed (allocation or uint32 range)")
+        try:
+            rp = np.ctypeslib.as_array(C.cast(prp, C.POINTER(C.c_uint32)), (n.value + 1,)).copy()
+            ci = np.ctypeslib.as_array(C.cast(pci, C.POINTER(C.c_uint32)), (max(m.value, 1),))[: m.value].copy()
+        finally:
+            self.lib.orc_free(prp)
+            self.lib.orc_free(pci)
+        return rp, ci
+
+    def gen_spec(self, spec):
+        """gen_bench_csr for a harness GraphSpec-like object (name, scale, ...)."""
+        return self.gen_bench_csr(spec.scale, spec.edge_factor, spec.target_unique, spec.relabel, spec.a,
+                                  spec.b, spec.c, spec.rng_seed)
+
+    def pick_seeds_u32(self, row_ptr, n, rng_seed):
+        """bench.cpp:200-218 over a uint32 CSR."""
+        rp = np.ascontiguousarray(row_ptr, np.uint32)
+        out = np.zeros(max(n, 1), np.uint64)
+        elig = C.c_uint64(0)
+        if self.lib.orc_pick_seeds_u32(len(rp) - 1, rp, n, rng_seed, out, C.byref(elig)) != 0:
+            raise RuntimeError(f"need {n} seeds but only {elig.value} nodes have out-degree >= 1")
+        return out[:n].copy()
+
+    def khop_many(self, row_ptr, col_idx, seeds, k, threads=0, work=False):
+        """(exact[ns], cumulative[ns]) of k_hop_count for every seed on all host
+        threads; with work=True also (E[ns], levels[ns, k+1])."""
+        rp = np.ascontiguousarray(row_ptr, np.uint32)
+        ci = np.ascontiguousarray(col_idx, np.uint32)
+        if len(ci) == 0:
+            ci = np.zeros(1, np.uint32)
+        sd = np.ascontiguousarray(seeds, np.uint64)
+        ns = len(sd)
+        ex = np.zeros(max(ns, 1), np.uint64)
+        cu = np.zeros(max(ns, 1), np.uint64)
+        ed = np.zeros(max(ns, 1), np.uint64) if work else None
+        lv = np.zeros((max(ns, 1), k + 1), np.uint64) if work else None
+        if ns:
+            self.lib.orc_khop_many(len(rp) - 1, rp, ci, sd, ns, k, threads, ex.ctypes.data, cu.ctypes.data,
+                                   None if ed is None else ed.ctypes.data, None if lv is None else lv.ctypes.data)
+        if work:
+            return ex[:ns], cu[:ns], ed[:ns], lv[:ns]
+        return ex[:ns], cu[:ns]
 
 def _csr_args(m):
     """(nrows, ncols, row_ptr, col_idx, vals|None) -> contiguous arrays kept alive by the caller."""
@@ -233,6 +299,11 @@ class Ref:
         L.ref_bfs_oracle_new.argtypes = [vp, vp, u64, u64]
         L.ref_bfs_oracle_count.argtypes = [vp, u64, u32, C.c_int, C.POINTER(u64)]
         L.ref_bfs_oracle_free.argtypes = [vp]
+        L.ref_matrix_from_csr_u32.restype = vp
+        L.ref_matrix_from_csr_u32.argtypes = [u64, vp, vp]
+        L.ref_matrix_free.argtypes = [vp]
+        L.ref_matrix_khop_jobs.argtypes = [vp, vp, vp, u64, C.c_int, C.c_int, vp, C.POINTER(C.c_double)]
+        L.ref_graph_khop_jobs.argtypes = [vp, vp, vp, u64, C.c_int, C.c_int, vp, C.POINTER(C.c_double)]
 
     def _check(self, rc):
         if rc != 0:
@@ -286,6 +357,19 @@ class Ref:
                                                src.ctypes.data, dst.ctypes.data, C.byref(m)))
         return src, dst
 
+    def matrix(self, row_ptr, col_idx):
+        """The reference's SparseMatrix::from_parts over a uint32 CSR (validated by
+        the reference); k_hop jobs then run the k_hop_frontier loop on it with
+        the PropertyGraph wrapper bypassed (ref_capi.cpp)."""
+        rp = np.ascontiguousarray(row_ptr, np.uint32)
+        ci = np.ascontiguousarray(col_idx, np.uint32)
+        if len(ci) == 0:
+            ci = np.zeros(1, np.uint32)
+        h = self.lib.ref_matrix_from_csr_u32(len(rp) - 1, rp.ctypes.data, ci.ctypes.data)
+        if not h:
+            raise RefError(3, self.lib.ref_last_error().decode())
+        return RefMatrix(self, h)
+
     def bfs_oracle(self, src, dst, n):
         src = np.ascontiguousarray(src, np.uint32)
         dst = np.ascontiguousarray(dst, np.uint32)
@@ -295,9 +379,39 @@ class Ref:
         return RefBfs(self, h)
 
 
+def _jobs(ref, fn, h, seeds, ks, mode, threads):
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    ks = np.ascontiguousarray(ks, np.uint32)
+    counts = np.zeros(max(len(seeds), 1), np.uint64)
+    el = C.c_double()
+    ref._check(fn(h, seeds.ctypes.data, ks.ctypes.data, len(seeds), mode, threads, counts.ctypes.data,
+                  C.byref(el)))
+    return counts[: len(seeds)], el.value
+
+
+class RefMatrix:
+    """A bare reference SparseMatrix (the 'wrapper bypassed' route for G4)."""
+
+    def __init__(self, ref: Ref, h):
+        self.ref, self.h = ref, h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_matrix_free(self.h)
+            self.h = None
+
+    def khop_jobs(self, seeds, ks, mode=EXACT, threads=1):
+        """(counts, wall seconds) of jobs i = (seeds[i], ks[i]), one query per thread."""
+        return _jobs(self.ref, self.ref.lib.ref_matrix_khop_jobs, self.h, seeds, ks, mode, threads)
+
+
 class RefGraph:
     def __init__(self, ref: Ref, h):
         self.ref, self.h = ref, h
+
+    def khop_jobs(self, seeds, ks, mode=EXACT, threads=1):
+        """(counts, wall seconds) of k_hop_count(seeds[i], ks[i]) jobs, one query per thread."""
+        return _jobs(self.ref, self.ref.lib.ref_graph_khop_jobs, self.h, seeds, ks, mode, threads)
 
     def __del__(self):
         if getattr(self, "h", None):

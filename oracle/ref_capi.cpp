@@ -23,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "matgraph/ast.hpp"
 #include "matgraph/bench.hpp"
 #include "matgraph/cypher.hpp"
 #include "matgraph/plan.hpp"
@@ -252,6 +253,112 @@ int ref_k_hop_count_many(void* g, const uint64_t* seeds, uint64_t nseeds, uint32
     if (status != 0) g_err = first_err;
     return status;
 }
+
+// ---- the reference's kernels on a bare matrix ("wrapper bypassed") ----------
+// For graphs too big for build_bench_graph on the host (BASELINE cfg4, 1.47B
+// edges: ~70 GB of pending buffers): the reference's own
+// SparseMatrix::from_parts (sparse.cpp:101-114, which validates the CSR) and
+// the k_hop_frontier loop body (execute.cpp:355-370) over it — vxm with the
+// complemented visited mask and ewise_union, exactly as k_hop_frontier calls
+// them; only the PropertyGraph wrapper (relation_matrix) is bypassed.
+void* ref_matrix_from_csr_u32(uint64_t n, const uint32_t* row_ptr, const uint32_t* col_idx) {
+    try {
+        const uint64_t m = row_ptr[n];
+        std::vector<uint64_t> rp(row_ptr, row_ptr + n + 1), ci(col_idx, col_idx + m);
+        return new matgraph_ref::SparseMatrix(
+            matgraph_ref::SparseMatrix::from_parts(n, n, std::move(rp), std::move(ci)));
+    } catch (const std::exception& e) {
+        fail(e);
+        return nullptr;
+    }
+}
+
+void ref_matrix_free(void* m) { delete static_cast<matgraph_ref::SparseMatrix*>(m); }
+
+}  // extern "C"
+
+namespace {
+// execute.cpp:347-371 with adj given (the seed / k checks of :348-354 kept)
+uint64_t matrix_k_hop_count(const matgraph_ref::SparseMatrix& adj, uint64_t seed, uint32_t k, int mode) {
+    using matgraph_ref::BitVector;
+    if (seed >= adj.nrows())
+        throw matgraph_ref::ContractError("k-hop seed " + std::to_string(seed) + " is not an allocated node");
+    if (k < 1 || k > matgraph_ref::kMaxHops)
+        throw matgraph_ref::ContractError("k-hop count " + std::to_string(k) + " outside [1, 32]");
+    const uint64_t dim = adj.nrows();
+    BitVector frontier = BitVector::from_sorted(dim, {seed});
+    BitVector visited = frontier;
+    for (uint32_t hop = 1; hop <= k; ++hop) {
+        frontier = matgraph_ref::vxm(frontier, adj, &visited, /*complement_mask=*/true);
+        if (frontier.empty()) break;
+        visited = matgraph_ref::ewise_union(visited, frontier);
+    }
+    if (mode == 0) return frontier.nvals();
+    return visited.nvals() - 1;  // visited minus the seed (execute.cpp:364-370)
+}
+
+// A pool over (seed, k) jobs: one whole query per thread at a time, jobs taken
+// in the order given (callers put the deep ones first). Returns 0 or the
+// first failure (g_err set).
+template <typename F>
+int run_jobs(uint64_t njobs, int threads, double* elapsed_s, F&& one) {
+    if (threads < 1) threads = 1;
+    std::atomic<uint64_t> cursor{0};
+    std::atomic<int> status{0};
+    std::string first_err;
+    std::atomic<bool> err_taken{false};
+    auto worker = [&] {
+        for (;;) {
+            const uint64_t i = cursor.fetch_add(1);
+            if (i >= njobs) return;
+            try {
+                one(i);
+            } catch (const std::exception& e) {
+                if (!err_taken.exchange(true)) {
+                    first_err = e.what();
+                    status = 1;
+                }
+                return;
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+    worker();
+    for (auto& t : pool) t.join();
+    *elapsed_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (status != 0) g_err = first_err;
+    return status;
+}
+}  // namespace
+
+extern "C" {
+
+// jobs i = (seeds[i], ks[i]) on the bare matrix; counts[i] = k_hop_count
+int ref_matrix_khop_jobs(void* m, const uint64_t* seeds, const uint32_t* ks, uint64_t njobs, int mode,
+                         int threads, uint64_t* counts, double* elapsed_s) {
+    const auto& adj = *static_cast<matgraph_ref::SparseMatrix*>(m);
+    return run_jobs(njobs, threads, elapsed_s,
+                    [&](uint64_t i) { counts[i] = matrix_k_hop_count(adj, seeds[i], ks[i], mode); });
+}
+
+// the same job pool over the full store: matgraph_ref::k_hop_count itself
+int ref_graph_khop_jobs(void* g, const uint64_t* seeds, const uint32_t* ks, uint64_t njobs, int mode,
+                        int threads, uint64_t* counts, double* elapsed_s) {
+    auto* graph = static_cast<PropertyGraph*>(g);
+    try {
+        graph->relation_matrix();  // flush once, outside the timed region
+    } catch (const std::exception& e) { return fail(e); }
+    return run_jobs(njobs, threads, elapsed_s, [&](uint64_t i) {
+        counts[i] = matgraph_ref::k_hop_count(
+            *graph, {seeds[i], ks[i], matgraph_ref::RelationRef::any(), to_mode(mode)});
+    });
+}
+
+// (pick_seeds, bench.cpp:200-218, takes a PropertyGraph: for a bare matrix
+// callers use the oracle's restatement orc_pick_seeds_u32, pinned to the
+// reference's seeds by tests/test_bench_oracle.py.)
 
 // Runs a Cypher query through the reference's parse -> plan -> execute
 // (proj/core/src/cypher.cpp, plan.cpp, execute.cpp:342-345) and returns the

@@ -77,8 +77,11 @@ SIGNATURES = [
     ("mgk_khop_count_device", _int, [_vp, _vp, _u64, _u32, _int, _int, _vp, _vp]),
     ("mgk_khop_count_device_ks", _int, [_vp, _vp, _u64, _vp, _u32, _int, _vp, _vp]),
     ("mgk_khop_device_stats", _int, [_vp, _vp, C.POINTER(MgkStats)]),
+    ("mgk_khop_device_check", _int, [_vp, _vp]),
     ("mgk_graph_replicate", _int, [_vp, _int, C.POINTER(_vp)]),
     ("mgk_khop_count_ks", _int, [_vp, _vp, _u64, _vp, _u32, _int, _vp]),
+    ("mgk_khop_count_schedule", _int, [_vp, _vp, _vp, _vp, _u32, _int, _vp]),
+    ("mgk_khop_count_device_schedule", _int, [_vp, _vp, _vp, _vp, _u32, _int, _vp, _vp]),
     ("mgk_khop_count_multi", _int, [_vp, _int, _vp, _u64, _u32, _int, _vp]),
     ("mgk_khop_frontier", _int, [_vp, _u64, _u32, _int, _vp, _u64, _u64p]),
     ("mgk_walk_count", _int, [_vp, _vp, _u64, _u32, _u32, _int, _vp]),

@@ -208,8 +208,13 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
                        Span span, int engine, unsigned long long* d_counts,
                        cudaStream_t stream, uint32_t* grid, uint32_t* block, int* used_engine,
                        int* W_out, bool keep_result = false, const uint32_t* h_seeds = nullptr,
-                       unsigned long long* d_counts1 = nullptr) {
-    const uint32_t k = span.hi;
+                       unsigned long long* d_counts1 = nullptr, const Span* xspans = nullptr,
+                       unsigned long long* const* xouts = nullptr, uint32_t nx = 0) {
+    uint32_t k = span.hi, lo = span.lo;
+    for (uint32_t j = 0; j < nx; ++j) {
+        k = std::max(k, xspans[j].hi);
+        lo = std::min(lo, xspans[j].lo);
+    }
     // the engines zero the per-hop counters themselves (first launch of a call)
     cudaError_t e = cudaSuccess;
     if (nseeds == 0) {
@@ -222,7 +227,15 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.d_seeds = d_seeds;
     L.nseeds = nseeds;
     L.k = k;
-    L.min_hop = span.lo;
+    L.min_hop = lo;
+    L.nextra = nx;
+    L.ans_lo = span.lo;
+    L.ans_hi = span.hi;
+    for (uint32_t j = 0; j < nx; ++j) {
+        L.xlo[j] = xspans[j].lo;
+        L.xhi[j] = xspans[j].hi;
+        L.xout[j] = xouts[j];
+    }
     L.seed_visited = span.seed_visited ? 1u : 0u;
     L.d_counts = d_counts;
     L.d_counts1 = d_counts1;
@@ -232,6 +245,7 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
     L.host_io = h_seeds != nullptr;
     L.h_seeds = h_seeds;
     engine = resolve_engine(engine, nseeds, k);
+    if (nx && engine != MGK_ENGINE_LANES) return cudaErrorInvalidValue;  // fused windows are LANES-only
     *used_engine = engine;
     if (engine == MGK_ENGINE_SINGLE) {
         e = launch_single(L);
@@ -364,6 +378,21 @@ cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block
 }  // namespace mgk
 
 using namespace mgk;
+
+namespace {
+// The device path's seed check (dev_id, mgk_device.cuh): read and clear the
+// graph's flag; a set flag is the reference's ContractError for the seed.
+int take_bad_seed(mgk::Graph* g) {
+    unsigned int bad = 0;
+    cudaError_t e = cudaMemcpy(&bad, g->bad_seed, 4, cudaMemcpyDeviceToHost);
+    if (e) return fail_cuda(e, "device check");
+    if (!bad) return MGK_OK;
+    e = cudaMemset(g->bad_seed, 0, 4);
+    if (e) return fail_cuda(e, "device check");
+    return fail(MGK_ECONTRACT, "k-hop seed outside [0, %u) on the device path (not an allocated node)",
+                g->dg.n);
+}
+}  // namespace
 
 extern "C" {
 
@@ -629,6 +658,39 @@ std::vector<int> plan_k1_fusion(const Graph* g, uint64_t nseeds, const Span* spa
     return fused;
 }
 
+// LANES sections of one seed list share one traversal: the first LANES
+// section (the lead) runs to the deepest hop of them all and answers the
+// others from its per-lane hop counts (a window's count is a sum of per-hop
+// frontier sizes, which do not depend on how deep the traversal goes).
+// lanes_lead[w] = the lead answering section w, or -1.
+std::vector<int> plan_lanes_fusion(uint64_t nseeds, const Span* spans, uint32_t n, int engine,
+                                   const std::vector<int>& k1_fused) {
+    std::vector<int> lead(n, -1);
+    int first = -1, taken = 0;
+    for (uint32_t w = 0; w < n; ++w) {
+        if (k1_fused[w] >= 0 || resolve_engine(engine, nseeds, spans[w].hi) != MGK_ENGINE_LANES) continue;
+        if (first < 0) {
+            first = (int)w;
+        } else if (spans[w].seed_visited == spans[first].seed_visited && taken < Launch::kMaxExtra) {
+            lead[w] = first;
+            ++taken;
+        }
+    }
+    return lead;
+}
+
+// the windows a lead section also answers, and where they go
+void lanes_extras(const std::vector<int>& lead, uint32_t w, const Span* spans, unsigned long long* base,
+                  uint64_t nseeds, std::vector<Span>& xs, std::vector<unsigned long long*>& xo) {
+    xs.clear();
+    xo.clear();
+    for (uint32_t j = 0; j < lead.size(); ++j)
+        if (lead[j] == (int)w) {
+            xs.push_back(spans[j]);
+            xo.push_back(base + j * nseeds);
+        }
+}
+
 int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const Span* spans, uint32_t nspans,
                      int engine, uint64_t* counts, mgk_stats* stats, const char* what) {
     Graph* g = &h->g;
@@ -653,15 +715,18 @@ int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const
     float ms = 0.f;
     bool seeds_on_device = false;
     const std::vector<int> fused = plan_k1_fusion(g, nseeds, spans, nspans, engine);
+    const std::vector<int> lead = plan_lanes_fusion(nseeds, spans, nspans, engine, fused);
     int k1_of = -1;  // the section a fused k = 2 launch also answers
     uint32_t last_run = 0;
     for (uint32_t w = 0; w < nspans; ++w) {
         if (fused[w] >= 0) k1_of = (int)w;
-        else last_run = w;
+        else if (lead[w] < 0) last_run = w;
     }
+    std::vector<Span> xs;
+    std::vector<unsigned long long*> xo;
     do {
         for (uint32_t w = 0; w < nspans && !e; ++w) {
-            if (fused[w] >= 0) continue;  // answered by the k = 2 launch
+            if (fused[w] >= 0 || lead[w] >= 0) continue;  // answered by another section's launch
             const int eng = resolve_engine(engine, nseeds, spans[w].hi);
             const bool host_io = eng == MGK_ENGINE_SINGLE;
             if (!host_io && !seeds_on_device) {
@@ -671,15 +736,20 @@ int count_impl_multi(mgk_graph* h, const uint64_t* seeds, uint64_t nseeds, const
             const bool last = w == last_run;
             unsigned long long* out = host_io ? ws->h_counts_dev : ws->d_counts;
             unsigned long long* out1 = (k1_of >= 0 && fused[k1_of] == (int)w) ? out + k1_of * nseeds : nullptr;
+            lanes_extras(lead, w, spans, out, nseeds, xs, xo);
             if (stats && last && (e = cudaEventRecord(ws->ev0, ws->stream))) break;
             if ((e = run_engine(g, ws, host_io ? ws->h_seeds_dev : ws->d_seeds, nseeds, spans[w], eng,
                                 out + w * nseeds, ws->stream, &grid, &block, &used, &W, false,
-                                host_io ? hs : nullptr, out1)))
+                                host_io ? hs : nullptr, out1, xs.data(), xo.data(), (uint32_t)xs.size())))
                 break;
             if (stats && last && (e = cudaEventRecord(ws->ev1, ws->stream))) break;
-            if (!host_io && (e = cudaMemcpyAsync(ws->h_counts + w * nseeds, ws->d_counts + w * nseeds,
-                                                 nseeds * 8, cudaMemcpyDeviceToHost, ws->stream)))
-                break;
+            if (!host_io) {
+                for (uint32_t j = 0; j < nspans && !e; ++j)
+                    if (j == w || lead[j] == (int)w)
+                        e = cudaMemcpyAsync(ws->h_counts + j * nseeds, ws->d_counts + j * nseeds, nseeds * 8,
+                                            cudaMemcpyDeviceToHost, ws->stream);
+                if (e) break;
+            }
         }
         if (e) break;
         if ((e = cudaStreamSynchronize(ws->stream))) break;
@@ -851,12 +921,14 @@ Workspace* stream_workspace(mgk_graph* h, cudaStream_t s, int* rc) {
 int count_device_multi(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, const Span* spans, uint32_t nspans,
                        int engine, uint64_t* d_counts, void* stream) {
     Graph* g = &h->g;
+    if (nseeds && g->dg.n == 0) return fail(MGK_ECONTRACT, "k-hop seed on a graph with no nodes");
     DeviceGuard dg(g->device);
     cudaStream_t s = (cudaStream_t)stream;
     int rc = MGK_OK;
     Workspace* ws = stream_workspace(h, s, &rc);
     if (!ws) return rc;
     const std::vector<int> fused = plan_k1_fusion(g, nseeds, spans, nspans, engine);
+    const std::vector<int> lead = plan_lanes_fusion(nseeds, spans, nspans, engine, fused);
     int k1_of = -1;
     for (uint32_t w = 0; w < nspans; ++w)
         if (fused[w] >= 0) k1_of = (int)w;
@@ -864,11 +936,14 @@ int count_device_multi(mgk_graph* h, const uint32_t* d_seeds, uint64_t nseeds, c
     uint32_t grid = 0, block = 0;
     int used = 0, W = 0;
     cudaError_t e = cudaSuccess;
+    std::vector<Span> xs;
+    std::vector<unsigned long long*> xo;
     for (uint32_t w = 0; w < nspans && !e; ++w) {
-        if (fused[w] >= 0) continue;  // answered by the k = 2 launch
+        if (fused[w] >= 0 || lead[w] >= 0) continue;  // answered by another section's launch
         unsigned long long* out1 = (k1_of >= 0 && fused[k1_of] == (int)w) ? out + k1_of * nseeds : nullptr;
+        lanes_extras(lead, w, spans, out, nseeds, xs, xo);
         e = run_engine(g, ws, d_seeds, nseeds, spans[w], engine, out + w * nseeds, s, &grid, &block, &used, &W, false,
-                       nullptr, out1);
+                       nullptr, out1, xs.data(), xo.data(), (uint32_t)xs.size());
     }
     ws->misc_engine = used;
     ws->misc_W = W;
@@ -907,6 +982,81 @@ int mgk_khop_count_device_ks(mgk_graph* h, const uint32_t* d_seeds, uint64_t nse
     return count_device_multi(h, d_seeds, nseeds, spans.data(), nks, MGK_ENGINE_AUTO, d_counts, stream);
 }
 
+// run_khop_benchmark's sections (bench.cpp:311-343) in one call: section j is
+// k_hop_count(seeds[i], ks[j]) for the prefix i < nseeds_per_k[j] of one
+// master seed list. Consecutive sections with the same prefix length share
+// their launches (count_*_multi).
+namespace {
+int check_schedule(const uint64_t* nseeds_per_k, const uint32_t* ks, uint32_t nks, uint64_t* total,
+                   uint64_t* longest) {
+    if (nks && (!nseeds_per_k || !ks)) return fail(MGK_ECONTRACT, "null argument");
+    *total = *longest = 0;
+    for (uint32_t j = 0; j < nks; ++j) {  // bench.cpp:297-309, the reference's messages
+        if (ks[j] < 1 || ks[j] > MGK_MAX_HOPS)
+            return fail(MGK_ECONTRACT, "hop count %u outside [1, %d]", ks[j], MGK_MAX_HOPS);
+        if (nseeds_per_k[j] == 0) return fail(MGK_ECONTRACT, "seed count for k=%u must be at least 1", ks[j]);
+        *total += nseeds_per_k[j];
+        *longest = std::max(*longest, nseeds_per_k[j]);
+    }
+    return MGK_OK;
+}
+}  // namespace
+
+int mgk_khop_count_schedule(mgk_graph* h, const uint64_t* seeds, const uint64_t* nseeds_per_k, const uint32_t* ks,
+                            uint32_t nks, int mode, uint64_t* counts) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    uint64_t total = 0, longest = 0;
+    int rc = check_schedule(nseeds_per_k, ks, nks, &total, &longest);
+    if (rc) return rc;
+    if (total && (!seeds || !counts)) return fail(MGK_ECONTRACT, "null argument");
+    for (uint32_t j = 0; j < nks; ++j)  // execute.cpp:348-354 for every query of the section
+        if ((rc = check_query(&h->g, seeds, nseeds_per_k[j], ks[j]))) return rc;
+    uint64_t off = 0;
+    for (uint32_t a = 0; a < nks;) {
+        uint32_t b = a + 1;
+        while (b < nks && nseeds_per_k[b] == nseeds_per_k[a]) ++b;
+        std::vector<Span> spans;
+        for (uint32_t j = a; j < b; ++j) spans.push_back(span_of(ks[j], mode));
+        if ((rc = count_impl_multi(h, seeds, nseeds_per_k[a], spans.data(), b - a, MGK_ENGINE_AUTO, counts + off,
+                                   nullptr, "k-hop count")))
+            return rc;
+        off += (b - a) * nseeds_per_k[a];
+        a = b;
+    }
+    return MGK_OK;
+}
+
+int mgk_khop_count_device_schedule(mgk_graph* h, const uint32_t* d_seeds, const uint64_t* nseeds_per_k,
+                                   const uint32_t* ks, uint32_t nks, int mode, uint64_t* d_counts, void* stream) {
+    if (!h) return fail(MGK_ECONTRACT, "null graph");
+    if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
+    uint64_t total = 0, longest = 0;
+    int rc = check_schedule(nseeds_per_k, ks, nks, &total, &longest);
+    if (rc) return rc;
+    uint64_t off = 0;
+    for (uint32_t a = 0; a < nks;) {
+        uint32_t b = a + 1;
+        while (b < nks && nseeds_per_k[b] == nseeds_per_k[a]) ++b;
+        std::vector<Span> spans;
+        for (uint32_t j = a; j < b; ++j) spans.push_back(span_of(ks[j], mode));
+        if ((rc = count_device_multi(h, d_seeds, nseeds_per_k[a], spans.data(), b - a, MGK_ENGINE_AUTO,
+                                     d_counts + off, stream)))
+            return rc;
+        off += (b - a) * nseeds_per_k[a];
+        a = b;
+    }
+    return MGK_OK;
+}
+
+int mgk_khop_device_check(mgk_graph* h, void* stream) {
+    if (!h) return fail(MGK_ECONTRACT, "null argument");
+    DeviceGuard dg(h->g.device);
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e) return fail_cuda(e, "device check");
+    return take_bad_seed(&h->g);
+}
+
 int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     if (!h || !stats) return fail(MGK_ECONTRACT, "null argument");
     Workspace* ws = nullptr;
@@ -922,6 +1072,7 @@ int mgk_khop_device_stats(mgk_graph* h, void* stream, mgk_stats* stats) {
     cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
     if (!e) e = cudaMemcpy(lc, ws->lc, sizeof lc, cudaMemcpyDeviceToHost);
     if (e) return fail_cuda(e, "stats");
+    if (int rc = take_bad_seed(&h->g)) return rc;
     fill_stats(stats, lc, ws->misc_engine, ws->misc_W, ws->misc_nseeds, ws->misc_grid, ws->misc_block, 0.f,
                ws->last_launches, ws->last_path);
     return MGK_OK;

@@ -32,8 +32,17 @@ __device__ __forceinline__ uint32_t atom_or_keep(uint32_t* p, uint32_t v, unsign
     return old;
 }
 
-// device id of an external vertex id (locality relabelling; identity if none)
+// device id of an external seed id (locality relabelling; identity if none).
+// A seed >= n (the device path does not range-check on the host) raises the
+// graph's bad_seed flag and is replaced by vertex 0, so no read goes out of
+// bounds; the call's answers are then undefined and the host reports
+// MGK_ECONTRACT at the next checked call (mgk_khop_device_stats /
+// mgk_khop_device_check).
 __device__ __forceinline__ uint32_t dev_id(const DevGraph& g, uint32_t x) {
+    if (x >= g.n) {
+        atomicOr(g.bad_seed, 1u);
+        x = 0;
+    }
     return g.perm ? __ldg(g.perm + x) : x;
 }
 
@@ -63,7 +72,7 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 // same grid so profilers that skip cooperative launches still see the kernel.
 // Each CTA reads the generation once per launch (grid_barrier_init, before its
 // first arrival, so no barrier can complete before the read); a barrier is
-// then one release-add per CTA and an acquire spin on the generation — the
+// then one acq_rel add per CTA and an acquire spin on the generation — the
 // release / acquire pair orders every thread's memory traffic of the phase
 // (through the CTA barriers on both sides), like cooperative_groups grid.sync().
 static __shared__ unsigned int s_bar_gen;
@@ -83,13 +92,14 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar) {
     if (threadIdx.x == 0) {
         const unsigned int gen = s_bar_gen;
         unsigned int old;
-        asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        // acq_rel: the arrival publishes this CTA's phase (release) and, for
+        // the last arriver, synchronises with every earlier arrival's release
+        // in the counter's RMW chain (acquire) — so the last CTA's next-phase
+        // loads (L1-allocating ones included) see the other CTAs' writes
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
         if (old == gridDim.x - 1) {
             asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(bar + 1), "r"(gen + 1) : "memory");
-            // an acquire here too: the last arriver's SM must also drop stale
-            // L1 lines before the next phase reads what other SMs wrote
-            (void)ld_acquire_gpu(bar + 1);
         } else {
             while (ld_acquire_gpu(bar + 1) == gen) {
             }

@@ -289,6 +289,9 @@ cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
     MGK_TRY(cudaMalloc(&g->ri, mp * 4));
     MGK_TRY(cudaMalloc(&g->no_in, (size_t)(g->dg.nwords + 1) * 4));
     MGK_TRY(cudaMalloc(&g->pull_skip, (size_t)(g->dg.nwords + 1) * 4));
+    MGK_TRY(cudaMalloc(&g->bad_seed, 4));
+    MGK_TRY(cudaMemset(g->bad_seed, 0, 4));
+    g->dg.bad_seed = g->bad_seed;
     g->bytes = 2 * (size_t)(n + 1) * 4 + 2 * mp * 4 + 2 * (size_t)(g->dg.nwords + 1) * 4;
     g->dg.rp = g->rp;
     g->dg.ci = g->ci;
@@ -592,6 +595,7 @@ cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
     dst->dg.ri = dst->ri;
     dst->dg.no_in = dst->no_in;
     dst->dg.pull_skip = dst->pull_skip;
+    dst->dg.bad_seed = dst->bad_seed;
     const size_t mp = (size_t)std::max<uint64_t>(m, 1);
     const size_t nh = (size_t)std::max<uint32_t>(src->dg.nheavy, 1);
     MGK_TRY(cudaMalloc(&dst->heavy, nh * sizeof(uint2)));
@@ -660,6 +664,9 @@ void free_device_graph(Graph* g) {
     cudaFree(g->perm);
     cudaFree(g->inv);
     cudaFree(g->k2_split);
+    cudaFree(g->bad_seed);
+    g->bad_seed = nullptr;
+    g->dg.bad_seed = nullptr;
     g->k2_split = nullptr;
     g->k2_split_bits = g->k2_split_R = 0;
     g->rp = g->ci = g->cp = g->ri = g->no_in = g->pull_skip = nullptr;

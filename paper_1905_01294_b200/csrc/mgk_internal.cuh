@@ -41,6 +41,9 @@ struct DevGraph {
     // external id (perm) and back (inv); null = identity
     const uint32_t* perm = nullptr;
     const uint32_t* inv = nullptr;
+    // set (never cleared on the device) when a device-path call meets a seed
+    // >= n; the host reports it as MGK_ECONTRACT at the next checked call
+    unsigned int* bad_seed = nullptr;
 };
 constexpr uint32_t kHeavyIn = 1024;
 constexpr uint32_t kHeavyChunk = 1024;
@@ -171,6 +174,7 @@ struct Graph {
     uint2* heavy = nullptr;
     uint32_t* perm = nullptr;
     uint32_t* inv = nullptr;
+    unsigned int* bad_seed = nullptr;
     uint64_t bytes = 0;
     // on-chip k = 2: per vertex, where its (ascending) row crosses each bitmap
     // slice boundary ([n][R-1] absolute col_idx positions), built on first use
@@ -194,6 +198,14 @@ struct Launch {
     uint32_t seed_visited;  // 1 for k_hop_*, 0 for walk_targets
     unsigned long long* d_counts;
     unsigned long long* d_counts1 = nullptr;  // on-chip k = 2 only: also the k = 1 answers
+    // LANES only: further hop windows answered by the same traversal (the
+    // harness's sections over one seed list, e.g. k = 3 and k = 6): window j
+    // counts hops [xlo[j], xhi[j]] (xhi <= k, xlo >= min_hop) into xout[j]
+    static constexpr int kMaxExtra = 7;
+    uint32_t nextra = 0;
+    uint32_t ans_lo = 0, ans_hi = 0;  // d_counts' own window when nextra > 0 (else [min_hop, k])
+    uint32_t xlo[kMaxExtra] = {}, xhi[kMaxExtra] = {};
+    unsigned long long* xout[kMaxExtra] = {};
     cudaStream_t stream;
     Tuning tuning;
     int lanes_words;  // LANES engine only

@@ -784,24 +784,53 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 // events and the launch is part of the measured call)
 struct K2Device {
     int optin = 0, nsm = 0;
-    size_t smem_set = 0;  // dynamic smem the kernel attribute allows
-    size_t occ_smem = 0;  // occupancy cached for this smem size
-    int occ = 0;
+    size_t occ_smem[8] = {};  // occupancy cache: dynamic smem -> CTAs per SM
+    int occ[8] = {};
+    int nocc = 0;
 };
-K2Device& k2_device() {
+std::mutex& k2_mutex() {
     static std::mutex mu;
+    return mu;
+}
+// Looked up once per device under the mutex; the kernel's dynamic shared
+// memory limit is raised to the opt-in maximum at that point, so no later call
+// can lower it for another thread's larger graph.
+K2Device& k2_device() {
     static K2Device devs[64];
     static bool ready[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     dev &= 63;
-    std::lock_guard<std::mutex> lk(mu);
+    std::lock_guard<std::mutex> lk(k2_mutex());
     if (!ready[dev]) {
         cudaDeviceGetAttribute(&devs[dev].optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaDeviceGetAttribute(&devs[dev].nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, devs[dev].optin) !=
+            cudaSuccess) {
+            (void)cudaGetLastError();
+            devs[dev].optin = 0;  // k2_eligible then declines every call on this device
+        }
         ready[dev] = true;
     }
     return devs[dev];
+}
+// CTAs per SM of k2_kernel at `smem` bytes of dynamic shared memory (cached
+// per device under the same mutex).
+cudaError_t k2_occupancy(K2Device& kd, size_t smem, int* per_sm) {
+    std::lock_guard<std::mutex> lk(k2_mutex());
+    for (int i = 0; i < kd.nocc; ++i)
+        if (kd.occ_smem[i] == smem) {
+            *per_sm = kd.occ[i];
+            return cudaSuccess;
+        }
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k2_kernel, kK2Block, smem);
+    if (e) return e;
+    const int slot = kd.nocc < 8 ? kd.nocc++ : 7;
+    kd.occ_smem[slot] = smem;
+    kd.occ[slot] = occ;
+    *per_sm = occ;
+    return cudaSuccess;
 }
 
 // bitmap words one CTA can hold (MGK_K2_SLICE_WORDS caps it, for tests of many slices)
@@ -820,6 +849,7 @@ bool k2_eligible(const Launch& L) {
     if (off || L.k != 2 || L.min_hop < 1 || L.keep_result || !L.g->dg.rows_unique) return false;
     if (L.tuning.force_dir != 0 || L.nseeds == 0) return false;
     const int optin = k2_device().optin;
+    if (optin <= (int)kK2Fixed + 4096) return false;
     const uint64_t maxw = k2_max_words(optin);
     const uint64_t nw = L.g->dg.nwords;
     return (nw + maxw - 1) / maxw <= kK2MaxR;
@@ -849,18 +879,9 @@ cudaError_t launch_k2(Launch& L) {
     const uint32_t rbits = (uint32_t)((((uint64_t)gr->dg.n + R - 1) / R + 127) / 128 * 128);
     const uint32_t rwords = rbits / 32;
     const size_t smem = (size_t)rwords * 4 + kK2Fixed;
-    if (smem > kd.smem_set) {  // per device (the attribute is per context)
-        if ((e = cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)))
-            return e;
-        kd.smem_set = smem;
-    }
-    if (kd.occ_smem != smem) {
-        int per_sm = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_kernel, kK2Block, smem))) return e;
-        kd.occ = per_sm;
-        kd.occ_smem = smem;
-    }
-    const int per_sm = kd.occ;
+    if (smem > (size_t)optin) return cudaErrorInvalidValue;
+    int per_sm = 0;
+    if ((e = k2_occupancy(kd, smem, &per_sm))) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const uint32_t grid = (uint32_t)(per_sm * nsm) / R * R;
     const uint32_t G = grid / R;

@@ -37,6 +37,10 @@ struct MSParams {
     uint64_t nseeds;
     uint32_t k;             // max hop
     uint32_t min_hop;       // answer = sum over hops [min_hop, k] of each lane's |F_h|
+    uint32_t ans_lo, ans_hi;  // the window answered into counts
+    uint32_t nextra;        // further windows [xlo, xhi] -> xout (Launch::xout)
+    uint32_t xlo[Launch::kMaxExtra], xhi[Launch::kMaxExtra];
+    unsigned long long* xout[Launch::kMaxExtra];
     uint32_t seed_visited;  // 0: walk_targets semantics (the seed is not pre-visited)
     unsigned long long* counts;
     unsigned long long* V;
@@ -682,8 +686,13 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         // ---- answers ------------------------------------------------------------------
         if (gtid < lanes) {
             unsigned long long r = 0;
-            for (uint32_t h = P.min_hop; h <= P.k; ++h) r += P.lane_cnt[h * LB + gtid];
+            for (uint32_t h = P.ans_lo; h <= P.ans_hi; ++h) r += P.lane_cnt[h * LB + gtid];
             P.counts[bt * LB + gtid] = r;
+            for (uint32_t j = 0; j < P.nextra; ++j) {
+                unsigned long long x = 0;
+                for (uint32_t h = P.xlo[j]; h <= P.xhi[j]; ++h) x += P.lane_cnt[h * LB + gtid];
+                P.xout[j][bt * LB + gtid] = x;
+            }
         }
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
@@ -722,6 +731,14 @@ cudaError_t launch_w(Launch& L) {
     P.nseeds = L.nseeds;
     P.k = L.k;
     P.min_hop = L.min_hop;
+    P.nextra = L.nextra;
+    P.ans_lo = L.nextra ? L.ans_lo : L.min_hop;
+    P.ans_hi = L.nextra ? L.ans_hi : L.k;
+    for (int j = 0; j < Launch::kMaxExtra; ++j) {
+        P.xlo[j] = L.xlo[j];
+        P.xhi[j] = L.xhi[j];
+        P.xout[j] = L.xout[j];
+    }
     P.seed_visited = L.seed_visited;
     P.counts = L.d_counts;
     P.V = ws->lv;

@@ -352,6 +352,45 @@ def k_hop_count_sections(graph: DeviceGraph, seeds, ks, mode=TraverseMode.Exact)
     return counts
 
 
+def k_hop_count_schedule(graph: DeviceGraph, seeds, nseeds_per_k, ks, mode=TraverseMode.Exact):
+    """The harness's whole schedule in one call (run_khop_benchmark,
+    bench.cpp:311-343): section j = k_hop_count(seeds[i], ks[j]) for the
+    prefix i < nseeds_per_k[j] of one master list. Returns a list of uint64
+    arrays, one per section (mgk_khop_count_schedule)."""
+    seeds = np.ascontiguousarray(seeds, np.uint64)
+    ns = np.ascontiguousarray(nseeds_per_k, np.uint64)
+    ks = np.ascontiguousarray(ks, np.uint32)
+    if len(ns) != len(ks):
+        raise ContractError(f"schedule pairs {len(ks)} hop counts with {len(ns)} seed counts")
+    if len(ns) and int(ns.max()) > len(seeds):
+        raise ContractError(f"schedule needs {int(ns.max())} seeds, {len(seeds)} given")
+    if graph.node_count < graph.nrows and len(seeds) and len(ns):  # the C ABI checks against nrows
+        bad = np.flatnonzero(seeds[: int(ns.max())] >= graph.node_count)
+        if len(bad):
+            raise ContractError(f"k-hop seed {int(seeds[bad[0]])} is not an allocated node")
+    counts = np.zeros(max(int(ns.sum()) if len(ns) else 0, 1), np.uint64)
+    if len(ks):
+        _check(_lib.lib().mgk_khop_count_schedule(graph.handle, seeds.ctypes.data if len(seeds) else None,
+                                                  ns.ctypes.data, ks.ctypes.data, len(ks), int(mode),
+                                                  counts.ctypes.data))
+    out, off = [], 0
+    for n in ns.tolist():
+        out.append(counts[off:off + n].copy())
+        off += n
+    return out
+
+
+def k_hop_count_device_schedule(graph: DeviceGraph, d_seeds_ptr: int, nseeds_per_k, ks, mode: int,
+                                d_counts_ptr: int, stream_ptr: int = 0):
+    """Device-resident schedule (mgk_khop_count_device_schedule): sections back
+    to back in d_counts (uint64), async on the stream."""
+    ns = np.ascontiguousarray(nseeds_per_k, np.uint64)
+    ks = np.ascontiguousarray(ks, np.uint32)
+    _check(_lib.lib().mgk_khop_count_device_schedule(graph.handle, C.c_void_p(d_seeds_ptr), ns.ctypes.data,
+                                                     ks.ctypes.data, len(ks), int(mode), C.c_void_p(d_counts_ptr),
+                                                     C.c_void_p(stream_ptr)))
+
+
 def k_hop_count_multi(replicas, seeds, k: int, mode=TraverseMode.Exact):
     """One batch over replicas of the same graph (e.g. one per GPU, made with
     DeviceGraph.replicate): contiguous seed shards, one host thread per
@@ -393,6 +432,12 @@ def k_hop_count_device_sections(graph: DeviceGraph, d_seeds_ptr: int, nseeds: in
                                                C.c_void_p(stream_ptr)))
 
 
+def device_check(graph: DeviceGraph, stream_ptr: int = 0) -> None:
+    """mgk_khop_device_check: wait for the stream; ContractError when a
+    device-path call met a seed >= node count since the last check."""
+    _check(_lib.lib().mgk_khop_device_check(graph.handle, C.c_void_p(stream_ptr)))
+
+
 def device_stats(graph: DeviceGraph, stream_ptr: int = 0) -> dict:
     st = MgkStats()
     _check(_lib.lib().mgk_khop_device_stats(graph.handle, C.c_void_p(stream_ptr), C.byref(st)))
@@ -406,5 +451,7 @@ def device_count() -> int:
 __all__ = ["ContractError", "HarnessError", "Error", "DeviceError", "SnapshotError", "snapshot_check", "mxm",
            "SEMIRING_BOOL_OR_AND", "SEMIRING_PLUS_TIMES", "SEMIRING_MIN_PLUS", "TraverseMode", "KHopQuery",
            "Tuning", "DeviceGraph", "k_hop_count", "k_hop_frontier", "k_hop_count_batch",
-           "k_hop_count_device", "k_hop_count_device_sections", "k_hop_count_multi", "k_hop_count_sections", "walk_count_batch", "walk_targets", "device_stats", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
+           "k_hop_count_device", "k_hop_count_device_sections", "k_hop_count_schedule",
+           "k_hop_count_device_schedule", "k_hop_count_multi", "k_hop_count_sections", "walk_count_batch",
+           "walk_targets", "device_stats", "device_check", "device_count", "ENGINE_AUTO", "ENGINE_SINGLE",
            "ENGINE_LANES", "K_MAX_HOPS"]
