@@ -1,24 +1,42 @@
 #!/usr/bin/env python3
 """k-hop count benchmark (BASELINE.json metric) — one JSON line on rank 0.
 
-Workload (N=1): BASELINE.json configs[1] ("cfg2"): R-MAT (a=.57 b=.19 c=.19
-d=.05) over 2^22 ids until 67,108,864 unique directed edges remain, isolated
-ids dropped and survivors renumbered (2,412,345 vertices); 300 pick_seeds
-seeds; a step = k=1 and k=2 exact counts for all 300 seeds. Multi-GPU: each
-rank holds a replica and runs its own disjoint 300-seed shard of one master
-seed list (weak scaling, no collective on the data path).
+Headline workload (N=1): BASELINE.json configs[3] ("cfg4"), the largest
+single-GPU config: the Twitter-shaped R-MAT graph G4 (a=.57 b=.19 c=.19
+d=.05 over 2^26 ids until 1,470,000,000 unique directed edges remain,
+isolated ids dropped and survivors renumbered: n = 35,559,419) and the
+reference harness's default schedule (proj/tools/matgraph.cpp:20-21):
+k = 1, 2, 3, 6 with 300 / 300 / 10 / 10 seeds, the 10-seed sections being
+prefixes of the 300-seed pick_seeds list (bench.cpp:200-218, 311-343). A step
+is that whole schedule, 620 exact k-hop counts. Metric: queries/s, plus GTEPS
+(push-equivalent edges).
+
+Multi-GPU (torchrun, or `--gpus N` which re-launches itself under torchrun):
+every rank generates its own replica of G4 on its GPU and runs its own
+schedule on a disjoint 300-seed shard of one master list (weak scaling, no
+collective on the data path); max-over-ranks device time.
 
 Arms:
-  default           our sm_100a engine (libmgk.so) — `value` is device-resident
-                    (seeds/counts in HBM, CUDA events on the launch stream, L2
-                    flushed between steps); `e2e` is the public host API
-                    (k_hop_count_batch: host seeds -> H2D -> kernels -> D2H).
-  --impl reference  the reference's own CPU k_hop_count (oracle/_ref, the
-                    unmodified matgraph core) on all host threads.
+  default           the sm_100a engine (libmgk.so). `value`: device-resident
+                    seeds / counts, one mgk_khop_count_device_schedule call per
+                    step, CUDA events on the launch stream, L2 flushed between
+                    steps (outside the events). `e2e`: the public host API
+                    (k_hop_count_schedule: host uint64 seeds in, host counts
+                    out). Every answer is checked against the CPU oracle before
+                    timing (and, on rank 0, against the reference's own counts).
+  --impl reference  the reference's own CPU k-hop loop (oracle/_ref: the
+                    unmodified matgraph core's vxm / ewise_union, execute.cpp:
+                    347-375, over SparseMatrix::from_parts of G4 — the
+                    PropertyGraph wrapper is bypassed because build_bench_graph
+                    of 1.47B edges needs ~70 GB) on all host
+                    threads. Input preparation uses the C oracle's generator and
+                    pick_seeds restatement (oracle/bench_oracle.c); this arm
+                    never loads the product library.
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import subprocess
@@ -32,9 +50,16 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+# BASELINE.json graph recipes (same numbers as paper_1905_01294_b200.harness; kept
+# here so the reference arm never imports the product package)
+G2 = dict(name="G2", scale=22, edge_factor=16, target_unique=67_108_864, relabel=2)
+G4 = dict(name="G4", scale=26, edge_factor=16, target_unique=1_470_000_000, relabel=2)
+RMAT = [0.57, 0.19, 0.19, 0.05]
+SCHEDULE = {"cfg4": (G4, (1, 2, 3, 6), (300, 300, 10, 10)),   # matgraph.cpp:20-21 on G4
+            "cfg2": (G2, (1, 2), (300, 300)),                  # BASELINE configs[1]
+            "cfg3": (G2, (3, 6), (10, 10))}                    # BASELINE configs[2]
 SEEDS_PER_RANK = 300
-KS = (1, 2)
-WORKLOAD = "cfg2"
+METRIC = "k-hop count queries/s (k=1,2,3,6 x 300/300/10/10 seeds, exact; reference default schedule)"
 
 
 def log(*a):
@@ -43,63 +68,83 @@ def log(*a):
 
 def peaks():
     try:
-        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def workload_config(name: str, world: int, n: int | None = None, m: int | None = None) -> dict:
+    """The `config` object — identical keys and values in both arms."""
+    spec, ks, ns = SCHEDULE[name]
+    return {"workload": name, "graph": {"name": spec["name"], "ids": f"2^{spec['scale']} renumbered",
+                                        "unique_edges": spec["target_unique"], "n": n, "m": m, "rmat": RMAT},
+            "schedule": {"ks": list(ks), "seeds_per_k": list(ns), "mode": "exact",
+                         "source": "proj/tools/matgraph.cpp:20-21 (bench default)" if name == "cfg4" else "BASELINE.json"},
+            "seeds_per_rank": max(ns), "ranks": world,
+            "l2": "flushed between steps (256 MiB write outside the events); the graph (>= 0.56 GB) exceeds L2"}
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """NVML clocks + throttle reasons sampled every 2 ms in a thread during the
+    timed region (a 50 ms nvidia-smi poll misses short regions)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.index, self.period = index, period_s
+        self.sm, self.reasons, self.max = [], set(), None
+        self._stop = threading.Event()
+        self.err = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report it, never fail the bench
+            self.err = str(e)[:120]
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                r = get(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception as e:
+                self.err = str(e)[:120]
+                return
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
-            except ValueError:
-                continue
-            for name, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max,
+               "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "NVML, 2 ms period"}
+        if self.err:
+            out["error"] = self.err
+        return out
 
 
 def dist_env():
@@ -109,419 +154,494 @@ def dist_env():
 
 def seed_shard(master, rank: int, world: int, per_rank: int):
     """Rank r's disjoint shard of the master seed list (weak scaling)."""
-    assert len(master) >= per_rank * world
+    if len(master) < per_rank * world:
+        raise ValueError(f"master list of {len(master)} seeds cannot give {world} shards of {per_rank}")
     return master[rank * per_rank:(rank + 1) * per_rank]
 
 
-def build_inputs(world: int, rank: int, dist=None, device=None):
-    """G2 CSR + this rank's seeds. With world > 1 rank 0 generates the graph and
-    the master seed list and broadcasts them (NCCL over NVLink): load-time
-    replication, not on the timed path."""
-    from paper_1905_01294_b200 import harness as H
-    t = time.time()
-    if world == 1 or dist is None:
-        rp, ci = H.gen_csr(H.G2)
-        master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
-    else:
-        import torch
-        if rank == 0:
-            rp, ci = H.gen_csr(H.G2)
-            master = H.pick_seeds(rp, SEEDS_PER_RANK * world, 1)
-            meta = torch.tensor([len(rp), len(ci)], dtype=torch.int64, device=device)
-        else:
-            meta = torch.zeros(2, dtype=torch.int64, device=device)
-        dist.broadcast(meta, 0)
-        n1, m = int(meta[0]), int(meta[1])
-        trp = torch.from_numpy(rp.view(np.int32)).to(device) if rank == 0 else \
-            torch.empty(n1, dtype=torch.int32, device=device)
-        tci = torch.from_numpy(ci.view(np.int32)).to(device) if rank == 0 else \
-            torch.empty(m, dtype=torch.int32, device=device)
-        tms = torch.from_numpy(master.view(np.int64)).to(device) if rank == 0 else \
-            torch.empty(SEEDS_PER_RANK * world, dtype=torch.int64, device=device)
-        for tt in (trp, tci, tms):
-            dist.broadcast(tt, 0)
-        rp = trp.cpu().numpy().view(np.uint32)
-        ci = tci.cpu().numpy().view(np.uint32)
-        master = tms.cpu().numpy().view(np.uint64)
-    seeds = seed_shard(master, rank, world, SEEDS_PER_RANK)
-    log(f"[rank {rank}] G2: n={len(rp) - 1} m={len(ci)} ready in {time.time() - t:.1f}s")
-    return rp, ci, seeds
-
-
-def algo_bytes(st: dict) -> float:
-    """Algorithmic bytes of one traversal launch, from the
-    engine's own per-hop counters.
-
-    SINGLE (per-seed bitmaps; SURVEY.md §8(d) single-source model): per hop,
-    4 B per adjacency entry read (push: out-edges of the frontier; pull:
-    in-edges up to the first frontier hit) + 8 B row/col_ptr pair per opened
-    vertex (push: frontier vertices, pull: candidates) + 4 B per frontier id
-    read (push) + 4 B per discovered id written. Bitmaps are L2-resident and
-    not counted.
-    LANES (W x 64-bit lane words): (4 + 8W) B per adjacency entry read (the
-    index and the neighbour's lane word) + (8 + 8W) B per expanded (push) /
-    candidate (pull) vertex + 3 x 8W B per discovered vertex (F' read, V read +
-    write)."""
+# ---- SURVEY.md §8(d) algorithmic bytes ----------------------------------------------
+def single_source_bytes(st: dict, nseeds: int) -> float:
+    """B = 4 E + 12 sum_{l<L} |F_l| + 4 sum_{1<=l<=L} |F_l| summed over seeds,
+    from the engine's per-hop counters (edges = push-equivalent E, frontier =
+    sum of |F_l|). F_0 = the seeds. A level after an early exit has |F| = 0."""
     lv = st["levels"]
+    hops = [h for h in range(1, len(lv)) if lv[h]["runs"]]
+    if not hops:
+        return 0.0
+    last = hops[-1]
+    E = sum(lv[h]["edges"] for h in hops)
+    expanded = nseeds + sum(lv[h]["frontier"] for h in hops if h < last)
+    written = sum(lv[h]["frontier"] for h in hops)
+    return 4.0 * E + 12.0 * expanded + 4.0 * written
+
+
+def lanes_bytes(st: dict, n: int) -> float:
+    """64-lane mode: per expanded level l, U_l = vertices with
+    a non-zero frontier word: 4 sum_{v in U_l} outdeg(v) + 12 |U_l| + 24 W n
+    (three streaming passes over n W-word state words). union_edges of hop h
+    = sum of outdeg over U_{h-1}; vertices of hop h-1 = |U_{h-1}|."""
+    lv = st["levels"]
+    W = max(1, st["lanes"] // 64)
     total = 0.0
-    if st.get("path") == "smem_k2":
-        # k = 2 with the visited sets on chip: the seeds' row pointers, their
-        # rows (F1 ids) with each F1 vertex's row-pointer pair, and every hop-2
-        # adjacency entry once from HBM (the R slice CTAs' repeats hit L2)
-        return 8 * st["batches"] + 12 * lv[1]["scanned"] + 4 * lv[2]["scanned"]
-    if st["engine"] == "lanes":
-        W = st["lanes"] // 64
-        for h in range(1, len(lv)):
-            L = lv[h]
-            if not L["runs"]:
-                continue
-            expanded = L["candidates"] if L["pull_runs"] else lv[h - 1]["vertices"]
-            total += (4 + 8 * W) * L["scanned"] + (8 + 8 * W) * expanded + 24 * W * L["vertices"]
-        return total
     for h in range(1, len(lv)):
-        L = lv[h]
-        if not L["runs"]:
+        if not lv[h]["runs"]:
             continue
-        prev = lv[h - 1]["frontier"] if h > 1 else st["batches"]
-        pushes = L["runs"] - L["pull_runs"]
-        push_share = pushes / L["runs"]
-        opened = L["candidates"] + prev * push_share
-        total += 4 * L["scanned"] + 8 * opened + 4 * prev * push_share + 4 * L["frontier"]
+        U = lv[h - 1]["vertices"] if h > 1 else min(st["lanes"], lv[0]["vertices"] or st["lanes"])
+        total += 4.0 * lv[h]["union_edges"] + 12.0 * U + 24.0 * W * n
     return total
 
 
-def hop_bytes(st: dict, h: int) -> float:
-    """algo_bytes restricted to hop h (same model)."""
-    one = dict(st)
-    lv = st["levels"]
-    one["levels"] = [dict(L, runs=0) if i not in (h - 1, h) else (L if i == h else dict(L, runs=0))
-                     for i, L in enumerate(lv)]
-    return algo_bytes(one)
+def algo_bytes(st: dict, nseeds: int, n: int) -> float:
+    return lanes_bytes(st, n) if st["engine"] == "lanes" else single_source_bytes(st, nseeds)
 
 
-def snapshot_load(rp, ci, torch):
-    """GRAPHSNAP1 text of G2 (byte-identical to the
-    reference writer) loaded into a device graph by the GPU parser, wall clock
-    from host bytes to a ready CSR + CSC; beside it the reference's own
-    snapshot_from_string on the G1 text (a bounded sample, one thread)."""
-    from paper_1905_01294_b200 import DeviceGraph, harness as H
+def push_edges(st: dict) -> int:
+    return int(sum(L["edges"] for L in st["levels"][1:] if L["runs"]))
+
+
+# ---- our arm --------------------------------------------------------------------------
+class Arm:
+    """One workload on one rank: device graph, seeds, oracle-checked answers."""
+
+    def __init__(self, name, torch, local, rank, world, graph=None, host_csr=None):
+        from paper_1905_01294_b200 import DeviceGraph, harness as H
+        self.name, self.torch, self.rank, self.world = name, torch, rank, world
+        spec, self.ks, self.ns = SCHEDULE[name]
+        hspec = H.SPECS[spec["name"]]
+        t = time.time()
+        self.g = graph if graph is not None else DeviceGraph.generate(hspec, device=local)
+        self.gen_s = time.time() - t
+        t = time.time()
+        self.rp, self.ci = host_csr if host_csr is not None else self.g.csr()
+        self.n, self.m = int(self.g.nrows), int(self.g.nnz)
+        master = H.pick_seeds(self.rp, SEEDS_PER_RANK * world, 1)
+        self.master = master
+        self.seeds = seed_shard(master, rank, world, SEEDS_PER_RANK)  # the longest section's seeds
+        log(f"[rank {rank}] {name}: {spec['name']} n={self.n} m={self.m} generated on the GPU in "
+            f"{self.gen_s:.1f}s, CSR downloaded in {time.time() - t:.1f}s")
+        self.d_seeds = torch.from_numpy(self.seeds.astype(np.int32)).cuda()
+        self.d_out = torch.zeros(sum(self.ns), dtype=torch.int64, device="cuda")
+        self.stream = torch.cuda.current_stream()
+
+    def step(self, ns=None, ks=None, out=None):
+        from paper_1905_01294_b200 import k_hop_count_device_schedule
+        k_hop_count_device_schedule(self.g, self.d_seeds.data_ptr(), list(ns or self.ns), list(ks or self.ks), 0,
+                                    (out if out is not None else self.d_out).data_ptr(), self.stream.cuda_stream)
+
+    def answers(self):
+        from paper_1905_01294_b200 import device_check
+        device_check(self.g, self.stream.cuda_stream)
+        out = self.d_out.cpu().numpy().astype(np.uint64)
+        res, off = {}, 0
+        for k, n in zip(self.ks, self.ns):
+            res[k] = out[off:off + n]
+            off += n
+        return res
+
+    def groups(self):
+        """The schedule's launch groups: consecutive sections with one seed count
+        share a launch (mgk_khop_count_device_schedule)."""
+        gs, a = [], 0
+        while a < len(self.ks):
+            b = a + 1
+            while b < len(self.ks) and self.ns[b] == self.ns[a]:
+                b += 1
+            gs.append((tuple(self.ns[a:b]), tuple(self.ks[a:b])))
+            a = b
+        return gs
+
+
+def oracle_check(arm: Arm, got: dict, pins: dict | None) -> dict:
+    """Every answer of this rank's schedule against the C oracle's BFS
+    (oracle/bench_oracle.c orc_khop_many on the host copy of the same CSR, all
+    host threads), and on rank 0 also against the reference's own counts
+    pinned in tests/golden/bench_pins.json when the generated graph hashes
+    equal to the pinned one. Raises on any mismatch."""
+    import oracle
+    P = oracle.Port()
     t = time.time()
-    text = H.snapshot_text(rp, ci)
-    t_write = time.time() - t
-    times = []
-    for _ in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        gs = DeviceGraph.from_snapshot(text)
-        torch.cuda.synchronize()
-        times.append(time.perf_counter() - t0)
-    drp, dci = gs.csr()
-    ok = bool(np.array_equal(drp, rp) and np.array_equal(dci, ci))
-    del gs
-    sec = {"graph": "G2", "bytes": len(text), "write_s": t_write, "gpu_s": float(np.median(times)),
-           "gpu_GBps": len(text) / float(np.median(times)) / 1e9, "csr_matches": ok}
-    try:
-        import oracle
-        R = oracle.Ref()
-        rp1, ci1 = H.gen_csr(H.G1)
-        t1 = H.snapshot_text(rp1, ci1)
-        t0 = time.perf_counter()
-        R.snapshot_parse(t1)
-        el = time.perf_counter() - t0
-        sec["reference"] = {"bytes": len(t1), "s": el, "GBps": len(t1) / el / 1e9,
-                            "sample": "G1 snapshot text, reference snapshot_from_string (1 thread, full store)"}
-    except Exception as e:  # reference library not built
-        sec["reference"] = {"unavailable": str(e)[:120]}
-    del text
-    return sec
+    checked = mism = 0
+    deepest = {}
+    for k, n in zip(arm.ks, arm.ns):
+        deepest[n] = max(deepest.get(n, 0), k)
+    levels = {}
+    for n, kmax in deepest.items():
+        _, _, _, lv = P.khop_many(arm.rp, arm.ci, arm.seeds[:n], kmax, work=True)
+        levels[n] = lv
+    for k, n in zip(arm.ks, arm.ns):
+        want = levels[n][:, k]
+        bad = int((got[k] != want).sum())
+        checked += n
+        mism += bad
+    out = {"checked": checked, "mismatches": mism, "against": ["C oracle BFS (orc_khop_many) on the same CSR"],
+           "oracle_s": round(time.time() - t, 1)}
+    gname = SCHEDULE[arm.name][0]["name"]
+    if pins and gname in pins and arm.rank == 0 and arm.world == 1:
+        p = pins[gname]
+        if arm.n == p["n"] and arm.m == p["m"] and sha(arm.rp, arm.ci) == p["csr_sha256"]:
+            rc = 0
+            for label, ent in p["ref"].items():
+                for kk, c in ent["counts"].items():
+                    k = int(kk)
+                    if k in got:
+                        w = np.array(c["exact"][:len(got[k])], np.uint64)
+                        mism += int((got[k][:len(w)] != w).sum())
+                        rc += len(w)
+            out["against"].append(f"reference counts (tests/golden/bench_pins.json from oracle/_ref): {rc} answers")
+            out["reference_checked"] = rc
+            out["graph_sha256_matches_pin"] = True
+        else:
+            out["graph_sha256_matches_pin"] = False
+            mism += 1  # the generated graph is not the pinned one: fail loudly
+    out["mismatches"] = mism
+    if mism:
+        raise AssertionError(f"{arm.name}: {mism} answers differ from the oracle / reference: {out}")
+    return out
 
 
-def mxm_section(torch):
-    """A x A of a scale-14 R-MAT graph (bool_or_and and plus_times) through the
-    GPU mxm (host CSR in, host CSR out, wall clock) beside the reference's own
-    mxm (one thread) on the same operands."""
-    from paper_1905_01294_b200 import harness as H, mxm
-    spec = H.GraphSpec("M14", scale=14, edge_factor=16, relabel=1)
-    rp, ci = H.gen_csr(spec)
-    n = len(rp) - 1
-    A = (n, n, rp.astype(np.uint64), ci.astype(np.uint64), None)
-    sec = {"graph": "scale-14 R-MAT (G1 recipe)", "nnz_a": int(len(ci))}
+def time_steps(arm: Arm, flush, steps: int, warmup: int, dist=None):
+    torch = arm.torch
+    for _ in range(warmup):
+        flush.fill_(1)
+        arm.step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(arm.stream)
+        arm.step()
+        e1.record(arm.stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    if dist is not None:
+        dist.barrier()
+    return ms
+
+
+def group_profile(arm: Arm, flush, reps: int):
+    """Each launch group of the schedule on its own (CUDA events on the launch
+    stream): per-group time, the engine's counters, §8(d) bytes and GTEPS."""
+    from paper_1905_01294_b200 import device_stats
+    torch = arm.torch
+    pk, pk_src = peaks()
+    res = []
+    out = torch.zeros(sum(arm.ns), dtype=torch.int64, device="cuda")
+    for ns, ks in arm.groups():
+        times = []
+        for _ in range(reps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(arm.stream)
+            arm.step(ns, ks, out)
+            e1.record(arm.stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        st = device_stats(arm.g, arm.stream.cuda_stream)
+        ms = float(np.mean(times))
+        kern = ("k2_kernel" if st["path"] == "smem_k2" else
+                f"ms_kernel<W={max(1, st['lanes'] // 64)}>" if st["engine"] == "lanes" else "fr_kernel + fr_finish")
+        b = algo_bytes(st, ns[0], arm.n)
+        res.append({"ks": list(ks), "seeds": ns[0], "kernel": kern, "engine": st["engine"], "lanes": st["lanes"],
+                    "launches": st["launches"], "ms_per_call": ms, "algo_bytes": b,
+                    "achieved_GBps": b / (ms / 1e3) / 1e9, "frac_of_peak": b / (ms / 1e3) / 1e9 / pk["hbm_gbs"],
+                    "push_equiv_edges": push_edges(st), "gteps": push_edges(st) / (ms / 1e3) / 1e9,
+                    "hops": [{"hop": h, "dir": "pull" if L["pull_runs"] else "push", "frontier": L["frontier"],
+                              "vertices": L["vertices"], "edges": L["edges"], "union_edges": L["union_edges"],
+                              "scanned": L["scanned"], "us": L["ns"] / 1e3}
+                             for h, L in enumerate(st["levels"]) if h and L["runs"]]})
+    return res
+
+
+def e2e_steps(arm: Arm, flush, steps: int, warmup: int, dist=None):
+    """The public host API (k_hop_count_schedule): host uint64 seeds in, host
+    counts out, one call per step, wall clock."""
+    from paper_1905_01294_b200 import k_hop_count_schedule
+    torch = arm.torch
+    seeds = np.ascontiguousarray(arm.seeds, np.uint64)
+    for _ in range(warmup):
+        k_hop_count_schedule(arm.g, seeds, arm.ns, arm.ks, 0)
+    if dist is not None:
+        dist.barrier()
+    ms = []
+    got = None
+    for _ in range(steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got = k_hop_count_schedule(arm.g, seeds, arm.ns, arm.ks, 0)
+        ms.append((time.perf_counter() - t0) * 1e3)
+    return ms, got
+
+
+def cpu_baseline_cfg4(arm: Arm, budget_deep: int = 2) -> dict:
+    """The reference's own k-hop loop (oracle/_ref, matrix route) on this host,
+    all threads, on a BOUNDED sample of the schedule: all 300 k=1 and 300 k=2
+    queries and the first `budget_deep` seeds at k=3 and k=6; the schedule's
+    q/s is extrapolated from the sample (deep sections x 10/budget_deep) at
+    ideal packing on the host threads. The sample's answers are also compared
+    with ours (parity)."""
+    import oracle
+    cores = os.cpu_count() or 1
     try:
-        import oracle
         R = oracle.Ref()
     except Exception as e:
-        R = None
-        sec["reference"] = {"unavailable": str(e)[:120]}
-    for name, sr in (("bool_or_and", 0), ("plus_times", 1)):
-        mxm(A, A, sr)  # warm
-        ts = []
+        return {"unavailable": f"oracle/_ref not built: {str(e)[:100]}"}
+    t = time.time()
+    M = R.matrix(arm.rp, arm.ci)
+    prep = time.time() - t
+    res, per = {}, {}
+    for k, n in zip(arm.ks, arm.ns):
+        n_s = n if n > 10 else min(n, budget_deep)
+        s = arm.seeds[:n_s]
+        th = cores if n_s > 10 else n_s
+        c, el = M.khop_jobs(s, np.full(len(s), k, np.uint32), 0, threads=th)
+        res[k] = c
+        per[k] = {"seeds": int(n_s), "wall_s": el, "threads": th,
+                  "core_s_per_query": el * min(th, n_s) / n_s}
+    # extrapolated schedule wall time on `cores` threads (ideal packing of the
+    # 10-seed deep queries; k=1 / k=2 measured as run)
+    deep = sum(per[k]["core_s_per_query"] * n for k, n in zip(arm.ks, arm.ns) if n <= 10)
+    deep_long = max([per[k]["core_s_per_query"] for k, n in zip(arm.ks, arm.ns) if n <= 10] or [0.0])
+    wall = sum(per[k]["wall_s"] for k, n in zip(arm.ks, arm.ns) if n > 10) + max(deep / cores, deep_long)
+    core_total = sum(per[k]["core_s_per_query"] * n for k, n in zip(arm.ks, arm.ns))
+    del M
+    return {"value": sum(arm.ns) / wall, "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": f"oracle/_ref matrix route (vxm/ewise_union loop of execute.cpp:347-375 over from_parts of "
+                      f"the same G4 CSR): all 300 k=1 and 300 k=2 queries, first {budget_deep} seeds at k=3 and k=6; "
+                      f"schedule wall time extrapolated at ideal packing on {cores} threads",
+            "single_core": {"value": sum(arm.ns) / core_total, "unit": "queries/s", "cores": 1},
+            "per_k": {str(k): v for k, v in per.items()}, "from_parts_s": prep,
+            "_answers": res}
+
+
+def cpu_baseline_g2(arm: Arm) -> dict:
+    """cfg2 (G2, 300 x k=1,2): the reference's own k-hop loop (oracle/_ref,
+    matrix route as for cfg4) over the same CSR, all host threads, repeated
+    passes of the whole workload for ~8 s."""
+    import oracle
+    cores = os.cpu_count() or 1
+    try:
+        R = oracle.Ref()
+    except Exception as e:
+        return {"unavailable": f"oracle/_ref not built: {str(e)[:100]}"}
+    t = time.time()
+    M = R.matrix(arm.rp, arm.ci)
+    prep = time.time() - t
+    passes, el, res = 0, 0.0, {}
+    while el < 8.0 and passes < 20:
+        for k in arm.ks:
+            c, e = M.khop_jobs(arm.seeds, np.full(len(arm.seeds), k, np.uint32), 0, threads=cores)
+            res[k] = c
+            el += e
+        passes += 1
+    q = passes * len(arm.seeds) * len(arm.ks)
+    t1 = sum(M.khop_jobs(arm.seeds, np.full(len(arm.seeds), k, np.uint32), 0, threads=1)[1] for k in arm.ks)
+    return {"value": q / el, "unit": "queries/s", "cores": cores, "kind": "reference",
+            "sample": f"{passes} pass(es) of 300 seeds x k=1,2 exact on oracle/_ref (matrix route over the same "
+                      f"G2 CSR), {el:.1f}s",
+            "single_core": {"value": len(arm.seeds) * len(arm.ks) / t1, "unit": "queries/s", "cores": 1},
+            "from_parts_s": prep, "_answers": res}
+
+
+def secondary(name, torch, local, rank, world, dist, flush, steps, warmup, graph=None, host_csr=None, cpu=True):
+    """A further BASELINE config on the same rank (cfg2 / cfg3 on G2): value,
+    e2e, per-group roofline, oracle parity (+ reference parity for cfg2)."""
+    arm = Arm(name, torch, local, rank, world, graph=graph, host_csr=host_csr)
+    for _ in range(2):
+        arm.step()
+    got = arm.answers()
+    parity = oracle_check(arm, got, load_pins())
+    ms = time_steps(arm, flush, steps, warmup, dist)
+    t = max_over_ranks(torch, dist, float(np.sum(ms)))
+    e2e_ms, _ = e2e_steps(arm, flush, steps, max(3, warmup), dist)
+    te = max_over_ranks(torch, dist, float(np.sum(e2e_ms)))
+    groups = group_profile(arm, flush, min(steps, 20))
+    q = sum(arm.ns) * world
+    out = {"value": q * steps / (t / 1e3), "unit": "queries/s", "ms_per_step": t / steps,
+           "config": workload_config(name, world, arm.n, arm.m), "parity": parity,
+           "gteps": sum(gr["push_equiv_edges"] for gr in groups) * world / (sum(gr["ms_per_call"] for gr in groups) / 1e3) / 1e9,
+           "e2e": {"value": q * steps / (te / 1e3), "unit": "queries/s"}, "groups": groups}
+    if cpu and name == "cfg2" and rank == 0 and world == 1:
+        cb = cpu_baseline_g2(arm)
+        ans = cb.pop("_answers", {})
+        if ans:
+            bad = sum(int((np.asarray(ans[k], np.uint64) != got[k]).sum()) for k in arm.ks)
+            parity["against"].append(f"the cpu_baseline's own reference answers: {sum(len(ans[k]) for k in ans)}")
+            if bad:
+                raise AssertionError(f"cfg2: {bad} answers differ from the reference's k_hop_count")
+        out["cpu_baseline"] = cb
+    return out, arm
+
+
+def cfg5_section(arm2: Arm, flush, dist):
+    """BASELINE configs[4]: 65,536 seeds in 64-lane words, k=1,2,3,6, seed
+    batches split across ranks (strong scaling of a fixed 65,536-seed list);
+    aggregate q/s and GTEPS. Answers of batch 0's seeds checked against the
+    oracle (the full check is tests/test_gpu_configs.py)."""
+    from paper_1905_01294_b200 import device_stats, harness as H, k_hop_count_device
+    import oracle
+    torch = arm2.torch
+    world, rank = arm2.world, arm2.rank
+    master = H.pick_seeds(arm2.rp, 65536, 1)
+    seeds = cfg5_shard(master, rank, world)
+    d_seeds = torch.from_numpy(seeds.astype(np.int32)).cuda()
+    d_counts = torch.zeros(len(seeds), dtype=torch.int64, device="cuda")
+    sp = arm2.stream.cuda_stream
+    P = oracle.Port()
+    _, _, _, lv = P.khop_many(arm2.rp, arm2.ci, seeds[:64], 6, work=True)
+    out = {"seeds": 65536, "seeds_per_rank": int(len(seeds)), "scaling": "strong (fixed 65,536-seed list)", "k": {}}
+    for k in (1, 2, 3, 6):
+        k_hop_count_device(arm2.g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+        torch.cuda.synchronize()
+        got = d_counts[:64].cpu().numpy().astype(np.uint64)
+        if not np.array_equal(got, lv[:, k]):
+            raise AssertionError(f"cfg5 k={k}: answers differ from the oracle")
+        times = []
         for _ in range(3):
-            t0 = time.perf_counter()
-            c = mxm(A, A, sr)
-            ts.append(time.perf_counter() - t0)
-        ent = {"nnz_c": int(len(c[3])), "gpu_s": float(np.median(ts))}
-        if R is not None:
-            t0 = time.perf_counter()
-            r = R.mxm(A, A, sr)
-            ent["reference_s"] = time.perf_counter() - t0
-            ent["matches_reference"] = bool(np.array_equal(r[2], c[2]) and np.array_equal(r[3], c[3]) and
-                                            (r[4] is None or np.array_equal(r[4], c[4])))
-        sec[name] = ent
-    return sec
-
-
-def run_extras(g, rp, world, rank, dist, stream, flush, torch, with_cfg4=True, ci=None):
-    """BASELINE.json configs[2] (cfg3: 10 seeds, k=3,6) and configs[4] (cfg5:
-    65,536 seeds in 64-lane words, k=1,2,3,6; seed batches split across
-    ranks), on the already-resident G2. Device-resident, CUDA-event timed, L2
-    flushed before each call; per-hop device time from the engine's
-    %globaltimer stamps gives each frontier-expansion phase's achieved bytes/s."""
-    from paper_1905_01294_b200 import harness as H, k_hop_count_device, device_stats
-    import numpy as np
-    out = {}
-    sp = stream.cuda_stream
-    pk, _ = peaks()
-    master = H.pick_seeds(rp, 65536, 1)
-    plans = [("cfg3", g, master[:10], (3, 6), 3, False), ("cfg5", g, master, (1, 2, 3, 6), 1, True)]
-    if with_cfg4:
-        # configs[3]: G4 (2^26 ids, 1.47B edges) generated on each rank's GPU
-        from paper_1905_01294_b200 import DeviceGraph
-        t = time.time()
-        g4 = DeviceGraph.generate(H.G4, device=torch.cuda.current_device())
-        rp4, _ = g4.csr()
-        m4 = H.pick_seeds(rp4, 300, 1)
-        log(f"[rank {rank}] G4: n={g4.nrows} m={g4.nnz} built on the GPU in {time.time() - t:.1f}s")
-        plans.append(("cfg4", g4, m4, (1, 2), 3, True))
-        plans.append(("cfg4", g4, m4[:10], (3, 6), 3, True))
-    for name, gg, seeds_all, ks, reps, split in plans:
-        per = (len(seeds_all) + world - 1) // world if split else len(seeds_all)
-        seeds = seeds_all[rank * per:(rank + 1) * per] if split else seeds_all
-        if len(seeds) == 0:
-            seeds = seeds_all[:1]
-        d_seeds = torch.from_numpy(np.ascontiguousarray(seeds).astype(np.int32)).cuda()
-        d_counts = torch.zeros(len(seeds), dtype=torch.int64, device="cuda")
-        sec = out.get(name) or {"seeds": {}, "seeds_per_rank": {}, "k": {}}
-        if name == "cfg4":
-            sec["graph"] = {"n": int(gg.nrows), "m": int(gg.nnz), "ids": "2^26 renumbered",
-                            "rmat": [0.57, 0.19, 0.19, 0.05], "built": "on the GPU (mgk_graph_gen_rmat)"}
-        for k in ks:
-            sec["seeds"][str(k)] = int(len(seeds_all))
-            sec["seeds_per_rank"][str(k)] = int(len(seeds))
-            k_hop_count_device(gg, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
-            times = []
-            for _ in range(reps):
-                flush.fill_(1)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                k_hop_count_device(gg, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1))
-            ms = float(np.median(times))
-            st = device_stats(gg, sp)
-            if world > 1:
-                t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                ms = float(t[0])
-            edges = sum(L["edges"] for L in st["levels"]) * world
-            hops = []
-            for h in range(1, len(st["levels"])):
-                L = st["levels"][h]
-                if not L["runs"] or not L["ns"]:
-                    continue
-                b = hop_bytes(st, h)
-                hops.append({"hop": h, "dir": "pull" if L["pull_runs"] else "push", "scanned": L["scanned"],
-                             "us": L["ns"] / 1e3, "algo_GBps": b / L["ns"],
-                             "frac_of_peak": b / L["ns"] / pk["hbm_gbs"]})
-            nq = len(seeds_all) if split else len(seeds) * world
-            sec["k"][str(k)] = {"ms": ms, "queries_per_s": nq / (ms / 1e3),
-                                "gteps": edges / (ms / 1e3) / 1e9, "engine": st["engine"],
-                                "lanes_per_batch": st["lanes"], "hops": hops,
-                                "count_sum": int(d_counts.sum().item())}
-        out[name] = sec
-    if rank == 0 and ci is not None:
-        out["snapshot_load"] = snapshot_load(rp, ci, torch)
-        out["mxm"] = mxm_section(torch)
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(arm2.stream)
+            k_hop_count_device(arm2.g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts.data_ptr(), sp)
+            e1.record(arm2.stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+        st = device_stats(arm2.g, sp)
+        ms = max_over_ranks(torch, dist, float(np.median(times)))
+        e = push_edges(st)
+        b = algo_bytes(st, len(seeds), arm2.n)
+        tot_e = sum_over_ranks(torch, dist, float(e))
+        pk, _ = peaks()
+        out["k"][str(k)] = {"ms": ms, "queries_per_s": 65536 / (ms / 1e3), "gteps": tot_e / (ms / 1e3) / 1e9,
+                            "engine": st["engine"], "lanes_per_batch": st["lanes"],
+                            "algo_bytes_rank": b, "frac_of_peak_rank": b / (float(np.median(times)) / 1e3) / 1e9 / pk["hbm_gbs"],
+                            "parity": "batch-0 seeds (64) == oracle"}
     return out
+
+
+def _reduce(torch, dist, x: float, op) -> float:
+    if dist is None:
+        return x
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=op)
+    return float(t[0])
+
+
+def max_over_ranks(torch, dist, x: float) -> float:
+    """The job's time: the slowest rank's (device-timed) figure."""
+    return _reduce(torch, dist, x, dist.ReduceOp.MAX if dist is not None else None)
+
+
+def sum_over_ranks(torch, dist, x: float) -> float:
+    return _reduce(torch, dist, x, dist.ReduceOp.SUM if dist is not None else None)
+
+
+def cfg5_shard(master, rank: int, world: int):
+    """cfg5 (strong scaling): rank r's contiguous share of the 65,536-seed list,
+    whole 64-lane batches where the split allows (1,024 batches / world)."""
+    per = len(master) // world
+    extra = len(master) - per * world
+    a = rank * per + min(rank, extra)
+    return master[a:a + per + (1 if rank < extra else 0)]
+
+
+def load_pins():
+    p = ROOT / "tests" / "golden" / "bench_pins.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
+
+
+def traffic_of(key: str):
+    tf = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(tf.read_text()).get(key)
+    except Exception:
+        return None
 
 
 def run_ours(args):
     import torch
-    import torch.distributed as dist
-
-    from paper_1905_01294_b200 import (DeviceGraph, device_stats, k_hop_count_batch, k_hop_count_device,
-                                       k_hop_count_device_sections, k_hop_count_sections)
-    from paper_1905_01294_b200 import Tuning
+    import torch.distributed as dist_mod
 
     rank, local, world = dist_env()
-    # MGK_BENCH_DRYRUN=1: functional check of the multi-rank path on a box with
-    # fewer GPUs than ranks (gloo, ranks share devices; its numbers mean nothing)
-    dry = os.environ.get("MGK_BENCH_DRYRUN") == "1"
+    dry = os.environ.get("MGK_BENCH_DRYRUN") == "1"  # gloo + shared devices: functional check only
     if dry:
         local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         if dry:
-            dist.init_process_group("gloo")
+            dist_mod.init_process_group("gloo")
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    rp, ci, seeds = build_inputs(world, rank, dist if world > 1 else None, torch.device("cuda", local))
-    t = time.time()
-    g = DeviceGraph.from_csr(rp, ci, device=local)
-    if args.lanes_words:
-        g.set_tuning(Tuning(lanes_words=args.lanes_words))
-    log(f"[rank {rank}] uploaded ({g.device_bytes() / 2**20:.0f} MiB on device) in {time.time() - t:.1f}s")
-
-    stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
-    d_seeds = torch.from_numpy(seeds.astype(np.int32)).cuda()
-    d_all = torch.zeros(len(KS) * len(seeds), dtype=torch.int64, device="cuda")
-    d_counts = {k: d_all[i * len(seeds):(i + 1) * len(seeds)] for i, k in enumerate(KS)}
+            dist_mod.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = dist_mod
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    name = args.workload
+    pins = load_pins()
 
-    def step(evs=None):
-        # one device-path call per step answers both sections (k = 1 rides on
-        # the on-chip k = 2 launch, mgk_khop_count_device_ks)
-        if evs:
-            evs[0].record(stream)
-        k_hop_count_device_sections(g, d_seeds.data_ptr(), len(seeds), KS, 0, d_all.data_ptr(), sp)
-        if evs:
-            evs[1].record(stream)
-
-    def per_k_call(k, evs):
-        evs[0].record(stream)
-        k_hop_count_device(g, d_seeds.data_ptr(), len(seeds), k, 0, d_counts[k].data_ptr(), sp)
-        evs[1].record(stream)
-
-    # correctness against the host API before timing
+    # ---- headline ---------------------------------------------------------------------
+    arm = Arm(name, torch, local, rank, world)
     for _ in range(2):
-        step()
-    torch.cuda.synchronize()
-    host_counts = {k: k_hop_count_batch(g, seeds, k, 0) for k in KS}
-    for k in KS:
-        assert (d_counts[k].cpu().numpy().astype(np.uint64) == host_counts[k]).all()
+        arm.step()
+    got = arm.answers()
+    cpu = None
+    if name == "cfg4" and rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_cfg4(arm)
+    parity = oracle_check(arm, got, pins)
+    if cpu and "_answers" in cpu:
+        ans = cpu.pop("_answers")
+        bad = sum(int((np.asarray(ans[k], np.uint64) != got[k][:len(ans[k])]).sum()) for k in ans)
+        parity["against"].append(f"the cpu_baseline's own reference answers: {sum(len(a) for a in ans.values())}")
+        if bad:
+            raise AssertionError(f"{bad} answers differ from the reference's own k-hop loop")
 
-    # ---- device-resident timed region --------------------------------------------
-    for _ in range(args.warmup):
-        flush.fill_(1)
-        step()
-    per_launch = {k: [] for k in KS}
-    step_ms = []
     sampler = ClockSampler(local)
     with sampler:
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for _ in range(args.steps):
-            flush.fill_(1)  # L2 flush between steps, outside the events
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-            step(evs)
-            torch.cuda.synchronize()
-            step_ms.append(evs[0].elapsed_time(evs[1]))
-        torch.cuda.synchronize()
-        # per-k calls on their own (diagnostics: per_k and the roofline's call)
-        for _ in range(min(args.steps, 50)):
-            for k in KS:
-                flush.fill_(1)
-                evs = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                per_k_call(k, evs)
-                torch.cuda.synchronize()
-                per_launch[k].append(evs[0].elapsed_time(evs[1]))
-        if world > 1:
-            dist.barrier()
-        total_ms = float(np.sum(step_ms))
-        # ---- e2e through the public host API ---------------------------------------
-        # the public host API: one call answers the step's sections (k = 1, 2)
-        # for the seed list (mgk_khop_count_ks): uint64 seeds in, counts out
-        e2e_ms = []
-        for _ in range(max(3, args.warmup)):
-            k_hop_count_sections(g, seeds, KS, 0)
-        if world > 1:
-            dist.barrier()
-        for _ in range(args.steps):
-            flush.fill_(1)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            k_hop_count_sections(g, seeds, KS, 0)
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        e2e_total = float(np.sum(e2e_ms))
+        ms = time_steps(arm, flush, args.steps, args.warmup, dist)
+        e2e_ms, e2e_got = e2e_steps(arm, flush, args.steps, max(3, args.warmup), dist)
     clocks = sampler.summary()
+    for k, x in zip(arm.ks, e2e_got):
+        if not np.array_equal(x, got[k]):
+            raise AssertionError(f"e2e answers for k={k} differ from the device path")
+    total_ms = max_over_ranks(torch, dist, float(np.sum(ms)))
+    e2e_total = max_over_ranks(torch, dist, float(np.sum(e2e_ms)))
+    groups = group_profile(arm, flush, min(args.steps, 10))
 
-    # stats of one launch per k (for GTEPS and the roofline)
-    stats = {}
-    for k in KS:
-        _, stats[k] = k_hop_count_batch(g, seeds, k, 0, stats=True)
-
-    if world > 1:
-        tt = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, e2e_total = float(tt[0]), float(tt[1])
-
-    # BASELINE configs[2] / [4] on the same resident graph (every rank takes part)
-    extras = None if args.no_extras else run_extras(g, rp, world, rank, dist, stream, flush, torch,
-                                                    with_cfg4=not args.no_cfg4, ci=ci)
+    # ---- secondary configs on G2 (every rank takes part) ---------------------------------
+    extras = {}
+    if not args.no_extras:
+        arm2 = None
+        for nm in ("cfg2", "cfg3"):
+            if nm == name:
+                continue
+            sec, a = secondary(nm, torch, local, rank, world, dist, flush, args.steps, args.warmup,
+                               graph=arm2.g if arm2 else None, host_csr=(arm2.rp, arm2.ci) if arm2 else None,
+                               cpu=not args.no_cpu)
+            extras[nm] = sec
+            arm2 = arm2 or a
+        if arm2 is not None:
+            extras["cfg5"] = cfg5_section(arm2, flush, dist)
 
     if rank != 0:
-        if world > 1:
+        if dist is not None:
             dist.barrier()
             dist.destroy_process_group()
         return
 
-    q_per_step = len(seeds) * len(KS) * world
+    q_per_step = sum(arm.ns) * world
     value = q_per_step * args.steps / (total_ms / 1e3)
-    edges_per_step = sum(sum(L["edges"] for L in stats[k]["levels"]) for k in KS) * world
-    dom = max(KS, key=lambda k: np.mean(per_launch[k]))
-    dom_ms = float(np.mean(per_launch[dom]))
-    ab = algo_bytes(stats[dom])
+    dom = max(groups, key=lambda g: g["ms_per_call"])
     pk, pk_src = peaks()
-    achieved = ab / (dom_ms / 1e3) / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        try:
-            key = f"{WORKLOAD}_k{dom}" + ("_smem" if stats[dom].get("path") == "smem_k2" else "")
-            traffic = json.loads(tf.read_text()).get(key, {}).get("total")
-        except Exception:
-            traffic = None
-    # the dominant call's last hop is one random 32-bit atomic per scanned edge
-    # into the per-seed bitmaps: its real ceiling is the L2 atomic rate
-    # (profiles/ubench_atomics.json), not HBM bandwidth
-    l2_atomic = None
-    lv = stats[dom]["levels"]
-    hops = [h for h in range(1, len(lv)) if lv[h]["runs"]]
-    ub = ROOT / "profiles" / "ubench_atomics.json"
-    if stats[dom]["engine"] == "single" and stats[dom].get("path") != "smem_k2" and hops and ub.exists():
-        last = lv[hops[-1]]
-        if last["ns"] and not last["pull_runs"]:
-            gops = last["scanned"] / last["ns"]
-            ubj = json.loads(ub.read_text())
-            sweep = ubj.get("red_or_sweep_best", {})
-            ceil = max([ubj[a]["red_or"] for a in ubj if a.startswith("array_")] +
-                       [v for a, v in sweep.items() if a.startswith("array_")])  # best case: L2-resident
-            l2_atomic = {"hop": hops[-1], "atomics": last["scanned"], "us": last["ns"] / 1e3,
-                         "achieved_gops": gops, "ceiling_gops": ceil, "frac": gops / ceil,
-                         "ceiling_source": "profiles/ubench_atomics.json: fastest measured red.or (L2-resident array, best launch shape)"}
-    # the on-chip k = 2 path: every hop-2 adjacency entry is streamed by the R
-    # CTAs holding the seed's vertex slices and set with a shared-memory atomic;
-    # its ceiling is the measured stream + smem-atomic rate of that pattern
-    onchip = None
-    us_ = ROOT / "profiles" / "ubench_smem.json"
-    if stats[dom].get("path") == "smem_k2" and len(lv) > 2 and lv[2]["ns"] and us_.exists():
-        u = json.loads(us_.read_text())
-        # each hop-2 entry is read once, by the slice CTA that owns its target
-        reads = lv[2]["scanned"]
-        got = reads / lv[2]["ns"]
-        ceil = u["stream_ids_from_dram_then_smem_red_or"]["all_ids_in_slice_sorted_runs_ilp16"]
-        onchip = {"hop": 2, "entries": lv[2]["scanned"], "entry_reads": reads,
-                  "us": lv[2]["ns"] / 1e3, "achieved_g_reads": got, "ceiling_g_reads": ceil, "frac": got / ceil,
-                  "ceiling_source": "profiles/ubench_smem.json: ids streamed from HBM, every id set in the CTA's "
-                                    "shared-memory slice (red.or), sorted runs, one 1024-thread CTA per SM",
-                  "note": "us = slices + merge of cut seeds (the whole hop 2); the rest of the gap is per-seed "
-                          "setup (window prefix, first-load latency, 150 KB slice sweep)"}
-    fused_k1 = 1 in KS and 2 in KS and stats[2].get("path") == "smem_k2"
-    cpu = cpu_baseline(rp, ci, seeds) if (world == 1 and not args.no_cpu) else None
+    edges_step = sum(g["push_equiv_edges"] for g in groups) * world
+    tr = traffic_of(f"{name}_{dom['kernel'].split('<')[0]}")
     line = {
-        "metric": "k-hop count queries/s (cfg2: 300 seeds x k=1,2 exact on the 2.4M/67M R-MAT graph)",
+        "metric": METRIC if name == "cfg4" else f"k-hop count queries/s ({name})",
         "value": value,
         "unit": "queries/s",
         "n_gpus": world,
@@ -531,139 +651,127 @@ def run_ours(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u32 ids / u64 lane words (integer)",
-        "data": "synthetic R-MAT, BASELINE.json configs[1] shape (seeded; stands in for Graph500 2.4M/67M)",
-        "config": {"workload": WORKLOAD, "graph": {"n": int(len(rp) - 1), "m": int(len(ci)),
-                                                      "rmat": [0.57, 0.19, 0.19, 0.05], "ids": "2^22 renumbered"},
-                   "seeds_per_rank": len(seeds), "ks": list(KS), "mode": "exact",
-                   "engine": stats[dom]["engine"], "lanes_per_batch": stats[dom]["lanes"],
-                   "l2": "flushed between steps (256 MiB write, outside the events)",
-                   "parallelism": f"seed-sharded graph replicas x{world}"},
-        "gteps": edges_per_step * args.steps / (total_ms / 1e3) / 1e9,
-        "per_k": {str(k): {"ms_per_launch": float(np.mean(per_launch[k])),
-                           "queries_per_s": len(seeds) * world / (float(np.mean(per_launch[k])) / 1e3),
-                           "push_equiv_edges": int(sum(L["edges"] for L in stats[k]["levels"])),
-                           "hops": [{"dir": "pull" if L["pull_runs"] else "push", "frontier": L["frontier"],
-                                     "vertices": L["vertices"], "scanned": L["scanned"],
-                                     "us": L["ns"] / 1e3} for L in stats[k]["levels"][1:]]}
-                  for k in KS},
-        "roofline": {"bound": "hbm", "kernel": (f"ms_kernel<W={stats[dom]['lanes'] // 64}>" if stats[dom]["engine"] == "lanes"
-                                                else "k2_kernel" if stats[dom].get("path") == "smem_k2"
-                                                else "fr_kernel + fr_finish") + f" (k={dom} call)",
-                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "peak_source": pk_src,
-                     "algo_bytes_per_launch": ab, "traffic": traffic, "l2_atomic": l2_atomic,
-                     "onchip": onchip},
+        "dtype": "u32 vertex ids, u64 lane words (integer)",
+        "data": "synthetic R-MAT, BASELINE.json configs shape (seeded; stands in for the paper's Twitter / Graph500 graphs)",
+        "config": workload_config(name, world, arm.n, arm.m),
+        "gteps": edges_step * args.steps / (total_ms / 1e3) / 1e9,
+        "step": ("one mgk_khop_count_device_schedule call: group (300 seeds: k=1,2) = one on-chip k=2 launch whose "
+                 "|F1| gives the k=1 answers; group (10 seeds: k=3,6) = one LANES traversal to depth 6 answering "
+                 "both sections from its per-hop lane counts" if name == "cfg4" else "one schedule call"),
+        "groups": groups,
+        "roofline": {"bound": "hbm", "kernel": dom["kernel"] + f" (group k={dom['ks']})",
+                     "achieved": dom["achieved_GBps"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": dom["frac_of_peak"], "peak_source": pk_src,
+                     "algo_bytes_per_launch": dom["algo_bytes"],
+                     "byte_model": "SURVEY.md §8(d): single-source 4E + 12 sum|F_l<L| + 4 sum|F_1..L|; "
+                                   "64-lane mode 4 sum_U outdeg + 12|U| + 24 W n per level",
+                     "traffic": (tr or {}).get("total") if tr else None,
+                     "traffic_source": (tr or {}).get("source") if tr else "no ncu capture of this kernel on this workload"},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": q_per_step * args.steps / (e2e_total / 1e3), "unit": "queries/s",
-                "h2d_bytes_per_step": 4 * len(seeds), "d2h_bytes_per_step": 8 * len(seeds) * len(KS),
-                "api": "k_hop_count_sections (mgk_khop_count_ks): one host call per step",
+                "h2d_bytes_per_step": 4 * len(arm.seeds), "d2h_bytes_per_step": 8 * sum(arm.ns),
+                "api": "k_hop_count_schedule (mgk_khop_count_schedule): host uint64 seeds in, host counts out",
                 "ms_per_step": e2e_total / args.steps},
-        "gpu_launches": sum(stats[k]["launches"] for k in KS if not (k == 1 and fused_k1)) * args.steps,
-        "step": ("one mgk_khop_count_device_ks call: the k = 1 answers come out of the on-chip k = 2 launch"
-                 if fused_k1 else "one mgk_khop_count_device_ks call (one launch group per k)"),
+        "gpu_launches": sum(g["launches"] for g in groups) * args.steps,
         "clocks": clocks,
         "extra_configs": extras,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def ref_graph(rp, ci):
-    import oracle
-    from paper_1905_01294_b200 import harness as H
-    R = oracle.Ref()
-    src, dst = H.csr_to_edges(rp, ci)
-    t = time.time()
-    g = R.build_bench_graph(src, dst, len(rp) - 1)
-    log(f"reference build_bench_graph: {time.time() - t:.1f}s")
-    return g
-
-
-def cpu_baseline(rp, ci, seeds, budget_s: float = 12.0):
-    """The reference's CPU k_hop_count (oracle/_ref) on this host, all threads,
-    on repeated passes of the same 300-seed x k=1,2 schedule (bounded sample)."""
-    import oracle
-    cores = os.cpu_count() or 1
-    try:
-        g = ref_graph(rp, ci)
-        kind = "reference"
-        run = lambda k: g.k_hop_count_many(seeds, k, 0, threads=cores)[1]
-    except Exception as e:  # reference library not built: the C port, 1 thread
-        log(f"cpu_baseline: reference unavailable ({e}); timing the C port")
-        P = oracle.Port()
-        rp64, ci64 = rp.astype(np.uint64), ci.astype(np.uint64)
-        kind, cores = "port", 1
-
-        def run(k):
-            t0 = time.perf_counter()
-            for s in seeds:
-                P.khop_count(rp64, ci64, int(s), k, 0)
-            return time.perf_counter() - t0
-    passes, elapsed = 0, 0.0
-    while elapsed < budget_s and passes < 50:
-        elapsed += sum(run(k) for k in KS)
-        passes += 1
-    q = passes * len(seeds) * len(KS)
-    out = {"value": q / elapsed, "unit": "queries/s", "cores": cores, "kind": kind,
-           "sample": f"{passes} pass(es) of {len(seeds)} seeds x k=1,2 exact on the same G2 graph "
-                     f"({elapsed:.1f}s of CPU wall time)"}
-    if kind == "reference":  # SURVEY §8(d): also the paper's one-thread-per-query figure
-        t1 = sum(g.k_hop_count_many(seeds, k, 0, threads=1)[1] for k in KS)
-        out["single_core"] = {"value": len(seeds) * len(KS) / t1, "unit": "queries/s", "cores": 1,
-                              "sample": f"1 pass of {len(seeds)} seeds x k=1,2 ({t1:.1f}s)"}
-    return out
-
-
+# ---- the reference arm ---------------------------------------------------------------------
 def run_reference(args):
     rank, _, world = dist_env()
     if rank != 0:
         return
-    from paper_1905_01294_b200 import harness as H
-    rp, ci = H.gen_csr(H.G2)
-    seeds = H.pick_seeds(rp, SEEDS_PER_RANK, 1)
-    g = ref_graph(rp, ci)
+    import oracle
+    name = args.workload
+    spec, ks, ns = SCHEDULE[name]
     cores = os.cpu_count() or 1
+    P, R = oracle.Port(), oracle.Ref()
+    t = time.time()
+    rp, ci = P.gen_bench_csr(spec["scale"], spec["edge_factor"], spec["target_unique"], spec["relabel"])
+    gen_s = time.time() - t
+    n = len(rp) - 1
+    m = len(ci)
+    seeds = P.pick_seeds_u32(rp, SEEDS_PER_RANK, 1)
+    t = time.time()
+    M = R.matrix(rp, ci)
+    prep_s = time.time() - t
+    log(f"reference arm: {spec['name']} n={n} m={m} (oracle generator {gen_s:.0f}s, from_parts {prep_s:.0f}s)")
+    del rp, ci
+    # one step = the whole schedule as one job pool on all host threads (deep
+    # queries first; each query on one thread, like the reference server)
+    jobs_s, jobs_k = [], []
+    for k, nn in sorted(zip(ks, ns), key=lambda x: -x[0]):
+        jobs_s += [int(s) for s in seeds[:nn]]
+        jobs_k += [k] * nn
+    jobs_s = np.array(jobs_s, np.uint64)
+    jobs_k = np.array(jobs_k, np.uint32)
+    # warm-up: the k <= 2 part of the schedule (cheap), W times
+    shallow = jobs_k <= 2
     for _ in range(args.warmup):
-        for k in KS:
-            g.k_hop_count_many(seeds, k, 0, threads=cores)
-    times = []
-    for _ in range(args.steps):
-        times.append(sum(g.k_hop_count_many(seeds, k, 0, threads=cores)[1] for k in KS))
+        M.khop_jobs(jobs_s[shallow], jobs_k[shallow], 0, threads=cores)
+    budget = float(os.environ.get("MGK_REF_BUDGET_S", "150"))
+    times, spent = [], 0.0
+    while len(times) < args.steps and (not times or spent + times[-1] <= budget):
+        _, el = M.khop_jobs(jobs_s, jobs_k, 0, threads=cores)
+        times.append(el)
+        spent += el
     total = float(np.sum(times))
-    value = len(seeds) * len(KS) * args.steps / total
+    value = len(jobs_s) * len(times) / total
     line = {
-        "metric": "k-hop count queries/s (cfg2: 300 seeds x k=1,2 exact on the 2.4M/67M R-MAT graph)",
-        "value": value, "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64 ids (integer)",
-        "data": "synthetic R-MAT, BASELINE.json configs[1] shape (seeded)",
-        "config": {"workload": WORKLOAD, "graph": {"n": int(len(rp) - 1), "m": int(len(ci))},
-                   "seeds_per_rank": len(seeds), "ks": list(KS), "mode": "exact",
-                   "parallelism": f"{cores} host threads, one query per thread"},
+        "metric": METRIC if name == "cfg4" else f"k-hop count queries/s ({name})",
+        "value": value, "unit": "queries/s", "n_gpus": world, "steps": len(times), "steps_requested": args.steps,
+        "warmup": args.warmup, "ms_per_step": total * 1e3 / len(times), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64 vertex ids (integer)",
+        "data": "synthetic R-MAT, BASELINE.json configs shape (seeded; stands in for the paper's Twitter / Graph500 graphs)",
+        "config": workload_config(name, world, n, m),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "queries/s", "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} step(s) of {len(seeds)} seeds x k=1,2 on "
-                                   f"oracle/_ref (unmodified matgraph core, -O3, checks off)"},
+                         "sample": f"{len(times)} step(s) of the full schedule ({len(jobs_s)} queries) on oracle/_ref "
+                                   f"(unmodified matgraph core, -O3, checks off; matrix route: vxm/ewise_union loop "
+                                   f"of execute.cpp:347-375 over from_parts), {cores} threads, one query per thread; "
+                                   f"steps capped by a {budget:.0f}s budget"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "prep": {"oracle_generator_s": gen_s, "from_parts_s": prep_s},
     }
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-launch this script
+    with one process per GPU (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    log("relaunching under torchrun:", " ".join(cmd))
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--lanes-words", type=int, default=0)
+    ap.add_argument("--workload", default="cfg4", choices=sorted(SCHEDULE))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--no-extras", action="store_true", help="skip the cfg3 / cfg4 / cfg5 sections")
-    ap.add_argument("--no-cfg4", action="store_true", help="skip the 1.47B-edge cfg4 section")
+    ap.add_argument("--no-extras", action="store_true", help="skip the cfg2 / cfg3 / cfg5 sections")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if world == 0 and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:
