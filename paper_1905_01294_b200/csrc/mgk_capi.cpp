@@ -176,6 +176,21 @@ int pick_words(const Graph* g, uint64_t nseeds) {
     return W;
 }
 
+// LANES lane-word width: batches of at most 8 / 16 seeds use one uint8 /
+// uint16 word per vertex (state arrays 8x / 4x smaller, so a dense pull's
+// per-edge gathers stay in L2 on large graphs); wider batches use uint64
+// words. MGK_LANE_BITS=8|16|64 forces a width (tests; a forced narrow width
+// wider batches cannot use falls back to 64).
+int pick_lane_bits(const Graph* g, uint64_t nseeds) {
+    if (g->tuning.lanes_words) return 64;
+    int bits = nseeds <= 8 ? 8 : nseeds <= 16 ? 16 : 64;
+    if (const char* e = std::getenv("MGK_LANE_BITS")) {
+        const int f = std::atoi(e);
+        if (f == 8 || f == 16 || f == 64) bits = f;
+    }
+    return (bits < 64 && nseeds > (uint64_t)bits) ? 64 : bits;
+}
+
 int check_query(const Graph* g, const uint64_t* seeds, uint64_t nseeds, uint32_t k) {
     // execute.cpp:348-354: seed first, then k
     for (uint64_t i = 0; i < nseeds; ++i)
@@ -251,8 +266,9 @@ cudaError_t run_engine(Graph* g, Workspace* ws, const uint32_t* d_seeds, uint64_
         e = launch_single(L);
         *W_out = 0;
     } else {
-        L.lanes_words = pick_words(g, nseeds);
-        *W_out = L.lanes_words;
+        L.lane_bits = pick_lane_bits(g, nseeds);
+        L.lanes_words = L.lane_bits == 64 ? pick_words(g, nseeds) : 1;
+        *W_out = L.lane_bits == 64 ? 64 * L.lanes_words : L.lane_bits;  // lanes per batch
         e = launch_lanes(L);
     }
     *grid = L.grid;
@@ -290,7 +306,7 @@ void fill_stats(mgk_stats* st, const LevelCounters* lc, int engine, int W, uint6
     std::memset(st, 0, sizeof *st);
     st->path = path;
     st->engine = (uint32_t)engine;
-    st->lanes = engine == MGK_ENGINE_LANES ? 64u * (uint32_t)W : 1u;
+    st->lanes = engine == MGK_ENGINE_LANES ? (uint32_t)W : 1u;  // W = lanes per batch
     st->batches = (uint32_t)(engine == MGK_ENGINE_LANES ? (nseeds + st->lanes - 1) / st->lanes : nseeds);
     st->grid = grid;
     st->block = block;

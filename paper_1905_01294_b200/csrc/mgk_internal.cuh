@@ -209,6 +209,7 @@ struct Launch {
     cudaStream_t stream;
     Tuning tuning;
     int lanes_words;  // LANES engine only
+    int lane_bits = 64;  // LANES: 64 (lanes_words uint64 words per vertex), or 16 / 8 (one narrow word)
     bool keep_result = false;  // SINGLE: leave slot 0's bitmaps for k_hop_frontier
     // d_seeds / d_counts are mapped pinned HOST memory (host calls, SINGLE):
     // each group's seeds then travel inside its launch and the answers are

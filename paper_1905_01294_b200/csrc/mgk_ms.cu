@@ -20,6 +20,8 @@
 // touches: a discovery list per hop (raw list R, one entry per vertex whose
 // F' became non-zero) drives the finalize pass, the clearing of the previous
 // frontier and the final clearing of V.
+#include <type_traits>
+
 #include "mgk_device.cuh"
 
 namespace mgk {
@@ -110,6 +112,66 @@ __device__ __forceinline__ void store_lw(unsigned long long* p, const LaneWord<W
     }
 }
 
+// Lane-word storage. NB = 64: W uint64 words per vertex (64 W lanes).
+// NB = 16 / 8 (W = 1): a uint16 / uint8 per vertex for batches of at most 16 /
+// 8 seeds, so the state arrays of a 35.6M-vertex graph (G4) are 71 / 36 MB
+// instead of 285 MB and the per-edge gathers of a dense pull hit L2.
+// Narrow words are OR-ed with a 32-bit atomic on the containing word (the
+// other sub-words' mask bits are zero); plain sub-word stores elsewhere touch
+// only their own bytes.
+template <int W, int NB>
+struct LS;
+
+template <int W>
+struct LS<W, 64> {
+    static constexpr uint32_t kLanes = 64 * W;
+    __device__ static __forceinline__ LaneWord<W> load(const unsigned long long* b, size_t v) {
+        return load_lw<W>(b + v * W);
+    }
+    __device__ static __forceinline__ LaneWord<W> load_cg(const unsigned long long* b, size_t v) {
+        return load_lw_cg<W>(b + v * W);
+    }
+    __device__ static __forceinline__ void store(unsigned long long* b, size_t v, const LaneWord<W>& x) {
+        store_lw<W>(b + v * W, x);
+    }
+    __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
+        atomicOr(b + v * W + i, m);
+    }
+    __host__ __device__ static constexpr size_t words64(size_t n) { return n * W; }
+};
+
+template <int NB>
+struct LSNarrow {
+    static_assert(NB == 8 || NB == 16, "narrow lane words are 8 or 16 bits");
+    using T = typename std::conditional<NB == 16, unsigned short, unsigned char>::type;
+    static constexpr uint32_t kLanes = NB;
+    __device__ static __forceinline__ LaneWord<1> load(const unsigned long long* b, size_t v) {
+        LaneWord<1> r;
+        r.w[0] = reinterpret_cast<const T*>(b)[v];
+        return r;
+    }
+    __device__ static __forceinline__ LaneWord<1> load_cg(const unsigned long long* b, size_t v) {
+        LaneWord<1> r;
+        if constexpr (NB == 16)
+            r.w[0] = __ldcg(reinterpret_cast<const unsigned short*>(b) + v);
+        else
+            r.w[0] = __ldcg(reinterpret_cast<const unsigned char*>(b) + v);
+        return r;
+    }
+    __device__ static __forceinline__ void store(unsigned long long* b, size_t v, const LaneWord<1>& x) {
+        reinterpret_cast<T*>(b)[v] = (T)x.w[0];
+    }
+    __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int, unsigned long long m) {
+        constexpr uint32_t per = 32 / NB;
+        atomicOr(reinterpret_cast<unsigned int*>(b) + v / per, (unsigned int)m << (NB * (v % per)));
+    }
+    __host__ __device__ static constexpr size_t words64(size_t n) { return (n * NB + 63) / 64; }
+};
+template <>
+struct LS<1, 16> : LSNarrow<16> {};
+template <>
+struct LS<1, 8> : LSNarrow<8> {};
+
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.items1 : P.items0;
 }
@@ -165,7 +227,7 @@ __device__ __forceinline__ void count_discovered(const DevGraph& g, uint32_t u, 
 }
 
 // ---- push expand -----------------------------------------------------------------
-template <int W>
+template <int W, int NB>
 __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
                            const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
                            QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
@@ -190,8 +252,8 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
             uint32_t u = 0;
             if (valid) {
                 u = __ldg(g.ci + pos);
-                const LaneWord<W> f = load_lw<W>(Fc + (size_t)src * W);
-                const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
+                const LaneWord<W> f = LS<W, NB>::load(Fc, src);
+                const LaneWord<W> vis = LS<W, NB>::load(P.V, u);
                 LaneWord<W> m;
                 bool any = false;
 #pragma unroll
@@ -200,13 +262,12 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
                     any |= m.w[i] != 0;
                 }
                 if (any) {
-                    unsigned long long* fn = Fn + (size_t)u * W;
-                    const LaneWord<W> cur = load_lw_cg<W>(fn);
+                    const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u);
                     bool need = false;
 #pragma unroll
                     for (int i = 0; i < W; ++i) {
                         if ((cur.w[i] & m.w[i]) != m.w[i]) {
-                            atomicOr(fn + i, m.w[i]);
+                            LS<W, NB>::atomic_or(Fn, u, i, m.w[i]);
                             need = true;
                         }
                     }
@@ -258,7 +319,7 @@ __device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>
 
 // Warp-wide: OR of the lane words of in-neighbours ri[b..e), stopping early
 // once `need` is covered. Returns the OR (all lanes) and the entries read.
-template <int W>
+template <int W, int NB>
 __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
                                                        uint32_t b, uint32_t e, const LaneWord<W>& need,
                                                        uint32_t& scanned) {
@@ -271,7 +332,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
         const uint32_t pe = min(e, p0 + 256);
 #pragma unroll 2
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = load_lw<W>(Fc + (size_t)__ldg(P.g.ri + p) * W);
+            const LaneWord<W> f = LS<W, NB>::load(Fc, __ldg(P.g.ri + p));
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -299,7 +360,7 @@ struct ChunkGrab {
     }
 };
 
-template <int W>
+template <int W, int NB>
 __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
@@ -319,7 +380,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
         bool cand = false;
         if (!((skip >> lane) & 1u)) {
-            vis = load_lw<W>(P.V + (size_t)u * W);
+            vis = LS<W, NB>::load(P.V, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
@@ -340,15 +401,15 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             bool done = false;
             for (; p + 2 <= e && !done; p += 2) {
                 const uint32_t v0 = __ldg(g.ri + p), v1 = __ldg(g.ri + p + 1);
-                const LaneWord<W> f0 = load_lw<W>(Fc + (size_t)v0 * W);
-                const LaneWord<W> f1 = load_lw<W>(Fc + (size_t)v1 * W);
+                const LaneWord<W> f0 = LS<W, NB>::load(Fc, v0);
+                const LaneWord<W> f1 = LS<W, NB>::load(Fc, v1);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f0.w[i] | f1.w[i];
                 done = covers<W>(acc_w, need);
                 scanned += 2;
             }
             if (!done && p < e) {
-                const LaneWord<W> f = load_lw<W>(Fc + (size_t)__ldg(g.ri + p) * W);
+                const LaneWord<W> f = LS<W, NB>::load(Fc, __ldg(g.ri + p));
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -362,7 +423,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
 #pragma unroll
             for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i], j);
             uint32_t sc = 0;
-            const LaneWord<W> aj = warp_pull_range<W>(P, Fc, __shfl_sync(kFull, b, j),
+            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, __shfl_sync(kFull, b, j),
                                                       __shfl_sync(kFull, e, j), nj, sc);
             if ((int)lane == j) {
                 acc_w = aj;
@@ -378,7 +439,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 found |= res.w[i] != 0;
             }
             if (found) {
-                store_lw<W>(Fn + (size_t)u * W, res);
+                LS<W, NB>::store(Fn, u, res);
                 bool fresh = true;
 #pragma unroll
                 for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
@@ -401,7 +462,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     for (uint32_t t = tasks.c * tchunk; t < min(g.nheavy, (tasks.c + 1) * tchunk); ++t) {
         const uint2 task = __ldg(g.heavy + t);
         const uint32_t u = task.x;
-        const LaneWord<W> vis = load_lw<W>(P.V + (size_t)u * W);
+        const LaneWord<W> vis = LS<W, NB>::load(P.V, u);
         LaneWord<W> need;
         bool cand = false;
 #pragma unroll
@@ -413,17 +474,16 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         if (cand) {
             const uint32_t e = min(task.y + kHeavyChunk, __ldg(g.cp + u + 1));
             uint32_t sc = 0;
-            const LaneWord<W> aj = warp_pull_range<W>(P, Fc, task.y, e, need, sc);
+            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, task.y, e, need, sc);
             if (lane == 0) {
                 acc.scanned += sc;
                 acc.candidates += task.y == __ldg(g.cp + u);
                 bool any = false;
-                unsigned long long* fn = Fn + (size_t)u * W;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
                     const unsigned long long r = aj.w[i] & need.w[i];
                     if (r) {
-                        atomicOr(fn + i, r);
+                        LS<W, NB>::atomic_or(Fn, u, i, r);
                         any = true;
                     }
                 }
@@ -450,7 +510,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
 }
 
 // ---- finalize: V |= F', lane counts, next-hop items, clear old frontier -------
-template <int W>
+template <int W, int NB>
 __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR,
                                unsigned long long* Fn, bool mark_visited, bool touched_set, bool want_items,
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
@@ -476,9 +536,8 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
         bool expand = false;
         if (valid) {
             u = Rn[idx];
-            x = load_lw<W>(Fn + (size_t)u * W);
-            unsigned long long* vp = P.V + (size_t)u * W;
-            LaneWord<W> v = load_lw<W>(vp);
+            x = LS<W, NB>::load(Fn, u);
+            LaneWord<W> v = LS<W, NB>::load(P.V, u);
             uint32_t pc = 0;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
@@ -486,7 +545,7 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
                 act.w[i] |= x.w[i];
                 pc += __popcll(x.w[i]);
             }
-            store_lw<W>(vp, v);
+            LS<W, NB>::store(P.V, u, v);
             // push levels set a touched bit per discovery; pull levels only for
             // heavy vertices (discovered vertices in pull_skip are heavy: a
             // zero-in-degree vertex is never discovered)
@@ -505,13 +564,17 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             for (int i = 0; i < W; ++i) {
                 if (__ballot_sync(kFull, x.w[i] != 0) == 0) continue;
                 const uint32_t lo = (uint32_t)x.w[i], hi = (uint32_t)(x.w[i] >> 32);
+                constexpr int kLo = NB < 32 ? NB : 32;  // narrow words: only their own bits
 #pragma unroll
-                for (int bb = 0; bb < 32; ++bb) {
+                for (int bb = 0; bb < kLo; ++bb) {
                     const uint32_t c0 = __popc(__ballot_sync(kFull, (lo >> bb) & 1u));
-                    const uint32_t c1 = __popc(__ballot_sync(kFull, (hi >> bb) & 1u));
-                    if ((uint32_t)bb == lane) {
-                        cnt_lo[i] += c0;
-                        cnt_hi[i] += c1;
+                    if ((uint32_t)bb == lane) cnt_lo[i] += c0;
+                }
+                if constexpr (NB == 64) {
+#pragma unroll
+                    for (int bb = 0; bb < 32; ++bb) {
+                        const uint32_t c1 = __popc(__ballot_sync(kFull, (hi >> bb) & 1u));
+                        if ((uint32_t)bb == lane) cnt_hi[i] += c1;
                     }
                 }
             }
@@ -537,27 +600,27 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
 #pragma unroll
         for (int i = 0; i < W; ++i) {
             if (cnt_lo[i]) atomicAdd(&s_cnt[i * 64 + lane], (unsigned long long)cnt_lo[i]);
-            if (cnt_hi[i]) atomicAdd(&s_cnt[i * 64 + 32 + lane], (unsigned long long)cnt_hi[i]);
+            if (NB == 64 && cnt_hi[i]) atomicAdd(&s_cnt[i * 64 + 32 + lane], (unsigned long long)cnt_hi[i]);
         }
     }
 }
 
-template <int W>
+template <int W, int NB>
 __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F, uint32_t gtid,
                            uint32_t nthreads) {
     LaneWord<W> z;
 #pragma unroll
     for (int i = 0; i < W; ++i) z.w[i] = 0;
-    for (uint32_t i = gtid; i < n; i += nthreads) store_lw<W>(F + (size_t)R[i] * W, z);
+    for (uint32_t i = gtid; i < n; i += nthreads) LS<W, NB>::store(F, R[i], z);
 }
 
-template <int W>
+template <int W, int NB>
 __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     grid_barrier_init(P.bar);
     // qctl[parity] fields in this engine:
     //   nitems = |R| (discovery list tail), nfound = push items built for the
     //   frontier, edges = sum of outdeg over R, pad = push-equivalent edges.
-    constexpr uint32_t LB = 64 * W;
+    constexpr uint32_t LB = LS<W, NB>::kLanes;
     __shared__ uint32_t s_stage[kWarps][kStageCap];
     __shared__ unsigned long long s_cnt[LB];
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
@@ -592,7 +655,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (gtid < lanes) {
                 s = dev_id(g, P.seeds[bt * LB + gtid]);
                 const unsigned long long bit = 1ULL << (gtid & 63);
-                atomicOr(P.F0 + (size_t)s * W + (gtid >> 6), bit);
+                LS<W, NB>::atomic_or(P.F0, s, gtid >> 6, bit);
                 const uint32_t tb = 1u << (s & 31);
                 first = !(atomicOr(P.touched + (s >> 5), tb) & tb);
                 if (first) count_discovered(g, s, true, acc);
@@ -610,7 +673,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         bool pull = P.force_dir == 2;
         if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
         __syncthreads();
-        finalize_phase<W>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull, P.items0, &P.qctl[0].nfound, false,
+        finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull, P.items0, &P.qctl[0].nfound, false,
                           s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
         acc.pairs = 0;  // the seeds themselves are never counted
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
@@ -640,9 +703,9 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 LaneWord<W> act;
 #pragma unroll
                 for (int i = 0; i < W; ++i) act.w[i] = ld_volatile(P.active + cur * W + i);
-                pull_phase<W>(P, Fc, Fn, act, Rn, qn, acc, st, warp_gid, nwarps);
+                pull_phase<W, NB>(P, Fc, Fn, act, Rn, qn, acc, st, warp_gid, nwarps);
             } else {
-                push_phase<W>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
+                push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps);
             }
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
@@ -668,10 +731,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
-            finalize_phase<W>(P, Rn, nR, Fn, true, !was_pull, !last && !pull, items_of(P, nxt),
+            finalize_phase<W, NB>(P, Rn, nR, Fn, true, !was_pull, !last && !pull, items_of(P, nxt),
                               &qn->nfound, count_lanes, s_cnt, P.active + nxt * W, clog_used,
                               acc, st, warp_gid, nwarps);
-            clear_list<W>(Rc, nR_prev, Fc, gtid, nthreads);
+            clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
             __syncthreads();
             if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
@@ -697,10 +760,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
         if (clog_used <= P.clog_cap) {
-            clear_list<W>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
-            clear_list<W>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
+            clear_list<W, NB>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
+            clear_list<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
         } else {
-            for (size_t i = gtid; i < (size_t)g.n * W; i += nthreads) {
+            for (size_t i = gtid; i < LS<W, NB>::words64(g.n); i += nthreads) {
                 P.V[i] = 0;
                 P.F0[i] = 0;
                 P.F1[i] = 0;
@@ -710,7 +773,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     }
 }
 
-template <int W>
+template <int W, int NB>
 cudaError_t launch_w(Launch& L) {
     static int blocks_per_sm = 0, num_sms = 0;
     cudaError_t e;
@@ -718,7 +781,7 @@ cudaError_t launch_w(Launch& L) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W>, kBlock,
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W, NB>, kBlock,
                                                                 0)))
             return e;
         if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -764,7 +827,7 @@ cudaError_t launch_w(Launch& L) {
     L.block = kBlock;
     void* args[] = {&P};
     L.launches = 1;
-    return launch_persistent((const void*)ms_kernel<W>, L.grid, kBlock, args, L.stream);
+    return launch_persistent((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream);
 }
 
 }  // namespace
@@ -808,11 +871,13 @@ cudaError_t launch_lanes(Launch& L) {
     int W = L.lanes_words;
     cudaError_t e = ensure_lanes_ws(L.g, L.ws, W);
     if (e) return e;
+    if (L.lane_bits == 16) return launch_w<1, 16>(L);
+    if (L.lane_bits == 8) return launch_w<1, 8>(L);
     switch (W) {
-        case 1: return launch_w<1>(L);
-        case 2: return launch_w<2>(L);
-        case 4: return launch_w<4>(L);
-        case 8: return launch_w<8>(L);
+        case 1: return launch_w<1, 64>(L);
+        case 2: return launch_w<2, 64>(L);
+        case 4: return launch_w<4, 64>(L);
+        case 8: return launch_w<8, 64>(L);
         default: return cudaErrorInvalidValue;
     }
 }
