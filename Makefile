@@ -29,10 +29,11 @@ $(DROPIN): $(CSRC)/dropin/matgraph_b200.cpp include/matgraph_b200/khop.hpp inclu
 
 # the drop-in's C++ tests (linked with the C oracle as the checker)
 cpptest: $(CPPTEST)
-$(CPPTEST): tests/cpp/test_dropin.cpp tests/cpp/mini_test.hpp include/matgraph_b200/khop.hpp $(DROPIN) oracle/khop_oracle.c
+$(CPPTEST): tests/cpp/test_dropin.cpp tests/cpp/mini_test.hpp include/matgraph_b200/khop.hpp $(DROPIN) oracle/khop_oracle.c oracle/dropin_bfs.cpp
 	@mkdir -p build
 	gcc -std=c11 -O2 -fPIC -c -o build/khop_oracle.o oracle/khop_oracle.c
-	g++ $(CXXFLAGS_DROPIN) -Itests/cpp -o $@ tests/cpp/test_dropin.cpp build/khop_oracle.o \
+	g++ $(CXXFLAGS_DROPIN) -c -o build/dropin_bfs.o oracle/dropin_bfs.cpp
+	g++ $(CXXFLAGS_DROPIN) -Itests/cpp -o $@ tests/cpp/test_dropin.cpp build/khop_oracle.o build/dropin_bfs.o \
 	    -L$(PKG)/lib -lmatgraph_b200 -lmgk -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 

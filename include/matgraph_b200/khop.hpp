@@ -7,11 +7,15 @@
 //   proj/core/include/matgraph/bench.hpp:16-156   (RMAT, build_bench_graph, pick_seeds,
 //                                                  summarize, run_khop_benchmark, CSV)
 //   proj/core/include/matgraph/error.hpp:10-66    (Error, ContractError, HarnessError)
-// recompiles against this header unchanged. The traversal runs on a B200
+// compiles against this header with the same signatures (mangled names
+// included) for every symbol it declares. The traversal runs on a B200
 // through the C ABI of include/mgk.h; the relation matrix is uploaded once per
 // (relation, flush state) and cached like the reference caches its transpose
-// (graph.cpp:90-102). Not on the path (and not provided): labels, property
-// maps, the Cypher executor, the server, snapshots, mxm.
+// (graph.cpp:90-102). Labels and properties are accepted and stored (the
+// k-hop path never reads them). Not provided: the Cypher frontend / planner /
+// executor, the server, snapshots. BfsOracle (bench.hpp:73-91) is declared
+// here but defined only by the test infrastructure (oracle/dropin_bfs.cpp),
+// which the drop-in's test binaries link; the product library has no oracle.
 #pragma once
 
 #include <cstdint>
@@ -24,6 +28,8 @@
 #include <stdexcept>
 #include <string>
 #include <string_view>
+#include <tuple>
+#include <variant>
 #include <vector>
 
 struct mgk_graph;
@@ -125,6 +131,36 @@ std::uint64_t nvals(const BitVector& v);
 SparseMatrix mxm(const SparseMatrix& a, const SparseMatrix& b,
                  const Semiring& semiring = Semiring::bool_or_and(), const SparseMatrix* mask = nullptr);
 
+// ---- property values (value.hpp:10-46) ---------------------------------------------
+/// Int / float / bool / string; `Value("x")` is a string (no decay to bool).
+class Value {
+public:
+    enum class Type { Int, Float, Bool, String };
+    Value() : v_(std::int64_t{0}) {}
+    Value(std::int64_t i) : v_(i) {}
+    Value(int i) : v_(std::int64_t{i}) {}
+    Value(double d) : v_(d) {}
+    Value(bool b) : v_(b) {}
+    Value(std::string s) : v_(std::move(s)) {}
+    Value(std::string_view s) : v_(std::string(s)) {}
+    Value(const char* s) : v_(std::string(s)) {}
+    Type type() const noexcept { return static_cast<Type>(v_.index()); }
+    bool is_int() const noexcept { return type() == Type::Int; }
+    bool is_float() const noexcept { return type() == Type::Float; }
+    bool is_bool() const noexcept { return type() == Type::Bool; }
+    bool is_string() const noexcept { return type() == Type::String; }
+    bool is_numeric() const noexcept { return is_int() || is_float(); }
+    std::int64_t as_int() const { return std::get<std::int64_t>(v_); }
+    double as_float() const { return std::get<double>(v_); }
+    bool as_bool() const { return std::get<bool>(v_); }
+    const std::string& as_string() const { return std::get<std::string>(v_); }
+    friend bool operator==(const Value&, const Value&) = default;
+
+private:
+    std::variant<std::int64_t, double, bool, std::string> v_;
+};
+using PropertyMap = std::map<std::string, Value>;
+
 // ---- graph store (graph.hpp:20-124), load API + matrix access ---------------------
 struct RelationRef {
     std::optional<std::string> name;  // nullopt = ANY
@@ -158,17 +194,25 @@ public:
     PropertyGraph(const PropertyGraph&) = delete;
     PropertyGraph& operator=(const PropertyGraph&) = delete;
 
-    /// Allocates the next node id (labels / properties are not stored: the
-    /// k-hop path never reads them).
-    std::uint64_t create_node(const std::vector<std::string>& labels = {});
-    /// Records a directed typed edge (graph.cpp:54-82 contract and messages).
-    void create_edge(std::uint64_t src, const std::string& relation, std::uint64_t dst);
+    /// Allocates the next node id (graph.cpp:31-52: labels must be identifiers).
+    std::uint64_t create_node(const std::vector<std::string>& labels, PropertyMap props = {});
+    /// Records a directed typed edge (graph.cpp:54-82 contract and messages);
+    /// re-creating an edge overwrites its properties.
+    void create_edge(std::uint64_t src, const std::string& relation, std::uint64_t dst,
+                     PropertyMap props = {});
+    const PropertyMap& node_props(std::uint64_t id) const;
+    const PropertyMap* edge_props(std::uint64_t src, std::string_view relation, std::uint64_t dst) const;
+    /// Sorted labels of one node.
+    std::vector<std::string> node_labels(std::uint64_t id) const;
 
     std::uint64_t node_count() const noexcept { return node_count_; }
     std::uint64_t capacity() const noexcept { return capacity_; }
 
     /// Flushes pending edges; unknown names yield the empty matrix (graph.cpp:84-88).
     const SparseMatrix& relation_matrix(const RelationRef& rel = RelationRef::any()) const;
+    /// Transposed adjacency (graph.cpp:90-102): computed lazily on the host,
+    /// mutex-guarded, cached until the next write.
+    const SparseMatrix& transposed_matrix(const RelationRef& rel = RelationRef::any()) const;
     /// The matrix on `device` (uploaded on first use, cached until the next
     /// flush that changes it; mutex-guarded like transposed_matrix).
     const DeviceMatrix& device_matrix(const RelationRef& rel = RelationRef::any(),
@@ -183,6 +227,7 @@ private:
         SparseMatrix matrix;
         std::vector<std::pair<std::uint64_t, std::uint64_t>> pending;
         std::map<int, std::shared_ptr<DeviceMatrix>> device;
+        std::optional<SparseMatrix> transposed;
     };
     void grow_to(std::uint64_t needed);
     const Slot* find_slot(const RelationRef& rel) const;
@@ -194,6 +239,9 @@ private:
     mutable Slot any_;
     mutable Slot empty_;
     mutable std::unique_ptr<std::mutex> device_mutex_;
+    std::map<std::string, std::vector<std::uint64_t>, std::less<>> labels_;
+    std::vector<PropertyMap> node_props_;
+    std::map<std::tuple<std::uint64_t, std::string, std::uint64_t>, PropertyMap> edge_props_;
 };
 
 // ---- the k-hop kernel (execute.hpp:52-68) ------------------------------------------
@@ -247,9 +295,31 @@ using EdgeList = std::vector<EdgeTuple>;
 inline constexpr std::string_view kBenchRelation = "EDGE";
 
 EdgeList rmat_generate(const RmatParams& params);
+/// bench.cpp:139-173: `src<TAB>dst` lines, HarnessError with the line number.
+EdgeList load_edge_list(const std::filesystem::path& path);
+/// max endpoint + 1, 0 for an empty list (bench.cpp:175-183).
+std::uint64_t edge_list_node_count(const EdgeList& edges);
 PropertyGraph build_bench_graph(const EdgeList& edges, std::uint64_t node_count);
 std::vector<std::uint64_t> pick_seeds(const PropertyGraph& graph, std::size_t n,
                                       std::uint64_t rng_seed);
+
+/// Queue-based BFS oracle over a raw edge list (bench.hpp:73-91). DECLARED
+/// ONLY: the definition is test infrastructure (oracle/dropin_bfs.cpp over the
+/// C oracle), linked into test binaries, never into libmatgraph_b200.so.
+class BfsOracle {
+public:
+    BfsOracle(const EdgeList& edges, std::uint64_t node_count);
+    ~BfsOracle();
+    BfsOracle(BfsOracle&&) noexcept;
+    BfsOracle& operator=(BfsOracle&&) noexcept;
+    std::uint64_t count(std::uint64_t seed, std::uint32_t k, TraverseMode mode) const;
+    std::uint64_t node_count() const noexcept { return node_count_; }
+
+private:
+    void* impl_ = nullptr;
+    std::uint64_t node_count_ = 0;
+};
+std::uint64_t bfs_oracle(const PropertyGraph& graph, std::uint64_t seed, std::uint32_t k, TraverseMode mode);
 
 struct SeedRun {
     std::uint64_t seed = 0;
@@ -276,11 +346,11 @@ struct BenchSchedule {
     std::uint64_t rng_seed = 1;
     void validate() const;
 };
-/// bench.cpp:311-343: sequential per-query timing like the reference
-/// (batched = true issues one device call per section instead and spreads its
-/// wall time over the section's seeds).
-KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule,
-                              bool batched = false);
+/// bench.cpp:311-343: sequential per-query timing like the reference.
+KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule);
+/// Additive overload: batched = true issues one device call per section and
+/// spreads its wall time over the section's seeds.
+KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule, bool batched);
 std::string report_csv_string(const KHopReport& report);
 void report_csv(const KHopReport& report, const std::filesystem::path& path);
 

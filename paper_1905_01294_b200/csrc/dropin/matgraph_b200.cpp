@@ -204,6 +204,7 @@ void PropertyGraph::grow_to(std::uint64_t needed) {  // graph.cpp:236-248 (capac
         std::vector<std::uint64_t> ci(s.matrix.col_idx().begin(), s.matrix.col_idx().end());
         s.matrix = SparseMatrix::from_parts(cap, cap, std::move(rp), std::move(ci));
         s.device.clear();
+        s.transposed.reset();
     };
     for (auto& [name, slot] : relations_) {
         (void)name;
@@ -215,25 +216,60 @@ void PropertyGraph::grow_to(std::uint64_t needed) {  // graph.cpp:236-248 (capac
     capacity_ = cap;
 }
 
-std::uint64_t PropertyGraph::create_node(const std::vector<std::string>& labels) {
-    for (const auto& label : labels)
+std::uint64_t PropertyGraph::create_node(const std::vector<std::string>& labels, PropertyMap props) {
+    for (const auto& label : labels)  // graph.cpp:31-52
         if (!is_identifier(label))
             throw ContractError(fmt("label '%s' is not a valid identifier", label.c_str()));
+    for (const auto& kv : props)
+        if (!is_identifier(kv.first))
+            throw ContractError(fmt("property key '%s' is not a valid identifier", kv.first.c_str()));
     grow_to(node_count_ + 1);
-    return node_count_++;
+    const std::uint64_t id = node_count_++;
+    for (const auto& label : labels) {
+        auto& members = labels_[label];
+        if (members.empty() || members.back() != id) members.push_back(id);  // ids ascend
+    }
+    node_props_.push_back(std::move(props));
+    return id;
 }
 
-void PropertyGraph::create_edge(std::uint64_t src, const std::string& relation, std::uint64_t dst) {
+void PropertyGraph::create_edge(std::uint64_t src, const std::string& relation, std::uint64_t dst,
+                                PropertyMap props) {
     if (src >= node_count_ || dst >= node_count_)  // graph.cpp:56-60
         throw ContractError(fmt("unknown node id %llu in edge (%llu)-[:%s]->(%llu)",
                                 (unsigned long long)(src >= node_count_ ? src : dst),
                                 (unsigned long long)src, relation.c_str(), (unsigned long long)dst));
     if (!is_identifier(relation))
         throw ContractError(fmt("relation type '%s' is not a valid identifier", relation.c_str()));
+    for (const auto& kv : props)
+        if (!is_identifier(kv.first))
+            throw ContractError(fmt("property key '%s' is not a valid identifier", kv.first.c_str()));
     auto [it, inserted] = relations_.try_emplace(relation);
     if (inserted) it->second.matrix = SparseMatrix(capacity_, capacity_);
     it->second.pending.emplace_back(src, dst);
     any_.pending.emplace_back(src, dst);
+    auto key = std::make_tuple(src, relation, dst);
+    if (props.empty())
+        edge_props_.erase(key);  // re-creating an edge overwrites its properties
+    else
+        edge_props_[key] = std::move(props);
+}
+
+const PropertyMap& PropertyGraph::node_props(std::uint64_t id) const {
+    if (id >= node_count_) throw ContractError(fmt("unknown node id %llu", (unsigned long long)id));
+    return node_props_[id];
+}
+
+const PropertyMap* PropertyGraph::edge_props(std::uint64_t src, std::string_view relation, std::uint64_t dst) const {
+    auto it = edge_props_.find(std::make_tuple(src, std::string(relation), dst));
+    return it == edge_props_.end() ? nullptr : &it->second;
+}
+
+std::vector<std::string> PropertyGraph::node_labels(std::uint64_t id) const {
+    std::vector<std::string> out;
+    for (const auto& [label, members] : labels_)  // map order: sorted by name
+        if (std::binary_search(members.begin(), members.end(), id)) out.push_back(label);
+    return out;
 }
 
 void PropertyGraph::flush_slot(Slot& slot, std::uint64_t dim) {  // graph.cpp:182-215
@@ -253,7 +289,8 @@ void PropertyGraph::flush_slot(Slot& slot, std::uint64_t dim) {  // graph.cpp:18
     pending.clear();
     pending.shrink_to_fit();
     slot.matrix = SparseMatrix::from_parts(dim, dim, std::move(row_ptr), std::move(col_idx));
-    slot.device.clear();  // like slot.transposed.reset()
+    slot.device.clear();
+    slot.transposed.reset();
 }
 
 void PropertyGraph::flush() const {
@@ -274,6 +311,24 @@ const SparseMatrix& PropertyGraph::relation_matrix(const RelationRef& rel) const
     flush();
     const Slot* slot = find_slot(rel);
     return slot ? slot->matrix : empty_.matrix;
+}
+
+const SparseMatrix& PropertyGraph::transposed_matrix(const RelationRef& rel) const {
+    flush();  // graph.cpp:90-102: lazily, under a mutex, cached until the next write
+    const Slot* found = find_slot(rel);
+    Slot& slot = const_cast<Slot&>(found ? *found : empty_);
+    std::lock_guard lock(*device_mutex_);
+    if (!slot.transposed) {
+        const SparseMatrix& m = slot.matrix;  // counting sort by column (sparse.cpp:379-403)
+        std::vector<std::uint64_t> rp(m.ncols() + 1, 0), ci(m.nvals());
+        for (std::uint64_t c : m.col_idx()) rp[c + 1]++;
+        for (std::uint64_t c = 0; c < m.ncols(); ++c) rp[c + 1] += rp[c];
+        std::vector<std::uint64_t> pos(rp.begin(), rp.end() - 1);
+        for (std::uint64_t r = 0; r < m.nrows(); ++r)
+            for (std::uint64_t c : m.row(r)) ci[pos[c]++] = r;  // rows visited ascending
+        slot.transposed = SparseMatrix::from_parts(m.ncols(), m.nrows(), std::move(rp), std::move(ci));
+    }
+    return *slot.transposed;
 }
 
 const DeviceMatrix& PropertyGraph::device_matrix(const RelationRef& rel, int device) const {
@@ -409,9 +464,46 @@ EdgeList rmat_generate(const RmatParams& params) {  // bench.cpp:107-137 (same s
     return edges;
 }
 
+EdgeList load_edge_list(const std::filesystem::path& path) {  // bench.cpp:139-173
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw HarnessError("cannot open edge list '" + path.string() + "'");
+    constexpr std::uint32_t kIdCap = 1u << 24;
+    EdgeList edges;
+    std::string line;
+    std::size_t line_no = 0;
+    while (std::getline(in, line)) {
+        ++line_no;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        if (line.empty()) continue;
+        const std::size_t tab = line.find('\t');
+        if (tab == std::string::npos) throw HarnessError(fmt("edge list line %zu: expected 'src<TAB>dst'", line_no));
+        std::uint32_t ids[2] = {0, 0};
+        const char* bounds[3] = {line.data(), line.data() + tab + 1, line.data() + line.size()};
+        for (int i = 0; i < 2; ++i) {
+            const char* first = bounds[i];
+            const char* last = i == 0 ? line.data() + tab : bounds[2];
+            const auto [end, ec] = std::from_chars(first, last, ids[i]);
+            if (ec != std::errc{} || end != last)
+                throw HarnessError(fmt("edge list line %zu: malformed node id", line_no));
+            if (ids[i] >= kIdCap)
+                throw HarnessError(fmt("edge list line %zu: node id %u is at or above 2^24", line_no, ids[i]));
+        }
+        edges.push_back({ids[0], ids[1]});
+    }
+    if (in.bad()) throw HarnessError("I/O error reading '" + path.string() + "'");
+    return edges;
+}
+
+std::uint64_t edge_list_node_count(const EdgeList& edges) {  // bench.cpp:175-183
+    std::uint64_t max_id = 0;
+    for (const auto& e : edges) max_id = std::max<std::uint64_t>(max_id, std::max(e.src, e.dst));
+    return edges.empty() ? 0 : max_id + 1;
+}
+
 PropertyGraph build_bench_graph(const EdgeList& edges, std::uint64_t node_count) {  // bench.cpp:185-198
     PropertyGraph graph(std::max<std::uint64_t>(node_count, 1));
-    for (std::uint64_t id = 0; id < node_count; ++id) graph.create_node();
+    for (std::uint64_t id = 0; id < node_count; ++id)
+        graph.create_node({}, {{"id", Value(static_cast<std::int64_t>(id))}});
     const std::string relation(kBenchRelation);
     for (const auto& e : edges) {
         if (e.src >= node_count || e.dst >= node_count)
@@ -471,6 +563,10 @@ void BenchSchedule::validate() const {  // bench.cpp:297-309
         if (k < 1 || k > kMaxHops) throw ContractError(fmt("hop count %u outside [1, %u]", k, kMaxHops));
     for (std::size_t i = 0; i < seeds_per_k.size(); ++i)
         if (seeds_per_k[i] == 0) throw ContractError(fmt("seed count for k=%u must be at least 1", ks[i]));
+}
+
+KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule) {
+    return run_khop_benchmark(graph, schedule, false);
 }
 
 KHopReport run_khop_benchmark(const PropertyGraph& graph, const BenchSchedule& schedule, bool batched) {

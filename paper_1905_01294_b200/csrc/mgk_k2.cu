@@ -783,7 +783,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 // Per-device launch facts, looked up once (the host work between a caller's
 // events and the launch is part of the measured call)
 struct K2Device {
-    int optin = 0, nsm = 0;
+    int optin = 0, nsm = 0;  // optin: dynamic shared memory bytes one CTA may use
     size_t occ_smem[8] = {};  // occupancy cache: dynamic smem -> CTAs per SM
     int occ[8] = {};
     int nocc = 0;
@@ -805,6 +805,10 @@ K2Device& k2_device() {
     if (!ready[dev]) {
         cudaDeviceGetAttribute(&devs[dev].optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
         cudaDeviceGetAttribute(&devs[dev].nsm, cudaDevAttrMultiProcessorCount, dev);
+        // the opt-in limit covers static + dynamic shared memory: the dynamic
+        // part may use what the kernel's static arrays leave
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, k2_kernel) == cudaSuccess) devs[dev].optin -= (int)fa.sharedSizeBytes;
         if (cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, devs[dev].optin) !=
             cudaSuccess) {
             (void)cudaGetLastError();

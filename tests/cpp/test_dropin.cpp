@@ -371,3 +371,87 @@ GPU_TEST_CASE("mxm agrees with the C oracle across semirings") {
 }
 
 int main(int argc, char** argv) { return mini::run(argc, argv); }
+
+// ---- the rest of the reference's graph-load / harness signatures ------------------------
+TEST_CASE("create_node / create_edge accept labels and PropertyMap (graph.cpp:31-82)") {
+    PropertyGraph g;
+    for (std::int64_t i = 0; i < 4; ++i) g.create_node({}, {{"id", Value(i)}});
+    const std::uint64_t tagged = g.create_node({"Person", "Admin"}, {{"name", Value("ann")}, {"age", Value(41)}});
+    CHECK(tagged == 4);
+    CHECK(g.node_props(2).at("id") == Value(std::int64_t{2}));
+    CHECK(g.node_props(4).at("name").as_string() == "ann");
+    CHECK((g.node_labels(4) == std::vector<std::string>{"Admin", "Person"}));
+    g.create_edge(0, "R", 1, {{"w", Value(1.5)}});
+    CHECK(g.edge_props(0, "R", 1) && g.edge_props(0, "R", 1)->at("w").as_float() == 1.5);
+    g.create_edge(0, "R", 1);  // re-created without properties: the stored map is dropped
+    CHECK(g.edge_props(0, "R", 1) == nullptr);
+    CHECK_THROWS_WITH_AS(g.create_node({}, {{"bad key", Value(1)}}), "property key 'bad key' is not a valid identifier",
+                         ContractError);
+    CHECK_THROWS_WITH_AS(g.create_edge(0, "R", 1, {{"9x", Value(1)}}), "property key '9x' is not a valid identifier",
+                         ContractError);
+    CHECK(g.relation_matrix("R").nvals() == 1);
+}
+
+TEST_CASE("transposed_matrix is the CSR of A^T, cached until the next write (graph.cpp:90-102)") {
+    PropertyGraph g = path4();
+    g.create_edge(3, "R", 0);
+    const SparseMatrix& t = g.transposed_matrix("R");
+    CHECK(t.nrows() == g.relation_matrix("R").ncols());
+    for (std::uint64_t r = 0; r < 4; ++r)
+        for (std::uint64_t c = 0; c < 4; ++c) CHECK(t.contains(c, r) == g.relation_matrix("R").contains(r, c));
+    CHECK(&g.transposed_matrix("R") == &t);  // cached
+    g.create_edge(1, "R", 3);
+    CHECK(g.transposed_matrix("R").contains(3, 1));  // invalidated by the write
+    CHECK(g.transposed_matrix("NONE").nvals() == 0);
+}
+
+TEST_CASE("load_edge_list / edge_list_node_count (bench.cpp:139-183)") {
+    const auto dir = std::filesystem::temp_directory_path();
+    auto write = [&](const char* name, const std::string& text) {
+        const auto p = dir / name;
+        std::ofstream(p, std::ios::binary) << text;
+        return p;
+    };
+    const auto ok = write("mgk_el_ok.tsv", "0\t1\r\n\n5\t2\n");
+    const EdgeList e = load_edge_list(ok);
+    CHECK((e == EdgeList{{0, 1}, {5, 2}}));
+    CHECK(edge_list_node_count(e) == 6);
+    CHECK(edge_list_node_count({}) == 0);
+    CHECK_THROWS_WITH_AS(load_edge_list(write("mgk_el_a.tsv", "0\t1\n0 1\n")),
+                         "edge list line 2: expected 'src<TAB>dst'", HarnessError);
+    CHECK_THROWS_WITH_AS(load_edge_list(write("mgk_el_b.tsv", "0\tx\n")), "edge list line 1: malformed node id",
+                         HarnessError);
+    CHECK_THROWS_WITH_AS(load_edge_list(write("mgk_el_c.tsv", "16777216\t1\n")),
+                         "edge list line 1: node id 16777216 is at or above 2^24", HarnessError);
+    CHECK_THROWS_AS(load_edge_list(dir / "mgk_el_missing.tsv"), HarnessError);
+}
+
+TEST_CASE("BfsOracle (test infrastructure) keeps the reference's contract") {
+    const EdgeList e{{0, 1}, {1, 2}, {2, 0}};
+    BfsOracle o(e, 3);
+    CHECK(o.node_count() == 3);
+    CHECK(o.count(0, 1, TraverseMode::Exact) == 1);
+    CHECK(o.count(0, 3, TraverseMode::Cumulative) == 2);
+    CHECK_THROWS_WITH_AS(o.count(3, 1, TraverseMode::Exact), "oracle seed 3 is out of range", ContractError);
+    CHECK_THROWS_WITH_AS(o.count(0, 33, TraverseMode::Exact), "oracle hop count 33 outside [1, 32]", ContractError);
+    CHECK_THROWS_WITH_AS(BfsOracle(EdgeList{{0, 5}}, 3), "edge (0, 5) outside the 3-node range", ContractError);
+}
+
+GPU_TEST_CASE("run_khop_benchmark(graph, schedule): the reference's two-argument signature, checked by BfsOracle") {
+    RmatParams p;
+    p.scale = 9;
+    p.rng_seed = 4;
+    const EdgeList edges = rmat_generate(p);
+    PropertyGraph g = build_bench_graph(edges, p.node_count());
+    CHECK(g.node_props(7).at("id") == Value(std::int64_t{7}));  // bench.cpp:187-188
+    BfsOracle oracle(edges, p.node_count());
+    BenchSchedule s;
+    s.ks = {1, 2, 3, 6};
+    s.seeds_per_k = {20, 20, 5, 5};
+    const KHopReport r = run_khop_benchmark(g, s);
+    CHECK(r.sections.size() == 4);
+    for (const auto& sec : r.sections)
+        for (const auto& run : sec.runs) CHECK(run.count == oracle.count(run.seed, sec.k, TraverseMode::Exact));
+    CHECK(bfs_oracle(g, r.sections[0].runs[0].seed, 2, TraverseMode::Cumulative) ==
+          oracle.count(r.sections[0].runs[0].seed, 2, TraverseMode::Cumulative));
+}
