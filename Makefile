@@ -57,3 +57,59 @@ ref:
 
 clean:
 	rm -rf $(BUILD) $(LIB)
+
+# ---- the reference's OWN test files, unmodified, with the k-hop path on the GPU ----------
+# (needs /root/reference at build time; outputs in oracle/_ref/wrap travel to the box)
+#   ref_tests_gpu   proj/tests/test_execute.cpp + test_bench.cpp (doctest-compatible shim)
+#   acceptance_gpu  proj/tests/acceptance/acceptance_main.cpp (c1 = 8,000 k-hop counts)
+#   varlen_gpu      Cypher [*min..max] walks, both directions (tests/ref_wrap/varlen_main.cpp)
+# k_hop_count / k_hop_frontier are replaced at link time (ld --wrap, no source change);
+# Executor::apply(VarLenTraverseOp) gets the one-line binding of INTEGRATION.md §B, applied
+# by sed to a build-time copy of execute.cpp. Everything else is the reference's code.
+REFPROJ  ?= /root/reference/proj
+RW       := oracle/_ref/wrap
+FMT_DIR  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/flashinfer/data/spdlog/include/spdlog/fmt/bundled
+RW_CXX   := -std=c++20 -O2 -DNDEBUG -DFMT_HEADER_ONLY -DMATGRAPH_INTERNAL_CHECKS=0 -fPIC -w \
+            -I$(REFPROJ)/core/include -I$(REFPROJ)/tests -I$(RW)/include -Itests/ref_wrap -Itests/ref_wrap/doctest -Iinclude
+RW_CORE  := $(filter-out execute,$(basename $(notdir $(wildcard $(REFPROJ)/core/src/*.cpp))))
+RW_OBJS  := $(addprefix $(RW)/core/,$(addsuffix .o,$(RW_CORE))) $(RW)/core/execute_mgk.o $(RW)/mgk_bind.o
+RW_WRAP  := -Wl,--wrap=_ZN8matgraph11k_hop_countERKNS_13PropertyGraphERKNS_9KHopQueryE \
+            -Wl,--wrap=_ZN8matgraph14k_hop_frontierERKNS_13PropertyGraphERKNS_9KHopQueryE
+RW_LIBS  := -L$(PKG)/lib -lmgk -Wl,-rpath,'$$ORIGIN/../../../$(PKG)/lib' -lpthread
+
+.PHONY: refwrap
+refwrap: $(RW)/ref_tests_gpu $(RW)/acceptance_gpu $(RW)/varlen_gpu
+
+$(RW)/include/fmt:
+	mkdir -p $(RW)/include
+	ln -sfn $(FMT_DIR) $(RW)/include/fmt
+
+$(RW)/core/%.o: $(REFPROJ)/core/src/%.cpp | $(RW)/include/fmt
+	@mkdir -p $(RW)/core
+	g++ $(RW_CXX) -c -o $@ $<
+
+# the binding: apply(VarLenTraverseOp) calls mgk_bind::walk_targets (fails if the patch misses)
+$(RW)/core/execute_mgk.cpp: $(REFPROJ)/core/src/execute.cpp
+	@mkdir -p $(RW)/core
+	sed -e 's|^#include "matgraph/execute.hpp"$$|#include "matgraph/execute.hpp"\n#include "mgk_bind.hpp"|' \
+	    -e 's|walk_targets(adj, src, op.min, op.max)|::mgk_bind::walk_targets(graph_, op.relation, op.direction, adj, src, op.min, op.max)|' \
+	    $< > $@
+	test "$$(grep -c 'mgk_bind::walk_targets' $@)" = 1 && test "$$(grep -c 'mgk_bind.hpp' $@)" = 1
+
+$(RW)/core/execute_mgk.o: $(RW)/core/execute_mgk.cpp tests/ref_wrap/mgk_bind.hpp | $(RW)/include/fmt
+	g++ $(RW_CXX) -c -o $@ $<
+
+$(RW)/mgk_bind.o: tests/ref_wrap/mgk_bind.cpp tests/ref_wrap/mgk_bind.hpp include/mgk.h | $(RW)/include/fmt
+	g++ $(RW_CXX) -c -o $@ $<
+
+$(RW)/t_%.o: $(REFPROJ)/tests/%.cpp tests/ref_wrap/doctest/doctest.h | $(RW)/include/fmt
+	g++ $(RW_CXX) -c -o $@ $<
+
+$(RW)/ref_tests_gpu: $(RW)/t_test_main.o $(RW)/t_test_execute.o $(RW)/t_test_bench.o $(RW_OBJS) $(LIB)
+	g++ -o $@ $(filter %.o,$^) $(RW_WRAP) $(RW_LIBS)
+
+$(RW)/acceptance_gpu: $(REFPROJ)/tests/acceptance/acceptance_main.cpp $(RW_OBJS) $(LIB) | $(RW)/include/fmt
+	g++ $(RW_CXX) -o $@ $< $(filter %.o,$^) $(RW_WRAP) $(RW_LIBS)
+
+$(RW)/varlen_gpu: tests/ref_wrap/varlen_main.cpp $(RW_OBJS) $(LIB) | $(RW)/include/fmt
+	g++ $(RW_CXX) -o $@ $< $(filter %.o,$^) $(RW_WRAP) $(RW_LIBS)

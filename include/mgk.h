@@ -127,6 +127,11 @@ int mgk_graph_load_snapshot(int device, const char* text, uint64_t len, const ch
 int mgk_graph_load_snapshot_file(int device, const char* path, const char* relation, mgk_graph** out,
                                  uint64_t* node_count);
 int mgk_snapshot_check(const char* text, uint64_t len, uint64_t* node_count, uint64_t* edge_count);
+/* The transpose A^T as its own device graph (transposed_matrix, graph.cpp:90-102;
+ * transpose, sparse.cpp:379-403), built on the device from g's arrays: walks
+ * and k-hop counts over it follow edges backwards (the `<-` direction of a
+ * Cypher pattern, execute.cpp:35-39). Free with mgk_graph_free. */
+int mgk_graph_transpose(const mgk_graph* g, mgk_graph** out);
 int mgk_graph_free(mgk_graph* g);
 int mgk_graph_info(const mgk_graph* g, uint64_t* nrows, uint64_t* nnz, int* device);
 /* Copy the device CSR back (uint32; either pointer may be NULL). */

@@ -79,6 +79,7 @@ SIGNATURES = [
     ("mgk_khop_device_stats", _int, [_vp, _vp, C.POINTER(MgkStats)]),
     ("mgk_khop_device_check", _int, [_vp, _vp]),
     ("mgk_graph_replicate", _int, [_vp, _int, C.POINTER(_vp)]),
+    ("mgk_graph_transpose", _int, [_vp, C.POINTER(_vp)]),
     ("mgk_khop_count_ks", _int, [_vp, _vp, _u64, _vp, _u32, _int, _vp]),
     ("mgk_khop_count_schedule", _int, [_vp, _vp, _vp, _vp, _u32, _int, _vp]),
     ("mgk_khop_count_device_schedule", _int, [_vp, _vp, _vp, _vp, _u32, _int, _vp, _vp]),

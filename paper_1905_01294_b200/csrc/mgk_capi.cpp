@@ -865,6 +865,22 @@ int mgk_graph_replicate(const mgk_graph* src, int device, mgk_graph** out) {
     return MGK_OK;
 }
 
+int mgk_graph_transpose(const mgk_graph* src, mgk_graph** out) {
+    if (!src || !out) return fail(MGK_ECONTRACT, "null argument");
+    DeviceGuard dg(src->g.device);
+    auto* h = new (std::nothrow) mgk_graph();
+    if (!h) return fail(MGK_ENOMEM, "out of host memory");
+    h->g.device = src->g.device;
+    cudaError_t e = transpose_device_graph(&src->g, &h->g);
+    if (e) {
+        free_device_graph(&h->g);
+        delete h;
+        return fail_cuda(e, "graph transpose");
+    }
+    *out = h;
+    return MGK_OK;
+}
+
 int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64_t* seeds, uint64_t nseeds,
                          uint32_t k, int mode, uint64_t* counts) {
     if (!replicas || nreplicas < 1) return fail(MGK_ECONTRACT, "no replicas");

@@ -623,6 +623,53 @@ cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
     return cudaDeviceSynchronize();
 }
 
+namespace {
+// one warp per row: every entry (r, c) of A becomes the key (c << 32 | r) of
+// A^T, in external ids (inv maps a relabelled device id back; null = identity)
+__global__ void transpose_keys(const uint32_t* rp, const uint32_t* ci, uint32_t n, const uint32_t* inv,
+                               unsigned long long* keys) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t r = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+        const uint32_t b = rp[r], e = rp[r + 1];
+        const uint32_t xr = inv ? inv[r] : (uint32_t)r;
+        for (uint32_t p = b + lane; p < e; p += 32) {
+            const uint32_t c = ci[p];
+            keys[p] = ((unsigned long long)(inv ? inv[c] : c) << 32) | xr;
+        }
+    }
+}
+}  // namespace
+
+// A^T as its own device graph (CSR of A^T = CSC of A, rows ascending), built
+// from src's device arrays: the `<-` direction of a Cypher walk
+// (execute.cpp:35-39 uses transposed_matrix).
+cudaError_t transpose_device_graph(const Graph* src, Graph* dst) {
+    const uint32_t n = src->dg.n;
+    const uint64_t m = src->dg.m;
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    unsigned long long *keys = nullptr, *alt = nullptr;
+    cudaError_t e = cudaSuccess;
+    do {
+        const size_t mp = (size_t)std::max<uint64_t>(m, 1);
+        if ((e = cudaMallocAsync(&keys, mp * 8, s))) break;
+        if ((e = cudaMallocAsync(&alt, mp * 8, s))) break;
+        if (m) {
+            transpose_keys<<<std::min<uint64_t>((n + 7) / 8, 1u << 20), 256, 0, s>>>(src->dg.rp, src->dg.ci, n,
+                                                                                    src->dg.inv, keys);
+            if ((e = cudaGetLastError())) break;
+        }
+        dst->dg.n = n;
+        e = graph_from_keys(dst, keys, alt, m, s);
+    } while (0);
+    cudaFreeAsync(keys, s);
+    cudaFreeAsync(alt, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e;
+}
+
 // sort + unique (src << 32 | dst) keys, then CSR + CSC (keys/alt: m entries each, consumed)
 cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
                             cudaStream_t s) {

@@ -261,6 +261,7 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
                                          int relabel);
 void free_device_graph(Graph* g);
 cudaError_t replicate_device_graph(const Graph* src, Graph* dst);
+cudaError_t transpose_device_graph(const Graph* src, Graph* dst);
 // sort + unique (src << 32 | dst) keys into g (g->dg.n set; keys/alt hold m
 // entries each and are consumed); cudaErrorInvalidValue if >= 2^32 remain
 cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,

@@ -168,6 +168,13 @@ class DeviceGraph:
         _check(_lib.lib().mgk_graph_replicate(self.handle, device, C.byref(h)))
         return DeviceGraph(h.value, self.node_count)
 
+    def transpose(self):
+        """A^T as its own device graph (mgk_graph_transpose): traversals over it
+        follow edges backwards (the `<-` direction of a Cypher pattern)."""
+        h = C.c_void_p()
+        _check(_lib.lib().mgk_graph_transpose(self.handle, C.byref(h)))
+        return DeviceGraph(h.value, node_count=self.node_count)
+
     def close(self):
         if getattr(self, "_h", None) and self._h.value:
             _lib.lib().mgk_graph_free(self._h)

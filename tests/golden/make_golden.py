@@ -28,7 +28,9 @@ through oracle/ref_capi.cpp:
   and the dimension error texts.
 * walk_pins.json — walk_targets (execute.cpp:43-60, the VarLenTraverse step)
   through the reference's own Cypher executor: counts and ids of
-  MATCH (a {id: S})-[*min..max]->(b) on RMAT graphs and a cycle with a loop.
+  MATCH (a {id: S})-[*min..max]->(b) and of the reversed pattern
+  (a)<-[*min..max]-(b) (over transposed_matrix) on RMAT graphs and a cycle
+  with a loop.
 
 The GPU box never runs this script (no /root/reference there); it only reads
 the committed JSON.
@@ -183,8 +185,11 @@ def walk_pins(R: oracle.Ref) -> dict:
             for lo, hi in ranges:
                 cnt = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN count(b)")
                 ids = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN b")
+                # the reversed pattern walks the transpose (execute.cpp:35-39)
+                in_ids = g.cypher(f"MATCH (a {{id: {s}}})<-[*{lo}..{hi}]-(b) RETURN b")
                 cases.append({"seed": s, "min": lo, "max": hi, "count": int(cnt.split("\n")[1]),
-                              "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t]})
+                              "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t],
+                              "in_ids": [int(t[1:]) for t in in_ids.split("\n")[1:] if t]})
         out["graphs"].append({"scale": scale, "rng_seed": rng, "cases": cases})
     # the seed reappears on a cycle; a self-loop keeps a walk alive (test_execute.cpp:89-97)
     edges = [[0, 1], [1, 2], [2, 0], [1, 1], [2, 3]]
@@ -194,8 +199,10 @@ def walk_pins(R: oracle.Ref) -> dict:
     for s in range(4):
         for lo, hi in ((1, 1), (1, 3), (2, 2), (3, 3), (2, 5)):
             ids = g.cypher(f"MATCH (a {{id: {s}}})-[*{lo}..{hi}]->(b) RETURN b")
+            in_ids = g.cypher(f"MATCH (a {{id: {s}}})<-[*{lo}..{hi}]-(b) RETURN b")
             tl.append({"seed": s, "min": lo, "max": hi,
-                       "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t]})
+                       "ids": [int(t[1:]) for t in ids.split("\n")[1:] if t],
+                       "in_ids": [int(t[1:]) for t in in_ids.split("\n")[1:] if t]})
     out["cycle_loop"] = {"edges": edges, "node_count": 4, "cases": tl}
     return out
 
