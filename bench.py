@@ -178,16 +178,17 @@ def single_source_bytes(st: dict, nseeds: int) -> float:
 def lanes_bytes(st: dict, n: int) -> float:
     """64-lane mode: per expanded level l, U_l = vertices with
     a non-zero frontier word: 4 sum_{v in U_l} outdeg(v) + 12 |U_l| + 24 W n
-    (three streaming passes over n W-word state words). union_edges of hop h
-    = sum of outdeg over U_{h-1}; vertices of hop h-1 = |U_{h-1}|."""
+    (three streaming passes over n W-word state words), per batch. The
+    counters are summed over batches: union_edges of hop h = sum of outdeg
+    over U_{h-1}, vertices of hop h-1 = |U_{h-1}|, runs = batches expanded.""" 
     lv = st["levels"]
     W = max(1, st["lanes"] // 64)
     total = 0.0
     for h in range(1, len(lv)):
         if not lv[h]["runs"]:
             continue
-        U = lv[h - 1]["vertices"] if h > 1 else min(st["lanes"], lv[0]["vertices"] or st["lanes"])
-        total += 4.0 * lv[h]["union_edges"] + 12.0 * U + 24.0 * W * n
+        U = lv[h - 1]["vertices"]  # summed over the batches that expanded
+        total += 4.0 * lv[h]["union_edges"] + 12.0 * U + 24.0 * W * n * lv[h]["runs"]
     return total
 
 
