@@ -32,6 +32,37 @@ __device__ __forceinline__ uint32_t atom_or_keep(uint32_t* p, uint32_t v, unsign
     return old;
 }
 
+// L2 evict-first policy for streamed, read-once data (the CSC row_idx a pull
+// scans), so it does not push the frontier words out of L2.
+__device__ __forceinline__ unsigned long long l2_stream_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// immutable graph arrays: non-coherent path, L1-allocating, L2 priority `pol`
+__device__ __forceinline__ uint32_t ldg_hint(const uint32_t* p, unsigned long long pol) {
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+// state written earlier in the same launch (ordered by the grid barrier):
+// coherent loads, L2 priority `pol`
+__device__ __forceinline__ uint32_t ld_hint_u8(const void* p, unsigned long long pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u8 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_hint_u16(const void* p, unsigned long long pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u16 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_hint_u64(const void* p, unsigned long long pol) {
+    unsigned long long v;
+    asm volatile("ld.global.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 // device id of an external seed id (locality relabelling; identity if none).
 // A seed >= n (the device path does not range-check on the host) raises the
 // graph's bad_seed flag and is replaced by vertex 0, so no read goes out of

@@ -93,10 +93,22 @@ __global__ void heavy_count(const uint32_t* cp, uint32_t n, uint32_t* cnt, uint3
     }
 }
 
-__global__ void heavy_fill(const uint32_t* cp, uint32_t n, const uint32_t* off, uint2* tasks) {
+// one key (chunk << 32 | vertex) per heavy task; sorted, the list is
+// chunk-major: every heavy vertex's first chunk comes before any second
+// chunk, so a later chunk usually finds its vertex already covered (the pull
+// checks before scanning) — the hubs-first in-list order then makes most
+// heavy vertices cost one chunk
+__global__ void heavy_fill(uint32_t n, const uint32_t* off, unsigned long long* keys) {
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
         const uint32_t c = off[u + 1] - off[u];
-        for (uint32_t i = 0; i < c; ++i) tasks[off[u] + i] = make_uint2(u, cp[u] + i * kHeavyChunk);
+        for (uint32_t i = 0; i < c; ++i) keys[off[u] + i] = ((unsigned long long)i << 32) | u;
+    }
+}
+
+__global__ void heavy_tasks(const unsigned long long* keys, uint64_t nt, const uint32_t* cp, uint2* tasks) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = (uint32_t)keys[t], i = (uint32_t)(keys[t] >> 32);
+        tasks[t] = make_uint2(u, cp[u] + i * kHeavyChunk);
     }
 }
 
@@ -271,8 +283,18 @@ cudaError_t build_heavy(Graph* g, cudaStream_t s) {
     MGK_TRY(cudaMalloc(&g->heavy, (size_t)std::max<unsigned long long>(total, 1) * sizeof(uint2)));
     g->dg.heavy = g->heavy;
     g->bytes += (size_t)std::max<unsigned long long>(total, 1) * sizeof(uint2);
-    if (total) heavy_fill<<<blocks_for(n), kTB, 0, s>>>(g->cp, n, cnt, g->heavy);
-    MGK_TRY(cudaGetLastError());
+    if (total) {
+        unsigned long long *keys = nullptr, *alt = nullptr;
+        MGK_TRY(cudaMallocAsync(&keys, total * 8, s));
+        MGK_TRY(cudaMallocAsync(&alt, total * 8, s));
+        heavy_fill<<<blocks_for(n), kTB, 0, s>>>(n, cnt, keys);
+        MGK_TRY(cudaGetLastError());
+        MGK_TRY(radix_sort_keys(keys, alt, total, 64, s));
+        heavy_tasks<<<blocks_for(total), kTB, 0, s>>>(keys, total, g->cp, g->heavy);
+        MGK_TRY(cudaGetLastError());
+        MGK_TRY(cudaFreeAsync(keys, s));
+        MGK_TRY(cudaFreeAsync(alt, s));
+    }
     MGK_TRY(cudaFreeAsync(cnt, s));
     MGK_TRY(cudaFreeAsync(d_total, s));
     return cudaSuccess;

@@ -137,6 +137,17 @@ struct LS<W, 64> {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
         atomicOr(b + v * W + i, m);
     }
+    // a pull's per-edge frontier-word gather, L2 priority `pol` (evict-last)
+    __device__ static __forceinline__ LaneWord<W> gather(const unsigned long long* b, size_t v,
+                                                         unsigned long long pol) {
+        if constexpr (W == 1) {
+            LaneWord<W> r;
+            r.w[0] = ld_hint_u64(b + v, pol);
+            return r;
+        } else {
+            return load_lw<W>(b + v * W);
+        }
+    }
     __host__ __device__ static constexpr size_t words64(size_t n) { return n * W; }
 };
 
@@ -156,6 +167,15 @@ struct LSNarrow {
             r.w[0] = __ldcg(reinterpret_cast<const unsigned short*>(b) + v);
         else
             r.w[0] = __ldcg(reinterpret_cast<const unsigned char*>(b) + v);
+        return r;
+    }
+    __device__ static __forceinline__ LaneWord<1> gather(const unsigned long long* b, size_t v,
+                                                         unsigned long long pol) {
+        LaneWord<1> r;
+        if constexpr (NB == 16)
+            r.w[0] = ld_hint_u16(reinterpret_cast<const unsigned short*>(b) + v, pol);
+        else
+            r.w[0] = ld_hint_u8(reinterpret_cast<const unsigned char*>(b) + v, pol);
         return r;
     }
     __device__ static __forceinline__ void store(unsigned long long* b, size_t v, const LaneWord<1>& x) {
@@ -324,15 +344,18 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
                                                        uint32_t b, uint32_t e, const LaneWord<W>& need,
                                                        uint32_t& scanned) {
     const uint32_t lane = lane_id();
+    const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     LaneWord<W> acc;
 #pragma unroll
     for (int i = 0; i < W; ++i) acc.w[i] = 0;
     scanned = 0;
-    for (uint32_t p0 = b; p0 < e; p0 += 256) {
-        const uint32_t pe = min(e, p0 + 256);
+    // coverage is tested after 64, 128, then every 256 entries: hubs come first
+    // in every in-list, so most vertices that exit early do so in the first block
+    for (uint32_t p0 = b, blk = 64; p0 < e; p0 += blk, blk = min(2 * blk, 256u)) {
+        const uint32_t pe = min(e, p0 + blk);
 #pragma unroll 2
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = LS<W, NB>::load(Fc, __ldg(P.g.ri + p));
+            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -368,6 +391,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
     // chunks per warp, at least 8 words each, so the counter stays cold
+    const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     const uint32_t wchunk = max(8u, g.nwords / (nwarps * 8));
     ChunkGrab words(&P.misc[1], g.nwords, wchunk, warp_gid);
     for (; words.valid(); words.advance(nwarps))
@@ -400,16 +424,16 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             uint32_t p = b;
             bool done = false;
             for (; p + 2 <= e && !done; p += 2) {
-                const uint32_t v0 = __ldg(g.ri + p), v1 = __ldg(g.ri + p + 1);
-                const LaneWord<W> f0 = LS<W, NB>::load(Fc, v0);
-                const LaneWord<W> f1 = LS<W, NB>::load(Fc, v1);
+                const uint32_t v0 = ldg_hint(g.ri + p, pol_ri), v1 = ldg_hint(g.ri + p + 1, pol_ri);
+                const LaneWord<W> f0 = LS<W, NB>::gather(Fc, v0, pol_f);
+                const LaneWord<W> f1 = LS<W, NB>::gather(Fc, v1, pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f0.w[i] | f1.w[i];
                 done = covers<W>(acc_w, need);
                 scanned += 2;
             }
             if (!done && p < e) {
-                const LaneWord<W> f = LS<W, NB>::load(Fc, __ldg(g.ri + p));
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -469,6 +493,17 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         for (int i = 0; i < W; ++i) {
             need.w[i] = active.w[i] & ~vis.w[i];
             cand |= need.w[i] != 0;
+        }
+        if (cand && task.y != __ldg(g.cp + u)) {
+            // a later chunk (tasks are chunk-major): only the lanes the earlier
+            // chunks of u have not found yet; none left -> nothing to scan
+            const LaneWord<W> got = LS<W, NB>::load_cg(Fn, u);
+            cand = false;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                need.w[i] &= ~got.w[i];
+                cand |= need.w[i] != 0;
+            }
         }
         bool first = false;
         if (cand) {
