@@ -20,6 +20,7 @@
 // touches: a discovery list per hop (raw list R, one entry per vertex whose
 // F' became non-zero) drives the finalize pass, the clearing of the previous
 // frontier and the final clearing of V.
+#include <cstdlib>
 #include <type_traits>
 
 #include "mgk_device.cuh"
@@ -62,6 +63,7 @@ struct MSParams {
     unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
+    uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
 template <int W>
@@ -745,6 +747,8 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             }
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
+            unsigned long long t1 = 0;
+            if (P.diag && gtid == 0) t1 = globaltimer();
             // ---- decide the next hop's direction (uniform) ---------------------------
             nR = ld_volatile(&qn->nitems);
             const unsigned long long mf = ld_volatile(&qn->edges);
@@ -776,7 +780,14 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             block_flush(acc, qn, qn, &P.lc[hop], hop < P.k ? &P.lc[hop + 1] : nullptr,
                         &P.misc[0]);
             grid_barrier(P.bar);
-            if (gtid == 0) atomicAdd(&P.lc[hop].ns, globaltimer() - t0);
+            if (gtid == 0) {
+                const unsigned long long t2 = globaltimer();
+                atomicAdd(&P.lc[hop].ns, t2 - t0);
+                if (P.diag) {  // probe mode: phase split (the counters these fields hold are lost)
+                    P.lc[hop].union_edges = t1 - t0;
+                    P.lc[hop].candidates = t2 - t1;
+                }
+            }
             clog_used += nR;
             nR_prev = nR;
             if (nR == 0) break;
@@ -855,6 +866,11 @@ cudaError_t launch_w(Launch& L) {
     P.misc = ws->misc;
     P.lc = ws->lc;
     P.bar = reinterpret_cast<unsigned int*>(ws->misc + 8);
+    static const uint32_t diag = [] {
+        const char* e = std::getenv("MGK_MS_DIAG");
+        return e && e[0] == '1' ? 1u : 0u;
+    }();
+    P.diag = diag;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
