@@ -221,6 +221,11 @@ __device__ __forceinline__ void store_item(uint4* items, uint32_t at, uint32_t s
     items[at] = make_uint4(s, e, src, 0);
 }
 
+// entries per push work item: kChunk, or 32 kChunk for rows longer than that
+// (a warp consumes a long item in 32 strides; a hub row of 766K entries is then
+// 750 items instead of 24K, which one warp would otherwise have to write)
+__device__ __forceinline__ uint32_t item_len(uint32_t deg) { return deg > 32 * kChunk ? 32 * kChunk : kChunk; }
+
 template <typename Item>
 __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, const uint32_t* buf,
                                            uint32_t n, Item* items, unsigned int* nitems) {
@@ -229,7 +234,8 @@ __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, cons
     uint32_t tot = 0;
     for (uint32_t i = lane; i < n; i += 32) {
         const uint32_t u = buf[i];
-        tot += (__ldg(rp + u + 1) - __ldg(rp + u) + kChunk - 1) / kChunk;
+        const uint32_t d = __ldg(rp + u + 1) - __ldg(rp + u);
+        tot += (d + item_len(d) - 1) / item_len(d);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
@@ -245,7 +251,8 @@ __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, cons
             b = __ldg(rp + u);
             deg = __ldg(rp + u + 1) - b;
         }
-        const uint32_t nit = (deg + kChunk - 1) / kChunk;
+        const uint32_t cs = item_len(deg);
+        const uint32_t nit = (deg + cs - 1) / cs;
         const uint32_t incl = warp_incl_scan(nit);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         const uint32_t excl = incl - nit;
@@ -256,9 +263,10 @@ __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, cons
             const uint32_t dj = __shfl_sync(kFull, deg, j);
             const uint32_t ej = __shfl_sync(kFull, excl, j);
             const uint32_t uj = __shfl_sync(kFull, u, j);
+            const uint32_t cj = __shfl_sync(kFull, cs, j);
             if (x < total) {
-                const uint32_t s = bj + (x - ej) * kChunk;
-                store_item(items, base + x, s, min(s + kChunk, bj + dj), uj);
+                const uint32_t s = bj + (x - ej) * cj;
+                store_item(items, base + x, s, min(s + cj, bj + dj), uj);
             }
         }
         base += total;

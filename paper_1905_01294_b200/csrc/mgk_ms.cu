@@ -351,9 +351,10 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
 #pragma unroll
     for (int i = 0; i < W; ++i) acc.w[i] = 0;
     scanned = 0;
-    // coverage is tested after 64, 128, then every 256 entries: hubs come first
-    // in every in-list, so most vertices that exit early do so in the first block
-    for (uint32_t p0 = b, blk = 64; p0 < e; p0 += blk, blk = min(2 * blk, 256u)) {
+    // coverage is tested after 32, 64, 128, then every 256 entries: hubs come
+    // first in every in-list, so most vertices that exit early do so in the
+    // first blocks
+    for (uint32_t p0 = b, blk = 32; p0 < e; p0 += blk, blk = min(2 * blk, 256u)) {
         const uint32_t pe = min(e, p0 + blk);
 #pragma unroll 2
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
@@ -396,36 +397,47 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     const uint32_t wchunk = max(8u, g.nwords / (nwarps * 8));
     ChunkGrab words(&P.misc[1], g.nwords, wchunk, warp_gid);
+    // a word costs one round trip before its scan starts: the skip masks of 32
+    // words arrive with one coalesced load, and each lane's CSC bounds are
+    // loaded together with its visited word (not after it): in the sparse late
+    // hops most words have no candidate, and a dependent chain per word would
+    // dominate
     for (; words.valid(); words.advance(nwarps))
-    for (uint32_t w = words.c * wchunk; w < min(g.nwords, (words.c + 1) * wchunk); ++w) {
-        const uint32_t skip = __ldg(g.pull_skip + w);
+    for (uint32_t wb = words.c * wchunk, wend = min(g.nwords, (words.c + 1) * wchunk); wb < wend; wb += 32) {
+    const uint32_t skip_l = wb + lane < wend ? __ldg(g.pull_skip + wb + lane) : kFull;
+    for (uint32_t w = wb; w < min(wend, wb + 32); ++w) {
+        const uint32_t skip = __shfl_sync(kFull, skip_l, w - wb);
         if (skip == kFull) continue;
         const uint32_t u = w * 32 + lane;
         LaneWord<W> need, vis;
 #pragma unroll
         for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
         bool cand = false;
+        uint32_t b = 0, e = 0;
         if (!((skip >> lane) & 1u)) {
             vis = LS<W, NB>::load(P.V, u);
+            b = __ldg(g.cp + u);
+            e = __ldg(g.cp + u + 1);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
                 cand |= need.w[i] != 0;
             }
         }
-        uint32_t b = 0, e = 0;
-        if (cand) {
-            b = __ldg(g.cp + u);
-            e = __ldg(g.cp + u + 1);
-        }
         LaneWord<W> acc_w;
 #pragma unroll
         for (int i = 0; i < W; ++i) acc_w.w[i] = 0;
         uint32_t scanned = 0;
-        if (cand && e - b <= 32) {
+        // in-degree <= 32: the lane scans the whole list; larger lists: the lane
+        // scans the first kPre entries (hubs come first, so most reached vertices
+        // are settled there) and the warp takes the rest of an unsettled list
+        constexpr uint32_t kPre = 8;
+        bool settled = false;
+        if (cand) {
+            const uint32_t stop = e - b <= 32 ? e : b + kPre;
             uint32_t p = b;
             bool done = false;
-            for (; p + 2 <= e && !done; p += 2) {
+            for (; p + 2 <= stop && !done; p += 2) {
                 const uint32_t v0 = ldg_hint(g.ri + p, pol_ri), v1 = ldg_hint(g.ri + p + 1, pol_ri);
                 const LaneWord<W> f0 = LS<W, NB>::gather(Fc, v0, pol_f);
                 const LaneWord<W> f1 = LS<W, NB>::gather(Fc, v1, pol_f);
@@ -434,25 +446,30 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 done = covers<W>(acc_w, need);
                 scanned += 2;
             }
-            if (!done && p < e) {
+            if (!done && p < stop) {
                 const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
+                ++p;
+                done = covers<W>(acc_w, need);
             }
+            settled = done || p >= e;
+            b = p;  // where the warp continues an unsettled list
         }
-        unsigned mid = __ballot_sync(kFull, cand && e - b > 32);
+        unsigned mid = __ballot_sync(kFull, cand && !settled);
         while (mid) {
             const int j = __ffs(mid) - 1;
             mid &= mid - 1;
-            LaneWord<W> nj;
+            LaneWord<W> nj;  // the lanes lane j's pre-scan has not found yet
 #pragma unroll
-            for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i], j);
+            for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i] & ~acc_w.w[i], j);
             uint32_t sc = 0;
             const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, __shfl_sync(kFull, b, j),
                                                       __shfl_sync(kFull, e, j), nj, sc);
             if ((int)lane == j) {
-                acc_w = aj;
+#pragma unroll
+                for (int i = 0; i < W; ++i) acc_w.w[i] |= aj.w[i];
                 scanned += sc;
             }
         }
@@ -479,6 +496,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
         }
+    }
     }
     // heavy in-degree vertices: one kHeavyChunk-entry task per warp step,
     // handed out in chunks of about an eighth of a warp's share (misc[2])

@@ -9,7 +9,7 @@
 
 void hub_sim(uint64_t n, const uint32_t* rp, const uint32_t* ci, const uint32_t* cp, const uint32_t* ri,
              const uint32_t* seeds, int ns, int k, const uint32_t* rank, const uint32_t* H, int nH,
-             uint64_t* scanned, uint64_t* hub_hits /* [k][nH] */) {
+             uint64_t* scanned, uint64_t* hub_hits /* [k][nH] */, uint64_t* fhits /* [k] */) {
     uint32_t* V = calloc(n, 4);
     uint32_t* F = calloc(n, 4);
     uint32_t* Fn = calloc(n, 4);
@@ -25,6 +25,7 @@ void hub_sim(uint64_t n, const uint32_t* rp, const uint32_t* ci, const uint32_t*
                 const uint32_t v = ri[p];
                 acc |= F[v];
                 ++sc;
+                if (F[v]) fhits[h - 1]++;
                 for (int i = 0; i < nH; ++i) if (rank[v] < H[i]) hub_hits[(h - 1) * nH + i]++;
                 if ((acc & need) == need) break;
             }

@@ -19,10 +19,10 @@ rank = np.empty(n, np.uint32); rank[order] = np.arange(n, dtype=np.uint32)
 Hs = np.array([8192, 16384, 32768, 65536, 131072, 262144], np.uint32)
 seeds = P.pick_seeds_u32(rp, 10, 1).astype(np.uint32)
 k = 6
-sc = np.zeros(k, np.uint64); hh = np.zeros((k, len(Hs)), np.uint64)
+sc = np.zeros(k, np.uint64); fh = np.zeros(k, np.uint64); hh = np.zeros((k, len(Hs)), np.uint64)
 C.CDLL('scripts/sim/hub_sim.so').hub_sim(C.c_uint64(n), p(rp), p(ci), p(cp), p(ri), p(seeds), 10, k, p(rank),
-                                         p(Hs), len(Hs), p(sc), p(hh))
+                                         p(Hs), len(Hs), p(sc), p(hh), p(fh))
 for h in range(k):
     if sc[h]:
-        print(f"hop {h+1}: scanned {sc[h]/1e6:9.2f}M  hub share " +
+        print(f"hop {h+1}: scanned {sc[h]/1e6:9.2f}M  frontier-source share {fh[h]/sc[h]:.2f}  hub share " +
               " ".join(f"H={int(x)//1024}K:{hh[h,i]/sc[h]:.2f}" for i, x in enumerate(Hs)))
