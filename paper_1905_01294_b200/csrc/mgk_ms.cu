@@ -63,6 +63,12 @@ struct MSParams {
     unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
+    // per-lane directions (LB <= 64): each lane pushes or pulls by its own
+    // Beamer test; lane_E [2][LB] out-edges of the frontier just found (by hop
+    // parity), lane_mu [LB] unexplored in-edges of each lane
+    uint32_t perlane;
+    unsigned long long* lane_E;
+    unsigned long long* lane_mu;
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -253,7 +259,7 @@ template <int W, int NB>
 __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
                            const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
                            QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
-                           uint32_t nwarps) {
+                           uint32_t nwarps, const LaneWord<W>& pushm) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     const uint32_t G = items_per_warp(nitems, nwarps);
@@ -280,7 +286,7 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
                 bool any = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    m.w[i] = f.w[i] & ~vis.w[i];
+                    m.w[i] = f.w[i] & ~vis.w[i] & pushm.w[i];  // only the lanes pushing this hop
                     any |= m.w[i] != 0;
                 }
                 if (any) {
@@ -389,7 +395,7 @@ struct ChunkGrab {
 template <int W, int NB>
 __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
-                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps) {
+                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -482,11 +488,23 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 found |= res.w[i] != 0;
             }
             if (found) {
-                LS<W, NB>::store(Fn, u, res);
-                bool fresh = true;
+                if (mixed) {
+                    // pushing lanes may have reached u in this hop too: OR the
+                    // pulled lanes in, and list u once (the touched bit)
 #pragma unroll
-                for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
-                count_discovered(g, u, fresh, acc);
+                    for (int i = 0; i < W; ++i)
+                        if (res.w[i]) LS<W, NB>::atomic_or(Fn, u, i, res.w[i]);
+                    const uint32_t bit = 1u << (u & 31);
+                    found = !(atomicOr(P.touched + (u >> 5), bit) & bit);
+                } else {
+                    LS<W, NB>::store(Fn, u, res);
+                }
+                if (found) {
+                    bool fresh = true;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
+                    count_discovered(g, u, fresh, acc);
+                }
             }
         }
         acc.candidates += cand;
@@ -571,9 +589,13 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
-                               uint32_t warp_gid, uint32_t nwarps) {
+                               uint32_t warp_gid, uint32_t nwarps, unsigned long long* s_E = nullptr,
+                               unsigned long long* s_mu = nullptr) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
+    // per-lane Beamer inputs (W = 1): lane l of the warp sums lanes l and 32 + l
+    constexpr uint32_t LBs = W == 1 ? LS<W, NB>::kLanes : 0;
+    unsigned long long eA[2] = {0, 0}, mA[2] = {0, 0};
     LaneWord<W> act;
     uint32_t cnt_lo[W], cnt_hi[W];
 #pragma unroll
@@ -584,7 +606,7 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
     for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
         const uint32_t idx = base + lane;
         const bool valid = idx < nR;
-        uint32_t u = 0;
+        uint32_t u = 0, deg_of = 0, indeg_of = 0;
         LaneWord<W> x;
 #pragma unroll
         for (int i = 0; i < W; ++i) x.w[i] = 0;
@@ -611,6 +633,25 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             acc.pairs += pc;
             acc.pe += (unsigned long long)deg * pc;
             expand = want_items && deg > 0;
+            if constexpr (LBs > 0)
+                if (s_E) indeg_of = __ldg(g.cp + u + 1) - __ldg(g.cp + u);
+            deg_of = deg;
+        }
+        if constexpr (LBs > 0) {
+            // lane b's frontier out-edges and newly visited in-edges, one
+            // warp reduction per lane bit
+            if (s_E && __ballot_sync(kFull, x.w[0] != 0)) {
+#pragma unroll 4
+                for (uint32_t bb = 0; bb < LBs; ++bb) {
+                    const bool on = (x.w[0] >> bb) & 1ull;
+                    const uint32_t se = __reduce_add_sync(kFull, on ? deg_of : 0u);
+                    const uint32_t sm = __reduce_add_sync(kFull, on ? indeg_of : 0u);
+                    if (lane == (bb & 31)) {
+                        eA[bb >> 5] += se;
+                        mA[bb >> 5] += sm;
+                    }
+                }
+            }
         }
         if (count_lanes) {
             // column popcounts: lane l accumulates bit l (cnt_lo) and bit 32+l
@@ -658,6 +699,45 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             if (NB == 64 && cnt_hi[i]) atomicAdd(&s_cnt[i * 64 + 32 + lane], (unsigned long long)cnt_hi[i]);
         }
     }
+    if constexpr (LBs > 0) {
+        if (s_E) {
+#pragma unroll
+            for (uint32_t h = 0; h < 2; ++h)
+                if (h * 32 + lane < LBs) {
+                    if (eA[h]) atomicAdd(&s_E[h * 32 + lane], eA[h]);
+                    if (mA[h]) atomicAdd(&s_mu[h * 32 + lane], mA[h]);
+                }
+        }
+    }
+}
+
+// next-hop push items for the frontier vertices with a pushing lane (after the
+// per-lane direction decision)
+template <int W, int NB>
+__device__ void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
+                           const LaneWord<W>& pushm, uint4* items_n, unsigned int* item_tail, Stage<kStageCap>& st,
+                           uint32_t warp_gid, uint32_t nwarps) {
+    const uint32_t lane = lane_id();
+    const DevGraph& g = P.g;
+    for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
+        const uint32_t idx = base + lane;
+        bool expand = false;
+        uint32_t u = 0;
+        if (idx < nR) {
+            u = Rn[idx];
+            const LaneWord<W> x = LS<W, NB>::load(Fn, u);
+#pragma unroll
+            for (int i = 0; i < W; ++i) expand |= (x.w[i] & pushm.w[i]) != 0;
+            expand = expand && __ldg(g.rp + u + 1) > __ldg(g.rp + u);
+        }
+        st.push(expand, u);
+        if (st.full()) {
+            emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+            st.n = 0;
+        }
+    }
+    emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+    st.n = 0;
 }
 
 template <int W, int NB>
@@ -678,6 +758,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     constexpr uint32_t LB = LS<W, NB>::kLanes;
     __shared__ uint32_t s_stage[kWarps][kStageCap];
     __shared__ unsigned long long s_cnt[LB];
+    // per-lane Beamer inputs (W = 1 only) and the decided pull-lane mask
+    constexpr uint32_t LBs = W == 1 ? LB : 1;
+    __shared__ unsigned long long s_E[LBs], s_mu[LBs];
+    __shared__ uint32_t s_pm[2];
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = gridDim.x * kBlock;
     const uint32_t warp_gid = gtid >> 5;
@@ -695,6 +779,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         for (uint32_t i = gtid; i < (P.k + 1) * LB; i += nthreads) P.lane_cnt[i] = 0;
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
+        if (P.perlane && gtid < LB) {
+            P.lane_E[gtid] = P.lane_E[LB + gtid] = 0;
+            P.lane_mu[gtid] = g.m;
+        }
         if (gtid == 0) {
             P.misc[0] = g.m;
             P.misc[1] = P.misc[2] = 0;  // pull work counters
@@ -725,11 +813,20 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         grid_barrier(P.bar);
         // ---- finalize level 0 (V |= F0, hop-1 items) ------------------------------
         uint32_t nR = ld_volatile(&P.qctl[0].nitems);
-        bool pull = P.force_dir == 2;
+        // the lanes pulling the current hop (all or none when the words are wider
+        // than 64 lanes); hop 1 pushes unless a pull is forced
+        LaneWord<W> pullm;
+#pragma unroll
+        for (int i = 0; i < W; ++i) pullm.w[i] = P.force_dir == 2 ? ~0ull : 0ull;
+        const bool pull0 = P.force_dir == 2;
         if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+        if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
         __syncthreads();
-        finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull, P.items0, &P.qctl[0].nfound, false,
-                          s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
+        finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull0, P.items0, &P.qctl[0].nfound, false,
+                          s_cnt, P.active, 0, acc, st, warp_gid, nwarps, P.perlane ? s_E : nullptr, s_mu);
+        __syncthreads();
+        if (P.perlane && threadIdx.x < LB && s_mu[threadIdx.x])
+            atomicAdd(&P.lane_mu[threadIdx.x], 0ull - s_mu[threadIdx.x]);
         acc.pairs = 0;  // the seeds themselves are never counted
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
         grid_barrier(P.bar);
@@ -746,58 +843,112 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             uint32_t* Rc = R_of(P, cur);
             uint32_t* Rn = R_of(P, nxt);
             unsigned long long t0 = 0;
+            LaneWord<W> actc, pushm, pm;
+            bool anypush = false, anypull = false;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                actc.w[i] = ld_volatile(P.active + cur * W + i);
+                pushm.w[i] = actc.w[i] & ~pullm.w[i];
+                pm.w[i] = actc.w[i] & pullm.w[i];
+                anypush |= pushm.w[i] != 0;
+                anypull |= pm.w[i] != 0;
+            }
             if (gtid == 0) {
                 t0 = globaltimer();
                 atomicAdd(&P.lc[hop].runs, 1u);
-                if (pull) atomicAdd(&P.lc[hop].pull_runs, 1u);
+                if (anypull) atomicAdd(&P.lc[hop].pull_runs, 1u);
                 atomicAdd(&P.lc[hop].union_edges, ld_volatile(&qc->edges));
             }
             if (gtid < W) P.active[nxt * W + gtid] = 0;  // rebuilt by this hop's finalize
-            // ---- expand ---------------------------------------------------------------
-            if (pull) {
-                LaneWord<W> act;
-#pragma unroll
-                for (int i = 0; i < W; ++i) act.w[i] = ld_volatile(P.active + cur * W + i);
-                pull_phase<W, NB>(P, Fc, Fn, act, Rn, qn, acc, st, warp_gid, nwarps);
-            } else {
+            // ---- expand: pushing lanes from the frontier's items, pulling lanes
+            // over the CSC (both in one phase: disjoint lanes, and a vertex both
+            // reach is listed once through its touched bit) -------------------------
+            if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
-                              st, warp_gid, nwarps);
-            }
+                              st, warp_gid, nwarps, pushm);
+            if (anypull) pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush);
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
             unsigned long long t1 = 0;
             if (P.diag && gtid == 0) t1 = globaltimer();
-            // ---- decide the next hop's direction (uniform) ---------------------------
             nR = ld_volatile(&qn->nitems);
             const unsigned long long mf = ld_volatile(&qn->edges);
             const unsigned long long mu = ld_volatile(&P.misc[0]);
-            const bool was_pull = pull;
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
-            if (P.force_dir == 1) {
-                pull = false;
-            } else if (P.force_dir == 2) {
-                pull = true;
-            } else if (!pull) {
-                pull = mf * P.alpha > mu;
-            } else {
-                pull = (unsigned long long)nR * P.beta >= g.n;
-            }
+            if (P.perlane && gtid < LB) P.lane_E[nxt * LB + gtid] = 0;  // (parity of the hop before: read)
             const bool last = hop == P.k || nR == 0;
-            const bool count_lanes = hop >= P.min_hop;
+            const bool count_lanes = hop >= P.min_hop || P.perlane;
             // ---- finalize -------------------------------------------------------------
             if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+            if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
-            finalize_phase<W, NB>(P, Rn, nR, Fn, true, !was_pull, !last && !pull, items_of(P, nxt),
-                              &qn->nfound, count_lanes, s_cnt, P.active + nxt * W, clog_used,
-                              acc, st, warp_gid, nwarps);
+            finalize_phase<W, NB>(P, Rn, nR, Fn, true, anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
+                              s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
+                              (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
             __syncthreads();
             if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
+            if (P.perlane && threadIdx.x < LB) {
+                if (s_E[threadIdx.x]) atomicAdd(&P.lane_E[nxt * LB + threadIdx.x], s_E[threadIdx.x]);
+                if (s_mu[threadIdx.x]) atomicAdd(&P.lane_mu[threadIdx.x], 0ull - s_mu[threadIdx.x]);
+            }
             block_flush(acc, qn, qn, &P.lc[hop], hop < P.k ? &P.lc[hop + 1] : nullptr,
                         &P.misc[0]);
             grid_barrier(P.bar);
+            // ---- the next hop's directions (every CTA computes the same) ---------------
+            if (!last) {
+                if (P.perlane) {
+                    // lane l: push -> pull when its frontier's out-edges x alpha exceed
+                    // its unexplored in-edges; pull -> push when its frontier x beta < n
+                    if (threadIdx.x < 64) {
+                        const uint32_t l = threadIdx.x;
+                        bool pl = false;
+                        if (l < LB) {
+                            const unsigned long long cnt = ld_cg(&P.lane_cnt[hop * LB + l]);
+                            if (cnt) {
+                                if (P.force_dir)
+                                    pl = P.force_dir == 2;
+                                else if ((pullm.w[0] >> l) & 1ull)
+                                    pl = cnt * P.beta >= g.n;
+                                else
+                                    pl = ld_cg(&P.lane_E[nxt * LB + l]) * P.alpha > ld_cg(&P.lane_mu[l]);
+                            }
+                        }
+                        const uint32_t b = __ballot_sync(kFull, pl);
+                        if (lane_id() == 0) s_pm[threadIdx.x >> 5] = b;
+                    }
+                    __syncthreads();
+                    pullm.w[0] = ((unsigned long long)s_pm[1] << 32) | s_pm[0];
+                    __syncthreads();
+                } else {
+                    bool pn;
+                    if (P.force_dir == 1) {
+                        pn = false;
+                    } else if (P.force_dir == 2) {
+                        pn = true;
+                    } else if (!anypull) {
+                        pn = mf * P.alpha > mu;
+                    } else {
+                        pn = (unsigned long long)nR * P.beta >= g.n;
+                    }
+#pragma unroll
+                    for (int i = 0; i < W; ++i) pullm.w[i] = pn ? ~0ull : 0ull;
+                }
+                // items for the lanes pushing next
+                LaneWord<W> pn_push;
+                bool anyn = false;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & ~pullm.w[i];
+                    anyn |= pn_push.w[i] != 0;
+                }
+                if (anyn) {
+                    emit_phase<W, NB>(P, Rn, nR, Fn, pn_push, items_of(P, nxt), &qn->nfound, st, warp_gid, nwarps);
+                    grid_barrier(P.bar);
+                }
+            }
             if (gtid == 0) {
                 const unsigned long long t2 = globaltimer();
                 atomicAdd(&P.lc[hop].ns, t2 - t0);
@@ -889,6 +1040,10 @@ cudaError_t launch_w(Launch& L) {
         return e && e[0] == '1' ? 1u : 0u;
     }();
     P.diag = diag;
+    static const bool uniform = std::getenv("MGK_LANES_UNIFORM") != nullptr;  // A/B: one direction for all lanes
+    P.perlane = (W == 1 && !uniform) ? 1u : 0u;
+    P.lane_E = ws->lane_stat;
+    P.lane_mu = ws->lane_stat + 2 * 512;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -920,6 +1075,7 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     }
     if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
+    if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;

@@ -63,6 +63,7 @@ def run(gname, bits_list, reps=5):
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "both"
     bits = [int(b) for b in sys.argv[2:]] or [64, 16]
+    # MGK_LANES_UNIFORM=1 in the environment: one direction for all lanes (A/B)
     res = {}
     for gname in (["G2", "G4"] if which == "both" else [which]):
         res.update(run(gname, bits))
