@@ -49,6 +49,12 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lpthread
 
+# compile-time variants for A/B runs: make variant VAR=step4 VFLAGS="-DMGK_LIGHT_STEP=4"
+# -> build/var_step4/libmgk.so (load it with MGK_LIB_PATH)
+.PHONY: variant
+variant:
+	$(MAKE) lib BUILD=build/var_$(VAR) LIB=build/var_$(VAR)/libmgk.so NVFLAGS="$(NVFLAGS) $(VFLAGS)"
+
 oracle:
 	$(MAKE) -s -C oracle oracle
 

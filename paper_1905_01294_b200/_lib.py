@@ -11,7 +11,8 @@ import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libmgk.so"
+# MGK_LIB_PATH: an alternative build of the same library (A/B runs of compile-time variants)
+LIB_PATH = Path(os.environ.get("MGK_LIB_PATH") or PKG / "lib" / "libmgk.so")
 
 MGK_OK, MGK_ECONTRACT, MGK_EHARNESS, MGK_ECUDA, MGK_ENOMEM, MGK_ERANGE, MGK_ESNAPSHOT = range(7)
 ENGINE_AUTO, ENGINE_SINGLE, ENGINE_LANES = 0, 1, 2

@@ -221,12 +221,11 @@ __device__ __forceinline__ void store_item(uint4* items, uint32_t at, uint32_t s
     items[at] = make_uint4(s, e, src, 0);
 }
 
-// entries per push work item: kChunk, or 32 kChunk for rows of more than 1024
-// kChunk entries (a warp consumes a long item in 32 strides; a hub row of 766K
-// entries is then 750 items instead of 24K, which one warp would otherwise
-// have to write). Shorter rows keep short items so a small frontier still
-// spreads over every warp.
-__device__ __forceinline__ uint32_t item_len(uint32_t deg) { return deg > 1024 * kChunk ? 32 * kChunk : kChunk; }
+// entries per push work item (kChunk for every row: longer items made the
+// warps holding a hub row's items the push's critical path — a push entry is a
+// chain of dependent random accesses — which cost more than writing the hub's
+// many short items)
+__device__ __forceinline__ uint32_t item_len(uint32_t) { return kChunk; }
 
 template <typename Item>
 __device__ __forceinline__ void emit_items(const uint32_t* __restrict__ rp, const uint32_t* buf,

@@ -31,6 +31,15 @@ namespace {
 using namespace dev;
 
 constexpr int kBlock = 512;
+// pull tuning (compile-time; variants are built for A/B runs): entries a lane
+// scans per step of a short in-list, and entries of a longer list it scans
+// before the warp takes over
+#ifndef MGK_LIGHT_STEP
+#define MGK_LIGHT_STEP 2
+#endif
+#ifndef MGK_PRE
+#define MGK_PRE 8
+#endif
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
 
@@ -437,27 +446,31 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         // in-degree <= 32: the lane scans the whole list; larger lists: the lane
         // scans the first kPre entries (hubs come first, so most reached vertices
         // are settled there) and the warp takes the rest of an unsettled list
-        constexpr uint32_t kPre = 8;
+        constexpr uint32_t kPre = MGK_PRE;
+        constexpr uint32_t kStep = MGK_LIGHT_STEP;
         bool settled = false;
         if (cand) {
             const uint32_t stop = e - b <= 32 ? e : b + kPre;
             uint32_t p = b;
             bool done = false;
-            for (; p + 2 <= stop && !done; p += 2) {
-                const uint32_t v0 = ldg_hint(g.ri + p, pol_ri), v1 = ldg_hint(g.ri + p + 1, pol_ri);
-                const LaneWord<W> f0 = LS<W, NB>::gather(Fc, v0, pol_f);
-                const LaneWord<W> f1 = LS<W, NB>::gather(Fc, v1, pol_f);
+            for (; p + kStep <= stop && !done; p += kStep) {
+                uint32_t v[kStep];
 #pragma unroll
-                for (int i = 0; i < W; ++i) acc_w.w[i] |= f0.w[i] | f1.w[i];
+                for (uint32_t q = 0; q < kStep; ++q) v[q] = ldg_hint(g.ri + p + q, pol_ri);
+#pragma unroll
+                for (uint32_t q = 0; q < kStep; ++q) {
+                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
+#pragma unroll
+                    for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
+                }
                 done = covers<W>(acc_w, need);
-                scanned += 2;
+                scanned += kStep;
             }
-            if (!done && p < stop) {
+            for (; !done && p < stop; ++p) {
                 const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
-                ++p;
                 done = covers<W>(acc_w, need);
             }
             settled = done || p >= e;
@@ -1040,8 +1053,11 @@ cudaError_t launch_w(Launch& L) {
         return e && e[0] == '1' ? 1u : 0u;
     }();
     P.diag = diag;
-    static const bool uniform = std::getenv("MGK_LANES_UNIFORM") != nullptr;  // A/B: one direction for all lanes
-    P.perlane = (W == 1 && !uniform) ? 1u : 0u;
+    // per-lane directions are opt-in: measured slower (a push entry costs several
+    // pull entries here, so the lanes that keep pushing at the dense hop cost
+    // more than the pull scans they save)
+    static const bool perlane = std::getenv("MGK_LANES_PERLANE") != nullptr;
+    P.perlane = (W == 1 && perlane) ? 1u : 0u;
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
     P.alpha = L.tuning.alpha_lanes;
