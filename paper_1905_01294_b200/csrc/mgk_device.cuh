@@ -89,6 +89,7 @@ __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p);
 __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long* p) {
     return __ldcg(p);
 }
+__device__ __forceinline__ uint32_t ld_cg_u8(const uint8_t* p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned int ld_volatile(const unsigned int* p) {
     return *reinterpret_cast<const volatile unsigned int*>(p);
 }

@@ -140,6 +140,7 @@ struct Workspace {
     uint4* ms_items[2] = {nullptr, nullptr};
     unsigned long long* lane_cnt = nullptr;  // [(MGK_MAX_HOPS+1) * 64 * W]
     unsigned long long* active = nullptr;    // [2 * W]
+    uint8_t* wact = nullptr;                  // [2][nwords] pull words left unsettled (by hop parity)
     unsigned long long* lane_stat = nullptr;  // [3 * 512]: per-lane frontier out-edges (x2) and unexplored in-edges
     // shared small control block
     QCtl* qctl = nullptr;                    // [3]

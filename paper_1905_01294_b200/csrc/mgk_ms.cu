@@ -78,6 +78,7 @@ struct MSParams {
     uint32_t perlane;
     unsigned long long* lane_E;
     unsigned long long* lane_mu;
+    uint8_t* wact;  // [2][nwords] by hop parity: words a pull left unsettled
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -404,7 +405,8 @@ struct ChunkGrab {
 template <int W, int NB>
 __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
-                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed) {
+                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
+                           const uint8_t* wact_in, uint8_t* wact_out) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -419,7 +421,12 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     // dominate
     for (; words.valid(); words.advance(nwarps))
     for (uint32_t wb = words.c * wchunk, wend = min(g.nwords, (words.c + 1) * wchunk); wb < wend; wb += 32) {
-    const uint32_t skip_l = wb + lane < wend ? __ldg(g.pull_skip + wb + lane) : kFull;
+    // wact_in (a pull right after a pull): words whose vertices all settled in
+    // that pull have no candidate now (the active lanes only shrink and the
+    // visited sets only grow); wact_out records this pull's unsettled words
+    const uint32_t skip_l = wb + lane < wend ? ((wact_in && !ld_cg_u8(wact_in + wb + lane)) ? kFull
+                                                 : __ldg(g.pull_skip + wb + lane)) : kFull;
+    uint32_t unsettled = 0;  // bit q: word wb + q still has a candidate with lanes left
     for (uint32_t w = wb; w < min(wend, wb + 32); ++w) {
         const uint32_t skip = __shfl_sync(kFull, skip_l, w - wb);
         if (skip == kFull) continue;
@@ -522,48 +529,71 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         }
         acc.candidates += cand;
         acc.scanned += scanned;
+        bool left = false;
+#pragma unroll
+        for (int i = 0; i < W; ++i) left |= (need.w[i] & ~acc_w.w[i]) != 0;
+        if (__ballot_sync(kFull, cand && left)) unsettled |= 1u << (w - wb);
         st.push(found, u);
         if (st.full()) {
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
         }
     }
+    if (wact_out && wb + lane < wend) wact_out[wb + lane] = (unsettled >> lane) & 1u;
     }
-    // heavy in-degree vertices: one kHeavyChunk-entry task per warp step,
-    // handed out in chunks of about an eighth of a warp's share (misc[2])
-    const uint32_t tchunk = max(1u, g.nheavy / (nwarps * 8));
+    // heavy in-degree vertices: kHeavyChunk-entry tasks (chunk-major). A warp
+    // checks 32 tasks at once (one task per lane: record, visited word and,
+    // for a later chunk, what the earlier chunks found) and scans only the
+    // tasks with lanes left, one after the other; in the late hops almost every
+    // task is settled and costs one parallel round of loads, not a chain per task
+    const uint32_t tchunk = max(32u, (g.nheavy / (nwarps * 4) + 31) / 32 * 32);
     ChunkGrab tasks(&P.misc[2], g.nheavy, tchunk, warp_gid);
     for (; tasks.valid(); tasks.advance(nwarps))
-    for (uint32_t t = tasks.c * tchunk; t < min(g.nheavy, (tasks.c + 1) * tchunk); ++t) {
-        const uint2 task = __ldg(g.heavy + t);
-        const uint32_t u = task.x;
-        const LaneWord<W> vis = LS<W, NB>::load(P.V, u);
-        LaneWord<W> need;
-        bool cand = false;
+    for (uint32_t t0 = tasks.c * tchunk, tend = min(g.nheavy, (tasks.c + 1) * tchunk); t0 < tend; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        uint32_t u = 0, ty = 0, tb = 0;
+        LaneWord<W> vis, need;
 #pragma unroll
-        for (int i = 0; i < W; ++i) {
-            need.w[i] = active.w[i] & ~vis.w[i];
-            cand |= need.w[i] != 0;
-        }
-        if (cand && task.y != __ldg(g.cp + u)) {
-            // a later chunk (tasks are chunk-major): only the lanes the earlier
-            // chunks of u have not found yet; none left -> nothing to scan
-            const LaneWord<W> got = LS<W, NB>::load_cg(Fn, u);
-            cand = false;
+        for (int i = 0; i < W; ++i) vis.w[i] = need.w[i] = 0;
+        bool cand = false;
+        if (t < tend) {
+            const uint2 task = __ldg(g.heavy + t);
+            u = task.x;
+            ty = task.y;
+            tb = __ldg(g.cp + u);
+            vis = LS<W, NB>::load(P.V, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
-                need.w[i] &= ~got.w[i];
+                need.w[i] = active.w[i] & ~vis.w[i];
                 cand |= need.w[i] != 0;
+            }
+            if (cand && ty != tb) {
+                // a later chunk: only the lanes the earlier chunks of u have not
+                // found yet; none left -> nothing to scan
+                const LaneWord<W> got = LS<W, NB>::load_cg(Fn, u);
+                cand = false;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    need.w[i] &= ~got.w[i];
+                    cand |= need.w[i] != 0;
+                }
             }
         }
         bool first = false;
-        if (cand) {
-            const uint32_t e = min(task.y + kHeavyChunk, __ldg(g.cp + u + 1));
+        unsigned todo = __ballot_sync(kFull, cand);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t uj = __shfl_sync(kFull, u, j), yj = __shfl_sync(kFull, ty, j);
+            LaneWord<W> nj;
+#pragma unroll
+            for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i], j);
+            const uint32_t e = min(yj + kHeavyChunk, __ldg(g.cp + uj + 1));
             uint32_t sc = 0;
-            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, task.y, e, need, sc);
-            if (lane == 0) {
+            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, yj, e, nj, sc);
+            if ((int)lane == j) {
                 acc.scanned += sc;
-                acc.candidates += task.y == __ldg(g.cp + u);
+                acc.candidates += ty == tb;
                 bool any = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
@@ -844,6 +874,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
         grid_barrier(P.bar);
 
+        bool prev_pull = false;  // the hop before pulled: its unsettled words bound this pull's
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
         uint32_t hop = 1;
@@ -879,7 +910,11 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
-            if (anypull) pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush);
+            if (anypull)
+                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
+                                  (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
+                                  P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
+            prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
             unsigned long long t1 = 0;
@@ -1060,6 +1095,7 @@ cudaError_t launch_w(Launch& L) {
     P.perlane = (W == 1 && perlane) ? 1u : 0u;
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
+    P.wact = ws->wact;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1092,6 +1128,7 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
+    if (!ws->wact && (e = cudaMalloc(&ws->wact, 2 * ((size_t)g.nwords + 32)))) return e;
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;
