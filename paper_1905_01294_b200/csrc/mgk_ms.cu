@@ -546,7 +546,10 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     // for a later chunk, what the earlier chunks found) and scans only the
     // tasks with lanes left, one after the other; in the late hops almost every
     // task is settled and costs one parallel round of loads, not a chain per task
-    const uint32_t tchunk = max(32u, (g.nheavy / (nwarps * 4) + 31) / 32 * 32);
+    // (many tasks per warp: chunks of 32-task groups; few: single tasks, so the
+    // scans still spread over every warp)
+    const uint32_t tchunk = g.nheavy >= nwarps * 64 ? (g.nheavy / (nwarps * 4) + 31) / 32 * 32
+                                                    : max(1u, g.nheavy / (nwarps * 8));
     ChunkGrab tasks(&P.misc[2], g.nheavy, tchunk, warp_gid);
     for (; tasks.valid(); tasks.advance(nwarps))
     for (uint32_t t0 = tasks.c * tchunk, tend = min(g.nheavy, (tasks.c + 1) * tchunk); t0 < tend; t0 += 32) {
@@ -588,6 +591,20 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             LaneWord<W> nj;
 #pragma unroll
             for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i], j);
+            if (yj != __shfl_sync(kFull, tb, j)) {  // a later chunk: drop the lanes found meanwhile
+                const LaneWord<W> got = LS<W, NB>::load_cg(Fn, uj);
+                bool left = false;
+#pragma unroll
+                for (int i = 0; i < W; ++i) {
+                    nj.w[i] &= ~got.w[i];
+                    left |= nj.w[i] != 0;
+                }
+                if (!left) continue;
+                if ((int)lane == j) {
+#pragma unroll
+                    for (int i = 0; i < W; ++i) need.w[i] = nj.w[i];
+                }
+            }
             const uint32_t e = min(yj + kHeavyChunk, __ldg(g.cp + uj + 1));
             uint32_t sc = 0;
             const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, yj, e, nj, sc);
