@@ -548,12 +548,16 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
     // task is settled and costs one parallel round of loads, not a chain per task
     // (many tasks per warp: chunks of 32-task groups; few: single tasks, so the
     // scans still spread over every warp)
-    const uint32_t tchunk = g.nheavy >= nwarps * 64 ? (g.nheavy / (nwarps * 4) + 31) / 32 * 32
-                                                    : max(1u, g.nheavy / (nwarps * 8));
+    // Batched only after a pull (wact_in): then most tasks are settled; in the
+    // first, dense pull a task is checked right before its scan, which sees
+    // more of what its vertex's earlier chunks found
+    const uint32_t tchunk = (wact_in && g.nheavy >= nwarps * 64) ? (g.nheavy / (nwarps * 4) + 31) / 32 * 32
+                                                                 : max(1u, g.nheavy / (nwarps * 8));
+    const uint32_t tstep = (wact_in && g.nheavy >= nwarps * 64) ? 32u : 1u;
     ChunkGrab tasks(&P.misc[2], g.nheavy, tchunk, warp_gid);
     for (; tasks.valid(); tasks.advance(nwarps))
-    for (uint32_t t0 = tasks.c * tchunk, tend = min(g.nheavy, (tasks.c + 1) * tchunk); t0 < tend; t0 += 32) {
-        const uint32_t t = t0 + lane;
+    for (uint32_t t0 = tasks.c * tchunk, tend = min(g.nheavy, (tasks.c + 1) * tchunk); t0 < tend; t0 += tstep) {
+        const uint32_t t = lane < tstep ? t0 + lane : tend;
         uint32_t u = 0, ty = 0, tb = 0;
         LaneWord<W> vis, need;
 #pragma unroll
