@@ -155,7 +155,8 @@ struct LS<W, 64> {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
         atomicOr(b + v * W + i, m);
     }
-    // a pull's per-edge frontier-word gather, L2 priority `pol` (evict-last)
+    // a pull's per-edge frontier-word gather, L2 priority `pol` (evict-last);
+    // also used with an evict-first policy for the pull's visited-word reads
     __device__ static __forceinline__ LaneWord<W> gather(const unsigned long long* b, size_t v,
                                                          unsigned long long pol) {
         if constexpr (W == 1) {
@@ -165,6 +166,14 @@ struct LS<W, 64> {
         } else {
             return load_lw<W>(b + v * W);
         }
+    }
+    // the pull's next-frontier store: evict-first, so it does not displace the
+    // frontier words the gathers need
+    __device__ static __forceinline__ void store_stream(unsigned long long* b, size_t v, const LaneWord<W>& x) {
+        if constexpr (W == 1)
+            st_stream_u64(b + v, x.w[0]);
+        else
+            store_lw<W>(b + v * W, x);
     }
     __host__ __device__ static constexpr size_t words64(size_t n) { return n * W; }
 };
@@ -198,6 +207,12 @@ struct LSNarrow {
     }
     __device__ static __forceinline__ void store(unsigned long long* b, size_t v, const LaneWord<1>& x) {
         reinterpret_cast<T*>(b)[v] = (T)x.w[0];
+    }
+    __device__ static __forceinline__ void store_stream(unsigned long long* b, size_t v, const LaneWord<1>& x) {
+        if constexpr (NB == 16)
+            st_stream_u16(reinterpret_cast<unsigned short*>(b) + v, (uint32_t)x.w[0]);
+        else
+            st_stream_u8(reinterpret_cast<unsigned char*>(b) + v, (uint32_t)x.w[0]);
     }
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int, unsigned long long m) {
         constexpr uint32_t per = 32 / NB;
@@ -437,7 +452,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
         bool cand = false;
         uint32_t b = 0, e = 0;
         if (!((skip >> lane) & 1u)) {
-            vis = LS<W, NB>::load(P.V, u);
+            vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
             b = __ldg(g.cp + u);
             e = __ldg(g.cp + u + 1);
 #pragma unroll
@@ -517,7 +532,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                     const uint32_t bit = 1u << (u & 31);
                     found = !(atomicOr(P.touched + (u >> 5), bit) & bit);
                 } else {
-                    LS<W, NB>::store(Fn, u, res);
+                    LS<W, NB>::store_stream(Fn, u, res);
                 }
                 if (found) {
                     bool fresh = true;
