@@ -79,6 +79,10 @@ struct MSParams {
     unsigned long long* lane_E;
     unsigned long long* lane_mu;
     uint8_t* wact;  // [2][nwords] by hop parity: words a pull left unsettled
+    uint4* fblk;                  // compact frontier: [n / 64 + 1] {bits lo, bits hi, rank, 0} (zero between uses)
+    unsigned long long* fcomp;    // packed words, up to fcap of them
+    unsigned long long* fctot;    // [grid] per-CTA member counts
+    uint32_t fcap;                // compact only when the frontier has <= fcap vertices
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -155,6 +159,12 @@ struct LS<W, 64> {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
         atomicOr(b + v * W + i, m);
     }
+    // (W = 1) OR m into v's word; true for the caller whose OR found the word
+    // empty, i.e. the first to reach v in this hop (the word is zero between hops)
+    __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
+        static_assert(W == 1, "one word per vertex");
+        return atomicOr(b + v, m) == 0;
+    }
     // a pull's per-edge frontier-word gather, L2 priority `pol` (evict-last);
     // also used with an evict-first policy for the pull's visited-word reads
     __device__ static __forceinline__ LaneWord<W> gather(const unsigned long long* b, size_t v,
@@ -218,12 +228,45 @@ struct LSNarrow {
         constexpr uint32_t per = 32 / NB;
         atomicOr(reinterpret_cast<unsigned int*>(b) + v / per, (unsigned int)m << (NB * (v % per)));
     }
+    __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
+        constexpr uint32_t per = 32 / NB;
+        const uint32_t sh = NB * (v % per);
+        const unsigned int old = atomicOr(reinterpret_cast<unsigned int*>(b) + v / per, (unsigned int)m << sh);
+        return ((old >> sh) & ((1u << NB) - 1u)) == 0;
+    }
     __host__ __device__ static constexpr size_t words64(size_t n) { return (n * NB + 63) / 64; }
 };
 template <>
 struct LS<1, 16> : LSNarrow<16> {};
 template <>
 struct LS<1, 8> : LSNarrow<8> {};
+
+// The frontier a pull reads. Dense: one word per vertex (F). Compact (one
+// word per vertex, small frontier): per 64-vertex block a record {membership
+// bits, rank of the block's first member} and the members' words packed in
+// rank order — ~10 MB for G4's hop-3 frontier instead of a 71 MB array, so the
+// per-edge gathers of the first dense pull hit L2 instead of DRAM.
+struct FView {
+    const unsigned long long* F;
+    const uint4* blk;                 // null: dense
+    const unsigned long long* comp;
+};
+
+template <int W, int NB>
+__device__ __forceinline__ LaneWord<W> fgather(const FView& fv, uint32_t v, unsigned long long pol) {
+    if constexpr (W == 1) {
+        if (fv.blk) {
+            const uint4 r = fv.blk[v >> 6];
+            const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
+            const uint32_t o = v & 63;
+            LaneWord<1> x;
+            x.w[0] = 0;
+            if ((bits >> o) & 1ull) x = LS<W, NB>::load(fv.comp, r.z + __popcll(bits & ((1ull << o) - 1ull)));
+            return x;
+        }
+    }
+    return LS<W, NB>::gather(fv.F, v, pol);
+}
 
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.items1 : P.items0;
@@ -273,11 +316,6 @@ __device__ void block_flush(Acc& a, QCtl* q, QCtl* qf, LevelCounters* lc, LevelC
     a.zero();
 }
 
-__device__ __forceinline__ void count_discovered(const DevGraph& g, uint32_t u, bool first, Acc& acc) {
-    acc.found += 1;
-    acc.edges += __ldg(g.rp + u + 1) - __ldg(g.rp + u);
-    if (first) acc.indeg += __ldg(g.cp + u + 1) - __ldg(g.cp + u);
-}
 
 // ---- push expand -----------------------------------------------------------------
 template <int W, int NB>
@@ -315,24 +353,22 @@ __device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitem
                     any |= m.w[i] != 0;
                 }
                 if (any) {
-                    const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u);
-                    bool need = false;
+                    if constexpr (W == 1) {
+                        // one atomic: the OR that finds the word empty lists u
+                        first = LS<W, NB>::atomic_or_first(Fn, u, m.w[0]);
+                    } else {
+                        const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u);
+                        bool need = false;
 #pragma unroll
-                    for (int i = 0; i < W; ++i) {
-                        if ((cur.w[i] & m.w[i]) != m.w[i]) {
-                            LS<W, NB>::atomic_or(Fn, u, i, m.w[i]);
-                            need = true;
+                        for (int i = 0; i < W; ++i) {
+                            if ((cur.w[i] & m.w[i]) != m.w[i]) {
+                                LS<W, NB>::atomic_or(Fn, u, i, m.w[i]);
+                                need = true;
+                            }
                         }
-                    }
-                    if (need) {
-                        const uint32_t bit = 1u << (u & 31);
-                        const uint32_t old = atomicOr(P.touched + (u >> 5), bit);
-                        if (!(old & bit)) {
-                            first = true;
-                            bool fresh = true;
-#pragma unroll
-                            for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
-                            count_discovered(g, u, fresh, acc);
+                        if (need) {  // several words: the touched bit decides who lists u
+                            const uint32_t bit = 1u << (u & 31);
+                            first = !(atomicOr(P.touched + (u >> 5), bit) & bit);
                         }
                     }
                 }
@@ -373,7 +409,7 @@ __device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>
 // Warp-wide: OR of the lane words of in-neighbours ri[b..e), stopping early
 // once `need` is covered. Returns the OR (all lanes) and the entries read.
 template <int W, int NB>
-__device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
+__device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const FView& Fc,
                                                        uint32_t b, uint32_t e, const LaneWord<W>& need,
                                                        uint32_t& scanned) {
     const uint32_t lane = lane_id();
@@ -389,7 +425,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
         const uint32_t pe = min(e, p0 + blk);
 #pragma unroll 2
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
+            const LaneWord<W> f = fgather<W, NB>(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -418,7 +454,7 @@ struct ChunkGrab {
 };
 
 template <int W, int NB>
-__device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
+__device__ void pull_phase(const MSParams& P, const FView& Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
                            const uint8_t* wact_in, uint8_t* wact_out) {
@@ -481,7 +517,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 for (uint32_t q = 0; q < kStep; ++q) v[q] = ldg_hint(g.ri + p + q, pol_ri);
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
-                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
+                    const LaneWord<W> f = fgather<W, NB>(Fc, v[q], pol_f);
 #pragma unroll
                     for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 }
@@ -489,7 +525,7 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
+                const LaneWord<W> f = fgather<W, NB>(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -524,21 +560,12 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             }
             if (found) {
                 if (mixed) {
-                    // pushing lanes may have reached u in this hop too: OR the
-                    // pulled lanes in, and list u once (the touched bit)
-#pragma unroll
-                    for (int i = 0; i < W; ++i)
-                        if (res.w[i]) LS<W, NB>::atomic_or(Fn, u, i, res.w[i]);
-                    const uint32_t bit = 1u << (u & 31);
-                    found = !(atomicOr(P.touched + (u >> 5), bit) & bit);
+                    // pushing lanes may have reached u in this hop too (mixed hops
+                    // only with one word per vertex): OR the pulled lanes in, and
+                    // list u once
+                    if constexpr (W == 1) found = LS<W, NB>::atomic_or_first(Fn, u, res.w[0]);
                 } else {
                     LS<W, NB>::store_stream(Fn, u, res);
-                }
-                if (found) {
-                    bool fresh = true;
-#pragma unroll
-                    for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
-                    count_discovered(g, u, fresh, acc);
                 }
             }
         }
@@ -630,23 +657,24 @@ __device__ void pull_phase(const MSParams& P, const unsigned long long* Fc, unsi
             if ((int)lane == j) {
                 acc.scanned += sc;
                 acc.candidates += ty == tb;
-                bool any = false;
+                // several chunks of one vertex (and, in a mixed hop, pushing
+                // lanes) OR into its word: the first to find it empty lists it
+                if constexpr (W == 1) {
+                    const unsigned long long r = aj.w[0] & need.w[0];
+                    if (r) first = LS<W, NB>::atomic_or_first(Fn, u, r);
+                } else {
+                    bool any = false;
 #pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    const unsigned long long r = aj.w[i] & need.w[i];
-                    if (r) {
-                        LS<W, NB>::atomic_or(Fn, u, i, r);
-                        any = true;
+                    for (int i = 0; i < W; ++i) {
+                        const unsigned long long r = aj.w[i] & need.w[i];
+                        if (r) {
+                            LS<W, NB>::atomic_or(Fn, u, i, r);
+                            any = true;
+                        }
                     }
-                }
-                if (any) {  // several chunks of one vertex: the first one enqueues it
-                    const uint32_t bit = 1u << (u & 31);
-                    first = !(atomicOr(P.touched + (u >> 5), bit) & bit);
-                    if (first) {
-                        bool fresh = true;
-#pragma unroll
-                        for (int i = 0; i < W; ++i) fresh &= vis.w[i] == 0;
-                        count_discovered(g, u, fresh, acc);
+                    if (any) {
+                        const uint32_t bit = 1u << (u & 31);
+                        first = !(atomicOr(P.touched + (u >> 5), bit) & bit);
                     }
                 }
             }
@@ -694,6 +722,9 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             u = Rn[idx];
             x = LS<W, NB>::load(Fn, u);
             LaneWord<W> v = LS<W, NB>::load(P.V, u);
+            bool fresh = true;  // no lane had visited u: its in-edges leave the unexplored set
+#pragma unroll
+            for (int i = 0; i < W; ++i) fresh &= v.w[i] == 0;
             uint32_t pc = 0;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
@@ -705,15 +736,20 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             // push levels set a touched bit per discovery; pull levels only for
             // heavy vertices (discovered vertices in pull_skip are heavy: a
             // zero-in-degree vertex is never discovered)
-            if (touched_set || ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u))
-                atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
+            if constexpr (W > 1)  // (one word per vertex: the word itself decides who lists u)
+                if (touched_set || ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u))
+                    atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
             if (clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
             const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
+            const bool need_in = fresh || (LBs > 0 && s_E);
+            const uint32_t indeg = need_in ? __ldg(g.cp + u + 1) - __ldg(g.cp + u) : 0;
+            acc.found += 1;  // distinct vertices discovered, their out-edges, fresh in-edges
+            acc.edges += deg;
+            if (fresh) acc.indeg += indeg;
             acc.pairs += pc;
             acc.pe += (unsigned long long)deg * pc;
             expand = want_items && deg > 0;
-            if constexpr (LBs > 0)
-                if (s_E) indeg_of = __ldg(g.cp + u + 1) - __ldg(g.cp + u);
+            indeg_of = indeg;
             deg_of = deg;
         }
         if constexpr (LBs > 0) {
@@ -828,6 +864,67 @@ __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F,
     for (uint32_t i = gtid; i < n; i += nthreads) LS<W, NB>::store(F, R[i], z);
 }
 
+// Compact frontier for the pull: membership bits of the nR frontier vertices
+// R, each 64-vertex block's rank (a grid-wide exclusive scan of the blocks'
+// popcounts), then each member's word packed at its rank. Three grid barriers.
+template <int W, int NB>
+__device__ void build_compact(const MSParams& P, const uint32_t* R, uint32_t nR, const unsigned long long* F,
+                              unsigned long long* s_scr, uint32_t gtid, uint32_t nthreads) {
+    const uint32_t nblk = (P.g.n + 63) / 64;
+    for (uint32_t i = gtid; i < nR; i += nthreads) {
+        const uint32_t u = R[i];
+        atomicOr(reinterpret_cast<unsigned long long*>(P.fblk + (u >> 6)), 1ull << (u & 63));
+    }
+    grid_barrier(P.bar);
+    // each CTA ranks a contiguous range of blocks, kBlock records per tile
+    const uint32_t per = (nblk + gridDim.x - 1) / gridDim.x;
+    const uint32_t lo = min(nblk, blockIdx.x * per), hi = min(nblk, lo + per);
+    __shared__ uint32_t s_wsum[kWarps];
+    uint32_t run = 0;  // members before this tile within the CTA's range
+    for (uint32_t t0 = lo; t0 < hi; t0 += kBlock) {
+        const uint32_t b = t0 + threadIdx.x;
+        uint32_t c = 0;
+        if (b < hi) {
+            const uint4 r = P.fblk[b];
+            c = __popc(r.x) + __popc(r.y);
+        }
+        const uint32_t incl = warp_incl_scan(c);
+        if (lane_id() == 31) s_wsum[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        uint32_t before = 0, tot = 0;
+        for (uint32_t w = 0; w < kWarps; ++w) {
+            const uint32_t x = s_wsum[w];
+            before += w < (threadIdx.x >> 5) ? x : 0;
+            tot += x;
+        }
+        if (b < hi) P.fblk[b].z = run + before + incl - c;
+        run += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) P.fctot[blockIdx.x] = run;
+    grid_barrier(P.bar);
+    // add the members of the CTAs before this one
+    if (threadIdx.x == 0) {
+        unsigned long long base = 0;
+        for (uint32_t c = 0; c < blockIdx.x; ++c) base += ld_cg(P.fctot + c);
+        s_scr[0] = base;
+    }
+    __syncthreads();
+    const uint32_t base = (uint32_t)s_scr[0];
+    __syncthreads();
+    if (base)
+        for (uint32_t b = lo + threadIdx.x; b < hi; b += kBlock) P.fblk[b].z += base;
+    grid_barrier(P.bar);
+    for (uint32_t i = gtid; i < nR; i += nthreads) {
+        const uint32_t u = R[i];
+        const uint4 r = P.fblk[u >> 6];
+        const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
+        const uint32_t o = u & 63;
+        LS<W, NB>::store(P.fcomp, r.z + __popcll(bits & ((1ull << o) - 1ull)), LS<W, NB>::load(F, u));
+    }
+    grid_barrier(P.bar);
+}
+
 template <int W, int NB>
 __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     grid_barrier_init(P.bar);
@@ -880,7 +977,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 LS<W, NB>::atomic_or(P.F0, s, gtid >> 6, bit);
                 const uint32_t tb = 1u << (s & 31);
                 first = !(atomicOr(P.touched + (s >> 5), tb) & tb);
-                if (first) count_discovered(g, s, true, acc);
+
             }
             if (blockIdx.x * kBlock < lanes) {
                 st.push(first, s);
@@ -946,8 +1043,16 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
+            // a pure pull from a small frontier reads it compacted (FView)
+            const bool compact = W == 1 && anypull && !anypush && P.fblk && nR_prev <= P.fcap;
+            FView fv{Fc, nullptr, nullptr};
+            if (compact) {
+                build_compact<W, NB>(P, Rc, nR_prev, Fc, s_cnt, gtid, nthreads);
+                fv.blk = P.fblk;
+                fv.comp = P.fcomp;
+            }
             if (anypull)
-                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
+                pull_phase<W, NB>(P, fv, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
                                   (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
                                   P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
             prev_pull = anypull;
@@ -956,8 +1061,6 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             unsigned long long t1 = 0;
             if (P.diag && gtid == 0) t1 = globaltimer();
             nR = ld_volatile(&qn->nitems);
-            const unsigned long long mf = ld_volatile(&qn->edges);
-            const unsigned long long mu = ld_volatile(&P.misc[0]);
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
             if (P.perlane && gtid < LB) P.lane_E[nxt * LB + gtid] = 0;  // (parity of the hop before: read)
             const bool last = hop == P.k || nR == 0;
@@ -971,6 +1074,9 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
                               (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
+            if (compact)  // the records are zero between uses
+                for (uint32_t i = gtid; i < nR_prev; i += nthreads)
+                    reinterpret_cast<uint4*>(P.fblk)[Rc[i] >> 6] = make_uint4(0, 0, 0, 0);
             __syncthreads();
             if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
@@ -1007,6 +1113,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                     pullm.w[0] = ((unsigned long long)s_pm[1] << 32) | s_pm[0];
                     __syncthreads();
                 } else {
+                    // (the finalize counted the new frontier's out-edges and the
+                    // in-edges that left the unexplored set)
+                    const unsigned long long mf = ld_volatile(&qn->edges);
+                    const unsigned long long mu = ld_volatile(&P.misc[0]);
                     bool pn;
                     if (P.force_dir == 1) {
                         pn = false;
@@ -1132,6 +1242,10 @@ cudaError_t launch_w(Launch& L) {
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
     P.wact = ws->wact;
+    P.fblk = W == 1 ? ws->fblk : nullptr;
+    P.fcomp = ws->fcomp;
+    P.fctot = ws->fctot;
+    P.fcap = gr->dg.n / 8;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1165,6 +1279,14 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
     if (!ws->wact && (e = cudaMalloc(&ws->wact, 2 * ((size_t)g.nwords + 32)))) return e;
+    if (!ws->fblk) {  // compact frontier (W = 1 pulls): records zeroed once, kept zero between uses
+        const size_t nblk = ((size_t)g.n + 63) / 64 + 1;
+        if ((e = cudaMalloc(&ws->fblk, nblk * sizeof(uint4)))) return e;
+        if ((e = cudaMemset(ws->fblk, 0, nblk * sizeof(uint4)))) return e;
+        if ((e = cudaMalloc(&ws->fcomp, ((size_t)g.n / 8 + 64) * 8))) return e;
+        if ((e = cudaMalloc(&ws->fctot, 8192 * 8))) return e;
+        ws->bytes += nblk * sizeof(uint4) + ((size_t)g.n / 8 + 64) * 8 + 8192 * 8;
+    }
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;
