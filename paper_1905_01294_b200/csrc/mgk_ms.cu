@@ -736,9 +736,11 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
             // push levels set a touched bit per discovery; pull levels only for
             // heavy vertices (discovered vertices in pull_skip are heavy: a
             // zero-in-degree vertex is never discovered)
-            if constexpr (W > 1)  // (one word per vertex: the word itself decides who lists u)
-                if (touched_set || ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u))
-                    atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
+            // touched bits: the seeds' (level 0) and, with several words per
+            // vertex, the push's and the heavy pull tasks' (one word per
+            // vertex: the word itself decides who lists u)
+            if (touched_set || (W > 1 && ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u)))
+                atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
             if (clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
             const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
             const bool need_in = fresh || (LBs > 0 && s_E);
@@ -1070,7 +1072,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
-            finalize_phase<W, NB>(P, Rn, nR, Fn, true, anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
+            finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
                               (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
