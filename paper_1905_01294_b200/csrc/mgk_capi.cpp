@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <new>
 #include <optional>
 #include <string>
@@ -384,6 +385,59 @@ cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, voi
     }();
     if (noncoop) return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, 0, stream);
     return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(block), args, 0, stream);
+}
+
+// Persistent launch whose accesses to [base, base + bytes) are marked
+// L2-persisting (the frontier words a pull gathers per edge): the device's
+// persisting L2 set-aside is raised to its maximum once, and the window's hit
+// ratio is the share of the window that fits it.
+cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, void** args, cudaStream_t stream,
+                                 void* base, size_t bytes) {
+    static const bool noncoop = [] {
+        const char* v = std::getenv("MGK_NONCOOP");
+        return v && v[0] == '1';
+    }();
+    static std::mutex mu;
+    static int maxp[64] = {};
+    static bool done[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    dev &= 63;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!done[dev]) {
+            if (cudaDeviceGetAttribute(&maxp[dev], cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+                cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp[dev]) != cudaSuccess) {
+                cudaGetLastError();
+                maxp[dev] = 0;
+            }
+            done[dev] = true;
+        }
+    }
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (!noncoop) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    if (maxp[dev] > 0 && bytes > 0) {
+        attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[na].val.accessPolicyWindow.base_ptr = base;
+        attr[na].val.accessPolicyWindow.num_bytes = bytes;
+        attr[na].val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)maxp[dev] / (float)bytes);
+        attr[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++na;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block, void** args, size_t smem,

@@ -1046,7 +1046,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
             // a pure pull from a small frontier reads it compacted (FView)
-            const bool compact = W == 1 && anypull && !anypush && P.fblk && nR_prev <= P.fcap;
+            const bool compact = W == 1 && anypull && !anypush && P.fblk && P.fcap && nR_prev <= P.fcap;
             FView fv{Fc, nullptr, nullptr};
             if (compact) {
                 build_compact<W, NB>(P, Rc, nR_prev, Fc, s_cnt, gtid, nthreads);
@@ -1218,6 +1218,10 @@ cudaError_t launch_w(Launch& L) {
     P.V = ws->lv;
     P.F0 = ws->lf[0];
     P.F1 = ws->lf[1];
+    // narrow words: both frontier arrays inside lf[0]'s allocation (n uint64
+    // words hold 8 / NB * ... of them), adjacent, so one L2 window covers them
+    const size_t fbytes = NB < 64 ? ((size_t)gr->dg.n * NB / 8 + 255) / 256 * 256 : 0;
+    if (NB < 64) P.F1 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws->lf[0]) + fbytes);
     P.touched = ws->touched;
     P.R0 = ws->rlog;
     P.R1 = ws->rlog + gr->dg.n;
@@ -1247,7 +1251,10 @@ cudaError_t launch_w(Launch& L) {
     P.fblk = W == 1 ? ws->fblk : nullptr;
     P.fcomp = ws->fcomp;
     P.fctot = ws->fctot;
-    P.fcap = gr->dg.n / 8;
+    // compact frontier reads (measured slower: two dependent L2 hits per edge
+    // cost more than one gather from the dense words) are opt-in
+    static const bool compact = std::getenv("MGK_COMPACT_FRONTIER") != nullptr;
+    P.fcap = compact ? gr->dg.n / 8 : 0;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1255,6 +1262,13 @@ cudaError_t launch_w(Launch& L) {
     L.block = kBlock;
     void* args[] = {&P};
     L.launches = 1;
+    static const bool persist = [] {
+        const char* v = std::getenv("MGK_L2_PERSIST");
+        return v && v[0] == '1';
+    }();
+    if (persist && NB < 64)
+        return launch_persistent_l2((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream, ws->lf[0],
+                                    2 * fbytes);
     return launch_persistent((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream);
 }
 
