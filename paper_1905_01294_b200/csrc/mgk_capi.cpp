@@ -398,7 +398,7 @@ cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, 
         return v && v[0] == '1';
     }();
     static std::mutex mu;
-    static int maxp[64] = {};
+    static int maxp[64] = {}, maxw[64] = {};
     static bool done[64] = {};
     int dev = 0;
     cudaGetDevice(&dev);
@@ -407,6 +407,7 @@ cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, 
         std::lock_guard<std::mutex> lk(mu);
         if (!done[dev]) {
             if (cudaDeviceGetAttribute(&maxp[dev], cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+                cudaDeviceGetAttribute(&maxw[dev], cudaDevAttrMaxAccessPolicyWindowSize, dev) != cudaSuccess ||
                 cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp[dev]) != cudaSuccess) {
                 cudaGetLastError();
                 maxp[dev] = 0;
@@ -421,7 +422,8 @@ cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, 
         attr[na].val.cooperative = 1;
         ++na;
     }
-    if (maxp[dev] > 0 && bytes > 0) {
+    if (maxp[dev] > 0 && maxw[dev] > 0 && bytes > 0) {
+        bytes = std::min(bytes, (size_t)maxw[dev]);  // the window's size is capped by the device
         attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
         attr[na].val.accessPolicyWindow.base_ptr = base;
         attr[na].val.accessPolicyWindow.num_bytes = bytes;

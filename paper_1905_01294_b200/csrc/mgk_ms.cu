@@ -1220,8 +1220,10 @@ cudaError_t launch_w(Launch& L) {
     P.F1 = ws->lf[1];
     // narrow words: both frontier arrays inside lf[0]'s allocation (n uint64
     // words hold 8 / NB * ... of them), adjacent, so one L2 window covers them
+    static const bool separate = std::getenv("MGK_F1_SEPARATE") != nullptr;  // A/B of the layout
     const size_t fbytes = NB < 64 ? ((size_t)gr->dg.n * NB / 8 + 255) / 256 * 256 : 0;
-    if (NB < 64) P.F1 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws->lf[0]) + fbytes);
+    if (NB < 64 && !separate)
+        P.F1 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws->lf[0]) + fbytes);
     P.touched = ws->touched;
     P.R0 = ws->rlog;
     P.R1 = ws->rlog + gr->dg.n;
@@ -1286,7 +1288,9 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
         ws->lv = ws->lf[0] = ws->lf[1] = ws->lane_cnt = ws->active = nullptr;
     }
     const DevGraph& g = gr->dg;
-    const size_t words = (size_t)g.n * W + 2;
+    // (+64 words: the narrow layout puts both frontier arrays, 256-B aligned,
+    // in lf[0], which must hold 2 round_up(2 n, 256) bytes even for tiny n)
+    const size_t words = (size_t)g.n * W + 66;
     for (unsigned long long** p : {&ws->lv, &ws->lf[0], &ws->lf[1]}) {
         if ((e = cudaMalloc(p, words * 8))) return e;
         if ((e = cudaMemset(*p, 0, words * 8))) return e;
