@@ -141,9 +141,6 @@ struct Workspace {
     unsigned long long* lane_cnt = nullptr;  // [(MGK_MAX_HOPS+1) * 64 * W]
     unsigned long long* active = nullptr;    // [2 * W]
     uint8_t* wact = nullptr;                  // [2][nwords] pull words left unsettled (by hop parity)
-    uint4* fblk = nullptr;                    // compact frontier records [n / 64 + 1] (zero between uses)
-    unsigned long long* fcomp = nullptr;      // compact frontier words [n / 8 + 64]
-    unsigned long long* fctot = nullptr;      // [8192] per-CTA member counts
     unsigned long long* lane_stat = nullptr;  // [3 * 512]: per-lane frontier out-edges (x2) and unexplored in-edges
     // shared small control block
     QCtl* qctl = nullptr;                    // [3]

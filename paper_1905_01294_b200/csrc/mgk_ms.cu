@@ -40,6 +40,14 @@ constexpr int kBlock = 512;
 #ifndef MGK_PRE
 #define MGK_PRE 8
 #endif
+// The phases are separate (non-inlined) functions: each gets its own register
+// allocation within the kernel's 64, so the pull's inner loops do not inherit
+// the spills of the finalize's per-lane bookkeeping
+#ifdef MGK_INLINE_PHASES
+#define MGK_PHASE __device__
+#else
+#define MGK_PHASE __device__ __noinline__
+#endif
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
 
@@ -79,10 +87,6 @@ struct MSParams {
     unsigned long long* lane_E;
     unsigned long long* lane_mu;
     uint8_t* wact;  // [2][nwords] by hop parity: words a pull left unsettled
-    uint4* fblk;                  // compact frontier: [n / 64 + 1] {bits lo, bits hi, rank, 0} (zero between uses)
-    unsigned long long* fcomp;    // packed words, up to fcap of them
-    unsigned long long* fctot;    // [grid] per-CTA member counts
-    uint32_t fcap;                // compact only when the frontier has <= fcap vertices
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -241,33 +245,6 @@ struct LS<1, 16> : LSNarrow<16> {};
 template <>
 struct LS<1, 8> : LSNarrow<8> {};
 
-// The frontier a pull reads. Dense: one word per vertex (F). Compact (one
-// word per vertex, small frontier): per 64-vertex block a record {membership
-// bits, rank of the block's first member} and the members' words packed in
-// rank order — ~10 MB for G4's hop-3 frontier instead of a 71 MB array, so the
-// per-edge gathers of the first dense pull hit L2 instead of DRAM.
-struct FView {
-    const unsigned long long* F;
-    const uint4* blk;                 // null: dense
-    const unsigned long long* comp;
-};
-
-template <int W, int NB>
-__device__ __forceinline__ LaneWord<W> fgather(const FView& fv, uint32_t v, unsigned long long pol) {
-    if constexpr (W == 1) {
-        if (fv.blk) {
-            const uint4 r = fv.blk[v >> 6];
-            const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
-            const uint32_t o = v & 63;
-            LaneWord<1> x;
-            x.w[0] = 0;
-            if ((bits >> o) & 1ull) x = LS<W, NB>::load(fv.comp, r.z + __popcll(bits & ((1ull << o) - 1ull)));
-            return x;
-        }
-    }
-    return LS<W, NB>::gather(fv.F, v, pol);
-}
-
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.items1 : P.items0;
 }
@@ -319,7 +296,7 @@ __device__ void block_flush(Acc& a, QCtl* q, QCtl* qf, LevelCounters* lc, LevelC
 
 // ---- push expand -----------------------------------------------------------------
 template <int W, int NB>
-__device__ void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
+MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
                            const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
                            QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
                            uint32_t nwarps, const LaneWord<W>& pushm) {
@@ -409,7 +386,7 @@ __device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>
 // Warp-wide: OR of the lane words of in-neighbours ri[b..e), stopping early
 // once `need` is covered. Returns the OR (all lanes) and the entries read.
 template <int W, int NB>
-__device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const FView& Fc,
+__device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
                                                        uint32_t b, uint32_t e, const LaneWord<W>& need,
                                                        uint32_t& scanned) {
     const uint32_t lane = lane_id();
@@ -425,7 +402,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
         const uint32_t pe = min(e, p0 + blk);
 #pragma unroll 2
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = fgather<W, NB>(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
+            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -454,7 +431,7 @@ struct ChunkGrab {
 };
 
 template <int W, int NB>
-__device__ void pull_phase(const MSParams& P, const FView& Fc, unsigned long long* Fn,
+MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
                            const uint8_t* wact_in, uint8_t* wact_out) {
@@ -517,7 +494,7 @@ __device__ void pull_phase(const MSParams& P, const FView& Fc, unsigned long lon
                 for (uint32_t q = 0; q < kStep; ++q) v[q] = ldg_hint(g.ri + p + q, pol_ri);
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
-                    const LaneWord<W> f = fgather<W, NB>(Fc, v[q], pol_f);
+                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
 #pragma unroll
                     for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 }
@@ -525,7 +502,7 @@ __device__ void pull_phase(const MSParams& P, const FView& Fc, unsigned long lon
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const LaneWord<W> f = fgather<W, NB>(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -691,7 +668,7 @@ __device__ void pull_phase(const MSParams& P, const FView& Fc, unsigned long lon
 
 // ---- finalize: V |= F', lane counts, next-hop items, clear old frontier -------
 template <int W, int NB>
-__device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR,
+MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR,
                                unsigned long long* Fn, bool mark_visited, bool touched_set, bool want_items,
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
@@ -831,7 +808,7 @@ __device__ void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t n
 // next-hop push items for the frontier vertices with a pushing lane (after the
 // per-lane direction decision)
 template <int W, int NB>
-__device__ void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
+MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
                            const LaneWord<W>& pushm, uint4* items_n, unsigned int* item_tail, Stage<kStageCap>& st,
                            uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
@@ -864,67 +841,6 @@ __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F,
 #pragma unroll
     for (int i = 0; i < W; ++i) z.w[i] = 0;
     for (uint32_t i = gtid; i < n; i += nthreads) LS<W, NB>::store(F, R[i], z);
-}
-
-// Compact frontier for the pull: membership bits of the nR frontier vertices
-// R, each 64-vertex block's rank (a grid-wide exclusive scan of the blocks'
-// popcounts), then each member's word packed at its rank. Three grid barriers.
-template <int W, int NB>
-__device__ void build_compact(const MSParams& P, const uint32_t* R, uint32_t nR, const unsigned long long* F,
-                              unsigned long long* s_scr, uint32_t gtid, uint32_t nthreads) {
-    const uint32_t nblk = (P.g.n + 63) / 64;
-    for (uint32_t i = gtid; i < nR; i += nthreads) {
-        const uint32_t u = R[i];
-        atomicOr(reinterpret_cast<unsigned long long*>(P.fblk + (u >> 6)), 1ull << (u & 63));
-    }
-    grid_barrier(P.bar);
-    // each CTA ranks a contiguous range of blocks, kBlock records per tile
-    const uint32_t per = (nblk + gridDim.x - 1) / gridDim.x;
-    const uint32_t lo = min(nblk, blockIdx.x * per), hi = min(nblk, lo + per);
-    __shared__ uint32_t s_wsum[kWarps];
-    uint32_t run = 0;  // members before this tile within the CTA's range
-    for (uint32_t t0 = lo; t0 < hi; t0 += kBlock) {
-        const uint32_t b = t0 + threadIdx.x;
-        uint32_t c = 0;
-        if (b < hi) {
-            const uint4 r = P.fblk[b];
-            c = __popc(r.x) + __popc(r.y);
-        }
-        const uint32_t incl = warp_incl_scan(c);
-        if (lane_id() == 31) s_wsum[threadIdx.x >> 5] = incl;
-        __syncthreads();
-        uint32_t before = 0, tot = 0;
-        for (uint32_t w = 0; w < kWarps; ++w) {
-            const uint32_t x = s_wsum[w];
-            before += w < (threadIdx.x >> 5) ? x : 0;
-            tot += x;
-        }
-        if (b < hi) P.fblk[b].z = run + before + incl - c;
-        run += tot;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) P.fctot[blockIdx.x] = run;
-    grid_barrier(P.bar);
-    // add the members of the CTAs before this one
-    if (threadIdx.x == 0) {
-        unsigned long long base = 0;
-        for (uint32_t c = 0; c < blockIdx.x; ++c) base += ld_cg(P.fctot + c);
-        s_scr[0] = base;
-    }
-    __syncthreads();
-    const uint32_t base = (uint32_t)s_scr[0];
-    __syncthreads();
-    if (base)
-        for (uint32_t b = lo + threadIdx.x; b < hi; b += kBlock) P.fblk[b].z += base;
-    grid_barrier(P.bar);
-    for (uint32_t i = gtid; i < nR; i += nthreads) {
-        const uint32_t u = R[i];
-        const uint4 r = P.fblk[u >> 6];
-        const unsigned long long bits = ((unsigned long long)r.y << 32) | r.x;
-        const uint32_t o = u & 63;
-        LS<W, NB>::store(P.fcomp, r.z + __popcll(bits & ((1ull << o) - 1ull)), LS<W, NB>::load(F, u));
-    }
-    grid_barrier(P.bar);
 }
 
 template <int W, int NB>
@@ -1045,16 +961,8 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
-            // a pure pull from a small frontier reads it compacted (FView)
-            const bool compact = W == 1 && anypull && !anypush && P.fblk && P.fcap && nR_prev <= P.fcap;
-            FView fv{Fc, nullptr, nullptr};
-            if (compact) {
-                build_compact<W, NB>(P, Rc, nR_prev, Fc, s_cnt, gtid, nthreads);
-                fv.blk = P.fblk;
-                fv.comp = P.fcomp;
-            }
             if (anypull)
-                pull_phase<W, NB>(P, fv, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
+                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
                                   (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
                                   P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
             prev_pull = anypull;
@@ -1076,9 +984,6 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
                               (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
-            if (compact)  // the records are zero between uses
-                for (uint32_t i = gtid; i < nR_prev; i += nthreads)
-                    reinterpret_cast<uint4*>(P.fblk)[Rc[i] >> 6] = make_uint4(0, 0, 0, 0);
             __syncthreads();
             if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
@@ -1250,13 +1155,6 @@ cudaError_t launch_w(Launch& L) {
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
     P.wact = ws->wact;
-    P.fblk = W == 1 ? ws->fblk : nullptr;
-    P.fcomp = ws->fcomp;
-    P.fctot = ws->fctot;
-    // compact frontier reads (measured slower: two dependent L2 hits per edge
-    // cost more than one gather from the dense words) are opt-in
-    static const bool compact = std::getenv("MGK_COMPACT_FRONTIER") != nullptr;
-    P.fcap = compact ? gr->dg.n / 8 : 0;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1299,14 +1197,6 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
     if (!ws->wact && (e = cudaMalloc(&ws->wact, 2 * ((size_t)g.nwords + 32)))) return e;
-    if (!ws->fblk) {  // compact frontier (W = 1 pulls): records zeroed once, kept zero between uses
-        const size_t nblk = ((size_t)g.n + 63) / 64 + 1;
-        if ((e = cudaMalloc(&ws->fblk, nblk * sizeof(uint4)))) return e;
-        if ((e = cudaMemset(ws->fblk, 0, nblk * sizeof(uint4)))) return e;
-        if ((e = cudaMalloc(&ws->fcomp, ((size_t)g.n / 8 + 64) * 8))) return e;
-        if ((e = cudaMalloc(&ws->fctot, 8192 * 8))) return e;
-        ws->bytes += nblk * sizeof(uint4) + ((size_t)g.n / 8 + 64) * 8 + 8192 * 8;
-    }
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;
