@@ -40,6 +40,10 @@ constexpr int kBlock = 512;
 #ifndef MGK_PRE
 #define MGK_PRE 8
 #endif
+#ifndef MGK_WPR_UNROLL  // warp-cooperative in-list scans: entries per lane in flight
+#define MGK_WPR_UNROLL 2
+#endif
+constexpr int kWprUnroll = MGK_WPR_UNROLL;
 // The phases are inlined into the kernel (separate non-inlined functions, each
 // with its own register allocation, measured 19 % slower on G4)
 #ifdef MGK_NOINLINE_PHASES
@@ -399,7 +403,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
     // first blocks
     for (uint32_t p0 = b, blk = 32; p0 < e; p0 += blk, blk = min(2 * blk, 256u)) {
         const uint32_t pe = min(e, p0 + blk);
-#pragma unroll 2
+#pragma unroll kWprUnroll
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
             const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
 #pragma unroll
