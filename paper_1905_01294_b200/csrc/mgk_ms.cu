@@ -35,7 +35,7 @@ constexpr int kBlock = 512;
 // scans per step of a short in-list, and entries of a longer list it scans
 // before the warp takes over
 #ifndef MGK_LIGHT_STEP
-#define MGK_LIGHT_STEP 2
+#define MGK_LIGHT_STEP 4
 #endif
 #ifndef MGK_PRE
 #define MGK_PRE 8
@@ -44,6 +44,18 @@ constexpr int kBlock = 512;
 #define MGK_WPR_UNROLL 2
 #endif
 constexpr int kWprUnroll = MGK_WPR_UNROLL;
+
+// a lane's own in-list (read a few entries at a time by the same lane: its
+// 32-byte sectors are re-read until the list is done, so by default they keep
+// normal L2 priority; MGK_RI_LIGHT_STREAM marks them evict-first too)
+__device__ __forceinline__ uint32_t ld_ri_lane(const uint32_t* p, unsigned long long pol) {
+#ifdef MGK_RI_LIGHT_STREAM
+    return dev::ldg_hint(p, pol);
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
 // The phases are inlined into the kernel (separate non-inlined functions, each
 // with its own register allocation, measured 19 % slower on G4)
 #ifdef MGK_NOINLINE_PHASES
@@ -494,7 +506,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             for (; p + kStep <= stop && !done; p += kStep) {
                 uint32_t v[kStep];
 #pragma unroll
-                for (uint32_t q = 0; q < kStep; ++q) v[q] = ldg_hint(g.ri + p + q, pol_ri);
+                for (uint32_t q = 0; q < kStep; ++q) v[q] = ld_ri_lane(g.ri + p + q, pol_ri);
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
                     const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
@@ -505,7 +517,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(g.ri + p, pol_ri), pol_f);
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ld_ri_lane(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
