@@ -165,8 +165,10 @@ int mgk_khop_count_ks(mgk_graph* g, const uint64_t* seeds, uint64_t nseeds, cons
  * NVLink / NVSwitch when the devices differ; a plain device copy otherwise):
  * load-time replication instead of re-uploading from the host.
  * mgk_khop_count_multi answers one batch over nreplicas replicas of the same
- * graph: the seeds are split into contiguous shards, one host thread and the
- * replica's own stream per shard, each writing a disjoint range of counts.
+ * graph: the seeds are split into shards — cost-balanced by out-degree
+ * (longest first) when the per-seed engine runs (k <= 2), contiguous for the
+ * lane engine — one host thread and the replica's own stream per shard, each
+ * writing disjoint entries of counts.
  * Same validation and messages as mgk_khop_count (checked once, in seed order,
  * before any device work). Replaces the "mgk_khop_count_multi_gpu" entry
  * SURVEY §8(b) lists; the reference has no multi-device path. */

@@ -951,16 +951,51 @@ int mgk_khop_count_multi(mgk_graph* const* replicas, int nreplicas, const uint64
     if (mode != MGK_EXACT && mode != MGK_CUMULATIVE) return fail(MGK_ECONTRACT, "unknown traverse mode %d", mode);
     int rc = check_query(&replicas[0]->g, seeds, nseeds, k);
     if (rc) return rc;
-    // contiguous shards, one host thread (and the replica's own stream) each;
-    // no collective: every shard writes a disjoint range of `counts`
+    // One host thread (and the replica's own stream) per shard; no collective:
+    // every shard writes disjoint entries of `counts`. Per-seed engines (k <= 2)
+    // get cost-balanced shards — a seed's work follows its out-degree and varies
+    // ~10x — by longest-first greedy on the degrees; the lane
+    // engine's 64-seed batches take contiguous shards.
     const Span span = span_of(k, mode);
     std::vector<int> rcs(nreplicas, MGK_OK);
     std::vector<std::string> errs(nreplicas);
+    std::vector<std::vector<uint64_t>> part(nreplicas);
+    const bool balance = nreplicas > 1 && k <= 2 && nseeds >= 2 * (uint64_t)nreplicas;
+    if (balance) {
+        std::vector<uint32_t> s32(nseeds), deg(nseeds);
+        for (uint64_t i = 0; i < nseeds; ++i) s32[i] = (uint32_t)seeds[i];
+        {
+            DeviceGuard dg(replicas[0]->g.device);
+            cudaError_t e = seed_degrees(&replicas[0]->g, s32.data(), nseeds, deg.data());
+            if (e) return fail_cuda(e, "seed degrees");
+        }
+        std::vector<uint64_t> order(nseeds);
+        for (uint64_t i = 0; i < nseeds; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](uint64_t x, uint64_t y) { return deg[x] > deg[y]; });
+        std::vector<uint64_t> load(nreplicas, 0);
+        for (uint64_t i : order) {
+            const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+            part[r].push_back(i);
+            load[r] += (uint64_t)deg[i] + 1;
+        }
+        for (auto& p : part) std::sort(p.begin(), p.end());
+    }
     auto run = [&](int i) {
-        const uint64_t a = nseeds * (uint64_t)i / nreplicas, b = nseeds * (uint64_t)(i + 1) / nreplicas;
-        if (b == a) return;
-        rcs[i] = count_impl(replicas[i], seeds + a, b - a, span, MGK_ENGINE_AUTO, counts + a, nullptr,
-                            "k-hop count");
+        if (balance) {
+            const auto& idx = part[i];
+            if (idx.empty()) return;
+            std::vector<uint64_t> s(idx.size()), c(idx.size());
+            for (size_t j = 0; j < idx.size(); ++j) s[j] = seeds[idx[j]];
+            rcs[i] = count_impl(replicas[i], s.data(), s.size(), span, MGK_ENGINE_AUTO, c.data(), nullptr,
+                                "k-hop count");
+            if (!rcs[i])
+                for (size_t j = 0; j < idx.size(); ++j) counts[idx[j]] = c[j];
+        } else {
+            const uint64_t a = nseeds * (uint64_t)i / nreplicas, b = nseeds * (uint64_t)(i + 1) / nreplicas;
+            if (b == a) return;
+            rcs[i] = count_impl(replicas[i], seeds + a, b - a, span, MGK_ENGINE_AUTO, counts + a, nullptr,
+                                "k-hop count");
+        }
         if (rcs[i]) errs[i] = t_err;
     };
     std::vector<std::thread> ts;

@@ -692,6 +692,45 @@ cudaError_t transpose_device_graph(const Graph* src, Graph* dst) {
     return e;
 }
 
+namespace {
+__global__ void gather_degrees(const uint32_t* rp, const uint32_t* perm, uint32_t n, const uint32_t* seeds,
+                               uint64_t ns, uint32_t* deg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ns; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = seeds[i];
+        if (s >= n) {
+            deg[i] = 0;
+            continue;
+        }
+        if (perm) s = perm[s];
+        deg[i] = rp[s + 1] - rp[s];
+    }
+}
+}  // namespace
+
+// out-degrees of (external) seed ids, for cost-balanced seed shards
+cudaError_t seed_degrees(const Graph* g, const uint32_t* h_seeds, uint64_t ns, uint32_t* h_deg) {
+    if (ns == 0) return cudaSuccess;
+    cudaStream_t s;
+    MGK_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint32_t *d_s = nullptr, *d_d = nullptr;
+    cudaError_t e = cudaSuccess;
+    do {
+        if ((e = cudaMallocAsync(&d_s, ns * 4, s))) break;
+        if ((e = cudaMallocAsync(&d_d, ns * 4, s))) break;
+        if ((e = cudaMemcpyAsync(d_s, h_seeds, ns * 4, cudaMemcpyHostToDevice, s))) break;
+        gather_degrees<<<(unsigned)std::min<uint64_t>((ns + 255) / 256, 4096), 256, 0, s>>>(g->dg.rp, g->dg.perm, g->dg.n,
+                                                                                          d_s, ns, d_d);
+        if ((e = cudaGetLastError())) break;
+        if ((e = cudaMemcpyAsync(h_deg, d_d, ns * 4, cudaMemcpyDeviceToHost, s))) break;
+        e = cudaStreamSynchronize(s);
+    } while (0);
+    cudaFreeAsync(d_s, s);
+    cudaFreeAsync(d_d, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return e;
+}
+
 // sort + unique (src << 32 | dst) keys, then CSR + CSC (keys/alt: m entries each, consumed)
 cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
                             cudaStream_t s) {

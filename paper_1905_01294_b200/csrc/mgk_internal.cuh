@@ -266,6 +266,7 @@ cudaError_t build_device_graph_generated(Graph* g, uint32_t scale, uint32_t edge
 void free_device_graph(Graph* g);
 cudaError_t replicate_device_graph(const Graph* src, Graph* dst);
 cudaError_t transpose_device_graph(const Graph* src, Graph* dst);
+cudaError_t seed_degrees(const Graph* g, const uint32_t* h_seeds, uint64_t ns, uint32_t* h_deg);
 // sort + unique (src << 32 | dst) keys into g (g->dg.n set; keys/alt hold m
 // entries each and are consumed); cudaErrorInvalidValue if >= 2^32 remain
 cudaError_t graph_from_keys(Graph* g, unsigned long long*& keys, unsigned long long*& alt, uint64_t m,
