@@ -389,7 +389,7 @@ cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, voi
 // persisting L2 set-aside is raised to its maximum once, and the window's hit
 // ratio is the share of the window that fits it.
 cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, void** args, cudaStream_t stream,
-                                 void* base, size_t bytes, size_t smem) {
+                                 void* base, size_t bytes) {
     static const bool noncoop = [] {
         const char* v = std::getenv("MGK_NONCOOP");
         return v && v[0] == '1';
@@ -432,7 +432,7 @@ cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, 
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = 0;
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = na;

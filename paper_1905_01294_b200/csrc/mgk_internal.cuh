@@ -232,7 +232,7 @@ cudaError_t launch_persistent(const void* fn, uint32_t grid, uint32_t block, voi
 cudaError_t launch_persistent_smem(const void* fn, uint32_t grid, uint32_t block, void** args, size_t smem,
                                    cudaStream_t stream);
 cudaError_t launch_persistent_l2(const void* fn, uint32_t grid, uint32_t block, void** args, cudaStream_t stream,
-                                 void* base, size_t bytes, size_t smem = 0);
+                                 void* base, size_t bytes);
 
 cudaError_t launch_single(Launch& L);
 // SINGLE, k = 2 counts with the visited sets in shared memory (mgk_k2.cu)

@@ -21,7 +21,6 @@
 // F' became non-zero) drives the finalize pass, the clearing of the previous
 // frontier and the final clearing of V.
 #include <cstdlib>
-#include <mutex>
 #include <type_traits>
 
 #include "mgk_device.cuh"
@@ -45,13 +44,6 @@ constexpr int kBlock = 512;
 #define MGK_WPR_UNROLL 2
 #endif
 constexpr int kWprUnroll = MGK_WPR_UNROLL;
-// a dense word's in-lists are copied into the warp's shared-memory stage
-// (coalesced) before its lanes scan them: the lanes' dependent chains then start
-// at a shared-memory read instead of a global one
-#ifndef MGK_RI_STAGE
-#define MGK_RI_STAGE 1024
-#endif
-constexpr uint32_t kRiStage = MGK_RI_STAGE;  // entries per warp (dynamic shared memory)
 
 // a lane's own in-list (read a few entries at a time by the same lane: its
 // 32-byte sectors are re-read until the list is done, so by default they keep
@@ -457,7 +449,7 @@ template <int W, int NB>
 MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
-                           const uint8_t* wact_in, uint8_t* wact_out, uint32_t* s_ri) {
+                           const uint8_t* wact_in, uint8_t* wact_out) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -506,28 +498,15 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
         // are settled there) and the warp takes the rest of an unsettled list
         constexpr uint32_t kPre = MGK_PRE;
         constexpr uint32_t kStep = MGK_LIGHT_STEP;
-        // stage [R0, R0 + slen): the span of the candidates' lane scans, up to
-        // kRiStage entries, when at least 8 lanes have a candidate
-        const uint32_t stop = cand ? (e - b <= 32 ? e : b + kPre) : 0;
-        uint32_t R0 = 0, slen = 0;
-        if (kRiStage > 0 && __popc(__ballot_sync(kFull, cand)) >= 8) {
-            R0 = __reduce_min_sync(kFull, cand ? b : 0xFFFFFFFFu);
-            slen = min(__reduce_max_sync(kFull, stop) - R0, kRiStage);
-#pragma unroll 8
-            for (uint32_t i = lane; i < slen; i += 32) s_ri[i] = ldg_hint(g.ri + R0 + i, pol_ri);
-            __syncwarp();
-        }
         bool settled = false;
         if (cand) {
+            const uint32_t stop = e - b <= 32 ? e : b + kPre;
             uint32_t p = b;
             bool done = false;
             for (; p + kStep <= stop && !done; p += kStep) {
                 uint32_t v[kStep];
 #pragma unroll
-                for (uint32_t q = 0; q < kStep; ++q) {
-                    const uint32_t x = p + q - R0;
-                    v[q] = x < slen ? s_ri[x] : ld_ri_lane(g.ri + p + q, pol_ri);
-                }
+                for (uint32_t q = 0; q < kStep; ++q) v[q] = ld_ri_lane(g.ri + p + q, pol_ri);
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
                     const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
@@ -538,8 +517,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const uint32_t x = p - R0;
-                const LaneWord<W> f = LS<W, NB>::gather(Fc, x < slen ? s_ri[x] : ld_ri_lane(g.ri + p, pol_ri), pol_f);
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ld_ri_lane(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -548,7 +526,6 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             settled = done || p >= e;
             b = p;  // where the warp continues an unsettled list
         }
-        __syncwarp();  // s_ri is rewritten by the next word
         unsigned mid = __ballot_sync(kFull, cand && !settled);
         while (mid) {
             const int j = __ffs(mid) - 1;
@@ -894,7 +871,6 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
     constexpr uint32_t LBs = W == 1 ? LB : 1;
     __shared__ unsigned long long s_E[LBs], s_mu[LBs];
     __shared__ uint32_t s_pm[2];
-    extern __shared__ uint32_t ms_dyn[];  // [kWarps][kRiStage]: the pull's in-list stage
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = gridDim.x * kBlock;
     const uint32_t warp_gid = gtid >> 5;
@@ -1003,8 +979,7 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (anypull)
                 pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
                                   (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
-                                  P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords,
-                                  ms_dyn + (threadIdx.x >> 5) * kRiStage);
+                                  P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
             prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
@@ -1131,29 +1106,16 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
 
 template <int W, int NB>
 cudaError_t launch_w(Launch& L) {
-    // per device (the shared-memory attribute is per context): the dynamic
-    // shared memory limit and the occupancy at it, looked up once under a mutex
-    static std::mutex mu;
-    static int blocks_per_sm_d[64] = {}, num_sms_d[64] = {};
-    constexpr size_t kDyn = (size_t)kWarps * kRiStage * 4;
+    static int blocks_per_sm = 0, num_sms = 0;
     cudaError_t e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dev &= 63;
-    int blocks_per_sm, num_sms;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (blocks_per_sm_d[dev] == 0) {
-            cudaDeviceGetAttribute(&num_sms_d[dev], cudaDevAttrMultiProcessorCount, dev);
-            if ((e = cudaFuncSetAttribute(ms_kernel<W, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDyn)))
-                return e;
-            int bps = 0;
-            if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, ms_kernel<W, NB>, kBlock, kDyn))) return e;
-            if (bps < 1) return cudaErrorInvalidConfiguration;
-            blocks_per_sm_d[dev] = bps;
-        }
-        blocks_per_sm = blocks_per_sm_d[dev];
-        num_sms = num_sms_d[dev];
+    if (blocks_per_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W, NB>, kBlock,
+                                                                0)))
+            return e;
+        if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
     }
     const Graph* gr = L.g;
     Workspace* ws = L.ws;
@@ -1221,8 +1183,8 @@ cudaError_t launch_w(Launch& L) {
     }();
     if (persist && NB < 64)
         return launch_persistent_l2((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream, ws->lf[0],
-                                    2 * fbytes, kDyn);
-    return launch_persistent_smem((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, kDyn, L.stream);
+                                    2 * fbytes);
+    return launch_persistent((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream);
 }
 
 }  // namespace
