@@ -1090,8 +1090,13 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
         }
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
-        if (clog_used <= P.clog_cap) {
+        if (clog_used <= P.clog_cap && clog_used * 8 <= g.n) {
             clear_list<W, NB>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
+            clear_list<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
+        } else if (clog_used <= P.clog_cap) {
+            // most vertices visited: stream zeros over V (coalesced) instead of
+            // one scattered store per visited vertex
+            for (size_t i = gtid; i < LS<W, NB>::words64(g.n); i += nthreads) P.V[i] = 0;
             clear_list<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
         } else {
             for (size_t i = gtid; i < LS<W, NB>::words64(g.n); i += nthreads) {
