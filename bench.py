@@ -740,8 +740,18 @@ def run_reference(args):
                                    f"steps capped by a {budget:.0f}s budget"},
         "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "prep": {"oracle_generator_s": gen_s, "from_parts_s": prep_s},
+        # evidence for the driver: this arm ran without the product library
+        "product_library_loaded": product_library_loaded(),
     }
     print(json.dumps(line), flush=True)
+
+
+def product_library_loaded() -> bool:
+    try:
+        with open("/proc/self/maps") as f:
+            return any("libmgk" in ln or "libmatgraph_b200" in ln for ln in f)
+    except OSError:
+        return False
 
 
 def relaunch_under_torchrun(args) -> int:
