@@ -129,7 +129,6 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->active);
     cudaFree(ws->lane_stat);
     cudaFree(ws->wact);
-    cudaFree(ws->fhash);
     cudaFree(ws->qctl);
     cudaFree(ws->misc);
     cudaFree(ws->lc);

@@ -141,8 +141,6 @@ struct Workspace {
     unsigned long long* lane_cnt = nullptr;  // [(MGK_MAX_HOPS+1) * 64 * W]
     unsigned long long* active = nullptr;    // [2 * W]
     uint8_t* wact = nullptr;                  // [2][nwords] pull words left unsettled (by hop parity)
-    unsigned long long* fhash = nullptr;      // hashed small frontier table (2^fhash_bits slots, empty = ~0)
-    uint32_t fhash_bits = 0;
     unsigned long long* lane_stat = nullptr;  // [3 * 512]: per-lane frontier out-edges (x2) and unexplored in-edges
     // shared small control block
     QCtl* qctl = nullptr;                    // [3]

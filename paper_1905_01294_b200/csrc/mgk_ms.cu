@@ -102,8 +102,6 @@ struct MSParams {
     unsigned long long* lane_E;
     unsigned long long* lane_mu;
     uint8_t* wact;  // [2][nwords] by hop parity: words a pull left unsettled
-    unsigned long long* fhash;  // hashed small frontier (narrow words), kHashEmpty between uses
-    uint32_t fhash_max_bits;    // table capacity 2^bits slots (0: off)
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -262,15 +260,6 @@ struct LS<1, 16> : LSNarrow<16> {};
 template <>
 struct LS<1, 8> : LSNarrow<8> {};
 
-// A small frontier as an open-addressing table (narrow words only): slot =
-// key << 32 | word, key 0xFFFFFFFF = empty, linear probing (four slots per
-// 32-byte sector, so a probe sequence rarely leaves its sector). At ~2 slots
-// per member the table is a third of the dense word array on G4's hop-3
-// frontier (32 MB vs 71 MB) and stays in L2, so a pull's per-edge gather is
-// one L2 hit instead of a DRAM miss half the time.
-constexpr unsigned long long kHashEmpty = ~0ull;
-__device__ __forceinline__ uint32_t fhash_slot(uint32_t v, uint32_t bits) { return (v * 0x9E3779B1u) >> (32 - bits); }
-
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.items1 : P.items0;
 }
@@ -411,35 +400,10 @@ __device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>
 
 // Warp-wide: OR of the lane words of in-neighbours ri[b..e), stopping early
 // once `need` is covered. Returns the OR (all lanes) and the entries read.
-template <int W, int NB, bool HASH>
-__device__ __forceinline__ LaneWord<W> fgather(const MSParams& P, const unsigned long long* Fc, uint32_t v,
-                                               unsigned long long pol, uint32_t bits) {
-    if constexpr (HASH) {
-        const uint32_t mask = (1u << bits) - 1u;
-        uint32_t h = fhash_slot(v, bits);
-        LaneWord<W> r;
-        r.w[0] = 0;
-        for (;;) {
-            const unsigned long long x = ld_hint_u64(P.fhash + h, pol);
-            const uint32_t key = (uint32_t)(x >> 32);
-            if (key == v) {
-                r.w[0] = x & 0xFFFFFFFFull;
-                break;
-            }
-            if (key == 0xFFFFFFFFu) break;
-            h = (h + 1) & mask;
-        }
-        return r;
-    } else {
-        (void)bits;
-        return LS<W, NB>::gather(Fc, v, pol);
-    }
-}
-
-template <int W, int NB, bool HASH>
+template <int W, int NB>
 __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
                                                        uint32_t b, uint32_t e, const LaneWord<W>& need,
-                                                       uint32_t& scanned, uint32_t hbits) {
+                                                       uint32_t& scanned) {
     const uint32_t lane = lane_id();
     const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     LaneWord<W> acc;
@@ -453,7 +417,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
         const uint32_t pe = min(e, p0 + blk);
 #pragma unroll kWprUnroll
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = fgather<W, NB, HASH>(P, Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f, hbits);
+            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -481,11 +445,11 @@ struct ChunkGrab {
     }
 };
 
-template <int W, int NB, bool HASH>
+template <int W, int NB>
 MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
-                           const uint8_t* wact_in, uint8_t* wact_out, uint32_t hbits) {
+                           const uint8_t* wact_in, uint8_t* wact_out) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -545,7 +509,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 for (uint32_t q = 0; q < kStep; ++q) v[q] = ld_ri_lane(g.ri + p + q, pol_ri);
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
-                    const LaneWord<W> f = fgather<W, NB, HASH>(P, Fc, v[q], pol_f, hbits);
+                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
 #pragma unroll
                     for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 }
@@ -553,7 +517,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const LaneWord<W> f = fgather<W, NB, HASH>(P, Fc, ld_ri_lane(g.ri + p, pol_ri), pol_f, hbits);
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ld_ri_lane(g.ri + p, pol_ri), pol_f);
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -570,8 +534,8 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
 #pragma unroll
             for (int i = 0; i < W; ++i) nj.w[i] = __shfl_sync(kFull, need.w[i] & ~acc_w.w[i], j);
             uint32_t sc = 0;
-            const LaneWord<W> aj = warp_pull_range<W, NB, HASH>(P, Fc, __shfl_sync(kFull, b, j),
-                                                      __shfl_sync(kFull, e, j), nj, sc, hbits);
+            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, __shfl_sync(kFull, b, j),
+                                                      __shfl_sync(kFull, e, j), nj, sc);
             if ((int)lane == j) {
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= aj.w[i];
@@ -681,7 +645,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             }
             const uint32_t e = min(yj + kHeavyChunk, __ldg(g.cp + uj + 1));
             uint32_t sc = 0;
-            const LaneWord<W> aj = warp_pull_range<W, NB, HASH>(P, Fc, yj, e, nj, sc, hbits);
+            const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, yj, e, nj, sc);
             if ((int)lane == j) {
                 acc.scanned += sc;
                 acc.candidates += ty == tb;
@@ -1012,36 +976,10 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
-            // a pure pull from a small frontier gathers from it hashed (narrow words)
-            uint32_t hbits = 0;
-            if constexpr (NB < 64) {
-                if (anypull && !anypush && P.fhash_max_bits) {
-                    hbits = 16;
-                    while (hbits < P.fhash_max_bits && (1ull << hbits) < 2ull * nR_prev) ++hbits;
-                    if ((1ull << hbits) < 2ull * nR_prev) hbits = 0;  // too big a frontier: dense
-                }
-                if (hbits) {
-                    const uint32_t mask = (1u << hbits) - 1u;
-                    for (uint32_t i = gtid; i < nR_prev; i += nthreads) {
-                        const uint32_t u = Rc[i];
-                        const unsigned long long x =
-                            ((unsigned long long)u << 32) | (unsigned long long)LS<W, NB>::load(Fc, u).w[0];
-                        uint32_t h = fhash_slot(u, hbits);
-                        while (atomicCAS(P.fhash + h, kHashEmpty, x) != kHashEmpty) h = (h + 1) & mask;
-                    }
-                    grid_barrier(P.bar);
-                }
-            }
-            const auto wact_in = (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr;
-            const auto wact_out = P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords;
-            if (anypull) {
-                if (hbits)
-                    pull_phase<W, NB, true>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush, wact_in,
-                                            wact_out, hbits);
-                else
-                    pull_phase<W, NB, false>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush, wact_in,
-                                             wact_out, 0);
-            }
+            if (anypull)
+                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
+                                  (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
+                                  P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
             prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
@@ -1061,8 +999,6 @@ __global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
                               (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
-            if (hbits)  // the table is empty between uses
-                for (uint32_t i = gtid; i < (1u << hbits); i += nthreads) P.fhash[i] = kHashEmpty;
             __syncthreads();
             if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
                 atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
@@ -1239,9 +1175,6 @@ cudaError_t launch_w(Launch& L) {
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
     P.wact = ws->wact;
-    static const bool nohash = std::getenv("MGK_NO_FRONTIER_HASH") != nullptr;
-    P.fhash = ws->fhash;
-    P.fhash_max_bits = (NB < 64 && !nohash) ? ws->fhash_bits : 0;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1284,14 +1217,6 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
     if (!ws->wact && (e = cudaMalloc(&ws->wact, 2 * ((size_t)g.nwords + 32)))) return e;
-    if (!ws->fhash) {  // hashed small frontiers: up to 2^bits >= n / 4 slots (<= n / 8 members), all empty
-        uint32_t bits = 16;
-        while (bits < 30 && (1ull << bits) < (uint64_t)g.n / 4) ++bits;
-        if ((e = cudaMalloc(&ws->fhash, (size_t)8 << bits))) return e;
-        if ((e = cudaMemset(ws->fhash, 0xFF, (size_t)8 << bits))) return e;
-        ws->fhash_bits = bits;
-        ws->bytes += (size_t)8 << bits;
-    }
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;
