@@ -30,7 +30,13 @@ namespace {
 
 using namespace dev;
 
-constexpr int kBlock = 512;
+#ifndef MGK_MS_BLOCK
+#define MGK_MS_BLOCK 256
+#endif
+#ifndef MGK_MS_MINB  // resident CTAs per SM the register budget is sized for (0: compiler's choice)
+#define MGK_MS_MINB 0
+#endif
+constexpr int kBlock = MGK_MS_BLOCK;
 // pull tuning (compile-time; variants are built for A/B runs): entries a lane
 // scans per step of a short in-list, and entries of a longer list it scans
 // before the warp takes over
@@ -858,8 +864,16 @@ __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F,
     for (uint32_t i = gtid; i < n; i += nthreads) LS<W, NB>::store(F, R[i], z);
 }
 
+// resident CTAs per SM the register budget is sized for, per instance: one
+// word per vertex runs best at 48 registers and 40 warps per SM (more warps to
+// hide the gathers' latency), wide words keep their registers
+template <int W>
+constexpr int ms_min_blocks() {
+    return MGK_MS_MINB > 0 ? MGK_MS_MINB : (W == 1 ? 5 * 256 / kBlock : 512 / kBlock);
+}
+
 template <int W, int NB>
-__global__ void __launch_bounds__(kBlock) ms_kernel(MSParams P) {
+__global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams P) {
     grid_barrier_init(P.bar);
     // qctl[parity] fields in this engine:
     //   nitems = |R| (discovery list tail), nfound = push items built for the
