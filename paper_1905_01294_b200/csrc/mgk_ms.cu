@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
 #pragma unroll
         for (int i = 0; i < W; ++i) pullm.w[i] = P.force_dir == 2 ? ~0ull : 0ull;
         const bool pull0 = P.force_dir == 2;
-        if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+        for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;  // (LB may exceed the block)
         if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
         __syncthreads();
         finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull0, P.items0, &P.qctl[0].nfound, false,
@@ -1005,7 +1005,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             const bool last = hop == P.k || nR == 0;
             const bool count_lanes = hop >= P.min_hop || P.perlane;
             // ---- finalize -------------------------------------------------------------
-            if (threadIdx.x < LB) s_cnt[threadIdx.x] = 0;
+            for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;
             if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
@@ -1014,8 +1014,9 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
                               (P.perlane && !last) ? s_E : nullptr, s_mu);
             clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
             __syncthreads();
-            if (count_lanes && threadIdx.x < LB && s_cnt[threadIdx.x])
-                atomicAdd(&P.lane_cnt[hop * LB + threadIdx.x], s_cnt[threadIdx.x]);
+            if (count_lanes)
+                for (uint32_t t = threadIdx.x; t < LB; t += kBlock)
+                    if (s_cnt[t]) atomicAdd(&P.lane_cnt[hop * LB + t], s_cnt[t]);
             if (P.perlane && threadIdx.x < LB) {
                 if (s_E[threadIdx.x]) atomicAdd(&P.lane_E[nxt * LB + threadIdx.x], s_E[threadIdx.x]);
                 if (s_mu[threadIdx.x]) atomicAdd(&P.lane_mu[threadIdx.x], 0ull - s_mu[threadIdx.x]);
