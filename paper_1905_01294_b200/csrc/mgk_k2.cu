@@ -101,7 +101,6 @@ struct K2Params {
     // from their slice's queue (q[r], zero between launches), seeds with at
     // least the mean work first
     uint32_t dyn;
-    uint32_t nobig;  // MGK_K2_NOBIG=1: one pass in index order (experiments)
     unsigned long long* q;  // [kK2MaxR]
     uint32_t inline_seeds[kK2Inline];
 };
@@ -354,7 +353,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     if (P.dyn) {
         // the mean hop-2 work of the seeds with any (a few thousand seeds at most
         // are summed by every CTA; larger batches take one pass in index order)
-        if (P.ns <= 4096 && !P.nobig) {
+        if (P.ns <= 4096) {
             unsigned long long sum = 0, cnt = 0;
             for (uint64_t i = threadIdx.x; i < P.ns; i += kK2Block) {
                 const unsigned long long v = ld_cg(P.w + i);
@@ -1096,8 +1095,6 @@ cudaError_t launch_k2(Launch& L) {
     // dynamic per-slice seed queues (default) or the static work line (MGK_K2_STATIC=1)
     static const uint32_t stat = std::getenv("MGK_K2_STATIC") != nullptr ? 1u : 0u;
     Q.dyn = stat ? 0u : 1u;
-    static const uint32_t nobig = std::getenv("MGK_K2_NOBIG") != nullptr ? 1u : 0u;
-    Q.nobig = nobig;
     Q.q = ws->k2_misc + 16;
     if (L.host_io && ns <= kK2Inline) {
         Q.seeds = nullptr;
