@@ -97,11 +97,6 @@ struct K2Params {
     unsigned long long seedcost;  // work-line units charged per seed (its fixed cost)
     uint32_t snapdiv;
     uint32_t diag;  // MGK_K2_DIAG=1: phase timings in level 0 of the stats  // group boundaries within (group size / snapdiv) of a seed edge move to it
-    // dynamic mode: no work line; the CTAs holding slice r take whole seeds
-    // from their slice's queue (q[r], zero between launches), seeds with at
-    // least the mean work first
-    uint32_t dyn;
-    unsigned long long* q;  // [kK2MaxR]
     uint32_t inline_seeds[kK2Inline];
 };
 
@@ -184,23 +179,6 @@ __global__ void k2_split_kernel(DevGraph g, uint32_t R, uint32_t rbits, uint32_t
             }
             out[(size_t)v * (R - 1) + r - 1] = lo;
         }
-    }
-}
-
-// Dynamic mode: the next seed for slice r's CTAs (thread 0 calls it). Queue
-// positions [0, ns) visit the seeds with w >= big, [ns, 2 ns) the others
-// (big = 0: one pass over all); seeds without hop-2 entries are skipped.
-__device__ uint64_t k2_grab(const K2Params& P, uint32_t r, unsigned long long big) {
-    const uint64_t ns = P.ns, end = big ? 2 * ns : ns;
-    for (;;) {
-        const unsigned long long j = atomicAdd(P.q + r, 1ull);
-        if (j >= end) return ~0ull;
-        const bool second = j >= ns;
-        const uint64_t i = second ? j - ns : j;
-        const unsigned long long w = ld_cg(P.w + i);
-        if (w == 0) continue;
-        if (big && (w >= big) == second) continue;  // the other pass takes it
-        return i;
     }
 }
 
@@ -349,28 +327,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     // the merge (read after the next grid barrier)
     const uint32_t G = P.ngroups, R = P.R;
     const uint32_t grp = blockIdx.x / R, rr = blockIdx.x % R;
-    unsigned long long W = 0, big = 0;
-    if (P.dyn) {
-        // the mean hop-2 work of the seeds with any (a few thousand seeds at most
-        // are summed by every CTA; larger batches take one pass in index order)
-        if (P.ns <= 4096) {
-            unsigned long long sum = 0, cnt = 0;
-            for (uint64_t i = threadIdx.x; i < P.ns; i += kK2Block) {
-                const unsigned long long v = ld_cg(P.w + i);
-                sum += v;
-                cnt += v != 0;
-            }
-            unsigned long long dummy;
-            const unsigned long long tsum = block_excl_scan(sum, &dummy, s_warp);
-            const unsigned long long tcnt = block_excl_scan(cnt, &dummy, s_warp);
-            big = tcnt ? (tsum + tcnt - 1) / tcnt : 0;
-        }
-        W = 1;
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            P.misc[4] = 0;  // no cut seeds
-            P.misc[0] = globaltimer();
-        }
-    } else {
+    unsigned long long W;
+    {
         unsigned long long* s_b = s_misc;  // [0] group start, [1] group end, [2] first seed, [3] its ws
         unsigned int* s_ncut = reinterpret_cast<unsigned int*>(s_misc + 4);
         const uint64_t per = (P.ns + kK2Block - 1) / kK2Block;
@@ -446,43 +404,25 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             P.misc[4] = *s_ncut;
             P.misc[0] = globaltimer();
         }
-    }  // static work line
+    }
 
     // ---- phase 2: group slices of the work line -----------------------------------
     const uint32_t rlo = rr * P.rbits;
-    const bool dyn = P.dyn != 0;
-    const unsigned long long glo = dyn ? 0 : (W ? s_misc[0] : 0), ghi = dyn ? ~0ull : (W ? s_misc[1] : 0);
-    unsigned long long wnext = dyn ? 0 : s_misc[3];  // work-line start of the first seed (static)
-    // seed records {sinfo, w, f1win} prefetched into slot rec_slot, and the
+    const unsigned long long glo = W ? s_misc[0] : 0, ghi = W ? s_misc[1] : 0;
+    const uint64_t ifirst = s_misc[2];
+    unsigned long long wnext = s_misc[3];  // work-line start of seed ifirst
+    // seed records {sinfo, w, f1win} prefetched into slots (i & 1), and the
     // next seed's first window staged during this seed's sweep
     unsigned long long* s_rec = s_misc + 8;  // [2][4]
-    volatile unsigned long long* s_grab = s_misc + 16;
-    uint64_t rec_i = ~0ull;                  // seed whose record is in slot rec_slot
-    uint32_t rec_slot = 0;
+    uint64_t rec_i = ~0ull;                  // seed whose record is in slot rec_i & 1
     bool staged = false;                     // seed rec_i's first window is in stg
-    uint64_t i = 0;
-    if (dyn) {  // the first seed of this CTA's slice queue
-        if (threadIdx.x == 0) *s_grab = blockIdx.x < G * R ? k2_grab(P, rr, big) : ~0ull;
-        __syncthreads();
-        i = *s_grab;
-        __syncthreads();
-    } else {
-        i = s_misc[2];
-    }
     if (glo < ghi) {
-        while (dyn ? i != ~0ull : i < P.ns) {
-            uint64_t nxt = i + 1;
-            if (dyn) {  // grabbed one ahead, so its record can be prefetched
-                if (threadIdx.x == 0) *s_grab = k2_grab(P, rr, big);
-                __syncthreads();
-                nxt = *s_grab;
-                __syncthreads();
-            }
+        for (uint64_t i = ifirst; i < P.ns; ++i) {
             unsigned long long v0;
             uint4 si;
             uint32_t ow;
             if (i == rec_i) {
-                const unsigned long long* r = s_rec + rec_slot * 4;
+                const unsigned long long* r = s_rec + (i & 1) * 4;
                 const uint2 x0 = *reinterpret_cast<const uint2*>(r), x1 = *reinterpret_cast<const uint2*>(r + 1);
                 si = make_uint4(x0.x, x0.y, x1.x, x1.y);
                 v0 = r[2];
@@ -495,24 +435,20 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             }
             const unsigned long long ws = wnext, we = ws + (v0 ? v0 + P.seedcost : 0);
             wnext = we;
-            if (!dyn && ws >= ghi) break;
-            if (we == ws) {
-                i = nxt;
-                continue;
-            }
-            const bool have_next = dyn ? nxt != ~0ull : (nxt < P.ns && we < ghi);
+            if (ws >= ghi) break;
+            if (we == ws) continue;
+            const bool have_next = i + 1 < P.ns && we < ghi;
             if (have_next && threadIdx.x == 0) {  // the next record, into the other slot
-                const uint32_t d = (uint32_t)__cvta_generic_to_shared(s_rec + (rec_slot ^ 1) * 4);
-                cp_async8(d, P.sinfo + nxt);
-                cp_async8(d + 8, reinterpret_cast<const char*>(P.sinfo + nxt) + 8);
-                cp_async8(d + 16, P.w + nxt);
-                cp_async4(d + 24, P.f1win + nxt);
+                const uint32_t d = (uint32_t)__cvta_generic_to_shared(s_rec + ((i + 1) & 1) * 4);
+                cp_async8(d, P.sinfo + i + 1);
+                cp_async8(d + 8, reinterpret_cast<const char*>(P.sinfo + i + 1) + 8);
+                cp_async8(d + 16, P.w + i + 1);
+                cp_async4(d + 24, P.f1win + i + 1);
                 cp_async_commit();
             }
             // this group's part of the seed: on the work line, then in adjacency
-            // entries (the first seedcost units of a seed carry no entries); a
-            // dynamic CTA takes whole seeds
-            const unsigned long long a2 = dyn ? 0 : max(glo, ws) - ws, z2 = dyn ? v0 + P.seedcost : min(ghi, we) - ws;
+            // entries (the first seedcost units of a seed carry no entries)
+            const unsigned long long a2 = max(glo, ws) - ws, z2 = min(ghi, we) - ws;
             const unsigned long long a = a2 > P.seedcost ? a2 - P.seedcost : 0;
             const unsigned long long z = z2 > P.seedcost ? z2 - P.seedcost : 0;
             const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
@@ -693,7 +629,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             // this group: its work-line start is this seed's end)
             staged = false;
             if (have_next) {
-                const unsigned long long* r = s_rec + (rec_slot ^ 1) * 4;
+                const unsigned long long* r = s_rec + ((i + 1) & 1) * 4;
                 const uint2 x1 = *reinterpret_cast<const uint2*>(r + 1);
                 const uint32_t noff = x1.y, ndeg = x1.x;
                 if (r[2] != 0 && noff != kNoF1 && P.R <= 2 && ndeg <= kK2Stg) {
@@ -712,11 +648,10 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                     cp_async_commit();
                     staged = true;
                 }
-                rec_i = nxt;
-                rec_slot ^= 1;
+                rec_i = i + 1;
             }
             // the slice is complete: popcount it (whole seed) or stage it (cut seed)
-            const bool whole = dyn || (ws >= glo && we <= ghi);
+            const bool whole = ws >= glo && we <= ghi;
             uint4* bm4 = reinterpret_cast<uint4*>(bm);
             const uint32_t n4 = P.rwords / 4;
             if (whole) {
@@ -741,7 +676,6 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                 }
             }
             __syncthreads();
-            i = nxt;
         }
     }
     grid_barrier(P.bar);
@@ -787,7 +721,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             if (lane == 0 && pc) atomicAdd(&P.acc[i], (unsigned long long)pc);
         }
     }
-    if (!P.dyn) grid_barrier(P.bar);  // (dynamic mode: no cut seeds)
+    grid_barrier(P.bar);
     if (gtid == 0) P.misc[2] = globaltimer();
 
     // ---- phase 4: answers and the per-hop counters ---------------------------------
@@ -828,8 +762,6 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
     if (gtid == 0) {
         P.lc[1].runs = (unsigned)P.ns;
         P.misc[5] = P.misc[6] = P.misc[7] = 0;  // allocators (every CTA is past phase 2)
-        if (P.dyn)
-            for (uint32_t r = 0; r < P.R; ++r) P.q[r] = 0;
         const unsigned long long now = globaltimer();
         P.lc[0].ns = ld_cg(&P.misc[0]) - t0;                  // phases 0-1
         P.lc[2].ns = ld_cg(&P.misc[2]) - ld_cg(&P.misc[0]);  // slices + merge
@@ -1037,9 +969,9 @@ cudaError_t launch_k2(Launch& L) {
         if ((e = cudaMalloc(&ws->k2_cuts, (size_t)G * 16))) return e;
         ws->k2_groups = G;
     }
-    if (!ws->k2_misc) {  // [16] counters and timestamps + [kK2MaxR] slice queues
-        if ((e = cudaMalloc(&ws->k2_misc, (16 + kK2MaxR) * 8))) return e;
-        if ((e = cudaMemset(ws->k2_misc, 0, (16 + kK2MaxR) * 8))) return e;
+    if (!ws->k2_misc) {
+        if ((e = cudaMalloc(&ws->k2_misc, 128))) return e;
+        if ((e = cudaMemset(ws->k2_misc, 0, 128))) return e;
         if ((e = cudaStreamSynchronize(0))) return e;
     }
     K2Params Q;  // ~2 KB with the inline seeds; the launch copies it
@@ -1092,10 +1024,6 @@ cudaError_t launch_k2(Launch& L) {
     Q.snapdiv = (uint32_t)snapdiv;
     static const uint32_t diag = std::getenv("MGK_K2_DIAG") != nullptr ? 1u : 0u;
     Q.diag = diag;
-    // dynamic per-slice seed queues (default) or the static work line (MGK_K2_STATIC=1)
-    static const uint32_t stat = std::getenv("MGK_K2_STATIC") != nullptr ? 1u : 0u;
-    Q.dyn = stat ? 0u : 1u;
-    Q.q = ws->k2_misc + 16;
     if (L.host_io && ns <= kK2Inline) {
         Q.seeds = nullptr;
         std::memcpy(Q.inline_seeds, L.h_seeds, (size_t)ns * 4);
