@@ -1,5 +1,6 @@
-"""Timing breakdown of the cfg2 k=2 call (G2, 300 seeds): kernel ms, setup
-(phases 0-1), slices (phase 2), slices + merge, answers; min over 10 calls."""
+"""Timing breakdown of the on-chip k=2 call (G2 = cfg2 by default, or G4): kernel
+us, setup (phases 0-1), slices (phase 2), slices + merge, answers; min over 10
+calls. usage: k2probe.py [nseeds] [G2|G4]"""
 import os
 import sys
 from pathlib import Path
@@ -9,8 +10,8 @@ os.environ.setdefault("MGK_K2_DIAG", "1")  # phase timings in level 0 of the sta
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1905_01294_b200 import DeviceGraph, harness as H, k_hop_count_batch  # noqa: E402
 
-rp, ci = H.gen_csr(H.G2)
-g = DeviceGraph.from_csr(rp, ci)
+g = DeviceGraph.generate(H.SPECS[sys.argv[2] if len(sys.argv) > 2 else "G2"])
+rp, _ = g.csr()
 seeds = H.pick_seeds(rp, int(sys.argv[1]) if len(sys.argv) > 1 else 300, 1)
 rows = []
 for _ in range(12):
