@@ -164,14 +164,6 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void smem_or(uint32_t base, uint32_t word, uint32_t bit) {
     asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(base + word * 4), "r"(bit));
 }
-// the same with the old word returned: 1 when the bit is new (the slice's
-// members are counted as they arrive, so a whole seed's slice needs no
-// popcount sweep — it is only zeroed, with stores)
-__device__ __forceinline__ uint32_t smem_or_new(uint32_t base, uint32_t word, uint32_t bit) {
-    uint32_t old;
-    asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(base + word * 4), "r"(bit));
-    return (old & bit) ? 0u : 1u;
-}
 
 // Where each row crosses the slice boundaries r * rbits (rows ascend): the
 // CTA holding slice r streams only [split r-1, split r) of every F1 row.
@@ -461,9 +453,8 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             const unsigned long long z = z2 > P.seedcost ? z2 - P.seedcost : 0;
             const uint32_t s = si.x, b = si.y, deg = si.z, off = si.w;
             const bool v1 = a2 == 0;  // the part holding offset 0 also holds {s} u F1
-            uint32_t nb = 0;          // bits this thread set first in the seed's slice
             if (v1 && !P.walk && threadIdx.x == 0 && s - rlo < P.rbits)
-                nb += smem_or_new(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
+                smem_or(bm_base, (s - rlo) >> 5, 1u << ((s - rlo) & 31));
             unsigned long long wbase = 0;  // seed-local entry offset of the current window
             uint32_t j0 = 0;
             if (staged) cp_async_wait_all();  // this thread's staged rows
@@ -516,7 +507,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
                         }
                         sr2[h] = min(lo, d2[h]);
                         lr2[h] = min(hi, d2[h]) - sr2[h];
-                        if (v1 && v - rlo < P.rbits) nb += smem_or_new(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
+                        if (v1 && v - rlo < P.rbits) smem_or(bm_base, (v - rlo) >> 5, 1u << ((v - rlo) & 31));
                     }
                 }
                 // one scan of (whole << 32 | slice): both prefixes (a window's
@@ -597,7 +588,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 #pragma unroll
                             for (int q = 0; q < kK2Ilp; ++q) {
                                 const uint32_t t = u[q] - rlo;
-                                if (t < P.rbits) nb += smem_or_new(bm_base, t >> 5, 1u << (t & 31));
+                                if (t < P.rbits) smem_or(bm_base, t >> 5, 1u << (t & 31));
                             }
                         }
                         if (xb < xe) {  // tail (< 32 * kK2Ilp entries): one masked block
@@ -619,7 +610,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
 #pragma unroll
                             for (int q = 0; q < kK2Ilp; ++q) {
                                 const uint32_t t = u[q] - rlo;
-                                if (((valid >> q) & 1u) && t < P.rbits) nb += smem_or_new(bm_base, t >> 5, 1u << (t & 31));
+                                if (((valid >> q) & 1u) && t < P.rbits) smem_or(bm_base, t >> 5, 1u << (t & 31));
                             }
                         }
                     }
@@ -630,7 +621,7 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             if (v1)  // F1 rows in windows the loop did not reach
                 for (uint32_t j = j0 + threadIdx.x; j < deg; j += kK2Block) {
                     const uint32_t v = (off != kNoF1 ? ld_cg(P.f1v + off + j) : __ldg(g.ci + b + j)) - rlo;
-                    if (v < P.rbits) nb += smem_or_new(bm_base, v >> 5, 1u << (v & 31));
+                    if (v < P.rbits) smem_or(bm_base, v >> 5, 1u << (v & 31));
                 }
             if (have_next && threadIdx.x == 0) cp_async_wait_all();  // the next record
             __syncthreads();
@@ -664,12 +655,17 @@ __global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
             uint4* bm4 = reinterpret_cast<uint4*>(bm);
             const uint32_t n4 = P.rwords / 4;
             if (whole) {
-                uint32_t pc = nb;
+                uint32_t pc = 0;
+#pragma unroll 4
+                for (uint32_t q = threadIdx.x; q < n4; q += kK2Block) {
+                    const uint4 x = bm4[q];
+                    const uint32_t c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+                    pc += c;
+                    if (c) bm4[q] = make_uint4(0, 0, 0, 0);
+                }
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) pc += __shfl_xor_sync(kFull, pc, d);
                 if (lane == 0 && pc) atomicAdd(&P.acc[i], (unsigned long long)pc);
-#pragma unroll 4
-                for (uint32_t q = threadIdx.x; q < n4; q += kK2Block) bm4[q] = make_uint4(0, 0, 0, 0);
             } else {
                 const uint32_t slot = ws < glo ? 0 : 1;
                 uint4* dst = reinterpret_cast<uint4*>(P.stage + ((size_t)(grp * 2 + slot) * R + rr) * P.rwords);
