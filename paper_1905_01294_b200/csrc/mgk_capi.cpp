@@ -128,7 +128,7 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     cudaFree(ws->lane_cnt);
     cudaFree(ws->active);
     cudaFree(ws->lane_stat);
-    cudaFree(ws->wact);
+    cudaFree(ws->umask);
     cudaFree(ws->qctl);
     cudaFree(ws->misc);
     cudaFree(ws->lc);

@@ -105,6 +105,25 @@ __global__ void heavy_fill(uint32_t n, const uint32_t* off, unsigned long long* 
     }
 }
 
+// hub_end[u]: first position of u's in-list (descending source out-degree)
+// whose source has out-degree < D (binary search)
+__global__ void hub_end_kernel(const uint32_t* cp, const uint32_t* ri, const uint32_t* rp, uint32_t n, uint32_t D,
+                               uint32_t* hub_end) {
+    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t lo = cp[u], hi = cp[u + 1];
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            const uint32_t v = ri[mid];
+            if (rp[v + 1] - rp[v] >= D)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        hub_end[u] = lo;
+    }
+}
+
 __global__ void heavy_tasks(const unsigned long long* keys, uint64_t nt, const uint32_t* cp, uint2* tasks) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t u = (uint32_t)keys[t], i = (uint32_t)(keys[t] >> 32);
@@ -137,8 +156,9 @@ __global__ void swap_halves(unsigned long long* keys, uint64_t m) {
     }
 }
 
-// ((~indeg) << 32 | v): ascending order = descending in-degree, ties by id
-__global__ void indeg_keys(const uint32_t* cp, uint32_t n, unsigned long long* keys) {
+// ((~deg) << 32 | v): ascending order = descending degree, ties by id (cp:
+// in-degree from the CSC, or rp: out-degree from the CSR)
+__global__ void deg_keys(const uint32_t* cp, uint32_t n, unsigned long long* keys) {
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < n;
          v += (uint64_t)gridDim.x * blockDim.x)
         keys[v] = ((unsigned long long)(0xFFFFFFFFu - (cp[v + 1] - cp[v])) << 32) | v;
@@ -188,6 +208,7 @@ cudaError_t radix_sort_keys(unsigned long long*& keys, unsigned long long*& alt,
 }
 
 cudaError_t build_heavy(Graph* g, cudaStream_t s);
+cudaError_t build_hub_end(Graph* g, cudaStream_t s);
 
 // (col << 32 | row) sorted keys -> (col << 32 | ~outdeg(row)) keys + row values
 __global__ void make_deg_keys(unsigned long long* keys, uint32_t* vals, uint64_t m,
@@ -297,7 +318,30 @@ cudaError_t build_heavy(Graph* g, cudaStream_t s) {
     }
     MGK_TRY(cudaFreeAsync(cnt, s));
     MGK_TRY(cudaFreeAsync(d_total, s));
-    return cudaSuccess;
+    return build_hub_end(g, s);
+}
+
+// LANES split pull (opt-in, MGK_HUB_DEG=D): the out-degree threshold and
+// every vertex's hub-prefix end
+uint32_t hub_deg_default() {
+    static const uint32_t d = [] {
+        const char* e = std::getenv("MGK_HUB_DEG");
+        return e ? (uint32_t)std::atoi(e) : 0u;
+    }();
+    return d;
+}
+
+cudaError_t build_hub_end(Graph* g, cudaStream_t s) {
+    const uint32_t n = g->dg.n;
+    if (hub_deg_default() == 0) return cudaSuccess;
+    if (!g->hub_end) {
+        MGK_TRY(cudaMalloc(&g->hub_end, (size_t)(n + 1) * 4));
+        g->bytes += (size_t)(n + 1) * 4;
+    }
+    g->dg.hub_end = g->hub_end;
+    g->dg.hub_deg = hub_deg_default();
+    hub_end_kernel<<<blocks_for(n), kTB, 0, s>>>(g->cp, g->ri, g->rp, n, std::max(g->dg.hub_deg, 1u), g->hub_end);
+    return cudaGetLastError();
 }
 
 cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
@@ -376,7 +420,8 @@ cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
     const uint32_t n = g->dg.n;
     const uint64_t m = g->dg.m;
     const char* on = std::getenv("MGK_RELABEL");
-    if (!g->dg.rows_unique || m == 0 || n < 2 || !(on && on[0] == '1')) return cudaSuccess;
+    if (!g->dg.rows_unique || m == 0 || n < 2 || !(on && (on[0] == '1' || on[0] == '2'))) return cudaSuccess;
+    const bool by_out = on[0] == '2';
     uint32_t *perm = nullptr, *inv = nullptr;
     MGK_TRY(cudaMalloc(&perm, (size_t)n * 4));
     MGK_TRY(cudaMalloc(&inv, (size_t)n * 4));
@@ -384,7 +429,7 @@ cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
         unsigned long long *kv = nullptr, *ka = nullptr;
         MGK_TRY(cudaMallocAsync(&kv, (size_t)n * 8, s));
         MGK_TRY(cudaMallocAsync(&ka, (size_t)n * 8, s));
-        indeg_keys<<<blocks_for(n), kTB, 0, s>>>(g->cp, n, kv);
+        deg_keys<<<blocks_for(n), kTB, 0, s>>>(by_out ? g->rp : g->cp, n, kv);
         MGK_TRY(radix_sort_keys(kv, ka, n, 64, s));
         perm_from_sorted<<<blocks_for(n), kTB, 0, s>>>(kv, n, perm, inv);
         MGK_TRY(cudaGetLastError());
@@ -396,8 +441,9 @@ cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
     MGK_TRY(cudaStreamSynchronize(s));
     Graph old;
     old.rp = g->rp, old.ci = g->ci, old.cp = g->cp, old.ri = g->ri;
-    old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy;
+    old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy, old.hub_end = g->hub_end;
     g->heavy = nullptr;
+    g->hub_end = nullptr;
     cudaError_t e = graph_from_sorted_keys(g, keys, alt, m, s);
     if (!e) e = cudaStreamSynchronize(s);
     cudaFreeAsync(keys, s);
@@ -634,6 +680,11 @@ cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
     MGK_TRY(cp(dst->no_in, src->no_in, (size_t)(src->dg.nwords + 1) * 4));
     MGK_TRY(cp(dst->pull_skip, src->pull_skip, (size_t)(src->dg.nwords + 1) * 4));
     MGK_TRY(cp(dst->heavy, src->heavy, nh * sizeof(uint2)));
+    if (src->hub_end) {
+        MGK_TRY(cudaMalloc(&dst->hub_end, (size_t)(n + 1) * 4));
+        MGK_TRY(cp(dst->hub_end, src->hub_end, (size_t)(n + 1) * 4));
+    }
+    dst->dg.hub_end = dst->hub_end;
     if (src->perm) {
         MGK_TRY(cudaMalloc(&dst->perm, (size_t)n * 4));
         MGK_TRY(cudaMalloc(&dst->inv, (size_t)n * 4));
@@ -769,6 +820,9 @@ void free_device_graph(Graph* g) {
     cudaFree(g->no_in);
     cudaFree(g->pull_skip);
     cudaFree(g->heavy);
+    cudaFree(g->hub_end);
+    g->hub_end = nullptr;
+    g->dg.hub_end = nullptr;
     cudaFree(g->perm);
     cudaFree(g->inv);
     cudaFree(g->k2_split);

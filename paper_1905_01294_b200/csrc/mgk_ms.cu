@@ -51,6 +51,7 @@ constexpr int kBlock = MGK_MS_BLOCK;
 #endif
 constexpr int kWprUnroll = MGK_WPR_UNROLL;
 
+
 // a lane's own in-list (read a few entries at a time by the same lane: its
 // 32-byte sectors are re-read until the list is done, so by default they keep
 // normal L2 priority; MGK_RI_LIGHT_STREAM marks them evict-first too)
@@ -107,7 +108,7 @@ struct MSParams {
     uint32_t perlane;
     unsigned long long* lane_E;
     unsigned long long* lane_mu;
-    uint8_t* wact;  // [2][nwords] by hop parity: words a pull left unsettled
+    uint32_t* umask;  // [2][nwords] by hop parity: per word, the vertices a pull left unsettled
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
 
@@ -184,6 +185,11 @@ struct LS<W, 64> {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
         atomicOr(b + v * W + i, m);
     }
+    // fire-and-forget OR (no return value: the split pull's push half)
+    __device__ static __forceinline__ void red_or(unsigned long long* b, size_t v, unsigned long long m) {
+        static_assert(W == 1, "one word per vertex");
+        asm volatile("red.global.or.b64 [%0], %1;" ::"l"(b + v), "l"(m) : "memory");
+    }
     // (W = 1) OR m into v's word; true for the caller whose OR found the word
     // empty, i.e. the first to reach v in this hop (the word is zero between hops)
     __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
@@ -253,6 +259,12 @@ struct LSNarrow {
         constexpr uint32_t per = 32 / NB;
         atomicOr(reinterpret_cast<unsigned int*>(b) + v / per, (unsigned int)m << (NB * (v % per)));
     }
+    __device__ static __forceinline__ void red_or(unsigned long long* b, size_t v, unsigned long long m) {
+        constexpr uint32_t per = 32 / NB;
+        asm volatile("red.global.or.b32 [%0], %1;" ::"l"(reinterpret_cast<unsigned int*>(b) + v / per),
+                     "r"((unsigned int)m << (NB * (v % per)))
+                     : "memory");
+    }
     __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
         constexpr uint32_t per = 32 / NB;
         const uint32_t sh = NB * (v % per);
@@ -266,6 +278,7 @@ struct LS<1, 16> : LSNarrow<16> {};
 template <>
 struct LS<1, 8> : LSNarrow<8> {};
 
+
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.items1 : P.items0;
 }
@@ -276,9 +289,12 @@ __device__ __forceinline__ unsigned long long* F_of(const MSParams& P, uint32_t 
     return (i & 1) ? P.F1 : P.F0;
 }
 
+// per-thread counters of a phase (flushed per block after the phase; 32-bit:
+// a thread's share of a phase stays far below 2^32, except pe = sum deg x lanes)
 struct Acc {
-    unsigned long long found, edges, indeg, scanned, candidates, pairs, pe;
-    __device__ void zero() { found = edges = indeg = scanned = candidates = pairs = pe = 0; }
+    uint32_t found, edges, indeg, scanned, candidates, pairs;
+    unsigned long long pe;
+    __device__ void zero() { found = edges = indeg = scanned = candidates = pairs = 0; pe = 0; }
 };
 
 // Block reduce + flush. found/edges/indeg describe discovered vertices (-> q);
@@ -383,6 +399,80 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nitems
     st.n = 0;
 }
 
+// ---- split pull, push half ---------------------------------------------------
+// The first pull after a push hop (one word per vertex) is split by source
+// out-degree: in-neighbours with out-degree >= hub_deg (a prefix of every
+// in-list) are pulled, and the frontier vertices below hub_deg push their
+// words over all their out-edges with fire-and-forget ORs. Such a frontier is
+// small and its low-degree members are scattered: the pull would gather the
+// (mostly zero) words of every low-degree in-neighbour of every unvisited
+// vertex, the push touches only the frontier's own edges. Visited lanes are
+// masked off afterwards by the list pass.
+template <int W, int NB>
+MGK_PHASE void split_push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
+                                 const unsigned long long* Fc, unsigned long long* Fn, Acc& acc,
+                                 uint32_t warp_gid, uint32_t nwarps) {
+    if constexpr (W == 1) {
+        const uint32_t lane = lane_id();
+        const DevGraph& g = P.g;
+        const unsigned long long pol_ci = l2_stream_policy();
+        const uint32_t G = items_per_warp(nitems, nwarps);
+        for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
+            const uint32_t idx = base + lane;
+            const uint4 it = (lane < G && idx < nitems) ? items[idx] : make_uint4(0, 0, 0, 0);
+            const uint32_t len = it.y - it.x;
+            const uint32_t incl = warp_incl_scan(len);
+            const uint32_t total = __shfl_sync(kFull, incl, 31);
+            const uint32_t off = it.x - (incl - len);
+            // the item's source word, once per item
+            const unsigned long long fw = len ? LS<W, NB>::load(Fc, it.z).w[0] : 0ull;
+            for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+                const uint32_t x = x0 + lane;
+                const bool valid = x < total;
+                const uint32_t j = warp_owner(incl, valid ? x : total - 1);
+                const uint32_t pos = __shfl_sync(kFull, off, j) + x;
+                const unsigned long long f = __shfl_sync(kFull, fw, j);
+                if (valid) LS<W, NB>::red_or(Fn, ldg_hint(g.ci + pos, pol_ci), f);
+                acc.scanned += valid;
+            }
+        }
+    }
+}
+
+// ---- split pull, list pass: Fn &= ~V over all vertices; the vertices with
+// lanes left form the discovery list (ascending) --------------------------------
+template <int W, int NB>
+MGK_PHASE void split_list_phase(const MSParams& P, unsigned long long* Fn, uint32_t* Rn, QCtl* qn,
+                                Stage<kStageCap>& st, uint32_t gtid, uint32_t nthreads) {
+    if constexpr (W == 1) {
+        const DevGraph& g = P.g;
+        const uint32_t n_up = (g.n + 31) & ~31u;  // whole warps (the stage push is warp-wide)
+        for (uint32_t base = gtid & ~31u; base < n_up; base += nthreads) {
+            const uint32_t u = base + lane_id();
+            bool found = false;
+            if (u < g.n) {
+                const unsigned long long x = LS<W, NB>::load_cg(Fn, u).w[0];
+                if (x) {
+                    const unsigned long long y = x & ~LS<W, NB>::load_cg(P.V, u).w[0];
+                    if (y != x) {
+                        LaneWord<1> t;
+                        t.w[0] = y;
+                        LS<W, NB>::store(Fn, u, t);
+                    }
+                    found = y != 0;
+                }
+            }
+            st.push(found, u);
+            if (st.full()) {
+                emit_list(st.buf, st.n, Rn, &qn->nitems);
+                st.n = 0;
+            }
+        }
+        emit_list(st.buf, st.n, Rn, &qn->nitems);
+        st.n = 0;
+    }
+}
+
 // ---- pull expand -------------------------------------------------------------
 // Vertices are split by in-degree: <= 32 in-edges are scanned by one thread
 // (two lane-word gathers in flight per step), 33..kHeavyIn by the word's warp
@@ -408,8 +498,8 @@ __device__ __forceinline__ bool covers(const LaneWord<W>& acc, const LaneWord<W>
 // once `need` is covered. Returns the OR (all lanes) and the entries read.
 template <int W, int NB>
 __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const unsigned long long* Fc,
-                                                       uint32_t b, uint32_t e, const LaneWord<W>& need,
-                                                       uint32_t& scanned) {
+                                                       uint32_t b, uint32_t e,
+                                                       const LaneWord<W>& need, uint32_t& scanned) {
     const uint32_t lane = lane_id();
     const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     LaneWord<W> acc;
@@ -455,7 +545,7 @@ template <int W, int NB>
 MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
                            Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
-                           const uint8_t* wact_in, uint8_t* wact_out) {
+                           const uint32_t* um_in, uint32_t* um_out, bool split, uint32_t* s_nm, uint32_t* s_cb) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -463,32 +553,19 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
     const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
     const uint32_t wchunk = max(8u, g.nwords / (nwarps * 8));
     ChunkGrab words(&P.misc[1], g.nwords, wchunk, warp_gid);
-    // a word costs one round trip before its scan starts: the skip masks of 32
-    // words arrive with one coalesced load, and each lane's CSC bounds are
-    // loaded together with its visited word (not after it): in the sparse late
-    // hops most words have no candidate, and a dependent chain per word would
-    // dominate
-    for (; words.valid(); words.advance(nwarps))
-    for (uint32_t wb = words.c * wchunk, wend = min(g.nwords, (words.c + 1) * wchunk); wb < wend; wb += 32) {
-    // wact_in (a pull right after a pull): words whose vertices all settled in
-    // that pull have no candidate now (the active lanes only shrink and the
-    // visited sets only grow); wact_out records this pull's unsettled words
-    const uint32_t skip_l = wb + lane < wend ? ((wact_in && !ld_cg_u8(wact_in + wb + lane)) ? kFull
-                                                 : __ldg(g.pull_skip + wb + lane)) : kFull;
-    uint32_t unsettled = 0;  // bit q: word wb + q still has a candidate with lanes left
-    for (uint32_t w = wb; w < min(wend, wb + 32); ++w) {
-        const uint32_t skip = __shfl_sync(kFull, skip_l, w - wb);
-        if (skip == kFull) continue;
-        const uint32_t u = w * 32 + lane;
+    // one candidate per lane (valid): visited word, CSC bounds, the lane's scan
+    // of a short list (or the first kPre entries), the warp's scans of the
+    // unsettled longer lists, the next-frontier store; true when lanes are left
+    auto visit = [&](bool valid, uint32_t u, bool& found) -> bool {
         LaneWord<W> need, vis;
 #pragma unroll
         for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
         bool cand = false;
         uint32_t b = 0, e = 0;
-        if (!((skip >> lane) & 1u)) {
+        if (valid) {
             vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
             b = __ldg(g.cp + u);
-            e = __ldg(g.cp + u + 1);
+            e = split ? __ldg(g.hub_end + u) : __ldg(g.cp + u + 1);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
@@ -548,7 +625,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 scanned += sc;
             }
         }
-        bool found = false;
+        found = false;
         if (cand) {
             LaneWord<W> res;
 #pragma unroll
@@ -572,14 +649,52 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
         bool left = false;
 #pragma unroll
         for (int i = 0; i < W; ++i) left |= (need.w[i] & ~acc_w.w[i]) != 0;
-        if (__ballot_sync(kFull, cand && left)) unsettled |= 1u << (w - wb);
-        st.push(found, u);
+        st.push(found && !split, u);  // split: the list pass lists every discovery
         if (st.full()) {
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
         }
+        return cand && left;
+    };
+    // Candidates are packed into lanes: the warp walks 32 words at a time,
+    // appends each word's candidates (not pull_skip; after a pull only the
+    // vertices that pull left unsettled, um_in) to a per-warp buffer in shared
+    // memory and visits them 32 at a time, so no lane idles on a skipped,
+    // settled or zero-in-degree vertex (the late pulls have a few candidates
+    // per word). um_out receives this pull's unsettled vertices: the next
+    // pull's candidates are among them (the active lanes only shrink and the
+    // visited sets only grow).
+    for (; words.valid(); words.advance(nwarps))
+    for (uint32_t wb = words.c * wchunk, wend = min(g.nwords, (words.c + 1) * wchunk); wb < wend; wb += 32) {
+    const uint32_t wq = wb + lane;
+    const uint32_t mq = wq < wend ? ~__ldg(g.pull_skip + wq) & (um_in ? __ldcg(um_in + wq) : kFull) : 0u;
+    s_nm[lane] = 0;
+    uint32_t fill = 0;  // warp-uniform: candidates waiting in s_cb
+    __syncwarp();
+    const uint32_t nw = min(wend - wb, 32u);
+    for (uint32_t q = 0; q <= nw; ++q) {
+        if (q < nw) {
+            const uint32_t m = __shfl_sync(kFull, mq, q);
+            if (m == 0) continue;
+            if ((m >> lane) & 1u) s_cb[fill + __popc(m & lanemask_lt())] = (wb + q) * 32 + lane;
+            fill += __popc(m);
+            __syncwarp();
+            if (fill < 32) continue;
+        } else if (fill == 0) {
+            break;
+        }
+        // one round: the first 32 waiting candidates (the group's last round may be partial)
+        const bool valid = lane < fill;
+        const uint32_t u = valid ? s_cb[lane] : 0u;
+        __syncwarp();
+        if (fill > 32 && lane < fill - 32) s_cb[lane] = s_cb[32 + lane];
+        fill = fill > 32 ? fill - 32 : 0;
+        __syncwarp();
+        bool found;
+        if (visit(valid, u, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
     }
-    if (wact_out && wb + lane < wend) wact_out[wb + lane] = (unsettled >> lane) & 1u;
+    __syncwarp();
+    if (um_out && wq < wend) um_out[wq] = s_nm[lane];
     }
     // heavy in-degree vertices: kHeavyChunk-entry tasks (chunk-major). A warp
     // checks 32 tasks at once (one task per lane: record, visited word and,
@@ -588,12 +703,12 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
     // task is settled and costs one parallel round of loads, not a chain per task
     // (many tasks per warp: chunks of 32-task groups; few: single tasks, so the
     // scans still spread over every warp)
-    // Batched only after a pull (wact_in): then most tasks are settled; in the
+    // Batched only after a pull (um_in): then most tasks are settled; in the
     // first, dense pull a task is checked right before its scan, which sees
     // more of what its vertex's earlier chunks found
-    const uint32_t tchunk = (wact_in && g.nheavy >= nwarps * 64) ? (g.nheavy / (nwarps * 4) + 31) / 32 * 32
-                                                                 : max(1u, g.nheavy / (nwarps * 8));
-    const uint32_t tstep = (wact_in && g.nheavy >= nwarps * 64) ? 32u : 1u;
+    const uint32_t tchunk = (um_in && g.nheavy >= nwarps * 64) ? (g.nheavy / (nwarps * 4) + 31) / 32 * 32
+                                                               : max(1u, g.nheavy / (nwarps * 8));
+    const uint32_t tstep = (um_in && g.nheavy >= nwarps * 64) ? 32u : 1u;
     ChunkGrab tasks(&P.misc[2], g.nheavy, tchunk, warp_gid);
     for (; tasks.valid(); tasks.advance(nwarps))
     for (uint32_t t0 = tasks.c * tchunk, tend = min(g.nheavy, (tasks.c + 1) * tchunk); t0 < tend; t0 += tstep) {
@@ -608,12 +723,14 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             u = task.x;
             ty = task.y;
             tb = __ldg(g.cp + u);
+            if (split && ty >= __ldg(g.hub_end + u)) ty = kFull;  // a chunk past the hub prefix
             vis = LS<W, NB>::load(P.V, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
                 cand |= need.w[i] != 0;
             }
+            if (ty == kFull) cand = false;
             if (cand && ty != tb) {
                 // a later chunk: only the lanes the earlier chunks of u have not
                 // found yet; none left -> nothing to scan
@@ -649,7 +766,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                     for (int i = 0; i < W; ++i) need.w[i] = nj.w[i];
                 }
             }
-            const uint32_t e = min(yj + kHeavyChunk, __ldg(g.cp + uj + 1));
+            const uint32_t e = min(yj + kHeavyChunk, split ? __ldg(g.hub_end + uj) : __ldg(g.cp + uj + 1));
             uint32_t sc = 0;
             const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, yj, e, nj, sc);
             if ((int)lane == j) {
@@ -677,7 +794,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 }
             }
         }
-        st.push(first, u);
+        st.push(first && !split, u);
         if (st.full()) {
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
@@ -695,9 +812,14 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
                                uint32_t warp_gid, uint32_t nwarps, unsigned long long* s_E = nullptr,
-                               unsigned long long* s_mu = nullptr) {
+                               unsigned long long* s_mu = nullptr, bool dense = false) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
+    // dense (a list of more than n/8, one word per vertex): sweep every vertex
+    // instead of the list, with all of a vertex's loads (frontier and visited
+    // words, CSR / CSC bounds) issued at once and coalesced -- one round trip
+    // per vertex instead of two dependent ones; the discovered vertices are
+    // those with a non-zero new word. The list itself stays as built.
     // per-lane Beamer inputs (W = 1): lane l of the warp sums lanes l and 32 + l
     constexpr uint32_t LBs = W == 1 ? LS<W, NB>::kLanes : 0;
     unsigned long long eA[2] = {0, 0}, mA[2] = {0, 0};
@@ -708,18 +830,36 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
         act.w[i] = 0;
         cnt_lo[i] = cnt_hi[i] = 0;
     }
-    for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
+    const uint32_t lim = dense ? g.n : nR;
+    for (uint32_t base = warp_gid * 32; base < lim; base += nwarps * 32) {
         const uint32_t idx = base + lane;
-        const bool valid = idx < nR;
+        bool valid = idx < lim;
         uint32_t u = 0, deg_of = 0, indeg_of = 0;
-        LaneWord<W> x;
+        LaneWord<W> x, v;
 #pragma unroll
-        for (int i = 0; i < W; ++i) x.w[i] = 0;
+        for (int i = 0; i < W; ++i) x.w[i] = v.w[i] = 0;
+        uint32_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;
         bool expand = false;
-        if (valid) {
+        if (dense) {
+            if (valid) {
+                u = idx;
+                x = LS<W, NB>::load(Fn, u);
+                v = LS<W, NB>::load(P.V, u);
+                r0 = __ldg(g.rp + u);
+                r1 = __ldg(g.rp + u + 1);
+                c0 = __ldg(g.cp + u);
+                c1 = __ldg(g.cp + u + 1);
+                bool any = false;
+#pragma unroll
+                for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
+                valid = any;
+            }
+        } else if (valid) {
             u = Rn[idx];
             x = LS<W, NB>::load(Fn, u);
-            LaneWord<W> v = LS<W, NB>::load(P.V, u);
+            v = LS<W, NB>::load(P.V, u);
+        }
+        if (valid) {
             bool fresh = true;  // no lane had visited u: its in-edges leave the unexplored set
 #pragma unroll
             for (int i = 0; i < W; ++i) fresh &= v.w[i] == 0;
@@ -739,10 +879,19 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             // vertex: the word itself decides who lists u)
             if (touched_set || (W > 1 && ((__ldg(g.pull_skip + (u >> 5)) >> (u & 31)) & 1u)))
                 atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
-            if (clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
-            const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
+            // (a dense sweep writes no copy: the batch's V is then cleared by streaming)
+            if (!dense && clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
             const bool need_in = fresh || (LBs > 0 && s_E);
-            const uint32_t indeg = need_in ? __ldg(g.cp + u + 1) - __ldg(g.cp + u) : 0;
+            if (!dense) {
+                r0 = __ldg(g.rp + u);
+                r1 = __ldg(g.rp + u + 1);
+                if (need_in) {
+                    c0 = __ldg(g.cp + u);
+                    c1 = __ldg(g.cp + u + 1);
+                }
+            }
+            const uint32_t deg = r1 - r0;
+            const uint32_t indeg = need_in ? c1 - c0 : 0;
             acc.found += 1;  // distinct vertices discovered, their out-edges, fresh in-edges
             acc.edges += deg;
             if (fresh) acc.indeg += indeg;
@@ -831,7 +980,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
 template <int W, int NB>
 MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
                            const LaneWord<W>& pushm, uint4* items_n, unsigned int* item_tail, Stage<kStageCap>& st,
-                           uint32_t warp_gid, uint32_t nwarps) {
+                           uint32_t warp_gid, uint32_t nwarps, uint32_t max_deg = kFull) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
@@ -843,7 +992,8 @@ MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, co
             const LaneWord<W> x = LS<W, NB>::load(Fn, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) expand |= (x.w[i] & pushm.w[i]) != 0;
-            expand = expand && __ldg(g.rp + u + 1) > __ldg(g.rp + u);
+            const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
+            expand = expand && deg > 0 && deg < max_deg;
         }
         st.push(expand, u);
         if (st.full()) {
@@ -862,6 +1012,23 @@ __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F,
 #pragma unroll
     for (int i = 0; i < W; ++i) z.w[i] = 0;
     for (uint32_t i = gtid; i < n; i += nthreads) LS<W, NB>::store(F, R[i], z);
+}
+
+// Zero the lane words of the listed vertices: one scattered store each, or,
+// for a list of more than 1/8 of the vertices (a dense pull's frontier),
+// streaming 16-byte zeros over the whole array (coalesced, a fraction of the
+// stores' time)
+template <int W, int NB>
+__device__ void clear_words(const uint32_t* R, uint32_t nlist, unsigned long long* F, uint32_t nv, uint32_t gtid,
+                            uint32_t nthreads) {
+    if ((uint64_t)nlist * 8 <= nv) {
+        clear_list<W, NB>(R, nlist, F, gtid, nthreads);
+        return;
+    }
+    const size_t w64 = LS<W, NB>::words64(nv);
+    uint4* f4 = reinterpret_cast<uint4*>(F);
+    for (size_t i = gtid; i < w64 / 2; i += nthreads) f4[i] = make_uint4(0, 0, 0, 0);
+    if ((w64 & 1) && gtid == 0) F[w64 - 1] = 0;
 }
 
 // resident CTAs per SM the register budget is sized for, per instance: one
@@ -885,6 +1052,8 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
     constexpr uint32_t LBs = W == 1 ? LB : 1;
     __shared__ unsigned long long s_E[LBs], s_mu[LBs];
     __shared__ uint32_t s_pm[2];
+    __shared__ uint32_t s_nm[kWarps][32];  // pull: unsettled-vertex masks of a warp's 32 words
+    __shared__ uint32_t s_cb[kWarps][64];  // pull: a warp's waiting candidates
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = gridDim.x * kBlock;
     const uint32_t warp_gid = gtid >> 5;
@@ -955,6 +1124,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
         grid_barrier(P.bar);
 
         bool prev_pull = false;  // the hop before pulled: its unsettled words bound this pull's
+        bool split = false;      // this hop is a split pull (its push items were emitted by the hop before)
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
         uint32_t hop = 1;
@@ -990,10 +1160,19 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
+            // a pull after a pull visits only the vertices that pull left unsettled
             if (anypull)
                 pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
-                                  (!P.perlane && prev_pull) ? P.wact + (size_t)cur * g.nwords : nullptr,
-                                  P.perlane ? nullptr : P.wact + (size_t)nxt * g.nwords);
+                                  (!P.perlane && prev_pull) ? P.umask + (size_t)cur * g.nwords : nullptr,
+                                  P.perlane ? nullptr : P.umask + (size_t)nxt * g.nwords, split,
+                                  s_nm[threadIdx.x >> 5], s_cb[threadIdx.x >> 5]);
+            if (split) {
+                grid_barrier(P.bar);
+                split_push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, acc, warp_gid,
+                                        nwarps);
+                grid_barrier(P.bar);
+                split_list_phase<W, NB>(P, Fn, Rn, qn, st, gtid, nthreads);
+            }
             prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
@@ -1011,8 +1190,9 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             __syncthreads();
             finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
-                              (P.perlane && !last) ? s_E : nullptr, s_mu);
-            clear_list<W, NB>(Rc, nR_prev, Fc, gtid, nthreads);
+                              (P.perlane && !last) ? s_E : nullptr, s_mu,
+                              W == 1 && !P.perlane && (uint64_t)nR * 8 > g.n);
+            clear_words<W, NB>(Rc, nR_prev, Fc, g.n, gtid, nthreads);
             __syncthreads();
             if (count_lanes)
                 for (uint32_t t = threadIdx.x; t < LB; t += kBlock)
@@ -1025,6 +1205,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
                         &P.misc[0]);
             grid_barrier(P.bar);
             // ---- the next hop's directions (every CTA computes the same) ---------------
+            bool split_next = false;
             if (!last) {
                 if (P.perlane) {
                     // lane l: push -> pull when its frontier's out-edges x alpha exceed
@@ -1061,22 +1242,27 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
                         pn = true;
                     } else if (!anypull) {
                         pn = mf * P.alpha > mu;
+                        // the first pull after pushes is split by source out-degree
+                        // (one word per vertex; forced directions keep whole pulls)
+                        split_next = W == 1 && pn && g.hub_deg > 0 && g.hub_end != nullptr;
                     } else {
                         pn = (unsigned long long)nR * P.beta >= g.n;
                     }
 #pragma unroll
                     for (int i = 0; i < W; ++i) pullm.w[i] = pn ? ~0ull : 0ull;
                 }
-                // items for the lanes pushing next
+                // items for the lanes pushing next (a split pull: the frontier
+                // vertices below hub_deg, all lanes)
                 LaneWord<W> pn_push;
                 bool anyn = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & ~pullm.w[i];
+                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & (split_next ? ~0ull : ~pullm.w[i]);
                     anyn |= pn_push.w[i] != 0;
                 }
                 if (anyn) {
-                    emit_phase<W, NB>(P, Rn, nR, Fn, pn_push, items_of(P, nxt), &qn->nfound, st, warp_gid, nwarps);
+                    emit_phase<W, NB>(P, Rn, nR, Fn, pn_push, items_of(P, nxt), &qn->nfound, st, warp_gid, nwarps,
+                                      split_next ? g.hub_deg : kFull);
                     grid_barrier(P.bar);
                 }
             }
@@ -1090,6 +1276,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             }
             clog_used += nR;
             nR_prev = nR;
+            split = split_next;
             if (nR == 0) break;
         }
         // ---- answers ------------------------------------------------------------------
@@ -1107,12 +1294,12 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
         if (clog_used <= P.clog_cap && clog_used * 8 <= g.n) {
             clear_list<W, NB>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
-            clear_list<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
+            clear_words<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), g.n, gtid, nthreads);
         } else if (clog_used <= P.clog_cap) {
             // most vertices visited: stream zeros over V (coalesced) instead of
             // one scattered store per visited vertex
             for (size_t i = gtid; i < LS<W, NB>::words64(g.n); i += nthreads) P.V[i] = 0;
-            clear_list<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), gtid, nthreads);
+            clear_words<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), g.n, gtid, nthreads);
         } else {
             for (size_t i = gtid; i < LS<W, NB>::words64(g.n); i += nthreads) {
                 P.V[i] = 0;
@@ -1189,7 +1376,7 @@ cudaError_t launch_w(Launch& L) {
     P.perlane = (W == 1 && perlane) ? 1u : 0u;
     P.lane_E = ws->lane_stat;
     P.lane_mu = ws->lane_stat + 2 * 512;
-    P.wact = ws->wact;
+    P.umask = ws->umask;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
     P.force_dir = L.tuning.force_dir;
@@ -1231,7 +1418,7 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
-    if (!ws->wact && (e = cudaMalloc(&ws->wact, 2 * ((size_t)g.nwords + 32)))) return e;
+    if (!ws->umask && (e = cudaMalloc(&ws->umask, 2 * ((size_t)g.nwords + 32) * 4))) return e;
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
         if ((e = cudaMalloc(&ws->touched, (size_t)(g.nwords + 1) * 4))) return e;

@@ -23,6 +23,22 @@ def run(gname, bits_list, reps=5):
     rp, _ = g.csr()
     seeds = H.pick_seeds(rp, 10, 1)
     print(f"{gname}: n={g.nrows} m={g.nnz} ({time.time() - t:.1f}s)", flush=True)
+    # the k = 2 group of the schedule (300 seeds, on-chip k2 kernel)
+    s300 = torch.from_numpy(H.pick_seeds(rp, 300, 1).astype(np.int32)).cuda()
+    c300 = torch.zeros(300, dtype=torch.int64, device="cuda")
+    st0 = torch.cuda.current_stream()
+    fl = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    k2t = []
+    for _ in range(6):
+        fl.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st0)
+        k_hop_count_device(g, s300.data_ptr(), 300, 2, 0, c300.data_ptr(), st0.cuda_stream)
+        e1.record(st0)
+        torch.cuda.synchronize()
+        k2t.append(e0.elapsed_time(e1))
+    print(f"{gname} k2 300 seeds: {np.median(k2t[1:]):.3f} ms sum={int(c300.sum())}", flush=True)
+    del fl
     d_seeds = torch.from_numpy(seeds.astype(np.int32)).cuda()
     d_counts = torch.zeros(10, dtype=torch.int64, device="cuda")
     s = torch.cuda.current_stream()
