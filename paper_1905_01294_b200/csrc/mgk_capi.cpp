@@ -127,7 +127,6 @@ void destroy_ws(Workspace* ws, bool own_stream) {
     for (auto* p : ws->ms_items) cudaFree(p);
     cudaFree(ws->lane_cnt);
     cudaFree(ws->active);
-    cudaFree(ws->lane_stat);
     cudaFree(ws->umask);
     cudaFree(ws->qctl);
     cudaFree(ws->misc);

@@ -105,25 +105,6 @@ __global__ void heavy_fill(uint32_t n, const uint32_t* off, unsigned long long* 
     }
 }
 
-// hub_end[u]: first position of u's in-list (descending source out-degree)
-// whose source has out-degree < D (binary search)
-__global__ void hub_end_kernel(const uint32_t* cp, const uint32_t* ri, const uint32_t* rp, uint32_t n, uint32_t D,
-                               uint32_t* hub_end) {
-    for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < n;
-         u += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t lo = cp[u], hi = cp[u + 1];
-        while (lo < hi) {
-            const uint32_t mid = lo + (hi - lo) / 2;
-            const uint32_t v = ri[mid];
-            if (rp[v + 1] - rp[v] >= D)
-                lo = mid + 1;
-            else
-                hi = mid;
-        }
-        hub_end[u] = lo;
-    }
-}
-
 __global__ void heavy_tasks(const unsigned long long* keys, uint64_t nt, const uint32_t* cp, uint2* tasks) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < nt; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t u = (uint32_t)keys[t], i = (uint32_t)(keys[t] >> 32);
@@ -208,7 +189,6 @@ cudaError_t radix_sort_keys(unsigned long long*& keys, unsigned long long*& alt,
 }
 
 cudaError_t build_heavy(Graph* g, cudaStream_t s);
-cudaError_t build_hub_end(Graph* g, cudaStream_t s);
 
 // (col << 32 | row) sorted keys -> (col << 32 | ~outdeg(row)) keys + row values
 __global__ void make_deg_keys(unsigned long long* keys, uint32_t* vals, uint64_t m,
@@ -318,31 +298,9 @@ cudaError_t build_heavy(Graph* g, cudaStream_t s) {
     }
     MGK_TRY(cudaFreeAsync(cnt, s));
     MGK_TRY(cudaFreeAsync(d_total, s));
-    return build_hub_end(g, s);
+    return cudaSuccess;
 }
 
-// LANES split pull (opt-in, MGK_HUB_DEG=D): the out-degree threshold and
-// every vertex's hub-prefix end
-uint32_t hub_deg_default() {
-    static const uint32_t d = [] {
-        const char* e = std::getenv("MGK_HUB_DEG");
-        return e ? (uint32_t)std::atoi(e) : 0u;
-    }();
-    return d;
-}
-
-cudaError_t build_hub_end(Graph* g, cudaStream_t s) {
-    const uint32_t n = g->dg.n;
-    if (hub_deg_default() == 0) return cudaSuccess;
-    if (!g->hub_end) {
-        MGK_TRY(cudaMalloc(&g->hub_end, (size_t)(n + 1) * 4));
-        g->bytes += (size_t)(n + 1) * 4;
-    }
-    g->dg.hub_end = g->hub_end;
-    g->dg.hub_deg = hub_deg_default();
-    hub_end_kernel<<<blocks_for(n), kTB, 0, s>>>(g->cp, g->ri, g->rp, n, std::max(g->dg.hub_deg, 1u), g->hub_end);
-    return cudaGetLastError();
-}
 
 cudaError_t alloc_graph(Graph* g, uint32_t n, uint64_t m) {
     g->dg.n = n;
@@ -441,9 +399,8 @@ cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
     MGK_TRY(cudaStreamSynchronize(s));
     Graph old;
     old.rp = g->rp, old.ci = g->ci, old.cp = g->cp, old.ri = g->ri;
-    old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy, old.hub_end = g->hub_end;
+    old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy;
     g->heavy = nullptr;
-    g->hub_end = nullptr;
     cudaError_t e = graph_from_sorted_keys(g, keys, alt, m, s);
     if (!e) e = cudaStreamSynchronize(s);
     cudaFreeAsync(keys, s);
@@ -680,11 +637,6 @@ cudaError_t replicate_device_graph(const Graph* src, Graph* dst) {
     MGK_TRY(cp(dst->no_in, src->no_in, (size_t)(src->dg.nwords + 1) * 4));
     MGK_TRY(cp(dst->pull_skip, src->pull_skip, (size_t)(src->dg.nwords + 1) * 4));
     MGK_TRY(cp(dst->heavy, src->heavy, nh * sizeof(uint2)));
-    if (src->hub_end) {
-        MGK_TRY(cudaMalloc(&dst->hub_end, (size_t)(n + 1) * 4));
-        MGK_TRY(cp(dst->hub_end, src->hub_end, (size_t)(n + 1) * 4));
-    }
-    dst->dg.hub_end = dst->hub_end;
     if (src->perm) {
         MGK_TRY(cudaMalloc(&dst->perm, (size_t)n * 4));
         MGK_TRY(cudaMalloc(&dst->inv, (size_t)n * 4));
@@ -820,9 +772,6 @@ void free_device_graph(Graph* g) {
     cudaFree(g->no_in);
     cudaFree(g->pull_skip);
     cudaFree(g->heavy);
-    cudaFree(g->hub_end);
-    g->hub_end = nullptr;
-    g->dg.hub_end = nullptr;
     cudaFree(g->perm);
     cudaFree(g->inv);
     cudaFree(g->k2_split);

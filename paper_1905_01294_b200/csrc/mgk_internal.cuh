@@ -34,11 +34,6 @@ struct DevGraph {
     const uint32_t* pull_skip = nullptr;  // no_in | heavy: what the per-word pull pass skips
     const uint2* heavy = nullptr;         // {vertex, first CSC entry} per task
     uint32_t nheavy = 0;
-    // LANES split pull (mgk_ms.cu): in-lists are ordered by descending source
-    // out-degree, so the in-neighbours with out-degree >= hub_deg form a
-    // prefix; hub_end[u] = the CSC position where u's prefix ends
-    const uint32_t* hub_end = nullptr;
-    uint32_t hub_deg = 0;
     // every CSR row strictly ascending (no duplicate entries): hop 1 from a
     // seed is then its row minus the seed itself, with no test-and-set
     uint32_t rows_unique = 0;
@@ -146,7 +141,6 @@ struct Workspace {
     unsigned long long* lane_cnt = nullptr;  // [(MGK_MAX_HOPS+1) * 64 * W]
     unsigned long long* active = nullptr;    // [2 * W]
     uint32_t* umask = nullptr;                // [2][nwords] per word, vertices a pull left unsettled (by hop parity)
-    unsigned long long* lane_stat = nullptr;  // [3 * 512]: per-lane frontier out-edges (x2) and unexplored in-edges
     // shared small control block
     QCtl* qctl = nullptr;                    // [3]
     unsigned long long* misc = nullptr;      // [16]
@@ -179,7 +173,6 @@ struct Graph {
     uint32_t* no_in = nullptr;
     uint32_t* pull_skip = nullptr;
     uint2* heavy = nullptr;
-    uint32_t* hub_end = nullptr;
     uint32_t* perm = nullptr;
     uint32_t* inv = nullptr;
     unsigned int* bad_seed = nullptr;

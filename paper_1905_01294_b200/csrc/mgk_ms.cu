@@ -102,12 +102,6 @@ struct MSParams {
     unsigned int* bar;
     LevelCounters* lc;
     uint32_t alpha, beta, force_dir;
-    // per-lane directions (LB <= 64): each lane pushes or pulls by its own
-    // Beamer test; lane_E [2][LB] out-edges of the frontier just found (by hop
-    // parity), lane_mu [LB] unexplored in-edges of each lane
-    uint32_t perlane;
-    unsigned long long* lane_E;
-    unsigned long long* lane_mu;
     uint32_t* umask;  // [2][nwords] by hop parity: per word, the vertices a pull left unsettled
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
 };
@@ -185,11 +179,6 @@ struct LS<W, 64> {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int i, unsigned long long m) {
         atomicOr(b + v * W + i, m);
     }
-    // fire-and-forget OR (no return value: the split pull's push half)
-    __device__ static __forceinline__ void red_or(unsigned long long* b, size_t v, unsigned long long m) {
-        static_assert(W == 1, "one word per vertex");
-        asm volatile("red.global.or.b64 [%0], %1;" ::"l"(b + v), "l"(m) : "memory");
-    }
     // (W = 1) OR m into v's word; true for the caller whose OR found the word
     // empty, i.e. the first to reach v in this hop (the word is zero between hops)
     __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
@@ -258,12 +247,6 @@ struct LSNarrow {
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int, unsigned long long m) {
         constexpr uint32_t per = 32 / NB;
         atomicOr(reinterpret_cast<unsigned int*>(b) + v / per, (unsigned int)m << (NB * (v % per)));
-    }
-    __device__ static __forceinline__ void red_or(unsigned long long* b, size_t v, unsigned long long m) {
-        constexpr uint32_t per = 32 / NB;
-        asm volatile("red.global.or.b32 [%0], %1;" ::"l"(reinterpret_cast<unsigned int*>(b) + v / per),
-                     "r"((unsigned int)m << (NB * (v % per)))
-                     : "memory");
     }
     __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
         constexpr uint32_t per = 32 / NB;
@@ -399,80 +382,6 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nitems
     st.n = 0;
 }
 
-// ---- split pull, push half ---------------------------------------------------
-// The first pull after a push hop (one word per vertex) is split by source
-// out-degree: in-neighbours with out-degree >= hub_deg (a prefix of every
-// in-list) are pulled, and the frontier vertices below hub_deg push their
-// words over all their out-edges with fire-and-forget ORs. Such a frontier is
-// small and its low-degree members are scattered: the pull would gather the
-// (mostly zero) words of every low-degree in-neighbour of every unvisited
-// vertex, the push touches only the frontier's own edges. Visited lanes are
-// masked off afterwards by the list pass.
-template <int W, int NB>
-MGK_PHASE void split_push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
-                                 const unsigned long long* Fc, unsigned long long* Fn, Acc& acc,
-                                 uint32_t warp_gid, uint32_t nwarps) {
-    if constexpr (W == 1) {
-        const uint32_t lane = lane_id();
-        const DevGraph& g = P.g;
-        const unsigned long long pol_ci = l2_stream_policy();
-        const uint32_t G = items_per_warp(nitems, nwarps);
-        for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
-            const uint32_t idx = base + lane;
-            const uint4 it = (lane < G && idx < nitems) ? items[idx] : make_uint4(0, 0, 0, 0);
-            const uint32_t len = it.y - it.x;
-            const uint32_t incl = warp_incl_scan(len);
-            const uint32_t total = __shfl_sync(kFull, incl, 31);
-            const uint32_t off = it.x - (incl - len);
-            // the item's source word, once per item
-            const unsigned long long fw = len ? LS<W, NB>::load(Fc, it.z).w[0] : 0ull;
-            for (uint32_t x0 = 0; x0 < total; x0 += 32) {
-                const uint32_t x = x0 + lane;
-                const bool valid = x < total;
-                const uint32_t j = warp_owner(incl, valid ? x : total - 1);
-                const uint32_t pos = __shfl_sync(kFull, off, j) + x;
-                const unsigned long long f = __shfl_sync(kFull, fw, j);
-                if (valid) LS<W, NB>::red_or(Fn, ldg_hint(g.ci + pos, pol_ci), f);
-                acc.scanned += valid;
-            }
-        }
-    }
-}
-
-// ---- split pull, list pass: Fn &= ~V over all vertices; the vertices with
-// lanes left form the discovery list (ascending) --------------------------------
-template <int W, int NB>
-MGK_PHASE void split_list_phase(const MSParams& P, unsigned long long* Fn, uint32_t* Rn, QCtl* qn,
-                                Stage<kStageCap>& st, uint32_t gtid, uint32_t nthreads) {
-    if constexpr (W == 1) {
-        const DevGraph& g = P.g;
-        const uint32_t n_up = (g.n + 31) & ~31u;  // whole warps (the stage push is warp-wide)
-        for (uint32_t base = gtid & ~31u; base < n_up; base += nthreads) {
-            const uint32_t u = base + lane_id();
-            bool found = false;
-            if (u < g.n) {
-                const unsigned long long x = LS<W, NB>::load_cg(Fn, u).w[0];
-                if (x) {
-                    const unsigned long long y = x & ~LS<W, NB>::load_cg(P.V, u).w[0];
-                    if (y != x) {
-                        LaneWord<1> t;
-                        t.w[0] = y;
-                        LS<W, NB>::store(Fn, u, t);
-                    }
-                    found = y != 0;
-                }
-            }
-            st.push(found, u);
-            if (st.full()) {
-                emit_list(st.buf, st.n, Rn, &qn->nitems);
-                st.n = 0;
-            }
-        }
-        emit_list(st.buf, st.n, Rn, &qn->nitems);
-        st.n = 0;
-    }
-}
-
 // ---- pull expand -------------------------------------------------------------
 // Vertices are split by in-degree: <= 32 in-edges are scanned by one thread
 // (two lane-word gathers in flight per step), 33..kHeavyIn by the word's warp
@@ -544,8 +453,8 @@ struct ChunkGrab {
 template <int W, int NB>
 MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsigned long long* Fn,
                            const LaneWord<W>& active, uint32_t* Rn, QCtl* qn, Acc& acc,
-                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps, bool mixed,
-                           const uint32_t* um_in, uint32_t* um_out, bool split, uint32_t* s_nm, uint32_t* s_cb) {
+                           Stage<kStageCap>& st, uint32_t warp_gid, uint32_t nwarps,
+                           const uint32_t* um_in, uint32_t* um_out, uint32_t* s_nm, uint32_t* s_cb) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
@@ -565,7 +474,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
         if (valid) {
             vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
             b = __ldg(g.cp + u);
-            e = split ? __ldg(g.hub_end + u) : __ldg(g.cp + u + 1);
+            e = __ldg(g.cp + u + 1);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
@@ -633,23 +542,14 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 res.w[i] = acc_w.w[i] & need.w[i];
                 found |= res.w[i] != 0;
             }
-            if (found) {
-                if (mixed) {
-                    // pushing lanes may have reached u in this hop too (mixed hops
-                    // only with one word per vertex): OR the pulled lanes in, and
-                    // list u once
-                    if constexpr (W == 1) found = LS<W, NB>::atomic_or_first(Fn, u, res.w[0]);
-                } else {
-                    LS<W, NB>::store_stream(Fn, u, res);
-                }
-            }
+            if (found) LS<W, NB>::store_stream(Fn, u, res);
         }
         acc.candidates += cand;
         acc.scanned += scanned;
         bool left = false;
 #pragma unroll
         for (int i = 0; i < W; ++i) left |= (need.w[i] & ~acc_w.w[i]) != 0;
-        st.push(found && !split, u);  // split: the list pass lists every discovery
+        st.push(found, u);
         if (st.full()) {
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
@@ -723,14 +623,12 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             u = task.x;
             ty = task.y;
             tb = __ldg(g.cp + u);
-            if (split && ty >= __ldg(g.hub_end + u)) ty = kFull;  // a chunk past the hub prefix
             vis = LS<W, NB>::load(P.V, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
                 cand |= need.w[i] != 0;
             }
-            if (ty == kFull) cand = false;
             if (cand && ty != tb) {
                 // a later chunk: only the lanes the earlier chunks of u have not
                 // found yet; none left -> nothing to scan
@@ -766,14 +664,14 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                     for (int i = 0; i < W; ++i) need.w[i] = nj.w[i];
                 }
             }
-            const uint32_t e = min(yj + kHeavyChunk, split ? __ldg(g.hub_end + uj) : __ldg(g.cp + uj + 1));
+            const uint32_t e = min(yj + kHeavyChunk, __ldg(g.cp + uj + 1));
             uint32_t sc = 0;
             const LaneWord<W> aj = warp_pull_range<W, NB>(P, Fc, yj, e, nj, sc);
             if ((int)lane == j) {
                 acc.scanned += sc;
                 acc.candidates += ty == tb;
-                // several chunks of one vertex (and, in a mixed hop, pushing
-                // lanes) OR into its word: the first to find it empty lists it
+                // several chunks of one vertex OR into its word: the first to
+                // find it empty lists it
                 if constexpr (W == 1) {
                     const unsigned long long r = aj.w[0] & need.w[0];
                     if (r) first = LS<W, NB>::atomic_or_first(Fn, u, r);
@@ -794,7 +692,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 }
             }
         }
-        st.push(first && !split, u);
+        st.push(first, u);
         if (st.full()) {
             emit_list(st.buf, st.n, Rn, &qn->nitems);
             st.n = 0;
@@ -811,8 +709,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
-                               uint32_t warp_gid, uint32_t nwarps, unsigned long long* s_E = nullptr,
-                               unsigned long long* s_mu = nullptr, bool dense = false) {
+                               uint32_t warp_gid, uint32_t nwarps, bool dense = false) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // dense (a list of more than n/8, one word per vertex): sweep every vertex
@@ -820,9 +717,6 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
     // words, CSR / CSC bounds) issued at once and coalesced -- one round trip
     // per vertex instead of two dependent ones; the discovered vertices are
     // those with a non-zero new word. The list itself stays as built.
-    // per-lane Beamer inputs (W = 1): lane l of the warp sums lanes l and 32 + l
-    constexpr uint32_t LBs = W == 1 ? LS<W, NB>::kLanes : 0;
-    unsigned long long eA[2] = {0, 0}, mA[2] = {0, 0};
     LaneWord<W> act;
     uint32_t cnt_lo[W], cnt_hi[W];
 #pragma unroll
@@ -834,7 +728,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
     for (uint32_t base = warp_gid * 32; base < lim; base += nwarps * 32) {
         const uint32_t idx = base + lane;
         bool valid = idx < lim;
-        uint32_t u = 0, deg_of = 0, indeg_of = 0;
+        uint32_t u = 0;
         LaneWord<W> x, v;
 #pragma unroll
         for (int i = 0; i < W; ++i) x.w[i] = v.w[i] = 0;
@@ -881,7 +775,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                 atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
             // (a dense sweep writes no copy: the batch's V is then cleared by streaming)
             if (!dense && clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
-            const bool need_in = fresh || (LBs > 0 && s_E);
+            const bool need_in = fresh;
             if (!dense) {
                 r0 = __ldg(g.rp + u);
                 r1 = __ldg(g.rp + u + 1);
@@ -898,24 +792,6 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             acc.pairs += pc;
             acc.pe += (unsigned long long)deg * pc;
             expand = want_items && deg > 0;
-            indeg_of = indeg;
-            deg_of = deg;
-        }
-        if constexpr (LBs > 0) {
-            // lane b's frontier out-edges and newly visited in-edges, one
-            // warp reduction per lane bit
-            if (s_E && __ballot_sync(kFull, x.w[0] != 0)) {
-#pragma unroll 4
-                for (uint32_t bb = 0; bb < LBs; ++bb) {
-                    const bool on = (x.w[0] >> bb) & 1ull;
-                    const uint32_t se = __reduce_add_sync(kFull, on ? deg_of : 0u);
-                    const uint32_t sm = __reduce_add_sync(kFull, on ? indeg_of : 0u);
-                    if (lane == (bb & 31)) {
-                        eA[bb >> 5] += se;
-                        mA[bb >> 5] += sm;
-                    }
-                }
-            }
         }
         if (count_lanes) {
             // column popcounts: lane l accumulates bit l (cnt_lo) and bit 32+l
@@ -963,16 +839,6 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             if (NB == 64 && cnt_hi[i]) atomicAdd(&s_cnt[i * 64 + 32 + lane], (unsigned long long)cnt_hi[i]);
         }
     }
-    if constexpr (LBs > 0) {
-        if (s_E) {
-#pragma unroll
-            for (uint32_t h = 0; h < 2; ++h)
-                if (h * 32 + lane < LBs) {
-                    if (eA[h]) atomicAdd(&s_E[h * 32 + lane], eA[h]);
-                    if (mA[h]) atomicAdd(&s_mu[h * 32 + lane], mA[h]);
-                }
-        }
-    }
 }
 
 // next-hop push items for the frontier vertices with a pushing lane (after the
@@ -980,7 +846,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
 template <int W, int NB>
 MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
                            const LaneWord<W>& pushm, uint4* items_n, unsigned int* item_tail, Stage<kStageCap>& st,
-                           uint32_t warp_gid, uint32_t nwarps, uint32_t max_deg = kFull) {
+                           uint32_t warp_gid, uint32_t nwarps) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
@@ -992,8 +858,7 @@ MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, co
             const LaneWord<W> x = LS<W, NB>::load(Fn, u);
 #pragma unroll
             for (int i = 0; i < W; ++i) expand |= (x.w[i] & pushm.w[i]) != 0;
-            const uint32_t deg = __ldg(g.rp + u + 1) - __ldg(g.rp + u);
-            expand = expand && deg > 0 && deg < max_deg;
+            expand = expand && __ldg(g.rp + u + 1) > __ldg(g.rp + u);
         }
         st.push(expand, u);
         if (st.full()) {
@@ -1048,10 +913,6 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
     constexpr uint32_t LB = LS<W, NB>::kLanes;
     __shared__ uint32_t s_stage[kWarps][kStageCap];
     __shared__ unsigned long long s_cnt[LB];
-    // per-lane Beamer inputs (W = 1 only) and the decided pull-lane mask
-    constexpr uint32_t LBs = W == 1 ? LB : 1;
-    __shared__ unsigned long long s_E[LBs], s_mu[LBs];
-    __shared__ uint32_t s_pm[2];
     __shared__ uint32_t s_nm[kWarps][32];  // pull: unsettled-vertex masks of a warp's 32 words
     __shared__ uint32_t s_cb[kWarps][64];  // pull: a warp's waiting candidates
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
@@ -1071,10 +932,6 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
         for (uint32_t i = gtid; i < (P.k + 1) * LB; i += nthreads) P.lane_cnt[i] = 0;
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
-        if (P.perlane && gtid < LB) {
-            P.lane_E[gtid] = P.lane_E[LB + gtid] = 0;
-            P.lane_mu[gtid] = g.m;
-        }
         if (gtid == 0) {
             P.misc[0] = g.m;
             P.misc[1] = P.misc[2] = 0;  // pull work counters
@@ -1112,19 +969,15 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
         for (int i = 0; i < W; ++i) pullm.w[i] = P.force_dir == 2 ? ~0ull : 0ull;
         const bool pull0 = P.force_dir == 2;
         for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;  // (LB may exceed the block)
-        if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
         __syncthreads();
         finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull0, P.items0, &P.qctl[0].nfound, false,
-                          s_cnt, P.active, 0, acc, st, warp_gid, nwarps, P.perlane ? s_E : nullptr, s_mu);
+                          s_cnt, P.active, 0, acc, st, warp_gid, nwarps);
         __syncthreads();
-        if (P.perlane && threadIdx.x < LB && s_mu[threadIdx.x])
-            atomicAdd(&P.lane_mu[threadIdx.x], 0ull - s_mu[threadIdx.x]);
         acc.pairs = 0;  // the seeds themselves are never counted
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
         grid_barrier(P.bar);
 
         bool prev_pull = false;  // the hop before pulled: its unsettled words bound this pull's
-        bool split = false;      // this hop is a split pull (its push items were emitted by the hop before)
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
         uint32_t hop = 1;
@@ -1154,25 +1007,16 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
                 atomicAdd(&P.lc[hop].union_edges, ld_volatile(&qc->edges));
             }
             if (gtid < W) P.active[nxt * W + gtid] = 0;  // rebuilt by this hop's finalize
-            // ---- expand: pushing lanes from the frontier's items, pulling lanes
-            // over the CSC (both in one phase: disjoint lanes, and a vertex both
-            // reach is listed once through its touched bit) -------------------------
+            // ---- expand: a push from the frontier's items or a pull over the CSC -----
             if (anypush)
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
             // a pull after a pull visits only the vertices that pull left unsettled
             if (anypull)
-                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps, anypush,
-                                  (!P.perlane && prev_pull) ? P.umask + (size_t)cur * g.nwords : nullptr,
-                                  P.perlane ? nullptr : P.umask + (size_t)nxt * g.nwords, split,
+                pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps,
+                                  prev_pull ? P.umask + (size_t)cur * g.nwords : nullptr,
+                                  P.umask + (size_t)nxt * g.nwords,
                                   s_nm[threadIdx.x >> 5], s_cb[threadIdx.x >> 5]);
-            if (split) {
-                grid_barrier(P.bar);
-                split_push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, acc, warp_gid,
-                                        nwarps);
-                grid_barrier(P.bar);
-                split_list_phase<W, NB>(P, Fn, Rn, qn, st, gtid, nthreads);
-            }
             prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
@@ -1180,57 +1024,26 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             if (P.diag && gtid == 0) t1 = globaltimer();
             nR = ld_volatile(&qn->nitems);
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
-            if (P.perlane && gtid < LB) P.lane_E[nxt * LB + gtid] = 0;  // (parity of the hop before: read)
             const bool last = hop == P.k || nR == 0;
-            const bool count_lanes = hop >= P.min_hop || P.perlane;
+            const bool count_lanes = hop >= P.min_hop;
             // ---- finalize -------------------------------------------------------------
             for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;
-            if (threadIdx.x < LBs) s_E[threadIdx.x] = s_mu[threadIdx.x] = 0;
             if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
             __syncthreads();
             finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
-                              (P.perlane && !last) ? s_E : nullptr, s_mu,
-                              W == 1 && !P.perlane && (uint64_t)nR * 8 > g.n);
+                              W == 1 && (uint64_t)nR * 8 > g.n);
             clear_words<W, NB>(Rc, nR_prev, Fc, g.n, gtid, nthreads);
             __syncthreads();
             if (count_lanes)
                 for (uint32_t t = threadIdx.x; t < LB; t += kBlock)
                     if (s_cnt[t]) atomicAdd(&P.lane_cnt[hop * LB + t], s_cnt[t]);
-            if (P.perlane && threadIdx.x < LB) {
-                if (s_E[threadIdx.x]) atomicAdd(&P.lane_E[nxt * LB + threadIdx.x], s_E[threadIdx.x]);
-                if (s_mu[threadIdx.x]) atomicAdd(&P.lane_mu[threadIdx.x], 0ull - s_mu[threadIdx.x]);
-            }
             block_flush(acc, qn, qn, &P.lc[hop], hop < P.k ? &P.lc[hop + 1] : nullptr,
                         &P.misc[0]);
             grid_barrier(P.bar);
             // ---- the next hop's directions (every CTA computes the same) ---------------
-            bool split_next = false;
             if (!last) {
-                if (P.perlane) {
-                    // lane l: push -> pull when its frontier's out-edges x alpha exceed
-                    // its unexplored in-edges; pull -> push when its frontier x beta < n
-                    if (threadIdx.x < 64) {
-                        const uint32_t l = threadIdx.x;
-                        bool pl = false;
-                        if (l < LB) {
-                            const unsigned long long cnt = ld_cg(&P.lane_cnt[hop * LB + l]);
-                            if (cnt) {
-                                if (P.force_dir)
-                                    pl = P.force_dir == 2;
-                                else if ((pullm.w[0] >> l) & 1ull)
-                                    pl = cnt * P.beta >= g.n;
-                                else
-                                    pl = ld_cg(&P.lane_E[nxt * LB + l]) * P.alpha > ld_cg(&P.lane_mu[l]);
-                            }
-                        }
-                        const uint32_t b = __ballot_sync(kFull, pl);
-                        if (lane_id() == 0) s_pm[threadIdx.x >> 5] = b;
-                    }
-                    __syncthreads();
-                    pullm.w[0] = ((unsigned long long)s_pm[1] << 32) | s_pm[0];
-                    __syncthreads();
-                } else {
+                {
                     // (the finalize counted the new frontier's out-edges and the
                     // in-edges that left the unexplored set)
                     const unsigned long long mf = ld_volatile(&qn->edges);
@@ -1242,27 +1055,22 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
                         pn = true;
                     } else if (!anypull) {
                         pn = mf * P.alpha > mu;
-                        // the first pull after pushes is split by source out-degree
-                        // (one word per vertex; forced directions keep whole pulls)
-                        split_next = W == 1 && pn && g.hub_deg > 0 && g.hub_end != nullptr;
                     } else {
                         pn = (unsigned long long)nR * P.beta >= g.n;
                     }
 #pragma unroll
                     for (int i = 0; i < W; ++i) pullm.w[i] = pn ? ~0ull : 0ull;
                 }
-                // items for the lanes pushing next (a split pull: the frontier
-                // vertices below hub_deg, all lanes)
+                // items for the lanes pushing next
                 LaneWord<W> pn_push;
                 bool anyn = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & (split_next ? ~0ull : ~pullm.w[i]);
+                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & ~pullm.w[i];
                     anyn |= pn_push.w[i] != 0;
                 }
                 if (anyn) {
-                    emit_phase<W, NB>(P, Rn, nR, Fn, pn_push, items_of(P, nxt), &qn->nfound, st, warp_gid, nwarps,
-                                      split_next ? g.hub_deg : kFull);
+                    emit_phase<W, NB>(P, Rn, nR, Fn, pn_push, items_of(P, nxt), &qn->nfound, st, warp_gid, nwarps);
                     grid_barrier(P.bar);
                 }
             }
@@ -1276,7 +1084,6 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
             }
             clog_used += nR;
             nR_prev = nR;
-            split = split_next;
             if (nR == 0) break;
         }
         // ---- answers ------------------------------------------------------------------
@@ -1369,13 +1176,6 @@ cudaError_t launch_w(Launch& L) {
         return e && e[0] == '1' ? 1u : 0u;
     }();
     P.diag = diag;
-    // per-lane directions are opt-in: measured slower (a push entry costs several
-    // pull entries here, so the lanes that keep pushing at the dense hop cost
-    // more than the pull scans they save)
-    static const bool perlane = std::getenv("MGK_LANES_PERLANE") != nullptr;
-    P.perlane = (W == 1 && perlane) ? 1u : 0u;
-    P.lane_E = ws->lane_stat;
-    P.lane_mu = ws->lane_stat + 2 * 512;
     P.umask = ws->umask;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
@@ -1417,7 +1217,6 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
     }
     if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
-    if (!ws->lane_stat && (e = cudaMalloc(&ws->lane_stat, 3 * 512 * 8))) return e;
     if (!ws->umask && (e = cudaMalloc(&ws->umask, 2 * ((size_t)g.nwords + 32) * 4))) return e;
     ws->bytes += 3 * words * 8;
     if (!ws->touched) {
