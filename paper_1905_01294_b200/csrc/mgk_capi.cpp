@@ -178,17 +178,17 @@ int pick_words(const Graph* g, uint64_t nseeds) {
     return W;
 }
 
-// LANES lane-word width: batches of at most 8 / 16 seeds use one uint8 /
-// uint16 word per vertex (state arrays 8x / 4x smaller, so a dense pull's
-// per-edge gathers stay in L2 on large graphs); wider batches use uint64
-// words. MGK_LANE_BITS=8|16|64 forces a width (tests; a forced narrow width
-// wider batches cannot use falls back to 64).
+// LANES lane-word width: batches of at most 8 / 10 / 16 seeds use one uint8 /
+// 10-bit (three per uint32) / uint16 word per vertex (state arrays 8x / 6x /
+// 4x smaller, so a dense pull's per-edge gathers stay in L2 on large graphs);
+// wider batches use uint64 words. MGK_LANE_BITS=8|10|16|64 forces a width
+// (tests; a forced narrow width wider batches cannot use falls back to 64).
 int pick_lane_bits(const Graph* g, uint64_t nseeds) {
     if (g->tuning.lanes_words) return 64;
-    int bits = nseeds <= 8 ? 8 : nseeds <= 16 ? 16 : 64;
+    int bits = nseeds <= 8 ? 8 : nseeds <= 10 ? 10 : nseeds <= 16 ? 16 : 64;
     if (const char* e = std::getenv("MGK_LANE_BITS")) {
         const int f = std::atoi(e);
-        if (f == 8 || f == 16 || f == 64) bits = f;
+        if (f == 8 || f == 10 || f == 16 || f == 64) bits = f;
     }
     return (bits < 64 && nseeds > (uint64_t)bits) ? 64 : bits;
 }

@@ -44,7 +44,7 @@ constexpr int kBlock = MGK_MS_BLOCK;
 #define MGK_LIGHT_STEP 4
 #endif
 #ifndef MGK_PRE
-#define MGK_PRE 8
+#define MGK_PRE 16
 #endif
 #ifndef MGK_WPR_UNROLL  // warp-cooperative in-list scans: entries per lane in flight
 #define MGK_WPR_UNROLL 2
@@ -260,6 +260,70 @@ template <>
 struct LS<1, 16> : LSNarrow<16> {};
 template <>
 struct LS<1, 8> : LSNarrow<8> {};
+
+// NB = 10: three 10-bit lane words per 32-bit word (batches of 9 or 10 seeds:
+// the reference schedule's deep sections). G4's state arrays are then 47 MB
+// instead of 71 MB -- under the ~64 MB where random loads fall off L2
+// (profiles/ubench_atomics.json: 214 G/s at 64 MB, 163 G/s at 90 MB).
+// Neighbouring vertices share a 32-bit word, so every write is an atomic on
+// it (OR to set, AND to clear); reads extract the field.
+template <>
+struct LS<1, 10> {
+    static constexpr uint32_t kLanes = 10;
+    static constexpr uint32_t kMask = 0x3FFu;
+    __device__ static __forceinline__ uint32_t word(size_t v) { return __umulhi((uint32_t)v, 0xAAAAAAABu) >> 1; }
+    __device__ static __forceinline__ uint32_t shift(size_t v) { return 10u * ((uint32_t)v - 3u * word(v)); }
+    __device__ static __forceinline__ unsigned int* at(unsigned long long* b, size_t v) {
+        return reinterpret_cast<unsigned int*>(b) + word(v);
+    }
+    __device__ static __forceinline__ const unsigned int* at(const unsigned long long* b, size_t v) {
+        return reinterpret_cast<const unsigned int*>(b) + word(v);
+    }
+    __device__ static __forceinline__ LaneWord<1> load(const unsigned long long* b, size_t v) {
+        LaneWord<1> r;
+        r.w[0] = (*at(b, v) >> shift(v)) & kMask;
+        return r;
+    }
+    __device__ static __forceinline__ LaneWord<1> load_cg(const unsigned long long* b, size_t v) {
+        LaneWord<1> r;
+        r.w[0] = (__ldcg(at(b, v)) >> shift(v)) & kMask;
+        return r;
+    }
+    __device__ static __forceinline__ LaneWord<1> gather(const unsigned long long* b, size_t v,
+                                                         unsigned long long pol) {
+        uint32_t w;
+        asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(w) : "l"(at(b, v)), "l"(pol));
+        LaneWord<1> r;
+        r.w[0] = (w >> shift(v)) & kMask;
+        return r;
+    }
+    // x holds every lane of v's word: the bits not yet set are OR-ed in, and a
+    // zero word clears the field (the callers' only two cases)
+    __device__ static __forceinline__ void store(unsigned long long* b, size_t v, const LaneWord<1>& x) {
+        if (x.w[0])
+            atomicOr(at(b, v), (unsigned int)x.w[0] << shift(v));
+        else
+            atomicAnd(at(b, v), ~(kMask << shift(v)));
+    }
+    __device__ static __forceinline__ void store_stream(unsigned long long* b, size_t v, const LaneWord<1>& x) {
+        store(b, v, x);
+    }
+    __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int, unsigned long long m) {
+        atomicOr(at(b, v), (unsigned int)m << shift(v));
+    }
+    __device__ static __forceinline__ bool atomic_or_first(unsigned long long* b, size_t v, unsigned long long m) {
+        const uint32_t sh = shift(v);
+        const unsigned int old = atomicOr(at(b, v), (unsigned int)m << sh);
+        return ((old >> sh) & kMask) == 0;
+    }
+    __host__ __device__ static constexpr size_t words64(size_t n) { return ((n + 2) / 3 + 1) / 2; }
+};
+
+// bytes of one narrow lane-word array for n vertices
+template <int W, int NB>
+constexpr size_t narrow_bytes(size_t n) {
+    return NB == 64 ? 0 : LS<W, NB>::words64(n) * 8;
+}
 
 
 __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
@@ -734,24 +798,22 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
         for (int i = 0; i < W; ++i) x.w[i] = v.w[i] = 0;
         uint32_t r0 = 0, r1 = 0, c0 = 0, c1 = 0;
         bool expand = false;
-        if (dense) {
-            if (valid) {
-                u = idx;
-                x = LS<W, NB>::load(Fn, u);
-                v = LS<W, NB>::load(P.V, u);
-                r0 = __ldg(g.rp + u);
-                r1 = __ldg(g.rp + u + 1);
-                c0 = __ldg(g.cp + u);
-                c1 = __ldg(g.cp + u + 1);
+        // all of a vertex's loads at once (the stores below would otherwise
+        // keep the bounds' loads behind them)
+        if (valid) {
+            u = dense ? idx : Rn[idx];
+            x = LS<W, NB>::load(Fn, u);
+            v = LS<W, NB>::load(P.V, u);
+            r0 = __ldg(g.rp + u);
+            r1 = __ldg(g.rp + u + 1);
+            c0 = __ldg(g.cp + u);
+            c1 = __ldg(g.cp + u + 1);
+            if (dense) {
                 bool any = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
                 valid = any;
             }
-        } else if (valid) {
-            u = Rn[idx];
-            x = LS<W, NB>::load(Fn, u);
-            v = LS<W, NB>::load(P.V, u);
         }
         if (valid) {
             bool fresh = true;  // no lane had visited u: its in-edges leave the unexplored set
@@ -764,7 +826,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                 act.w[i] |= x.w[i];
                 pc += __popcll(x.w[i]);
             }
-            LS<W, NB>::store(P.V, u, v);
+            if (NB != 10 || mark_visited) LS<W, NB>::store(P.V, u, v);
             // push levels set a touched bit per discovery; pull levels only for
             // heavy vertices (discovered vertices in pull_skip are heavy: a
             // zero-in-degree vertex is never discovered)
@@ -775,17 +837,8 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                 atomicAnd(P.touched + (u >> 5), ~(1u << (u & 31)));
             // (a dense sweep writes no copy: the batch's V is then cleared by streaming)
             if (!dense && clog_base + idx < P.clog_cap) P.clog[clog_base + idx] = u;
-            const bool need_in = fresh;
-            if (!dense) {
-                r0 = __ldg(g.rp + u);
-                r1 = __ldg(g.rp + u + 1);
-                if (need_in) {
-                    c0 = __ldg(g.cp + u);
-                    c1 = __ldg(g.cp + u + 1);
-                }
-            }
             const uint32_t deg = r1 - r0;
-            const uint32_t indeg = need_in ? c1 - c0 : 0;
+            const uint32_t indeg = fresh ? c1 - c0 : 0;
             acc.found += 1;  // distinct vertices discovered, their out-edges, fresh in-edges
             acc.edges += deg;
             if (fresh) acc.indeg += indeg;
@@ -1155,7 +1208,7 @@ cudaError_t launch_w(Launch& L) {
     // narrow words: both frontier arrays inside lf[0]'s allocation (n uint64
     // words hold 8 / NB * ... of them), adjacent, so one L2 window covers them
     static const bool separate = std::getenv("MGK_F1_SEPARATE") != nullptr;  // A/B of the layout
-    const size_t fbytes = NB < 64 ? ((size_t)gr->dg.n * NB / 8 + 255) / 256 * 256 : 0;
+    const size_t fbytes = (narrow_bytes<W, NB>(gr->dg.n) + 255) / 256 * 256;
     if (NB < 64 && !separate)
         P.F1 = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ws->lf[0]) + fbytes);
     P.touched = ws->touched;
@@ -1239,6 +1292,7 @@ cudaError_t launch_lanes(Launch& L) {
     cudaError_t e = ensure_lanes_ws(L.g, L.ws, W);
     if (e) return e;
     if (L.lane_bits == 16) return launch_w<1, 16>(L);
+    if (L.lane_bits == 10) return launch_w<1, 10>(L);
     if (L.lane_bits == 8) return launch_w<1, 8>(L);
     switch (W) {
         case 1: return launch_w<1, 64>(L);

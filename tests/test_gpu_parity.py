@@ -154,6 +154,27 @@ def test_directions_and_lane_widths(port, g1, force, words):
         g.set_tuning(Tuning())
 
 
+@pytest.mark.parametrize("force", [0, 1, 2])
+def test_narrow_lane_words(port, g1, force, monkeypatch):
+    """Batches of <= 8 / 10 / 16 seeds use 8-bit, 10-bit (three per 32-bit
+    word, atomics for every write) and 16-bit lane words; each width, forced
+    with MGK_LANE_BITS, and the 64-bit words give the oracle's counts."""
+    rp, ci, g = g1
+    seeds = H.pick_seeds(rp, 60, 11)
+    groups = [seeds[0:10], seeds[10:20], seeds[20:29], seeds[29:37], seeds[37:38]]
+    want = {(j, k, m): oracle_counts(port, rp, ci, grp, k, m)
+            for j, grp in enumerate(groups) for k in (1, 2, 3, 6) for m in (0, 1)}
+    try:
+        g.set_tuning(Tuning(force_dir=force))
+        for bits in ("8", "10", "16", "64"):
+            monkeypatch.setenv("MGK_LANE_BITS", bits)
+            for (j, k, m), w in want.items():
+                got = k_hop_count_batch(g, groups[j], k, m, engine=ENGINE_LANES).tolist()
+                assert got == w, (bits, j, k, m)
+    finally:
+        g.set_tuning(Tuning())
+
+
 def test_duplicate_and_isolated_seeds(port, g1):
     rp, ci, g = g1
     deg = np.diff(rp.astype(np.int64))
