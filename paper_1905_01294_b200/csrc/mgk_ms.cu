@@ -52,6 +52,7 @@ constexpr int kBlock = MGK_MS_BLOCK;
 constexpr int kWprUnroll = MGK_WPR_UNROLL;
 
 
+
 // a lane's own in-list (read a few entries at a time by the same lane: its
 // 32-byte sectors are re-read until the list is done, so by default they keep
 // normal L2 priority; MGK_RI_LIGHT_STREAM marks them evict-first too)
@@ -305,8 +306,12 @@ struct LS<1, 10> {
         else
             atomicAnd(at(b, v), ~(kMask << shift(v)));
     }
+    // the pull's next-frontier write (the field is zero): an OR at L2 evict-first
+    // priority, so it does not displace the frontier words the gathers need
     __device__ static __forceinline__ void store_stream(unsigned long long* b, size_t v, const LaneWord<1>& x) {
-        store(b, v, x);
+        asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(at(b, v)),
+                     "r"((unsigned int)x.w[0] << shift(v)), "l"(l2_stream_policy())
+                     : "memory");
     }
     __device__ static __forceinline__ void atomic_or(unsigned long long* b, size_t v, int, unsigned long long m) {
         atomicOr(at(b, v), (unsigned int)m << shift(v));
@@ -529,16 +534,13 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
     // one candidate per lane (valid): visited word, CSC bounds, the lane's scan
     // of a short list (or the first kPre entries), the warp's scans of the
     // unsettled longer lists, the next-frontier store; true when lanes are left
-    auto visit = [&](bool valid, uint32_t u, bool& found) -> bool {
-        LaneWord<W> need, vis;
+    // (the candidate's visited word and CSC bounds are loaded by the caller)
+    auto visit = [&](bool valid, uint32_t u, const LaneWord<W>& vis, uint32_t b, uint32_t e, bool& found) -> bool {
+        LaneWord<W> need;
 #pragma unroll
-        for (int i = 0; i < W; ++i) need.w[i] = vis.w[i] = 0;
+        for (int i = 0; i < W; ++i) need.w[i] = 0;
         bool cand = false;
-        uint32_t b = 0, e = 0;
         if (valid) {
-            vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
-            b = __ldg(g.cp + u);
-            e = __ldg(g.cp + u + 1);
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 need.w[i] = active.w[i] & ~vis.w[i];
@@ -654,8 +656,17 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
         if (fill > 32 && lane < fill - 32) s_cb[lane] = s_cb[32 + lane];
         fill = fill > 32 ? fill - 32 : 0;
         __syncwarp();
+        LaneWord<W> vis;
+#pragma unroll
+        for (int i = 0; i < W; ++i) vis.w[i] = 0;
+        uint32_t b = 0, e = 0;
+        if (valid) {
+            vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
+            b = ldg_hint(g.cp + u, pol_ri);
+            e = ldg_hint(g.cp + u + 1, pol_ri);
+        }
         bool found;
-        if (visit(valid, u, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
+        if (visit(valid, u, vis, b, e, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
     }
     __syncwarp();
     if (um_out && wq < wend) um_out[wq] = s_nm[lane];
