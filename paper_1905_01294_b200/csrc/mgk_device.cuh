@@ -19,7 +19,7 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 // the streamed adjacency (loaded evict-first) until the cleanup pass.
 __device__ __forceinline__ unsigned long long l2_keep_policy() {
     unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 __device__ __forceinline__ void red_or_keep(uint32_t* p, uint32_t v, unsigned long long pol) {
@@ -36,7 +36,7 @@ __device__ __forceinline__ uint32_t atom_or_keep(uint32_t* p, uint32_t v, unsign
 // scans), so it does not push the frontier words out of L2.
 __device__ __forceinline__ unsigned long long l2_stream_policy() {
     unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
 // immutable graph arrays: non-coherent path, L1-allocating, L2 priority `pol`

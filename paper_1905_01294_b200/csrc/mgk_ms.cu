@@ -479,7 +479,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
                                                        uint32_t b, uint32_t e,
                                                        const LaneWord<W>& need, uint32_t& scanned) {
     const uint32_t lane = lane_id();
-    const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
+    // (the L2 policies are re-created at each load: one instruction, no live 64-bit registers)
     LaneWord<W> acc;
 #pragma unroll
     for (int i = 0; i < W; ++i) acc.w[i] = 0;
@@ -491,7 +491,7 @@ __device__ __forceinline__ LaneWord<W> warp_pull_range(const MSParams& P, const 
         const uint32_t pe = min(e, p0 + blk);
 #pragma unroll kWprUnroll
         for (uint32_t p = p0 + lane; p < pe; p += 32) {
-            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, pol_ri), pol_f);
+            const LaneWord<W> f = LS<W, NB>::gather(Fc, ldg_hint(P.g.ri + p, l2_stream_policy()), l2_keep_policy());
 #pragma unroll
             for (int i = 0; i < W; ++i) acc.w[i] |= f.w[i];
         }
@@ -528,7 +528,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
     const DevGraph& g = P.g;
     // candidate words in chunks, spread dynamically (misc[1]); about 8
     // chunks per warp, at least 8 words each, so the counter stays cold
-    const unsigned long long pol_ri = l2_stream_policy(), pol_f = l2_keep_policy();
+    // (the L2 policies are re-created at each load: one instruction, no live 64-bit registers)
     const uint32_t wchunk = max(8u, g.nwords / (nwarps * 8));
     ChunkGrab words(&P.misc[1], g.nwords, wchunk, warp_gid);
     // one candidate per lane (valid): visited word, CSC bounds, the lane's scan
@@ -564,10 +564,10 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             for (; p + kStep <= stop && !done; p += kStep) {
                 uint32_t v[kStep];
 #pragma unroll
-                for (uint32_t q = 0; q < kStep; ++q) v[q] = ld_ri_lane(g.ri + p + q, pol_ri);
+                for (uint32_t q = 0; q < kStep; ++q) v[q] = ld_ri_lane(g.ri + p + q, l2_stream_policy());
 #pragma unroll
                 for (uint32_t q = 0; q < kStep; ++q) {
-                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], pol_f);
+                    const LaneWord<W> f = LS<W, NB>::gather(Fc, v[q], l2_keep_policy());
 #pragma unroll
                     for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 }
@@ -575,7 +575,7 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
                 scanned += kStep;
             }
             for (; !done && p < stop; ++p) {
-                const LaneWord<W> f = LS<W, NB>::gather(Fc, ld_ri_lane(g.ri + p, pol_ri), pol_f);
+                const LaneWord<W> f = LS<W, NB>::gather(Fc, ld_ri_lane(g.ri + p, l2_stream_policy()), l2_keep_policy());
 #pragma unroll
                 for (int i = 0; i < W; ++i) acc_w.w[i] |= f.w[i];
                 ++scanned;
@@ -661,9 +661,9 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
         for (int i = 0; i < W; ++i) vis.w[i] = 0;
         uint32_t b = 0, e = 0;
         if (valid) {
-            vis = LS<W, NB>::gather(P.V, u, pol_ri);  // read once per pull: evict-first
-            b = ldg_hint(g.cp + u, pol_ri);
-            e = ldg_hint(g.cp + u + 1, pol_ri);
+            vis = LS<W, NB>::gather(P.V, u, l2_stream_policy());  // read once per pull: evict-first
+            b = ldg_hint(g.cp + u, l2_stream_policy());
+            e = ldg_hint(g.cp + u + 1, l2_stream_policy());
         }
         bool found;
         if (visit(valid, u, vis, b, e, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
@@ -962,14 +962,19 @@ __device__ void clear_words(const uint32_t* R, uint32_t nlist, unsigned long lon
 
 // resident CTAs per SM the register budget is sized for, per instance: one
 // word per vertex runs best at 48 registers and 40 warps per SM (more warps to
-// hide the gathers' latency), wide words keep their registers
-template <int W>
+// hide the gathers' latency), wide words keep their registers. Narrow words
+// on graphs whose lane-word arrays outgrow L2's fast range (kWideState) get a
+// 40-register / 48-warp instance: their dense pull waits on gathers that miss
+// L2 more often, and more warps in flight hide it (G4 10 seeds k=6: 5.16 ->
+// 4.96 ms), while on small graphs the extra spills cost more (G2 +7 %).
+template <int W, int MB>
 constexpr int ms_min_blocks() {
-    return MGK_MS_MINB > 0 ? MGK_MS_MINB : (W == 1 ? 5 * 256 / kBlock : 512 / kBlock);
+    return MGK_MS_MINB > 0 ? MGK_MS_MINB : (W == 1 ? MB * 256 / kBlock : 512 / kBlock);
 }
+constexpr size_t kWideState = 16u << 20;
 
-template <int W, int NB>
-__global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams P) {
+template <int W, int NB, int MB>
+__global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSParams P) {
     grid_barrier_init(P.bar);
     // qctl[parity] fields in this engine:
     //   nitems = |R| (discovery list tail), nfound = push items built for the
@@ -1182,7 +1187,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W>()) ms_kernel(MSParams
     }
 }
 
-template <int W, int NB>
+template <int W, int NB, int MB>
 cudaError_t launch_w(Launch& L) {
     static int blocks_per_sm = 0, num_sms = 0;
     cudaError_t e;
@@ -1190,7 +1195,7 @@ cudaError_t launch_w(Launch& L) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W, NB>, kBlock,
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, ms_kernel<W, NB, MB>, kBlock,
                                                                 0)))
             return e;
         if (blocks_per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -1253,9 +1258,9 @@ cudaError_t launch_w(Launch& L) {
         return v && v[0] == '1';
     }();
     if (persist && NB < 64)
-        return launch_persistent_l2((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream, ws->lf[0],
+        return launch_persistent_l2((const void*)ms_kernel<W, NB, MB>, L.grid, kBlock, args, L.stream, ws->lf[0],
                                     2 * fbytes);
-    return launch_persistent((const void*)ms_kernel<W, NB>, L.grid, kBlock, args, L.stream);
+    return launch_persistent((const void*)ms_kernel<W, NB, MB>, L.grid, kBlock, args, L.stream);
 }
 
 }  // namespace
@@ -1302,14 +1307,17 @@ cudaError_t launch_lanes(Launch& L) {
     int W = L.lanes_words;
     cudaError_t e = ensure_lanes_ws(L.g, L.ws, W);
     if (e) return e;
-    if (L.lane_bits == 16) return launch_w<1, 16>(L);
-    if (L.lane_bits == 10) return launch_w<1, 10>(L);
-    if (L.lane_bits == 8) return launch_w<1, 8>(L);
+    const uint32_t n = L.g->dg.n;
+    if (L.lane_bits == 16)
+        return narrow_bytes<1, 16>(n) > kWideState ? launch_w<1, 16, 6>(L) : launch_w<1, 16, 5>(L);
+    if (L.lane_bits == 10)
+        return narrow_bytes<1, 10>(n) > kWideState ? launch_w<1, 10, 6>(L) : launch_w<1, 10, 5>(L);
+    if (L.lane_bits == 8) return launch_w<1, 8, 5>(L);
     switch (W) {
-        case 1: return launch_w<1, 64>(L);
-        case 2: return launch_w<2, 64>(L);
-        case 4: return launch_w<4, 64>(L);
-        case 8: return launch_w<8, 64>(L);
+        case 1: return launch_w<1, 64, 5>(L);
+        case 2: return launch_w<2, 64, 5>(L);
+        case 4: return launch_w<4, 64, 5>(L);
+        case 8: return launch_w<8, 64, 5>(L);
         default: return cudaErrorInvalidValue;
     }
 }
