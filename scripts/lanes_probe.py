@@ -66,7 +66,8 @@ def run(gname, bits_list, reps=5):
             st = device_stats(g, s.cuda_stream)
             diag = os.environ.get("MGK_MS_DIAG") == "1"
             hops = [(h, "pull" if L["pull_runs"] else "push", L["scanned"], round(L["ns"] / 1e3, 1)) +
-                    ((round(L["union_edges"] / 1e3, 1), round(L["candidates"] / 1e3, 1)) if diag else ())
+                    ((round(L["union_edges"] / 1e3, 1), round(L["candidates"] / 1e3, 1),
+                      round(L["edges"] / 1e3, 1)) if diag else ())
                     for h, L in enumerate(st["levels"]) if h and L["runs"]]
             out[f"{gname}_b{bits}_k{k}"] = {"ms": float(np.median(ts)), "lanes": st["lanes"], "hops": hops}
             print(f"{gname} bits={bits} k={k}: {np.median(ts):.3f} ms lanes={st['lanes']} hops={hops}", flush=True)
