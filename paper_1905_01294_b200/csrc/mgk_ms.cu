@@ -858,23 +858,27 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             expand = want_items && deg > 0;
         }
         if (count_lanes) {
-            // column popcounts: lane l accumulates bit l (cnt_lo) and bit 32+l
-            // (cnt_hi) of each lane word over the warp's 32 entries
+            // column sums of the warp's 32 lane words by SWAR: five lane bits
+            // are spread into 6-bit fields of a 32-bit word (the product places
+            // five copies of the 5-bit group side by side, the mask keeps bit j
+            // of copy j), one redux.add per group of five lanes (a field reaches
+            // at most 32); lane l keeps lane bit l (cnt_lo) and 32 + l (cnt_hi)
+            // -- 2 (10-bit words) to 13 (64-bit) reductions instead of a ballot
+            // per lane bit
+            constexpr int kBits = NB < 64 ? NB : 64;
+            constexpr int kGroups = (kBits + 4) / 5;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 if (__ballot_sync(kFull, x.w[i] != 0) == 0) continue;
-                const uint32_t lo = (uint32_t)x.w[i], hi = (uint32_t)(x.w[i] >> 32);
-                constexpr int kLo = NB < 32 ? NB : 32;  // narrow words: only their own bits
+                const unsigned long long xw = x.w[i];
 #pragma unroll
-                for (int bb = 0; bb < kLo; ++bb) {
-                    const uint32_t c0 = __popc(__ballot_sync(kFull, (lo >> bb) & 1u));
-                    if ((uint32_t)bb == lane) cnt_lo[i] += c0;
-                }
-                if constexpr (NB == 64) {
-#pragma unroll
-                    for (int bb = 0; bb < 32; ++bb) {
-                        const uint32_t c1 = __popc(__ballot_sync(kFull, (hi >> bb) & 1u));
-                        if ((uint32_t)bb == lane) cnt_hi[i] += c1;
+                for (int q = 0; q < kGroups; ++q) {
+                    const uint32_t f = ((uint32_t)(xw >> (5 * q)) & 31u) * 0x108421u & 0x1041041u;
+                    const uint32_t sum = __reduce_add_sync(kFull, f);
+                    if (lane / 5 == (uint32_t)q && lane < (uint32_t)kBits)
+                        cnt_lo[i] += (sum >> (6 * (lane % 5))) & 63u;
+                    if constexpr (NB == 64) {
+                        if ((32 + lane) / 5 == (uint32_t)q) cnt_hi[i] += (sum >> (6 * ((32 + lane) % 5))) & 63u;
                     }
                 }
             }
