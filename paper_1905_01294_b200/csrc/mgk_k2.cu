@@ -42,7 +42,13 @@ namespace {
 
 using namespace dev;
 
-constexpr int kK2Block = 768;  // 80 registers, no spills (1024 threads spilled at 64)
+#ifndef MGK_K2_BLOCK
+#define MGK_K2_BLOCK 768  // 80 registers, no spills (1024 threads spilled at 64)
+#endif
+#ifndef MGK_K2_MINB
+#define MGK_K2_MINB 1  // CTAs per SM the register budget is sized for
+#endif
+constexpr int kK2Block = MGK_K2_BLOCK;
 constexpr int kK2Warps = kK2Block / 32;
 constexpr uint32_t kK2Win = 2 * kK2Block;  // F1 rows per prefix window (2 per thread)
 constexpr uint32_t kK2Task = 32;   // F1 rows per phase-0 task (1 per lane)
@@ -182,7 +188,7 @@ __global__ void k2_split_kernel(DevGraph g, uint32_t R, uint32_t rbits, uint32_t
     }
 }
 
-__global__ void __launch_bounds__(kK2Block, 1) k2_kernel(K2Params P) {
+__global__ void __launch_bounds__(kK2Block, MGK_K2_MINB) k2_kernel(K2Params P) {
     extern __shared__ __align__(16) unsigned char k2_smem[];
     grid_barrier_init(P.bar);
     uint32_t* bm = reinterpret_cast<uint32_t*>(k2_smem);
@@ -809,6 +815,11 @@ K2Device& k2_device() {
         // part may use what the kernel's static arrays leave
         cudaFuncAttributes fa{};
         if (cudaFuncGetAttributes(&fa, k2_kernel) == cudaSuccess) devs[dev].optin -= (int)fa.sharedSizeBytes;
+        if (MGK_K2_MINB > 1) {  // several CTAs per SM: each gets its share of the SM's shared memory
+            int per_sm = 0;
+            cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            devs[dev].optin = std::min(devs[dev].optin, per_sm / MGK_K2_MINB - 1024 - (int)fa.sharedSizeBytes);
+        }
         if (cudaFuncSetAttribute(k2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, devs[dev].optin) !=
             cudaSuccess) {
             (void)cudaGetLastError();
