@@ -96,6 +96,7 @@ struct MSParams {
     uint64_t clog_cap;
     uint4* items0;
     uint4* items1;
+    uint32_t items_cap;  // uint4 slots of each items array (heavy records fill it from the end)
     unsigned long long* lane_cnt;  // [(k+1) * 64W]
     unsigned long long* active;    // [2 * W]
     QCtl* qctl;                    // [2] by hop parity; .pad = push-equivalent edges
@@ -337,6 +338,99 @@ __device__ __forceinline__ uint4* items_of(const MSParams& P, uint32_t i) {
 __device__ __forceinline__ uint32_t* R_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.R1 : P.R0;
 }
+
+// Push work items of the LANES engine. A vertex with at most kHeavyItems
+// items (out-degree <= 2048) gets its kChunk-entry items written by the warp
+// that lists it; a heavier one (a hub: G4's reach 10^6 out-edges) gets ONE
+// record {u, row begin, degree, first virtual item} at the end of the items
+// array instead, and the push derives its items from the records by a binary
+// search -- one warp writing a hub's ~10^5 items was the critical path of the
+// finalize before a push (G4 10 seeds, hop 1: 89 us for 448 vertices).
+// misc[kHeavyCtl + parity] = (records << 40) | virtual items; one 64-bit
+// atomic per warp reserves both, so record slots ascend with their first item.
+constexpr uint32_t kHeavyItems = 64;
+constexpr int kHeavyCtl = 4;
+constexpr int kHeavyShift = 40;
+
+__device__ __forceinline__ void emit_items_lanes(const MSParams& P, const uint32_t* buf, uint32_t n, uint4* items,
+                                                 unsigned int* nitems) {
+    if (n == 0) return;
+    const uint32_t lane = lane_id();
+    const uint32_t* rp = P.g.rp;
+    unsigned long long* hctl = P.misc + kHeavyCtl + (items == P.items0 ? 0 : 1);
+    uint4* hrec = items + P.items_cap - 1;  // record r at hrec[-r]
+    uint32_t tot = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t u = buf[i];
+        const uint32_t d = __ldg(rp + u + 1) - __ldg(rp + u);
+        const uint32_t nit = (d + kChunk - 1) / kChunk;
+        tot += nit > kHeavyItems ? 0 : nit;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(kFull, tot, d);
+    uint32_t base = 0;
+    if (lane == 0 && tot) base = atomicAdd(nitems, tot);
+    base = __shfl_sync(kFull, base, 0);
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+        const uint32_t i = i0 + lane;
+        uint32_t u = 0, b = 0, deg = 0;
+        if (i < n) {
+            u = buf[i];
+            b = __ldg(rp + u);
+            deg = __ldg(rp + u + 1) - b;
+        }
+        const uint32_t all = (deg + kChunk - 1) / kChunk;
+        const bool heavy = all > kHeavyItems;
+        const uint32_t nit = heavy ? 0 : all;
+        const unsigned hm = __ballot_sync(kFull, heavy);
+        if (hm) {  // records of this group's hubs: one reservation for all of them
+            const uint32_t hn = heavy ? all : 0;
+            const uint32_t hincl = warp_incl_scan(hn);
+            unsigned long long hb = 0;
+            if (lane == 31)
+                hb = atomicAdd(hctl, ((unsigned long long)__popc(hm) << kHeavyShift) | (unsigned long long)hincl);
+            hb = __shfl_sync(kFull, hb, 31);
+            if (heavy) {
+                const uint32_t slot = (uint32_t)(hb >> kHeavyShift) + __popc(hm & lanemask_lt());
+                const uint32_t first = (uint32_t)(hb & ((1ull << kHeavyShift) - 1)) + hincl - hn;
+                *(hrec - slot) = make_uint4(u, b, deg, first);
+            }
+        }
+        const uint32_t incl = warp_incl_scan(nit);
+        const uint32_t total = __shfl_sync(kFull, incl, 31);
+        const uint32_t excl = incl - nit;
+        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
+            const uint32_t x = x0 + lane;
+            const uint32_t j = warp_owner(incl, x < total ? x : total - 1);
+            const uint32_t bj = __shfl_sync(kFull, b, j);
+            const uint32_t dj = __shfl_sync(kFull, deg, j);
+            const uint32_t ej = __shfl_sync(kFull, excl, j);
+            const uint32_t uj = __shfl_sync(kFull, u, j);
+            if (x < total) {
+                const uint32_t s = bj + (x - ej) * kChunk;
+                items[base + x] = make_uint4(s, min(s + kChunk, bj + dj), uj, 0);
+            }
+        }
+        base += total;
+    }
+    __syncwarp();
+}
+
+// item x of a push: written (x < nlight) or derived from the heavy records
+__device__ __forceinline__ uint4 push_item(const uint4* items, uint32_t cap, uint32_t nlight, uint32_t nrec,
+                                           uint32_t x) {
+    if (x < nlight) return items[x];
+    const uint32_t c = x - nlight;
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(items + cap - 1);  // record r's first item: hw[3 - 4 r]
+    uint32_t lo = 0, hi = nrec;  // last record whose first item <= c
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldcg(hw + 3 - 4 * (int64_t)mid) <= c) lo = mid; else hi = mid;
+    }
+    const uint4 r = __ldcg(items + cap - 1 - lo);
+    const uint32_t s = r.y + (c - r.w) * kChunk;
+    return make_uint4(s, min(s + kChunk, r.y + r.z), r.x, 0);
+}
 __device__ __forceinline__ unsigned long long* F_of(const MSParams& P, uint32_t i) {
     return (i & 1) ? P.F1 : P.F0;
 }
@@ -384,33 +478,57 @@ __device__ void block_flush(Acc& a, QCtl* q, QCtl* qf, LevelCounters* lc, LevelC
 
 
 // ---- push expand -----------------------------------------------------------------
+// Entries per lane per round (their loads issued together): a push entry is a
+// chain of dependent accesses (in-list entry -> visited word -> atomic), so a
+// round costs a full memory latency; one-word lanes take PU of them at once.
+#ifndef MGK_PUSH_UNROLL
+#define MGK_PUSH_UNROLL 1  // 2 and 4 measured: no gain (G4 hop 2 push ~105 us either way)
+#endif
+// finalize lists of more than n / kDenseDiv vertices are swept densely (one word per vertex)
+#ifndef MGK_DENSE_DIV
+#define MGK_DENSE_DIV 8  // 16 and 32 measured slower: the dense sweep is latency-bound (G4 hop 2: 136 -> 185 us at 32)
+#endif
+constexpr uint64_t kDenseDiv = MGK_DENSE_DIV;
+template <int W>
+constexpr int push_unroll() { return W == 1 ? MGK_PUSH_UNROLL : 1; }
+
 template <int W, int NB>
-MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nitems,
+MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nlight, unsigned long long hctl,
                            const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
                            QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
                            uint32_t nwarps, const LaneWord<W>& pushm) {
+    constexpr int PU = push_unroll<W>();
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
+    const uint32_t nrec = (uint32_t)(hctl >> kHeavyShift);
+    const uint32_t nitems = nlight + (uint32_t)(hctl & ((1ull << kHeavyShift) - 1));
     const uint32_t G = items_per_warp(nitems, nwarps);
     for (uint32_t base = warp_gid * G; base < nitems; base += nwarps * G) {
         const uint32_t idx = base + lane;
-        const uint4 it = (lane < G && idx < nitems) ? items[idx] : make_uint4(0, 0, 0, 0);
+        const uint4 it = (lane < G && idx < nitems) ? push_item(items, P.items_cap, nlight, nrec, idx)
+                                                     : make_uint4(0, 0, 0, 0);
         const uint32_t len = it.y - it.x;
         const uint32_t incl = warp_incl_scan(len);
         const uint32_t total = __shfl_sync(kFull, incl, 31);
         const uint32_t off = it.x - (incl - len);
-        for (uint32_t x0 = 0; x0 < total; x0 += 32) {
-            const uint32_t x = x0 + lane;
-            const bool valid = x < total;
-            const uint32_t j = warp_owner(incl, valid ? x : total - 1);
-            const uint32_t pos = __shfl_sync(kFull, off, j) + x;
-            const uint32_t src = __shfl_sync(kFull, it.z, j);
-            bool first = false;
-            uint32_t u = 0;
-            if (valid) {
-                u = __ldg(g.ci + pos);
-                const LaneWord<W> f = LS<W, NB>::load(Fc, src);
-                const LaneWord<W> vis = LS<W, NB>::load(P.V, u);
+        for (uint32_t x0 = 0; x0 < total; x0 += 32 * PU) {
+            uint32_t u[PU], src[PU];
+            bool valid[PU], first[PU];
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                const uint32_t x = x0 + 32 * q + lane;
+                valid[q] = x < total;
+                const uint32_t j = warp_owner(incl, valid[q] ? x : total - 1);
+                const uint32_t pos = __shfl_sync(kFull, off, j) + x;
+                src[q] = __shfl_sync(kFull, it.z, j);
+                u[q] = valid[q] ? __ldg(g.ci + pos) : 0;
+                first[q] = false;
+            }
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                if (!valid[q]) continue;
+                const LaneWord<W> f = LS<W, NB>::load(Fc, src[q]);
+                const LaneWord<W> vis = LS<W, NB>::load(P.V, u[q]);
                 LaneWord<W> m;
                 bool any = false;
 #pragma unroll
@@ -421,29 +539,32 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nitems
                 if (any) {
                     if constexpr (W == 1) {
                         // one atomic: the OR that finds the word empty lists u
-                        first = LS<W, NB>::atomic_or_first(Fn, u, m.w[0]);
+                        first[q] = LS<W, NB>::atomic_or_first(Fn, u[q], m.w[0]);
                     } else {
-                        const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u);
+                        const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u[q]);
                         bool need = false;
 #pragma unroll
                         for (int i = 0; i < W; ++i) {
                             if ((cur.w[i] & m.w[i]) != m.w[i]) {
-                                LS<W, NB>::atomic_or(Fn, u, i, m.w[i]);
+                                LS<W, NB>::atomic_or(Fn, u[q], i, m.w[i]);
                                 need = true;
                             }
                         }
                         if (need) {  // several words: the touched bit decides who lists u
-                            const uint32_t bit = 1u << (u & 31);
-                            first = !(atomicOr(P.touched + (u >> 5), bit) & bit);
+                            const uint32_t bit = 1u << (u[q] & 31);
+                            first[q] = !(atomicOr(P.touched + (u[q] >> 5), bit) & bit);
                         }
                     }
                 }
             }
-            acc.scanned += valid;
-            st.push(first, u);
-            if (st.full()) {
-                emit_list(st.buf, st.n, Rn, &qn->nitems);
-                st.n = 0;
+#pragma unroll
+            for (int q = 0; q < PU; ++q) {
+                acc.scanned += valid[q];
+                st.push(first[q], u[q]);
+                if (st.full()) {
+                    emit_list(st.buf, st.n, Rn, &qn->nitems);
+                    st.n = 0;
+                }
             }
         }
     }
@@ -784,7 +905,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
-                               uint32_t warp_gid, uint32_t nwarps, bool dense = false) {
+                               uint32_t warp_gid, uint32_t nwarps, bool dense = false, bool dense_few = false) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // dense (a list of more than n/8, one word per vertex): sweep every vertex
@@ -792,6 +913,10 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
     // words, CSR / CSC bounds) issued at once and coalesced -- one round trip
     // per vertex instead of two dependent ones; the discovered vertices are
     // those with a non-zero new word. The list itself stays as built.
+    // dense_few (a list of n/kDenseDiv .. n/4): the sweep reads only the
+    // frontier and visited words of every vertex (coalesced) and the bounds of
+    // the discovered ones -- cheaper than the list's scattered loads (G4 hop 2:
+    // 1.85M of 35.6M vertices)
     LaneWord<W> act;
     uint32_t cnt_lo[W], cnt_hi[W];
 #pragma unroll
@@ -815,15 +940,23 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             u = dense ? idx : Rn[idx];
             x = LS<W, NB>::load(Fn, u);
             v = LS<W, NB>::load(P.V, u);
-            r0 = __ldg(g.rp + u);
-            r1 = __ldg(g.rp + u + 1);
-            c0 = __ldg(g.cp + u);
-            c1 = __ldg(g.cp + u + 1);
+            if (!dense_few) {
+                r0 = __ldg(g.rp + u);
+                r1 = __ldg(g.rp + u + 1);
+                c0 = __ldg(g.cp + u);
+                c1 = __ldg(g.cp + u + 1);
+            }
             if (dense) {
                 bool any = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
                 valid = any;
+            }
+            if (dense_few && valid) {
+                r0 = __ldg(g.rp + u);
+                r1 = __ldg(g.rp + u + 1);
+                c0 = __ldg(g.cp + u);
+                c1 = __ldg(g.cp + u + 1);
             }
         }
         if (valid) {
@@ -886,13 +1019,13 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
         if (want_items) {
             st.push(expand, u);
             if (st.full()) {
-                emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+                emit_items_lanes(P, st.buf, st.n, items_n, item_tail);
                 st.n = 0;
             }
         }
     }
     if (want_items) {
-        emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+        emit_items_lanes(P, st.buf, st.n, items_n, item_tail);
         st.n = 0;
     }
 #pragma unroll
@@ -930,11 +1063,11 @@ MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, co
         }
         st.push(expand, u);
         if (st.full()) {
-            emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+            emit_items_lanes(P, st.buf, st.n, items_n, item_tail);
             st.n = 0;
         }
     }
-    emit_items(g.rp, st.buf, st.n, items_n, item_tail);
+    emit_items_lanes(P, st.buf, st.n, items_n, item_tail);
     st.n = 0;
 }
 
@@ -1008,6 +1141,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         if (gtid == 0) {
             P.misc[0] = g.m;
             P.misc[1] = P.misc[2] = 0;  // pull work counters
+            P.misc[kHeavyCtl] = P.misc[kHeavyCtl + 1] = 0;  // heavy push records by parity
         }
         if (bt == 0)  // the first lc write is after the barrier below
             for (uint32_t i = gtid; i < (MGK_MAX_HOPS + 2) * (sizeof(LevelCounters) / 8); i += nthreads)
@@ -1050,6 +1184,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
         grid_barrier(P.bar);
 
+        bool any_dense = false;  // a dense finalize listed nothing in clog: V is cleared by streaming
         bool prev_pull = false;  // the hop before pulled: its unsettled words bound this pull's
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
@@ -1082,7 +1217,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             if (gtid < W) P.active[nxt * W + gtid] = 0;  // rebuilt by this hop's finalize
             // ---- expand: a push from the frontier's items or a pull over the CSC -----
             if (anypush)
-                push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), Fc, Fn, Rn, qn, acc,
+                push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), ld_volatile(&P.misc[kHeavyCtl + cur]), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
             // a pull after a pull visits only the vertices that pull left unsettled
             if (anypull)
@@ -1099,13 +1234,18 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
             const bool last = hop == P.k || nR == 0;
             const bool count_lanes = hop >= P.min_hop;
+            const bool dense = W == 1 && (uint64_t)nR * kDenseDiv > g.n;
             // ---- finalize -------------------------------------------------------------
             for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;
-            if (gtid == 0) *qc = QCtl{0, 0, 0, 0, 0};  // parity reused by hop + 1
+            if (gtid == 0) {  // parity reused by hop + 1
+                *qc = QCtl{0, 0, 0, 0, 0};
+                P.misc[kHeavyCtl + cur] = 0;
+            }
             __syncthreads();
             finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
-                              W == 1 && (uint64_t)nR * 8 > g.n);
+                              dense, dense && (uint64_t)nR * 4 <= g.n);
+            any_dense |= dense;
             clear_words<W, NB>(Rc, nR_prev, Fc, g.n, gtid, nthreads);
             __syncthreads();
             if (count_lanes)
@@ -1172,7 +1312,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         }
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
-        if (clog_used <= P.clog_cap && clog_used * 8 <= g.n) {
+        if (!any_dense && clog_used <= P.clog_cap && clog_used * 8 <= g.n) {
             clear_list<W, NB>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
             clear_words<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), g.n, gtid, nthreads);
         } else if (clog_used <= P.clog_cap) {
@@ -1238,6 +1378,7 @@ cudaError_t launch_w(Launch& L) {
     P.clog_cap = ws->rlog_cap - 2 * (uint64_t)gr->dg.n;
     P.items0 = ws->ms_items[0];
     P.items1 = ws->ms_items[1];
+    P.items_cap = (uint32_t)(gr->dg.m / kChunk + gr->dg.n + 64);  // as allocated (ensure_lanes_ws)
     P.lane_cnt = ws->lane_cnt;
     P.active = ws->active;
     P.qctl = ws->qctl;
