@@ -905,7 +905,7 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
                                uint4* items_n, unsigned int* item_tail, bool count_lanes,
                                unsigned long long* s_cnt, unsigned long long* active_n,
                                uint64_t clog_base, Acc& acc, Stage<kStageCap>& st,
-                               uint32_t warp_gid, uint32_t nwarps, bool dense = false, bool dense_few = false) {
+                               uint32_t warp_gid, uint32_t nwarps, bool dense = false) {
     const uint32_t lane = lane_id();
     const DevGraph& g = P.g;
     // dense (a list of more than n/8, one word per vertex): sweep every vertex
@@ -913,10 +913,9 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
     // words, CSR / CSC bounds) issued at once and coalesced -- one round trip
     // per vertex instead of two dependent ones; the discovered vertices are
     // those with a non-zero new word. The list itself stays as built.
-    // dense_few (a list of n/kDenseDiv .. n/4): the sweep reads only the
-    // frontier and visited words of every vertex (coalesced) and the bounds of
-    // the discovered ones -- cheaper than the list's scattered loads (G4 hop 2:
-    // 1.85M of 35.6M vertices)
+    // (Measured and removed: a "dense_few" sweep for lists of n/32 .. n/4 that
+    // loads the bounds of the discovered vertices only -- G4 hop 2 unchanged,
+    // and the split loads cost the fully dense sweeps of hops 3 / 4 +65 us each.)
     LaneWord<W> act;
     uint32_t cnt_lo[W], cnt_hi[W];
 #pragma unroll
@@ -940,23 +939,15 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             u = dense ? idx : Rn[idx];
             x = LS<W, NB>::load(Fn, u);
             v = LS<W, NB>::load(P.V, u);
-            if (!dense_few) {
-                r0 = __ldg(g.rp + u);
-                r1 = __ldg(g.rp + u + 1);
-                c0 = __ldg(g.cp + u);
-                c1 = __ldg(g.cp + u + 1);
-            }
+            r0 = __ldg(g.rp + u);
+            r1 = __ldg(g.rp + u + 1);
+            c0 = __ldg(g.cp + u);
+            c1 = __ldg(g.cp + u + 1);
             if (dense) {
                 bool any = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
                 valid = any;
-            }
-            if (dense_few && valid) {
-                r0 = __ldg(g.rp + u);
-                r1 = __ldg(g.rp + u + 1);
-                c0 = __ldg(g.cp + u);
-                c1 = __ldg(g.cp + u + 1);
             }
         }
         if (valid) {
@@ -1171,10 +1162,8 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         uint32_t nR = ld_volatile(&P.qctl[0].nitems);
         // the lanes pulling the current hop (all or none when the words are wider
         // than 64 lanes); hop 1 pushes unless a pull is forced
-        LaneWord<W> pullm;
-#pragma unroll
-        for (int i = 0; i < W; ++i) pullm.w[i] = P.force_dir == 2 ? ~0ull : 0ull;
         const bool pull0 = P.force_dir == 2;
+        bool pull_hop = pull0;  // (one flag for all lanes: a mask per lane word stayed live across the hop)
         for (uint32_t t = threadIdx.x; t < LB; t += kBlock) s_cnt[t] = 0;  // (LB may exceed the block)
         __syncthreads();
         finalize_phase<W, NB>(P, P.R0, nR, P.F0, P.seed_visited != 0, true, !pull0, P.items0, &P.qctl[0].nfound, false,
@@ -1184,7 +1173,6 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         block_flush(acc, &P.qctl[0], &P.qctl[0], &P.lc[0], &P.lc[1], &P.misc[0]);
         grid_barrier(P.bar);
 
-        bool any_dense = false;  // a dense finalize listed nothing in clog: V is cleared by streaming
         bool prev_pull = false;  // the hop before pulled: its unsettled words bound this pull's
         uint64_t clog_used = nR;
         uint32_t nR_prev = nR;
@@ -1197,19 +1185,22 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             unsigned long long* Fn = F_of(P, nxt);
             uint32_t* Rc = R_of(P, cur);
             uint32_t* Rn = R_of(P, nxt);
-            unsigned long long t0 = 0;
             LaneWord<W> actc, pushm, pm;
             bool anypush = false, anypull = false;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
                 actc.w[i] = ld_volatile(P.active + cur * W + i);
-                pushm.w[i] = actc.w[i] & ~pullm.w[i];
-                pm.w[i] = actc.w[i] & pullm.w[i];
+                pushm.w[i] = pull_hop ? 0ull : actc.w[i];
+                pm.w[i] = pull_hop ? actc.w[i] : 0ull;
                 anypush |= pushm.w[i] != 0;
                 anypull |= pm.w[i] != 0;
             }
             if (gtid == 0) {
-                t0 = globaltimer();
+                // the hop's start time is subtracted here and its end time added below:
+                // no 64-bit timestamp stays live across the phases (registers)
+                const unsigned long long t0 = globaltimer();
+                atomicAdd(&P.lc[hop].ns, 0ULL - t0);
+                if (P.diag) P.misc[6] = t0;
                 atomicAdd(&P.lc[hop].runs, 1u);
                 if (anypull) atomicAdd(&P.lc[hop].pull_runs, 1u);
                 atomicAdd(&P.lc[hop].union_edges, ld_volatile(&qc->edges));
@@ -1228,8 +1219,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             prev_pull = anypull;
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
-            unsigned long long t1 = 0;
-            if (P.diag && gtid == 0) t1 = globaltimer();
+            if (P.diag && gtid == 0) P.misc[7] = globaltimer();
             nR = ld_volatile(&qn->nitems);
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
             const bool last = hop == P.k || nR == 0;
@@ -1244,8 +1234,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             __syncthreads();
             finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
-                              dense, dense && (uint64_t)nR * 4 <= g.n);
-            any_dense |= dense;
+                              dense);
             clear_words<W, NB>(Rc, nR_prev, Fc, g.n, gtid, nthreads);
             __syncthreads();
             if (count_lanes)
@@ -1271,15 +1260,14 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                     } else {
                         pn = (unsigned long long)nR * P.beta >= g.n;
                     }
-#pragma unroll
-                    for (int i = 0; i < W; ++i) pullm.w[i] = pn ? ~0ull : 0ull;
+                    pull_hop = pn;
                 }
                 // items for the lanes pushing next
                 LaneWord<W> pn_push;
                 bool anyn = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & ~pullm.w[i];
+                    pn_push.w[i] = pull_hop ? 0ull : ld_volatile(P.active + nxt * W + i);
                     anyn |= pn_push.w[i] != 0;
                 }
                 if (anyn) {
@@ -1289,10 +1277,10 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             }
             if (gtid == 0) {
                 const unsigned long long t2 = globaltimer();
-                atomicAdd(&P.lc[hop].ns, t2 - t0);
+                atomicAdd(&P.lc[hop].ns, t2);
                 if (P.diag) {  // probe mode: phase split (the counters these fields hold are lost)
-                    P.lc[hop].union_edges = t1 - t0;
-                    P.lc[hop].candidates = t2 - t1;
+                    P.lc[hop].union_edges = P.misc[7] - P.misc[6];
+                    P.lc[hop].candidates = t2 - P.misc[7];
                 }
             }
             clog_used += nR;
@@ -1312,7 +1300,11 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         }
         // ---- clear V and the last frontier (state is all-zero between batches) ---------
         const uint32_t last_par = (hop > P.k ? P.k : hop) & 1;
-        if (!any_dense && clog_used <= P.clog_cap && clog_used * 8 <= g.n) {
+        // (a dense finalize lists nothing in clog: it needs nR * kDenseDiv > n, and
+        // then clog_used * kClearDiv > n too, so V is cleared by streaming; no flag
+        // is kept across the hops -- one more live register spilled the pull)
+        constexpr uint64_t kClearDiv = kDenseDiv > 8 ? kDenseDiv : 8;
+        if (clog_used <= P.clog_cap && clog_used * kClearDiv <= g.n) {
             clear_list<W, NB>(P.clog, (uint32_t)clog_used, P.V, gtid, nthreads);
             clear_words<W, NB>(R_of(P, last_par), nR_prev, F_of(P, last_par), g.n, gtid, nthreads);
         } else if (clog_used <= P.clog_cap) {
