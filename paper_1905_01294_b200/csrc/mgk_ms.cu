@@ -73,6 +73,12 @@ __device__ __forceinline__ uint32_t ld_ri_lane(const uint32_t* p, unsigned long 
 #endif
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
+// first pull: lanes with at most m / MGK_STRAG frontier out-edges keep pushing (0: off; env MGK_STRAG).
+// G4, 10 seeds: hop 3 scans 666M -> 248M entries (213M pulled + the stragglers' pushes), k = 6 5.31 -> 3.82 ms;
+// 16 / 256 measured: 3.87 / 4.29 ms
+#ifndef MGK_STRAG_DEFAULT
+#define MGK_STRAG_DEFAULT 64
+#endif
 
 struct MSParams {
     DevGraph g;
@@ -106,6 +112,11 @@ struct MSParams {
     uint32_t alpha, beta, force_dir;
     uint32_t* umask;  // [2][nwords] by hop parity: per word, the vertices a pull left unsettled
     uint32_t diag;  // MGK_MS_DIAG=1: per hop, expand-phase ns in lc.union_edges, finalize ns in lc.candidates
+    // Straggler lanes (one word per vertex): at the first pull, a lane whose
+    // frontier has at most m / strag out-edges keeps pushing (0: off). lane_E
+    // [64]: per-lane out-edges of the frontier just found.
+    uint32_t strag;
+    unsigned long long* lane_E;
 };
 
 template <int W>
@@ -1062,6 +1073,43 @@ MGK_PHASE void emit_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, co
     st.n = 0;
 }
 
+// Per-lane out-edges of the frontier just found (one word per vertex): for
+// each listed vertex, its out-degree is added to every lane whose bit is set in
+// its new word -- one warp reduction per lane bit. Runs once per traversal,
+// before the first pull: the lanes with few frontier edges ("stragglers": a
+// low-degree seed's hop-2 frontier is a handful of vertices) then keep pushing,
+// so the pull's early exit no longer waits for lanes almost no in-list covers.
+template <int W, int NB>
+MGK_PHASE void lane_edges_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR, const unsigned long long* Fn,
+                                uint32_t warp_gid, uint32_t nwarps) {
+    if constexpr (W == 1) {
+        constexpr uint32_t kBits = LS<W, NB>::kLanes;
+        const uint32_t lane = lane_id();
+        const DevGraph& g = P.g;
+        unsigned long long e_lo = 0, e_hi = 0;
+        for (uint32_t base = warp_gid * 32; base < nR; base += nwarps * 32) {
+            const uint32_t idx = base + lane;
+            unsigned long long x = 0;
+            uint32_t deg = 0;
+            if (idx < nR) {
+                const uint32_t u = Rn[idx];
+                x = LS<W, NB>::load(Fn, u).w[0];
+                deg = min(__ldg(g.rp + u + 1) - __ldg(g.rp + u), 1u << 26);  // (32 of them fit 32 bits)
+            }
+            if (__ballot_sync(kFull, x != 0 && deg != 0) == 0) continue;
+#pragma unroll 2
+            for (uint32_t b = 0; b < kBits; ++b) {
+                const uint32_t sum = __reduce_add_sync(kFull, ((x >> b) & 1ull) ? deg : 0u);
+                if (lane == (b & 31)) {
+                    if (b < 32) e_lo += sum; else e_hi += sum;
+                }
+            }
+        }
+        if (lane < kBits && e_lo) atomicAdd(&P.lane_E[lane], e_lo);
+        if (32 + lane < kBits && e_hi) atomicAdd(&P.lane_E[32 + lane], e_hi);
+    }
+}
+
 template <int W, int NB>
 __device__ void clear_list(const uint32_t* R, uint32_t n, unsigned long long* F, uint32_t gtid,
                            uint32_t nthreads) {
@@ -1112,6 +1160,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
     __shared__ unsigned long long s_cnt[LB];
     __shared__ uint32_t s_nm[kWarps][32];  // pull: unsettled-vertex masks of a warp's 32 words
     __shared__ uint32_t s_cb[kWarps][64];  // pull: a warp's waiting candidates
+    __shared__ unsigned long long s_strag;  // lanes that push while the others pull (the next hop's; 0: none)
     const uint32_t gtid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = gridDim.x * kBlock;
     const uint32_t warp_gid = gtid >> 5;
@@ -1129,6 +1178,8 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
         for (uint32_t i = gtid; i < (P.k + 1) * LB; i += nthreads) P.lane_cnt[i] = 0;
         if (gtid < 2 * W) P.active[gtid] = 0;
         if (gtid < 2) P.qctl[gtid] = QCtl{0, 0, 0, 0, 0};
+        if (W == 1 && gtid < LB) P.lane_E[gtid] = 0;
+        if (threadIdx.x == 0) s_strag = 0;
         if (gtid == 0) {
             P.misc[0] = g.m;
             P.misc[1] = P.misc[2] = 0;  // pull work counters
@@ -1185,14 +1236,17 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             unsigned long long* Fn = F_of(P, nxt);
             uint32_t* Rc = R_of(P, cur);
             uint32_t* Rn = R_of(P, nxt);
-            LaneWord<W> actc, pushm, pm;
+            // the lanes pulling this hop: all active ones of a pull hop but its
+            // straggler lanes, which push (only with one word per vertex); the
+            // pushing lanes' mask is rebuilt after the pull (not kept across it)
+            LaneWord<W> pm;
             bool anypush = false, anypull = false;
 #pragma unroll
             for (int i = 0; i < W; ++i) {
-                actc.w[i] = ld_volatile(P.active + cur * W + i);
-                pushm.w[i] = pull_hop ? 0ull : actc.w[i];
-                pm.w[i] = pull_hop ? actc.w[i] : 0ull;
-                anypush |= pushm.w[i] != 0;
+                const unsigned long long a = ld_volatile(P.active + cur * W + i);
+                const unsigned long long sm = (W == 1 && pull_hop) ? s_strag : 0ull;
+                pm.w[i] = pull_hop ? (a & ~sm) : 0ull;
+                anypush |= (pull_hop ? (a & sm) : a) != 0;
                 anypull |= pm.w[i] != 0;
             }
             if (gtid == 0) {
@@ -1207,16 +1261,46 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             }
             if (gtid < W) P.active[nxt * W + gtid] = 0;  // rebuilt by this hop's finalize
             // ---- expand: a push from the frontier's items or a pull over the CSC -----
-            if (anypush)
+            // A mixed hop (straggler lanes push, the others pull) pulls first: the
+            // pull stores its words and lists its discoveries as in a pure pull,
+            // and after a barrier the push ORs the stragglers' lanes in, listing a
+            // vertex only when it finds the word still empty. Such a pull's
+            // unsettled masks ignore the stragglers' needs, so the next pull does
+            // not read them and visits every word again.
+            if (anypush && !pull_hop) {
+                LaneWord<W> pushm;
+#pragma unroll
+                for (int i = 0; i < W; ++i) pushm.w[i] = ld_volatile(P.active + cur * W + i);
                 push_phase<W, NB>(P, items_of(P, cur), ld_volatile(&qc->nfound), ld_volatile(&P.misc[kHeavyCtl + cur]), Fc, Fn, Rn, qn, acc,
                               st, warp_gid, nwarps, pushm);
+            }
             // a pull after a pull visits only the vertices that pull left unsettled
             if (anypull)
                 pull_phase<W, NB>(P, Fc, Fn, pm, Rn, qn, acc, st, warp_gid, nwarps,
                                   prev_pull ? P.umask + (size_t)cur * g.nwords : nullptr,
-                                  P.umask + (size_t)nxt * g.nwords,
+                                  P.umask + (size_t)nxt * g.nwords,  // (a mixed hop's: never read)
                                   s_nm[threadIdx.x >> 5], s_cb[threadIdx.x >> 5]);
             prev_pull = anypull;
+            if constexpr (W == 1) {
+                // the stragglers' push of a mixed hop; its operands are derived again
+                // from the hop number (laundered), so none of them is held in a
+                // register across the pull
+                const unsigned long long sm = pull_hop ? *(volatile unsigned long long*)&s_strag : 0ull;
+                if (sm) {
+                    uint32_t h2 = hop;
+                    asm volatile("" : "+r"(h2));
+                    const uint32_t c2 = (h2 - 1) & 1, n2 = h2 & 1;
+                    LaneWord<W> pushm;
+                    pushm.w[0] = ld_volatile(P.active + c2) & sm;
+                    if (pushm.w[0]) {
+                        grid_barrier(P.bar);
+                        push_phase<W, NB>(P, items_of(P, c2), ld_volatile(&P.qctl[c2].nfound),
+                                          ld_volatile(&P.misc[kHeavyCtl + c2]), F_of(P, c2), F_of(P, n2), R_of(P, n2),
+                                          &P.qctl[n2], acc, st, warp_gid, nwarps, pushm);
+                        prev_pull = false;
+                    }
+                }
+            }
             block_flush(acc, qn, qn, &P.lc[hop], nullptr, &P.misc[0]);
             grid_barrier(P.bar);
             if (P.diag && gtid == 0) P.misc[7] = globaltimer();
@@ -1231,6 +1315,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                 *qc = QCtl{0, 0, 0, 0, 0};
                 P.misc[kHeavyCtl + cur] = 0;
             }
+            if (W == 1 && P.strag && gtid < LB) P.lane_E[gtid] = 0;  // (read last before the expand barrier)
             __syncthreads();
             finalize_phase<W, NB>(P, Rn, nR, Fn, true, W > 1 && anypush, false, items_of(P, nxt), &qn->nfound, count_lanes,
                               s_cnt, P.active + nxt * W, clog_used, acc, st, warp_gid, nwarps,
@@ -1260,6 +1345,28 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                     } else {
                         pn = (unsigned long long)nR * P.beta >= g.n;
                     }
+                    // the first pull of a traversal: lanes whose frontier has few
+                    // out-edges keep pushing (every CTA computes the same mask)
+                    if constexpr (W == 1) {
+                        const bool first_pull = P.strag && pn && !anypull && P.force_dir == 0;
+                        if (first_pull) {
+                            lane_edges_phase<W, NB>(P, Rn, nR, Fn, warp_gid, nwarps);
+                            grid_barrier(P.bar);
+                        }
+                        __syncthreads();  // (s_strag's readers are past the hop's top)
+                        if (threadIdx.x == 0) {  // one thread per CTA: the lanes (active in the
+                            // next frontier) with at most m / strag frontier out-edges
+                            unsigned long long sm = 0;
+                            if (first_pull) {
+                                const unsigned long long an = ld_volatile(P.active + nxt * W);
+                                for (uint32_t l = 0; l < LB; ++l)
+                                    if (((an >> l) & 1ull) && ld_cg(&P.lane_E[l]) * P.strag <= g.m) sm |= 1ull << l;
+                                if (sm == an) sm = 0;  // every lane a straggler: a plain pull
+                            }
+                            s_strag = sm;
+                        }
+                        __syncthreads();
+                    }
                     pull_hop = pn;
                 }
                 // items for the lanes pushing next
@@ -1267,7 +1374,7 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                 bool anyn = false;
 #pragma unroll
                 for (int i = 0; i < W; ++i) {
-                    pn_push.w[i] = pull_hop ? 0ull : ld_volatile(P.active + nxt * W + i);
+                    pn_push.w[i] = ld_volatile(P.active + nxt * W + i) & (pull_hop ? (W == 1 ? s_strag : 0ull) : ~0ull);
                     anyn |= pn_push.w[i] != 0;
                 }
                 if (anyn) {
@@ -1382,6 +1489,12 @@ cudaError_t launch_w(Launch& L) {
         return e && e[0] == '1' ? 1u : 0u;
     }();
     P.diag = diag;
+    static const uint32_t strag = [] {
+        const char* e = std::getenv("MGK_STRAG");
+        return e ? (uint32_t)std::atoi(e) : (uint32_t)MGK_STRAG_DEFAULT;
+    }();
+    P.strag = W == 1 ? strag : 0u;
+    P.lane_E = ws->lane_cnt + (size_t)(MGK_MAX_HOPS + 1) * 64 * W;  // the row after the hops' counts
     P.umask = ws->umask;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
@@ -1421,7 +1534,7 @@ cudaError_t ensure_lanes_ws(const Graph* gr, Workspace* ws, int W) {
         if ((e = cudaMalloc(p, words * 8))) return e;
         if ((e = cudaMemset(*p, 0, words * 8))) return e;
     }
-    if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 1) * 64 * W * 8))) return e;
+    if ((e = cudaMalloc(&ws->lane_cnt, (size_t)(MGK_MAX_HOPS + 2) * 64 * W * 8))) return e;  // (+ lane_E)
     if ((e = cudaMalloc(&ws->active, (size_t)2 * W * 8))) return e;
     if (!ws->umask && (e = cudaMalloc(&ws->umask, 2 * ((size_t)g.nwords + 32) * 4))) return e;
     ws->bytes += 3 * words * 8;
@@ -1445,10 +1558,15 @@ cudaError_t launch_lanes(Launch& L) {
     cudaError_t e = ensure_lanes_ws(L.g, L.ws, W);
     if (e) return e;
     const uint32_t n = L.g->dg.n;
+    // MGK_MS_MB=5 / 6 forces the narrow instances' CTAs per SM (A/B runs)
+    static const int mb = [] {
+        const char* v = std::getenv("MGK_MS_MB");
+        return v ? std::atoi(v) : 0;
+    }();
     if (L.lane_bits == 16)
-        return narrow_bytes<1, 16>(n) > kWideState ? launch_w<1, 16, 6>(L) : launch_w<1, 16, 5>(L);
+        return (mb ? mb == 6 : narrow_bytes<1, 16>(n) > kWideState) ? launch_w<1, 16, 6>(L) : launch_w<1, 16, 5>(L);
     if (L.lane_bits == 10)
-        return narrow_bytes<1, 10>(n) > kWideState ? launch_w<1, 10, 6>(L) : launch_w<1, 10, 5>(L);
+        return (mb ? mb == 6 : narrow_bytes<1, 10>(n) > kWideState) ? launch_w<1, 10, 6>(L) : launch_w<1, 10, 5>(L);
     if (L.lane_bits == 8) return launch_w<1, 8, 5>(L);
     switch (W) {
         case 1: return launch_w<1, 64, 5>(L);
