@@ -71,7 +71,9 @@ def full(rep, key, out_md=None):
         lines.append(f"| dram read+write (bytes) | {rd + wr:.0f} | byte |")
         lines.append("")
         kname = name.split("(")[0].split("::")[-1]
-        traffic.setdefault(key, {})[kname] = rd + wr
+        if key not in traffic or "source" in traffic[key]:
+            traffic[key] = {}  # a new capture replaces the entry of an older one
+        traffic[key][kname] = rd + wr
     # stall attribution by source line
     try:
         txt = subprocess.run([sys.executable, str(ROOT / "scripts" / "ncu_lines.py"), rep, "15"],
@@ -79,7 +81,9 @@ def full(rep, key, out_md=None):
         lines += ["## warp-stall samples by source line (top 15)", "", "```", txt.strip(), "```", ""]
     except Exception:
         pass
-    traffic[key]["total"] = sum(v for k, v in traffic[key].items() if k != "total")
+    traffic[key]["total"] = sum(v for k, v in traffic[key].items() if k not in ("total", "source"))
+    if out_md:
+        traffic[key]["source"] = str(Path(out_md).relative_to(ROOT)) if Path(out_md).is_absolute() else str(out_md)
     traffic_file.write_text(json.dumps(traffic, indent=1) + "\n")
     md = "\n".join(lines) + "\n"
     if out_md:
