@@ -45,6 +45,13 @@ __device__ __forceinline__ uint32_t ldg_hint(const uint32_t* p, unsigned long lo
     asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ uint4 ldg_hint_v4(const uint4* p, unsigned long long pol) {
+    uint4 v;
+    asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
 // state written earlier in the same launch (ordered by the grid barrier):
 // coherent loads, L2 priority `pol`
 __device__ __forceinline__ uint32_t ld_hint_u8(const void* p, unsigned long long pol) {

@@ -401,6 +401,8 @@ cudaError_t locality_relabel(Graph* g, cudaStream_t s) {
     old.rp = g->rp, old.ci = g->ci, old.cp = g->cp, old.ri = g->ri;
     old.no_in = g->no_in, old.pull_skip = g->pull_skip, old.heavy = g->heavy;
     g->heavy = nullptr;
+    cudaFree(g->top4);  // (derived from the CSC being replaced; rebuilt on the next use)
+    g->top4 = nullptr;
     cudaError_t e = graph_from_sorted_keys(g, keys, alt, m, s);
     if (!e) e = cudaStreamSynchronize(s);
     cudaFreeAsync(keys, s);
@@ -775,6 +777,8 @@ void free_device_graph(Graph* g) {
     cudaFree(g->perm);
     cudaFree(g->inv);
     cudaFree(g->k2_split);
+    cudaFree(g->top4);
+    g->top4 = nullptr;
     cudaFree(g->bad_seed);
     g->bad_seed = nullptr;
     g->dg.bad_seed = nullptr;

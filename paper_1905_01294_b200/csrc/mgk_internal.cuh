@@ -181,6 +181,11 @@ struct Graph {
     // slice boundary ([n][R-1] absolute col_idx positions), built on first use
     uint32_t* k2_split = nullptr;
     uint32_t k2_split_bits = 0, k2_split_R = 0;
+    // LANES pull: the first four in-neighbours of every vertex (its in-list's
+    // head, padded with its first entry), one dense uint4 per vertex, built on
+    // first use -- a candidate's first frontier-word gathers then start with
+    // its visited word and CSC bounds, from a coalesced load
+    uint4* top4 = nullptr;
     Tuning tuning;
     std::mutex mu;
     std::vector<std::unique_ptr<Workspace>> free_ws;

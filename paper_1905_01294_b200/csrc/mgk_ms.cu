@@ -76,6 +76,10 @@ constexpr int kStageCap = 256;
 // first pull: lanes with at most m / MGK_STRAG frontier out-edges keep pushing (0: off; env MGK_STRAG).
 // G4, 10 seeds: hop 3 scans 666M -> 248M entries (213M pulled + the stragglers' pushes), k = 6 5.31 -> 3.82 ms;
 // 16 / 256 measured: 3.87 / 4.29 ms
+// one-word pulls start a candidate's scan from Graph::top4 (0: from the in-list; A/B builds)
+#ifndef MGK_TOP4
+#define MGK_TOP4 1
+#endif
 #ifndef MGK_STRAG_DEFAULT
 #define MGK_STRAG_DEFAULT 64
 #endif
@@ -117,6 +121,7 @@ struct MSParams {
     // [64]: per-lane out-edges of the frontier just found.
     uint32_t strag;
     unsigned long long* lane_E;
+    const uint4* top4;  // Graph::top4 (one word per vertex; nullptr: in-lists read from their first entry)
 };
 
 template <int W>
@@ -667,7 +672,8 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
     // of a short list (or the first kPre entries), the warp's scans of the
     // unsettled longer lists, the next-frontier store; true when lanes are left
     // (the candidate's visited word and CSC bounds are loaded by the caller)
-    auto visit = [&](bool valid, uint32_t u, const LaneWord<W>& vis, uint32_t b, uint32_t e, bool& found) -> bool {
+    auto visit = [&](bool valid, uint32_t u, const LaneWord<W>& vis, uint32_t b, uint32_t e, const uint4& t4,
+                     bool& found) -> bool {
         LaneWord<W> need;
 #pragma unroll
         for (int i = 0; i < W; ++i) need.w[i] = 0;
@@ -693,6 +699,19 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
             const uint32_t stop = e - b <= 32 ? e : b + kPre;
             uint32_t p = b;
             bool done = false;
+            if constexpr (W == 1 && MGK_TOP4) {
+                // the list's first four entries came with the visited word and the
+                // bounds (padding repeats the first entry: every gather is valid)
+                if (P.top4) {
+                    const uint32_t tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc_w.w[0] |= LS<W, NB>::gather(Fc, tv[q], l2_keep_policy()).w[0];
+                    const uint32_t d4 = min(e - b, 4u);
+                    scanned += d4;
+                    p = b + d4;
+                    done = covers<W>(acc_w, need);
+                }
+            }
             for (; p + kStep <= stop && !done; p += kStep) {
                 uint32_t v[kStep];
 #pragma unroll
@@ -792,13 +811,17 @@ MGK_PHASE void pull_phase(const MSParams& P, const unsigned long long* Fc, unsig
 #pragma unroll
         for (int i = 0; i < W; ++i) vis.w[i] = 0;
         uint32_t b = 0, e = 0;
+        uint4 t4 = make_uint4(0, 0, 0, 0);
         if (valid) {
             vis = LS<W, NB>::gather(P.V, u, l2_stream_policy());  // read once per pull: evict-first
             b = ldg_hint(g.cp + u, l2_stream_policy());
             e = ldg_hint(g.cp + u + 1, l2_stream_policy());
+            if constexpr (W == 1 && MGK_TOP4) {
+                if (P.top4) t4 = ldg_hint_v4(P.top4 + u, l2_stream_policy());
+            }
         }
         bool found;
-        if (visit(valid, u, vis, b, e, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
+        if (visit(valid, u, vis, b, e, t4, found)) atomicOr(&s_nm[(u >> 5) - wb], 1u << (u & 31));
     }
     __syncwarp();
     if (um_out && wq < wend) um_out[wq] = s_nm[lane];
@@ -1430,6 +1453,40 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
     }
 }
 
+// Graph::top4: the first four in-neighbours of every vertex, padded with the first
+__global__ void top4_kernel(DevGraph g, uint4* out) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < g.n; u += gridDim.x * blockDim.x) {
+        const uint32_t b = __ldg(g.cp + u), d = __ldg(g.cp + u + 1) - b;
+        uint4 t = make_uint4(0, 0, 0, 0);
+        if (d) {
+            t.x = __ldg(g.ri + b);
+            t.y = d > 1 ? __ldg(g.ri + b + 1) : t.x;
+            t.z = d > 2 ? __ldg(g.ri + b + 2) : t.x;
+            t.w = d > 3 ? __ldg(g.ri + b + 3) : t.x;
+        }
+        out[u] = t;
+    }
+}
+
+cudaError_t ensure_top4(const Graph* gr, cudaStream_t stream) {
+    static const bool off = std::getenv("MGK_NO_TOP4") != nullptr;
+    if (off || !MGK_TOP4 || gr->top4) return cudaSuccess;
+    Graph* gm = const_cast<Graph*>(gr);
+    std::lock_guard<std::mutex> lk(gm->mu);
+    if (gm->top4) return cudaSuccess;
+    uint4* t = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&t, (size_t)std::max<uint32_t>(gm->dg.n, 1) * sizeof(uint4)))) return e;
+    top4_kernel<<<1184, 256, 0, stream>>>(gm->dg, t);
+    if ((e = cudaGetLastError()) || (e = cudaStreamSynchronize(stream))) {
+        cudaFree(t);
+        return e;
+    }
+    gm->top4 = t;
+    gm->bytes += (size_t)gm->dg.n * sizeof(uint4);
+    return cudaSuccess;
+}
+
 template <int W, int NB, int MB>
 cudaError_t launch_w(Launch& L) {
     static int blocks_per_sm = 0, num_sms = 0;
@@ -1495,6 +1552,12 @@ cudaError_t launch_w(Launch& L) {
     }();
     P.strag = W == 1 ? strag : 0u;
     P.lane_E = ws->lane_cnt + (size_t)(MGK_MAX_HOPS + 1) * 64 * W;  // the row after the hops' counts
+    P.top4 = nullptr;
+    if (W == 1) {
+        cudaError_t te = ensure_top4(gr, L.stream);
+        if (te) return te;
+        P.top4 = gr->top4;
+    }
     P.umask = ws->umask;
     P.alpha = L.tuning.alpha_lanes;
     P.beta = L.tuning.beta;
