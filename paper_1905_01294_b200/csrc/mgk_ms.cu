@@ -74,14 +74,15 @@ __device__ __forceinline__ uint32_t ld_ri_lane(const uint32_t* p, unsigned long 
 constexpr int kWarps = kBlock / 32;
 constexpr int kStageCap = 256;
 // first pull: lanes with at most m / MGK_STRAG frontier out-edges keep pushing (0: off; env MGK_STRAG).
-// G4, 10 seeds: hop 3 scans 666M -> 248M entries (213M pulled + the stragglers' pushes), k = 6 5.31 -> 3.82 ms;
-// 16 / 256 measured: 3.87 / 4.29 ms
+// G4, 10 seeds, m/64: hop 3 scans 666M -> 248M entries (213M pulled + the stragglers' pushes), k = 6 5.31 -> 3.82 ms
+// (16 / 256: 3.87 / 4.29 ms); with the mixed hop's push as fire-and-forget ORs (no list) m/32 is best: 3.57 ms
+// (m/16 3.57, m/64 3.72; G2 0.430 vs 0.457 ms at m/64)
 // one-word pulls start a candidate's scan from Graph::top4 (0: from the in-list; A/B builds)
 #ifndef MGK_TOP4
 #define MGK_TOP4 1
 #endif
 #ifndef MGK_STRAG_DEFAULT
-#define MGK_STRAG_DEFAULT 64
+#define MGK_STRAG_DEFAULT 32
 #endif
 
 struct MSParams {
@@ -498,7 +499,7 @@ __device__ void block_flush(Acc& a, QCtl* q, QCtl* qf, LevelCounters* lc, LevelC
 // chain of dependent accesses (in-list entry -> visited word -> atomic), so a
 // round costs a full memory latency; one-word lanes take PU of them at once.
 #ifndef MGK_PUSH_UNROLL
-#define MGK_PUSH_UNROLL 1  // 2 and 4 measured: no gain (G4 hop 2 push ~105 us either way)
+#define MGK_PUSH_UNROLL 4
 #endif
 // finalize lists of more than n / kDenseDiv vertices are swept densely (one word per vertex)
 #ifndef MGK_DENSE_DIV
@@ -508,7 +509,10 @@ constexpr uint64_t kDenseDiv = MGK_DENSE_DIV;
 template <int W>
 constexpr int push_unroll() { return W == 1 ? MGK_PUSH_UNROLL : 1; }
 
-template <int W, int NB>
+// kList = false (the stragglers' push of a mixed hop): the ORs are fire-and-
+// forget (a `red`: ~1.5x the rate of an atomic that returns) and nothing is
+// listed -- that hop's finalize sweeps every vertex.
+template <int W, int NB, bool kList = true>
 MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nlight, unsigned long long hctl,
                            const unsigned long long* Fc, unsigned long long* Fn, uint32_t* Rn,
                            QCtl* qn, Acc& acc, Stage<kStageCap>& st, uint32_t warp_gid,
@@ -540,35 +544,59 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nlight
                 u[q] = valid[q] ? __ldg(g.ci + pos) : 0;
                 first[q] = false;
             }
+            if constexpr (W == 1) {
+                // the round's visited words first, then its atomics (the OR that finds
+                // the word empty lists u): every load of the round is in flight before
+                // the first atomic, and no atomic waits for another's result
+                unsigned long long m[PU];
 #pragma unroll
-            for (int q = 0; q < PU; ++q) {
-                if (!valid[q]) continue;
-                const LaneWord<W> f = LS<W, NB>::load(Fc, src[q]);
-                const LaneWord<W> vis = LS<W, NB>::load(P.V, u[q]);
-                LaneWord<W> m;
-                bool any = false;
-#pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    m.w[i] = f.w[i] & ~vis.w[i] & pushm.w[i];  // only the lanes pushing this hop
-                    any |= m.w[i] != 0;
+                for (int q = 0; q < PU; ++q) {
+                    m[q] = 0;
+                    // (also masking the lanes u's new word already holds, to spare hub
+                    // targets' atomics, measured slower: G4 mixed hop's push 780 -> 900 us)
+                    if (valid[q])
+                        m[q] = LS<W, NB>::load(Fc, src[q]).w[0] & pushm.w[0] & ~LS<W, NB>::load(P.V, u[q]).w[0];
                 }
-                if (any) {
-                    if constexpr (W == 1) {
-                        // one atomic: the OR that finds the word empty lists u
-                        first[q] = LS<W, NB>::atomic_or_first(Fn, u[q], m.w[0]);
-                    } else {
-                        const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u[q]);
-                        bool need = false;
 #pragma unroll
-                        for (int i = 0; i < W; ++i) {
-                            if ((cur.w[i] & m.w[i]) != m.w[i]) {
-                                LS<W, NB>::atomic_or(Fn, u[q], i, m.w[i]);
-                                need = true;
+                for (int q = 0; q < PU; ++q) {
+                    if (m[q]) {
+                        if constexpr (kList)
+                            first[q] = LS<W, NB>::atomic_or_first(Fn, u[q], m[q]);
+                        else
+                            LS<W, NB>::atomic_or(Fn, u[q], 0, m[q]);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < PU; ++q) {
+                    if (!valid[q]) continue;
+                    const LaneWord<W> f = LS<W, NB>::load(Fc, src[q]);
+                    const LaneWord<W> vis = LS<W, NB>::load(P.V, u[q]);
+                    LaneWord<W> m;
+                    bool any = false;
+#pragma unroll
+                    for (int i = 0; i < W; ++i) {
+                        m.w[i] = f.w[i] & ~vis.w[i] & pushm.w[i];  // only the lanes pushing this hop
+                        any |= m.w[i] != 0;
+                    }
+                    if (any) {
+                        if constexpr (W == 1) {
+                            // one atomic: the OR that finds the word empty lists u
+                            first[q] = LS<W, NB>::atomic_or_first(Fn, u[q], m.w[0]);
+                        } else {
+                            const LaneWord<W> cur = LS<W, NB>::load_cg(Fn, u[q]);
+                            bool need = false;
+#pragma unroll
+                            for (int i = 0; i < W; ++i) {
+                                if ((cur.w[i] & m.w[i]) != m.w[i]) {
+                                    LS<W, NB>::atomic_or(Fn, u[q], i, m.w[i]);
+                                    need = true;
+                                }
                             }
-                        }
-                        if (need) {  // several words: the touched bit decides who lists u
-                            const uint32_t bit = 1u << (u[q] & 31);
-                            first[q] = !(atomicOr(P.touched + (u[q] >> 5), bit) & bit);
+                            if (need) {  // several words: the touched bit decides who lists u
+                                const uint32_t bit = 1u << (u[q] & 31);
+                                first[q] = !(atomicOr(P.touched + (u[q] >> 5), bit) & bit);
+                            }
                         }
                     }
                 }
@@ -576,16 +604,20 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nlight
 #pragma unroll
             for (int q = 0; q < PU; ++q) {
                 acc.scanned += valid[q];
-                st.push(first[q], u[q]);
-                if (st.full()) {
-                    emit_list(st.buf, st.n, Rn, &qn->nitems);
-                    st.n = 0;
+                if constexpr (kList) {
+                    st.push(first[q], u[q]);
+                    if (st.full()) {
+                        emit_list(st.buf, st.n, Rn, &qn->nitems);
+                        st.n = 0;
+                    }
                 }
             }
         }
     }
-    emit_list(st.buf, st.n, Rn, &qn->nitems);
-    st.n = 0;
+    if constexpr (kList) {
+        emit_list(st.buf, st.n, Rn, &qn->nitems);
+        st.n = 0;
+    }
 }
 
 // ---- pull expand -------------------------------------------------------------
@@ -1317,7 +1349,8 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                     pushm.w[0] = ld_volatile(P.active + c2) & sm;
                     if (pushm.w[0]) {
                         grid_barrier(P.bar);
-                        push_phase<W, NB>(P, items_of(P, c2), ld_volatile(&P.qctl[c2].nfound),
+                        if (P.diag && gtid == 0) P.misc[3] = globaltimer();  // probe: where the pull part ended
+                        push_phase<W, NB, false>(P, items_of(P, c2), ld_volatile(&P.qctl[c2].nfound),
                                           ld_volatile(&P.misc[kHeavyCtl + c2]), F_of(P, c2), F_of(P, n2), R_of(P, n2),
                                           &P.qctl[n2], acc, st, warp_gid, nwarps, pushm);
                         prev_pull = false;
@@ -1328,6 +1361,9 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
             grid_barrier(P.bar);
             if (P.diag && gtid == 0) P.misc[7] = globaltimer();
             nR = ld_volatile(&qn->nitems);
+            // a mixed hop's push listed nothing: the hop counts as one that found
+            // every vertex -- a dense finalize, streamed clears, and the next hop pulls
+            if (W == 1 && anypull && !prev_pull && hop > 1 && P.force_dir == 0 && P.strag) nR = g.n;
             if (gtid == 0) P.misc[1] = P.misc[2] = 0;  // read again only after the finalize barrier
             const bool last = hop == P.k || nR == 0;
             const bool count_lanes = hop >= P.min_hop;
@@ -1411,6 +1447,10 @@ __global__ void __launch_bounds__(kBlock, ms_min_blocks<W, MB>()) ms_kernel(MSPa
                 if (P.diag) {  // probe mode: phase split (the counters these fields hold are lost)
                     P.lc[hop].union_edges = P.misc[7] - P.misc[6];
                     P.lc[hop].candidates = t2 - P.misc[7];
+                    if (P.misc[3]) {  // a mixed hop: its pull part's ns in lc.edges
+                        P.lc[hop].edges = P.misc[3] - P.misc[6];
+                        P.misc[3] = 0;
+                    }
                 }
             }
             clog_used += nR;
