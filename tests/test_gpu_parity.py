@@ -396,6 +396,23 @@ def test_replicas_and_multi(port, g1):
         k_hop_count_multi(reps, seeds, 0)
 
 
+@pytest.mark.parametrize("strag", ["0", "2", "32", "4096", "100000000"])
+def test_straggler_thresholds(strag):
+    """The LANES engine's straggler lanes (lanes with at most m / MGK_STRAG
+    frontier out-edges push while the others pull, mgk_ms.cu): off, nearly every
+    lane a straggler, the default, and thresholds only tiny frontiers meet --
+    all give the oracle's counts, in every narrow lane-word width."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    worker = Path(__file__).resolve().parent / "helpers" / "strag_worker.py"
+    env = dict(os.environ, MGK_STRAG=strag)
+    r = subprocess.run([sys.executable, str(worker)], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:]
+
+
 def test_two_processes_share_one_gpu():
     """Regression: workspace zeroing ran on the legacy stream, unordered with
     the engines' non-blocking streams; with another process on the GPU the
