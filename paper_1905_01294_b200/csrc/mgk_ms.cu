@@ -554,8 +554,14 @@ MGK_PHASE void push_phase(const MSParams& P, const uint4* items, uint32_t nlight
                     m[q] = 0;
                     // (also masking the lanes u's new word already holds, to spare hub
                     // targets' atomics, measured slower: G4 mixed hop's push 780 -> 900 us)
-                    if (valid[q])
-                        m[q] = LS<W, NB>::load(Fc, src[q]).w[0] & pushm.w[0] & ~LS<W, NB>::load(P.V, u[q]).w[0];
+                    // (kList = false: no visited-word gather either -- the finalize
+                    // masks every new word with the visited one, and a lane bit at a
+                    // vertex the lane already visited is inert for one hop: every
+                    // out-neighbour of such a vertex was reached by that lane before)
+                    if (valid[q]) {
+                        m[q] = LS<W, NB>::load(Fc, src[q]).w[0] & pushm.w[0];
+                        if constexpr (kList) m[q] &= ~LS<W, NB>::load(P.V, u[q]).w[0];
+                    }
                 }
 #pragma unroll
                 for (int q = 0; q < PU; ++q) {
@@ -1009,11 +1015,16 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             r1 = __ldg(g.rp + u + 1);
             c0 = __ldg(g.cp + u);
             c1 = __ldg(g.cp + u + 1);
-            if (dense) {
+            // lanes that had visited u are dropped here (only a mixed hop's push,
+            // which does not read the visited words, sets any)
+            {
                 bool any = false;
 #pragma unroll
-                for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
-                valid = any;
+                for (int i = 0; i < W; ++i) {
+                    x.w[i] &= ~v.w[i];
+                    any |= x.w[i] != 0;
+                }
+                if (dense || W == 1) valid = any;
             }
         }
         if (valid) {

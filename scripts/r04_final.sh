@@ -10,9 +10,9 @@ python scripts/bench_summary.py gpurun_out/bench.json
 head -c 400 gpurun_out/bench_ref.json; echo
 export MGK_NONCOOP=1
 NCU="ncu --set full --clock-control none --import-source on"
-timeout 900 $NCU -k regex:ms_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/r04d_ms_cfg4_k6 -f python scripts/prof_target.py G4 6 10 > gpurun_out/ncu_ms_cfg4.log 2>&1
-timeout 600 $NCU -k regex:ms_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/r04d_ms_cfg3_k6 -f python scripts/prof_target.py G2 6 10 > gpurun_out/ncu_ms_cfg3.log 2>&1
+timeout 900 $NCU -k regex:ms_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/r04e_ms_cfg4_k6 -f python scripts/prof_target.py G4 6 10 > gpurun_out/ncu_ms_cfg4.log 2>&1
+timeout 600 $NCU -k regex:ms_kernel --launch-skip 2 --launch-count 1 -o gpurun_out/r04e_ms_cfg3_k6 -f python scripts/prof_target.py G2 6 10 > gpurun_out/ncu_ms_cfg3.log 2>&1
 unset MGK_NONCOOP
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r04d_launches_cfg4.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r04e_launches_cfg4.csv \
     python bench.py --steps 2 --warmup 3 --no-extras --no-cpu > gpurun_out/ncu_launches.log 2>&1
 ls -la gpurun_out | grep r04d
