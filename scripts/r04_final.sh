@@ -15,4 +15,4 @@ timeout 600 $NCU -k regex:ms_kernel --launch-skip 2 --launch-count 1 -o gpurun_o
 unset MGK_NONCOOP
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/r04e_launches_cfg4.csv \
     python bench.py --steps 2 --warmup 3 --no-extras --no-cpu > gpurun_out/ncu_launches.log 2>&1
-ls -la gpurun_out | grep r04d
+ls -la gpurun_out | grep r04e
