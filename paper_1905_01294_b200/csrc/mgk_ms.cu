@@ -1015,17 +1015,23 @@ MGK_PHASE void finalize_phase(const MSParams& P, const uint32_t* Rn, uint32_t nR
             r1 = __ldg(g.rp + u + 1);
             c0 = __ldg(g.cp + u);
             c1 = __ldg(g.cp + u + 1);
-            // lanes that had visited u are dropped here (only a mixed hop's push,
-            // which does not read the visited words, sets any)
-            {
+            if (dense) {
                 bool any = false;
 #pragma unroll
-                for (int i = 0; i < W; ++i) {
-                    x.w[i] &= ~v.w[i];
-                    any |= x.w[i] != 0;
-                }
-                if (dense || W == 1) valid = any;
+                for (int i = 0; i < W; ++i) any |= x.w[i] != 0;
+                valid = any;
             }
+        }
+        if (valid) {
+            // lanes that had visited u are dropped here (only a mixed hop's push,
+            // which does not read the visited words, sets any)
+            bool any = false;
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                x.w[i] &= ~v.w[i];
+                any |= x.w[i] != 0;
+            }
+            valid = any;
         }
         if (valid) {
             bool fresh = true;  // no lane had visited u: its in-edges leave the unexplored set
